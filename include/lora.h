@@ -1,0 +1,171 @@
+/*
+ * include/lora.h -- C ABI of liblora.so: the B200 (sm_100a) hot path of JORA
+ * (arXiv 2403.11366), the LoRA-adapted projection and its backward.
+ *
+ * The operation (PAPER.md = the paper text, /root/reference/PAPER.md):
+ *   PAPER.md:109 (Sec. 3): frozen W0 in R^{m x n}, trainable A in R^{r x n},
+ *     B in R^{m x r}, r << m, n; W0 x + b0 is tuned to W0 x + b0 + B A x.
+ *   PAPER.md:115-120 (Eq. 1): Output = W0 x + b0 + B A x = (W0 + B A) x + b0.
+ *   only A and B are trained (no gradient for W0, b0).
+ *   PAPER.md:80-81 (Listing 3): LORA_R, LORA_ALPHA -> s = alpha / r.
+ * Row-vector orientation used here (R1), for T tokens:
+ *   forward : h = x A^T [T,r];  y = x W0^T + s h B^T (+ b0)          [T,m]
+ *   backward: gh = s dy B [T,r]; dx = dy W0 + gh A [T,n];
+ *             dA = gh^T x [r,n]; dB = s dy^T h [m,r]
+ *   merge   : W' = W0 + s B A [m,n]   (Eq. 1 line 2; PAPER.md:92-106 export)
+ *
+ * Conventions for every call:
+ *   - Tensor pointers are DEVICE pointers to row-major, contiguous tensors.
+ *     "bf16" tensors hold IEEE bfloat16 values (2 bytes each); fp32 tensors
+ *     hold float.  The caller owns all memory; the library never allocates
+ *     device memory inside a call (scratch comes from `workspace`).
+ *   - Every device pointer must be 16-byte aligned.  d_in and d_out must be
+ *     multiples of 8 (so bf16 rows are 16-byte multiples, as TMA requires);
+ *     1 <= rank <= 64; tokens >= 0.  Violations -> LORA_ERR_SHAPE /
+ *     LORA_ERR_ALIGN / LORA_ERR_UNSUPPORTED, returned before anything is
+ *     launched and with no output written.
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).  All work
+ *     is enqueued asynchronously on it; asynchronous faults surface at the
+ *     caller's synchronisation.  A failed launch returns LORA_ERR_CUDA.
+ *   - Outputs must not alias inputs (the one exception: lora_merge with
+ *     w_out == w0, an explicit in-place merge).
+ *   - lora_last_error() returns a thread-local, human-readable description of
+ *     the last failure (names the offending shapes / pointers).
+ *   - y and dx are rounded once to bf16 (round-to-nearest-even); h, gh, dA,
+ *     dB are fp32; all products accumulate in fp32 (R4, R5).
+ */
+#ifndef LORA_B200_H_
+#define LORA_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    LORA_OK = 0,
+    LORA_ERR_INVALID = 1,     /* NULL required pointer, bad enum, bad comm */
+    LORA_ERR_SHAPE = 2,       /* non-positive / non-multiple-of-8 dims, shard mismatch */
+    LORA_ERR_ALIGN = 3,       /* a pointer is not 16-byte aligned */
+    LORA_ERR_UNSUPPORTED = 4, /* rank > 64, device is not sm_100 */
+    LORA_ERR_CUDA = 5,        /* CUDA runtime/driver failure */
+    LORA_ERR_NCCL = 6,        /* NCCL failure */
+    LORA_ERR_WORKSPACE = 7    /* workspace NULL or smaller than *_workspace_bytes() */
+} lora_status;
+
+/* One LoRA linear.  tokens = T (batch x seq), d_in = n, d_out = m, rank = r,
+ * alpha = the LoRA alpha of Listing 3; s = alpha / rank is
+ * computed in fp32. */
+typedef struct {
+    int64_t tokens;
+    int64_t d_in;
+    int64_t d_out;
+    int32_t rank;
+    float alpha;
+} lora_dims;
+
+/* Bytes of device scratch lora_linear_fwd needs for `dims` (O(d_out * 64)). */
+size_t lora_linear_fwd_workspace_bytes(const lora_dims* dims);
+
+/*
+ * Forward, Eq. 1 line 1:  y = x W0^T + s (x A^T) B^T (+ bias)
+ *   x    [T, n] bf16     w0 [m, n] bf16     a [r, n] bf16     b [m, r] bf16
+ *   bias [m] bf16 or NULL (Llama-2 projections have none)
+ *   y    [T, m] bf16 (out)
+ *   h_out [T, r] fp32 (out, optional): h = x A^T, unscaled, saved for the
+ *         backward (dB = s dy^T h); NULL skips the store.
+ * One fused launch computes x W0^T and x A^T in the same tensor-core pass and
+ * adds (s h) B^T in its epilogue (kernel K1).
+ */
+lora_status lora_linear_fwd(const lora_dims* dims, const void* x, const void* w0,
+                            const void* a, const void* b, const void* bias,
+                            void* y, float* h_out,
+                            void* workspace, size_t workspace_bytes, void* stream);
+
+/* Bytes of device scratch lora_linear_bwd needs for `dims`. */
+size_t lora_linear_bwd_workspace_bytes(const lora_dims* dims);
+
+/*
+ * Backward of Eq. 1 for trainable A, B and frozen W0, b0:
+ *   dy      [T, m] bf16      upstream gradient
+ *   h_saved [T, r] fp32      h from lora_linear_fwd, or NULL (recomputed)
+ *   dx      [T, n] bf16 out  dy W0 + gh A, or NULL (input grad not needed)
+ *   da      [r, n] fp32 out  gh^T x            (NULL skips)
+ *   db      [m, r] fp32 out  s dy^T h          (NULL skips)
+ *   accumulate: 0 overwrite da/db, 1 add into them (gradient accumulation).
+ * No gradient for W0 or bias is produced (frozen base).
+ */
+lora_status lora_linear_bwd(const lora_dims* dims, const void* x, const void* w0,
+                            const void* a, const void* b, const float* h_saved,
+                            const void* dy, void* dx, float* da, float* db,
+                            int accumulate,
+                            void* workspace, size_t workspace_bytes, void* stream);
+
+/*
+ * Merge for export, Eq. 1 line 2 (script PAPER.md:92-106):
+ *   w_out[i,k] = RNE_bf16( W0[i,k] + s * sum_j B[i,j] A[j,k] ), fp32 math.
+ * dims->tokens is ignored.  w_out == w0 performs the merge in place;
+ * otherwise w_out must not overlap any input.  The bias is unaffected.
+ */
+lora_status lora_merge(const lora_dims* dims, const void* w0, const void* a,
+                       const void* b, void* w_out, void* stream);
+
+const char* lora_status_string(lora_status status);
+const char* lora_last_error(void);
+
+/* Library / device information.  lora_device_check returns LORA_OK if the
+ * current CUDA device is sm_100 (B200), LORA_ERR_UNSUPPORTED otherwise. */
+int lora_version(void);
+lora_status lora_device_check(void);
+
+/* Number of kernel launches the last fwd / bwd / merge call on this thread
+ * enqueued (for the bench's gpu_launches accounting). */
+int lora_last_launch_count(void);
+
+/* ---------------- Tensor parallelism (R10-R13) ------
+ * One process per GPU.  COLUMN: W0 and B sharded on d_out, A replicated;
+ * ROW: W0 and A sharded on d_in, B replicated.  `local` holds the LOCAL shard
+ * dims (column: d_out / N; row: d_in / N).  Collectives are NCCL all-reduces
+ * (sum) over NVLink on `stream`:
+ *   COLUMN fwd: none.             COLUMN bwd: dx (bf16), dA (fp32).
+ *   ROW    fwd: y (bf16).         ROW    bwd: dB (fp32).
+ * The LoRA-gradient all-reduce is a SUM with no 1/N (R12); pass
+ * reduce_lora_grads = 0 to leave it to a bucketed lora_allreduce call. */
+typedef struct lora_comm lora_comm;
+typedef enum { LORA_TP_COLUMN = 0, LORA_TP_ROW = 1 } lora_tp_mode;
+typedef enum { LORA_DT_F32 = 0, LORA_DT_BF16 = 1 } lora_dtype;
+
+#define LORA_COMM_ID_BYTES 128
+lora_status lora_comm_unique_id(uint8_t id[LORA_COMM_ID_BYTES]);
+lora_status lora_comm_init(int nranks, int rank, const uint8_t id[LORA_COMM_ID_BYTES],
+                           lora_comm** out);
+lora_status lora_comm_destroy(lora_comm* comm);
+int lora_comm_size(const lora_comm* comm);
+int lora_comm_rank(const lora_comm* comm);
+
+/* In-place sum all-reduce of `count` elements of `dtype`. */
+lora_status lora_allreduce(lora_comm* comm, void* buf, size_t count, lora_dtype dtype,
+                           void* stream);
+
+/* Row mode: only rank 0 adds the bias (it is not sharded). */
+lora_status lora_tp_linear_fwd(lora_comm* comm, lora_tp_mode mode, const lora_dims* local,
+                               const void* x, const void* w0, const void* a, const void* b,
+                               const void* bias, void* y, float* h_out,
+                               void* workspace, size_t workspace_bytes, void* stream);
+
+/* Workspace for lora_tp_linear_bwd: lora_linear_bwd_workspace_bytes(local)
+ * plus fp32 scratch for the reduced partial gradient. */
+size_t lora_tp_linear_bwd_workspace_bytes(const lora_dims* local);
+
+lora_status lora_tp_linear_bwd(lora_comm* comm, lora_tp_mode mode, const lora_dims* local,
+                               const void* x, const void* w0, const void* a, const void* b,
+                               const float* h_saved, const void* dy, void* dx,
+                               float* da, float* db, int accumulate, int reduce_lora_grads,
+                               void* workspace, size_t workspace_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LORA_B200_H_ */

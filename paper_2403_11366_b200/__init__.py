@@ -1,0 +1,244 @@
+"""paper_2403_11366_b200 -- B200-native LoRA-linear hot path of JORA (arXiv 2403.11366).
+
+Thin Python binding over the C ABI of ``liblora.so`` (``include/lora.h``).
+It only marshals arguments (torch tensors -> device pointers, the current
+CUDA stream) -- every step of the path runs in the sm_100a kernels of
+``csrc/``.  There is no CPU fallback: if the library is missing, importing
+this package raises, and every call on a non-B200 device returns an error.
+
+Functions keep the C names:
+    lora_linear_fwd   y = x W0^T + s (x A^T) B^T (+ b0)   (Eq. 1, :117)
+    lora_linear_bwd   dx, dA, dB (A, B trainable, W0 frozen)
+    lora_merge        W0 + s B A                           (Eq. 1 line 2, :118)
+with s = alpha / r (Listing 3).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+
+import torch
+
+__all__ = [
+    "LoraError", "lora_dims", "lib", "lora_linear_fwd", "lora_linear_bwd", "lora_merge",
+    "lora_linear_fwd_workspace_bytes", "lora_linear_bwd_workspace_bytes",
+    "lora_last_launch_count", "lora_device_check", "LIB_PATH", "header_functions",
+]
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "liblora.so")
+HEADER_PATH = os.path.join(os.path.dirname(_PKG), "include", "lora.h")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `python -m paper_2403_11366_b200.build` "
+        "(there is no CPU fallback for the LoRA hot path)")
+
+lib = ctypes.CDLL(LIB_PATH)
+
+
+class lora_dims(ctypes.Structure):
+    _fields_ = [("tokens", ctypes.c_int64), ("d_in", ctypes.c_int64), ("d_out", ctypes.c_int64),
+                ("rank", ctypes.c_int32), ("alpha", ctypes.c_float)]
+
+
+_vp = ctypes.c_void_p
+_fp = ctypes.c_void_p  # float* passed as raw address
+_dp = ctypes.POINTER(lora_dims)
+_st = ctypes.c_int
+
+lib.lora_linear_fwd_workspace_bytes.argtypes = [_dp]
+lib.lora_linear_fwd_workspace_bytes.restype = ctypes.c_size_t
+lib.lora_linear_bwd_workspace_bytes.argtypes = [_dp]
+lib.lora_linear_bwd_workspace_bytes.restype = ctypes.c_size_t
+lib.lora_linear_fwd.argtypes = [_dp, _vp, _vp, _vp, _vp, _vp, _vp, _fp, _vp, ctypes.c_size_t, _vp]
+lib.lora_linear_fwd.restype = _st
+lib.lora_linear_bwd.argtypes = [_dp, _vp, _vp, _vp, _vp, _fp, _vp, _vp, _fp, _fp, ctypes.c_int,
+                                _vp, ctypes.c_size_t, _vp]
+lib.lora_linear_bwd.restype = _st
+lib.lora_merge.argtypes = [_dp, _vp, _vp, _vp, _vp, _vp]
+lib.lora_merge.restype = _st
+lib.lora_status_string.argtypes = [_st]
+lib.lora_status_string.restype = ctypes.c_char_p
+lib.lora_last_error.restype = ctypes.c_char_p
+lib.lora_version.restype = ctypes.c_int
+lib.lora_device_check.restype = _st
+lib.lora_last_launch_count.restype = ctypes.c_int
+lib.lora_comm_unique_id.argtypes = [ctypes.c_char_p]
+lib.lora_comm_unique_id.restype = _st
+lib.lora_comm_init.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_char_p, ctypes.POINTER(_vp)]
+lib.lora_comm_init.restype = _st
+lib.lora_comm_destroy.argtypes = [_vp]
+lib.lora_comm_destroy.restype = _st
+lib.lora_comm_size.argtypes = [_vp]
+lib.lora_comm_size.restype = ctypes.c_int
+lib.lora_comm_rank.argtypes = [_vp]
+lib.lora_comm_rank.restype = ctypes.c_int
+lib.lora_allreduce.argtypes = [_vp, _vp, ctypes.c_size_t, ctypes.c_int, _vp]
+lib.lora_allreduce.restype = _st
+lib.lora_tp_linear_fwd.argtypes = [_vp, ctypes.c_int, _dp, _vp, _vp, _vp, _vp, _vp, _vp, _fp, _vp,
+                                   ctypes.c_size_t, _vp]
+lib.lora_tp_linear_fwd.restype = _st
+lib.lora_tp_linear_bwd_workspace_bytes.argtypes = [_dp]
+lib.lora_tp_linear_bwd_workspace_bytes.restype = ctypes.c_size_t
+lib.lora_tp_linear_bwd.argtypes = [_vp, ctypes.c_int, _dp, _vp, _vp, _vp, _vp, _fp, _vp, _vp, _fp, _fp,
+                                   ctypes.c_int, ctypes.c_int, _vp, ctypes.c_size_t, _vp]
+lib.lora_tp_linear_bwd.restype = _st
+
+STATUS = {0: "LORA_OK", 1: "LORA_ERR_INVALID", 2: "LORA_ERR_SHAPE", 3: "LORA_ERR_ALIGN",
+          4: "LORA_ERR_UNSUPPORTED", 5: "LORA_ERR_CUDA", 6: "LORA_ERR_NCCL", 7: "LORA_ERR_WORKSPACE"}
+
+
+class LoraError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        self.name = STATUS.get(status, str(status))
+        msg = lib.lora_last_error().decode(errors="replace")
+        super().__init__(f"{where}: {self.name}: {msg}")
+
+
+def _check(st: int, where: str) -> None:
+    if st != 0:
+        raise LoraError(st, where)
+
+
+def header_functions() -> list[str]:
+    """Names of every function include/lora.h declares (for ABI tests)."""
+    txt = open(HEADER_PATH).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(lora_[a-z0-9_]+)\s*\(", txt)))
+
+
+def dims(tokens: int, d_in: int, d_out: int, rank: int, alpha: float) -> lora_dims:
+    return lora_dims(int(tokens), int(d_in), int(d_out), int(rank), float(alpha))
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if isinstance(t, int):
+        return t
+    return t.data_ptr()
+
+
+def _stream(stream):
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def _bf16(t, name, shape):
+    if not (t.is_cuda and t.dtype == torch.bfloat16 and t.is_contiguous()):
+        raise ValueError(f"{name} must be a contiguous CUDA bf16 tensor")
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} has shape {tuple(t.shape)}, expected {tuple(shape)}")
+
+
+def _f32(t, name, shape):
+    if not (t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()):
+        raise ValueError(f"{name} must be a contiguous CUDA fp32 tensor")
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} has shape {tuple(t.shape)}, expected {tuple(shape)}")
+
+
+_ws_cache: dict = {}
+
+
+def _workspace(nbytes: int, device) -> torch.Tensor:
+    """Per-device scratch (single-stream use; pass `workspace=` for concurrent streams)."""
+    key = torch.device(device).index
+    ws = _ws_cache.get(key)
+    if ws is None or ws.numel() < nbytes:
+        ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+        _ws_cache[key] = ws
+    return ws
+
+
+def lora_linear_fwd_workspace_bytes(d: lora_dims) -> int:
+    return int(lib.lora_linear_fwd_workspace_bytes(ctypes.byref(d)))
+
+
+def lora_linear_bwd_workspace_bytes(d: lora_dims) -> int:
+    return int(lib.lora_linear_bwd_workspace_bytes(ctypes.byref(d)))
+
+
+def lora_last_launch_count() -> int:
+    return int(lib.lora_last_launch_count())
+
+
+def lora_device_check() -> None:
+    _check(lib.lora_device_check(), "lora_device_check")
+
+
+def lora_linear_fwd(x, w0, a, b, alpha, bias=None, y=None, h_out=None, want_h=True,
+                    workspace=None, stream=None):
+    """Forward of Eq. 1.  x [T,n], w0 [m,n], a [r,n], b [m,r]
+    (bf16, CUDA).  Returns (y [T,m] bf16, h [T,r] fp32 or None)."""
+    T, n = x.shape
+    m, r = b.shape
+    _bf16(x, "x", (T, n)); _bf16(w0, "w0", (m, n)); _bf16(a, "a", (r, n)); _bf16(b, "b", (m, r))
+    if bias is not None:
+        _bf16(bias, "bias", (m,))
+    if y is None:
+        y = torch.empty((T, m), dtype=torch.bfloat16, device=x.device)
+    _bf16(y, "y", (T, m))
+    if h_out is None and want_h:
+        h_out = torch.empty((T, r), dtype=torch.float32, device=x.device)
+    if h_out is not None:
+        _f32(h_out, "h_out", (T, r))
+    d = dims(T, n, m, r, alpha)
+    need = lora_linear_fwd_workspace_bytes(d)
+    ws = workspace if workspace is not None else _workspace(need, x.device)
+    st = lib.lora_linear_fwd(ctypes.byref(d), _ptr(x), _ptr(w0), _ptr(a), _ptr(b), _ptr(bias),
+                             _ptr(y), _ptr(h_out), _ptr(ws), ws.numel(), _stream(stream))
+    _check(st, "lora_linear_fwd")
+    return y, h_out
+
+
+def lora_linear_bwd(x, w0, a, b, dy, alpha, h_saved=None, want_dx=True, dx=None, da=None, db=None,
+                    accumulate=False, want_da=True, want_db=True, workspace=None, stream=None):
+    """Backward of Eq. 1.  Returns (dx [T,n] bf16 | None,
+    dA [r,n] fp32 | None, dB [m,r] fp32 | None)."""
+    T, n = x.shape
+    m, r = b.shape
+    _bf16(x, "x", (T, n)); _bf16(w0, "w0", (m, n)); _bf16(a, "a", (r, n)); _bf16(b, "b", (m, r))
+    _bf16(dy, "dy", (T, m))
+    if h_saved is not None:
+        _f32(h_saved, "h_saved", (T, r))
+    if dx is None and want_dx:
+        dx = torch.empty((T, n), dtype=torch.bfloat16, device=x.device)
+    if dx is not None:
+        _bf16(dx, "dx", (T, n))
+    if da is None and want_da:
+        da = torch.zeros((r, n), dtype=torch.float32, device=x.device)
+    if db is None and want_db:
+        db = torch.zeros((m, r), dtype=torch.float32, device=x.device)
+    if da is not None:
+        _f32(da, "da", (r, n))
+    if db is not None:
+        _f32(db, "db", (m, r))
+    d = dims(T, n, m, r, alpha)
+    need = lora_linear_bwd_workspace_bytes(d)
+    ws = workspace if workspace is not None else _workspace(need, x.device)
+    st = lib.lora_linear_bwd(ctypes.byref(d), _ptr(x), _ptr(w0), _ptr(a), _ptr(b), _ptr(h_saved),
+                             _ptr(dy), _ptr(dx), _ptr(da), _ptr(db), 1 if accumulate else 0,
+                             _ptr(ws), ws.numel(), _stream(stream))
+    _check(st, "lora_linear_bwd")
+    return dx, da, db
+
+
+def lora_merge(w0, a, b, alpha, w_out=None, stream=None):
+    """W' = bf16(W0 + s B A) (Eq. 1 line 2).  w_out=w0 merges in place."""
+    m, n = w0.shape
+    r = a.shape[0]
+    _bf16(w0, "w0", (m, n)); _bf16(a, "a", (r, n)); _bf16(b, "b", (m, r))
+    if w_out is None:
+        w_out = torch.empty_like(w0)
+    _bf16(w_out, "w_out", (m, n))
+    d = dims(0, n, m, r, alpha)
+    st = lib.lora_merge(ctypes.byref(d), _ptr(w0), _ptr(a), _ptr(b), _ptr(w_out), _stream(stream))
+    _check(st, "lora_merge")
+    return w_out

@@ -1,0 +1,76 @@
+"""In-tree build of liblora.so (sm_100a) with nvcc.
+
+    python -m paper_2403_11366_b200.build [--force]
+
+Produces paper_2403_11366_b200/liblora.so next to this file.  The library is
+statically linked against cudart; the driver API (cuTensorMapEncodeTiled) is
+resolved at run time and NCCL is dlopen'ed by lora_comm_init, so the library
+loads (and can be validated) on a machine without a GPU.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+INCLUDE = os.path.join(ROOT, "include")
+LIB = os.path.join(PKG, "liblora.so")
+SOURCES = ["lora_gemm.cu", "lora_aux.cu", "lora_api.cpp", "lora_comm.cpp"]
+HEADERS = ["sm100_ptx.cuh", "lora_kernels.h", "lora_internal.h"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _nccl_include() -> str:
+    try:
+        import nvidia.nccl  # noqa: F401  (pip wheel nvidia-nccl-cu12, same as torch's)
+        base = os.path.dirname(nvidia.nccl.__file__) if getattr(nvidia.nccl, "__file__", None) \
+            else list(nvidia.nccl.__path__)[0]
+        inc = os.path.join(base, "include")
+        if os.path.exists(os.path.join(inc, "nccl.h")):
+            return inc
+    except Exception:
+        pass
+    return "/usr/include"
+
+
+def nccl_library() -> str | None:
+    """Path of the NCCL shared library torch uses (for LORA_NCCL_LIB)."""
+    try:
+        import nvidia.nccl
+        base = list(nvidia.nccl.__path__)[0]
+        p = os.path.join(base, "lib", "libnccl.so.2")
+        if os.path.exists(p):
+            return p
+    except Exception:
+        pass
+    return None
+
+
+def _stale() -> bool:
+    if not os.path.exists(LIB):
+        return True
+    t = os.path.getmtime(LIB)
+    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS] + [os.path.join(INCLUDE, "lora.h")]
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and not _stale():
+        return LIB
+    nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+    cmd = [nvcc, *ARCH, "-O3", "-std=c++17", "-lineinfo", "-shared", "-Xcompiler", "-fPIC",
+           "-Xptxas", "-v" if verbose else "-O3",
+           "-I", INCLUDE, "-I", CSRC, "-I", _nccl_include(),
+           "-DLORA_BUILD", "-o", LIB + ".tmp",
+           *[os.path.join(CSRC, f) for f in SOURCES], "-ldl", "-lpthread"]
+    subprocess.check_call(cmd)
+    os.replace(LIB + ".tmp", LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+    print(LIB)

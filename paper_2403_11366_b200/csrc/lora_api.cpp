@@ -1,0 +1,428 @@
+// lora_api.cpp -- C ABI of liblora.so (see include/lora.h for the contract).
+//
+// Validation is synchronous and complete before anything is enqueued; every
+// compute step runs in the sm_100a kernels of lora_gemm.cu / lora_aux.cu.
+// There is no CPU fallback: a missing or non-sm_100 device is an error.
+#include "lora.h"
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "lora_internal.h"
+#include "lora_kernels.h"
+
+using namespace lora_sm100;
+
+namespace lora_host {
+
+static thread_local std::string g_last_error;
+static thread_local int g_last_launches = 0;
+
+lora_status fail(lora_status st, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return st;
+}
+
+void set_launches(int n) { g_last_launches = n; }
+int get_launches() { return g_last_launches; }
+
+lora_status cuda_fail(cudaError_t e, const char* what) {
+    return fail(LORA_ERR_CUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+// ------------------------------------------------------------ device info
+struct DevInfo {
+    int sms = 0;
+    int major = 0, minor = 0;
+    bool ok = false;
+};
+
+static lora_status device_info(DevInfo* out) {
+    static std::mutex mu;
+    static DevInfo cache[64];
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    if (dev < 0 || dev >= 64) return fail(LORA_ERR_CUDA, "device ordinal %d out of range", dev);
+    std::lock_guard<std::mutex> lk(mu);
+    if (!cache[dev].ok) {
+        DevInfo d;
+        if ((e = cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess)
+            return cuda_fail(e, "cudaDeviceGetAttribute(SM count)");
+        cudaDeviceGetAttribute(&d.major, cudaDevAttrComputeCapabilityMajor, dev);
+        cudaDeviceGetAttribute(&d.minor, cudaDevAttrComputeCapabilityMinor, dev);
+        d.ok = true;
+        cache[dev] = d;
+    }
+    *out = cache[dev];
+    if (!(out->major == 10 && out->minor == 0))
+        return fail(LORA_ERR_UNSUPPORTED, "device %d is sm_%d%d; liblora.so is built for sm_100a (B200)",
+                    dev, out->major, out->minor);
+    return LORA_OK;
+}
+
+// ------------------------------------------------------------ TMA descriptors
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                                  CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                  CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    return fn;
+}
+
+// 2-D bf16 tensor [outer, inner] (row-major, row pitch row_bytes), box
+// [box_outer, box_inner].  Out-of-bounds box elements read as zero.
+static lora_status encode_2d(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer,
+                             uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer, int swizzle_bytes,
+                             const char* name) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return fail(LORA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
+    cuuint64_t dims[2] = {inner, outer};
+    cuuint64_t strides[1] = {row_bytes};
+    cuuint32_t box[2] = {box_inner, box_outer};
+    cuuint32_t estr[2] = {1, 1};
+    CUtensorMapSwizzle sw = swizzle_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                            : swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                  : CU_TENSOR_MAP_SWIZZLE_32B;
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        return fail(LORA_ERR_CUDA, "cuTensorMapEncodeTiled(%s: %llu x %llu, box %u x %u) failed: %d", name,
+                    (unsigned long long)outer, (unsigned long long)inner, box_outer, box_inner, (int)r);
+    return LORA_OK;
+}
+
+// ------------------------------------------------------------ validation
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+static bool overlap(const void* a, size_t na, const void* b, size_t nb) {
+    if (!a || !b || na == 0 || nb == 0) return false;
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(a), b0 = reinterpret_cast<uintptr_t>(b);
+    return a0 < b0 + nb && b0 < a0 + na;
+}
+
+lora_status check_dims(const lora_dims* d, bool need_tokens) {
+    if (!d) return fail(LORA_ERR_INVALID, "dims is NULL");
+    if (need_tokens && d->tokens < 0)
+        return fail(LORA_ERR_SHAPE, "tokens = %lld must be >= 0", (long long)d->tokens);
+    if (d->d_in < 8 || d->d_in % 8 != 0)
+        return fail(LORA_ERR_SHAPE, "d_in = %lld must be a positive multiple of 8", (long long)d->d_in);
+    if (d->d_out < 8 || d->d_out % 8 != 0)
+        return fail(LORA_ERR_SHAPE, "d_out = %lld must be a positive multiple of 8", (long long)d->d_out);
+    if (d->rank < 1) return fail(LORA_ERR_SHAPE, "rank = %d must be >= 1", d->rank);
+    if (d->rank > 64) return fail(LORA_ERR_UNSUPPORTED, "rank = %d > 64 is not supported", d->rank);
+    if (d->d_in > (int64_t(1) << 31) || d->d_out > (int64_t(1) << 31) || d->tokens > (int64_t(1) << 31))
+        return fail(LORA_ERR_UNSUPPORTED, "dimension exceeds 2^31");
+    if (!std::isfinite(d->alpha)) return fail(LORA_ERR_INVALID, "alpha is not finite");
+    return LORA_OK;
+}
+
+int r_pad_of(int r) { return r <= 16 ? 16 : (r <= 32 ? 32 : 64); }
+
+static size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
+
+struct FwdWs {
+    size_t bpad, total;
+};
+static FwdWs fwd_ws(const lora_dims* d) {
+    FwdWs w;
+    w.bpad = 0;
+    w.total = align256(size_t(d->d_out) * r_pad_of(d->rank) * 2);
+    return w;
+}
+
+constexpr int kPlanSMs = 148;  // workspace sizing must not depend on the device
+
+struct BwdWs {
+    size_t bt, at, gh, h, part, total;
+    GradReducePlan plan;
+};
+static BwdWs bwd_ws(const lora_dims* d) {
+    BwdWs w;
+    const int64_t T = d->tokens, n = d->d_in, m = d->d_out;
+    const int r = d->rank;
+    w.plan = plan_grad_reduce(T > 0 ? T : 1, n, m, r, kPlanSMs);
+    size_t off = 0;
+    w.bt = off; off += align256(size_t(r) * m * 2);
+    w.at = off; off += align256(size_t(n) * r_pad_of(r) * 2);
+    w.gh = off; off += align256(size_t(T > 0 ? T : 0) * r * 4);
+    w.h = off; off += align256(size_t(T > 0 ? T : 0) * r * 4);
+    w.part = off; off += align256(grad_reduce_partial_bytes(w.plan, n, m, r));
+    w.total = off;
+    return w;
+}
+
+// ------------------------------------------------------------ forward
+lora_status fwd_impl(const lora_dims* d, const void* x, const void* w0, const void* a, const void* b,
+                     const void* bias, void* y, float* h_out, void* ws, size_t ws_bytes,
+                     cudaStream_t stream, int* launches) {
+    lora_status st = check_dims(d, true);
+    if (st != LORA_OK) return st;
+    const int64_t T = d->tokens, n = d->d_in, m = d->d_out;
+    const int r = d->rank;
+    if (!w0 || !a || !b || (T > 0 && (!x || !y)))
+        return fail(LORA_ERR_INVALID, "lora_linear_fwd: x, w0, a, b, y must be non-NULL");
+    const void* ptrs[] = {x, w0, a, b, bias, y, h_out, ws};
+    const char* names[] = {"x", "w0", "a", "b", "bias", "y", "h_out", "workspace"};
+    for (int i = 0; i < 8; ++i)
+        if (ptrs[i] && !aligned16(ptrs[i]))
+            return fail(LORA_ERR_ALIGN, "lora_linear_fwd: %s = %p is not 16-byte aligned", names[i], ptrs[i]);
+    const FwdWs W = fwd_ws(d);
+    if (!ws || ws_bytes < W.total)
+        return fail(LORA_ERR_WORKSPACE, "lora_linear_fwd: workspace %zu bytes < required %zu", ws ? ws_bytes : 0,
+                    W.total);
+    const size_t yb = size_t(T) * m * 2, hb = h_out ? size_t(T) * r * 4 : 0;
+    const void* ins[] = {x, w0, a, b, bias};
+    const size_t inb[] = {size_t(T) * n * 2, size_t(m) * n * 2, size_t(r) * n * 2, size_t(m) * r * 2,
+                          bias ? size_t(m) * 2 : 0};
+    for (int i = 0; i < 5; ++i) {
+        if (overlap(y, yb, ins[i], inb[i]) || overlap(h_out, hb, ins[i], inb[i]) ||
+            overlap(ws, W.total, ins[i], inb[i]))
+            return fail(LORA_ERR_INVALID, "lora_linear_fwd: an output/workspace overlaps input %s", names[i]);
+    }
+    if (overlap(y, yb, h_out, hb)) return fail(LORA_ERR_INVALID, "lora_linear_fwd: y overlaps h_out");
+    DevInfo dev;
+    if ((st = device_info(&dev)) != LORA_OK) return st;
+    if (T == 0) return LORA_OK;
+
+    const int rp = r_pad_of(r);
+    const int BN = fused_gemm_block_n(rp);
+    auto* bpad = reinterpret_cast<__nv_bfloat16*>(static_cast<uint8_t*>(ws) + W.bpad);
+    cudaError_t e = launch_pack(static_cast<const __nv_bfloat16*>(a), static_cast<const __nv_bfloat16*>(b), n, m, r,
+                                rp, bpad, nullptr, nullptr, dev.sms, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "pack launch");
+    ++*launches;
+    FusedGemmMaps maps;
+    if ((st = encode_2d(&maps.act, x, n, T, n * 2, 64, 128, 128, "x")) != LORA_OK) return st;
+    if ((st = encode_2d(&maps.w, w0, n, m, n * 2, 64, BN, 128, "w0")) != LORA_OK) return st;
+    if ((st = encode_2d(&maps.nar, a, n, r, n * 2, 64, rp, 128, "a")) != LORA_OK) return st;
+    if ((st = encode_2d(&maps.tail, bpad, rp, m, rp * 2, rp, BN, rp * 2, "b_pad")) != LORA_OK) return st;
+    FusedGemmParams p;
+    p.T = T; p.K = n; p.N_out = m; p.r = r;
+    p.scale = d->alpha / static_cast<float>(r);
+    p.bias = static_cast<const __nv_bfloat16*>(bias);
+    p.out = static_cast<__nv_bfloat16*>(y);
+    p.side_out = h_out;
+    e = launch_fused_gemm(kModeFwd, rp, maps, p, dev.sms, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "fused forward launch");
+    ++*launches;
+    return LORA_OK;
+}
+
+// ------------------------------------------------------------ backward
+lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const void* a, const void* b,
+                     const float* h_saved, const void* dy, void* dx, float* da, float* db, int accumulate,
+                     void* ws, size_t ws_bytes, cudaStream_t stream, int* launches) {
+    lora_status st = check_dims(d, true);
+    if (st != LORA_OK) return st;
+    const int64_t T = d->tokens, n = d->d_in, m = d->d_out;
+    const int r = d->rank;
+    if (!w0 || !a || !b || (T > 0 && (!x || !dy)))
+        return fail(LORA_ERR_INVALID, "lora_linear_bwd: x, w0, a, b, dy must be non-NULL");
+    if (accumulate != 0 && accumulate != 1) return fail(LORA_ERR_INVALID, "accumulate must be 0 or 1");
+    const void* ptrs[] = {x, w0, a, b, h_saved, dy, dx, da, db, ws};
+    const char* names[] = {"x", "w0", "a", "b", "h_saved", "dy", "dx", "da", "db", "workspace"};
+    for (int i = 0; i < 10; ++i)
+        if (ptrs[i] && !aligned16(ptrs[i]))
+            return fail(LORA_ERR_ALIGN, "lora_linear_bwd: %s = %p is not 16-byte aligned", names[i], ptrs[i]);
+    const BwdWs W = bwd_ws(d);
+    if (!ws || ws_bytes < W.total)
+        return fail(LORA_ERR_WORKSPACE, "lora_linear_bwd: workspace %zu bytes < required %zu", ws ? ws_bytes : 0,
+                    W.total);
+    const void* ins[] = {x, w0, a, b, h_saved, dy};
+    const size_t inb[] = {size_t(T) * n * 2, size_t(m) * n * 2, size_t(r) * n * 2, size_t(m) * r * 2,
+                          h_saved ? size_t(T) * r * 4 : 0, size_t(T) * m * 2};
+    const void* outs[] = {dx, da, db, ws};
+    const size_t outb[] = {dx ? size_t(T) * n * 2 : 0, da ? size_t(r) * n * 4 : 0, db ? size_t(m) * r * 4 : 0,
+                           W.total};
+    for (int o = 0; o < 4; ++o) {
+        for (int i = 0; i < 6; ++i)
+            if (overlap(outs[o], outb[o], ins[i], inb[i]))
+                return fail(LORA_ERR_INVALID, "lora_linear_bwd: output %s overlaps input %s",
+                            o == 3 ? "workspace" : names[6 + o], names[i]);
+        for (int o2 = o + 1; o2 < 4; ++o2)
+            if (overlap(outs[o], outb[o], outs[o2], outb[o2]))
+                return fail(LORA_ERR_INVALID, "lora_linear_bwd: outputs overlap each other");
+    }
+    DevInfo dev;
+    if ((st = device_info(&dev)) != LORA_OK) return st;
+    cudaError_t e;
+    if (T == 0) {
+        if (!accumulate) {
+            if ((e = launch_fill_zero(da, int64_t(r) * n, stream)) != cudaSuccess) return cuda_fail(e, "memset dA");
+            if ((e = launch_fill_zero(db, int64_t(m) * r, stream)) != cudaSuccess) return cuda_fail(e, "memset dB");
+        }
+        return LORA_OK;
+    }
+    const float s = d->alpha / static_cast<float>(r);
+    const int rp = r_pad_of(r);
+    uint8_t* wsb = static_cast<uint8_t*>(ws);
+    auto* bt = reinterpret_cast<__nv_bfloat16*>(wsb + W.bt);
+    auto* at = reinterpret_cast<__nv_bfloat16*>(wsb + W.at);
+    float* gh = reinterpret_cast<float*>(wsb + W.gh);
+    float* hbuf = reinterpret_cast<float*>(wsb + W.h);
+    float* part = reinterpret_cast<float*>(wsb + W.part);
+    const auto* xa = static_cast<const __nv_bfloat16*>(x);
+    const auto* aa = static_cast<const __nv_bfloat16*>(a);
+    const auto* ba = static_cast<const __nv_bfloat16*>(b);
+    const auto* dya = static_cast<const __nv_bfloat16*>(dy);
+    const bool need_gh = dx || da;
+    const bool need_h = db && !h_saved;
+
+    if (need_gh) {
+        if ((e = launch_pack(aa, ba, n, m, r, rp, nullptr, bt, dx ? at : nullptr, dev.sms, stream)) != cudaSuccess)
+            return cuda_fail(e, "pack launch");
+        ++*launches;
+    }
+    if (dx) {
+        const int BN = fused_gemm_block_n(rp);
+        FusedGemmMaps maps;
+        if ((st = encode_2d(&maps.act, dy, m, T, m * 2, 64, 128, 128, "dy")) != LORA_OK) return st;
+        if ((st = encode_2d(&maps.w, w0, n, m, n * 2, 64, 64, 128, "w0")) != LORA_OK) return st;
+        if ((st = encode_2d(&maps.nar, bt, m, r, m * 2, 64, rp, 128, "b^T")) != LORA_OK) return st;
+        if ((st = encode_2d(&maps.tail, at, rp, n, rp * 2, rp, BN, rp * 2, "a^T_pad")) != LORA_OK) return st;
+        FusedGemmParams p;
+        p.T = T; p.K = m; p.N_out = n; p.r = r; p.scale = s;
+        p.bias = nullptr;
+        p.out = static_cast<__nv_bfloat16*>(dx);
+        p.side_out = gh;
+        if ((e = launch_fused_gemm(kModeDx, rp, maps, p, dev.sms, stream)) != cudaSuccess)
+            return cuda_fail(e, "fused dX launch");
+        ++*launches;
+    } else if (da) {
+        // gh = s dY B via the row-projection kernel on B^T [r, m]
+        if ((e = launch_rowproj(dya, T, m, bt, r, s, gh, stream)) != cudaSuccess) return cuda_fail(e, "gh rowproj");
+        ++*launches;
+    }
+    const float* hsrc = h_saved;
+    if (need_h) {
+        if ((e = launch_rowproj(xa, T, n, aa, r, 1.0f, hbuf, stream)) != cudaSuccess) return cuda_fail(e, "h rowproj");
+        ++*launches;
+        hsrc = hbuf;
+    }
+    if (da || db) {
+        int nl = 0;
+        e = launch_grad_reduce(W.plan, T, n, m, r, s, xa, gh, dya, hsrc, part, da, db, accumulate, stream, &nl);
+        if (e != cudaSuccess) return cuda_fail(e, "grad reduce launch");
+        *launches += nl;
+    }
+    return LORA_OK;
+}
+
+lora_status merge_impl(const lora_dims* d, const void* w0, const void* a, const void* b, void* w_out,
+                       cudaStream_t stream, int* launches) {
+    lora_status st = check_dims(d, false);
+    if (st != LORA_OK) return st;
+    const int64_t n = d->d_in, m = d->d_out;
+    const int r = d->rank;
+    if (!w0 || !a || !b || !w_out) return fail(LORA_ERR_INVALID, "lora_merge: w0, a, b, w_out must be non-NULL");
+    const void* ptrs[] = {w0, a, b, w_out};
+    const char* names[] = {"w0", "a", "b", "w_out"};
+    for (int i = 0; i < 4; ++i)
+        if (!aligned16(ptrs[i]))
+            return fail(LORA_ERR_ALIGN, "lora_merge: %s = %p is not 16-byte aligned", names[i], ptrs[i]);
+    const size_t wb = size_t(m) * n * 2;
+    if (w_out != w0 && overlap(w_out, wb, w0, wb))
+        return fail(LORA_ERR_INVALID, "lora_merge: w_out partially overlaps w0 (only w_out == w0 is allowed)");
+    if (overlap(w_out, wb, a, size_t(r) * n * 2) || overlap(w_out, wb, b, size_t(m) * r * 2))
+        return fail(LORA_ERR_INVALID, "lora_merge: w_out overlaps a or b");
+    DevInfo dev;
+    if ((st = device_info(&dev)) != LORA_OK) return st;
+    cudaError_t e = launch_merge(static_cast<const __nv_bfloat16*>(w0), static_cast<const __nv_bfloat16*>(a),
+                                 static_cast<const __nv_bfloat16*>(b), n, m, r, d->alpha / static_cast<float>(r),
+                                 static_cast<__nv_bfloat16*>(w_out), stream);
+    if (e != cudaSuccess) return cuda_fail(e, "merge launch");
+    ++*launches;
+    return LORA_OK;
+}
+
+size_t fwd_workspace(const lora_dims* d) { return check_dims(d, true) == LORA_OK ? fwd_ws(d).total : 0; }
+size_t bwd_workspace(const lora_dims* d) { return check_dims(d, true) == LORA_OK ? bwd_ws(d).total : 0; }
+
+}  // namespace lora_host
+
+// ============================================================ C ABI
+using namespace lora_host;
+
+extern "C" {
+
+size_t lora_linear_fwd_workspace_bytes(const lora_dims* dims) { return fwd_workspace(dims); }
+size_t lora_linear_bwd_workspace_bytes(const lora_dims* dims) { return bwd_workspace(dims); }
+
+lora_status lora_linear_fwd(const lora_dims* dims, const void* x, const void* w0, const void* a, const void* b,
+                            const void* bias, void* y, float* h_out, void* workspace, size_t workspace_bytes,
+                            void* stream) {
+    int launches = 0;
+    lora_status st = fwd_impl(dims, x, w0, a, b, bias, y, h_out, workspace, workspace_bytes,
+                              static_cast<cudaStream_t>(stream), &launches);
+    set_launches(launches);
+    return st;
+}
+
+lora_status lora_linear_bwd(const lora_dims* dims, const void* x, const void* w0, const void* a, const void* b,
+                            const float* h_saved, const void* dy, void* dx, float* da, float* db, int accumulate,
+                            void* workspace, size_t workspace_bytes, void* stream) {
+    int launches = 0;
+    lora_status st = bwd_impl(dims, x, w0, a, b, h_saved, dy, dx, da, db, accumulate, workspace, workspace_bytes,
+                              static_cast<cudaStream_t>(stream), &launches);
+    set_launches(launches);
+    return st;
+}
+
+lora_status lora_merge(const lora_dims* dims, const void* w0, const void* a, const void* b, void* w_out,
+                       void* stream) {
+    int launches = 0;
+    lora_status st = merge_impl(dims, w0, a, b, w_out, static_cast<cudaStream_t>(stream), &launches);
+    set_launches(launches);
+    return st;
+}
+
+const char* lora_status_string(lora_status s) {
+    switch (s) {
+        case LORA_OK: return "LORA_OK";
+        case LORA_ERR_INVALID: return "LORA_ERR_INVALID";
+        case LORA_ERR_SHAPE: return "LORA_ERR_SHAPE";
+        case LORA_ERR_ALIGN: return "LORA_ERR_ALIGN";
+        case LORA_ERR_UNSUPPORTED: return "LORA_ERR_UNSUPPORTED";
+        case LORA_ERR_CUDA: return "LORA_ERR_CUDA";
+        case LORA_ERR_NCCL: return "LORA_ERR_NCCL";
+        case LORA_ERR_WORKSPACE: return "LORA_ERR_WORKSPACE";
+    }
+    return "LORA_ERR_UNKNOWN";
+}
+
+const char* lora_last_error(void) { return g_last_error.c_str(); }
+
+int lora_version(void) { return 100; }
+
+lora_status lora_device_check(void) {
+    DevInfo d;
+    return device_info(&d);
+}
+
+int lora_last_launch_count(void) { return get_launches(); }
+
+}  // extern "C"

@@ -1,0 +1,216 @@
+// lora_comm.cpp -- tensor-parallel LoRA linear over NCCL (NVLink 5 / NVSwitch).
+//
+// "JORA parallelizes all parameters ... Projection and
+// Embedding layers are sharded on the non-sequential dimension."  Read as
+// Megatron column/row parallelism inside the block (R10); A/B are
+// sharded with the side of W0 they touch, the other factor is replicated
+// (R11); partial results are SUMMED with no 1/N (R12).
+//   COLUMN (q, k, v, gate, up): W0, B split on d_out; A replicated.
+//     fwd  y_local = lora_fwd(local)                       -- no collective
+//     bwd  dx = sum_ranks(dY_i W0_i + gh_i A)   all-reduce bf16 [T, n]
+//          dA = sum_ranks(gh_i^T x)             all-reduce fp32 [r, n]
+//          dB_i = s dY_i^T h                    local
+//   ROW (o, down): W0, A split on d_in; B replicated.
+//     fwd  y = sum_ranks(x_i W0_i^T + s (x_i A_i^T) B^T)   all-reduce bf16 [T, m]
+//     bwd  dx_i, dA_i local; dB = sum_ranks(s dY^T h_i)   all-reduce fp32 [m, r]
+// NCCL is resolved with dlopen at lora_comm_init, so single-GPU use of
+// liblora.so never needs libnccl.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cstdlib>
+#include <cstring>
+
+#include "lora_internal.h"
+#include "lora_kernels.h"
+
+using namespace lora_host;
+
+namespace {
+
+struct NcclApi {
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*);
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int);
+    ncclResult_t (*CommDestroy)(ncclComm_t);
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t);
+    const char* (*GetErrorString)(ncclResult_t);
+    bool ok = false;
+};
+
+NcclApi* nccl() {
+    static NcclApi api;
+    static bool tried = false;
+    if (tried) return api.ok ? &api : nullptr;
+    tried = true;
+    const char* cands[] = {getenv("LORA_NCCL_LIB"), "libnccl.so.2", "libnccl.so"};
+    void* h = nullptr;
+    for (const char* c : cands) {
+        if (!c || !*c) continue;
+        h = dlopen(c, RTLD_NOW | RTLD_GLOBAL);
+        if (h) break;
+    }
+    if (!h) return nullptr;
+    api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+    api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
+    api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
+    api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(dlsym(h, "ncclAllReduce"));
+    api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+    api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllReduce && api.GetErrorString;
+    return api.ok ? &api : nullptr;
+}
+
+lora_status nccl_fail(NcclApi* api, ncclResult_t r, const char* what) {
+    return fail(LORA_ERR_NCCL, "%s: %s", what, api ? api->GetErrorString(r) : "NCCL unavailable");
+}
+
+size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
+
+}  // namespace
+
+struct lora_comm {
+    ncclComm_t comm;
+    int nranks;
+    int rank;
+};
+
+static_assert(sizeof(ncclUniqueId) == LORA_COMM_ID_BYTES, "NCCL unique id size");
+
+static lora_status allreduce_impl(lora_comm* c, void* buf, size_t count, lora_dtype dt, cudaStream_t st) {
+    NcclApi* api = nccl();
+    if (!api) return fail(LORA_ERR_NCCL, "libnccl could not be loaded (set LORA_NCCL_LIB)");
+    if (count == 0 || c->nranks == 1) return LORA_OK;
+    ncclResult_t r = api->AllReduce(buf, buf, count, dt == LORA_DT_F32 ? ncclFloat32 : ncclBfloat16, ncclSum,
+                                    c->comm, st);
+    if (r != ncclSuccess) return nccl_fail(api, r, "ncclAllReduce");
+    return LORA_OK;
+}
+
+extern "C" {
+
+lora_status lora_comm_unique_id(uint8_t id[LORA_COMM_ID_BYTES]) {
+    if (!id) return fail(LORA_ERR_INVALID, "id is NULL");
+    NcclApi* api = nccl();
+    if (!api) return fail(LORA_ERR_NCCL, "libnccl could not be loaded (set LORA_NCCL_LIB)");
+    ncclUniqueId u;
+    ncclResult_t r = api->GetUniqueId(&u);
+    if (r != ncclSuccess) return nccl_fail(api, r, "ncclGetUniqueId");
+    memcpy(id, &u, sizeof u);
+    return LORA_OK;
+}
+
+lora_status lora_comm_init(int nranks, int rank, const uint8_t id[LORA_COMM_ID_BYTES], lora_comm** out) {
+    if (!out || !id) return fail(LORA_ERR_INVALID, "lora_comm_init: NULL argument");
+    if (nranks < 1 || rank < 0 || rank >= nranks)
+        return fail(LORA_ERR_INVALID, "lora_comm_init: rank %d / nranks %d invalid", rank, nranks);
+    NcclApi* api = nccl();
+    if (!api) return fail(LORA_ERR_NCCL, "libnccl could not be loaded (set LORA_NCCL_LIB)");
+    ncclUniqueId u;
+    memcpy(&u, id, sizeof u);
+    lora_comm* c = new lora_comm();
+    c->nranks = nranks;
+    c->rank = rank;
+    ncclResult_t r = api->CommInitRank(&c->comm, nranks, u, rank);
+    if (r != ncclSuccess) {
+        delete c;
+        return nccl_fail(api, r, "ncclCommInitRank");
+    }
+    *out = c;
+    return LORA_OK;
+}
+
+lora_status lora_comm_destroy(lora_comm* c) {
+    if (!c) return LORA_OK;
+    NcclApi* api = nccl();
+    if (api) api->CommDestroy(c->comm);
+    delete c;
+    return LORA_OK;
+}
+
+int lora_comm_size(const lora_comm* c) { return c ? c->nranks : 0; }
+int lora_comm_rank(const lora_comm* c) { return c ? c->rank : -1; }
+
+lora_status lora_allreduce(lora_comm* c, void* buf, size_t count, lora_dtype dt, void* stream) {
+    if (!c) return fail(LORA_ERR_INVALID, "lora_allreduce: comm is NULL");
+    if (dt != LORA_DT_F32 && dt != LORA_DT_BF16) return fail(LORA_ERR_INVALID, "lora_allreduce: bad dtype");
+    if (count && !buf) return fail(LORA_ERR_INVALID, "lora_allreduce: buf is NULL");
+    return allreduce_impl(c, buf, count, dt, static_cast<cudaStream_t>(stream));
+}
+
+size_t lora_tp_linear_bwd_workspace_bytes(const lora_dims* local) {
+    const size_t base = bwd_workspace(local);
+    if (!base) return 0;
+    const size_t scratch = size_t(local->rank) * (local->d_in > local->d_out ? local->d_in : local->d_out) * 4;
+    return base + align256(scratch);
+}
+
+lora_status lora_tp_linear_fwd(lora_comm* c, lora_tp_mode mode, const lora_dims* local, const void* x,
+                               const void* w0, const void* a, const void* b, const void* bias, void* y,
+                               float* h_out, void* workspace, size_t workspace_bytes, void* stream) {
+    int launches = 0;
+    if (!c) return fail(LORA_ERR_INVALID, "lora_tp_linear_fwd: comm is NULL");
+    if (mode != LORA_TP_COLUMN && mode != LORA_TP_ROW) return fail(LORA_ERR_INVALID, "bad TP mode");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    // row mode: the (unsharded) bias is added once, by rank 0
+    const void* b0 = (mode == LORA_TP_ROW && c->rank != 0) ? nullptr : bias;
+    lora_status s = fwd_impl(local, x, w0, a, b, b0, y, h_out, workspace, workspace_bytes, st, &launches);
+    set_launches(launches);
+    if (s != LORA_OK || mode == LORA_TP_COLUMN) return s;
+    return allreduce_impl(c, y, size_t(local->tokens) * local->d_out, LORA_DT_BF16, st);
+}
+
+lora_status lora_tp_linear_bwd(lora_comm* c, lora_tp_mode mode, const lora_dims* local, const void* x,
+                               const void* w0, const void* a, const void* b, const float* h_saved,
+                               const void* dy, void* dx, float* da, float* db, int accumulate,
+                               int reduce_lora_grads, void* workspace, size_t workspace_bytes, void* stream) {
+    int launches = 0;
+    if (!c) return fail(LORA_ERR_INVALID, "lora_tp_linear_bwd: comm is NULL");
+    if (mode != LORA_TP_COLUMN && mode != LORA_TP_ROW) return fail(LORA_ERR_INVALID, "bad TP mode");
+    lora_status s = check_dims(local, true);
+    if (s != LORA_OK) return s;
+    const size_t need = lora_tp_linear_bwd_workspace_bytes(local);
+    if (!workspace || workspace_bytes < need)
+        return fail(LORA_ERR_WORKSPACE, "lora_tp_linear_bwd: workspace %zu < required %zu", workspace_bytes, need);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t base = bwd_workspace(local);
+    float* scratch = reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) + base);
+    // the gradient that is a partial sum on this rank
+    float* partial_grad = (mode == LORA_TP_COLUMN) ? da : db;
+    const size_t pcount = (mode == LORA_TP_COLUMN) ? size_t(local->rank) * local->d_in
+                                                   : size_t(local->d_out) * local->rank;
+    const bool via_scratch = reduce_lora_grads && accumulate && partial_grad && c->nranks > 1;
+    float* da_out = (via_scratch && mode == LORA_TP_COLUMN) ? scratch : da;
+    float* db_out = (via_scratch && mode == LORA_TP_ROW) ? scratch : db;
+    // bwd_impl sees a workspace that excludes the scratch tail
+    if (via_scratch) {
+        // da/db written with overwrite semantics into scratch, then reduced and added
+        s = bwd_impl(local, x, w0, a, b, h_saved, dy, dx, da_out, db_out, 0, workspace, base, st, &launches);
+        if (s == LORA_OK && mode == LORA_TP_COLUMN && db)
+            s = bwd_impl(local, x, w0, a, b, h_saved, dy, nullptr, nullptr, db, 1, workspace, base, st, &launches);
+        if (s == LORA_OK && mode == LORA_TP_ROW && da)
+            s = bwd_impl(local, x, w0, a, b, h_saved, dy, nullptr, da, nullptr, 1, workspace, base, st, &launches);
+    } else {
+        s = bwd_impl(local, x, w0, a, b, h_saved, dy, dx, da, db, accumulate, workspace, base, st, &launches);
+    }
+    if (s != LORA_OK) {
+        set_launches(launches);
+        return s;
+    }
+    if (mode == LORA_TP_COLUMN && dx) {
+        s = allreduce_impl(c, dx, size_t(local->tokens) * local->d_in, LORA_DT_BF16, st);
+        if (s != LORA_OK) return s;
+    }
+    if (reduce_lora_grads && partial_grad) {
+        float* red = via_scratch ? scratch : partial_grad;
+        s = allreduce_impl(c, red, pcount, LORA_DT_F32, st);
+        if (s != LORA_OK) return s;
+        if (via_scratch) {
+            cudaError_t e = lora_sm100::launch_add_f32(partial_grad, scratch, static_cast<int64_t>(pcount), st);
+            if (e != cudaSuccess) return cuda_fail(e, "grad accumulate launch");
+            ++launches;
+        }
+    }
+    set_launches(launches);
+    return LORA_OK;
+}
+
+}  // extern "C"

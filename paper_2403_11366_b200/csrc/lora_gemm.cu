@@ -1,0 +1,352 @@
+// lora_gemm.cu -- fused LoRA-linear tensor-core kernels for sm_100a (B200).
+//
+// K1 (MODE_FWD), Eq. 1 line 1 in row-vector form:
+//     acc  = x W0^T            (base GEMM, tcgen05, fp32 accumulator in TMEM)
+//     h    = x A^T             (same pass: A's r_pad rows are appended to the
+//                               W0 tile, so ONE 128 x 256 MMA per k-step
+//                               produces BN = 256 - r_pad output columns and
+//                               the r_pad columns of h)
+//     y    = bf16(acc + bf16(s h) B^T + b0)   (epilogue: a K = r_pad "tail"
+//                               MMA adds the low-rank update into the same
+//                               TMEM accumulator, then one RNE to bf16)
+// K2 (MODE_DX), the input gradient of Eq. 1 (W0 frozen):
+//     acc  = dY W0             (W0 [m, n] read as an MN-major B operand: no
+//                               transposed weight copy)
+//     gh   = s dY B            (same pass: narrow N = r_pad MMA on the dY tile
+//                               already in shared memory)
+//     dX   = bf16(acc + bf16(gh) A)  (epilogue tail MMA)
+//
+// Structure (one CTA per SM, persistent over output tiles, 6 warps):
+//   warp 0     : TMA producer (cp.async.bulk.tensor, SWIZZLE_128B, an
+//                STAGES-deep shared-memory ring guarded by mbarriers)
+//   warp 1     : tcgen05.mma issuer (one elected thread), TMEM allocator
+//   warps 2..5 : epilogue (tcgen05.ld from TMEM, side output h / gh, tail
+//                MMA, bf16 conversion, global stores)
+// TMEM holds two 256-column fp32 accumulators (512 columns), so the epilogue
+// of tile i overlaps the main loop of tile i+1.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "lora_kernels.h"
+#include "sm100_ptx.cuh"
+
+namespace lora_sm100 {
+
+constexpr int BM = 128;            // UMMA M (rows = tokens per tile)
+constexpr int BK = 64;             // k-block: 64 bf16 = one 128-byte swizzle row
+constexpr int UMMA_K = 16;         // K per tcgen05.mma kind::f16
+constexpr int NT = 256;            // TMEM columns per accumulator buffer
+constexpr int NUM_THREADS = 192;   // 6 warps
+constexpr int SMEM_LIMIT = 227 * 1024;
+
+__host__ __device__ constexpr int round_up(int v, int a) { return (v + a - 1) / a * a; }
+__host__ __device__ constexpr int cmin(int a, int b) { return a < b ? a : b; }
+
+template <int MODE, int R_PAD>
+struct GemmCfg {
+    static constexpr int BN = NT - R_PAD;                         // output columns per tile
+    static constexpr int A_BYTES = BM * BK * 2;                   // activation tile (16 KiB)
+    static constexpr int NB64 = (BN + 63) / 64;                   // MN-major W0 column blocks (dx)
+    static constexpr int B_BYTES = (MODE == kModeFwd) ? NT * BK * 2 : NB64 * 64 * BK * 2;
+    static constexpr int N_BYTES = (MODE == kModeFwd) ? 0 : R_PAD * BK * 2;  // narrow operand
+    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES + N_BYTES;
+    static constexpr int TAIL_ROW = R_PAD * 2;                    // 32 / 64 / 128 bytes
+    static constexpr uint32_t TAIL_LAYOUT =
+        TAIL_ROW == 32 ? kLayoutSW32 : (TAIL_ROW == 64 ? kLayoutSW64 : kLayoutSW128);
+    static constexpr int TAILB_BYTES = BN * TAIL_ROW;             // B_pad / A^T tile
+    static constexpr int SH_BYTES = BM * TAIL_ROW;                // bf16(s h) / bf16(gh) tile
+    static constexpr int BAR_BYTES = 1024;
+    static constexpr int FIXED = round_up(TAILB_BYTES, 1024) + round_up(SH_BYTES, 1024) +
+                                 BAR_BYTES + 1024 /* alignment slack */;
+    static constexpr int STAGES = cmin(8, (SMEM_LIMIT - FIXED) / STAGE_BYTES);
+    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + FIXED;
+    static_assert(STAGES >= 2, "shared memory budget");
+    static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N");
+    static_assert((BN * 128) % 1024 == 0, "A rows must start on a swizzle atom");
+};
+
+template <int MODE, int R_PAD>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+lora_fused_gemm_kernel(const __grid_constant__ CUtensorMap tm_act,   // x or dY   [T, K]
+                       const __grid_constant__ CUtensorMap tm_w,     // W0        [m, n]
+                       const __grid_constant__ CUtensorMap tm_nar,   // A [r,n] / B^T [r,m]
+                       const __grid_constant__ CUtensorMap tm_tail,  // B_pad [m,R] / A^T_pad [n,R]
+                       const FusedGemmParams p) {
+    using C = GemmCfg<MODE, R_PAD>;
+    constexpr int BN = C::BN;
+
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* stage_base = smem;
+    uint8_t* s_tailb = smem + C::STAGES * C::STAGE_BYTES;
+    uint8_t* s_h = s_tailb + round_up(C::TAILB_BYTES, 1024);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(s_h + round_up(C::SH_BYTES, 1024));
+    uint64_t* full = bars;
+    uint64_t* empty = bars + C::STAGES;
+    uint64_t* tmem_full = bars + 2 * C::STAGES;
+    uint64_t* tmem_empty = tmem_full + 2;
+    uint64_t* tailop_full = tmem_empty + 2;
+    uint64_t* tailop_empty = tailop_full + 1;
+    uint64_t* tail_done = tailop_empty + 1;
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tail_done + 1);
+
+    const int num_t_blks = static_cast<int>((p.T + BM - 1) / BM);
+    const int num_n_blks = static_cast<int>((p.N_out + BN - 1) / BN);
+    const int num_tiles = num_t_blks * num_n_blks;
+    const int num_k_blks = static_cast<int>((p.K + BK - 1) / BK);
+    const uint32_t warp = warp_id();
+    const uint32_t lane = lane_id();
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tm_act);
+        tma_prefetch_desc(&tm_w);
+        tma_prefetch_desc(&tm_nar);
+        tma_prefetch_desc(&tm_tail);
+    }
+    if (warp == 1 && lane == 0) {
+        for (int s = 0; s < C::STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tmem_full[a], 1);
+            mbar_init(&tmem_empty[a], 4);  // one arrive per epilogue warp
+        }
+        mbar_init(tailop_full, 1);
+        mbar_init(tailop_empty, 1);
+        mbar_init(tail_done, 1);
+        fence_mbar_init();
+    }
+    if (warp == 2) tmem_alloc<512>(tmem_holder);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_holder;
+
+    if (warp == 0) {
+        // ===================== TMA producer =====================
+        if (elect_one()) {
+            const uint64_t pol_w = l2_policy_evict_last();
+            uint32_t stage = 0, phase = 0, tl = 0;
+            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++tl) {
+                const int n_blk = tile / num_t_blks;
+                const int t_blk = tile - n_blk * num_t_blks;
+                const int t0 = t_blk * BM;
+                const int n0 = n_blk * BN;
+                for (int kb = 0; kb < num_k_blks; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    uint8_t* sA = stage_base + stage * C::STAGE_BYTES;
+                    uint8_t* sB = sA + C::A_BYTES;
+                    mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+                    const int k0 = kb * BK;
+                    tma_load_2d(sA, &tm_act, k0, t0, &full[stage]);
+                    if constexpr (MODE == kModeFwd) {
+                        tma_load_2d_hint(sB, &tm_w, k0, n0, &full[stage], pol_w);      // W0 rows
+                        tma_load_2d(sB + BN * 128, &tm_nar, k0, 0, &full[stage]);       // A rows
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < C::NB64; ++j)
+                            tma_load_2d_hint(sB + j * (64 * 128), &tm_w, n0 + 64 * j, k0,
+                                             &full[stage], pol_w);
+                        tma_load_2d(sB + C::B_BYTES, &tm_nar, k0, 0, &full[stage]);    // B^T rows
+                    }
+                    if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+                }
+                // tail operand for this tile (B_pad rows n0.. or A^T rows n0..)
+                mbar_wait(tailop_empty, (tl & 1) ^ 1);
+                mbar_arrive_expect_tx(tailop_full, C::TAILB_BYTES);
+                tma_load_2d(s_tailb, &tm_tail, 0, n0, tailop_full);
+            }
+        }
+    } else if (warp == 1) {
+        // ===================== MMA issuer =====================
+        if (elect_one()) {
+            constexpr uint32_t idesc_main = (MODE == kModeFwd) ? make_idesc_bf16(BM, NT, 0, 0)
+                                                               : make_idesc_bf16(BM, BN, 0, 1);
+            constexpr uint32_t idesc_nar = make_idesc_bf16(BM, R_PAD, 0, 0);
+            uint32_t stage = 0, phase = 0, tl = 0;
+            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++tl) {
+                const uint32_t acc = tl & 1;
+                const uint32_t acc_phase = (tl >> 1) & 1;
+                mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + acc * NT;
+                for (int kb = 0; kb < num_k_blks; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t a_addr = smem_u32(stage_base + stage * C::STAGE_BYTES);
+                    const uint32_t b_addr = a_addr + C::A_BYTES;
+#pragma unroll
+                    for (int kk = 0; kk < BK / UMMA_K; ++kk) {
+                        const uint32_t accum = (kb | kk) != 0;
+                        const uint64_t a_desc = make_smem_desc(a_addr + kk * 32, 16, 1024, kLayoutSW128);
+                        if constexpr (MODE == kModeFwd) {
+                            // [W0 rows ; A rows] as one K-major N = 256 operand
+                            const uint64_t b_desc = make_smem_desc(b_addr + kk * 32, 16, 1024, kLayoutSW128);
+                            umma_f16(d_tmem, a_desc, b_desc, idesc_main, accum);
+                        } else {
+                            // W0 MN-major: 64-column blocks at LBO = 8 KiB, 8-row k groups at SBO = 1 KiB
+                            const uint64_t b_desc = make_smem_desc(b_addr + kk * (UMMA_K * 128), 64 * 128,
+                                                                   1024, kLayoutSW128);
+                            umma_f16(d_tmem, a_desc, b_desc, idesc_main, accum);
+                            const uint64_t n_desc = make_smem_desc(b_addr + C::B_BYTES + kk * 32, 16, 1024,
+                                                                   kLayoutSW128);
+                            umma_f16(d_tmem + BN, a_desc, n_desc, idesc_nar, accum);
+                        }
+                    }
+                    umma_commit(&empty[stage]);  // frees the smem slot when these MMAs finish
+                    if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+                }
+                umma_commit(&tmem_full[acc]);
+            }
+        }
+    } else {
+        // ===================== epilogue (warps 2..5) =====================
+        const uint32_t ew = warp - 2;            // epilogue warp index 0..3
+        const uint32_t quarter = warp & 3;       // TMEM lane quarter this warp may access
+        const uint32_t row_local = quarter * 32 + lane;
+        constexpr uint32_t idesc_tail = make_idesc_bf16(BM, BN, 0, 0);
+        constexpr uint32_t tail_sbo = 8 * C::TAIL_ROW;
+        const float store_scale = (MODE == kModeFwd) ? 1.0f : p.scale;  // h unscaled, gh = s G B
+        uint32_t tl = 0;
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++tl) {
+            const int n_blk = tile / num_t_blks;
+            const int t_blk = tile - n_blk * num_t_blks;
+            const int64_t row = static_cast<int64_t>(t_blk) * BM + row_local;
+            const int n0 = n_blk * BN;
+            const uint32_t acc = tl & 1;
+            const uint32_t acc_phase = (tl >> 1) & 1;
+            mbar_wait(&tmem_full[acc], acc_phase);
+            tc_fence_after();
+            const uint32_t tbase = tmem_base + ((quarter * 32) << 16) + acc * NT;
+
+            // (1) the r_pad low-rank columns: h = x A^T (fwd) or G B (dx)
+            float hv[R_PAD];
+#pragma unroll
+            for (int c = 0; c < R_PAD / 16; ++c) {
+                uint32_t v[16];
+                tmem_ld_32x32b_x16(tbase + BN + 16 * c, v);
+                tmem_ld_wait();
+#pragma unroll
+                for (int e = 0; e < 16; ++e) hv[16 * c + e] = __uint_as_float(v[e]);
+            }
+            // (2) side output: h (fwd, for dB) / gh (dx, for dA); one tile column per row block
+            if (p.side_out != nullptr && n_blk == 0 && row < p.T) {
+                float* dst = p.side_out + row * p.r;
+#pragma unroll
+                for (int j = 0; j < R_PAD; ++j)
+                    if (j < p.r) dst[j] = store_scale * hv[j];
+            }
+            // (3) bf16(s h) / bf16(gh) -> swizzled K-major smem tile (tail MMA A operand)
+#pragma unroll
+            for (int c = 0; c < R_PAD / 8; ++c) {
+                uint4 q;
+                q.x = pack_bf16x2(p.scale * hv[8 * c + 0], p.scale * hv[8 * c + 1]);
+                q.y = pack_bf16x2(p.scale * hv[8 * c + 2], p.scale * hv[8 * c + 3]);
+                q.z = pack_bf16x2(p.scale * hv[8 * c + 4], p.scale * hv[8 * c + 5]);
+                q.w = pack_bf16x2(p.scale * hv[8 * c + 6], p.scale * hv[8 * c + 7]);
+                *reinterpret_cast<uint4*>(s_h + swizzled_offset(row_local, c, C::TAIL_ROW)) = q;
+            }
+            fence_proxy_async_smem();
+            named_bar_sync(1, 128);
+            // (4) tail MMA: acc[:, 0:BN] += s_h (128 x r_pad) * tail_tile (BN x r_pad)^T
+            if (ew == 0 && lane == 0) {
+                mbar_wait(tailop_full, tl & 1);
+                tc_fence_after();
+                const uint32_t h_addr = smem_u32(s_h);
+                const uint32_t t_addr = smem_u32(s_tailb);
+#pragma unroll
+                for (int kk = 0; kk < R_PAD / UMMA_K; ++kk) {
+                    const uint64_t a_desc = make_smem_desc(h_addr + kk * 32, 16, tail_sbo, C::TAIL_LAYOUT);
+                    const uint64_t b_desc = make_smem_desc(t_addr + kk * 32, 16, tail_sbo, C::TAIL_LAYOUT);
+                    umma_f16(tmem_base + acc * NT, a_desc, b_desc, idesc_tail, 1u);
+                }
+                umma_commit(tail_done);
+            }
+            mbar_wait(tail_done, tl & 1);
+            tc_fence_after();
+            if (ew == 0 && lane == 0) mbar_arrive(tailop_empty);
+
+            // (5) drain: acc -> (+ b0) -> bf16 (RNE) -> global
+            const bool row_ok = row < p.T;
+            __nv_bfloat16* out_row = p.out + row * p.N_out;
+#pragma unroll 1
+            for (int c = 0; c < BN / 16; ++c) {
+                uint32_t v[16];
+                tmem_ld_32x32b_x16(tbase + 16 * c, v);
+                tmem_ld_wait();
+                const int64_t col = n0 + 16 * c;
+                if (row_ok && col < p.N_out) {
+                    float f[16];
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) f[e] = __uint_as_float(v[e]);
+                    if (MODE == kModeFwd && p.bias != nullptr) {
+#pragma unroll
+                        for (int e = 0; e < 16; ++e)
+                            if (col + e < p.N_out) f[e] += __bfloat162float(p.bias[col + e]);
+                    }
+                    uint4 q0, q1;
+                    q0.x = pack_bf16x2(f[0], f[1]);   q0.y = pack_bf16x2(f[2], f[3]);
+                    q0.z = pack_bf16x2(f[4], f[5]);   q0.w = pack_bf16x2(f[6], f[7]);
+                    q1.x = pack_bf16x2(f[8], f[9]);   q1.y = pack_bf16x2(f[10], f[11]);
+                    q1.z = pack_bf16x2(f[12], f[13]); q1.w = pack_bf16x2(f[14], f[15]);
+                    *reinterpret_cast<uint4*>(out_row + col) = q0;               // N_out % 8 == 0
+                    if (col + 8 < p.N_out) *reinterpret_cast<uint4*>(out_row + col + 8) = q1;
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tmem_empty[acc]);
+        }
+    }
+
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc<512>(tmem_base);
+    }
+}
+
+// ----------------------------------------------------------------------------
+// host side
+// ----------------------------------------------------------------------------
+template <int MODE, int R_PAD>
+static cudaError_t launch_impl(const FusedGemmMaps& maps, const FusedGemmParams& p, int num_sms,
+                               cudaStream_t stream) {
+    using C = GemmCfg<MODE, R_PAD>;
+    auto kern = lora_fused_gemm_kernel<MODE, R_PAD>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         C::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    const int64_t tiles = ((p.T + BM - 1) / BM) * ((p.N_out + C::BN - 1) / C::BN);
+    const int grid = static_cast<int>(tiles < num_sms ? tiles : num_sms);
+    if (grid <= 0) return cudaSuccess;
+    kern<<<grid, NUM_THREADS, C::SMEM_BYTES, stream>>>(maps.act, maps.w, maps.nar, maps.tail, p);
+    return cudaGetLastError();
+}
+
+int fused_gemm_block_n(int r_pad) { return NT - r_pad; }
+
+cudaError_t launch_fused_gemm(int mode, int r_pad, const FusedGemmMaps& maps,
+                              const FusedGemmParams& p, int num_sms, cudaStream_t stream) {
+    if (mode == kModeFwd) {
+        switch (r_pad) {
+            case 16: return launch_impl<kModeFwd, 16>(maps, p, num_sms, stream);
+            case 32: return launch_impl<kModeFwd, 32>(maps, p, num_sms, stream);
+            case 64: return launch_impl<kModeFwd, 64>(maps, p, num_sms, stream);
+        }
+    } else {
+        switch (r_pad) {
+            case 16: return launch_impl<kModeDx, 16>(maps, p, num_sms, stream);
+            case 32: return launch_impl<kModeDx, 32>(maps, p, num_sms, stream);
+            case 64: return launch_impl<kModeDx, 64>(maps, p, num_sms, stream);
+        }
+    }
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace lora_sm100

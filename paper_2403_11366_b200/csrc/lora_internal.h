@@ -1,0 +1,24 @@
+// lora_internal.h -- shared host-side helpers of liblora.so (not public ABI).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "lora.h"
+
+namespace lora_host {
+
+lora_status fail(lora_status st, const char* fmt, ...);
+lora_status cuda_fail(cudaError_t e, const char* what);
+lora_status check_dims(const lora_dims* d, bool need_tokens);
+void set_launches(int n);
+int get_launches();
+
+lora_status fwd_impl(const lora_dims* d, const void* x, const void* w0, const void* a, const void* b,
+                     const void* bias, void* y, float* h_out, void* ws, size_t ws_bytes,
+                     cudaStream_t stream, int* launches);
+lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const void* a, const void* b,
+                     const float* h_saved, const void* dy, void* dx, float* da, float* db, int accumulate,
+                     void* ws, size_t ws_bytes, cudaStream_t stream, int* launches);
+size_t fwd_workspace(const lora_dims* d);
+size_t bwd_workspace(const lora_dims* d);
+
+}  // namespace lora_host

@@ -1,0 +1,103 @@
+"""C-ABI tests that need no GPU: the library loads, exports every symbol
+include/lora.h declares, and validates its arguments synchronously (returning
+the documented status before any CUDA call).  No compute is invoked here."""
+import ctypes
+
+import pytest
+
+import paper_2403_11366_b200 as L
+
+
+def test_library_exports_every_header_symbol():
+    names = L.header_functions()
+    assert "lora_linear_fwd" in names and "lora_linear_bwd" in names and "lora_merge" in names
+    missing = [n for n in names if not hasattr(L.lib, n)]
+    assert not missing, f"liblora.so lacks {missing}"
+    assert L.lib.lora_version() >= 100
+
+
+def test_sass_is_sm100a_tensor_core_code():
+    """The fused GEMMs must be tcgen05 (UTC*MMA) fed by TMA (UTMALDG)."""
+    import shutil
+    import subprocess
+    if not shutil.which("cuobjdump"):
+        pytest.skip("cuobjdump not available")
+    out = subprocess.run(["cuobjdump", "-sass", L.LIB_PATH], capture_output=True, text=True).stdout
+    assert "UTCHMMA" in out and "UTMALDG" in out and "LDTM" in out
+    assert "sm_100a" in subprocess.run(["cuobjdump", "-lelf", L.LIB_PATH], capture_output=True,
+                                       text=True).stdout
+    assert " HMMA" not in out  # no legacy mma.sync path
+
+
+def test_status_strings():
+    for code, name in L.STATUS.items():
+        assert L.lib.lora_status_string(code).decode() == name
+
+
+def _fwd(d, x=16, w0=32, a=48, b=64, bias=None, y=80, h=None, ws=4096, wsb=1 << 20):
+    return L.lib.lora_linear_fwd(ctypes.byref(d), x, w0, a, b, bias, y, h, ws, wsb, None)
+
+
+def test_fwd_validation_codes():
+    ok = L.dims(128, 64, 64, 4, 16.0)
+    # fake (never dereferenced) 16-byte-aligned addresses; validation fails first
+    assert _fwd(L.dims(128, 60, 64, 4, 16.0)) == 2            # d_in % 8
+    assert "d_in" in L.lib.lora_last_error().decode()
+    assert _fwd(L.dims(128, 64, 0, 4, 16.0)) == 2             # d_out
+    assert _fwd(L.dims(-1, 64, 64, 4, 16.0)) == 2             # tokens
+    assert _fwd(L.dims(128, 64, 64, 0, 16.0)) == 2            # rank
+    assert _fwd(L.dims(128, 64, 64, 65, 16.0)) == 4           # rank > 64
+    assert _fwd(L.dims(128, 64, 64, 4, float("nan"))) == 1    # alpha
+    assert L.lib.lora_linear_fwd(None, 16, 32, 48, 64, None, 80, None, 4096, 1 << 20, None) == 1
+    assert _fwd(ok, x=None) == 1                              # NULL input
+    assert _fwd(ok, x=24) == 3                                # misaligned
+    assert "x" in L.lib.lora_last_error().decode()
+    assert _fwd(ok, wsb=8) == 7                               # workspace too small
+    assert _fwd(ok, ws=None) == 7
+    # output overlapping an input
+    assert _fwd(ok, x=1 << 20, y=(1 << 20) + 16 * 1024) == 1
+
+
+def test_bwd_and_merge_validation_codes():
+    d = L.dims(128, 64, 64, 4, 16.0)
+    need = L.lora_linear_bwd_workspace_bytes(d)
+    assert need > 0
+    f = L.lib.lora_linear_bwd
+    base = dict(x=1 << 30, w0=2 << 30, a=3 << 30, b=4 << 30, h=None, dy=5 << 30, dx=6 << 30,
+                da=7 << 30, db=8 << 30, acc=0, ws=9 << 30, wsb=need)
+
+    def call(**kw):
+        p = dict(base, **kw)
+        return f(ctypes.byref(kw.pop("d", d)), p["x"], p["w0"], p["a"], p["b"], p["h"], p["dy"],
+                 p["dx"], p["da"], p["db"], p["acc"], p["ws"], p["wsb"], None)
+
+    assert call(dy=None) == 1
+    assert call(acc=2) == 1
+    assert call(db=(8 << 30) + 4) == 3
+    assert call(wsb=need - 1) == 7
+    assert call(da=1 << 30) == 1       # dA aliases x
+    m = L.lib.lora_merge
+    assert m(ctypes.byref(L.dims(0, 64, 64, 4, 16.0)), 1 << 30, 2 << 30, 3 << 30, (1 << 30) + 64, None) == 1
+    assert m(ctypes.byref(L.dims(0, 64, 64, 4, 16.0)), 1 << 30, 2 << 30, 3 << 30, None, None) == 1
+    assert m(ctypes.byref(L.dims(0, 64, 12, 4, 16.0)), 1 << 30, 2 << 30, 3 << 30, 4 << 30, None) == 2
+
+
+def test_workspace_sizes_scale_with_shape():
+    f = L.lora_linear_fwd_workspace_bytes
+    assert f(L.dims(2048, 4096, 4096, 8, 16.0)) >= 4096 * 16 * 2
+    assert f(L.dims(2048, 4096, 4096, 8, 16.0)) == f(L.dims(7, 4096, 4096, 8, 16.0))
+    b = L.lora_linear_bwd_workspace_bytes
+    assert b(L.dims(4096, 4096, 11008, 16, 16.0)) > b(L.dims(2048, 4096, 11008, 16, 16.0))
+    assert b(L.dims(128, 60, 64, 4, 16.0)) == 0          # invalid dims -> 0
+
+
+def test_no_device_is_an_error_not_a_fallback():
+    """With valid arguments and no usable B200, the call fails loudly
+    (LORA_ERR_CUDA / LORA_ERR_UNSUPPORTED) instead of computing on the CPU."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    d = L.dims(128, 64, 64, 4, 16.0)
+    st = _fwd(d, x=1 << 30, w0=2 << 30, a=3 << 30, b=4 << 30, y=5 << 30, ws=6 << 30)
+    assert st in (4, 5)
+    assert L.lib.lora_device_check() in (4, 5)

@@ -1,0 +1,298 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the fp64 oracle on
+the same seeded bf16 inputs.  Tolerances from north_star (BASELINE.json):
+relative Frobenius error <= 1e-2 for y, dX and <= 2e-2 for dA, dB; bit-exact
+where the arithmetic is exact (integer-valued inputs)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from synth import bf16_bits_to_f64, f32_to_bf16_bits, make_lora_inputs  # noqa: E402
+from tests.gpu_util import (TOL_GRAD, TOL_OUT, bits_of, dev_bf16, host_f64, relF,  # noqa: E402
+                            rne_bf16_f64)
+
+
+@pytest.fixture(scope="module")
+def L():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2403_11366_b200 as L
+    L.lora_device_check()
+    return L
+
+
+def _run(L, d, alpha, bias=None, h_saved=True, want_dx=True):
+    x, w0, a, b, dy = (dev_bf16(d[k]) for k in ("x", "w0", "a", "b", "dy"))
+    bb = dev_bf16(bias) if bias is not None else None
+    y, h = L.lora_linear_fwd(x, w0, a, b, alpha, bias=bb)
+    dx, da, db = L.lora_linear_bwd(x, w0, a, b, dy, alpha, h_saved=h if h_saved else None,
+                                   want_dx=want_dx)
+    torch.cuda.synchronize()
+    return dict(y=y, h=h, dx=dx, da=da, db=db)
+
+
+def _check_against_oracle(oracle_mod, L, d, alpha, rows=None, bias=None, **kw):
+    out = _run(L, d, alpha, bias=bias, **kw)
+    yo, ho = oracle_mod.lora_fwd(d["x"], d["w0"], d["a"], d["b"], alpha, bias=bias, rows=rows)
+    go = oracle_mod.lora_bwd(d["x"], d["w0"], d["a"], d["b"], d["dy"], alpha, rows=rows)
+    sel = slice(None) if rows is None else rows
+    errs = {
+        "y": relF(host_f64(out["y"])[sel], yo),
+        "h": relF(host_f64(out["h"])[sel], ho),
+        "da": relF(host_f64(out["da"]), go["da"]),
+        "db": relF(host_f64(out["db"]), go["db"]),
+    }
+    if out["dx"] is not None:
+        errs["dx"] = relF(host_f64(out["dx"])[sel], go["dx"])
+    assert errs["y"] <= TOL_OUT, errs
+    assert errs.get("dx", 0.0) <= TOL_OUT, errs
+    assert errs["da"] <= TOL_GRAD and errs["db"] <= TOL_GRAD, errs
+    assert errs["h"] <= 1e-4, errs  # h is an fp32 accumulation of the same bf16 products
+    return out, errs
+
+
+# ------------------------------------------------------------------ configs
+def test_cfg1_parity(oracle_mod, L):
+    """BASELINE.json configs[0]: 64 -> 64, r = 4, 128 tokens (alpha = 16, s = 4)."""
+    d = make_lora_inputs(128, 64, 64, 4, seed=2403)
+    _, errs = _check_against_oracle(oracle_mod, L, d, 16.0)
+    print("cfg1 relF", errs)
+
+
+@pytest.mark.parametrize("shape", [
+    (300, 200, 264, 5),     # ragged T, n, m; r < 16
+    (1, 8, 8, 1),           # minimum sizes
+    (129, 64, 520, 17),     # r_pad = 32, m spans tiles with a ragged tail
+    (257, 136, 256, 33),    # r_pad = 64
+    (64, 1024, 8, 64),      # max rank, d_out smaller than a tile
+    (700, 512, 488, 16),    # several row and column tiles
+    (130, 256, 240, 8),     # exactly one BN = 240 column tile
+    (256, 72, 1000, 12),    # K smaller than two k-blocks, many column tiles
+])
+def test_ragged_shapes_and_ranks(oracle_mod, L, shape):
+    T, n, m, r = shape
+    d = make_lora_inputs(T, n, m, r, seed=100 + r)
+    _check_against_oracle(oracle_mod, L, d, 16.0)
+
+
+def test_cfg2_full_size_sampled_rows(oracle_mod, L):
+    """BASELINE.json configs[1] at full size in the bench's launch
+    configuration: y, dX checked on sampled rows (first, last, random), dA and
+    dB in full."""
+    T, n, m, r = 2048, 4096, 4096, 8
+    d = make_lora_inputs(T, n, m, r, seed=2403)
+    rng = np.random.default_rng(7)
+    rows = np.unique(np.concatenate([[0, 1, 127, 128, T - 1], rng.choice(T, 40, replace=False)]))
+    _, errs = _check_against_oracle(oracle_mod, L, d, 16.0, rows=rows)
+    print("cfg2 relF", errs)
+
+
+# ------------------------------------------------------------------ exact pins
+def test_worked_example_embedded_bit_exact(oracle_mod, L):
+    """tests/golden/worked_example.json (SPEC.md:324 extended), zero-padded to
+    an ABI-legal 128 x 64 -> 64, r = 4: results are small integers, so the GPU
+    must match bitwise and every padding element must be exactly 0."""
+    from tests.test_oracle_pins import embed_worked_example
+    e = embed_worked_example()
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "worked_example.json")))["expected"]
+    out = _run(L, e, e["alpha"])
+    y, dx, da, db = (host_f64(out[k]) for k in ("y", "dx", "da", "db"))
+    ey = np.zeros_like(y); ey[0, :2] = g["y"][0]
+    edx = np.zeros_like(dx); edx[0, :2] = g["dx"][0]
+    eda = np.zeros_like(da); eda[0, :2] = g["da"][0]
+    edb = np.zeros_like(db); edb[:2, 0] = [v[0] for v in g["db"]]
+    np.testing.assert_array_equal(y, ey)
+    np.testing.assert_array_equal(dx, edx)
+    np.testing.assert_array_equal(da, eda)
+    np.testing.assert_array_equal(db, edb)
+
+
+def _ternary_certified(oracle_mod, T, n, m, r, alpha):
+    s = alpha / r
+    for seed in range(50):
+        d = make_lora_inputs(T, n, m, r, seed=9000 + seed, dist="ternary")
+        _, h = oracle_mod.lora_fwd(d["x"], d["w0"], d["a"], d["b"], alpha)
+        go = oracle_mod.lora_bwd(d["x"], d["w0"], d["a"], d["b"], d["dy"], alpha)
+        sh, gh = s * h, go["gh"]
+        # the bf16 tail operands bf16(s h) and bf16(gh) must be exact
+        if np.array_equal(rne_bf16_f64(sh), sh) and np.array_equal(rne_bf16_f64(gh), gh):
+            return d
+    raise AssertionError("no certified ternary input found")
+
+
+@pytest.mark.parametrize("shape", [(128, 64, 64, 4), (300, 200, 264, 5), (200, 128, 496, 24)])
+def test_integer_exact_bitwise(oracle_mod, L, shape):
+    """Ternary inputs {-1, 0, 0, 1} (SURVEY.md 8(c) pin 5): all products and
+    sums are integers far below 2^24, so fp32 accumulation is exact and the GPU
+    must equal RNE_bf16(oracle) bitwise for y, dX and the oracle exactly for dA,
+    dB.  Catches swizzle / layout / indexing bugs a tolerance could hide."""
+    T, n, m, r = shape
+    alpha = 4.0 * r  # s = 4: a power of two, so s h is an exact integer
+    d = _ternary_certified(oracle_mod, T, n, m, r, alpha)
+    out = _run(L, d, alpha)
+    yo, ho = oracle_mod.lora_fwd(d["x"], d["w0"], d["a"], d["b"], alpha)
+    go = oracle_mod.lora_bwd(d["x"], d["w0"], d["a"], d["b"], d["dy"], alpha)
+    np.testing.assert_array_equal(host_f64(out["y"]), rne_bf16_f64(yo))
+    np.testing.assert_array_equal(host_f64(out["h"]), ho)
+    np.testing.assert_array_equal(host_f64(out["dx"]), rne_bf16_f64(go["dx"]))
+    np.testing.assert_array_equal(host_f64(out["da"]), go["da"])
+    np.testing.assert_array_equal(host_f64(out["db"]), go["db"])
+
+
+def test_b_zero_fresh_adapter(oracle_mod, L):
+    """PAPER.md:113 (B initialised to zeros): y and dX equal the base GEMM
+    bitwise (the kernel with A = 0 as well), dA == 0 exactly, and y matches
+    cuBLAS x W0^T within the output tolerance."""
+    T, n, m, r = 384, 512, 640, 8
+    d = make_lora_inputs(T, n, m, r, seed=31, zero_b=True)
+    out = _run(L, d, 16.0)
+    d0 = dict(d, a=np.zeros_like(d["a"]))
+    out0 = _run(L, d0, 16.0)
+    assert torch.equal(out["y"], out0["y"]) and torch.equal(out["dx"], out0["dx"])
+    assert torch.count_nonzero(out["da"]).item() == 0
+    x, w0 = dev_bf16(d["x"]), dev_bf16(d["w0"])
+    ref = (x.float() @ w0.float().t())
+    assert relF(host_f64(out["y"]), host_f64(ref)) <= TOL_OUT
+    go = oracle_mod.lora_bwd(d["x"], d["w0"], d["a"], d["b"], d["dy"], 16.0)
+    assert relF(host_f64(out["db"]), go["db"]) <= TOL_GRAD
+
+
+def test_lora_delta_branch(oracle_mod, L):
+    """A tolerance on y alone could hide a broken low-rank branch: the GPU's
+    y - y|_{B=0} must match the oracle's s h B^T (SURVEY.md 8(c) pin 10)."""
+    T, n, m, r = 256, 1024, 768, 8
+    d = make_lora_inputs(T, n, m, r, seed=33)
+    out = _run(L, d, 16.0)
+    out0 = _run(L, dict(d, b=np.zeros_like(d["b"])), 16.0)
+    yo, _ = oracle_mod.lora_fwd(d["x"], d["w0"], d["a"], d["b"], 16.0)
+    yo0, _ = oracle_mod.lora_fwd(d["x"], d["w0"], d["a"], np.zeros_like(d["b"]), 16.0)
+    assert relF(host_f64(out["y"]) - host_f64(out0["y"]), yo - yo0) <= 2e-2
+
+
+# ------------------------------------------------------------------ API paths
+def test_recompute_h_and_skip_dx(oracle_mod, L):
+    """h_saved = NULL recomputes h (K3a); dx = NULL computes gh by K3a."""
+    T, n, m, r = 300, 256, 200, 6
+    d = make_lora_inputs(T, n, m, r, seed=41)
+    _check_against_oracle(oracle_mod, L, d, 16.0, h_saved=False)
+    out = _run(L, d, 16.0, want_dx=False)
+    go = oracle_mod.lora_bwd(d["x"], d["w0"], d["a"], d["b"], d["dy"], 16.0)
+    assert out["dx"] is None
+    assert relF(host_f64(out["da"]), go["da"]) <= TOL_GRAD
+    assert relF(host_f64(out["db"]), go["db"]) <= TOL_GRAD
+
+
+def test_bias(oracle_mod, L):
+    d = make_lora_inputs(200, 128, 136, 4, seed=43, bias=True)
+    _check_against_oracle(oracle_mod, L, d, 16.0, bias=d["bias"])
+
+
+def test_accumulate(L):
+    d = make_lora_inputs(256, 128, 192, 8, seed=45)
+    x, w0, a, b, dy = (dev_bf16(d[k]) for k in ("x", "w0", "a", "b", "dy"))
+    y, h = L.lora_linear_fwd(x, w0, a, b, 16.0)
+    _, da1, db1 = L.lora_linear_bwd(x, w0, a, b, dy, 16.0, h_saved=h)
+    da = da1.clone() * 0.5
+    db = db1.clone() * 0.25
+    L.lora_linear_bwd(x, w0, a, b, dy, 16.0, h_saved=h, want_dx=False, da=da, db=db, accumulate=True)
+    torch.cuda.synchronize()
+    # the second call skips dx, so gh comes from K3a (another fp32 summation order)
+    assert torch.allclose(da, 1.5 * da1, rtol=1e-4, atol=1e-4)
+    assert torch.allclose(db, 1.25 * db1, rtol=1e-6, atol=1e-6)
+
+
+def test_zero_tokens(L):
+    d = make_lora_inputs(1, 64, 64, 4, seed=47)
+    w0, a, b = (dev_bf16(d[k]) for k in ("w0", "a", "b"))
+    x = torch.empty((0, 64), dtype=torch.bfloat16, device="cuda")
+    dy = torch.empty((0, 64), dtype=torch.bfloat16, device="cuda")
+    y, h = L.lora_linear_fwd(x, w0, a, b, 16.0)
+    da = torch.full((4, 64), 3.0, device="cuda")
+    db = torch.full((64, 4), 3.0, device="cuda")
+    L.lora_linear_bwd(x, w0, a, b, dy, 16.0, h_saved=h, da=da, db=db)
+    torch.cuda.synchronize()
+    assert y.shape == (0, 64)
+    assert torch.count_nonzero(da).item() == 0 and torch.count_nonzero(db).item() == 0
+
+
+def test_determinism_and_row_permutation(L):
+    """Repeat calls are bitwise identical (fixed reduction orders); token rows
+    are independent, so permuting tokens permutes y and dX bitwise."""
+    T, n, m, r = 512, 384, 320, 16
+    d = make_lora_inputs(T, n, m, r, seed=49)
+    o1 = _run(L, d, 16.0)
+    o2 = _run(L, d, 16.0)
+    for k in ("y", "h", "dx", "da", "db"):
+        assert torch.equal(o1[k], o2[k]), k
+    perm = np.random.default_rng(3).permutation(T)
+    dp = dict(d, x=d["x"][perm], dy=d["dy"][perm])
+    op = _run(L, dp, 16.0)
+    pt = torch.as_tensor(perm, device="cuda")
+    assert torch.equal(op["y"], o1["y"][pt])
+    assert torch.equal(op["dx"], o1["dx"][pt])
+
+
+def test_launch_counts(L):
+    d = make_lora_inputs(256, 128, 128, 8, seed=51)
+    x, w0, a, b, dy = (dev_bf16(d[k]) for k in ("x", "w0", "a", "b", "dy"))
+    y, h = L.lora_linear_fwd(x, w0, a, b, 16.0)
+    assert L.lora_last_launch_count() == 2          # pack + fused K1
+    L.lora_linear_bwd(x, w0, a, b, dy, 16.0, h_saved=h)
+    assert L.lora_last_launch_count() == 4          # pack + K2 + K3 partial + finalize
+
+
+# ------------------------------------------------------------------ merge
+@pytest.mark.parametrize("shape", [(64, 64, 4), (4096, 4096, 8), (1000, 520, 33)])
+def test_merge_matches_oracle(oracle_mod, L, shape):
+    """lora_merge = RNE_bf16(W0 + s B A) (Eq. 1 line 2): >= 99.9% of elements
+    bit-equal to the rounded fp64 oracle, the rest within one bf16 ulp."""
+    n, m, r = shape
+    d = make_lora_inputs(1, n, m, r, seed=53)
+    w0, a, b = (dev_bf16(d[k]) for k in ("w0", "a", "b"))
+    wm = L.lora_merge(w0, a, b, 16.0)
+    torch.cuda.synchronize()
+    ref = rne_bf16_f64(oracle_mod.lora_merge(d["w0"], d["a"], d["b"], 16.0))
+    got = host_f64(wm)
+    eq = np.mean(got == ref)
+    assert eq >= 0.999, eq
+    # one bf16 ulp of the result, plus the fp32 evaluation error of W0 + s B A
+    # (which matters only where W0 and s B A cancel)
+    s = 16.0 / r
+    mag = np.abs(bf16_bits_to_f64(d["w0"])) + s * (np.abs(bf16_bits_to_f64(d["b"])) @
+                                                   np.abs(bf16_bits_to_f64(d["a"])))
+    assert np.all(np.abs(got - ref) <= np.abs(ref) * 2.0 ** -7 + mag * 2.0 ** -20)
+    # in place gives the same bits; W0 unchanged by the out-of-place call
+    assert np.array_equal(bits_of(w0), d["w0"])
+    w0c = w0.clone()
+    L.lora_merge(w0c, a, b, 16.0, w_out=w0c)
+    torch.cuda.synchronize()
+    assert torch.equal(w0c, wm)
+
+
+def test_merge_equivalence_forward(L):
+    """Eq. 1: the merged weight used as a plain base weight (B = 0) gives the
+    adapter forward within tolerance."""
+    T, n, m, r = 256, 512, 384, 8
+    d = make_lora_inputs(T, n, m, r, seed=55)
+    x, w0, a, b = (dev_bf16(d[k]) for k in ("x", "w0", "a", "b"))
+    y, _ = L.lora_linear_fwd(x, w0, a, b, 16.0)
+    wm = L.lora_merge(w0, a, b, 16.0)
+    y2, _ = L.lora_linear_fwd(x, wm, a, torch.zeros_like(b), 16.0)
+    torch.cuda.synchronize()
+    assert relF(host_f64(y2), host_f64(y)) <= TOL_OUT
+
+
+def test_frozen_base_untouched(L):
+    """fwd + bwd never write W0 (or any input)."""
+    d = make_lora_inputs(256, 256, 256, 8, seed=57)
+    t = {k: dev_bf16(d[k]) for k in ("x", "w0", "a", "b", "dy")}
+    _run(L, d, 16.0)
+    y, h = L.lora_linear_fwd(t["x"], t["w0"], t["a"], t["b"], 16.0)
+    L.lora_linear_bwd(t["x"], t["w0"], t["a"], t["b"], t["dy"], 16.0, h_saved=h)
+    torch.cuda.synchronize()
+    for k, v in t.items():
+        assert np.array_equal(bits_of(v), d[k]), k
