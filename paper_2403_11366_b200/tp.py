@@ -1,0 +1,182 @@
+"""Tensor parallelism for the LoRA linear, one process per GPU.
+
+PAPER.md:122: "JORA parallelizes all parameters of the Llama model using JAX's
+positional sharding module ... Projection and Embedding layers are sharded on
+the non-sequential dimension."  Read (R10-R13) as Megatron column /
+row parallelism inside the decoder block:
+
+  COLUMN (q, k, v, gate, up): W0 [m, n] and B [m, r] split on m (d_out),
+      A [r, n] replicated.  fwd: local, no collective.  bwd: dX and dA are
+      partial sums -> all-reduce; dB local.
+  ROW (o, down): W0 and A split on n (d_in), B replicated.  fwd: y is a
+      partial sum -> all-reduce (bias added once); bwd: dB partial ->
+      all-reduce; dX, dA local.
+
+Partial sums are reduced with a SUM (no 1/N; R12).  The collectives run in
+liblora.so over NCCL (lora_comm_*); torch.distributed is used only to
+broadcast the NCCL unique id (plumbing).  The sharding functions here are the
+host logic; they are covered on CPU by tests/test_tp_gloo.py.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+COLUMN = 0
+ROW = 1
+MODES = {"column": COLUMN, "row": ROW}
+
+
+@dataclass(frozen=True)
+class ShardSpec:
+    """How one LoRA linear is split across `world` ranks."""
+    mode: int          # COLUMN or ROW
+    world: int
+    rank: int
+    n: int             # full d_in
+    m: int             # full d_out
+
+    def __post_init__(self):
+        if self.world < 1 or not (0 <= self.rank < self.world):
+            raise ValueError(f"bad rank {self.rank} / world {self.world}")
+        axis, extent = ("d_out", self.m) if self.mode == COLUMN else ("d_in", self.n)
+        if extent % self.world != 0:
+            raise ValueError(f"divisibility violation: {axis} = {extent} is not divisible by N = {self.world}")
+        if (extent // self.world) % 8 != 0:
+            raise ValueError(f"shard of {axis} = {extent // self.world} is not a multiple of 8 (TMA rows)")
+
+    @property
+    def local_n(self) -> int:
+        return self.n // self.world if self.mode == ROW else self.n
+
+    @property
+    def local_m(self) -> int:
+        return self.m // self.world if self.mode == COLUMN else self.m
+
+    def slice(self):
+        """Slice of the sharded axis owned by this rank."""
+        ext = self.local_m if self.mode == COLUMN else self.local_n
+        return slice(self.rank * ext, (self.rank + 1) * ext)
+
+
+def shard_params(spec: ShardSpec, w0, a, b, bias=None):
+    """Local (W0, A, B, bias) of this rank (works on numpy arrays and torch tensors).
+    COLUMN: W0[rows], B[rows], A full, bias[rows].  ROW: W0[:, cols], A[:, cols],
+    B full, bias full (added once by rank 0)."""
+    sl = spec.slice()
+    if spec.mode == COLUMN:
+        return w0[sl], a, b[sl], (bias[sl] if bias is not None else None)
+    return w0[:, sl], a[:, sl], b, bias
+
+
+def shard_input(spec: ShardSpec, x):
+    """Local activation: COLUMN takes the full x; ROW takes x[:, cols]."""
+    return x if spec.mode == COLUMN else x[:, spec.slice()]
+
+
+def shard_output_grad(spec: ShardSpec, dy):
+    """Local upstream gradient: COLUMN takes dY[:, rows]; ROW the full dY."""
+    return dy[:, spec.slice()] if spec.mode == COLUMN else dy
+
+
+def partial_outputs(spec: ShardSpec):
+    """Which results are partial sums on each rank (reduced by a SUM)."""
+    if spec.mode == COLUMN:
+        return {"y": False, "dx": True, "da": True, "db": False}
+    return {"y": True, "dx": False, "da": False, "db": True}
+
+
+# --------------------------------------------------------------------- runtime
+class LoraComm:
+    """An NCCL communicator owned by liblora.so (lora_comm_*), created from a
+    unique id broadcast over an existing torch.distributed process group."""
+
+    def __init__(self, group=None):
+        import os
+
+        import torch
+        import torch.distributed as dist
+
+        from . import build as _build
+        from . import lib, _check
+        nccl = _build.nccl_library()
+        if nccl and "LORA_NCCL_LIB" not in os.environ:
+            os.environ["LORA_NCCL_LIB"] = nccl
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        uid = ctypes.create_string_buffer(128)
+        if self.rank == 0:
+            _check(lib.lora_comm_unique_id(uid), "lora_comm_unique_id")
+        if self.world > 1:
+            t = torch.frombuffer(bytearray(uid.raw), dtype=torch.uint8).clone()
+            if dist.get_backend(group) == "nccl":
+                t = t.cuda()
+            dist.broadcast(t, src=0, group=group)
+            uid = ctypes.create_string_buffer(bytes(t.cpu().tolist()), 128)
+        self._h = ctypes.c_void_p()
+        _check(lib.lora_comm_init(self.world, self.rank, uid, ctypes.byref(self._h)), "lora_comm_init")
+
+    @property
+    def handle(self):
+        return self._h
+
+    def allreduce(self, t, stream=None):
+        import torch
+
+        from . import lib, _check, _stream
+        dt = 0 if t.dtype == torch.float32 else 1
+        _check(lib.lora_allreduce(self._h, t.data_ptr(), t.numel(), dt, _stream(stream)), "lora_allreduce")
+
+    def close(self):
+        from . import lib
+        if self._h:
+            lib.lora_comm_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+
+def tp_linear_fwd(comm: LoraComm, spec: ShardSpec, x, w0, a, b, alpha, bias=None, y=None, h_out=None,
+                  workspace=None, stream=None):
+    """lora_tp_linear_fwd on local shards.  Returns (y [T, local_m], h [T, r])."""
+    import torch
+
+    from . import _bf16, _check, _ptr, _stream, _workspace, dims, lib, lora_linear_fwd_workspace_bytes
+    T = x.shape[0]
+    r = a.shape[0]
+    n, m = spec.local_n, spec.local_m
+    _bf16(x, "x", (T, n)); _bf16(w0, "w0", (m, n)); _bf16(a, "a", (r, n)); _bf16(b, "b", (m, r))
+    if y is None:
+        y = torch.empty((T, m), dtype=torch.bfloat16, device=x.device)
+    if h_out is None:
+        h_out = torch.empty((T, r), dtype=torch.float32, device=x.device)
+    d = dims(T, n, m, r, alpha)
+    ws = workspace if workspace is not None else _workspace(lora_linear_fwd_workspace_bytes(d), x.device)
+    _check(lib.lora_tp_linear_fwd(comm.handle, spec.mode, ctypes.byref(d), _ptr(x), _ptr(w0), _ptr(a), _ptr(b),
+                                  _ptr(bias), _ptr(y), _ptr(h_out), _ptr(ws), ws.numel(), _stream(stream)),
+           "lora_tp_linear_fwd")
+    return y, h_out
+
+
+def tp_linear_bwd(comm: LoraComm, spec: ShardSpec, x, w0, a, b, dy, alpha, h_saved=None, dx=None, da=None,
+                  db=None, accumulate=False, reduce_lora_grads=True, want_dx=True, workspace=None, stream=None):
+    """lora_tp_linear_bwd on local shards.  Returns (dx, dA, dB) local tensors
+    (dx / dA / dB already summed across ranks where they are partial)."""
+    import torch
+
+    from . import _check, _ptr, _stream, _workspace, dims, lib
+    T = x.shape[0]
+    r = a.shape[0]
+    n, m = spec.local_n, spec.local_m
+    if dx is None and want_dx:
+        dx = torch.empty((T, n), dtype=torch.bfloat16, device=x.device)
+    if da is None:
+        da = torch.zeros((r, n), dtype=torch.float32, device=x.device)
+    if db is None:
+        db = torch.zeros((m, r), dtype=torch.float32, device=x.device)
+    d = dims(T, n, m, r, alpha)
+    need = int(lib.lora_tp_linear_bwd_workspace_bytes(ctypes.byref(d)))
+    ws = workspace if workspace is not None else _workspace(need, x.device)
+    _check(lib.lora_tp_linear_bwd(comm.handle, spec.mode, ctypes.byref(d), _ptr(x), _ptr(w0), _ptr(a), _ptr(b),
+                                  _ptr(h_saved), _ptr(dy), _ptr(dx), _ptr(da), _ptr(db), 1 if accumulate else 0,
+                                  1 if reduce_lora_grads else 0, _ptr(ws), ws.numel(), _stream(stream)),
+           "lora_tp_linear_bwd")
+    return dx, da, db
