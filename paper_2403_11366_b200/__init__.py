@@ -27,7 +27,7 @@ __all__ = [
 ]
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "liblora.so")
+LIB_PATH = os.environ.get("LORA_LIB_PATH") or os.path.join(_PKG, "liblora.so")
 HEADER_PATH = os.path.join(os.path.dirname(_PKG), "include", "lora.h")
 
 if not os.path.exists(LIB_PATH):

@@ -18,7 +18,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "liblora.so")
-SOURCES = ["lora_gemm.cu", "lora_aux.cu", "lora_api.cpp", "lora_comm.cpp"]
+SOURCES = ["lora_gemm.cu", "lora_grad.cu", "lora_aux.cu", "lora_api.cpp", "lora_comm.cpp"]
 HEADERS = ["sm100_ptx.cuh", "lora_kernels.h", "lora_internal.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -57,18 +57,21 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str | None = None,
+          defines: tuple = ()) -> str:
+    """Build liblora.so (or, with `out`/`defines`, an experiment variant)."""
+    target = out or LIB
+    if out is None and not force and not _stale():
         return LIB
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
     cmd = [nvcc, *ARCH, "-O3", "-std=c++17", "-lineinfo", "-shared", "-Xcompiler", "-fPIC",
            "-Xptxas", "-v" if verbose else "-O3",
            "-I", INCLUDE, "-I", CSRC, "-I", _nccl_include(),
-           "-DLORA_BUILD", "-o", LIB + ".tmp",
+           "-DLORA_BUILD", *[f"-D{d}" for d in defines], "-o", target + ".tmp",
            *[os.path.join(CSRC, f) for f in SOURCES], "-ldl", "-lpthread"]
     subprocess.check_call(cmd)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(target + ".tmp", target)
+    return target
 
 
 if __name__ == "__main__":

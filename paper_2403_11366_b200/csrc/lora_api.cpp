@@ -144,33 +144,43 @@ int r_pad_of(int r) { return r <= 16 ? 16 : (r <= 32 ? 32 : 64); }
 
 static size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 
+int r8_of(int r) { return (r + 7) / 8 * 8; }
+
+// CTA pairs (256-row tiles) once there are more than 128 tokens; the
+// LORA_CTA_GROUP environment variable (1 or 2) overrides, for experiments.
+static int cta_group_for(int64_t T) {
+    static const int forced = [] {
+        const char* s = getenv("LORA_CTA_GROUP");
+        return s ? atoi(s) : 0;
+    }();
+    if (forced == 1 || forced == 2) return forced;
+    return T > 128 ? 2 : 1;
+}
+
+// Forward workspace: B8 (B zero-padded to a multiple of 8 columns), used only
+// when r % 8 != 0 (sized unconditionally so it depends on dims alone).
 struct FwdWs {
-    size_t bpad, total;
+    size_t b8, total;
 };
 static FwdWs fwd_ws(const lora_dims* d) {
     FwdWs w;
-    w.bpad = 0;
-    w.total = align256(size_t(d->d_out) * r_pad_of(d->rank) * 2);
+    w.b8 = 0;
+    w.total = align256(size_t(d->d_out) * r8_of(d->rank) * 2);
     return w;
 }
 
-constexpr int kPlanSMs = 148;  // workspace sizing must not depend on the device
-
+// Backward workspace: B^T [r, m], gh [T, r] fp32, h [T, r] fp32 (when not saved).
 struct BwdWs {
-    size_t bt, at, gh, h, part, total;
-    GradReducePlan plan;
+    size_t bt, gh, h, total;
 };
 static BwdWs bwd_ws(const lora_dims* d) {
     BwdWs w;
-    const int64_t T = d->tokens, n = d->d_in, m = d->d_out;
+    const int64_t T = d->tokens > 0 ? d->tokens : 0;
     const int r = d->rank;
-    w.plan = plan_grad_reduce(T > 0 ? T : 1, n, m, r, kPlanSMs);
     size_t off = 0;
-    w.bt = off; off += align256(size_t(r) * m * 2);
-    w.at = off; off += align256(size_t(n) * r_pad_of(r) * 2);
-    w.gh = off; off += align256(size_t(T > 0 ? T : 0) * r * 4);
-    w.h = off; off += align256(size_t(T > 0 ? T : 0) * r * 4);
-    w.part = off; off += align256(grad_reduce_partial_bytes(w.plan, n, m, r));
+    w.bt = off; off += align256(size_t(r) * d->d_out * 2);
+    w.gh = off; off += align256(size_t(T) * r * 4);
+    w.h = off; off += align256(size_t(T) * r * 4);
     w.total = off;
     return w;
 }
@@ -209,24 +219,34 @@ lora_status fwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
     if (T == 0) return LORA_OK;
 
     const int rp = r_pad_of(r);
+    const int r8 = r8_of(r);
     const int BN = fused_gemm_block_n(rp);
-    auto* bpad = reinterpret_cast<__nv_bfloat16*>(static_cast<uint8_t*>(ws) + W.bpad);
-    cudaError_t e = launch_pack(static_cast<const __nv_bfloat16*>(a), static_cast<const __nv_bfloat16*>(b), n, m, r,
-                                rp, bpad, nullptr, nullptr, dev.sms, stream);
-    if (e != cudaSuccess) return cuda_fail(e, "pack launch");
-    ++*launches;
+    // B is read by TMA with its own row pitch when r % 8 == 0; otherwise a
+    // zero-padded copy B8 [m, r8] is made first (B6).
+    const void* bsrc = b;
+    if (r != r8) {
+        auto* b8 = reinterpret_cast<__nv_bfloat16*>(static_cast<uint8_t*>(ws) + W.b8);
+        cudaError_t e = launch_pack_b(static_cast<const __nv_bfloat16*>(b), m, r, b8, nullptr, dev.sms, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "pack launch");
+        ++*launches;
+        bsrc = b8;
+    }
     FusedGemmMaps maps;
+    const int cg = cta_group_for(T);
     if ((st = encode_2d(&maps.act, x, n, T, n * 2, 64, 128, 128, "x")) != LORA_OK) return st;
-    if ((st = encode_2d(&maps.w, w0, n, m, n * 2, 64, BN, 128, "w0")) != LORA_OK) return st;
+    // W0 rows of the [W0 ; A] B-operand tile: CTA pair splits it 128 / (BN - 128) + A rows
+    if ((st = encode_2d(&maps.w, w0, n, m, n * 2, 64, cg == 2 ? 128 : BN, 128, "w0")) != LORA_OK) return st;
+    maps.w2 = maps.w;
+    if (cg == 2 && (st = encode_2d(&maps.w2, w0, n, m, n * 2, 64, BN - 128, 128, "w0")) != LORA_OK) return st;
     if ((st = encode_2d(&maps.nar, a, n, r, n * 2, 64, rp, 128, "a")) != LORA_OK) return st;
-    if ((st = encode_2d(&maps.tail, bpad, rp, m, rp * 2, rp, BN, rp * 2, "b_pad")) != LORA_OK) return st;
+    if ((st = encode_2d(&maps.tail, bsrc, r8, m, r8 * 2, rp, BN / cg, rp * 2, "b")) != LORA_OK) return st;
     FusedGemmParams p;
     p.T = T; p.K = n; p.N_out = m; p.r = r;
     p.scale = d->alpha / static_cast<float>(r);
     p.bias = static_cast<const __nv_bfloat16*>(bias);
     p.out = static_cast<__nv_bfloat16*>(y);
     p.side_out = h_out;
-    e = launch_fused_gemm(kModeFwd, rp, maps, p, dev.sms, stream);
+    cudaError_t e = launch_fused_gemm(kModeFwd, rp, cg, maps, p, dev.sms, stream);
     if (e != cudaSuccess) return cuda_fail(e, "fused forward launch");
     ++*launches;
     return LORA_OK;
@@ -279,55 +299,59 @@ lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
     }
     const float s = d->alpha / static_cast<float>(r);
     const int rp = r_pad_of(r);
+    const int r8 = r8_of(r);
     uint8_t* wsb = static_cast<uint8_t*>(ws);
-    auto* bt = reinterpret_cast<__nv_bfloat16*>(wsb + W.bt);
-    auto* at = reinterpret_cast<__nv_bfloat16*>(wsb + W.at);
     float* gh = reinterpret_cast<float*>(wsb + W.gh);
     float* hbuf = reinterpret_cast<float*>(wsb + W.h);
-    float* part = reinterpret_cast<float*>(wsb + W.part);
     const auto* xa = static_cast<const __nv_bfloat16*>(x);
     const auto* aa = static_cast<const __nv_bfloat16*>(a);
-    const auto* ba = static_cast<const __nv_bfloat16*>(b);
     const auto* dya = static_cast<const __nv_bfloat16*>(dy);
     const bool need_gh = dx || da;
     const bool need_h = db && !h_saved;
 
+    // B^T [r, m] (B6): the K-major operand of K2's narrow dY B MMA and of K3a
+    auto* bt = reinterpret_cast<__nv_bfloat16*>(wsb + W.bt);
     if (need_gh) {
-        if ((e = launch_pack(aa, ba, n, m, r, rp, nullptr, bt, dx ? at : nullptr, dev.sms, stream)) != cudaSuccess)
+        if ((e = launch_pack_b(static_cast<const __nv_bfloat16*>(b), m, r, nullptr, bt, dev.sms, stream)) !=
+            cudaSuccess)
             return cuda_fail(e, "pack launch");
         ++*launches;
     }
+    (void)r8;
     if (dx) {
         const int BN = fused_gemm_block_n(rp);
         FusedGemmMaps maps;
+        const int cg = cta_group_for(T);
         if ((st = encode_2d(&maps.act, dy, m, T, m * 2, 64, 128, 128, "dy")) != LORA_OK) return st;
         if ((st = encode_2d(&maps.w, w0, n, m, n * 2, 64, 64, 128, "w0")) != LORA_OK) return st;
-        if ((st = encode_2d(&maps.nar, bt, m, r, m * 2, 64, rp, 128, "b^T")) != LORA_OK) return st;
-        if ((st = encode_2d(&maps.tail, at, rp, n, rp * 2, rp, BN, rp * 2, "a^T_pad")) != LORA_OK) return st;
+        maps.w2 = maps.w;
+        if ((st = encode_2d(&maps.nar, bt, m, r, m * 2, 64, rp / cg, 128, "b^T")) != LORA_OK) return st;
+        if ((st = encode_2d(&maps.tail, a, n, r, n * 2, 64, rp, 128, "a")) != LORA_OK) return st;
         FusedGemmParams p;
         p.T = T; p.K = m; p.N_out = n; p.r = r; p.scale = s;
         p.bias = nullptr;
         p.out = static_cast<__nv_bfloat16*>(dx);
         p.side_out = gh;
-        if ((e = launch_fused_gemm(kModeDx, rp, maps, p, dev.sms, stream)) != cudaSuccess)
+        if ((e = launch_fused_gemm(kModeDx, rp, cg, maps, p, dev.sms, stream)) != cudaSuccess)
             return cuda_fail(e, "fused dX launch");
         ++*launches;
+        (void)BN;
     } else if (da) {
         // gh = s dY B via the row-projection kernel on B^T [r, m]
-        if ((e = launch_rowproj(dya, T, m, bt, r, s, gh, stream)) != cudaSuccess) return cuda_fail(e, "gh rowproj");
+        if ((e = launch_rowproj(dya, T, m, bt, m, 0, r, s, gh, stream)) != cudaSuccess)
+            return cuda_fail(e, "gh rowproj");
         ++*launches;
     }
     const float* hsrc = h_saved;
     if (need_h) {
-        if ((e = launch_rowproj(xa, T, n, aa, r, 1.0f, hbuf, stream)) != cudaSuccess) return cuda_fail(e, "h rowproj");
+        if ((e = launch_rowproj(xa, T, n, aa, n, 0, r, 1.0f, hbuf, stream)) != cudaSuccess)
+            return cuda_fail(e, "h rowproj");
         ++*launches;
         hsrc = hbuf;
     }
     if (da || db) {
-        int nl = 0;
-        e = launch_grad_reduce(W.plan, T, n, m, r, s, xa, gh, dya, hsrc, part, da, db, accumulate, stream, &nl);
+        e = launch_grad_reduce(T, n, m, r, s, xa, gh, dya, hsrc, da, db, accumulate, stream, launches);
         if (e != cudaSuccess) return cuda_fail(e, "grad reduce launch");
-        *launches += nl;
     }
     return LORA_OK;
 }

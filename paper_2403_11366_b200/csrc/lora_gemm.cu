@@ -3,7 +3,7 @@
 // K1 (MODE_FWD), Eq. 1 line 1 in row-vector form:
 //     acc  = x W0^T            (base GEMM, tcgen05, fp32 accumulator in TMEM)
 //     h    = x A^T             (same pass: A's r_pad rows are appended to the
-//                               W0 tile, so ONE 128 x 256 MMA per k-step
+//                               W0 tile, so ONE 256-column MMA per k-step
 //                               produces BN = 256 - r_pad output columns and
 //                               the r_pad columns of h)
 //     y    = bf16(acc + bf16(s h) B^T + b0)   (epilogue: a K = r_pad "tail"
@@ -16,7 +16,7 @@
 //                               already in shared memory)
 //     dX   = bf16(acc + bf16(gh) A)  (epilogue tail MMA)
 //
-// Structure (one CTA per SM, persistent over output tiles, 6 warps):
+// Structure (persistent over output tiles, 6 warps per CTA):
 //   warp 0     : TMA producer (cp.async.bulk.tensor, SWIZZLE_128B, an
 //                STAGES-deep shared-memory ring guarded by mbarriers)
 //   warp 1     : tcgen05.mma issuer (one elected thread), TMEM allocator
@@ -24,6 +24,13 @@
 //                MMA, bf16 conversion, global stores)
 // TMEM holds two 256-column fp32 accumulators (512 columns), so the epilogue
 // of tile i overlaps the main loop of tile i+1.
+//
+// CG = 2 runs the same pipeline on a CTA pair (cluster of 2 on one TPC) with
+// tcgen05.mma.cta_group::2: a 256-row tile, each CTA stages its own 128 rows
+// of the activation and HALF of the B operand, the leader CTA issues the
+// MMAs for both, and both CTAs drain their own TMEM.  Per SM this halves the
+// B-operand bytes per k-step (32 KiB instead of 48 KiB), which buys a deeper
+// TMA ring for the same shared memory.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -35,7 +42,7 @@
 
 namespace lora_sm100 {
 
-constexpr int BM = 128;            // UMMA M (rows = tokens per tile)
+constexpr int BM = 128;            // rows per CTA (UMMA M per CTA)
 constexpr int BK = 64;             // k-block: 64 bf16 = one 128-byte swizzle row
 constexpr int UMMA_K = 16;         // K per tcgen05.mma kind::f16
 constexpr int NT = 256;            // TMEM columns per accumulator buffer
@@ -45,38 +52,122 @@ constexpr int SMEM_LIMIT = 227 * 1024;
 __host__ __device__ constexpr int round_up(int v, int a) { return (v + a - 1) / a * a; }
 __host__ __device__ constexpr int cmin(int a, int b) { return a < b ? a : b; }
 
-template <int MODE, int R_PAD>
+#ifndef LORA_STAGES_CAP
+#define LORA_STAGES_CAP 8
+#endif
+
+template <int MODE, int R_PAD, int CG>
 struct GemmCfg {
     static constexpr int BN = NT - R_PAD;                         // output columns per tile
+    static constexpr int BNH = BN / CG;                           // B-operand columns staged per CTA
     static constexpr int A_BYTES = BM * BK * 2;                   // activation tile (16 KiB)
-    static constexpr int NB64 = (BN + 63) / 64;                   // MN-major W0 column blocks (dx)
-    static constexpr int B_BYTES = (MODE == kModeFwd) ? NT * BK * 2 : NB64 * 64 * BK * 2;
-    static constexpr int N_BYTES = (MODE == kModeFwd) ? 0 : R_PAD * BK * 2;  // narrow operand
+    static constexpr int NBH = (BNH + 63) / 64;                   // MN-major W0 64-col blocks per CTA (dx)
+    static constexpr int B_BYTES = (MODE == kModeFwd) ? (NT / CG) * BK * 2 : NBH * 64 * BK * 2;
+    static constexpr int NAR_ROWS = R_PAD / CG;                   // B^T rows per CTA (dx)
+    static constexpr int N_BYTES = (MODE == kModeFwd) ? 0 : NAR_ROWS * BK * 2;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES + N_BYTES;
     static constexpr int TAIL_ROW = R_PAD * 2;                    // 32 / 64 / 128 bytes
     static constexpr uint32_t TAIL_LAYOUT =
         TAIL_ROW == 32 ? kLayoutSW32 : (TAIL_ROW == 64 ? kLayoutSW64 : kLayoutSW128);
-    static constexpr int TAILB_BYTES = BN * TAIL_ROW;             // B_pad / A^T tile
+    // tail B operand per CTA: fwd = B rows [BNH x R_PAD] K-major (swizzle = row size);
+    //                         dx  = A [R_PAD x NBH*64] MN-major, 64-column SW128 blocks
+    static constexpr int TAILB_BYTES = (MODE == kModeFwd) ? BNH * TAIL_ROW : NBH * R_PAD * 128;
     static constexpr int SH_BYTES = BM * TAIL_ROW;                // bf16(s h) / bf16(gh) tile
     static constexpr int BAR_BYTES = 1024;
     static constexpr int FIXED = round_up(TAILB_BYTES, 1024) + round_up(SH_BYTES, 1024) +
                                  BAR_BYTES + 1024 /* alignment slack */;
-    static constexpr int STAGES = cmin(8, (SMEM_LIMIT - FIXED) / STAGE_BYTES);
+    static constexpr int STAGES = cmin(LORA_STAGES_CAP, (SMEM_LIMIT - FIXED) / STAGE_BYTES);
     static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + FIXED;
     static_assert(STAGES >= 2, "shared memory budget");
     static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N");
-    static_assert((BN * 128) % 1024 == 0, "A rows must start on a swizzle atom");
+    static_assert(CG == 1 || (BN % 16 == 0 && R_PAD % 16 == 0 && BN > 128), "2-CTA split");
+    static_assert(MODE != kModeFwd || (((NT / CG) - (CG == 2 ? 128 : 0)) >= 0), "layout");
 };
 
-template <int MODE, int R_PAD>
+// 2-CTA helpers ---------------------------------------------------------------
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// arrive on the barrier at the same shared-memory offset in CTA `cta` of the cluster
+__device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t cta) {
+    asm volatile(
+        "{\n\t.reg .b32 ra;\n\t"
+        "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+        "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n\t}\n"
+        ::"r"(smem_u32(bar)), "r"(cta) : "memory");
+}
+template <int CG>
+__device__ __forceinline__ void tma_load(void* dst, const CUtensorMap* map, int32_t c0, int32_t c1, uint64_t* bar) {
+    if constexpr (CG == 1) {
+        tma_load_2d(dst, map, c0, c1, bar);
+    } else {
+        // both CTAs complete their bytes on the LEADER's barrier (peer bit cleared)
+        asm volatile(
+            "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%2, %3}], [%4];"
+            ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1),
+              "r"(smem_u32(bar) & 0xFEFFFFFFu)
+            : "memory");
+    }
+}
+template <int CG>
+__device__ __forceinline__ void umma(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    if constexpr (CG == 1) {
+        umma_f16(d, a, b, idesc, acc);
+    } else {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n"
+            ::"r"(d), "l"(a), "l"(b), "r"(idesc), "r"(acc) : "memory");
+    }
+}
+// commit this thread's outstanding tcgen05 ops to `bar` (CG = 2: in both CTAs)
+template <int CG>
+__device__ __forceinline__ void commit(uint64_t* bar) {
+    if constexpr (CG == 1) {
+        umma_commit(bar);
+    } else {
+        asm volatile(
+            "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+            ::"r"(smem_u32(bar)), "h"(static_cast<uint16_t>(3)) : "memory");
+    }
+}
+template <int CG>
+__device__ __forceinline__ void tmem_alloc_cg(uint32_t* dst) {
+    if constexpr (CG == 1) {
+        tmem_alloc<512>(dst);
+    } else {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(dst))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+}
+template <int CG>
+__device__ __forceinline__ void tmem_dealloc_cg(uint32_t taddr) {
+    if constexpr (CG == 1) {
+        tmem_dealloc<512>(taddr);
+    } else {
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(taddr) : "memory");
+    }
+}
+
+template <int MODE, int R_PAD, int CG>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 lora_fused_gemm_kernel(const __grid_constant__ CUtensorMap tm_act,   // x or dY   [T, K]
-                       const __grid_constant__ CUtensorMap tm_w,     // W0        [m, n]
-                       const __grid_constant__ CUtensorMap tm_nar,   // A [r,n] / B^T [r,m]
-                       const __grid_constant__ CUtensorMap tm_tail,  // B_pad [m,R] / A^T_pad [n,R]
+                       const __grid_constant__ CUtensorMap tm_w,     // W0 [m, n] (fwd CG=2: 128-row box)
+                       const __grid_constant__ CUtensorMap tm_w2,    // fwd CG=2: W0 box of BN-128 rows
+                       const __grid_constant__ CUtensorMap tm_nar,   // fwd: A [r,n]; dx: B^T [r,m]
+                       const __grid_constant__ CUtensorMap tm_tail,  // fwd: B [m,r8]; dx: A [r,n]
                        const FusedGemmParams p) {
-    using C = GemmCfg<MODE, R_PAD>;
+    using C = GemmCfg<MODE, R_PAD, CG>;
     constexpr int BN = C::BN;
+    constexpr int TM = BM * CG;                    // rows per tile
 
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -92,9 +183,14 @@ lora_fused_gemm_kernel(const __grid_constant__ CUtensorMap tm_act,   // x or dY 
     uint64_t* tailop_full = tmem_empty + 2;
     uint64_t* tailop_empty = tailop_full + 1;
     uint64_t* tail_done = tailop_empty + 1;
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tail_done + 1);
+    uint64_t* sh_full = tail_done + 1;             // CG = 2: peer's s_h tile written
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(sh_full + 1);
 
-    const int num_t_blks = static_cast<int>((p.T + BM - 1) / BM);
+    const uint32_t crank = (CG == 2) ? cluster_ctarank() : 0;
+    const bool leader = crank == 0;
+    const int pair = static_cast<int>(blockIdx.x) / CG;
+    const int npairs = static_cast<int>(gridDim.x) / CG;
+    const int num_t_blks = static_cast<int>((p.T + TM - 1) / TM);
     const int num_n_blks = static_cast<int>((p.N_out + BN - 1) / BN);
     const int num_tiles = num_t_blks * num_n_blks;
     const int num_k_blks = static_cast<int>((p.K + BK - 1) / BK);
@@ -104,6 +200,7 @@ lora_fused_gemm_kernel(const __grid_constant__ CUtensorMap tm_act,   // x or dY 
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tm_act);
         tma_prefetch_desc(&tm_w);
+        if (MODE == kModeFwd && CG == 2) tma_prefetch_desc(&tm_w2);
         tma_prefetch_desc(&tm_nar);
         tma_prefetch_desc(&tm_tail);
     }
@@ -114,65 +211,81 @@ lora_fused_gemm_kernel(const __grid_constant__ CUtensorMap tm_act,   // x or dY 
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tmem_full[a], 1);
-            mbar_init(&tmem_empty[a], 4);  // one arrive per epilogue warp
+            mbar_init(&tmem_empty[a], 4 * CG);  // one arrive per epilogue warp of the pair
         }
         mbar_init(tailop_full, 1);
         mbar_init(tailop_empty, 1);
         mbar_init(tail_done, 1);
+        mbar_init(sh_full, 1);
         fence_mbar_init();
     }
-    if (warp == 2) tmem_alloc<512>(tmem_holder);
+    if (warp == 2) tmem_alloc_cg<CG>(tmem_holder);
     tc_fence_before();
-    __syncthreads();
+    if constexpr (CG == 2) cluster_sync(); else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
 
     if (warp == 0) {
-        // ===================== TMA producer =====================
+        // ===================== TMA producer (both CTAs) =====================
         if (elect_one()) {
             const uint64_t pol_w = l2_policy_evict_last();
             uint32_t stage = 0, phase = 0, tl = 0;
-            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++tl) {
+            for (int tile = pair; tile < num_tiles; tile += npairs, ++tl) {
                 const int n_blk = tile / num_t_blks;
                 const int t_blk = tile - n_blk * num_t_blks;
-                const int t0 = t_blk * BM;
+                const int t0 = t_blk * TM + static_cast<int>(crank) * BM;
                 const int n0 = n_blk * BN;
+                const int nh0 = n0 + static_cast<int>(crank) * C::BNH;   // this CTA's B-operand columns
                 for (int kb = 0; kb < num_k_blks; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     uint8_t* sA = stage_base + stage * C::STAGE_BYTES;
                     uint8_t* sB = sA + C::A_BYTES;
-                    mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+                    if (leader) mbar_arrive_expect_tx(&full[stage], CG * C::STAGE_BYTES);
                     const int k0 = kb * BK;
-                    tma_load_2d(sA, &tm_act, k0, t0, &full[stage]);
+                    tma_load<CG>(sA, &tm_act, k0, t0, &full[stage]);
                     if constexpr (MODE == kModeFwd) {
-                        tma_load_2d_hint(sB, &tm_w, k0, n0, &full[stage], pol_w);      // W0 rows
-                        tma_load_2d(sB + BN * 128, &tm_nar, k0, 0, &full[stage]);       // A rows
+                        if (CG == 1) {
+                            tma_load_2d_hint(sB, &tm_w, k0, n0, &full[stage], pol_w);       // W0 rows
+                            tma_load<CG>(sB + BN * 128, &tm_nar, k0, 0, &full[stage]);        // A rows
+                        } else if (crank == 0) {
+                            tma_load<CG>(sB, &tm_w, k0, n0, &full[stage]);                    // W0 rows 0..127
+                        } else {
+                            tma_load<CG>(sB, &tm_w2, k0, n0 + 128, &full[stage]);             // W0 rows 128..BN-1
+                            tma_load<CG>(sB + (BN - 128) * 128, &tm_nar, k0, 0, &full[stage]); // A rows
+                        }
                     } else {
 #pragma unroll
-                        for (int j = 0; j < C::NB64; ++j)
-                            tma_load_2d_hint(sB + j * (64 * 128), &tm_w, n0 + 64 * j, k0,
-                                             &full[stage], pol_w);
-                        tma_load_2d(sB + C::B_BYTES, &tm_nar, k0, 0, &full[stage]);    // B^T rows
+                        for (int j = 0; j < C::NBH; ++j)
+                            tma_load<CG>(sB + j * (64 * 128), &tm_w, nh0 + 64 * j, k0, &full[stage]);
+                        // B^T [r, m] columns k0..k0+63, this CTA's R_PAD/CG rows
+                        tma_load<CG>(sB + C::B_BYTES, &tm_nar, k0, static_cast<int>(crank) * C::NAR_ROWS,
+                                     &full[stage]);
                     }
                     if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
                 }
-                // tail operand for this tile (B_pad rows n0.. or A^T rows n0..)
+                // tail operand for this tile: fwd B rows; dx A columns (this CTA's half)
                 mbar_wait(tailop_empty, (tl & 1) ^ 1);
-                mbar_arrive_expect_tx(tailop_full, C::TAILB_BYTES);
-                tma_load_2d(s_tailb, &tm_tail, 0, n0, tailop_full);
+                if (leader) mbar_arrive_expect_tx(tailop_full, CG * C::TAILB_BYTES);
+                if constexpr (MODE == kModeFwd) {
+                    tma_load<CG>(s_tailb, &tm_tail, 0, nh0, tailop_full);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < C::NBH; ++j)
+                        tma_load<CG>(s_tailb + j * (R_PAD * 128), &tm_tail, nh0 + 64 * j, 0, tailop_full);
+                }
             }
         }
     } else if (warp == 1) {
-        // ===================== MMA issuer =====================
-        if (elect_one()) {
-            constexpr uint32_t idesc_main = (MODE == kModeFwd) ? make_idesc_bf16(BM, NT, 0, 0)
-                                                               : make_idesc_bf16(BM, BN, 0, 1);
-            constexpr uint32_t idesc_nar = make_idesc_bf16(BM, R_PAD, 0, 0);
+        // ===================== MMA issuer (leader CTA) =====================
+        if (leader && elect_one()) {
+            constexpr uint32_t idesc_main = (MODE == kModeFwd) ? make_idesc_bf16(TM, NT, 0, 0)
+                                                               : make_idesc_bf16(TM, BN, 0, 1);
+            constexpr uint32_t idesc_nar = make_idesc_bf16(TM, R_PAD, 0, 0);  // B^T [r, m]: K-major
             uint32_t stage = 0, phase = 0, tl = 0;
-            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++tl) {
+            for (int tile = pair; tile < num_tiles; tile += npairs, ++tl) {
                 const uint32_t acc = tl & 1;
                 const uint32_t acc_phase = (tl >> 1) & 1;
-                mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
+                mbar_wait<CG == 2>(&tmem_empty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * NT;
                 for (int kb = 0; kb < num_k_blks; ++kb) {
@@ -187,36 +300,38 @@ lora_fused_gemm_kernel(const __grid_constant__ CUtensorMap tm_act,   // x or dY 
                         if constexpr (MODE == kModeFwd) {
                             // [W0 rows ; A rows] as one K-major N = 256 operand
                             const uint64_t b_desc = make_smem_desc(b_addr + kk * 32, 16, 1024, kLayoutSW128);
-                            umma_f16(d_tmem, a_desc, b_desc, idesc_main, accum);
+                            umma<CG>(d_tmem, a_desc, b_desc, idesc_main, accum);
                         } else {
                             // W0 MN-major: 64-column blocks at LBO = 8 KiB, 8-row k groups at SBO = 1 KiB
                             const uint64_t b_desc = make_smem_desc(b_addr + kk * (UMMA_K * 128), 64 * 128,
                                                                    1024, kLayoutSW128);
-                            umma_f16(d_tmem, a_desc, b_desc, idesc_main, accum);
+                            umma<CG>(d_tmem, a_desc, b_desc, idesc_main, accum);
+                            // B^T tile [R_PAD/CG rows x 64 k] K-major SW128 (an MN-major SW32 read
+                            // of B [m, r] measured 30% slower for the whole kernel)
                             const uint64_t n_desc = make_smem_desc(b_addr + C::B_BYTES + kk * 32, 16, 1024,
                                                                    kLayoutSW128);
-                            umma_f16(d_tmem + BN, a_desc, n_desc, idesc_nar, accum);
+                            umma<CG>(d_tmem + BN, a_desc, n_desc, idesc_nar, accum);
                         }
                     }
-                    umma_commit(&empty[stage]);  // frees the smem slot when these MMAs finish
+                    commit<CG>(&empty[stage]);  // frees the smem slot(s) when these MMAs finish
                     if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
                 }
-                umma_commit(&tmem_full[acc]);
+                commit<CG>(&tmem_full[acc]);
             }
         }
     } else {
-        // ===================== epilogue (warps 2..5) =====================
+        // ===================== epilogue (warps 2..5, both CTAs) =====================
         const uint32_t ew = warp - 2;            // epilogue warp index 0..3
         const uint32_t quarter = warp & 3;       // TMEM lane quarter this warp may access
         const uint32_t row_local = quarter * 32 + lane;
-        constexpr uint32_t idesc_tail = make_idesc_bf16(BM, BN, 0, 0);
+        constexpr uint32_t idesc_tail = make_idesc_bf16(TM, BN, 0, MODE == kModeFwd ? 0 : 1);
         constexpr uint32_t tail_sbo = 8 * C::TAIL_ROW;
         const float store_scale = (MODE == kModeFwd) ? 1.0f : p.scale;  // h unscaled, gh = s G B
         uint32_t tl = 0;
-        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++tl) {
+        for (int tile = pair; tile < num_tiles; tile += npairs, ++tl) {
             const int n_blk = tile / num_t_blks;
             const int t_blk = tile - n_blk * num_t_blks;
-            const int64_t row = static_cast<int64_t>(t_blk) * BM + row_local;
+            const int64_t row = static_cast<int64_t>(t_blk) * TM + crank * BM + row_local;
             const int n0 = n_blk * BN;
             const uint32_t acc = tl & 1;
             const uint32_t acc_phase = (tl >> 1) & 1;
@@ -253,19 +368,33 @@ lora_fused_gemm_kernel(const __grid_constant__ CUtensorMap tm_act,   // x or dY 
             }
             fence_proxy_async_smem();
             named_bar_sync(1, 128);
-            // (4) tail MMA: acc[:, 0:BN] += s_h (128 x r_pad) * tail_tile (BN x r_pad)^T
+            // (4) tail MMA: acc[:, 0:BN] += s_h (rows x r_pad) * tail_tile (BN x r_pad)^T
             if (ew == 0 && lane == 0) {
-                mbar_wait(tailop_full, tl & 1);
-                tc_fence_after();
-                const uint32_t h_addr = smem_u32(s_h);
-                const uint32_t t_addr = smem_u32(s_tailb);
+                if (CG == 2 && !leader) {
+                    mbar_arrive_cluster(sh_full, 0);      // our half of s_h is ready
+                } else {
+                    if (CG == 2) mbar_wait<true>(sh_full, tl & 1);
+                    mbar_wait(tailop_full, tl & 1);
+                    tc_fence_after();
+                    const uint32_t h_addr = smem_u32(s_h);
+                    const uint32_t t_addr = smem_u32(s_tailb);
+#ifndef LORA_PROBE_NO_TAIL
 #pragma unroll
-                for (int kk = 0; kk < R_PAD / UMMA_K; ++kk) {
-                    const uint64_t a_desc = make_smem_desc(h_addr + kk * 32, 16, tail_sbo, C::TAIL_LAYOUT);
-                    const uint64_t b_desc = make_smem_desc(t_addr + kk * 32, 16, tail_sbo, C::TAIL_LAYOUT);
-                    umma_f16(tmem_base + acc * NT, a_desc, b_desc, idesc_tail, 1u);
+                    for (int kk = 0; kk < R_PAD / UMMA_K; ++kk) {
+                        const uint64_t a_desc = make_smem_desc(h_addr + kk * 32, 16, tail_sbo, C::TAIL_LAYOUT);
+                        uint64_t b_desc;
+                        if constexpr (MODE == kModeFwd) {
+                            b_desc = make_smem_desc(t_addr + kk * 32, 16, tail_sbo, C::TAIL_LAYOUT);
+                        } else {
+                            // A [R_PAD rows j, 64-col blocks of k] MN-major: LBO = block stride
+                            b_desc = make_smem_desc(t_addr + kk * (UMMA_K * 128), R_PAD * 128, 1024,
+                                                    kLayoutSW128);
+                        }
+                        umma<CG>(tmem_base + acc * NT, a_desc, b_desc, idesc_tail, 1u);
+                    }
+#endif
+                    commit<CG>(tail_done);
                 }
-                umma_commit(tail_done);
             }
             mbar_wait(tail_done, tl & 1);
             tc_fence_after();
@@ -280,7 +409,11 @@ lora_fused_gemm_kernel(const __grid_constant__ CUtensorMap tm_act,   // x or dY 
                 tmem_ld_32x32b_x16(tbase + 16 * c, v);
                 tmem_ld_wait();
                 const int64_t col = n0 + 16 * c;
+#ifdef LORA_PROBE_NO_STORE
+                if (false) {
+#else
                 if (row_ok && col < p.N_out) {
+#endif
                     float f[16];
 #pragma unroll
                     for (int e = 0; e < 16; ++e) f[e] = __uint_as_float(v[e]);
@@ -300,53 +433,77 @@ lora_fused_gemm_kernel(const __grid_constant__ CUtensorMap tm_act,   // x or dY 
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tmem_empty[acc]);
+            if (lane == 0) {
+                if (CG == 1) mbar_arrive(&tmem_empty[acc]);
+                else mbar_arrive_cluster(&tmem_empty[acc], 0);  // the leader's MMA warp waits on it
+            }
         }
     }
 
-    __syncthreads();
+    tc_fence_before();
+    if constexpr (CG == 2) cluster_sync(); else __syncthreads();
     if (warp == 2) {
         tc_fence_after();
-        tmem_dealloc<512>(tmem_base);
+        tmem_dealloc_cg<CG>(tmem_base);
     }
 }
 
 // ----------------------------------------------------------------------------
 // host side
 // ----------------------------------------------------------------------------
-template <int MODE, int R_PAD>
+template <int MODE, int R_PAD, int CG>
 static cudaError_t launch_impl(const FusedGemmMaps& maps, const FusedGemmParams& p, int num_sms,
                                cudaStream_t stream) {
-    using C = GemmCfg<MODE, R_PAD>;
-    auto kern = lora_fused_gemm_kernel<MODE, R_PAD>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         C::SMEM_BYTES);
+    using C = GemmCfg<MODE, R_PAD, CG>;
+    auto kern = lora_fused_gemm_kernel<MODE, R_PAD, CG>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
     if (e != cudaSuccess) return e;
-    const int64_t tiles = ((p.T + BM - 1) / BM) * ((p.N_out + C::BN - 1) / C::BN);
-    const int grid = static_cast<int>(tiles < num_sms ? tiles : num_sms);
+    const int64_t tiles = ((p.T + BM * CG - 1) / (BM * CG)) * ((p.N_out + C::BN - 1) / C::BN);
+    const int64_t units = num_sms / CG;
+    const int grid = static_cast<int>((tiles < units ? tiles : units) * CG);
     if (grid <= 0) return cudaSuccess;
-    kern<<<grid, NUM_THREADS, C::SMEM_BYTES, stream>>>(maps.act, maps.w, maps.nar, maps.tail, p);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(NUM_THREADS);
+    cfg.dynamicSmemBytes = C::SMEM_BYTES;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, kern, maps.act, maps.w, maps.w2, maps.nar, maps.tail, p);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
 int fused_gemm_block_n(int r_pad) { return NT - r_pad; }
 
-cudaError_t launch_fused_gemm(int mode, int r_pad, const FusedGemmMaps& maps,
-                              const FusedGemmParams& p, int num_sms, cudaStream_t stream) {
+template <int CG>
+static cudaError_t dispatch(int mode, int r_pad, const FusedGemmMaps& maps, const FusedGemmParams& p, int num_sms,
+                           cudaStream_t stream) {
     if (mode == kModeFwd) {
         switch (r_pad) {
-            case 16: return launch_impl<kModeFwd, 16>(maps, p, num_sms, stream);
-            case 32: return launch_impl<kModeFwd, 32>(maps, p, num_sms, stream);
-            case 64: return launch_impl<kModeFwd, 64>(maps, p, num_sms, stream);
+            case 16: return launch_impl<kModeFwd, 16, CG>(maps, p, num_sms, stream);
+            case 32: return launch_impl<kModeFwd, 32, CG>(maps, p, num_sms, stream);
+            case 64: return launch_impl<kModeFwd, 64, CG>(maps, p, num_sms, stream);
         }
     } else {
         switch (r_pad) {
-            case 16: return launch_impl<kModeDx, 16>(maps, p, num_sms, stream);
-            case 32: return launch_impl<kModeDx, 32>(maps, p, num_sms, stream);
-            case 64: return launch_impl<kModeDx, 64>(maps, p, num_sms, stream);
+            case 16: return launch_impl<kModeDx, 16, CG>(maps, p, num_sms, stream);
+            case 32: return launch_impl<kModeDx, 32, CG>(maps, p, num_sms, stream);
+            case 64: return launch_impl<kModeDx, 64, CG>(maps, p, num_sms, stream);
         }
     }
     return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_fused_gemm(int mode, int r_pad, int cta_group, const FusedGemmMaps& maps,
+                              const FusedGemmParams& p, int num_sms, cudaStream_t stream) {
+    return cta_group == 2 ? dispatch<2>(mode, r_pad, maps, p, num_sms, stream)
+                          : dispatch<1>(mode, r_pad, maps, p, num_sms, stream);
 }
 
 }  // namespace lora_sm100

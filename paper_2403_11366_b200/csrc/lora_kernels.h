@@ -23,42 +23,31 @@ struct FusedGemmParams {
 };
 
 struct FusedGemmMaps {
-    CUtensorMap act, w, nar, tail;
+    CUtensorMap act, w, w2, nar, tail;
 };
 
-// K1 / K2.  r_pad in {16, 32, 64}; tiles are 128 x (256 - r_pad).
+// K1 / K2.  r_pad in {16, 32, 64}; tiles are (128 * cta_group) x (256 - r_pad).
+// cta_group = 2 runs on CTA pairs (tcgen05 cta_group::2); the TMA boxes of
+// `maps` must match (see lora_api.cpp).
 int fused_gemm_block_n(int r_pad);
-cudaError_t launch_fused_gemm(int mode, int r_pad, const FusedGemmMaps& maps,
+cudaError_t launch_fused_gemm(int mode, int r_pad, int cta_group, const FusedGemmMaps& maps,
                               const FusedGemmParams& p, int num_sms, cudaStream_t stream);
 
-// B6: adapter pack.  Any output pointer may be null (skipped).
-//   bpad [m, r_pad] = B zero-padded      (fwd tail operand, K-major)
-//   bt   [r, m]     = B^T                (dx narrow operand, K-major)
-//   at   [n, r_pad] = A^T zero-padded    (dx tail operand, K-major)
-cudaError_t launch_pack(const __nv_bfloat16* a, const __nv_bfloat16* b, int64_t n, int64_t m,
-                        int r, int r_pad, __nv_bfloat16* bpad, __nv_bfloat16* bt,
-                        __nv_bfloat16* at, int num_sms, cudaStream_t stream);
+// B6: b8 [m, roundup(r, 8)] = B zero-padded (fwd, only when r % 8 != 0: TMA
+// row pitch must be a multiple of 16 bytes); bt [r, m] = B^T (dx narrow
+// operand, K-major).  Either output may be null.
+cudaError_t launch_pack_b(const __nv_bfloat16* b, int64_t m, int r, __nv_bfloat16* b8, __nv_bfloat16* bt,
+                          int num_sms, cudaStream_t stream);
 
-// K3: dA = gh^T x, dB = s dY^T h.  Column-strip partial sums over token
-// chunks (fixed order) + a finalize pass; deterministic.
-struct GradReducePlan {
-    int r_bucket;        // register tile rank (4, 8, 16, 32, 64)
-    int cols_per_strip;  // 32 * columns-per-thread
-    int strips_a, strips_b;
-    int chunks;          // token chunks
-    int rows_per_chunk;
-};
-GradReducePlan plan_grad_reduce(int64_t T, int64_t n, int64_t m, int r, int num_sms);
-size_t grad_reduce_partial_bytes(const GradReducePlan& pl, int64_t n, int64_t m, int r);
-cudaError_t launch_grad_reduce(const GradReducePlan& pl, int64_t T, int64_t n, int64_t m, int r,
-                               float scale, const __nv_bfloat16* x, const float* gh,
-                               const __nv_bfloat16* dy, const float* h, float* partials,
-                               float* da, float* db, int accumulate, cudaStream_t stream,
-                               int* launches);
+// K3: dA = gh^T x, dB = s dY^T h; one CTA per 32-column strip over all tokens,
+// fixed summation order (deterministic), writes the final values.
+cudaError_t launch_grad_reduce(int64_t T, int64_t n, int64_t m, int r, float scale, const __nv_bfloat16* x,
+                               const float* gh, const __nv_bfloat16* dy, const float* h, float* da, float* db,
+                               int accumulate, cudaStream_t stream, int* launches);
 
-// K3a: out[t, j] = scale * sum_k X[t, k] P[j, k]   (h when not saved; gh when dx is skipped)
-cudaError_t launch_rowproj(const __nv_bfloat16* X, int64_t T, int64_t K, const __nv_bfloat16* P,
-                           int r, float scale, float* out, cudaStream_t stream);
+// K3a: out[t, j] = scale * sum_k X[t, k] P(j, k); P(j, k) = P[j * ldp + k], or P[k * ldp + j] if p_t.
+cudaError_t launch_rowproj(const __nv_bfloat16* X, int64_t T, int64_t K, const __nv_bfloat16* P, int64_t ldp,
+                           int p_t, int r, float scale, float* out, cudaStream_t stream);
 
 // K4: w_out = bf16(W0 + s * B A)
 cudaError_t launch_merge(const __nv_bfloat16* w0, const __nv_bfloat16* a, const __nv_bfloat16* b,

@@ -51,6 +51,15 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
         : "=r"(ok) : "r"(addr), "r"(parity) : "memory");
     return ok != 0;
 }
+__device__ __forceinline__ bool mbar_try_wait_cluster(uint32_t addr, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%1], %2, 1000000;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}\n"
+        : "=r"(ok) : "r"(addr), "r"(parity) : "memory");
+    return ok != 0;
+}
 __device__ __forceinline__ uint64_t globaltimer_ns() {
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -58,11 +67,15 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
 }
 // Blocking wait on the phase with parity `parity`.  A barrier that never
 // completes (a pipeline bug) traps after ~4 s instead of hanging the GPU.
+// kCluster: acquire at cluster scope (the barrier receives arrivals from the
+// peer CTA of a 2-CTA pair).
+template <bool kCluster = false>
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t addr = smem_u32(bar);
-    if (mbar_try_wait(addr, parity)) return;
+    auto probe = [&]() { return kCluster ? mbar_try_wait_cluster(addr, parity) : mbar_try_wait(addr, parity); };
+    if (probe()) return;
     const uint64_t t0 = globaltimer_ns();
-    while (!mbar_try_wait(addr, parity)) {
+    while (!probe()) {
         if (globaltimer_ns() - t0 > 4000000000ull) {
             printf("lora kernel: mbarrier wait timed out (block %d thread %d parity %u)\n",
                    blockIdx.x, threadIdx.x, parity);

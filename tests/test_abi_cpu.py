@@ -84,7 +84,7 @@ def test_bwd_and_merge_validation_codes():
 
 def test_workspace_sizes_scale_with_shape():
     f = L.lora_linear_fwd_workspace_bytes
-    assert f(L.dims(2048, 4096, 4096, 8, 16.0)) >= 4096 * 16 * 2
+    assert f(L.dims(2048, 4096, 4096, 8, 16.0)) >= 4096 * 8 * 2       # B8 [m, roundup(r, 8)]
     assert f(L.dims(2048, 4096, 4096, 8, 16.0)) == f(L.dims(7, 4096, 4096, 8, 16.0))
     b = L.lora_linear_bwd_workspace_bytes
     assert b(L.dims(4096, 4096, 11008, 16, 16.0)) > b(L.dims(2048, 4096, 11008, 16, 16.0))
