@@ -96,7 +96,7 @@ static EncodeTiledFn encode_fn() {
 // [box_outer, box_inner].  Out-of-bounds box elements read as zero.
 static lora_status encode_2d(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer,
                              uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer, int swizzle_bytes,
-                             const char* name) {
+                             const char* name, CUtensorMapDataType dtype = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16) {
     EncodeTiledFn fn = encode_fn();
     if (!fn) return fail(LORA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
     cuuint64_t dims[2] = {inner, outer};
@@ -105,8 +105,9 @@ static lora_status encode_2d(CUtensorMap* map, const void* ptr, uint64_t inner, 
     cuuint32_t estr[2] = {1, 1};
     CUtensorMapSwizzle sw = swizzle_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
                             : swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
-                                                  : CU_TENSOR_MAP_SWIZZLE_32B;
-    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                            : swizzle_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                                  : CU_TENSOR_MAP_SWIZZLE_NONE;
+    CUresult r = fn(map, dtype, 2, const_cast<void*>(ptr), dims, strides, box, estr,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS)
@@ -178,7 +179,7 @@ static BwdWs bwd_ws(const lora_dims* d) {
     const int64_t T = d->tokens > 0 ? d->tokens : 0;
     const int r = d->rank;
     size_t off = 0;
-    w.bt = off; off += align256(size_t(r) * d->d_out * 2);
+    w.bt = off;  // (no B^T copy is needed any more; kept as a zero-size slot)
     w.gh = off; off += align256(size_t(T) * r * 4);
     w.h = off; off += align256(size_t(T) * r * 4);
     w.total = off;
@@ -220,7 +221,7 @@ lora_status fwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
 
     const int rp = r_pad_of(r);
     const int r8 = r8_of(r);
-    const int BN = fused_gemm_block_n(rp);
+    const int BN = fused_gemm_block_n(kModeFwd, rp);
     // B is read by TMA with its own row pitch when r % 8 == 0; otherwise a
     // zero-padded copy B8 [m, r8] is made first (B6).
     const void* bsrc = b;
@@ -246,6 +247,7 @@ lora_status fwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
     p.bias = static_cast<const __nv_bfloat16*>(bias);
     p.out = static_cast<__nv_bfloat16*>(y);
     p.side_out = h_out;
+    p.side_in = nullptr;
     cudaError_t e = launch_fused_gemm(kModeFwd, rp, cg, maps, p, dev.sms, stream);
     if (e != cudaSuccess) return cuda_fail(e, "fused forward launch");
     ++*launches;
@@ -309,37 +311,29 @@ lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
     const bool need_gh = dx || da;
     const bool need_h = db && !h_saved;
 
-    // B^T [r, m] (B6): the K-major operand of K2's narrow dY B MMA and of K3a
-    auto* bt = reinterpret_cast<__nv_bfloat16*>(wsb + W.bt);
+    // K2a: gh = s dY B [T, r] fp32 (read by K2's epilogue tail and by K3's dA)
     if (need_gh) {
-        if ((e = launch_pack_b(static_cast<const __nv_bfloat16*>(b), m, r, nullptr, bt, dev.sms, stream)) !=
-            cudaSuccess)
-            return cuda_fail(e, "pack launch");
+        if ((e = launch_gh(dya, static_cast<const __nv_bfloat16*>(b), T, m, r, s, gh, stream)) != cudaSuccess)
+            return cuda_fail(e, "gh launch");
         ++*launches;
     }
     (void)r8;
     if (dx) {
-        const int BN = fused_gemm_block_n(rp);
         FusedGemmMaps maps;
         const int cg = cta_group_for(T);
         if ((st = encode_2d(&maps.act, dy, m, T, m * 2, 64, 128, 128, "dy")) != LORA_OK) return st;
         if ((st = encode_2d(&maps.w, w0, n, m, n * 2, 64, 64, 128, "w0")) != LORA_OK) return st;
         maps.w2 = maps.w;
-        if ((st = encode_2d(&maps.nar, bt, m, r, m * 2, 64, rp / cg, 128, "b^T")) != LORA_OK) return st;
+        maps.nar = maps.w;  // unused in the dX kernel
         if ((st = encode_2d(&maps.tail, a, n, r, n * 2, 64, rp, 128, "a")) != LORA_OK) return st;
         FusedGemmParams p;
         p.T = T; p.K = m; p.N_out = n; p.r = r; p.scale = s;
         p.bias = nullptr;
         p.out = static_cast<__nv_bfloat16*>(dx);
-        p.side_out = gh;
+        p.side_out = nullptr;
+        p.side_in = gh;
         if ((e = launch_fused_gemm(kModeDx, rp, cg, maps, p, dev.sms, stream)) != cudaSuccess)
             return cuda_fail(e, "fused dX launch");
-        ++*launches;
-        (void)BN;
-    } else if (da) {
-        // gh = s dY B via the row-projection kernel on B^T [r, m]
-        if ((e = launch_rowproj(dya, T, m, bt, m, 0, r, s, gh, stream)) != cudaSuccess)
-            return cuda_fail(e, "gh rowproj");
         ++*launches;
     }
     const float* hsrc = h_saved;
@@ -350,7 +344,27 @@ lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
         hsrc = hbuf;
     }
     if (da || db) {
-        e = launch_grad_reduce(T, n, m, r, s, xa, gh, dya, hsrc, da, db, accumulate, stream, launches);
+        const char* k3 = getenv("LORA_K3");  // experiments: "tma" | "ldg"; default: cluster
+        if (!k3 || (strcmp(k3, "tma") != 0 && strcmp(k3, "ldg") != 0)) {
+            e = launch_grad_reduce_cluster(T, n, m, r, s, xa, gh, dya, hsrc, da, db, accumulate, stream, launches);
+        } else if (r % 4 == 0 && strcmp(k3, "tma") == 0) {
+            // TMA-ring variant: coefficient rows (4r bytes) are TMA-legal when r % 4 == 0
+            GradMaps gm;
+            const int sc = grad_strip_cols();
+            if ((st = encode_2d(&gm.x, x, n, T, n * 2, sc, 64, 0, "x")) != LORA_OK) return st;
+            if ((st = encode_2d(&gm.dy, dy, m, T, m * 2, sc, 64, 0, "dy")) != LORA_OK) return st;
+            const float* ghp = da ? gh : hsrc;   // unused map when the gradient is not requested
+            const float* hp = db ? hsrc : gh;
+            if ((st = encode_2d(&gm.gh, ghp, r, T, size_t(r) * 4, r, 64, 0, "gh", CU_TENSOR_MAP_DATA_TYPE_FLOAT32)) !=
+                LORA_OK)
+                return st;
+            if ((st = encode_2d(&gm.h, hp, r, T, size_t(r) * 4, r, 64, 0, "h", CU_TENSOR_MAP_DATA_TYPE_FLOAT32)) !=
+                LORA_OK)
+                return st;
+            e = launch_grad_reduce_tma(gm, T, n, m, r, s, da, db, accumulate, stream, launches);
+        } else {
+            e = launch_grad_reduce(T, n, m, r, s, xa, gh, dya, hsrc, da, db, accumulate, stream, launches);
+        }
         if (e != cudaSuccess) return cuda_fail(e, "grad reduce launch");
     }
     return LORA_OK;

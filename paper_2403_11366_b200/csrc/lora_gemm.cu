@@ -12,8 +12,9 @@
 // K2 (MODE_DX), the input gradient of Eq. 1 (W0 frozen):
 //     acc  = dY W0             (W0 [m, n] read as an MN-major B operand: no
 //                               transposed weight copy)
-//     gh   = s dY B            (same pass: narrow N = r_pad MMA on the dY tile
-//                               already in shared memory)
+//     gh   = s dY B            (K2a pre-pass in lora_grad.cu, read by the
+//                               epilogue; a narrow in-loop MMA measured ~20%
+//                               slower for this kernel)
 //     dX   = bf16(acc + bf16(gh) A)  (epilogue tail MMA)
 //
 // Structure (persistent over output tiles, 6 warps per CTA):
@@ -55,17 +56,21 @@ __host__ __device__ constexpr int cmin(int a, int b) { return a < b ? a : b; }
 #ifndef LORA_STAGES_CAP
 #define LORA_STAGES_CAP 8
 #endif
+#ifndef LORA_DX_BN
+#define LORA_DX_BN 256
+#endif
 
 template <int MODE, int R_PAD, int CG>
 struct GemmCfg {
-    static constexpr int BN = NT - R_PAD;                         // output columns per tile
+    // fwd: BN + r_pad = 256 (h shares the accumulator); dx: gh comes from K2a,
+    // so the tile can be LORA_DX_BN wide (256 keeps the MN-major W0 boxes
+    // 128-byte aligned in global memory)
+    static constexpr int BN = (MODE == kModeFwd) ? NT - R_PAD : LORA_DX_BN;
     static constexpr int BNH = BN / CG;                           // B-operand columns staged per CTA
     static constexpr int A_BYTES = BM * BK * 2;                   // activation tile (16 KiB)
     static constexpr int NBH = (BNH + 63) / 64;                   // MN-major W0 64-col blocks per CTA (dx)
     static constexpr int B_BYTES = (MODE == kModeFwd) ? (NT / CG) * BK * 2 : NBH * 64 * BK * 2;
-    static constexpr int NAR_ROWS = R_PAD / CG;                   // B^T rows per CTA (dx)
-    static constexpr int N_BYTES = (MODE == kModeFwd) ? 0 : NAR_ROWS * BK * 2;
-    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES + N_BYTES;
+    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int TAIL_ROW = R_PAD * 2;                    // 32 / 64 / 128 bytes
     static constexpr uint32_t TAIL_LAYOUT =
         TAIL_ROW == 32 ? kLayoutSW32 : (TAIL_ROW == 64 ? kLayoutSW64 : kLayoutSW128);
@@ -162,7 +167,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 lora_fused_gemm_kernel(const __grid_constant__ CUtensorMap tm_act,   // x or dY   [T, K]
                        const __grid_constant__ CUtensorMap tm_w,     // W0 [m, n] (fwd CG=2: 128-row box)
                        const __grid_constant__ CUtensorMap tm_w2,    // fwd CG=2: W0 box of BN-128 rows
-                       const __grid_constant__ CUtensorMap tm_nar,   // fwd: A [r,n]; dx: B^T [r,m]
+                       const __grid_constant__ CUtensorMap tm_nar,   // fwd: A [r,n]; dx: unused
                        const __grid_constant__ CUtensorMap tm_tail,  // fwd: B [m,r8]; dx: A [r,n]
                        const FusedGemmParams p) {
     using C = GemmCfg<MODE, R_PAD, CG>;
@@ -257,9 +262,6 @@ lora_fused_gemm_kernel(const __grid_constant__ CUtensorMap tm_act,   // x or dY 
 #pragma unroll
                         for (int j = 0; j < C::NBH; ++j)
                             tma_load<CG>(sB + j * (64 * 128), &tm_w, nh0 + 64 * j, k0, &full[stage]);
-                        // B^T [r, m] columns k0..k0+63, this CTA's R_PAD/CG rows
-                        tma_load<CG>(sB + C::B_BYTES, &tm_nar, k0, static_cast<int>(crank) * C::NAR_ROWS,
-                                     &full[stage]);
                     }
                     if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
                 }
@@ -280,7 +282,6 @@ lora_fused_gemm_kernel(const __grid_constant__ CUtensorMap tm_act,   // x or dY 
         if (leader && elect_one()) {
             constexpr uint32_t idesc_main = (MODE == kModeFwd) ? make_idesc_bf16(TM, NT, 0, 0)
                                                                : make_idesc_bf16(TM, BN, 0, 1);
-            constexpr uint32_t idesc_nar = make_idesc_bf16(TM, R_PAD, 0, 0);  // B^T [r, m]: K-major
             uint32_t stage = 0, phase = 0, tl = 0;
             for (int tile = pair; tile < num_tiles; tile += npairs, ++tl) {
                 const uint32_t acc = tl & 1;
@@ -306,11 +307,8 @@ lora_fused_gemm_kernel(const __grid_constant__ CUtensorMap tm_act,   // x or dY 
                             const uint64_t b_desc = make_smem_desc(b_addr + kk * (UMMA_K * 128), 64 * 128,
                                                                    1024, kLayoutSW128);
                             umma<CG>(d_tmem, a_desc, b_desc, idesc_main, accum);
-                            // B^T tile [R_PAD/CG rows x 64 k] K-major SW128 (an MN-major SW32 read
-                            // of B [m, r] measured 30% slower for the whole kernel)
-                            const uint64_t n_desc = make_smem_desc(b_addr + C::B_BYTES + kk * 32, 16, 1024,
-                                                                   kLayoutSW128);
-                            umma<CG>(d_tmem + BN, a_desc, n_desc, idesc_nar, accum);
+                            // gh = s dY B comes from the K2a pre-pass: a separate narrow
+                            // N = r_pad MMA here cost ~20% of this kernel (A-operand re-reads)
                         }
                     }
                     commit<CG>(&empty[stage]);  // frees the smem slot(s) when these MMAs finish
@@ -326,7 +324,6 @@ lora_fused_gemm_kernel(const __grid_constant__ CUtensorMap tm_act,   // x or dY 
         const uint32_t row_local = quarter * 32 + lane;
         constexpr uint32_t idesc_tail = make_idesc_bf16(TM, BN, 0, MODE == kModeFwd ? 0 : 1);
         constexpr uint32_t tail_sbo = 8 * C::TAIL_ROW;
-        const float store_scale = (MODE == kModeFwd) ? 1.0f : p.scale;  // h unscaled, gh = s G B
         uint32_t tl = 0;
         for (int tile = pair; tile < num_tiles; tile += npairs, ++tl) {
             const int n_blk = tile / num_t_blks;
@@ -339,31 +336,39 @@ lora_fused_gemm_kernel(const __grid_constant__ CUtensorMap tm_act,   // x or dY 
             tc_fence_after();
             const uint32_t tbase = tmem_base + ((quarter * 32) << 16) + acc * NT;
 
-            // (1) the r_pad low-rank columns: h = x A^T (fwd) or G B (dx)
+            // (1) the r_pad low-rank values of this row: fwd h = x A^T from TMEM
+            //     columns [BN, BN + r_pad); dx gh = s dY B from the K2a pre-pass
             float hv[R_PAD];
+            if constexpr (MODE == kModeFwd) {
 #pragma unroll
-            for (int c = 0; c < R_PAD / 16; ++c) {
-                uint32_t v[16];
-                tmem_ld_32x32b_x16(tbase + BN + 16 * c, v);
-                tmem_ld_wait();
+                for (int c = 0; c < R_PAD / 16; ++c) {
+                    uint32_t v[16];
+                    tmem_ld_32x32b_x16(tbase + BN + 16 * c, v);
+                    tmem_ld_wait();
 #pragma unroll
-                for (int e = 0; e < 16; ++e) hv[16 * c + e] = __uint_as_float(v[e]);
-            }
-            // (2) side output: h (fwd, for dB) / gh (dx, for dA); one tile column per row block
-            if (p.side_out != nullptr && n_blk == 0 && row < p.T) {
-                float* dst = p.side_out + row * p.r;
+                    for (int e = 0; e < 16; ++e) hv[16 * c + e] = __uint_as_float(v[e]);
+                }
+                // (2) side output h (for dB = s dY^T h); one tile column per row block
+                if (p.side_out != nullptr && n_blk == 0 && row < p.T) {
+                    float* dst = p.side_out + row * p.r;
 #pragma unroll
-                for (int j = 0; j < R_PAD; ++j)
-                    if (j < p.r) dst[j] = store_scale * hv[j];
+                    for (int j = 0; j < R_PAD; ++j)
+                        if (j < p.r) dst[j] = hv[j];
+                }
+            } else {
+                const float* src = p.side_in + row * p.r;
+#pragma unroll
+                for (int j = 0; j < R_PAD; ++j) hv[j] = (j < p.r && row < p.T) ? __ldg(src + j) : 0.0f;
             }
             // (3) bf16(s h) / bf16(gh) -> swizzled K-major smem tile (tail MMA A operand)
+            const float op_scale = (MODE == kModeFwd) ? p.scale : 1.0f;
 #pragma unroll
             for (int c = 0; c < R_PAD / 8; ++c) {
                 uint4 q;
-                q.x = pack_bf16x2(p.scale * hv[8 * c + 0], p.scale * hv[8 * c + 1]);
-                q.y = pack_bf16x2(p.scale * hv[8 * c + 2], p.scale * hv[8 * c + 3]);
-                q.z = pack_bf16x2(p.scale * hv[8 * c + 4], p.scale * hv[8 * c + 5]);
-                q.w = pack_bf16x2(p.scale * hv[8 * c + 6], p.scale * hv[8 * c + 7]);
+                q.x = pack_bf16x2(op_scale * hv[8 * c + 0], op_scale * hv[8 * c + 1]);
+                q.y = pack_bf16x2(op_scale * hv[8 * c + 2], op_scale * hv[8 * c + 3]);
+                q.z = pack_bf16x2(op_scale * hv[8 * c + 4], op_scale * hv[8 * c + 5]);
+                q.w = pack_bf16x2(op_scale * hv[8 * c + 6], op_scale * hv[8 * c + 7]);
                 *reinterpret_cast<uint4*>(s_h + swizzled_offset(row_local, c, C::TAIL_ROW)) = q;
             }
             fence_proxy_async_smem();
@@ -479,7 +484,7 @@ static cudaError_t launch_impl(const FusedGemmMaps& maps, const FusedGemmParams&
     return cudaGetLastError();
 }
 
-int fused_gemm_block_n(int r_pad) { return NT - r_pad; }
+int fused_gemm_block_n(int mode, int r_pad) { return mode == kModeFwd ? NT - r_pad : LORA_DX_BN; }
 
 template <int CG>
 static cudaError_t dispatch(int mode, int r_pad, const FusedGemmMaps& maps, const FusedGemmParams& p, int num_sms,

@@ -19,7 +19,8 @@ struct FusedGemmParams {
     float scale;                  // s = alpha / r
     const __nv_bfloat16* bias;    // fwd only; may be null
     __nv_bfloat16* out;           // y or dx, [T, N_out]
-    float* side_out;              // fwd: h [T, r] (unscaled); dx: gh [T, r] = s dY B; may be null
+    float* side_out;              // fwd: h [T, r] (unscaled), may be null
+    const float* side_in;         // dx: gh [T, r] = s dY B (from K2a)
 };
 
 struct FusedGemmMaps {
@@ -29,7 +30,7 @@ struct FusedGemmMaps {
 // K1 / K2.  r_pad in {16, 32, 64}; tiles are (128 * cta_group) x (256 - r_pad).
 // cta_group = 2 runs on CTA pairs (tcgen05 cta_group::2); the TMA boxes of
 // `maps` must match (see lora_api.cpp).
-int fused_gemm_block_n(int r_pad);
+int fused_gemm_block_n(int mode, int r_pad);
 cudaError_t launch_fused_gemm(int mode, int r_pad, int cta_group, const FusedGemmMaps& maps,
                               const FusedGemmParams& p, int num_sms, cudaStream_t stream);
 
@@ -38,6 +39,25 @@ cudaError_t launch_fused_gemm(int mode, int r_pad, int cta_group, const FusedGem
 // operand, K-major).  Either output may be null.
 cudaError_t launch_pack_b(const __nv_bfloat16* b, int64_t m, int r, __nv_bfloat16* b8, __nv_bfloat16* bt,
                           int num_sms, cudaStream_t stream);
+
+// K2a: gh [T, r] = s dY B (fp32), read by K2's epilogue and by K3 (dA).
+cudaError_t launch_gh(const __nv_bfloat16* dy, const __nv_bfloat16* b, int64_t T, int64_t m, int r, float s,
+                      float* gh, cudaStream_t stream);
+
+// K3 (TMA ring variant, r % 4 == 0): x, dY boxes {32 cols, 64 rows} bf16, gh, h
+// boxes {r, 64 rows} fp32, no swizzle.
+struct GradMaps {
+    CUtensorMap x, dy, gh, h;
+};
+int grad_strip_cols();  // columns per K3 CTA (box inner extent of the x / dY maps)
+
+// K3 v3 (default): T split over a cluster of 8 CTAs, DSMEM reduction in rank order.
+cudaError_t launch_grad_reduce_cluster(int64_t T, int64_t n, int64_t m, int r, float scale,
+                                       const __nv_bfloat16* x, const float* gh, const __nv_bfloat16* dy,
+                                       const float* h, float* da, float* db, int accumulate,
+                                       cudaStream_t stream, int* launches);
+cudaError_t launch_grad_reduce_tma(const GradMaps& maps, int64_t T, int64_t n, int64_t m, int r, float scale,
+                                   float* da, float* db, int accumulate, cudaStream_t stream, int* launches);
 
 // K3: dA = gh^T x, dB = s dY^T h; one CTA per 32-column strip over all tokens,
 // fixed summation order (deterministic), writes the final values.

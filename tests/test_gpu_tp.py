@@ -1,0 +1,57 @@
+"""Tensor-parallel entry points on one B200 (N = 1): lora_tp_linear_fwd/bwd
+through a real NCCL communicator owned by liblora.so must equal the
+single-GPU calls bitwise (R13), in both COLUMN and ROW modes and
+with the LoRA-gradient reduction inside or left to a bucketed all-reduce."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from synth import make_lora_inputs  # noqa: E402
+from tests.gpu_util import dev_bf16  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def comm():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2403_11366_b200 import tp
+    c = tp.LoraComm()
+    yield c
+    c.close()
+
+
+@pytest.mark.parametrize("mode", ["column", "row"])
+@pytest.mark.parametrize("accumulate", [False, True])
+def test_tp_n1_equals_single_call(comm, mode, accumulate):
+    import paper_2403_11366_b200 as L
+    from paper_2403_11366_b200 import tp
+    T, n, m, r = 384, 512, 640, 8
+    d = make_lora_inputs(T, n, m, r, seed=61, bias=True)
+    x, w0, a, b, dy, bias = (dev_bf16(d[k]) for k in ("x", "w0", "a", "b", "dy", "bias"))
+    spec = tp.ShardSpec(tp.MODES[mode], 1, 0, n, m)
+    y1, h1 = L.lora_linear_fwd(x, w0, a, b, 16.0, bias=bias)
+    y2, h2 = tp.tp_linear_fwd(comm, spec, x, w0, a, b, 16.0, bias=bias)
+    da0 = torch.randn((r, n), device="cuda")
+    db0 = torch.randn((m, r), device="cuda")
+    dx1, da1, db1 = L.lora_linear_bwd(x, w0, a, b, dy, 16.0, h_saved=h1, da=da0.clone(), db=db0.clone(),
+                                      accumulate=accumulate)
+    dx2, da2, db2 = tp.tp_linear_bwd(comm, spec, x, w0, a, b, dy, 16.0, h_saved=h2, da=da0.clone(),
+                                     db=db0.clone(), accumulate=accumulate)
+    torch.cuda.synchronize()
+    for u, v in ((y1, y2), (h1, h2), (dx1, dx2), (da1, da2), (db1, db2)):
+        assert torch.equal(u, v)
+
+
+def test_allreduce_n1_identity(comm):
+    t = torch.randn(1000, device="cuda")
+    ref = t.clone()
+    comm.allreduce(t)
+    torch.cuda.synchronize()
+    assert torch.equal(t, ref)
+    tb = torch.randn(1000, device="cuda").bfloat16()
+    refb = tb.clone()
+    comm.allreduce(tb)
+    torch.cuda.synchronize()
+    assert torch.equal(tb, refb)

@@ -49,11 +49,28 @@ def time_one(T=2048, n=4096, m=4096, r=8, iters=50):
     x, w0, a, b, dy = (dev(d[k]) for k in ("x", "w0", "a", "b", "dy"))
     y, h = L.lora_linear_fwd(x, w0, a, b, 16.0)
     dx, _, _ = L.lora_linear_bwd(x, w0, a, b, dy, 16.0, h_saved=h, want_da=False, want_db=False)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    flush_w = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
+    flush_r = torch.zeros_like(flush_w)
+
+    class _Flush:  # write 256 MiB, then read 256 MiB: cold L2 without dirty lines
+        def fill_(self, v):
+            flush_w.fill_(float(v))
+            torch.sum(flush_r)
+
+    flush = _Flush()
     res = {}
+    da = torch.zeros((r, n), device="cuda")
+    db = torch.zeros((m, r), device="cuda")
     for name, fn in (("fwd", lambda: L.lora_linear_fwd(x, w0, a, b, 16.0, y=y, h_out=h)),
                      ("dx", lambda: L.lora_linear_bwd(x, w0, a, b, dy, 16.0, h_saved=h, dx=dx,
-                                                      want_da=False, want_db=False))):
+                                                      want_da=False, want_db=False)),
+                     ("grads_gh_k3", lambda: L.lora_linear_bwd(x, w0, a, b, dy, 16.0, h_saved=h, want_dx=False,
+                                                               da=da, db=db)),
+                     ("db_k3_only", lambda: L.lora_linear_bwd(x, w0, a, b, dy, 16.0, h_saved=h, want_dx=False,
+                                                              want_da=False, db=db)),
+                     # references for a 16 MiB read of dY on this box / in this harness
+                     ("torch_sum_dy", lambda: torch.sum(dy, dtype=torch.float32)),
+                     ("torch_copy_dy", lambda: dx.copy_(dy))):
         for _ in range(5):
             fn()
         ts = []
@@ -76,8 +93,10 @@ def run():
     out = {}
     jobs = [(name, os.path.join(OUT, f"liblora_{name}.so"), {}) for name in VARIANTS]
     # the in-tree library with the CTA-pair choice forced either way
-    jobs += [(f"tree_cg{cg}", os.path.join(ROOT, "paper_2403_11366_b200", "liblora.so"),
-              {"LORA_CTA_GROUP": str(cg)}) for cg in (1, 2)]
+    tree = os.path.join(ROOT, "paper_2403_11366_b200", "liblora.so")
+    jobs += [(f"tree_cg{cg}", tree, {"LORA_CTA_GROUP": str(cg)}) for cg in (1, 2)]
+    jobs += [("tree_k3ldg", tree, {"LORA_K3": "ldg"}), ("tree_k3tma", tree, {"LORA_K3": "tma"}),
+             ("tree_ghv1", tree, {"LORA_GH_V1": "1"})]
     for name, lib, extra in jobs:
         if not os.path.exists(lib):
             continue
