@@ -261,21 +261,21 @@ def run_ours(args, wl):
                 ev["f0"].record(stream)
             if comm is None:
                 L.lora_linear_fwd(e["x"], e["w0"], e["a"], e["b"], e["l"].alpha, y=e["y"], h_out=e["h"],
-                                  workspace=e["ws_f"], stream=stream)
+                                  workspace=e["ws_f"], stream=torch.cuda.current_stream())
             else:
                 tp.tp_linear_fwd(comm, e["spec"], e["x"], e["w0"], e["a"], e["b"], e["l"].alpha, y=e["y"],
-                                 h_out=e["h"], workspace=e["ws_f"], stream=stream)
+                                 h_out=e["h"], workspace=e["ws_f"], stream=torch.cuda.current_stream())
             launches["n"] += L.lora_last_launch_count()
             if ev is not None and e is lin[0]:
                 ev["f1"].record(stream)
         for e in lin:
             if comm is None:
                 L.lora_linear_bwd(e["x"], e["w0"], e["a"], e["b"], e["dy"], e["l"].alpha, h_saved=e["h"],
-                                  dx=e["dx"], da=e["da"], db=e["db"], workspace=e["ws_b"], stream=stream)
+                                  dx=e["dx"], da=e["da"], db=e["db"], workspace=e["ws_b"], stream=torch.cuda.current_stream())
             else:
                 tp.tp_linear_bwd(comm, e["spec"], e["x"], e["w0"], e["a"], e["b"], e["dy"], e["l"].alpha,
                                  h_saved=e["h"], dx=e["dx"], da=e["da"], db=e["db"], workspace=e["ws_b"],
-                                 reduce_lora_grads=True, stream=stream)
+                                 reduce_lora_grads=True, stream=torch.cuda.current_stream())
             launches["n"] += L.lora_last_launch_count()
 
     # L2 flush between timed steps, outside the event pairs: write a 2 x L2
@@ -319,6 +319,12 @@ def run_ours(args, wl):
         for _ in range(3):
             graph.replay()
         barrier()
+        # the graph must really contain the step: clear an output, replay, check it came back
+        lin[0]["y"].zero_()
+        graph.replay()
+        barrier()
+        if per_step_launches == 0 or int(torch.count_nonzero(lin[0]["y"]).item()) == 0:
+            raise RuntimeError("CUDA graph capture of the step is empty")
     ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
     ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
     fev = [dict(f0=torch.cuda.Event(enable_timing=True), f1=torch.cuda.Event(enable_timing=True))
@@ -344,7 +350,7 @@ def run_ours(args, wl):
             flush.fill_(i & 0xFF)
             fev[i]["f0"].record(stream)
             L.lora_linear_fwd(e["x"], e["w0"], e["a"], e["b"], e["l"].alpha, y=e["y"], h_out=e["h"],
-                              workspace=e["ws_f"], stream=stream)
+                              workspace=e["ws_f"], stream=torch.cuda.current_stream())
             fev[i]["f1"].record(stream)
         barrier()
     # the first linear's forward call (B6 pack + fused K1), timed on the launching stream

@@ -12,6 +12,9 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
+#include <chrono>
+#include <cstdlib>
 #include <mutex>
 #include <string>
 
@@ -172,18 +175,31 @@ static FwdWs fwd_ws(const lora_dims* d) {
 
 // Backward workspace: B^T [r, m], gh [T, r] fp32, h [T, r] fp32 (when not saved).
 struct BwdWs {
-    size_t bt, gh, h, total;
+    size_t b8, gh, h, flags, total;
 };
 static BwdWs bwd_ws(const lora_dims* d) {
     BwdWs w;
     const int64_t T = d->tokens > 0 ? d->tokens : 0;
     const int r = d->rank;
     size_t off = 0;
-    w.bt = off;  // (no B^T copy is needed any more; kept as a zero-size slot)
+    w.b8 = off; off += align256(size_t(d->d_out) * r8_of(r) * 2);    // only used when r % 8 != 0
     w.gh = off; off += align256(size_t(T) * r * 4);
     w.h = off; off += align256(size_t(T) * r * 4);
+    w.flags = off; off += align256(size_t(T / 128 + 2) * 8);         // >= row blocks x CTAs per pair
     w.total = off;
     return w;
+}
+
+// Value the dX kernel's gh flags take in one launch: a per-process random base
+// plus a counter, so stale workspace contents never match by accident.
+static uint64_t next_epoch() {
+    static std::atomic<uint64_t> counter{0};
+    static const uint64_t base = [] {
+        uint64_t v = static_cast<uint64_t>(std::chrono::high_resolution_clock::now().time_since_epoch().count());
+        v ^= reinterpret_cast<uintptr_t>(&counter) * 0x9E3779B97F4A7C15ull;
+        return v | 1ull;
+    }();
+    return base + 2 * counter.fetch_add(1);
 }
 
 // ------------------------------------------------------------ forward
@@ -247,7 +263,9 @@ lora_status fwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
     p.bias = static_cast<const __nv_bfloat16*>(bias);
     p.out = static_cast<__nv_bfloat16*>(y);
     p.side_out = h_out;
-    p.side_in = nullptr;
+    p.gh = nullptr;
+    p.flags = nullptr;
+    p.epoch = 0;
     cudaError_t e = launch_fused_gemm(kModeFwd, rp, cg, maps, p, dev.sms, stream);
     if (e != cudaSuccess) return cuda_fail(e, "fused forward launch");
     ++*launches;
@@ -311,29 +329,39 @@ lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
     const bool need_gh = dx || da;
     const bool need_h = db && !h_saved;
 
-    // K2a: gh = s dY B [T, r] fp32 (read by K2's epilogue tail and by K3's dA)
-    if (need_gh) {
-        if ((e = launch_gh(dya, static_cast<const __nv_bfloat16*>(b), T, m, r, s, gh, stream)) != cudaSuccess)
-            return cuda_fail(e, "gh launch");
-        ++*launches;
-    }
-    (void)r8;
     if (dx) {
+        // K2 computes gh = s dY B itself (first column tile of each row block)
+        const __nv_bfloat16* bsrc = static_cast<const __nv_bfloat16*>(b);
+        if (r != r8) {   // B rows of 2r bytes are not TMA-legal: B6 pads them to r8
+            auto* b8 = reinterpret_cast<__nv_bfloat16*>(wsb + W.b8);
+            if ((e = launch_pack_b(bsrc, m, r, b8, nullptr, dev.sms, stream)) != cudaSuccess)
+                return cuda_fail(e, "pack launch");
+            ++*launches;
+            bsrc = b8;
+        }
         FusedGemmMaps maps;
         const int cg = cta_group_for(T);
+        const int nar_h = fused_gemm_narrow_cols(rp, cg);
         if ((st = encode_2d(&maps.act, dy, m, T, m * 2, 64, 128, 128, "dy")) != LORA_OK) return st;
         if ((st = encode_2d(&maps.w, w0, n, m, n * 2, 64, 64, 128, "w0")) != LORA_OK) return st;
         maps.w2 = maps.w;
-        maps.nar = maps.w;  // unused in the dX kernel
+        if ((st = encode_2d(&maps.nar, bsrc, r8, m, r8 * 2, nar_h, 64, nar_h * 2, "b")) != LORA_OK) return st;
         if ((st = encode_2d(&maps.tail, a, n, r, n * 2, 64, rp, 128, "a")) != LORA_OK) return st;
         FusedGemmParams p;
         p.T = T; p.K = m; p.N_out = n; p.r = r; p.scale = s;
         p.bias = nullptr;
         p.out = static_cast<__nv_bfloat16*>(dx);
         p.side_out = nullptr;
-        p.side_in = gh;
+        p.gh = gh;
+        p.flags = reinterpret_cast<uint64_t*>(wsb + W.flags);
+        p.epoch = next_epoch();
         if ((e = launch_fused_gemm(kModeDx, rp, cg, maps, p, dev.sms, stream)) != cudaSuccess)
             return cuda_fail(e, "fused dX launch");
+        ++*launches;
+    } else if (da) {
+        // K2a: gh = s dY B [T, r] fp32 for dA when the input gradient is not requested
+        if ((e = launch_gh(dya, static_cast<const __nv_bfloat16*>(b), T, m, r, s, gh, stream)) != cudaSuccess)
+            return cuda_fail(e, "gh launch");
         ++*launches;
     }
     const float* hsrc = h_saved;

@@ -12,9 +12,13 @@
 // K2 (MODE_DX), the input gradient of Eq. 1 (W0 frozen):
 //     acc  = dY W0             (W0 [m, n] read as an MN-major B operand: no
 //                               transposed weight copy)
-//     gh   = s dY B            (K2a pre-pass in lora_grad.cu, read by the
-//                               epilogue; a narrow in-loop MMA measured ~20%
-//                               slower for this kernel)
+//     gh   = s dY B            (same pass, but only in the FIRST column tile of
+//                               each row block: that tile is 128 columns wide
+//                               and runs an extra narrow MMA on B [m, r] into
+//                               TMEM columns 128.., publishes gh to global and
+//                               raises a per-row-block flag; the other tiles are
+//                               256 wide -- 128-byte-aligned MN-major W0 boxes --
+//                               and wait for the flag before their tail)
 //     dX   = bf16(acc + bf16(gh) A)  (epilogue tail MMA)
 //
 // Structure (persistent over output tiles, 6 warps per CTA):
@@ -49,28 +53,32 @@ constexpr int UMMA_K = 16;         // K per tcgen05.mma kind::f16
 constexpr int NT = 256;            // TMEM columns per accumulator buffer
 constexpr int NUM_THREADS = 192;   // 6 warps
 constexpr int SMEM_LIMIT = 227 * 1024;
+constexpr int DX_BN0 = 128;        // dx: width of the first (gh-producing) column tile
 
 __host__ __device__ constexpr int round_up(int v, int a) { return (v + a - 1) / a * a; }
 __host__ __device__ constexpr int cmin(int a, int b) { return a < b ? a : b; }
+__host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 
 #ifndef LORA_STAGES_CAP
 #define LORA_STAGES_CAP 8
 #endif
-#ifndef LORA_DX_BN
-#define LORA_DX_BN 256
-#endif
 
 template <int MODE, int R_PAD, int CG>
 struct GemmCfg {
-    // fwd: BN + r_pad = 256 (h shares the accumulator); dx: gh comes from K2a,
-    // so the tile can be LORA_DX_BN wide (256 keeps the MN-major W0 boxes
-    // 128-byte aligned in global memory)
-    static constexpr int BN = (MODE == kModeFwd) ? NT - R_PAD : LORA_DX_BN;
-    static constexpr int BNH = BN / CG;                           // B-operand columns staged per CTA
+    // fwd: BN + r_pad = 256 (h shares the accumulator); dx: 256 (gh in the first tile)
+    static constexpr int BN = (MODE == kModeFwd) ? NT - R_PAD : NT;
+    static constexpr int BNH = BN / CG;                           // B-operand columns per CTA
     static constexpr int A_BYTES = BM * BK * 2;                   // activation tile (16 KiB)
-    static constexpr int NBH = (BNH + 63) / 64;                   // MN-major W0 64-col blocks per CTA (dx)
+    static constexpr int NBH = (BNH + 63) / 64;                   // dx: MN-major W0 64-col blocks per CTA
     static constexpr int B_BYTES = (MODE == kModeFwd) ? (NT / CG) * BK * 2 : NBH * 64 * BK * 2;
-    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    // dx narrow operand (first column tile only): B [m, r] rows k0..k0+63, NAR columns
+    // split over the pair; MN-major, swizzle = NAR_H * 2 bytes (32 / 64 / 128)
+    static constexpr int NAR = (MODE == kModeFwd) ? 0 : (CG == 2 ? cmax(32, R_PAD) : R_PAD);
+    static constexpr int NAR_H = NAR / CG;
+    static constexpr int NAR_BYTES = BK * NAR_H * 2;
+    static constexpr uint32_t NAR_LAYOUT =
+        NAR_H * 2 == 32 ? kLayoutSW32 : (NAR_H * 2 == 64 ? kLayoutSW64 : kLayoutSW128);
+    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES + NAR_BYTES;
     static constexpr int TAIL_ROW = R_PAD * 2;                    // 32 / 64 / 128 bytes
     static constexpr uint32_t TAIL_LAYOUT =
         TAIL_ROW == 32 ? kLayoutSW32 : (TAIL_ROW == 64 ? kLayoutSW64 : kLayoutSW128);
@@ -85,8 +93,24 @@ struct GemmCfg {
     static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + FIXED;
     static_assert(STAGES >= 2, "shared memory budget");
     static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N");
-    static_assert(CG == 1 || (BN % 16 == 0 && R_PAD % 16 == 0 && BN > 128), "2-CTA split");
-    static_assert(MODE != kModeFwd || (((NT / CG) - (CG == 2 ? 128 : 0)) >= 0), "layout");
+    static_assert(CG == 1 || (BN > 128 && R_PAD % 16 == 0), "2-CTA split");
+    static_assert(MODE == kModeFwd || DX_BN0 + NAR <= NT, "gh columns fit next to the first tile");
+};
+
+// Column tiling.  fwd: uniform BN-wide tiles.  dx: tile 0 is DX_BN0 wide (and
+// computes gh), tiles 1.. are BN wide starting at DX_BN0 (so every 64-column
+// W0 / A box starts 128-byte aligned).
+template <int MODE, int BN>
+struct ColTiles {
+    __device__ static int count(int64_t n_out) {
+        if (MODE == kModeFwd) return static_cast<int>((n_out + BN - 1) / BN);
+        return n_out <= DX_BN0 ? 1 : 1 + static_cast<int>((n_out - DX_BN0 + BN - 1) / BN);
+    }
+    __device__ static int start(int n_blk) {
+        if (MODE == kModeFwd) return n_blk * BN;
+        return n_blk == 0 ? 0 : DX_BN0 + (n_blk - 1) * BN;
+    }
+    __device__ static int width(int n_blk) { return (MODE == kModeFwd || n_blk != 0) ? BN : DX_BN0; }
 };
 
 // 2-CTA helpers ---------------------------------------------------------------
@@ -161,16 +185,25 @@ __device__ __forceinline__ void tmem_dealloc_cg(uint32_t taddr) {
         asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(taddr) : "memory");
     }
 }
+__device__ __forceinline__ uint64_t ld_acquire_u64(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u64(uint64_t* p, uint64_t v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 
 template <int MODE, int R_PAD, int CG>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 lora_fused_gemm_kernel(const __grid_constant__ CUtensorMap tm_act,   // x or dY   [T, K]
                        const __grid_constant__ CUtensorMap tm_w,     // W0 [m, n] (fwd CG=2: 128-row box)
                        const __grid_constant__ CUtensorMap tm_w2,    // fwd CG=2: W0 box of BN-128 rows
-                       const __grid_constant__ CUtensorMap tm_nar,   // fwd: A [r,n]; dx: unused
+                       const __grid_constant__ CUtensorMap tm_nar,   // fwd: A [r,n]; dx: B [m,r8]
                        const __grid_constant__ CUtensorMap tm_tail,  // fwd: B [m,r8]; dx: A [r,n]
                        const FusedGemmParams p) {
     using C = GemmCfg<MODE, R_PAD, CG>;
+    using Cols = ColTiles<MODE, C::BN>;
     constexpr int BN = C::BN;
     constexpr int TM = BM * CG;                    // rows per tile
 
@@ -196,7 +229,7 @@ lora_fused_gemm_kernel(const __grid_constant__ CUtensorMap tm_act,   // x or dY 
     const int pair = static_cast<int>(blockIdx.x) / CG;
     const int npairs = static_cast<int>(gridDim.x) / CG;
     const int num_t_blks = static_cast<int>((p.T + TM - 1) / TM);
-    const int num_n_blks = static_cast<int>((p.N_out + BN - 1) / BN);
+    const int num_n_blks = Cols::count(p.N_out);
     const int num_tiles = num_t_blks * num_n_blks;
     const int num_k_blks = static_cast<int>((p.K + BK - 1) / BK);
     const uint32_t warp = warp_id();
@@ -239,13 +272,19 @@ lora_fused_gemm_kernel(const __grid_constant__ CUtensorMap tm_act,   // x or dY 
                 const int n_blk = tile / num_t_blks;
                 const int t_blk = tile - n_blk * num_t_blks;
                 const int t0 = t_blk * TM + static_cast<int>(crank) * BM;
-                const int n0 = n_blk * BN;
-                const int nh0 = n0 + static_cast<int>(crank) * C::BNH;   // this CTA's B-operand columns
+                const int n0 = Cols::start(n_blk);
+                const int wh = Cols::width(n_blk) / CG;                 // this CTA's B-operand columns
+                const int nh0 = n0 + static_cast<int>(crank) * wh;
+                const int nb = (wh + 63) / 64;                          // dx: 64-column W0 / A blocks
+                const bool gh_tile = (MODE == kModeDx) && n_blk == 0;
+                const uint32_t stage_tx = (MODE == kModeFwd)
+                    ? static_cast<uint32_t>(C::STAGE_BYTES)
+                    : static_cast<uint32_t>(C::A_BYTES + nb * 64 * BK * 2 + (gh_tile ? C::NAR_BYTES : 0));
                 for (int kb = 0; kb < num_k_blks; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     uint8_t* sA = stage_base + stage * C::STAGE_BYTES;
                     uint8_t* sB = sA + C::A_BYTES;
-                    if (leader) mbar_arrive_expect_tx(&full[stage], CG * C::STAGE_BYTES);
+                    if (leader) mbar_arrive_expect_tx(&full[stage], CG * stage_tx);
                     const int k0 = kb * BK;
                     tma_load<CG>(sA, &tm_act, k0, t0, &full[stage]);
                     if constexpr (MODE == kModeFwd) {
@@ -259,20 +298,22 @@ lora_fused_gemm_kernel(const __grid_constant__ CUtensorMap tm_act,   // x or dY 
                             tma_load<CG>(sB + (BN - 128) * 128, &tm_nar, k0, 0, &full[stage]); // A rows
                         }
                     } else {
-#pragma unroll
-                        for (int j = 0; j < C::NBH; ++j)
+                        for (int j = 0; j < nb; ++j)
                             tma_load<CG>(sB + j * (64 * 128), &tm_w, nh0 + 64 * j, k0, &full[stage]);
+                        if (gh_tile)   // B rows k0..k0+63, this CTA's NAR_H columns
+                            tma_load<CG>(sB + C::B_BYTES, &tm_nar, static_cast<int>(crank) * C::NAR_H, k0,
+                                         &full[stage]);
                     }
                     if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
                 }
                 // tail operand for this tile: fwd B rows; dx A columns (this CTA's half)
                 mbar_wait(tailop_empty, (tl & 1) ^ 1);
-                if (leader) mbar_arrive_expect_tx(tailop_full, CG * C::TAILB_BYTES);
                 if constexpr (MODE == kModeFwd) {
+                    if (leader) mbar_arrive_expect_tx(tailop_full, CG * C::TAILB_BYTES);
                     tma_load<CG>(s_tailb, &tm_tail, 0, nh0, tailop_full);
                 } else {
-#pragma unroll
-                    for (int j = 0; j < C::NBH; ++j)
+                    if (leader) mbar_arrive_expect_tx(tailop_full, CG * nb * R_PAD * 128);
+                    for (int j = 0; j < nb; ++j)
                         tma_load<CG>(s_tailb + j * (R_PAD * 128), &tm_tail, nh0 + 64 * j, 0, tailop_full);
                 }
             }
@@ -280,10 +321,15 @@ lora_fused_gemm_kernel(const __grid_constant__ CUtensorMap tm_act,   // x or dY 
     } else if (warp == 1) {
         // ===================== MMA issuer (leader CTA) =====================
         if (leader && elect_one()) {
-            constexpr uint32_t idesc_main = (MODE == kModeFwd) ? make_idesc_bf16(TM, NT, 0, 0)
-                                                               : make_idesc_bf16(TM, BN, 0, 1);
+            constexpr uint32_t idesc_fwd = make_idesc_bf16(TM, NT, 0, 0);
+            constexpr uint32_t idesc_dx_full = make_idesc_bf16(TM, BN, 0, 1);
+            constexpr uint32_t idesc_dx_first = make_idesc_bf16(TM, DX_BN0, 0, 1);
+            constexpr uint32_t idesc_nar = make_idesc_bf16(TM, C::NAR > 0 ? C::NAR : 16, 0, 1);
             uint32_t stage = 0, phase = 0, tl = 0;
             for (int tile = pair; tile < num_tiles; tile += npairs, ++tl) {
+                const int n_blk = tile / num_t_blks;
+                const bool gh_tile = (MODE == kModeDx) && n_blk == 0;
+                const uint32_t idesc_main = (MODE == kModeFwd) ? idesc_fwd : (gh_tile ? idesc_dx_first : idesc_dx_full);
                 const uint32_t acc = tl & 1;
                 const uint32_t acc_phase = (tl >> 1) & 1;
                 mbar_wait<CG == 2>(&tmem_empty[acc], acc_phase ^ 1);
@@ -307,8 +353,13 @@ lora_fused_gemm_kernel(const __grid_constant__ CUtensorMap tm_act,   // x or dY 
                             const uint64_t b_desc = make_smem_desc(b_addr + kk * (UMMA_K * 128), 64 * 128,
                                                                    1024, kLayoutSW128);
                             umma<CG>(d_tmem, a_desc, b_desc, idesc_main, accum);
-                            // gh = s dY B comes from the K2a pre-pass: a separate narrow
-                            // N = r_pad MMA here cost ~20% of this kernel (A-operand re-reads)
+                            if (gh_tile) {
+                                // dY B: one MN-major atom of NAR_H columns per CTA, SBO = 8 rows
+                                const uint64_t n_desc = make_smem_desc(
+                                    b_addr + C::B_BYTES + kk * (UMMA_K * C::NAR_H * 2), 16, 8 * C::NAR_H * 2,
+                                    C::NAR_LAYOUT);
+                                umma<CG>(d_tmem + DX_BN0, a_desc, n_desc, idesc_nar, accum);
+                            }
                         }
                     }
                     commit<CG>(&empty[stage]);  // frees the smem slot(s) when these MMAs finish
@@ -322,43 +373,72 @@ lora_fused_gemm_kernel(const __grid_constant__ CUtensorMap tm_act,   // x or dY 
         const uint32_t ew = warp - 2;            // epilogue warp index 0..3
         const uint32_t quarter = warp & 3;       // TMEM lane quarter this warp may access
         const uint32_t row_local = quarter * 32 + lane;
-        constexpr uint32_t idesc_tail = make_idesc_bf16(TM, BN, 0, MODE == kModeFwd ? 0 : 1);
+        constexpr uint32_t idesc_tail_fwd = make_idesc_bf16(TM, BN, 0, 0);
+        constexpr uint32_t idesc_tail_dx_full = make_idesc_bf16(TM, BN, 0, 1);
+        constexpr uint32_t idesc_tail_dx_first = make_idesc_bf16(TM, DX_BN0, 0, 1);
         constexpr uint32_t tail_sbo = 8 * C::TAIL_ROW;
         uint32_t tl = 0;
         for (int tile = pair; tile < num_tiles; tile += npairs, ++tl) {
             const int n_blk = tile / num_t_blks;
             const int t_blk = tile - n_blk * num_t_blks;
             const int64_t row = static_cast<int64_t>(t_blk) * TM + crank * BM + row_local;
-            const int n0 = n_blk * BN;
+            const int n0 = Cols::start(n_blk);
+            const int width = Cols::width(n_blk);
+            const bool gh_tile = (MODE == kModeDx) && n_blk == 0;
             const uint32_t acc = tl & 1;
             const uint32_t acc_phase = (tl >> 1) & 1;
             mbar_wait(&tmem_full[acc], acc_phase);
             tc_fence_after();
             const uint32_t tbase = tmem_base + ((quarter * 32) << 16) + acc * NT;
 
-            // (1) the r_pad low-rank values of this row: fwd h = x A^T from TMEM
-            //     columns [BN, BN + r_pad); dx gh = s dY B from the K2a pre-pass
+            // (1) the r_pad low-rank values of this row
             float hv[R_PAD];
-            if constexpr (MODE == kModeFwd) {
+            if (MODE == kModeFwd || gh_tile) {
+                // fwd: h = x A^T in TMEM columns [BN, BN + r_pad); dx first tile: dY B in [128, ..)
+                const uint32_t col0 = (MODE == kModeFwd) ? BN : DX_BN0;
 #pragma unroll
                 for (int c = 0; c < R_PAD / 16; ++c) {
                     uint32_t v[16];
-                    tmem_ld_32x32b_x16(tbase + BN + 16 * c, v);
+                    tmem_ld_32x32b_x16(tbase + col0 + 16 * c, v);
                     tmem_ld_wait();
 #pragma unroll
                     for (int e = 0; e < 16; ++e) hv[16 * c + e] = __uint_as_float(v[e]);
                 }
-                // (2) side output h (for dB = s dY^T h); one tile column per row block
-                if (p.side_out != nullptr && n_blk == 0 && row < p.T) {
-                    float* dst = p.side_out + row * p.r;
+                if (MODE == kModeDx) {
+#pragma unroll
+                    for (int j = 0; j < R_PAD; ++j) hv[j] *= p.scale;     // gh = s (dY B)
+                }
+                // (2) side output: fwd h (for dB); dx gh (for the other tiles and for dA)
+                float* side = (MODE == kModeFwd) ? p.side_out : p.gh;
+                if (side != nullptr && (MODE == kModeDx || n_blk == 0) && row < p.T) {
+                    float* dst = side + row * p.r;
 #pragma unroll
                     for (int j = 0; j < R_PAD; ++j)
                         if (j < p.r) dst[j] = hv[j];
                 }
+                if (MODE == kModeDx) {
+                    // publish: every thread's gh stores, then one release of the flag
+                    __threadfence();
+                    named_bar_sync(1, 128);
+                    if (ew == 0 && lane == 0)
+                        st_release_u64(p.flags + static_cast<int64_t>(t_blk) * CG + crank, p.epoch);
+                }
             } else {
-                const float* src = p.side_in + row * p.r;
+                // dx, later tiles: wait for this row block's gh, then read it
+                const uint64_t* flag = p.flags + static_cast<int64_t>(t_blk) * CG + crank;
+                if (ld_acquire_u64(flag) != p.epoch) {
+                    const uint64_t t_start = globaltimer_ns();
+                    while (ld_acquire_u64(flag) != p.epoch) {
+                        __nanosleep(64);
+                        if (globaltimer_ns() - t_start > 4000000000ull) {
+                            printf("lora dX kernel: gh flag wait timed out (row block %d)\n", t_blk);
+                            __trap();
+                        }
+                    }
+                }
+                const float* src = p.gh + row * p.r;
 #pragma unroll
-                for (int j = 0; j < R_PAD; ++j) hv[j] = (j < p.r && row < p.T) ? __ldg(src + j) : 0.0f;
+                for (int j = 0; j < R_PAD; ++j) hv[j] = (j < p.r && row < p.T) ? src[j] : 0.0f;
             }
             // (3) bf16(s h) / bf16(gh) -> swizzled K-major smem tile (tail MMA A operand)
             const float op_scale = (MODE == kModeFwd) ? p.scale : 1.0f;
@@ -373,7 +453,7 @@ lora_fused_gemm_kernel(const __grid_constant__ CUtensorMap tm_act,   // x or dY 
             }
             fence_proxy_async_smem();
             named_bar_sync(1, 128);
-            // (4) tail MMA: acc[:, 0:BN] += s_h (rows x r_pad) * tail_tile (BN x r_pad)^T
+            // (4) tail MMA: acc[:, 0:width] += s_h (rows x r_pad) * tail_tile (width x r_pad)^T
             if (ew == 0 && lane == 0) {
                 if (CG == 2 && !leader) {
                     mbar_arrive_cluster(sh_full, 0);      // our half of s_h is ready
@@ -383,6 +463,8 @@ lora_fused_gemm_kernel(const __grid_constant__ CUtensorMap tm_act,   // x or dY 
                     tc_fence_after();
                     const uint32_t h_addr = smem_u32(s_h);
                     const uint32_t t_addr = smem_u32(s_tailb);
+                    const uint32_t idesc_tail = (MODE == kModeFwd)
+                        ? idesc_tail_fwd : (gh_tile ? idesc_tail_dx_first : idesc_tail_dx_full);
 #ifndef LORA_PROBE_NO_TAIL
 #pragma unroll
                     for (int kk = 0; kk < R_PAD / UMMA_K; ++kk) {
@@ -409,7 +491,7 @@ lora_fused_gemm_kernel(const __grid_constant__ CUtensorMap tm_act,   // x or dY 
             const bool row_ok = row < p.T;
             __nv_bfloat16* out_row = p.out + row * p.N_out;
 #pragma unroll 1
-            for (int c = 0; c < BN / 16; ++c) {
+            for (int c = 0; c < width / 16; ++c) {
                 uint32_t v[16];
                 tmem_ld_32x32b_x16(tbase + 16 * c, v);
                 tmem_ld_wait();
@@ -456,6 +538,14 @@ lora_fused_gemm_kernel(const __grid_constant__ CUtensorMap tm_act,   // x or dY 
 // ----------------------------------------------------------------------------
 // host side
 // ----------------------------------------------------------------------------
+static int64_t col_tiles_host(int mode, int r_pad, int64_t n_out) {
+    if (mode == kModeFwd) {
+        const int bn = NT - r_pad;
+        return (n_out + bn - 1) / bn;
+    }
+    return n_out <= DX_BN0 ? 1 : 1 + (n_out - DX_BN0 + NT - 1) / NT;
+}
+
 template <int MODE, int R_PAD, int CG>
 static cudaError_t launch_impl(const FusedGemmMaps& maps, const FusedGemmParams& p, int num_sms,
                                cudaStream_t stream) {
@@ -463,7 +553,7 @@ static cudaError_t launch_impl(const FusedGemmMaps& maps, const FusedGemmParams&
     auto kern = lora_fused_gemm_kernel<MODE, R_PAD, CG>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
     if (e != cudaSuccess) return e;
-    const int64_t tiles = ((p.T + BM * CG - 1) / (BM * CG)) * ((p.N_out + C::BN - 1) / C::BN);
+    const int64_t tiles = ((p.T + BM * CG - 1) / (BM * CG)) * col_tiles_host(MODE, R_PAD, p.N_out);
     const int64_t units = num_sms / CG;
     const int grid = static_cast<int>((tiles < units ? tiles : units) * CG);
     if (grid <= 0) return cudaSuccess;
@@ -484,7 +574,14 @@ static cudaError_t launch_impl(const FusedGemmMaps& maps, const FusedGemmParams&
     return cudaGetLastError();
 }
 
-int fused_gemm_block_n(int mode, int r_pad) { return mode == kModeFwd ? NT - r_pad : LORA_DX_BN; }
+int fused_gemm_block_n(int mode, int r_pad) { return mode == kModeFwd ? NT - r_pad : NT; }
+
+int fused_gemm_narrow_cols(int r_pad, int cta_group) {
+    const int nar = cta_group == 2 ? (r_pad > 32 ? r_pad : 32) : r_pad;
+    return nar / cta_group;
+}
+
+int64_t fused_gemm_row_blocks(int64_t T, int cta_group) { return (T + BM * cta_group - 1) / (BM * cta_group); }
 
 template <int CG>
 static cudaError_t dispatch(int mode, int r_pad, const FusedGemmMaps& maps, const FusedGemmParams& p, int num_sms,

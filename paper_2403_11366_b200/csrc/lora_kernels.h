@@ -20,7 +20,9 @@ struct FusedGemmParams {
     const __nv_bfloat16* bias;    // fwd only; may be null
     __nv_bfloat16* out;           // y or dx, [T, N_out]
     float* side_out;              // fwd: h [T, r] (unscaled), may be null
-    const float* side_in;         // dx: gh [T, r] = s dY B (from K2a)
+    float* gh;                    // dx: gh [T, r] = s dY B, written by the first column tile
+    uint64_t* flags;              // dx: one per (row block, CTA of the pair): gh published
+    uint64_t epoch;               // dx: value the flags take in this launch (never reset)
 };
 
 struct FusedGemmMaps {
@@ -31,6 +33,8 @@ struct FusedGemmMaps {
 // cta_group = 2 runs on CTA pairs (tcgen05 cta_group::2); the TMA boxes of
 // `maps` must match (see lora_api.cpp).
 int fused_gemm_block_n(int mode, int r_pad);
+int fused_gemm_narrow_cols(int r_pad, int cta_group);     // dx: B columns per CTA (TMA box inner)
+int64_t fused_gemm_row_blocks(int64_t T, int cta_group);  // dx: flags needed = row blocks * cta_group
 cudaError_t launch_fused_gemm(int mode, int r_pad, int cta_group, const FusedGemmMaps& maps,
                               const FusedGemmParams& p, int num_sms, cudaStream_t stream);
 
