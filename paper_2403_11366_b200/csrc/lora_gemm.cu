@@ -262,6 +262,11 @@ lora_fused_gemm_kernel(const __grid_constant__ CUtensorMap tm_act,   // x or dY 
     if constexpr (CG == 2) cluster_sync(); else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
+    // Programmatic dependent launch: everything above (barrier init, TMEM
+    // allocation, descriptor prefetch) overlapped the previous kernel's tail;
+    // no global memory is touched before the previous grid has completed.
+    griddep_wait();
+    if (threadIdx.x == 0) griddep_launch_dependents();
 
     if (warp == 0) {
         // ===================== TMA producer (both CTAs) =====================
@@ -562,19 +567,32 @@ static cudaError_t launch_impl(const FusedGemmMaps& maps, const FusedGemmParams&
     cfg.blockDim = dim3(NUM_THREADS);
     cfg.dynamicSmemBytes = C::SMEM_BYTES;
     cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = CG;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     e = cudaLaunchKernelEx(&cfg, kern, maps.act, maps.w, maps.w2, maps.nar, maps.tail, p);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
 int fused_gemm_block_n(int mode, int r_pad) { return mode == kModeFwd ? NT - r_pad : NT; }
+
+// Off by default: measured on B200 (cfg2 step replayed as a CUDA graph) PDL
+// launches were 6% slower than plain stream order (243 vs 258 us/step);
+// LORA_PDL=1 turns it on.
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* s = getenv("LORA_PDL");
+        return s && s[0] == '1';
+    }();
+    return on;
+}
 
 int fused_gemm_narrow_cols(int r_pad, int cta_group) {
     const int nar = cta_group == 2 ? (r_pad > 32 ? r_pad : 32) : r_pad;

@@ -606,6 +606,8 @@ __global__ void __launch_bounds__(256, (RB >= 64 ? 1 : 2)) grad_cluster_kernel(c
     rpc = (rpc + 7) / 8 * 8;
     const int64_t t_begin = rank * rpc;
     const int64_t t_end = (g.T < t_begin + rpc) ? g.T : t_begin + rpc;
+    griddep_wait();                       // programmatic dependent launch (see lora_gemm.cu)
+    if (threadIdx.x == 0) griddep_launch_dependents();
 
     float acc[CPT][RB];
 #pragma unroll
@@ -721,13 +723,15 @@ static cudaError_t launch_cluster_rb(int64_t n, int64_t m, const GradArgs& g, bo
     cfg.blockDim = dim3(256);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 1;
     attr[0].val.clusterDim.y = kCS;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     e = cudaLaunchKernelEx(&cfg, kern, g, ba);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();

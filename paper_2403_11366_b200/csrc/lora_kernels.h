@@ -11,6 +11,9 @@ namespace lora_sm100 {
 
 enum : int { kModeFwd = 0, kModeDx = 1 };
 
+// Programmatic dependent launch for the step's kernels (LORA_PDL=1; off by default).
+bool pdl_enabled();
+
 struct FusedGemmParams {
     int64_t T;                    // token rows
     int64_t K;                    // reduction extent (n fwd, m dx)
