@@ -267,6 +267,10 @@ lora_fused_gemm_kernel(const __grid_constant__ CUtensorMap tm_act,   // x or dY 
     // no global memory is touched before the previous grid has completed.
     griddep_wait();
     if (threadIdx.x == 0) griddep_launch_dependents();
+#ifdef LORA_PROBE_CLOCK
+    const long long probe_c0 = clock64();
+    const uint64_t probe_t0 = globaltimer_ns();
+#endif
 
     if (warp == 0) {
         // ===================== TMA producer (both CTAs) =====================
@@ -289,6 +293,14 @@ lora_fused_gemm_kernel(const __grid_constant__ CUtensorMap tm_act,   // x or dY 
                     mbar_wait(&empty[stage], phase ^ 1);
                     uint8_t* sA = stage_base + stage * C::STAGE_BYTES;
                     uint8_t* sB = sA + C::A_BYTES;
+#ifdef LORA_PROBE_NO_REFILL
+                    // timing experiment only: after the first fill the MMAs re-read stale tiles
+                    if (tl > 0 || kb >= C::STAGES) {
+                        if (leader) mbar_arrive(&full[stage]);
+                        if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+                        continue;
+                    }
+#endif
                     if (leader) mbar_arrive_expect_tx(&full[stage], CG * stage_tx);
                     const int k0 = kb * BK;
                     tma_load<CG>(sA, &tm_act, k0, t0, &full[stage]);
@@ -534,6 +546,11 @@ lora_fused_gemm_kernel(const __grid_constant__ CUtensorMap tm_act,   // x or dY 
 
     tc_fence_before();
     if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+#ifdef LORA_PROBE_CLOCK
+    if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1))
+        printf("PROBE_CLOCK mode=%d block=%d cycles=%lld ns=%llu\n", MODE, blockIdx.x, clock64() - probe_c0,
+               (unsigned long long)(globaltimer_ns() - probe_t0));
+#endif
     if (warp == 2) {
         tc_fence_after();
         tmem_dealloc_cg<CG>(tmem_base);

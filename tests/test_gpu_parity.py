@@ -91,6 +91,19 @@ def test_cfg2_full_size_sampled_rows(oracle_mod, L):
     print("cfg2 relF", errs)
 
 
+@pytest.mark.parametrize("shape", [(4096, 4096, 11008, 16), (4096, 11008, 4096, 16), (4096, 5120, 13824, 8),
+                                   (4096, 8192, 1024, 16)])
+def test_layer_set_shapes_sampled_rows(oracle_mod, L, shape):
+    """BASELINE.json configs[2..4] projection shapes (7B gate/up and down,
+    13B MLP, 70B GQA k/v) at T = 4096: y, dX on sampled rows, dA, dB in full."""
+    T, n, m, r = shape
+    d = make_lora_inputs(T, n, m, r, seed=300 + r)
+    rng = np.random.default_rng(11)
+    rows = np.unique(np.concatenate([[0, T - 1], rng.choice(T, 24, replace=False)]))
+    _, errs = _check_against_oracle(oracle_mod, L, d, 16.0, rows=rows)
+    print(shape, "relF", errs)
+
+
 # ------------------------------------------------------------------ exact pins
 def test_worked_example_embedded_bit_exact(oracle_mod, L):
     """tests/golden/worked_example.json (SPEC.md:324 extended), zero-padded to

@@ -70,7 +70,10 @@ def time_one(T=2048, n=4096, m=4096, r=8, iters=50):
                                                               want_da=False, db=db)),
                      # references for a 16 MiB read of dY on this box / in this harness
                      ("torch_sum_dy", lambda: torch.sum(dy, dtype=torch.float32)),
-                     ("torch_copy_dy", lambda: dx.copy_(dy))):
+                     ("torch_copy_dy", lambda: dx.copy_(dy)),
+                     # cuBLAS on the same base GEMM shapes (context for the GEMM efficiency)
+                     ("cublas_fwd_base", lambda: torch.matmul(x, w0.t(), out=y)),
+                     ("cublas_dx_base", lambda: torch.matmul(dy, w0, out=dx))):
         for _ in range(5):
             fn()
         ts = []
