@@ -252,10 +252,44 @@ def run_ours(args, wl):
         e["ws_b"] = torch.empty(max(256, int(L.lib.lora_tp_linear_bwd_workspace_bytes(ctypes.byref(dd)))),
                                 dtype=torch.uint8, device=dev)
         lin.append(e)
-    # LoRA-gradient bucket: the partial (sharded-side) grads of every linear, one all-reduce
     launches = {"n": 0}
 
+    # N = 1: the linears that share an input in the model (q,k,v / gate,up) run as
+    # one grouped call (one persistent launch per fused GEMM)
+    use_groups = comm is None and not args.no_group
+    groups = []
+    if use_groups:
+        for gidx in wl.groups:
+            members = [lin[i] for i in gidx]
+            ds = (L.lora_dims * len(members))(*[L.dims(e["l"].T, e["spec"].local_n, e["spec"].local_m, e["l"].r,
+                                                       e["l"].alpha) for e in members])
+            wsf = torch.empty(max(256, int(L.lib.lora_linear_fwd_grouped_workspace_bytes(len(members), ds))),
+                              dtype=torch.uint8, device=dev)
+            wsb = torch.empty(max(256, int(L.lib.lora_linear_bwd_grouped_workspace_bytes(len(members), ds))),
+                              dtype=torch.uint8, device=dev)
+            groups.append((members, wsf, wsb))
+
+    def step_grouped(ev=None):
+        cur = torch.cuda.current_stream()
+        for gi, (members, wsf, _) in enumerate(groups):
+            if ev is not None and gi == 0:
+                ev["f0"].record(stream)
+            L.lora_linear_fwd_grouped([(e["x"], e["w0"], e["a"], e["b"], None) for e in members],
+                                      [e["l"].alpha for e in members], outs=[(e["y"], e["h"]) for e in members],
+                                      workspace=wsf, stream=cur)
+            launches["n"] += L.lora_last_launch_count()
+            if ev is not None and gi == 0:
+                ev["f1"].record(stream)
+        for members, _, wsb in groups:
+            L.lora_linear_bwd_grouped([(e["x"], e["w0"], e["a"], e["b"], e["dy"], e["h"]) for e in members],
+                                      [e["l"].alpha for e in members],
+                                      outs=[(e["dx"], e["da"], e["db"]) for e in members], workspace=wsb,
+                                      stream=cur)
+            launches["n"] += L.lora_last_launch_count()
+
     def step(ev=None):
+        if use_groups:
+            return step_grouped(ev)
         for e in lin:
             if ev is not None and e is lin[0]:
                 ev["f0"].record(stream)
@@ -338,12 +372,13 @@ def run_ours(args, wl):
             if graph is not None:
                 graph.replay()
             else:
-                step(fev[i])
+                step(None if use_groups else fev[i])
             ev1[i].record(stream)
         barrier()
     step_ms = [ev0[i].elapsed_time(ev1[i]) for i in range(K)]
-    if graph is not None:
-        launches["n"] = per_step_launches * K
+    if graph is not None or use_groups:
+        if graph is not None:
+            launches["n"] = per_step_launches * K
         # time the first linear's forward call on its own (same flush discipline)
         e = lin[0]
         for i in range(K):
@@ -428,6 +463,7 @@ def run_ours(args, wl):
                        "global_batch": 1, "seq_len": tokens,
                        "parallelism": f"tp{world}" if world > 1 else "single",
                        "cuda_graph": graph is not None,
+                       "grouped_calls": [[wl.linears[i].name for i in g] for g in wl.groups] if use_groups else None,
                        "l2": "flushed between timed steps (2xL2 write then 2xL2 read, outside the "
                              "event pairs)"},
             "tokens_per_s": tokens * K / (total_ms * 1e-3),
@@ -461,6 +497,8 @@ def main():
     ap.add_argument("--config", default="cfg2", choices=sorted(WORKLOADS))
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-group", action="store_true",
+                    help="one call per linear instead of grouped calls for linears sharing an input")
     ap.add_argument("--graph", choices=["auto", "on", "off"], default="auto",
                     help="replay each step as one CUDA graph (auto: at N = 1)")
     args = ap.parse_args()

@@ -112,6 +112,31 @@ lora_status lora_linear_bwd(const lora_dims* dims, const void* x, const void* w0
 lora_status lora_merge(const lora_dims* dims, const void* w0, const void* a,
                        const void* b, void* w_out, void* stream);
 
+/* ---------------- Grouped calls: several independent LoRA linears ----------
+ * Equivalent to `count` single calls (bitwise identical results), but the
+ * fused tensor-core GEMMs of all problems whose rank falls in the same
+ * 16/32/64 bucket (and with the same T > 128 or not) run as ONE persistent
+ * launch, which removes per-launch prologue / tail time.  Typical use: the
+ * projections that share an input (q, k, v; gate, up).  Problems must not
+ * alias each other's outputs.  Workspace: the *_grouped_workspace_bytes()
+ * of the same dims array (problem g uses its own slice). */
+#define LORA_MAX_GROUP 8
+typedef struct {
+    const void* x; const void* w0; const void* a; const void* b; const void* bias;  /* as lora_linear_fwd */
+    void* y; float* h_out;
+} lora_fwd_problem;
+typedef struct {
+    const void* x; const void* w0; const void* a; const void* b; const float* h_saved;  /* as lora_linear_bwd */
+    const void* dy; void* dx; float* da; float* db;
+} lora_bwd_problem;
+
+size_t lora_linear_fwd_grouped_workspace_bytes(int count, const lora_dims* dims);
+lora_status lora_linear_fwd_grouped(int count, const lora_dims* dims, const lora_fwd_problem* problems,
+                                    void* workspace, size_t workspace_bytes, void* stream);
+size_t lora_linear_bwd_grouped_workspace_bytes(int count, const lora_dims* dims);
+lora_status lora_linear_bwd_grouped(int count, const lora_dims* dims, const lora_bwd_problem* problems,
+                                    int accumulate, void* workspace, size_t workspace_bytes, void* stream);
+
 const char* lora_status_string(lora_status status);
 const char* lora_last_error(void);
 

@@ -43,6 +43,18 @@ class lora_dims(ctypes.Structure):
                 ("rank", ctypes.c_int32), ("alpha", ctypes.c_float)]
 
 
+class lora_fwd_problem(ctypes.Structure):
+    _fields_ = [("x", ctypes.c_void_p), ("w0", ctypes.c_void_p), ("a", ctypes.c_void_p), ("b", ctypes.c_void_p),
+                ("bias", ctypes.c_void_p), ("y", ctypes.c_void_p), ("h_out", ctypes.c_void_p)]
+
+
+class lora_bwd_problem(ctypes.Structure):
+    _fields_ = [("x", ctypes.c_void_p), ("w0", ctypes.c_void_p), ("a", ctypes.c_void_p), ("b", ctypes.c_void_p),
+                ("h_saved", ctypes.c_void_p), ("dy", ctypes.c_void_p), ("dx", ctypes.c_void_p),
+                ("da", ctypes.c_void_p), ("db", ctypes.c_void_p)]
+
+
+LORA_MAX_GROUP = 8
 _vp = ctypes.c_void_p
 _fp = ctypes.c_void_p  # float* passed as raw address
 _dp = ctypes.POINTER(lora_dims)
@@ -57,6 +69,16 @@ lib.lora_linear_fwd.restype = _st
 lib.lora_linear_bwd.argtypes = [_dp, _vp, _vp, _vp, _vp, _fp, _vp, _vp, _fp, _fp, ctypes.c_int,
                                 _vp, ctypes.c_size_t, _vp]
 lib.lora_linear_bwd.restype = _st
+lib.lora_linear_fwd_grouped_workspace_bytes.argtypes = [ctypes.c_int, _dp]
+lib.lora_linear_fwd_grouped_workspace_bytes.restype = ctypes.c_size_t
+lib.lora_linear_bwd_grouped_workspace_bytes.argtypes = [ctypes.c_int, _dp]
+lib.lora_linear_bwd_grouped_workspace_bytes.restype = ctypes.c_size_t
+lib.lora_linear_fwd_grouped.argtypes = [ctypes.c_int, _dp, ctypes.POINTER(lora_fwd_problem), _vp, ctypes.c_size_t,
+                                        _vp]
+lib.lora_linear_fwd_grouped.restype = _st
+lib.lora_linear_bwd_grouped.argtypes = [ctypes.c_int, _dp, ctypes.POINTER(lora_bwd_problem), ctypes.c_int, _vp,
+                                        ctypes.c_size_t, _vp]
+lib.lora_linear_bwd_grouped.restype = _st
 lib.lora_merge.argtypes = [_dp, _vp, _vp, _vp, _vp, _vp]
 lib.lora_merge.restype = _st
 lib.lora_status_string.argtypes = [_st]
@@ -242,3 +264,65 @@ def lora_merge(w0, a, b, alpha, w_out=None, stream=None):
     st = lib.lora_merge(ctypes.byref(d), _ptr(w0), _ptr(a), _ptr(b), _ptr(w_out), _stream(stream))
     _check(st, "lora_merge")
     return w_out
+
+
+def lora_linear_fwd_grouped(problems, alphas, outs=None, workspace=None, stream=None):
+    """Grouped forward (one persistent launch for the fused GEMMs).
+
+    problems: list of (x, w0, a, b, bias_or_None); alphas: list of floats;
+    outs: optional list of (y, h_out).  Returns the list of (y, h)."""
+    G = len(problems)
+    if not 1 <= G <= LORA_MAX_GROUP:
+        raise ValueError(f"1 <= len(problems) <= {LORA_MAX_GROUP}")
+    dims_arr = (lora_dims * G)()
+    probs = (lora_fwd_problem * G)()
+    res = []
+    for g, (x, w0, a, b, bias) in enumerate(problems):
+        T, n = x.shape
+        m, r = b.shape
+        _bf16(x, "x", (T, n)); _bf16(w0, "w0", (m, n)); _bf16(a, "a", (r, n)); _bf16(b, "b", (m, r))
+        y, h = outs[g] if outs is not None else (None, None)
+        if y is None:
+            y = torch.empty((T, m), dtype=torch.bfloat16, device=x.device)
+        if h is None:
+            h = torch.empty((T, r), dtype=torch.float32, device=x.device)
+        dims_arr[g] = dims(T, n, m, r, alphas[g])
+        probs[g] = lora_fwd_problem(_ptr(x), _ptr(w0), _ptr(a), _ptr(b), _ptr(bias), _ptr(y), _ptr(h))
+        res.append((y, h))
+    need = int(lib.lora_linear_fwd_grouped_workspace_bytes(G, dims_arr))
+    ws = workspace if workspace is not None else _workspace(need, problems[0][0].device)
+    _check(lib.lora_linear_fwd_grouped(G, dims_arr, probs, _ptr(ws), ws.numel(), _stream(stream)),
+           "lora_linear_fwd_grouped")
+    return res
+
+
+def lora_linear_bwd_grouped(problems, alphas, outs=None, accumulate=False, workspace=None, stream=None):
+    """Grouped backward.  problems: list of (x, w0, a, b, dy, h_saved_or_None);
+    outs: optional list of (dx, da, db).  Returns the list of (dx, da, db)."""
+    G = len(problems)
+    if not 1 <= G <= LORA_MAX_GROUP:
+        raise ValueError(f"1 <= len(problems) <= {LORA_MAX_GROUP}")
+    dims_arr = (lora_dims * G)()
+    probs = (lora_bwd_problem * G)()
+    res = []
+    for g, (x, w0, a, b, dy, h) in enumerate(problems):
+        T, n = x.shape
+        m, r = b.shape
+        _bf16(x, "x", (T, n)); _bf16(w0, "w0", (m, n)); _bf16(a, "a", (r, n)); _bf16(b, "b", (m, r))
+        _bf16(dy, "dy", (T, m))
+        dx, da, db = outs[g] if outs is not None else (None, None, None)
+        if dx is None:
+            dx = torch.empty((T, n), dtype=torch.bfloat16, device=x.device)
+        if da is None:
+            da = torch.zeros((r, n), dtype=torch.float32, device=x.device)
+        if db is None:
+            db = torch.zeros((m, r), dtype=torch.float32, device=x.device)
+        dims_arr[g] = dims(T, n, m, r, alphas[g])
+        probs[g] = lora_bwd_problem(_ptr(x), _ptr(w0), _ptr(a), _ptr(b), _ptr(h), _ptr(dy), _ptr(dx), _ptr(da),
+                                    _ptr(db))
+        res.append((dx, da, db))
+    need = int(lib.lora_linear_bwd_grouped_workspace_bytes(G, dims_arr))
+    ws = workspace if workspace is not None else _workspace(need, problems[0][0].device)
+    _check(lib.lora_linear_bwd_grouped(G, dims_arr, probs, 1 if accumulate else 0, _ptr(ws), ws.numel(),
+                                       _stream(stream)), "lora_linear_bwd_grouped")
+    return res

@@ -202,10 +202,12 @@ static uint64_t next_epoch() {
     return base + 2 * counter.fetch_add(1);
 }
 
+static lora_status collect(GemmCollector* col, const FusedGemmMaps& maps, const FusedGemmParams& p, int rp, int cg);
+
 // ------------------------------------------------------------ forward
 lora_status fwd_impl(const lora_dims* d, const void* x, const void* w0, const void* a, const void* b,
                      const void* bias, void* y, float* h_out, void* ws, size_t ws_bytes,
-                     cudaStream_t stream, int* launches) {
+                     cudaStream_t stream, int* launches, GemmCollector* col) {
     lora_status st = check_dims(d, true);
     if (st != LORA_OK) return st;
     const int64_t T = d->tokens, n = d->d_in, m = d->d_out;
@@ -266,16 +268,52 @@ lora_status fwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
     p.gh = nullptr;
     p.flags = nullptr;
     p.epoch = 0;
+    if (col) return collect(col, maps, p, rp, cg);
     cudaError_t e = launch_fused_gemm(kModeFwd, rp, cg, maps, p, dev.sms, stream);
     if (e != cudaSuccess) return cuda_fail(e, "fused forward launch");
     ++*launches;
     return LORA_OK;
 }
 
+static lora_status collect(GemmCollector* col, const FusedGemmMaps& maps, const FusedGemmParams& p, int rp, int cg) {
+    if (col->count >= kMaxGroup) return fail(LORA_ERR_UNSUPPORTED, "more than %d grouped problems", kMaxGroup);
+    col->maps[col->count] = maps;
+    col->p[col->count] = p;
+    col->rp[col->count] = rp;
+    col->cg[col->count] = cg;
+    ++col->count;
+    return LORA_OK;
+}
+
+lora_status launch_collected(int mode, GemmCollector& col, cudaStream_t stream, int* launches) {
+    if (col.count == 0) return LORA_OK;
+    DevInfo dev;
+    lora_status st = device_info(&dev);
+    if (st != LORA_OK) return st;
+    static thread_local FusedGemmGroup grp;
+    bool done[kMaxGroup] = {};
+    for (int i = 0; i < col.count; ++i) {
+        if (done[i]) continue;
+        grp.count = 0;
+        for (int j = i; j < col.count; ++j) {
+            if (done[j] || col.rp[j] != col.rp[i] || col.cg[j] != col.cg[i]) continue;
+            grp.maps[grp.count] = col.maps[j];
+            grp.p[grp.count] = col.p[j];
+            ++grp.count;
+            done[j] = true;
+        }
+        cudaError_t e = launch_fused_gemm_group(mode, col.rp[i], col.cg[i], grp, dev.sms, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "grouped fused GEMM launch");
+        ++*launches;
+    }
+    return LORA_OK;
+}
+
 // ------------------------------------------------------------ backward
 lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const void* a, const void* b,
                      const float* h_saved, const void* dy, void* dx, float* da, float* db, int accumulate,
-                     void* ws, size_t ws_bytes, cudaStream_t stream, int* launches) {
+                     void* ws, size_t ws_bytes, cudaStream_t stream, int* launches, GemmCollector* col,
+                     int stages) {
     lora_status st = check_dims(d, true);
     if (st != LORA_OK) return st;
     const int64_t T = d->tokens, n = d->d_in, m = d->d_out;
@@ -311,7 +349,7 @@ lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
     if ((st = device_info(&dev)) != LORA_OK) return st;
     cudaError_t e;
     if (T == 0) {
-        if (!accumulate) {
+        if (!accumulate && (stages & 1)) {
             if ((e = launch_fill_zero(da, int64_t(r) * n, stream)) != cudaSuccess) return cuda_fail(e, "memset dA");
             if ((e = launch_fill_zero(db, int64_t(m) * r, stream)) != cudaSuccess) return cuda_fail(e, "memset dB");
         }
@@ -329,7 +367,7 @@ lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
     const bool need_gh = dx || da;
     const bool need_h = db && !h_saved;
 
-    if (dx) {
+    if (dx && (stages & 1)) {
         // K2 computes gh = s dY B itself (first column tile of each row block)
         const __nv_bfloat16* bsrc = static_cast<const __nv_bfloat16*>(b);
         if (r != r8) {   // B rows of 2r bytes are not TMA-legal: B6 pads them to r8
@@ -355,10 +393,16 @@ lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
         p.gh = gh;
         p.flags = reinterpret_cast<uint64_t*>(wsb + W.flags);
         p.epoch = next_epoch();
-        if ((e = launch_fused_gemm(kModeDx, rp, cg, maps, p, dev.sms, stream)) != cudaSuccess)
-            return cuda_fail(e, "fused dX launch");
-        ++*launches;
-    } else if (da) {
+        if (col) {
+            if ((st = collect(col, maps, p, rp, cg)) != LORA_OK) return st;
+        } else {
+            if ((e = launch_fused_gemm(kModeDx, rp, cg, maps, p, dev.sms, stream)) != cudaSuccess)
+                return cuda_fail(e, "fused dX launch");
+            ++*launches;
+        }
+    }
+    if (!(stages & 2)) return LORA_OK;
+    if (!dx && da) {
         // K2a: gh = s dY B [T, r] fp32 for dA when the input gradient is not requested
         if ((e = launch_gh(dya, static_cast<const __nv_bfloat16*>(b), T, m, r, s, gh, stream)) != cudaSuccess)
             return cuda_fail(e, "gh launch");
@@ -464,6 +508,95 @@ lora_status lora_merge(const lora_dims* dims, const void* w0, const void* a, con
     lora_status st = merge_impl(dims, w0, a, b, w_out, static_cast<cudaStream_t>(stream), &launches);
     set_launches(launches);
     return st;
+}
+
+// ---------------------------------------------------------------- grouped
+static size_t ws_align(size_t v) { return (v + 255) & ~size_t(255); }
+
+static lora_status check_group(int count, const lora_dims* dims, const void* probs, const char* fn) {
+    if (count < 1 || count > LORA_MAX_GROUP)
+        return fail(LORA_ERR_INVALID, "%s: count = %d must be in [1, %d]", fn, count, LORA_MAX_GROUP);
+    if (!dims || !probs) return fail(LORA_ERR_INVALID, "%s: dims / problems is NULL", fn);
+    return LORA_OK;
+}
+
+size_t lora_linear_fwd_grouped_workspace_bytes(int count, const lora_dims* dims) {
+    if (count < 1 || count > LORA_MAX_GROUP || !dims) return 0;
+    size_t total = 0;
+    for (int g = 0; g < count; ++g) {
+        const size_t w = fwd_workspace(&dims[g]);
+        if (!w) return 0;
+        total += ws_align(w);
+    }
+    return total;
+}
+
+size_t lora_linear_bwd_grouped_workspace_bytes(int count, const lora_dims* dims) {
+    if (count < 1 || count > LORA_MAX_GROUP || !dims) return 0;
+    size_t total = 0;
+    for (int g = 0; g < count; ++g) {
+        const size_t w = bwd_workspace(&dims[g]);
+        if (!w) return 0;
+        total += ws_align(w);
+    }
+    return total;
+}
+
+lora_status lora_linear_fwd_grouped(int count, const lora_dims* dims, const lora_fwd_problem* probs,
+                                    void* workspace, size_t workspace_bytes, void* stream) {
+    int launches = 0;
+    lora_status st = check_group(count, dims, probs, "lora_linear_fwd_grouped");
+    if (st != LORA_OK) return st;
+    const size_t need = lora_linear_fwd_grouped_workspace_bytes(count, dims);
+    if (!need) return fail(LORA_ERR_SHAPE, "lora_linear_fwd_grouped: invalid dims");
+    if (!workspace || workspace_bytes < need)
+        return fail(LORA_ERR_WORKSPACE, "lora_linear_fwd_grouped: workspace %zu < required %zu", workspace_bytes,
+                    need);
+    cudaStream_t st_ = static_cast<cudaStream_t>(stream);
+    GemmCollector col;
+    size_t off = 0;
+    for (int g = 0; g < count; ++g) {
+        const lora_fwd_problem& pr = probs[g];
+        const size_t wg = ws_align(fwd_workspace(&dims[g]));
+        st = fwd_impl(&dims[g], pr.x, pr.w0, pr.a, pr.b, pr.bias, pr.y, pr.h_out,
+                      static_cast<uint8_t*>(workspace) + off, wg, st_, &launches, &col);
+        if (st != LORA_OK) { set_launches(launches); return st; }
+        off += wg;
+    }
+    st = launch_collected(kModeFwd, col, st_, &launches);
+    set_launches(launches);
+    return st;
+}
+
+lora_status lora_linear_bwd_grouped(int count, const lora_dims* dims, const lora_bwd_problem* probs, int accumulate,
+                                    void* workspace, size_t workspace_bytes, void* stream) {
+    int launches = 0;
+    lora_status st = check_group(count, dims, probs, "lora_linear_bwd_grouped");
+    if (st != LORA_OK) return st;
+    const size_t need = lora_linear_bwd_grouped_workspace_bytes(count, dims);
+    if (!need) return fail(LORA_ERR_SHAPE, "lora_linear_bwd_grouped: invalid dims");
+    if (!workspace || workspace_bytes < need)
+        return fail(LORA_ERR_WORKSPACE, "lora_linear_bwd_grouped: workspace %zu < required %zu", workspace_bytes,
+                    need);
+    cudaStream_t st_ = static_cast<cudaStream_t>(stream);
+    GemmCollector col;
+    for (int stage = 1; stage <= 2; ++stage) {
+        size_t off = 0;
+        for (int g = 0; g < count; ++g) {
+            const lora_bwd_problem& pr = probs[g];
+            const size_t wg = ws_align(bwd_workspace(&dims[g]));
+            st = bwd_impl(&dims[g], pr.x, pr.w0, pr.a, pr.b, pr.h_saved, pr.dy, pr.dx, pr.da, pr.db, accumulate,
+                          static_cast<uint8_t*>(workspace) + off, wg, st_, &launches, &col, stage);
+            if (st != LORA_OK) { set_launches(launches); return st; }
+            off += wg;
+        }
+        if (stage == 1 && (st = launch_collected(kModeDx, col, st_, &launches)) != LORA_OK) {
+            set_launches(launches);
+            return st;
+        }
+    }
+    set_launches(launches);
+    return LORA_OK;
 }
 
 const char* lora_status_string(lora_status s) {

@@ -194,14 +194,32 @@ __device__ __forceinline__ void st_release_u64(uint64_t* p, uint64_t v) {
     asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// Tile `tile` of a group -> (problem g, row block, column block, k-blocks).
+struct TileRef {
+    int g, t_blk, n_blk, num_k_blks;
+};
+template <int TM>
+__device__ __forceinline__ TileRef decode_tile(const FusedGemmGroup& grp, int tile) {
+    int g = 0;
+    while (g + 1 < grp.count && tile >= grp.tile_start[g + 1]) ++g;
+    const FusedGemmParams& p = grp.p[g];
+    const int local = tile - grp.tile_start[g];
+    const int num_t_blks = static_cast<int>((p.T + TM - 1) / TM);
+    TileRef t;
+    t.g = g;
+    t.n_blk = local / num_t_blks;
+    t.t_blk = local - t.n_blk * num_t_blks;
+    t.num_k_blks = static_cast<int>((p.K + BK - 1) / BK);
+    return t;
+}
+
+// Maps per problem g (grp.maps[g]):
+//   act  x or dY [T, K]          w   W0 [m, n] (fwd CG=2: 128-row box)
+//   w2   fwd CG=2: W0 box of BN-128 rows
+//   nar  fwd: A [r,n]; dx: B [m,r8]          tail  fwd: B [m,r8]; dx: A [r,n]
 template <int MODE, int R_PAD, int CG>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
-lora_fused_gemm_kernel(const __grid_constant__ CUtensorMap tm_act,   // x or dY   [T, K]
-                       const __grid_constant__ CUtensorMap tm_w,     // W0 [m, n] (fwd CG=2: 128-row box)
-                       const __grid_constant__ CUtensorMap tm_w2,    // fwd CG=2: W0 box of BN-128 rows
-                       const __grid_constant__ CUtensorMap tm_nar,   // fwd: A [r,n]; dx: B [m,r8]
-                       const __grid_constant__ CUtensorMap tm_tail,  // fwd: B [m,r8]; dx: A [r,n]
-                       const FusedGemmParams p) {
+lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
     using C = GemmCfg<MODE, R_PAD, CG>;
     using Cols = ColTiles<MODE, C::BN>;
     constexpr int BN = C::BN;
@@ -228,19 +246,17 @@ lora_fused_gemm_kernel(const __grid_constant__ CUtensorMap tm_act,   // x or dY 
     const bool leader = crank == 0;
     const int pair = static_cast<int>(blockIdx.x) / CG;
     const int npairs = static_cast<int>(gridDim.x) / CG;
-    const int num_t_blks = static_cast<int>((p.T + TM - 1) / TM);
-    const int num_n_blks = Cols::count(p.N_out);
-    const int num_tiles = num_t_blks * num_n_blks;
-    const int num_k_blks = static_cast<int>((p.K + BK - 1) / BK);
+    const int num_tiles = grp.tile_start[grp.count];
     const uint32_t warp = warp_id();
     const uint32_t lane = lane_id();
 
-    if (warp == 0 && lane == 0) {
-        tma_prefetch_desc(&tm_act);
-        tma_prefetch_desc(&tm_w);
-        if (MODE == kModeFwd && CG == 2) tma_prefetch_desc(&tm_w2);
-        tma_prefetch_desc(&tm_nar);
-        tma_prefetch_desc(&tm_tail);
+    if (warp == 0 && lane < static_cast<uint32_t>(grp.count)) {
+        const FusedGemmMaps& mp = grp.maps[lane];
+        tma_prefetch_desc(&mp.act);
+        tma_prefetch_desc(&mp.w);
+        if (MODE == kModeFwd && CG == 2) tma_prefetch_desc(&mp.w2);
+        tma_prefetch_desc(&mp.nar);
+        tma_prefetch_desc(&mp.tail);
     }
     if (warp == 1 && lane == 0) {
         for (int s = 0; s < C::STAGES; ++s) {
@@ -278,8 +294,11 @@ lora_fused_gemm_kernel(const __grid_constant__ CUtensorMap tm_act,   // x or dY 
             const uint64_t pol_w = l2_policy_evict_last();
             uint32_t stage = 0, phase = 0, tl = 0;
             for (int tile = pair; tile < num_tiles; tile += npairs, ++tl) {
-                const int n_blk = tile / num_t_blks;
-                const int t_blk = tile - n_blk * num_t_blks;
+                const TileRef tr = decode_tile<TM>(grp, tile);
+                const FusedGemmMaps& mp = grp.maps[tr.g];
+                const int n_blk = tr.n_blk;
+                const int t_blk = tr.t_blk;
+                const int num_k_blks = tr.num_k_blks;
                 const int t0 = t_blk * TM + static_cast<int>(crank) * BM;
                 const int n0 = Cols::start(n_blk);
                 const int wh = Cols::width(n_blk) / CG;                 // this CTA's B-operand columns
@@ -303,22 +322,22 @@ lora_fused_gemm_kernel(const __grid_constant__ CUtensorMap tm_act,   // x or dY 
 #endif
                     if (leader) mbar_arrive_expect_tx(&full[stage], CG * stage_tx);
                     const int k0 = kb * BK;
-                    tma_load<CG>(sA, &tm_act, k0, t0, &full[stage]);
+                    tma_load<CG>(sA, &mp.act, k0, t0, &full[stage]);
                     if constexpr (MODE == kModeFwd) {
                         if (CG == 1) {
-                            tma_load_2d_hint(sB, &tm_w, k0, n0, &full[stage], pol_w);       // W0 rows
-                            tma_load<CG>(sB + BN * 128, &tm_nar, k0, 0, &full[stage]);        // A rows
+                            tma_load_2d_hint(sB, &mp.w, k0, n0, &full[stage], pol_w);       // W0 rows
+                            tma_load<CG>(sB + BN * 128, &mp.nar, k0, 0, &full[stage]);        // A rows
                         } else if (crank == 0) {
-                            tma_load<CG>(sB, &tm_w, k0, n0, &full[stage]);                    // W0 rows 0..127
+                            tma_load<CG>(sB, &mp.w, k0, n0, &full[stage]);                    // W0 rows 0..127
                         } else {
-                            tma_load<CG>(sB, &tm_w2, k0, n0 + 128, &full[stage]);             // W0 rows 128..BN-1
-                            tma_load<CG>(sB + (BN - 128) * 128, &tm_nar, k0, 0, &full[stage]); // A rows
+                            tma_load<CG>(sB, &mp.w2, k0, n0 + 128, &full[stage]);             // W0 rows 128..BN-1
+                            tma_load<CG>(sB + (BN - 128) * 128, &mp.nar, k0, 0, &full[stage]); // A rows
                         }
                     } else {
                         for (int j = 0; j < nb; ++j)
-                            tma_load<CG>(sB + j * (64 * 128), &tm_w, nh0 + 64 * j, k0, &full[stage]);
+                            tma_load<CG>(sB + j * (64 * 128), &mp.w, nh0 + 64 * j, k0, &full[stage]);
                         if (gh_tile)   // B rows k0..k0+63, this CTA's NAR_H columns
-                            tma_load<CG>(sB + C::B_BYTES, &tm_nar, static_cast<int>(crank) * C::NAR_H, k0,
+                            tma_load<CG>(sB + C::B_BYTES, &mp.nar, static_cast<int>(crank) * C::NAR_H, k0,
                                          &full[stage]);
                     }
                     if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
@@ -327,11 +346,11 @@ lora_fused_gemm_kernel(const __grid_constant__ CUtensorMap tm_act,   // x or dY 
                 mbar_wait(tailop_empty, (tl & 1) ^ 1);
                 if constexpr (MODE == kModeFwd) {
                     if (leader) mbar_arrive_expect_tx(tailop_full, CG * C::TAILB_BYTES);
-                    tma_load<CG>(s_tailb, &tm_tail, 0, nh0, tailop_full);
+                    tma_load<CG>(s_tailb, &mp.tail, 0, nh0, tailop_full);
                 } else {
                     if (leader) mbar_arrive_expect_tx(tailop_full, CG * nb * R_PAD * 128);
                     for (int j = 0; j < nb; ++j)
-                        tma_load<CG>(s_tailb + j * (R_PAD * 128), &tm_tail, nh0 + 64 * j, 0, tailop_full);
+                        tma_load<CG>(s_tailb + j * (R_PAD * 128), &mp.tail, nh0 + 64 * j, 0, tailop_full);
                 }
             }
         }
@@ -344,7 +363,9 @@ lora_fused_gemm_kernel(const __grid_constant__ CUtensorMap tm_act,   // x or dY 
             constexpr uint32_t idesc_nar = make_idesc_bf16(TM, C::NAR > 0 ? C::NAR : 16, 0, 1);
             uint32_t stage = 0, phase = 0, tl = 0;
             for (int tile = pair; tile < num_tiles; tile += npairs, ++tl) {
-                const int n_blk = tile / num_t_blks;
+                const TileRef tr = decode_tile<TM>(grp, tile);
+                const int n_blk = tr.n_blk;
+                const int num_k_blks = tr.num_k_blks;
                 const bool gh_tile = (MODE == kModeDx) && n_blk == 0;
                 const uint32_t idesc_main = (MODE == kModeFwd) ? idesc_fwd : (gh_tile ? idesc_dx_first : idesc_dx_full);
                 const uint32_t acc = tl & 1;
@@ -396,8 +417,10 @@ lora_fused_gemm_kernel(const __grid_constant__ CUtensorMap tm_act,   // x or dY 
         constexpr uint32_t tail_sbo = 8 * C::TAIL_ROW;
         uint32_t tl = 0;
         for (int tile = pair; tile < num_tiles; tile += npairs, ++tl) {
-            const int n_blk = tile / num_t_blks;
-            const int t_blk = tile - n_blk * num_t_blks;
+            const TileRef tr = decode_tile<TM>(grp, tile);
+            const FusedGemmParams& p = grp.p[tr.g];
+            const int n_blk = tr.n_blk;
+            const int t_blk = tr.t_blk;
             const int64_t row = static_cast<int64_t>(t_blk) * TM + crank * BM + row_local;
             const int n0 = Cols::start(n_blk);
             const int width = Cols::width(n_blk);
@@ -569,13 +592,19 @@ static int64_t col_tiles_host(int mode, int r_pad, int64_t n_out) {
 }
 
 template <int MODE, int R_PAD, int CG>
-static cudaError_t launch_impl(const FusedGemmMaps& maps, const FusedGemmParams& p, int num_sms,
-                               cudaStream_t stream) {
+static cudaError_t launch_impl(FusedGemmGroup& grp, int num_sms, cudaStream_t stream) {
     using C = GemmCfg<MODE, R_PAD, CG>;
     auto kern = lora_fused_gemm_kernel<MODE, R_PAD, CG>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
     if (e != cudaSuccess) return e;
-    const int64_t tiles = ((p.T + BM * CG - 1) / (BM * CG)) * col_tiles_host(MODE, R_PAD, p.N_out);
+    if (grp.count < 1 || grp.count > kMaxGroup) return cudaErrorInvalidValue;
+    int64_t tiles = 0;
+    for (int g = 0; g < grp.count; ++g) {
+        grp.tile_start[g] = static_cast<int>(tiles);
+        const FusedGemmParams& p = grp.p[g];
+        tiles += ((p.T + BM * CG - 1) / (BM * CG)) * col_tiles_host(MODE, R_PAD, p.N_out);
+    }
+    grp.tile_start[grp.count] = static_cast<int>(tiles);
     const int64_t units = num_sms / CG;
     const int grid = static_cast<int>((tiles < units ? tiles : units) * CG);
     if (grid <= 0) return cudaSuccess;
@@ -593,7 +622,7 @@ static cudaError_t launch_impl(const FusedGemmMaps& maps, const FusedGemmParams&
     attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
-    e = cudaLaunchKernelEx(&cfg, kern, maps.act, maps.w, maps.w2, maps.nar, maps.tail, p);
+    e = cudaLaunchKernelEx(&cfg, kern, grp);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
@@ -619,28 +648,36 @@ int fused_gemm_narrow_cols(int r_pad, int cta_group) {
 int64_t fused_gemm_row_blocks(int64_t T, int cta_group) { return (T + BM * cta_group - 1) / (BM * cta_group); }
 
 template <int CG>
-static cudaError_t dispatch(int mode, int r_pad, const FusedGemmMaps& maps, const FusedGemmParams& p, int num_sms,
-                           cudaStream_t stream) {
+static cudaError_t dispatch(int mode, int r_pad, FusedGemmGroup& grp, int num_sms, cudaStream_t stream) {
     if (mode == kModeFwd) {
         switch (r_pad) {
-            case 16: return launch_impl<kModeFwd, 16, CG>(maps, p, num_sms, stream);
-            case 32: return launch_impl<kModeFwd, 32, CG>(maps, p, num_sms, stream);
-            case 64: return launch_impl<kModeFwd, 64, CG>(maps, p, num_sms, stream);
+            case 16: return launch_impl<kModeFwd, 16, CG>(grp, num_sms, stream);
+            case 32: return launch_impl<kModeFwd, 32, CG>(grp, num_sms, stream);
+            case 64: return launch_impl<kModeFwd, 64, CG>(grp, num_sms, stream);
         }
     } else {
         switch (r_pad) {
-            case 16: return launch_impl<kModeDx, 16, CG>(maps, p, num_sms, stream);
-            case 32: return launch_impl<kModeDx, 32, CG>(maps, p, num_sms, stream);
-            case 64: return launch_impl<kModeDx, 64, CG>(maps, p, num_sms, stream);
+            case 16: return launch_impl<kModeDx, 16, CG>(grp, num_sms, stream);
+            case 32: return launch_impl<kModeDx, 32, CG>(grp, num_sms, stream);
+            case 64: return launch_impl<kModeDx, 64, CG>(grp, num_sms, stream);
         }
     }
     return cudaErrorInvalidValue;
 }
 
+cudaError_t launch_fused_gemm_group(int mode, int r_pad, int cta_group, FusedGemmGroup& grp, int num_sms,
+                                    cudaStream_t stream) {
+    return cta_group == 2 ? dispatch<2>(mode, r_pad, grp, num_sms, stream)
+                          : dispatch<1>(mode, r_pad, grp, num_sms, stream);
+}
+
 cudaError_t launch_fused_gemm(int mode, int r_pad, int cta_group, const FusedGemmMaps& maps,
                               const FusedGemmParams& p, int num_sms, cudaStream_t stream) {
-    return cta_group == 2 ? dispatch<2>(mode, r_pad, maps, p, num_sms, stream)
-                          : dispatch<1>(mode, r_pad, maps, p, num_sms, stream);
+    static thread_local FusedGemmGroup grp;   // ~6 KiB: keep it off the stack
+    grp.count = 1;
+    grp.maps[0] = maps;
+    grp.p[0] = p;
+    return launch_fused_gemm_group(mode, r_pad, cta_group, grp, num_sms, stream);
 }
 
 }  // namespace lora_sm100

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include "lora.h"
+#include "lora_kernels.h"
 
 namespace lora_host {
 
@@ -12,12 +13,27 @@ lora_status check_dims(const lora_dims* d, bool need_tokens);
 void set_launches(int n);
 int get_launches();
 
+// Fused-GEMM problems gathered by the grouped entry points (launched together).
+struct GemmCollector {
+    int count = 0;
+    lora_sm100::FusedGemmMaps maps[lora_sm100::kMaxGroup];
+    lora_sm100::FusedGemmParams p[lora_sm100::kMaxGroup];
+    int rp[lora_sm100::kMaxGroup];
+    int cg[lora_sm100::kMaxGroup];
+};
+
+// col != nullptr: the fused GEMM is appended to `col` instead of launched.
+// bwd stages: bit 0 = validation, pack, K2 (launch or collect);
+//             bit 1 = everything after K2 (gh pre-pass, h recompute, K3).
 lora_status fwd_impl(const lora_dims* d, const void* x, const void* w0, const void* a, const void* b,
                      const void* bias, void* y, float* h_out, void* ws, size_t ws_bytes,
-                     cudaStream_t stream, int* launches);
+                     cudaStream_t stream, int* launches, GemmCollector* col = nullptr);
 lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const void* a, const void* b,
                      const float* h_saved, const void* dy, void* dx, float* da, float* db, int accumulate,
-                     void* ws, size_t ws_bytes, cudaStream_t stream, int* launches);
+                     void* ws, size_t ws_bytes, cudaStream_t stream, int* launches,
+                     GemmCollector* col = nullptr, int stages = 3);
+// launch the collected problems, one grouped launch per (r_pad, CTA group) class
+lora_status launch_collected(int mode, GemmCollector& col, cudaStream_t stream, int* launches);
 size_t fwd_workspace(const lora_dims* d);
 size_t bwd_workspace(const lora_dims* d);
 

@@ -32,6 +32,16 @@ struct FusedGemmMaps {
     CUtensorMap act, w, w2, nar, tail;
 };
 
+// A group of independent LoRA linears (same rank bucket) processed by ONE
+// persistent launch: the tiles of problem g occupy [tile_start[g], tile_start[g+1]).
+constexpr int kMaxGroup = 8;
+struct FusedGemmGroup {
+    FusedGemmMaps maps[kMaxGroup];
+    FusedGemmParams p[kMaxGroup];
+    int tile_start[kMaxGroup + 1];
+    int count;
+};
+
 // K1 / K2.  r_pad in {16, 32, 64}; tiles are (128 * cta_group) x (256 - r_pad).
 // cta_group = 2 runs on CTA pairs (tcgen05 cta_group::2); the TMA boxes of
 // `maps` must match (see lora_api.cpp).
@@ -40,6 +50,9 @@ int fused_gemm_narrow_cols(int r_pad, int cta_group);     // dx: B columns per C
 int64_t fused_gemm_row_blocks(int64_t T, int cta_group);  // dx: flags needed = row blocks * cta_group
 cudaError_t launch_fused_gemm(int mode, int r_pad, int cta_group, const FusedGemmMaps& maps,
                               const FusedGemmParams& p, int num_sms, cudaStream_t stream);
+// grouped variant: `grp.count` problems, tile_start filled in by the launcher
+cudaError_t launch_fused_gemm_group(int mode, int r_pad, int cta_group, FusedGemmGroup& grp, int num_sms,
+                                    cudaStream_t stream);
 
 // B6: b8 [m, roundup(r, 8)] = B zero-padded (fwd, only when r % 8 != 0: TMA
 // row pitch must be a multiple of 16 bytes); bt [r, m] = B^T (dx narrow

@@ -59,12 +59,25 @@ class Workload:
     description: str
     linears: tuple
     tp_modes: tuple  # per linear: "column" | "row" (PAPER.md:122 reading, R10)
+    groups: tuple    # linears that take the same input in the model (q,k,v / gate,up / q,v)
 
 
 def _wl(key, desc, T, r, alpha, specs):
     lin = tuple(LoraShape(nm, T, n, m, r, alpha) for nm, n, m, _ in specs)
     modes = tuple(md for _, _, _, md in specs)
-    return Workload(key, desc, lin, modes)
+    names = [nm for nm, _, _, _ in specs]
+    shared = [("q", "k", "v"), ("gate", "up")]
+    groups, seen = [], set()
+    for i, nm in enumerate(names):
+        if i in seen:
+            continue
+        g = [i]
+        for s in shared:
+            if nm in s:
+                g = [j for j, nj in enumerate(names) if nj in s]
+        seen.update(g)
+        groups.append(tuple(g))
+    return Workload(key, desc, lin, modes, tuple(groups))
 
 
 # BASELINE.json "configs", in order.  alpha = 16 (Listing 3 default,

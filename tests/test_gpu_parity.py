@@ -262,6 +262,45 @@ def test_launch_counts(L):
     assert L.lora_last_launch_count() == 2          # B8 pack (r % 8 != 0) + K1
 
 
+# ------------------------------------------------------------------ grouped
+def test_grouped_equals_single_calls(L):
+    """lora_linear_{fwd,bwd}_grouped == the single calls, bitwise: same tiles,
+    same k-order, only launched together (mixed shapes, T and rank buckets,
+    including an r % 8 != 0 problem and one with bias)."""
+    specs = [(512, 384, 640, 8, False), (300, 256, 136, 8, True), (512, 512, 256, 24, False),
+             (128, 64, 72, 5, False)]
+    probs, singles = [], []
+    for i, (T, n, m, r, bias) in enumerate(specs):
+        d = make_lora_inputs(T, n, m, r, seed=70 + i, bias=bias)
+        t = {k: dev_bf16(d[k]) for k in ("x", "w0", "a", "b", "dy")}
+        t["bias"] = dev_bf16(d["bias"]) if bias else None
+        probs.append(t)
+        y, h = L.lora_linear_fwd(t["x"], t["w0"], t["a"], t["b"], 16.0, bias=t["bias"])
+        dx, da, db = L.lora_linear_bwd(t["x"], t["w0"], t["a"], t["b"], t["dy"], 16.0, h_saved=h)
+        singles.append((y, h, dx, da, db))
+    alphas = [16.0] * len(specs)
+    fo = L.lora_linear_fwd_grouped([(t["x"], t["w0"], t["a"], t["b"], t["bias"]) for t in probs], alphas)
+    bo = L.lora_linear_bwd_grouped([(t["x"], t["w0"], t["a"], t["b"], t["dy"], h) for t, (_, h) in zip(probs, fo)],
+                                   alphas)
+    torch.cuda.synchronize()
+    for (y, h, dx, da, db), (yg, hg), (dxg, dag, dbg) in zip(singles, fo, bo):
+        for u, v in ((y, yg), (h, hg), (dx, dxg), (da, dag), (db, dbg)):
+            assert torch.equal(u, v)
+
+
+def test_grouped_launch_count(L):
+    """Two same-bucket problems: one fused launch each for fwd and dX."""
+    ts = []
+    for i in range(2):
+        d = make_lora_inputs(512, 256, 256, 8, seed=80 + i)
+        ts.append({k: dev_bf16(d[k]) for k in ("x", "w0", "a", "b", "dy")})
+    fo = L.lora_linear_fwd_grouped([(t["x"], t["w0"], t["a"], t["b"], None) for t in ts], [16.0, 16.0])
+    assert L.lora_last_launch_count() == 1
+    L.lora_linear_bwd_grouped([(t["x"], t["w0"], t["a"], t["b"], t["dy"], h) for t, (_, h) in zip(ts, fo)],
+                              [16.0, 16.0])
+    assert L.lora_last_launch_count() == 3      # one grouped dX launch + K3 per problem
+
+
 # ------------------------------------------------------------------ merge
 @pytest.mark.parametrize("shape", [(64, 64, 4), (4096, 4096, 8), (1000, 520, 33)])
 def test_merge_matches_oracle(oracle_mod, L, shape):
