@@ -275,6 +275,24 @@ lora_status fwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
     return LORA_OK;
 }
 
+lora_status launch_collected_k3(GemmCollector& col, cudaStream_t stream, int* launches) {
+    static thread_local GradGroup G;
+    bool done[kMaxGroup] = {};
+    for (int i = 0; i < col.k3_count; ++i) {
+        if (done[i]) continue;
+        G.count = 0;
+        for (int j = i; j < col.k3_count; ++j) {
+            if (done[j] || grad_rank_bucket(col.k3[j].r) != grad_rank_bucket(col.k3[i].r)) continue;
+            G.g[G.count++] = col.k3[j];
+            done[j] = true;
+        }
+        cudaError_t e = launch_grad_reduce_cluster_group(G, stream, launches);
+        if (e != cudaSuccess) return cuda_fail(e, "grouped grad reduce launch");
+    }
+    col.k3_count = 0;
+    return LORA_OK;
+}
+
 static lora_status collect(GemmCollector* col, const FusedGemmMaps& maps, const FusedGemmParams& p, int rp, int cg) {
     if (col->count >= kMaxGroup) return fail(LORA_ERR_UNSUPPORTED, "more than %d grouped problems", kMaxGroup);
     col->maps[col->count] = maps;
@@ -418,6 +436,11 @@ lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
     if (da || db) {
         const char* k3 = getenv("LORA_K3");  // experiments: "tma" | "ldg"; default: cluster
         if (!k3 || (strcmp(k3, "tma") != 0 && strcmp(k3, "ldg") != 0)) {
+            if (col) {   // grouped backward: one K3 launch for the whole group
+                if (col->k3_count >= kMaxGroup) return fail(LORA_ERR_UNSUPPORTED, "too many grouped problems");
+                col->k3[col->k3_count++] = make_grad_args(T, n, m, r, s, xa, gh, dya, hsrc, da, db, accumulate);
+                return LORA_OK;
+            }
             e = launch_grad_reduce_cluster(T, n, m, r, s, xa, gh, dya, hsrc, da, db, accumulate, stream, launches);
         } else if (r % 4 == 0 && strcmp(k3, "tma") == 0) {
             // TMA-ring variant: coefficient rows (4r bytes) are TMA-legal when r % 4 == 0
@@ -595,8 +618,9 @@ lora_status lora_linear_bwd_grouped(int count, const lora_dims* dims, const lora
             return st;
         }
     }
+    st = launch_collected_k3(col, st_, &launches);
     set_launches(launches);
-    return LORA_OK;
+    return st;
 }
 
 const char* lora_status_string(lora_status s) {

@@ -234,19 +234,6 @@ cudaError_t launch_gh(const bf16* dy, const bf16* b, int64_t T, int64_t m, int r
 }
 
 // ------------------------------------------------------------------ K3
-struct GradArgs {
-    const bf16* x;     // [T, n]
-    const float* gh;   // [T, r]   (dA coefficients, already scaled by s)
-    const bf16* dy;    // [T, m]
-    const float* h;    // [T, r]   (dB coefficients, unscaled)
-    float* da;         // [r, n] or null
-    float* db;         // [m, r] or null
-    int64_t T, n, m;
-    int r;
-    int strips_a;      // CTAs [0, strips_a) own dA strips, the rest dB strips
-    float scale_b;     // s
-    int accumulate;
-};
 
 #ifndef LORA_K3_STRIP
 #define LORA_K3_STRIP 32
@@ -577,7 +564,13 @@ __device__ __forceinline__ void cp_async_vec(void* dst_smem, const void* src) {
 constexpr int kCS = 8;
 
 template <int RB, int CPT>
-__global__ void __launch_bounds__(256, (RB >= 64 ? 1 : 2)) grad_cluster_kernel(const GradArgs g, int blocks_a) {
+__global__ void __launch_bounds__(256, (RB >= 64 ? 1 : 2)) grad_cluster_kernel(const __grid_constant__ GradGroup G) {
+    // problem of this column block (grouped launch): blocks [block_start[p], block_start[p+1])
+    int prob = 0;
+    while (prob + 1 < G.count && static_cast<int>(blockIdx.x) >= G.block_start[prob + 1]) ++prob;
+    const GradArgs& g = G.g[prob];
+    const int blocks_a = G.blocks_a[prob];
+    const int local_block = static_cast<int>(blockIdx.x) - G.block_start[prob];
     constexpr int CB = 32 * CPT;                 // columns per CTA
     constexpr int D = 16;                        // row segments in flight per warp
     constexpr int CHUNK = 8192 / RB;             // staged coefficient rows (32 KiB)
@@ -594,11 +587,11 @@ __global__ void __launch_bounds__(256, (RB >= 64 ? 1 : 2)) grad_cluster_kernel(c
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int rank = static_cast<int>(cluster.block_rank());
-    const bool is_a = static_cast<int>(blockIdx.x) < blocks_a;
+    const bool is_a = local_block < blocks_a;
     const bf16* X = is_a ? g.x : g.dy;
     const float* coef = is_a ? g.gh : g.h;
     const int64_t ncols = is_a ? g.n : g.m;
-    const int64_t cb0 = static_cast<int64_t>(is_a ? blockIdx.x : blockIdx.x - blocks_a) * CB;
+    const int64_t cb0 = static_cast<int64_t>(is_a ? local_block : local_block - blocks_a) * CB;
     const int64_t c0 = cb0 + lane * CPT;
     const bool col_ok = c0 < ncols;
     const int r = g.r;
@@ -707,19 +700,26 @@ __global__ void __launch_bounds__(256, (RB >= 64 ? 1 : 2)) grad_cluster_kernel(c
 }
 
 template <int RB, int CPT>
-static cudaError_t launch_cluster_rb(int64_t n, int64_t m, const GradArgs& g, bool want_a, bool want_b,
-                                     cudaStream_t stream) {
+static cudaError_t launch_cluster_rb(GradGroup& G, cudaStream_t stream) {
     constexpr int CB = 32 * CPT;
-    const int ba = want_a ? static_cast<int>((n + CB - 1) / CB) : 0;
-    const int bb = want_b ? static_cast<int>((m + CB - 1) / CB) : 0;
-    if (ba + bb == 0) return cudaSuccess;
+    int blocks = 0;
+    for (int p = 0; p < G.count; ++p) {
+        const GradArgs& g = G.g[p];
+        const int ba = g.da ? static_cast<int>((g.n + CB - 1) / CB) : 0;
+        const int bb = g.db ? static_cast<int>((g.m + CB - 1) / CB) : 0;
+        G.block_start[p] = blocks;
+        G.blocks_a[p] = ba;
+        blocks += ba + bb;
+    }
+    G.block_start[G.count] = blocks;
+    if (blocks == 0) return cudaSuccess;
     const int red_bytes = kWarps * RB * CB * 4, ring_bytes = kWarps * 16 * 32 * CPT * 2;
     const int smem = 8192 * 4 + (red_bytes > ring_bytes ? red_bytes : ring_bytes);
     auto kern = grad_cluster_kernel<RB, CPT>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(ba + bb, kCS);
+    cfg.gridDim = dim3(blocks, kCS);
     cfg.blockDim = dim3(256);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
@@ -732,27 +732,46 @@ static cudaError_t launch_cluster_rb(int64_t n, int64_t m, const GradArgs& g, bo
     attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
-    e = cudaLaunchKernelEx(&cfg, kern, g, ba);
+    e = cudaLaunchKernelEx(&cfg, kern, G);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
+}
+
+int grad_rank_bucket(int r) { return r <= 4 ? 4 : r <= 8 ? 8 : r <= 16 ? 16 : r <= 32 ? 32 : 64; }
+
+GradArgs make_grad_args(int64_t T, int64_t n, int64_t m, int r, float scale, const bf16* x, const float* gh,
+                        const bf16* dy, const float* h, float* da, float* db, int accumulate) {
+    GradArgs g = {};
+    g.x = x; g.gh = gh; g.dy = dy; g.h = h; g.da = da; g.db = db;
+    g.T = T; g.n = n; g.m = m; g.r = r; g.scale_b = scale; g.accumulate = accumulate;
+    return g;
+}
+
+cudaError_t launch_grad_reduce_cluster_group(GradGroup& G, cudaStream_t stream, int* launches) {
+    if (G.count < 1 || G.count > kMaxGroup) return cudaErrorInvalidValue;
+    const int rb = grad_rank_bucket(G.g[0].r);
+    for (int p = 1; p < G.count; ++p)
+        if (grad_rank_bucket(G.g[p].r) != rb) return cudaErrorInvalidValue;
+    cudaError_t e;
+    switch (rb) {
+        case 4: e = launch_cluster_rb<4, 8>(G, stream); break;
+        case 8: e = launch_cluster_rb<8, 8>(G, stream); break;
+        case 16: e = launch_cluster_rb<16, 4>(G, stream); break;
+        case 32: e = launch_cluster_rb<32, 2>(G, stream); break;
+        default: e = launch_cluster_rb<64, 2>(G, stream); break;
+    }
+    if (e == cudaSuccess && launches && G.block_start[G.count] > 0) ++*launches;
+    return e;
 }
 
 cudaError_t launch_grad_reduce_cluster(int64_t T, int64_t n, int64_t m, int r, float scale, const bf16* x,
                                        const float* gh, const bf16* dy, const float* h, float* da, float* db,
                                        int accumulate, cudaStream_t stream, int* launches) {
-    GradArgs g = {};
-    g.x = x; g.gh = gh; g.dy = dy; g.h = h; g.da = da; g.db = db;
-    g.T = T; g.n = n; g.m = m; g.r = r; g.scale_b = scale; g.accumulate = accumulate;
     if (!da && !db) return cudaSuccess;
-    if (!da) { g.x = dy; g.gh = h; }
-    cudaError_t e;
-    if (r <= 4) e = launch_cluster_rb<4, 8>(n, m, g, da != nullptr, db != nullptr, stream);
-    else if (r <= 8) e = launch_cluster_rb<8, 8>(n, m, g, da != nullptr, db != nullptr, stream);
-    else if (r <= 16) e = launch_cluster_rb<16, 4>(n, m, g, da != nullptr, db != nullptr, stream);
-    else if (r <= 32) e = launch_cluster_rb<32, 2>(n, m, g, da != nullptr, db != nullptr, stream);
-    else e = launch_cluster_rb<64, 2>(n, m, g, da != nullptr, db != nullptr, stream);
-    if (e == cudaSuccess && launches) ++*launches;
-    return e;
+    static thread_local GradGroup G;
+    G.count = 1;
+    G.g[0] = make_grad_args(T, n, m, r, scale, x, gh, dy, h, da, db, accumulate);
+    return launch_grad_reduce_cluster_group(G, stream, launches);
 }
 
 template <int RB, int CPT, int MINB>

@@ -20,6 +20,9 @@ struct GemmCollector {
     lora_sm100::FusedGemmParams p[lora_sm100::kMaxGroup];
     int rp[lora_sm100::kMaxGroup];
     int cg[lora_sm100::kMaxGroup];
+    // K3 (dA, dB) problems of the grouped backward, launched together at the end
+    int k3_count = 0;
+    lora_sm100::GradArgs k3[lora_sm100::kMaxGroup];
 };
 
 // col != nullptr: the fused GEMM is appended to `col` instead of launched.
@@ -34,6 +37,8 @@ lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
                      GemmCollector* col = nullptr, int stages = 3);
 // launch the collected problems, one grouped launch per (r_pad, CTA group) class
 lora_status launch_collected(int mode, GemmCollector& col, cudaStream_t stream, int* launches);
+// launch the collected K3 problems, one launch per rank bucket
+lora_status launch_collected_k3(GemmCollector& col, cudaStream_t stream, int* launches);
 size_t fwd_workspace(const lora_dims* d);
 size_t bwd_workspace(const lora_dims* d);
 

@@ -71,6 +71,32 @@ struct GradMaps {
 };
 int grad_strip_cols();  // columns per K3 CTA (box inner extent of the x / dY maps)
 
+struct GradArgs {
+    const __nv_bfloat16* x;   // [T, n]
+    const float* gh;          // [T, r]   (dA coefficients, already scaled by s)
+    const __nv_bfloat16* dy;  // [T, m]
+    const float* h;           // [T, r]   (dB coefficients, unscaled)
+    float* da;                // [r, n] or null
+    float* db;                // [m, r] or null
+    int64_t T, n, m;
+    int r;
+    int strips_a;             // (strip kernels) CTAs [0, strips_a) own dA strips
+    float scale_b;            // s
+    int accumulate;
+};
+// several problems of the same rank bucket in one K3 launch
+struct GradGroup {
+    GradArgs g[kMaxGroup];
+    int block_start[kMaxGroup + 1];
+    int blocks_a[kMaxGroup];
+    int count;
+};
+GradArgs make_grad_args(int64_t T, int64_t n, int64_t m, int r, float scale, const __nv_bfloat16* x,
+                        const float* gh, const __nv_bfloat16* dy, const float* h, float* da, float* db,
+                        int accumulate);
+int grad_rank_bucket(int r);
+cudaError_t launch_grad_reduce_cluster_group(GradGroup& G, cudaStream_t stream, int* launches);
+
 // K3 v3 (default): T split over a cluster of 8 CTAs, DSMEM reduction in rank order.
 cudaError_t launch_grad_reduce_cluster(int64_t T, int64_t n, int64_t m, int r, float scale,
                                        const __nv_bfloat16* x, const float* gh, const __nv_bfloat16* dy,
