@@ -275,7 +275,79 @@ lora_status fwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
     return LORA_OK;
 }
 
+// K3 implementation: "mma" (default, tensor cores), or the CUDA-core
+// experiments "cluster" | "tma" | "ldg" (LORA_K3).
+enum K3Mode { kK3Mma, kK3Cluster, kK3Tma, kK3Ldg };
+static K3Mode k3_mode() {
+    const char* v = getenv("LORA_K3");
+    if (!v) return kK3Mma;
+    if (!strcmp(v, "cluster")) return kK3Cluster;
+    if (!strcmp(v, "tma")) return kK3Tma;
+    if (!strcmp(v, "ldg")) return kK3Ldg;
+    return kK3Mma;
+}
+
+// K3 on the tensor cores for `count` problems: one dA set (X = x, C = gh) and
+// one dB set (X = dY, C = h, scale s) per problem; dA sets of problems that
+// share x (same pointer and shape) are stacked into one job, so x is read once.
+static lora_status launch_k3_mma(const GradArgs* pr, int count, cudaStream_t stream, int* launches) {
+    DevInfo dev;
+    lora_status st = device_info(&dev);
+    if (st != LORA_OK) return st;
+    static thread_local GradMmaGroup G;
+    const void* src[kMaxGradJobs];
+    int used[kMaxGradJobs];   // B-operand rows in use: 3 r8 per set (hi, mid, lo)
+    G.njobs = 0;
+    auto flush = [&]() -> lora_status {
+        if (G.njobs == 0) return LORA_OK;
+        cudaError_t e = launch_grad_mma(G, dev.sms, stream);
+        G.njobs = 0;
+        if (e != cudaSuccess) return cuda_fail(e, "K3 (tensor-core dA / dB) launch");
+        ++*launches;
+        return LORA_OK;
+    };
+    auto add = [&](const void* X, int64_t T, int64_t N, const float* coef, int r, float scale, float* out,
+                   int64_t stride_col, int64_t stride_k, int accumulate) -> lora_status {
+        const int r8 = (r + 7) / 8 * 8;
+        GradMmaSet s;
+        s.coef = coef; s.out = out; s.stride_col = stride_col; s.stride_k = stride_k;
+        s.r = r; s.r8 = r8; s.accumulate = accumulate; s.scale = scale;
+        for (int jb = 0; jb < G.njobs; ++jb) {
+            GradMmaJob& J = G.job[jb];
+            if (src[jb] == X && J.T == T && J.N == N && J.nsets < kMaxGradSets && used[jb] + 3 * r8 <= 256) {
+                s.row0 = used[jb];
+                J.set[J.nsets++] = s;
+                used[jb] += 3 * r8;
+                J.q_pad = (used[jb] + 15) / 16 * 16;
+                return LORA_OK;
+            }
+        }
+        if (G.njobs == kMaxGradJobs && (st = flush()) != LORA_OK) return st;
+        GradMmaJob& J = G.job[G.njobs];
+        lora_status es = encode_2d(&J.x, X, N, T, N * 2, 64, 64, 128, "K3 activation");
+        if (es != LORA_OK) return es;
+        J.T = T; J.N = N; J.nsets = 1; J.q_pad = (3 * r8 + 15) / 16 * 16;
+        s.row0 = 0;
+        J.set[0] = s;
+        used[G.njobs] = 3 * r8;
+        src[G.njobs++] = X;
+        return LORA_OK;
+    };
+    for (int i = 0; i < count; ++i) {
+        const GradArgs& g = pr[i];
+        if (g.da && (st = add(g.x, g.T, g.n, g.gh, g.r, 1.0f, g.da, 1, g.n, g.accumulate)) != LORA_OK) return st;
+        if (g.db && (st = add(g.dy, g.T, g.m, g.h, g.r, g.scale_b, g.db, g.r, 1, g.accumulate)) != LORA_OK)
+            return st;
+    }
+    return flush();
+}
+
 lora_status launch_collected_k3(GemmCollector& col, cudaStream_t stream, int* launches) {
+    if (k3_mode() == kK3Mma) {
+        lora_status st = launch_k3_mma(col.k3, col.k3_count, stream, launches);
+        col.k3_count = 0;
+        return st;
+    }
     static thread_local GradGroup G;
     bool done[kMaxGroup] = {};
     for (int i = 0; i < col.k3_count; ++i) {
@@ -434,15 +506,17 @@ lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
         hsrc = hbuf;
     }
     if (da || db) {
-        const char* k3 = getenv("LORA_K3");  // experiments: "tma" | "ldg"; default: cluster
-        if (!k3 || (strcmp(k3, "tma") != 0 && strcmp(k3, "ldg") != 0)) {
+        const K3Mode k3 = k3_mode();
+        if (k3 == kK3Mma || k3 == kK3Cluster) {
+            const GradArgs g = make_grad_args(T, n, m, r, s, xa, gh, dya, hsrc, da, db, accumulate);
             if (col) {   // grouped backward: one K3 launch for the whole group
                 if (col->k3_count >= kMaxGroup) return fail(LORA_ERR_UNSUPPORTED, "too many grouped problems");
-                col->k3[col->k3_count++] = make_grad_args(T, n, m, r, s, xa, gh, dya, hsrc, da, db, accumulate);
+                col->k3[col->k3_count++] = g;
                 return LORA_OK;
             }
+            if (k3 == kK3Mma) return launch_k3_mma(&g, 1, stream, launches);
             e = launch_grad_reduce_cluster(T, n, m, r, s, xa, gh, dya, hsrc, da, db, accumulate, stream, launches);
-        } else if (r % 4 == 0 && strcmp(k3, "tma") == 0) {
+        } else if (r % 4 == 0 && k3 == kK3Tma) {
             // TMA-ring variant: coefficient rows (4r bytes) are TMA-legal when r % 4 == 0
             GradMaps gm;
             const int sc = grad_strip_cols();

@@ -91,6 +91,35 @@ struct GradGroup {
     int blocks_a[kMaxGroup];
     int count;
 };
+// K3 on the tensor cores (default): O[c, q] = scale * sum_t X[t, c] C[t, q].
+// A JOB is one bf16 activation X [T, N] (TMA map, box {64 columns, 64 tokens},
+// SWIZZLE_128B) with up to kMaxGradSets coefficient SETS stacked along the MMA
+// N dimension (set j occupies rows [row0, row0 + 3 r8): hi, mid, lo).
+constexpr int kGradMmaCols = 256;   // X columns per CTA
+constexpr int kMaxGradSets = 8;
+constexpr int kMaxGradJobs = 16;
+struct GradMmaSet {
+    const float* coef;          // C [T, r] fp32 row-major
+    float* out;                 // O[c, k] at out[c * stride_col + k * stride_k]
+    int64_t stride_col, stride_k;
+    int r, r8, row0, accumulate;
+    float scale;
+};
+struct GradMmaJob {
+    CUtensorMap x;
+    int64_t T, N;
+    int nsets, q_pad;           // q_pad = roundup(3 * sum r8, 16) (MMA N, <= 256)
+    GradMmaSet set[kMaxGradSets];
+};
+struct GradMmaGroup {
+    GradMmaJob job[kMaxGradJobs];
+    int tile_start[kMaxGradJobs + 1];
+    int njobs;
+    int S, stages, stage_bytes, cs_bytes, region_bytes;   // filled in by launch_grad_mma
+};
+cudaError_t launch_grad_mma(GradMmaGroup& G, int num_sms, cudaStream_t stream);
+int grad_mma_cluster_size(int tiles, int kb_total, int num_sms);
+
 GradArgs make_grad_args(int64_t T, int64_t n, int64_t m, int r, float scale, const __nv_bfloat16* x,
                         const float* gh, const __nv_bfloat16* dy, const float* h, float* da, float* db,
                         int accumulate);
