@@ -252,6 +252,11 @@ def run_ours(args, wl):
         e["ws_b"] = torch.empty(max(256, int(L.lib.lora_tp_linear_bwd_workspace_bytes(ctypes.byref(dd)))),
                                 dtype=torch.uint8, device=dev)
         lin.append(e)
+    # the linears of a group read the SAME activation in the model (q/k/v read the
+    # attention input, gate/up the MLP input): one shared x tensor per group
+    for gidx in wl.groups:
+        for i in gidx[1:]:
+            lin[i]["x"] = lin[gidx[0]]["x"]
     launches = {"n": 0}
 
     # N = 1: the linears that share an input in the model (q,k,v / gate,up) run as
@@ -398,7 +403,8 @@ def run_ours(args, wl):
     gpu_launches = launches["n"]
 
     # ---- end to end through the public API with host buffers
-    hx = [e["x"].cpu().pin_memory() for e in lin]
+    xs = list({id(e["x"]): e["x"] for e in lin}.values())     # each distinct input once
+    hx = [t.cpu().pin_memory() for t in xs]
     hdy = [e["dy"].cpu().pin_memory() for e in lin]
     hda = [torch.empty_like(e["da"], device="cpu").pin_memory() for e in lin]
     hdb = [torch.empty_like(e["db"], device="cpu").pin_memory() for e in lin]
@@ -406,8 +412,9 @@ def run_ours(args, wl):
     d2h = sum(t.numel() * t.element_size() for t in hda + hdb)
 
     def e2e_step():
-        for e, a_, b_ in zip(lin, hx, hdy):
-            e["x"].copy_(a_, non_blocking=True)
+        for t, a_ in zip(xs, hx):
+            t.copy_(a_, non_blocking=True)
+        for e, b_ in zip(lin, hdy):
             e["dy"].copy_(b_, non_blocking=True)
         step()
         for e, a_, b_ in zip(lin, hda, hdb):
@@ -464,6 +471,7 @@ def run_ours(args, wl):
                        "parallelism": f"tp{world}" if world > 1 else "single",
                        "cuda_graph": graph is not None,
                        "grouped_calls": [[wl.linears[i].name for i in g] for g in wl.groups] if use_groups else None,
+                       "shared_inputs": [[wl.linears[i].name for i in g] for g in wl.groups if len(g) > 1],
                        "l2": "flushed between timed steps (2xL2 write then 2xL2 read, outside the "
                              "event pairs)"},
             "tokens_per_s": tokens * K / (total_ms * 1e-3),

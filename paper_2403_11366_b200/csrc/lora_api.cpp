@@ -175,7 +175,7 @@ static FwdWs fwd_ws(const lora_dims* d) {
 
 // Backward workspace: B^T [r, m], gh [T, r] fp32, h [T, r] fp32 (when not saved).
 struct BwdWs {
-    size_t b8, gh, h, flags, total;
+    size_t b8, gh, h, flags, cs_a, cs_b, total;
 };
 static BwdWs bwd_ws(const lora_dims* d) {
     BwdWs w;
@@ -186,6 +186,9 @@ static BwdWs bwd_ws(const lora_dims* d) {
     w.gh = off; off += align256(size_t(T) * r * 4);
     w.h = off; off += align256(size_t(T) * r * 4);
     w.flags = off; off += align256(size_t(T / 128 + 2) * 8);         // >= row blocks x CTAs per pair
+    const size_t cs = align256(size_t(3 * r8_of(r)) * size_t((T + 63) / 64 * 64) * 2);
+    w.cs_a = off; off += cs;                                         // K3s: split gh
+    w.cs_b = off; off += cs;                                         // K3s: split h
     w.total = off;
     return w;
 }
@@ -290,56 +293,94 @@ static K3Mode k3_mode() {
 // K3 on the tensor cores for `count` problems: one dA set (X = x, C = gh) and
 // one dB set (X = dY, C = h, scale s) per problem; dA sets of problems that
 // share x (same pointer and shape) are stacked into one job, so x is read once.
+// Two launches: K3s (split every coefficient matrix once) and K3.
+static int64_t t_pad_of(int64_t T) { return (T + 63) / 64 * 64; }
+
 static lora_status launch_k3_mma(const GradArgs* pr, int count, cudaStream_t stream, int* launches) {
     DevInfo dev;
     lora_status st = device_info(&dev);
     if (st != LORA_OK) return st;
+    if (count > kMaxGroup) return fail(LORA_ERR_UNSUPPORTED, "too many problems for one K3 launch");
     static thread_local GradMmaGroup G;
-    const void* src[kMaxGradJobs];
-    int used[kMaxGradJobs];   // B-operand rows in use: 3 r8 per set (hi, mid, lo)
-    G.njobs = 0;
-    auto flush = [&]() -> lora_status {
-        if (G.njobs == 0) return LORA_OK;
-        cudaError_t e = launch_grad_mma(G, dev.sms, stream);
-        G.njobs = 0;
-        if (e != cudaSuccess) return cuda_fail(e, "K3 (tensor-core dA / dB) launch");
-        ++*launches;
-        return LORA_OK;
-    };
-    auto add = [&](const void* X, int64_t T, int64_t N, const float* coef, int r, float scale, float* out,
-                   int64_t stride_col, int64_t stride_k, int accumulate) -> lora_status {
-        const int r8 = (r + 7) / 8 * 8;
-        GradMmaSet s;
-        s.coef = coef; s.out = out; s.stride_col = stride_col; s.stride_k = stride_k;
-        s.r = r; s.r8 = r8; s.accumulate = accumulate; s.scale = scale;
-        for (int jb = 0; jb < G.njobs; ++jb) {
-            GradMmaJob& J = G.job[jb];
-            if (src[jb] == X && J.T == T && J.N == N && J.nsets < kMaxGradSets && used[jb] + 3 * r8 <= 256) {
-                s.row0 = used[jb];
-                J.set[J.nsets++] = s;
-                used[jb] += 3 * r8;
-                J.q_pad = (used[jb] + 15) / 16 * 16;
-                return LORA_OK;
-            }
-        }
-        if (G.njobs == kMaxGradJobs && (st = flush()) != LORA_OK) return st;
-        GradMmaJob& J = G.job[G.njobs];
-        lora_status es = encode_2d(&J.x, X, N, T, N * 2, 64, 64, 128, "K3 activation");
-        if (es != LORA_OK) return es;
-        J.T = T; J.N = N; J.nsets = 1; J.q_pad = (3 * r8 + 15) / 16 * 16;
-        s.row0 = 0;
-        J.set[0] = s;
-        used[G.njobs] = 3 * r8;
-        src[G.njobs++] = X;
-        return LORA_OK;
-    };
+    static thread_local CoefSplitGroup SG;
+    struct Pending {
+        const void* X;
+        int64_t T, N;
+        const float* coef;
+        __nv_bfloat16* cs;
+        GradMmaSet set;
+    } sets[kMaxGradSetsTotal];
+    int ns = 0;
     for (int i = 0; i < count; ++i) {
         const GradArgs& g = pr[i];
-        if (g.da && (st = add(g.x, g.T, g.n, g.gh, g.r, 1.0f, g.da, 1, g.n, g.accumulate)) != LORA_OK) return st;
-        if (g.db && (st = add(g.dy, g.T, g.m, g.h, g.r, g.scale_b, g.db, g.r, 1, g.accumulate)) != LORA_OK)
+        const int r8 = (g.r + 7) / 8 * 8;
+        if (g.da) {
+            GradMmaSet s = {g.da, 1, g.n, g.r, r8, 0, g.accumulate, 1.0f};
+            sets[ns++] = {g.x, g.T, g.n, g.gh, g.cs_a, s};
+        }
+        if (g.db) {
+            GradMmaSet s = {g.db, g.r, 1, g.r, r8, 0, g.accumulate, g.scale_b};
+            sets[ns++] = {g.dy, g.T, g.m, g.h, g.cs_b, s};
+        }
+    }
+    if (ns == 0) return LORA_OK;
+    // group the sets into jobs: same activation (pointer, T, N), at most 256 B-operand rows
+    int job_of[kMaxGradSetsTotal];
+    int used[kMaxGradJobs];
+    int nj = 0;
+    const void* jx[kMaxGradJobs];
+    for (int i = 0; i < ns; ++i) {
+        job_of[i] = -1;
+        for (int j = 0; j < nj; ++j)
+            if (jx[j] == sets[i].X && G.job[j].T == sets[i].T && G.job[j].N == sets[i].N &&
+                used[j] + 3 * sets[i].set.r8 <= 256) {
+                job_of[i] = j;
+                break;
+            }
+        if (job_of[i] < 0) {
+            GradMmaJob& J = G.job[nj];
+            J.T = sets[i].T; J.N = sets[i].N; J.nsets = 0;
+            jx[nj] = sets[i].X;
+            used[nj] = 0;
+            job_of[i] = nj++;
+        }
+        used[job_of[i]] += 3 * sets[i].set.r8;
+    }
+    // sets in job order (each job's sets contiguous), row offsets, maps
+    int k = 0;
+    SG.count = 0;
+    for (int j = 0; j < nj; ++j) {
+        GradMmaJob& J = G.job[j];
+        J.set0 = k;
+        J.nsets = 0;
+        int row = 0;
+        for (int i = 0; i < ns; ++i) {
+            if (job_of[i] != j) continue;
+            GradMmaSet s = sets[i].set;
+            s.row0 = row;
+            row += 3 * s.r8;
+            G.set[k] = s;
+            const int64_t tp = t_pad_of(sets[i].T);
+            if ((st = encode_2d(&G.csmap[k], sets[i].cs, tp, 3 * s.r8, tp * 2, 64, 3 * s.r8, 128, "K3 split "
+                                "coefficients")) != LORA_OK)
+                return st;
+            SG.s[SG.count++] = {sets[i].coef, sets[i].cs, sets[i].T, tp, s.r, s.r8};
+            ++k;
+            ++J.nsets;
+        }
+        J.q_used = row;
+        J.q_pad = (row + 15) / 16 * 16;
+        if ((st = encode_2d(&G.xmap[j], jx[j], J.N, J.T, J.N * 2, 64, 64, 128, "K3 activation")) != LORA_OK)
             return st;
     }
-    return flush();
+    G.njobs = nj;
+    cudaError_t e = launch_coef_split(SG, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "K3s (coefficient split) launch");
+    ++*launches;
+    e = launch_grad_mma(G, dev.sms, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "K3 (tensor-core dA / dB) launch");
+    ++*launches;
+    return LORA_OK;
 }
 
 lora_status launch_collected_k3(GemmCollector& col, cudaStream_t stream, int* launches) {
@@ -508,7 +549,9 @@ lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
     if (da || db) {
         const K3Mode k3 = k3_mode();
         if (k3 == kK3Mma || k3 == kK3Cluster) {
-            const GradArgs g = make_grad_args(T, n, m, r, s, xa, gh, dya, hsrc, da, db, accumulate);
+            GradArgs g = make_grad_args(T, n, m, r, s, xa, gh, dya, hsrc, da, db, accumulate);
+            g.cs_a = reinterpret_cast<__nv_bfloat16*>(wsb + W.cs_a);
+            g.cs_b = reinterpret_cast<__nv_bfloat16*>(wsb + W.cs_b);
             if (col) {   // grouped backward: one K3 launch for the whole group
                 if (col->k3_count >= kMaxGroup) return fail(LORA_ERR_UNSUPPORTED, "too many grouped problems");
                 col->k3[col->k3_count++] = g;

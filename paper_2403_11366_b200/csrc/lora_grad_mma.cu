@@ -8,24 +8,25 @@
 // r >= 16 (2 T r (n + m) FMAs vs 148 SMs x 128 FMA/clk), but tiny for the
 // tensor cores; on tcgen05 the kernel is bound by reading X from HBM once.
 //
-// Mapping (one CTA = 256 X columns x one token slice):
-//   MMA   D[c, q] += X^T[c, t] Cs[q, t]     M = 128 columns (two MMAs per
-//         k-step for the CTA's 256 columns), N = q_pad, K = 16 tokens.
+// K3s (split pre-pass): Cs [3 r8, T_pad] bf16 = the fp32 coefficients as
+//   three bf16 rows hi + mid + lo (8 + 8 + 8 significand bits: C is
+//   represented exactly, so every tensor-core product is exact and only the
+//   fp32 accumulation rounds, as on the CUDA cores), token-contiguous, i.e.
+//   the K-major B operand of the MMA below.  Done once per coefficient
+//   matrix instead of once per column tile.
+// K3 (one CTA = 128 X columns x one token slice):
+//   MMA   D[c, q] += X^T[c, t] Cs[q, t]     M = 128 columns, N = q_pad, K = 16.
 //         A operand = the X tile exactly as TMA lands it ([64 tokens][64
 //         columns] SWIZZLE_128B boxes, read MN-major: no transpose pass).
-//   Cs    the fp32 coefficients split into three bf16 rows hi + mid + lo
-//         (8 + 8 + 8 significand bits: C is represented exactly, so every
-//         product is exact and only the fp32 accumulation rounds, as on the
-//         CUDA cores; x and dY are exact bf16), written K-major SW128 by four
-//         converter warps; several coefficient SETS sharing one X (dA of the
-//         q/k/v projections all read x) are stacked along N, so x is read once
-//         for all of them.
-//   split the tokens are split over a cluster of S CTAs (same columns); each
-//         CTA drains its TMEM partial into shared memory and the cluster sums
-//         the S partials over DSMEM in rank order: deterministic, no atomics,
-//         no global partial buffer, final values (or +=) written once.
+//         Several coefficient SETS sharing one X (dA of q/k/v all read x) are
+//         stacked along N, so x is read once for all of them.
+//   split when there are too few column tiles to fill the GPU the tokens are
+//         split over a cluster of S CTAs; each CTA drains its TMEM partial
+//         into shared memory and the cluster sums the S partials over DSMEM
+//         in rank order: deterministic, no atomics, no global partial buffer.
+//         With S = 1 the epilogue stores straight from TMEM.
 // Warp roles (192 threads): warp 0 TMA producer, warp 1 MMA issuer + TMEM
-// owner, warps 2..5 coefficient converters, then epilogue; all six reduce.
+// owner, warps 2..5 epilogue (one TMEM lane quarter each); all six reduce.
 #include <cooperative_groups.h>
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -40,13 +41,14 @@ namespace lora_sm100 {
 
 namespace {
 
-constexpr int KB = 64;              // tokens per k-block (one 128-byte SW128 row of the Cs operand)
+constexpr int KB = 64;              // tokens per k-block (one 128-byte SW128 row of Cs)
 constexpr int X_BOX = 64 * KB * 2;  // one [64 tokens][64 columns] bf16 box = 8 KiB
-constexpr int X_BYTES = 4 * X_BOX;  // 256 columns per CTA
+constexpr int X_BYTES = 2 * X_BOX;  // 128 columns per CTA
 constexpr int THREADS = 192;
-constexpr int PST = kGradMmaCols + 1;  // partial row stride (floats): conflict-free in both orders
-constexpr int SMEM_LIMIT = 227 * 1024;
-constexpr int MAX_STAGES = 6;
+constexpr int PA = kGradMmaCols + 4;   // dA partial row stride (floats)
+constexpr int SMEM_CTA_MAX = 227 * 1024;
+constexpr int SMEM_SM = 228 * 1024;
+constexpr int MAX_STAGES = 8;
 
 __device__ __forceinline__ void tmem_ld_32x32b_x8(uint32_t taddr, uint32_t (&v)[8]) {
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
@@ -54,38 +56,85 @@ __device__ __forceinline__ void tmem_ld_32x32b_x8(uint32_t taddr, uint32_t (&v)[
                    "=r"(v[7])
                  : "r"(taddr));
 }
-
-// 8 fp32 -> three 16-byte chunks of bf16: hi = RNE(v), mid = RNE(v - hi),
-// lo = RNE(v - hi - mid).  Both differences are exact in fp32 (Sterbenz), and
-// v - hi - mid has at most 8 significant bits left, so hi + mid + lo == v.
-__device__ __forceinline__ void split8(const float (&v)[8], uint4& hi, uint4& mid, uint4& lo) {
-    uint32_t h[4], md[4], l[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const __nv_bfloat162 hv = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
-        const float2 hf = __bfloat1622float2(hv);
-        const float r0 = v[2 * i] - hf.x, r1 = v[2 * i + 1] - hf.y;
-        const __nv_bfloat162 mv = __floats2bfloat162_rn(r0, r1);
-        const float2 mf = __bfloat1622float2(mv);
-        const __nv_bfloat162 lv = __floats2bfloat162_rn(r0 - mf.x, r1 - mf.y);
-        h[i] = *reinterpret_cast<const uint32_t*>(&hv);
-        md[i] = *reinterpret_cast<const uint32_t*>(&mv);
-        l[i] = *reinterpret_cast<const uint32_t*>(&lv);
-    }
-    hi = make_uint4(h[0], h[1], h[2], h[3]);
-    mid = make_uint4(md[0], md[1], md[2], md[3]);
-    lo = make_uint4(l[0], l[1], l[2], l[3]);
+__device__ __forceinline__ void tmem_alloc_n(uint32_t* dst, uint32_t ncols) {   // whole warp
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst)),
+                 "r"(ncols) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc_n(uint32_t taddr, uint32_t ncols) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
 }
 
-// 1-D bulk copy global -> shared (16-byte multiple), completes on `bar`
-__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                 ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
+// dB partials: [128 columns][r4 + 4] floats; dA partials: [r][PA]
+__device__ __host__ __forceinline__ int partial_floats(const GradMmaSet& st) {
+    return st.stride_col == 1 ? st.r * PA : kGradMmaCols * ((st.r + 3) / 4 * 4 + 4);
 }
 
 }  // namespace
 
+#ifdef LORA_PROBE_K3
+// timing experiment only: per-CTA globaltimer stamps (start, main loop done,
+// partial written, reduction done)
+__device__ unsigned long long lora_k3_probe[16384 * 4];
+extern "C" int lora_probe_k3_read(unsigned long long* host, int n) {
+    return static_cast<int>(cudaMemcpyFromSymbol(host, lora_k3_probe, sizeof(unsigned long long) * n));
+}
+#define K3_STAMP(i)                                                                                   \
+    do {                                                                                              \
+        if (threadIdx.x == 64)                                                                        \
+            lora_k3_probe[(blockIdx.x * gridDim.y + blockIdx.y) * 4 + (i)] = globaltimer_ns();        \
+    } while (0)
+#else
+#define K3_STAMP(i) do {} while (0)
+#endif
+
+// ------------------------------------------------------------------ K3s
+// grid (T_pad / 64, sets); block 256: stage the [64, r] fp32 chunk (contiguous)
+// in shared memory, then write the three bf16 rows per coefficient.
+__global__ void __launch_bounds__(256) coef_split_kernel(const __grid_constant__ CoefSplitGroup G) {
+    __shared__ float chunk[64 * 64];
+    const CoefSplitArgs& a = G.s[blockIdx.y];
+    const int64_t t0 = static_cast<int64_t>(blockIdx.x) * 64;
+    if (t0 >= a.T_pad) return;
+    const int rows = a.T - t0 < 64 ? (a.T - t0 > 0 ? static_cast<int>(a.T - t0) : 0) : 64;
+    for (int i = threadIdx.x; i < rows * a.r; i += 256) chunk[i] = a.coef[t0 * a.r + i];
+    __syncthreads();
+    // thread -> (coefficient k, token pair): two tokens per 32-bit store
+    for (int e = threadIdx.x; e < a.r8 * 32; e += 256) {
+        const int k = e / 32, tp = (e % 32) * 2;
+        uint32_t hv[2], mv[2], lv[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int t = tp + u;
+            const float v = (k < a.r && t < rows) ? chunk[t * a.r + k] : 0.0f;
+            const __nv_bfloat16 h = __float2bfloat16_rn(v);
+            const float r0 = v - __bfloat162float(h);
+            const __nv_bfloat16 md = __float2bfloat16_rn(r0);
+            const __nv_bfloat16 l = __float2bfloat16_rn(r0 - __bfloat162float(md));
+            hv[u] = __bfloat16_as_ushort(h);
+            mv[u] = __bfloat16_as_ushort(md);
+            lv[u] = __bfloat16_as_ushort(l);
+        }
+        __nv_bfloat16* base = a.cs + t0 + tp;
+        *reinterpret_cast<uint32_t*>(base + static_cast<int64_t>(k) * a.T_pad) = hv[0] | (hv[1] << 16);
+        *reinterpret_cast<uint32_t*>(base + static_cast<int64_t>(a.r8 + k) * a.T_pad) = mv[0] | (mv[1] << 16);
+        *reinterpret_cast<uint32_t*>(base + static_cast<int64_t>(2 * a.r8 + k) * a.T_pad) = lv[0] | (lv[1] << 16);
+    }
+}
+
+cudaError_t launch_coef_split(const CoefSplitGroup& G, cudaStream_t stream) {
+    if (G.count < 1 || G.count > kMaxGradSetsTotal) return cudaErrorInvalidValue;
+    int64_t tp = 0;
+    for (int i = 0; i < G.count; ++i) {
+        if (G.s[i].r < 1 || G.s[i].r > 64 || G.s[i].T_pad % 64 != 0) return cudaErrorInvalidValue;
+        tp = G.s[i].T_pad > tp ? G.s[i].T_pad : tp;
+    }
+    if (tp == 0) return cudaSuccess;
+    coef_split_kernel<<<dim3(static_cast<unsigned>(tp / 64), G.count), 256, 0, stream>>>(G);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ K3
 __global__ void __launch_bounds__(THREADS, 1) grad_mma_kernel(const __grid_constant__ GradMmaGroup G) {
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
@@ -93,13 +142,12 @@ __global__ void __launch_bounds__(THREADS, 1) grad_mma_kernel(const __grid_const
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int stages = G.stages;
     const int stage_bytes = G.stage_bytes;
-    // stage s: [X 32 KiB][Cs operand, cs_bytes][fp32 coefficient staging, 256 r bytes per set]
-    uint64_t* loaded = reinterpret_cast<uint64_t*>(smem + G.region_bytes);   // X + coefficients landed
-    uint64_t* full = loaded + MAX_STAGES;                                    // Cs operand written
-    uint64_t* empty = full + MAX_STAGES;                                     // MMAs of the stage done
+    // stage s: [X 16 KiB][Cs operand: q_pad rows x 128 bytes]
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + G.region_bytes);
+    uint64_t* empty = full + MAX_STAGES;
     uint64_t* tmem_full = empty + MAX_STAGES;
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tmem_full + 1);
-    float* partial = reinterpret_cast<float*>(smem);   // reuses the ring after the main loop
+    float* partial = reinterpret_cast<float*>(smem);   // S > 1: reuses the ring after the main loop
 
     const int tile = static_cast<int>(blockIdx.x);
     int jb = 0;
@@ -107,57 +155,66 @@ __global__ void __launch_bounds__(THREADS, 1) grad_mma_kernel(const __grid_const
     const GradMmaJob& J = G.job[jb];
     const int64_t col0 = static_cast<int64_t>(tile - G.tile_start[jb]) * kGradMmaCols;
     const int S = G.S;
-    const int rank = static_cast<int>(cluster.block_rank());
+    const int rank = S > 1 ? static_cast<int>(cluster.block_rank()) : 0;
     const int kb_total = static_cast<int>((J.T + KB - 1) / KB);
     const int kps = (kb_total + S - 1) / S;
     const int kb0 = rank * kps;
     const int nkb = kb0 < kb_total ? (kb_total - kb0 < kps ? kb_total - kb0 : kps) : 0;
-    const bool two = col0 + 128 < J.N;   // the second M = 128 half holds real columns
+    const bool two = col0 + 64 < J.N;   // the second 64-column box holds real columns
     const int q_pad = J.q_pad;
+    const int q_used = J.q_used;
     const uint32_t warp = warp_id(), lane = lane_id();
 
-    if (warp == 0 && lane == 0) tma_prefetch_desc(&J.x);
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&G.xmap[jb]);
+        for (int j = 0; j < J.nsets; ++j) tma_prefetch_desc(&G.csmap[J.set0 + j]);
+    }
     if (warp == 1) {
         if (lane == 0) {
             for (int s = 0; s < stages; ++s) {
-                mbar_init(&loaded[s], 1);     // producer (expect_tx)
-                mbar_init(&full[s], 4);       // 4 converter warps
+                mbar_init(&full[s], 1);
                 mbar_init(&empty[s], 1);
             }
             mbar_init(tmem_full, 1);
             fence_mbar_init();
         }
         __syncwarp();
-        tmem_alloc<512>(tmem_holder);
+        tmem_alloc_n(tmem_holder, G.tmem_cols);
+    }
+    if (warp >= 2 && q_pad > q_used) {
+        // Cs rows [q_used, q_pad) pad N to a multiple of 16: zero once (TMA never writes them)
+        const int pr = (q_pad - q_used) * 8;   // 16-byte chunks per stage
+        for (int e = static_cast<int>(threadIdx.x) - 64; e < pr * stages; e += 128) {
+            const int s = e / pr, rc = e - s * pr;
+            *reinterpret_cast<uint4*>(smem + s * stage_bytes + X_BYTES +
+                                      swizzled_offset(q_used + rc / 8, rc % 8, 128)) = make_uint4(0, 0, 0, 0);
+        }
+        fence_proxy_async_smem();
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
+    K3_STAMP(0);
 
     if (warp == 0) {
-        // ---------------- producer: X boxes [64 tokens][64 columns] (TMA) and the
-        // k-block's fp32 coefficient rows of every set (contiguous: 1-D bulk copy)
+        // ---------------- TMA producer: X boxes [64 tokens][64 columns] + Cs boxes [3 r8 rows][64 tokens]
         if (lane == 0) {
-            const int nbox = two ? 4 : 2;
+            const int nbox = two ? 2 : 1;
+            uint32_t tx = nbox * X_BOX;
+            for (int j = 0; j < J.nsets; ++j) tx += 3 * G.set[J.set0 + j].r8 * 128;
             const uint64_t pol = l2_policy_evict_first();
             for (int i = 0, s = 0, ph = 0; i < nkb; ++i) {
                 mbar_wait(&empty[s], ph ^ 1);
                 uint8_t* sx = smem + s * stage_bytes;
-                uint8_t* sstg = sx + X_BYTES + G.cs_bytes;
+                mbar_arrive_expect_tx(&full[s], tx);
                 const int t0 = (kb0 + i) * KB;
-                const int64_t rows = J.T - t0 < KB ? J.T - t0 : KB;
-                uint32_t tx = nbox * X_BOX;
-                for (int j = 0; j < J.nsets; ++j)
-                    tx += static_cast<uint32_t>((rows * J.set[j].r * 4 + 15) / 16 * 16);
-                mbar_arrive_expect_tx(&loaded[s], tx);
                 for (int b = 0; b < nbox; ++b)
-                    tma_load_2d_hint(sx + b * X_BOX, &J.x, static_cast<int32_t>(col0 + 64 * b), t0, &loaded[s],
-                                     pol);
-                // (the last k-block may round up past T * r floats by < 16 bytes: same 16-byte granule)
-                for (int j = 0, off = 0; j < J.nsets; off += 256 * J.set[j].r, ++j)
-                    bulk_load(sstg + off, J.set[j].coef + static_cast<int64_t>(t0) * J.set[j].r,
-                              static_cast<uint32_t>((rows * J.set[j].r * 4 + 15) / 16 * 16), &loaded[s]);
+                    tma_load_2d_hint(sx + b * X_BOX, &G.xmap[jb], static_cast<int32_t>(col0 + 64 * b), t0,
+                                     &full[s], pol);
+                for (int j = 0; j < J.nsets; ++j)
+                    tma_load_2d(sx + X_BYTES + G.set[J.set0 + j].row0 * 128, &G.csmap[J.set0 + j], t0, 0,
+                                &full[s]);
                 if (++s == stages) { s = 0; ph ^= 1; }
             }
         }
@@ -166,22 +223,15 @@ __global__ void __launch_bounds__(THREADS, 1) grad_mma_kernel(const __grid_const
         if (lane == 0) {
             const uint32_t idesc = make_idesc_bf16(128, static_cast<uint32_t>(q_pad), 1, 0);
             for (int i = 0, s = 0, ph = 0; i < nkb; ++i) {
-                mbar_wait(&loaded[s], ph);
                 mbar_wait(&full[s], ph);
                 tc_fence_after();
                 const uint32_t sx = smem_u32(smem + s * stage_bytes);
-                const uint32_t sc = sx + X_BYTES;
 #pragma unroll
                 for (int kk = 0; kk < KB / 16; ++kk) {
-                    const uint64_t b_desc = make_smem_desc(sc + kk * 32, 16, 1024, kLayoutSW128);
-                    const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
-                    // X^T: two 64-column boxes per M = 128 half, LBO = box stride, SBO = 8 tokens
-                    umma_f16(tmem_base, make_smem_desc(sx + kk * 16 * 128, X_BOX, 1024, kLayoutSW128), b_desc,
-                             idesc, acc);
-                    if (two)
-                        umma_f16(tmem_base + 256, make_smem_desc(sx + 2 * X_BOX + kk * 16 * 128, X_BOX, 1024,
-                                                                 kLayoutSW128),
-                                 b_desc, idesc, acc);
+                    // X^T: two 64-column boxes, LBO = box stride, SBO = 8 tokens; Cs K-major SW128
+                    umma_f16(tmem_base, make_smem_desc(sx + kk * 16 * 128, X_BOX, 1024, kLayoutSW128),
+                             make_smem_desc(sx + X_BYTES + kk * 32, 16, 1024, kLayoutSW128), idesc,
+                             (i > 0 || kk > 0) ? 1u : 0u);
                 }
                 umma_commit(&empty[s]);
                 if (++s == stages) { s = 0; ph ^= 1; }
@@ -189,156 +239,174 @@ __global__ void __launch_bounds__(THREADS, 1) grad_mma_kernel(const __grid_const
             if (nkb > 0) umma_commit(tmem_full); else mbar_arrive(tmem_full);
         }
     } else {
-        // ---------------- converters: Cs[q, t] rows (hi / mid / lo at row0 + {0, 1, 2} r8 + k)
-        const int ct = static_cast<int>(threadIdx.x) - 64;   // 0..127
-        int k8 = 0;                                          // sum of r8 over the sets
-        for (int j = 0; j < J.nsets; ++j) k8 += J.set[j].r8;
-        const int tasks = k8 * (KB / 8);
-        // rows [3 k8, q_pad) pad N to a multiple of 16: zero once (the ring never overwrites them)
-        for (int e = ct; e < (q_pad - 3 * k8) * (KB / 8) * stages; e += 128) {
-            const int s = e / ((q_pad - 3 * k8) * (KB / 8));
-            const int rc = e - s * ((q_pad - 3 * k8) * (KB / 8));
-            *reinterpret_cast<uint4*>(smem + s * stage_bytes + X_BYTES +
-                                      swizzled_offset(3 * k8 + rc / (KB / 8), rc % (KB / 8), 128)) =
-                make_uint4(0, 0, 0, 0);
-        }
-        for (int i = 0, s = 0, ph = 0; i < nkb; ++i) {
-            mbar_wait(&loaded[s], ph);   // (the producer waited for this stage's MMAs before refilling)
-            uint8_t* sc = smem + s * stage_bytes + X_BYTES;
-            const float* sstg = reinterpret_cast<const float*>(sc + G.cs_bytes);
-            const int64_t t0 = static_cast<int64_t>(kb0 + i) * KB;
-            for (int e = ct; e < tasks; e += 128) {
-                const int c = e / k8;          // 8-token chunk
-                int kk = e - c * k8;           // index into the stacked sets
-                int j = 0, off = 0;
-                while (kk >= J.set[j].r8) { kk -= J.set[j].r8; off += 64 * J.set[j].r; ++j; }
-                const GradMmaSet& st = J.set[j];
-                float v[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const int tl = c * 8 + u;
-                    v[u] = (kk < st.r && t0 + tl < J.T) ? sstg[off + tl * st.r + kk] : 0.0f;
-                }
-                uint4 hi, mid, lo;
-                split8(v, hi, mid, lo);
-                *reinterpret_cast<uint4*>(sc + swizzled_offset(st.row0 + kk, c, 128)) = hi;
-                *reinterpret_cast<uint4*>(sc + swizzled_offset(st.row0 + st.r8 + kk, c, 128)) = mid;
-                *reinterpret_cast<uint4*>(sc + swizzled_offset(st.row0 + 2 * st.r8 + kk, c, 128)) = lo;
-            }
-            fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&full[s]);
-            if (++s == stages) { s = 0; ph ^= 1; }
-        }
-        // ---------------- epilogue: TMEM -> partial[kbase + k][column] (hi + mid + lo)
+        // ---------------- epilogue: TMEM -> (hi + mid + lo) -> global (S = 1) or partial (S > 1)
         mbar_wait(tmem_full, 0);
         tc_fence_after();
+        K3_STAMP(1);
         const int lq = static_cast<int>(warp & 3);          // TMEM lane quarter of this warp
-        for (int mt = 0; mt < 2; ++mt) {
-            const int cl = mt * 128 + lq * 32 + static_cast<int>(lane);
-            const uint32_t tbase = tmem_base + (static_cast<uint32_t>(lq * 32) << 16) + mt * 256;
-            int kbase = 0;
-            for (int j = 0; j < J.nsets; ++j) {
-                const GradMmaSet& st = J.set[j];
-                for (int k0 = 0; k0 < st.r8; k0 += 8) {
-                    uint32_t h[8], md[8], l[8];
-                    const bool live = nkb > 0 && (mt == 0 || two);
-                    if (live) {   // warp-uniform
-                        tmem_ld_32x32b_x8(tbase + st.row0 + k0, h);
-                        tmem_ld_32x32b_x8(tbase + st.row0 + st.r8 + k0, md);
-                        tmem_ld_32x32b_x8(tbase + st.row0 + 2 * st.r8 + k0, l);
-                        tmem_ld_wait();
-                    }
-#pragma unroll
-                    for (int u = 0; u < 8; ++u)
-                        if (k0 + u < st.r)
-                            partial[(kbase + k0 + u) * PST + cl] =
-                                live ? (__uint_as_float(h[u]) + __uint_as_float(md[u])) + __uint_as_float(l[u])
-                                     : 0.0f;
+        const int cl = lq * 32 + static_cast<int>(lane);    // column within the tile
+        const bool col_ok = col0 + cl < J.N;
+        const uint32_t tbase = tmem_base + (static_cast<uint32_t>(lq * 32) << 16);
+        int poff = 0;
+        for (int j = 0; j < J.nsets; ++j) {
+            const GradMmaSet& st = G.set[J.set0 + j];
+            const int r4p = (st.r + 3) / 4 * 4 + 4;
+            for (int k0 = 0; k0 < st.r8; k0 += 8) {
+                uint32_t h[8], md[8], l[8];
+                if (nkb > 0) {   // warp-uniform
+                    tmem_ld_32x32b_x8(tbase + st.row0 + k0, h);
+                    tmem_ld_32x32b_x8(tbase + st.row0 + st.r8 + k0, md);
+                    tmem_ld_32x32b_x8(tbase + st.row0 + 2 * st.r8 + k0, l);
+                    tmem_ld_wait();
                 }
-                kbase += st.r;
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int k = k0 + u;
+                    if (k >= st.r) break;
+                    const float v = nkb > 0
+                        ? (__uint_as_float(h[u]) + __uint_as_float(md[u])) + __uint_as_float(l[u]) : 0.0f;
+                    if (S == 1) {
+                        if (col_ok) {
+                            float* dst = st.out + (col0 + cl) * st.stride_col + static_cast<int64_t>(k) * st.stride_k;
+                            *dst = st.accumulate ? *dst + st.scale * v : st.scale * v;
+                        }
+                    } else if (st.stride_col == 1) {
+                        partial[poff + k * PA + cl] = v;
+                    } else {
+                        partial[poff + cl * r4p + k] = v;
+                    }
+                }
             }
+            poff += partial_floats(st);
         }
     }
     tc_fence_before();
+    if (warp == 2) K3_STAMP(2);
+    if (S == 1) {
+        __syncthreads();
+        if (warp == 1) {
+            tc_fence_after();
+            tmem_dealloc_n(tmem_base, G.tmem_cols);
+        }
+        K3_STAMP(3);
+        return;
+    }
     cluster.sync();   // all partials of the cluster written (release / acquire)
     if (warp == 1) {
         tc_fence_after();
-        tmem_dealloc<512>(tmem_base);
+        tmem_dealloc_n(tmem_base, G.tmem_cols);
     }
 
     // ---------------- cluster reduction in rank order; rank q owns a 1/S share
-    int kbase = 0;
+    int poff = 0;
     for (int j = 0; j < J.nsets; ++j) {
-        const GradMmaSet& st = J.set[j];
-        const int E = st.r * kGradMmaCols;
-        const int per = (E + S - 1) / S;
-        const int e0 = rank * per;
-        const int e1 = e0 + per < E ? e0 + per : E;
-        const bool col_fast = st.stride_col == 1;   // dA^T: store O[c, q] at out[q * N + c]
-        for (int e = e0 + static_cast<int>(threadIdx.x); e < e1; e += THREADS) {
-            int k, c;
-            if (col_fast) { k = e / kGradMmaCols; c = e - k * kGradMmaCols; }
-            else { c = e / st.r; k = e - c * st.r; }
+        const GradMmaSet& st = G.set[J.set0 + j];
+        const bool is_a = st.stride_col == 1;           // dA^T: O[c, k] at out[k * N + c]
+        const int r4p = (st.r + 3) / 4 * 4 + 4;
+        const bool vec = is_a || st.r % 4 == 0;
+        const int inner = is_a ? kGradMmaCols : st.r;   // output-contiguous extent
+        const int outer = is_a ? st.r : kGradMmaCols;
+        const int ld = is_a ? PA : r4p;
+        const int U = vec ? outer * (inner / 4) : outer * inner;
+        const int per = (U + S - 1) / S;
+        const int u0 = rank * per;
+        const int u1 = u0 + per < U ? u0 + per : U;
+        for (int u = u0 + static_cast<int>(threadIdx.x); u < u1; u += THREADS) {
+            int o, in;
+            if (vec) { o = u / (inner / 4); in = (u - o * (inner / 4)) * 4; }
+            else { o = u / inner; in = u - o * inner; }
+            const int c = is_a ? in : o, k = is_a ? o : in;
             if (col0 + c >= J.N) continue;
-            const int o = (kbase + k) * PST + c;
-            float sum = 0.0f;
-            for (int q = 0; q < S; ++q) sum += cluster.map_shared_rank(partial, q)[o];
-            sum *= st.scale;
+            const int off = poff + o * ld + in;
             float* dst = st.out + (col0 + c) * st.stride_col + static_cast<int64_t>(k) * st.stride_k;
-            *dst = st.accumulate ? *dst + sum : sum;
+            if (vec) {
+                float4 v[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    if (q < S) v[q] = *reinterpret_cast<const float4*>(cluster.map_shared_rank(partial + off, q));
+                float4 sum = v[0];
+#pragma unroll
+                for (int q = 1; q < 8; ++q)
+                    if (q < S) { sum.x += v[q].x; sum.y += v[q].y; sum.z += v[q].z; sum.w += v[q].w; }
+                sum.x *= st.scale; sum.y *= st.scale; sum.z *= st.scale; sum.w *= st.scale;
+                float4* d4 = reinterpret_cast<float4*>(dst);
+                if (st.accumulate) {
+                    const float4 o4 = *d4;
+                    sum.x += o4.x; sum.y += o4.y; sum.z += o4.z; sum.w += o4.w;
+                }
+                *d4 = sum;
+            } else {
+                float v[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    if (q < S) v[q] = *cluster.map_shared_rank(partial + off, q);
+                float sum = v[0];
+#pragma unroll
+                for (int q = 1; q < 8; ++q)
+                    if (q < S) sum += v[q];
+                sum *= st.scale;
+                *dst = st.accumulate ? *dst + sum : sum;
+            }
         }
-        kbase += st.r;
+        poff += partial_floats(st);
     }
+    K3_STAMP(3);
     cluster.sync();   // peers may still read this CTA's partial
 }
 
-int grad_mma_cluster_size(int tiles, int kb_total, int num_sms) {
-    // minimise waves / S (per-CTA work ~ 1 / S); ties -> smaller S
+// Token split S (cluster size): minimise waves x (k-blocks per CTA + a fixed
+// cost of ~6 k-blocks for prologue, epilogue and reduction); ties -> smaller S.
+int grad_mma_cluster_size(int tiles, int kb_total, int slots) {
     int best = 1;
-    double best_cost = 1e30;
+    long best_cost = -1;
     for (int S = 1; S <= 8 && S <= kb_total; ++S) {
-        const int waves = (tiles * S + num_sms - 1) / num_sms;
-        const double cost = static_cast<double>(waves) / S + 1e-3 * S;
-        if (cost < best_cost - 1e-9) { best_cost = cost; best = S; }
+        const long waves = (static_cast<long>(tiles) * S + slots - 1) / slots;
+        const long cost = waves * ((kb_total + S - 1) / S + 6);
+        if (best_cost < 0 || cost < best_cost) { best_cost = cost; best = S; }
     }
     return best;
 }
 
 cudaError_t launch_grad_mma(GradMmaGroup& G, int num_sms, cudaStream_t stream) {
     if (G.njobs < 1 || G.njobs > kMaxGradJobs) return cudaErrorInvalidValue;
-    int tiles = 0, qmax = 16, rsum_max = 0, kb_max = 1;
+    int tiles = 0, qmax = 16, pmax = 0, kb_max = 1;
     for (int jb = 0; jb < G.njobs; ++jb) {
-        const GradMmaJob& J = G.job[jb];
-        if (J.q_pad < 16 || J.q_pad > 256 || J.q_pad % 16 != 0) return cudaErrorInvalidValue;
+        GradMmaJob& J = G.job[jb];
+        if (J.q_pad < 16 || J.q_pad > 256 || J.q_pad % 16 != 0 || J.q_used > J.q_pad) return cudaErrorInvalidValue;
         G.tile_start[jb] = tiles;
         tiles += static_cast<int>((J.N + kGradMmaCols - 1) / kGradMmaCols);
         qmax = J.q_pad > qmax ? J.q_pad : qmax;
-        int rs = 0;
-        for (int j = 0; j < J.nsets; ++j) rs += J.set[j].r;
-        rsum_max = rs > rsum_max ? rs : rsum_max;
+        int pf = 0;
+        for (int j = 0; j < J.nsets; ++j) pf += partial_floats(G.set[J.set0 + j]);
+        pmax = pf > pmax ? pf : pmax;
         const int kb = static_cast<int>((J.T + KB - 1) / KB);
         kb_max = kb > kb_max ? kb : kb_max;
     }
     G.tile_start[G.njobs] = tiles;
     if (tiles == 0) return cudaSuccess;
-    G.cs_bytes = (qmax * 128 + 1023) / 1024 * 1024;
-    G.stage_bytes = X_BYTES + G.cs_bytes + (rsum_max * 256 + 1023) / 1024 * 1024;
-    const int partial_bytes = rsum_max * PST * 4;
+    G.stage_bytes = X_BYTES + (qmax * 128 + 1023) / 1024 * 1024;
+    G.tmem_cols = 32;
+    while (G.tmem_cols < qmax) G.tmem_cols *= 2;
     const int fixed = 1024 /* barriers */ + 1024 /* alignment */;
-    int stages = (SMEM_LIMIT - fixed) / G.stage_bytes;
+    // two CTAs per SM when at least 3 stages fit in half the shared memory
+    int per_sm = 2;
+    int stages = (SMEM_SM / 2 - 1024 - fixed) / G.stage_bytes;
+    if (stages < 3) {
+        per_sm = 1;
+        stages = (SMEM_CTA_MAX - fixed) / G.stage_bytes;
+    }
     stages = stages > MAX_STAGES ? MAX_STAGES : stages;
     if (stages < 2) return cudaErrorInvalidValue;
     G.stages = stages;
+    G.S = grad_mma_cluster_size(tiles, kb_max, per_sm * num_sms);
     int region = stages * G.stage_bytes;
-    region = region > partial_bytes ? region : partial_bytes;
+    const int pbytes = G.S > 1 ? pmax * 4 : 0;
+    region = region > pbytes ? region : pbytes;
     G.region_bytes = (region + 1023) / 1024 * 1024;
-    if (G.region_bytes + fixed > SMEM_LIMIT) return cudaErrorInvalidValue;
-    G.S = grad_mma_cluster_size(tiles, kb_max, num_sms);
+    if (G.region_bytes + fixed > SMEM_CTA_MAX) return cudaErrorInvalidValue;
     const int smem = G.region_bytes + fixed;
     cudaError_t e = cudaFuncSetAttribute(grad_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    if (G.S > 8) return cudaErrorInvalidValue;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(tiles, G.S);
     cfg.blockDim = dim3(THREADS);

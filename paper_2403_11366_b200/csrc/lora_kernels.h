@@ -83,6 +83,8 @@ struct GradArgs {
     int strips_a;             // (strip kernels) CTAs [0, strips_a) own dA strips
     float scale_b;            // s
     int accumulate;
+    __nv_bfloat16* cs_a;      // tensor-core K3: split gh [3 r8, T_pad] (workspace)
+    __nv_bfloat16* cs_b;      // tensor-core K3: split h  [3 r8, T_pad] (workspace)
 };
 // several problems of the same rank bucket in one K3 launch
 struct GradGroup {
@@ -92,33 +94,51 @@ struct GradGroup {
     int count;
 };
 // K3 on the tensor cores (default): O[c, q] = scale * sum_t X[t, c] C[t, q].
-// A JOB is one bf16 activation X [T, N] (TMA map, box {64 columns, 64 tokens},
-// SWIZZLE_128B) with up to kMaxGradSets coefficient SETS stacked along the MMA
-// N dimension (set j occupies rows [row0, row0 + 3 r8): hi, mid, lo).
-constexpr int kGradMmaCols = 256;   // X columns per CTA
-constexpr int kMaxGradSets = 8;
+// A JOB is one bf16 activation X [T, N] (xmap: box {64 columns, 64 tokens},
+// SWIZZLE_128B) with the coefficient SETS stacked along the MMA N dimension:
+// set j occupies B-operand rows [row0, row0 + 3 r8) (hi, mid, lo), loaded by
+// TMA from its split array Cs [3 r8, T_pad] bf16 (csmap: box {64 tokens,
+// 3 r8 rows}, SWIZZLE_128B) that K3s wrote.
+constexpr int kGradMmaCols = 128;      // X columns per CTA (MMA M)
 constexpr int kMaxGradJobs = 16;
+constexpr int kMaxGradSetsTotal = 16;
 struct GradMmaSet {
-    const float* coef;          // C [T, r] fp32 row-major
     float* out;                 // O[c, k] at out[c * stride_col + k * stride_k]
     int64_t stride_col, stride_k;
     int r, r8, row0, accumulate;
     float scale;
 };
 struct GradMmaJob {
-    CUtensorMap x;
     int64_t T, N;
-    int nsets, q_pad;           // q_pad = roundup(3 * sum r8, 16) (MMA N, <= 256)
-    GradMmaSet set[kMaxGradSets];
+    int set0, nsets;            // sets [set0, set0 + nsets) of the group
+    int q_used, q_pad;          // q_used = 3 sum r8; q_pad = roundup(q_used, 16) (MMA N, <= 256)
 };
 struct GradMmaGroup {
+    CUtensorMap xmap[kMaxGradJobs];
+    CUtensorMap csmap[kMaxGradSetsTotal];
+    GradMmaSet set[kMaxGradSetsTotal];
     GradMmaJob job[kMaxGradJobs];
     int tile_start[kMaxGradJobs + 1];
     int njobs;
-    int S, stages, stage_bytes, cs_bytes, region_bytes;   // filled in by launch_grad_mma
+    // filled in by launch_grad_mma
+    int S, stages, stage_bytes, region_bytes, tmem_cols;
 };
 cudaError_t launch_grad_mma(GradMmaGroup& G, int num_sms, cudaStream_t stream);
-int grad_mma_cluster_size(int tiles, int kb_total, int num_sms);
+int grad_mma_cluster_size(int tiles, int kb_total, int slots);
+
+// K3s: cs [3 r8, T_pad] bf16 = exact hi / mid / lo split of coef [T, r] fp32
+// (rows k, r8 + k, 2 r8 + k; zero for k >= r and tokens >= T).
+struct CoefSplitArgs {
+    const float* coef;
+    __nv_bfloat16* cs;
+    int64_t T, T_pad;
+    int r, r8;
+};
+struct CoefSplitGroup {
+    CoefSplitArgs s[kMaxGradSetsTotal];
+    int count;
+};
+cudaError_t launch_coef_split(const CoefSplitGroup& G, cudaStream_t stream);
 
 GradArgs make_grad_args(int64_t T, int64_t n, int64_t m, int r, float scale, const __nv_bfloat16* x,
                         const float* gh, const __nv_bfloat16* dy, const float* h, float* da, float* db,
