@@ -33,6 +33,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 
 #include "lora_kernels.h"
 #include "sm100_ptx.cuh"
@@ -76,8 +78,12 @@ __device__ __host__ __forceinline__ int partial_floats(const GradMmaSet& st) {
 // timing experiment only: per-CTA globaltimer stamps (start, main loop done,
 // partial written, reduction done)
 __device__ unsigned long long lora_k3_probe[16384 * 4];
-extern "C" int lora_probe_k3_read(unsigned long long* host, int n) {
-    return static_cast<int>(cudaMemcpyFromSymbol(host, lora_k3_probe, sizeof(unsigned long long) * n));
+extern "C" int lora_probe_k3_read(unsigned long long* host, int n) {   // read, then clear
+    cudaError_t e = cudaMemcpyFromSymbol(host, lora_k3_probe, sizeof(unsigned long long) * n);
+    void* p = nullptr;
+    if (e == cudaSuccess) e = cudaGetSymbolAddress(&p, lora_k3_probe);
+    if (e == cudaSuccess) e = cudaMemset(p, 0, sizeof(lora_k3_probe));
+    return static_cast<int>(e);
 }
 #define K3_STAMP(i)                                                                                   \
     do {                                                                                              \
@@ -356,11 +362,14 @@ __global__ void __launch_bounds__(THREADS, 1) grad_mma_kernel(const __grid_const
 
 // Token split S (cluster size): minimise waves x (k-blocks per CTA + a fixed
 // cost of ~6 k-blocks for prologue, epilogue and reduction); ties -> smaller S.
-int grad_mma_cluster_size(int tiles, int kb_total, int slots) {
+// slots[S] = CTAs of cluster size S that can be co-resident (cluster
+// placement within GPCs makes this smaller than CTAs-per-SM x SMs for S > 1).
+int grad_mma_cluster_size(int tiles, int kb_total, const int* slots) {
     int best = 1;
     long best_cost = -1;
     for (int S = 1; S <= 8 && S <= kb_total; ++S) {
-        const long waves = (static_cast<long>(tiles) * S + slots - 1) / slots;
+        if (slots[S] <= 0) continue;
+        const long waves = (static_cast<long>(tiles) * S + slots[S] - 1) / slots[S];
         const long cost = waves * ((kb_total + S - 1) / S + 6);
         if (best_cost < 0 || cost < best_cost) { best_cost = cost; best = S; }
     }
@@ -391,34 +400,71 @@ cudaError_t launch_grad_mma(GradMmaGroup& G, int num_sms, cudaStream_t stream) {
     // two CTAs per SM when at least 3 stages fit in half the shared memory
     int per_sm = 2;
     int stages = (SMEM_SM / 2 - 1024 - fixed) / G.stage_bytes;
+#ifdef LORA_K3_ONE_PER_SM
+    stages = 0;   // experiment: one CTA per SM, deep ring
+#endif
     if (stages < 3) {
         per_sm = 1;
         stages = (SMEM_CTA_MAX - fixed) / G.stage_bytes;
     }
     stages = stages > MAX_STAGES ? MAX_STAGES : stages;
+#ifdef LORA_K3_STAGES
+    stages = stages > LORA_K3_STAGES ? LORA_K3_STAGES : stages;
+#endif
     if (stages < 2) return cudaErrorInvalidValue;
     G.stages = stages;
-    G.S = grad_mma_cluster_size(tiles, kb_max, per_sm * num_sms);
     int region = stages * G.stage_bytes;
-    const int pbytes = G.S > 1 ? pmax * 4 : 0;
-    region = region > pbytes ? region : pbytes;
+    region = region > pmax * 4 ? region : pmax * 4;   // (the partial only matters for S > 1)
     G.region_bytes = (region + 1023) / 1024 * 1024;
     if (G.region_bytes + fixed > SMEM_CTA_MAX) return cudaErrorInvalidValue;
     const int smem = G.region_bytes + fixed;
     cudaError_t e = cudaFuncSetAttribute(grad_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
+    if (smem > SMEM_SM / 2 - 1024) per_sm = 1;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(tiles, G.S);
     cfg.blockDim = dim3(THREADS);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 1;
-    attr[0].val.clusterDim.y = G.S;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    // co-resident CTAs per cluster size (cached per smem size and device)
+    static thread_local int cache_smem = -1, cache_dev = -1, slots[9];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cache_smem != smem || cache_dev != dev) {
+        slots[0] = 0;
+        slots[1] = per_sm * num_sms;
+        for (int S = 2; S <= 8; ++S) {
+            attr[0].val.clusterDim.y = S;
+            cfg.gridDim = dim3(1, S);
+            int nc = 0;
+            if (cudaOccupancyMaxActiveClusters(&nc, grad_mma_kernel, &cfg) != cudaSuccess) {
+                cudaGetLastError();
+                nc = 0;
+            }
+            slots[S] = nc * S;
+        }
+        // measured on B200: CTA pairs pack two per SM like single CTAs (the
+        // occupancy query reports one); S >= 3 clusters do not (query kept)
+        slots[2] = slots[2] > slots[1] ? slots[2] : slots[1];
+        cache_smem = smem;
+        cache_dev = dev;
+    }
+    G.S = grad_mma_cluster_size(tiles, kb_max, slots);
+    if (const char* fs = getenv("LORA_K3_S")) {   // experiments: force the token split
+        const int v = atoi(fs);
+        if (v >= 1 && v <= 8) G.S = v;
+    }
+    if (getenv("LORA_K3_DEBUG"))
+        printf("K3: tiles %d kb %d smem %d stages %d per_sm %d slots %d %d %d %d %d %d %d %d -> S = %d\n", tiles,
+               kb_max, smem, stages, per_sm, slots[1], slots[2], slots[3], slots[4], slots[5], slots[6], slots[7],
+               slots[8], G.S);
+    cfg.gridDim = dim3(tiles, G.S);
+    attr[0].val.clusterDim.y = G.S;
     e = cudaLaunchKernelEx(&cfg, grad_mma_kernel, G);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();

@@ -124,7 +124,7 @@ struct GradMmaGroup {
     int S, stages, stage_bytes, region_bytes, tmem_cols;
 };
 cudaError_t launch_grad_mma(GradMmaGroup& G, int num_sms, cudaStream_t stream);
-int grad_mma_cluster_size(int tiles, int kb_total, int slots);
+int grad_mma_cluster_size(int tiles, int kb_total, const int* slots /* [9], by cluster size */);
 
 // K3s: cs [3 r8, T_pad] bf16 = exact hi / mid / lo split of coef [T, r] fp32
 // (rows k, r8 + k, 2 r8 + k; zero for k >= r and tokens >= T).

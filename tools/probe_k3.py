@@ -18,7 +18,8 @@ OUT = os.path.join(ROOT, "build", "probe")
 
 VARIANTS = {
     "k3probe": ("LORA_PROBE_K3",),
-    "k3noconv": ("LORA_PROBE_K3", "LORA_PROBE_K3_NOCONV"),
+    "k3one": ("LORA_PROBE_K3", "LORA_K3_ONE_PER_SM"),
+    "k3st3": ("LORA_PROBE_K3", "LORA_K3_STAGES=3"),
 }
 EXTRA = json.loads(os.environ.get("PROBE_VARIANTS", "{}"))
 VARIANTS.update({k: tuple(v) for k, v in EXTRA.items()})
@@ -59,12 +60,16 @@ def one(T, n, ms, r, iters=20):
     flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)
     fn = getattr(L.lib, "lora_probe_k3_read", None)
     buf = (ctypes.c_ulonglong * (16384 * 4))()
+    if fn is not None:
+        fn(buf, 16384 * 4)   # clear stamps of earlier launches
     phases = []
     for it in range(iters):
         flush.fill_(float(it))
         torch.cuda.synchronize()
         L.lora_linear_bwd_grouped(probs, [16.0] * len(probs), outs=outs)
         torch.cuda.synchronize()
+        if fn is not None and it < 3:
+            fn(buf, 16384 * 4)
         if fn is not None and it >= 3:
             fn(buf, 16384 * 4)
             v = np.array(buf, dtype=np.uint64).reshape(-1, 4)
@@ -81,9 +86,6 @@ def one(T, n, ms, r, iters=20):
                 epi_us=float(np.median(v[:, 2] - v[:, 1])) / 1e3,
                 red_us=float(np.median(v[:, 3] - v[:, 2])) / 1e3,
             ))
-            buf = (ctypes.c_ulonglong * (16384 * 4))()
-            ctypes.memset(buf, 0, ctypes.sizeof(buf))
-            torch.cuda.synchronize()
     if not phases:
         return {}
     keys = phases[0].keys()
