@@ -56,6 +56,23 @@ def _load():
             ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_double,
             _u16p, _u16p, _u16p, _f64p]
         lib.oracle_lora_merge.restype = ctypes.c_int
+        _u8p = ctypes.POINTER(ctypes.c_uint8)
+        lib.oracle_lora_fwd_dropout.argtypes = [
+            ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_double,
+            _u16p, _u16p, _u16p, _u16p, _u16p, _u8p, ctypes.c_double, _i64p, ctypes.c_int64, _f64p, _f64p]
+        lib.oracle_lora_fwd_dropout.restype = ctypes.c_int
+        lib.oracle_lora_bwd_dropout.argtypes = [
+            ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_double,
+            _u16p, _u16p, _u16p, _u16p, _u16p, _u8p, ctypes.c_double, _i64p, ctypes.c_int64,
+            _f64p, _f64p, _f64p, _f64p]
+        lib.oracle_lora_bwd_dropout.restype = ctypes.c_int
+        lib.oracle_philox4x32_10.argtypes = [ctypes.POINTER(ctypes.c_uint32)] * 3
+        lib.oracle_philox4x32_10.restype = None
+        lib.oracle_dropout_threshold.argtypes = [ctypes.c_float]
+        lib.oracle_dropout_threshold.restype = ctypes.c_uint32
+        lib.oracle_dropout_mask.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_float, ctypes.c_uint64,
+                                            ctypes.c_uint64, _u8p]
+        lib.oracle_dropout_mask.restype = ctypes.c_int
         lib.oracle_scale.argtypes = [ctypes.c_int, ctypes.c_double]
         lib.oracle_scale.restype = ctypes.c_double
         lib.oracle_num_threads.restype = ctypes.c_int
@@ -93,12 +110,46 @@ def scale(r: int, alpha: float) -> float:
     return _load().oracle_scale(int(r), float(alpha))
 
 
-def lora_fwd(x, w0, a, b, alpha, bias=None, rows=None):
+def philox4x32_10(ctr, key):
+    """Philox4x32-10 block (Salmon et al., SC'11) -> 4 uint32 words."""
+    c = (ctypes.c_uint32 * 4)(*[int(v) & 0xFFFFFFFF for v in ctr])
+    k = (ctypes.c_uint32 * 2)(*[int(v) & 0xFFFFFFFF for v in key])
+    o = (ctypes.c_uint32 * 4)()
+    _load().oracle_philox4x32_10(c, k, o)
+    return tuple(int(v) for v in o)
+
+
+def dropout_threshold(p: float) -> int:
+    """floor(p 2^32) for the fp32 dropout probability p (keep iff word >= it)."""
+    return int(_load().oracle_dropout_threshold(float(np.float32(p))))
+
+
+def dropout_mask(T: int, n: int, p: float, seed: int, offset: int) -> np.ndarray:
+    """LoRA-dropout keep mask M [T, n] uint8 (Listing 3 LORA_DROPOUT, PAPER.md:82;
+    DESIGN.md R9): M[t,k] = Philox4x32-10((k/4, t, offset), seed)[k % 4] >= floor(p 2^32)."""
+    mask = np.empty((T, n), np.uint8)
+    rc = _load().oracle_dropout_mask(int(T), int(n), float(np.float32(p)), int(seed) & (2**64 - 1),
+                                     int(offset) & (2**64 - 1), mask.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)))
+    if rc != 0:
+        raise ValueError(f"oracle_dropout_mask failed rc={rc}")
+    return mask
+
+
+def _dropout_args(dropout, T, n):
+    """dropout = (p, seed, offset) -> (mask [T, n] uint8, q = 1 / (1 - p)); p is taken as fp32."""
+    p, seed, offset = dropout
+    p32 = float(np.float32(p))
+    mask = dropout_mask(T, n, p32, seed, offset)
+    return mask, 1.0 / (1.0 - p32)
+
+
+def lora_fwd(x, w0, a, b, alpha, bias=None, rows=None, dropout=None):
     """Eq. 1 line 1: y = x W0^T + s (x A^T) B^T (+ b0).
 
     All tensor arguments are bf16 bit patterns (uint16).  ``rows`` selects the
-    tokens to evaluate (None: all).  Returns (y [n_rows, m], h [n_rows, r]) in
-    float64.
+    tokens to evaluate (None: all).  ``dropout = (p, seed, offset)`` applies
+    LoRA dropout to the adapter input (R9).  Returns (y [n_rows, m],
+    h [n_rows, r]) in float64.
     """
     T, n = x.shape
     m, r = b.shape
@@ -110,15 +161,21 @@ def lora_fwd(x, w0, a, b, alpha, bias=None, rows=None):
     rs, rp, nr = _rows(rows, T)
     y = np.empty((nr, m), np.float64)
     h = np.empty((nr, r), np.float64)
-    rc = _load().oracle_lora_fwd(T, n, m, r, float(alpha), xp, wp, ap, bp, bip, rp, nr,
-                                 y.ctypes.data_as(_f64p), h.ctypes.data_as(_f64p))
+    if dropout is None:
+        rc = _load().oracle_lora_fwd(T, n, m, r, float(alpha), xp, wp, ap, bp, bip, rp, nr,
+                                     y.ctypes.data_as(_f64p), h.ctypes.data_as(_f64p))
+    else:
+        mask, q = _dropout_args(dropout, T, n)
+        rc = _load().oracle_lora_fwd_dropout(T, n, m, r, float(alpha), xp, wp, ap, bp, bip,
+                                             mask.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)), q, rp, nr,
+                                             y.ctypes.data_as(_f64p), h.ctypes.data_as(_f64p))
     if rc != 0:
         raise ValueError(f"oracle_lora_fwd failed rc={rc}")
     return y, h
 
 
-def lora_bwd(x, w0, a, b, dy, alpha, rows=None, want_dx=True):
-    """Backward of Eq. 1 for A, B trainable.
+def lora_bwd(x, w0, a, b, dy, alpha, rows=None, want_dx=True, dropout=None):
+    """Backward of Eq. 1 for A, B trainable; ``dropout`` as in lora_fwd.
 
     Returns dict with dx [n_rows, n] (or None), gh [T, r], da [r, n], db [m, r]
     in float64.
@@ -133,10 +190,15 @@ def lora_bwd(x, w0, a, b, dy, alpha, rows=None, want_dx=True):
     gh = np.empty((T, r), np.float64)
     da = np.empty((r, n), np.float64)
     db = np.empty((m, r), np.float64)
-    rc = _load().oracle_lora_bwd(
-        T, n, m, r, float(alpha), xp, wp, ap, bp, gp, rp, nr,
-        dx.ctypes.data_as(_f64p) if dx is not None else None,
-        gh.ctypes.data_as(_f64p), da.ctypes.data_as(_f64p), db.ctypes.data_as(_f64p))
+    outs = (dx.ctypes.data_as(_f64p) if dx is not None else None,
+            gh.ctypes.data_as(_f64p), da.ctypes.data_as(_f64p), db.ctypes.data_as(_f64p))
+    if dropout is None:
+        rc = _load().oracle_lora_bwd(T, n, m, r, float(alpha), xp, wp, ap, bp, gp, rp, nr, *outs)
+    else:
+        mask, q = _dropout_args(dropout, T, n)
+        rc = _load().oracle_lora_bwd_dropout(T, n, m, r, float(alpha), xp, wp, ap, bp, gp,
+                                             mask.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)), q, rp, nr,
+                                             *outs)
     if rc != 0:
         raise ValueError(f"oracle_lora_bwd failed rc={rc}")
     return {"dx": dx, "gh": gh, "da": da, "db": db}

@@ -29,6 +29,19 @@
  * Merge (Eq. 1, second line; PAPER.md:92-106 export script):
  *   W'[i,k] = W0[i,k] + s sum_j B[i,j] A[j,k]
  *
+ * LoRA dropout (Listing 3, LORA_DROPOUT = 0.05; placement per
+ * DESIGN.md reading R9: inverted dropout on the adapter input only, the
+ * frozen path never sees it): with keep mask M[t,k] in {0,1} and
+ * q = 1/(1-p),  xd[t,k] = q M[t,k] x[t,k]  replaces x in "A x":
+ *   h[t,j]  = sum_k xd[t,k] A[j,k]
+ *   dX[t,k] = sum_i G[t,i] W0[i,k] + q M[t,k] sum_j gh[t,j] A[j,k]
+ *   dA[j,k] = sum_t gh[t,j] xd[t,k]          (y, gh, dB unchanged given h)
+ * M is a pure function of (t, k, seed, offset, p) through Philox4x32-10
+ * (Salmon et al., SC'11), so the backward regenerates it:
+ *   (w0..w3) = Philox4x32-10(counter = (k/4, t, offset_lo, offset_hi),
+ *                            key = (seed_lo, seed_hi));
+ *   M[t,k] = (w_{k mod 4} >= floor(p 2^32)).
+ *
  * Arithmetic: every input is a bf16 bit pattern ("brain
  * floating point"), widened exactly to double; every sum is accumulated in
  * double in ascending index order, exactly as written above.  OpenMP only
@@ -85,26 +98,33 @@ static int64_t row_of(const int64_t* rows, int64_t q) { return rows ? rows[q] : 
  * bias may be NULL (Llama-2 projections have none).  Returns 0, or -1 on bad
  * arguments.
  */
-int oracle_lora_fwd(int64_t T, int64_t n, int64_t m, int r, double alpha,
-                    const uint16_t* x, const uint16_t* w0, const uint16_t* a,
-                    const uint16_t* b, const uint16_t* bias,
-                    const int64_t* rows, int64_t n_rows,
-                    double* y_out, double* h_out) {
+/* adapter input xd[t,k] of the dropout reading (mask == NULL: x itself) */
+static double xin(const uint16_t* x, const uint8_t* mask, double q, int64_t idx) {
+    if (!mask) return bf(x[idx]);
+    return mask[idx] ? q * bf(x[idx]) : 0.0;
+}
+
+static int lora_fwd_impl(int64_t T, int64_t n, int64_t m, int r, double alpha,
+                         const uint16_t* x, const uint16_t* w0, const uint16_t* a,
+                         const uint16_t* b, const uint16_t* bias,
+                         const uint8_t* mask, double q,
+                         const int64_t* rows, int64_t n_rows,
+                         double* y_out, double* h_out) {
     if (bad_dims(T, n, m, r) || !x || !w0 || !a || !b || !y_out) return -1;
     if (!rows && n_rows != T) return -1;
     const double s = oracle_scale(r, alpha);
-    int64_t q;
+    int64_t qq;
 #pragma omp parallel for schedule(dynamic, 1)
-    for (q = 0; q < n_rows; ++q) {
-        const int64_t t = row_of(rows, q);
+    for (qq = 0; qq < n_rows; ++qq) {
+        const int64_t t = row_of(rows, qq);
         const uint16_t* xt = x + t * n;
         double* h = (double*)malloc(sizeof(double) * (size_t)r);
-        /* h[t,j] = sum_k x[t,k] A[j,k]  -- "A x" of Eq. 1 */
+        /* h[t,j] = sum_k x[t,k] A[j,k]  -- "A x" of Eq. 1 (xd under dropout) */
         for (int j = 0; j < r; ++j) {
             double acc = 0.0;
-            for (int64_t k = 0; k < n; ++k) acc += bf(xt[k]) * bf(a[(int64_t)j * n + k]);
+            for (int64_t k = 0; k < n; ++k) acc += xin(x, mask, q, t * n + k) * bf(a[(int64_t)j * n + k]);
             h[j] = acc;
-            if (h_out) h_out[q * r + j] = acc;
+            if (h_out) h_out[qq * r + j] = acc;
         }
         for (int64_t i = 0; i < m; ++i) {
             /* base term W0 x */
@@ -116,11 +136,30 @@ int oracle_lora_fwd(int64_t T, int64_t n, int64_t m, int r, double alpha,
             for (int j = 0; j < r; ++j) lora += h[j] * bf(b[i * r + j]);
             double v = base + s * lora;
             if (bias) v += bf(bias[i]);
-            y_out[q * m + i] = v;
+            y_out[qq * m + i] = v;
         }
         free(h);
     }
     return 0;
+}
+
+int oracle_lora_fwd(int64_t T, int64_t n, int64_t m, int r, double alpha,
+                    const uint16_t* x, const uint16_t* w0, const uint16_t* a,
+                    const uint16_t* b, const uint16_t* bias,
+                    const int64_t* rows, int64_t n_rows,
+                    double* y_out, double* h_out) {
+    return lora_fwd_impl(T, n, m, r, alpha, x, w0, a, b, bias, NULL, 1.0, rows, n_rows, y_out, h_out);
+}
+
+/* Forward with LoRA dropout: mask [T, n] of 0/1, q = 1 / (1 - p). */
+int oracle_lora_fwd_dropout(int64_t T, int64_t n, int64_t m, int r, double alpha,
+                            const uint16_t* x, const uint16_t* w0, const uint16_t* a,
+                            const uint16_t* b, const uint16_t* bias,
+                            const uint8_t* mask, double q,
+                            const int64_t* rows, int64_t n_rows,
+                            double* y_out, double* h_out) {
+    if (!mask) return -1;
+    return lora_fwd_impl(T, n, m, r, alpha, x, w0, a, b, bias, mask, q, rows, n_rows, y_out, h_out);
 }
 
 /*
@@ -131,11 +170,12 @@ int oracle_lora_fwd(int64_t T, int64_t n, int64_t m, int r, double alpha,
  *   da_out : [r, n]   (nullable)        db_out : [m, r] (nullable)
  * dA and dB are reductions over all T tokens, so they always use every row.
  */
-int oracle_lora_bwd(int64_t T, int64_t n, int64_t m, int r, double alpha,
-                    const uint16_t* x, const uint16_t* w0, const uint16_t* a,
-                    const uint16_t* b, const uint16_t* dy,
-                    const int64_t* rows, int64_t n_rows,
-                    double* dx_out, double* gh_out, double* da_out, double* db_out) {
+static int lora_bwd_impl(int64_t T, int64_t n, int64_t m, int r, double alpha,
+                         const uint16_t* x, const uint16_t* w0, const uint16_t* a,
+                         const uint16_t* b, const uint16_t* dy,
+                         const uint8_t* mask, double q,
+                         const int64_t* rows, int64_t n_rows,
+                         double* dx_out, double* gh_out, double* da_out, double* db_out) {
     if (bad_dims(T, n, m, r) || !x || !w0 || !a || !b || !dy) return -1;
     if (dx_out && !rows && n_rows != T) return -1;
     const double s = oracle_scale(r, alpha);
@@ -148,7 +188,7 @@ int oracle_lora_bwd(int64_t T, int64_t n, int64_t m, int r, double alpha,
     for (t = 0; t < T; ++t) {
         for (int j = 0; j < r; ++j) {
             double acc = 0.0;
-            for (int64_t k = 0; k < n; ++k) acc += bf(x[t * n + k]) * bf(a[(int64_t)j * n + k]);
+            for (int64_t k = 0; k < n; ++k) acc += xin(x, mask, q, t * n + k) * bf(a[(int64_t)j * n + k]);
             h[t * r + j] = acc;
             double g = 0.0;
             for (int64_t i = 0; i < m; ++i) g += bf(dy[t * m + i]) * bf(b[i * r + j]);
@@ -160,10 +200,10 @@ int oracle_lora_bwd(int64_t T, int64_t n, int64_t m, int r, double alpha,
     /* dX[t,k] = sum_i G[t,i] W0[i,k] + sum_j gh[t,j] A[j,k]
      * (i-loop outside the k-loop: each dX[t,k] still sums i = 0..m-1 in order) */
     if (dx_out) {
-        int64_t q;
+        int64_t qq;
 #pragma omp parallel for schedule(dynamic, 1)
-        for (q = 0; q < n_rows; ++q) {
-            const int64_t tt = row_of(rows, q);
+        for (qq = 0; qq < n_rows; ++qq) {
+            const int64_t tt = row_of(rows, qq);
             double* base = (double*)calloc((size_t)n, sizeof(double));
             for (int64_t i = 0; i < m; ++i) {
                 const double g = bf(dy[tt * m + i]);
@@ -173,7 +213,8 @@ int oracle_lora_bwd(int64_t T, int64_t n, int64_t m, int r, double alpha,
             for (int64_t k = 0; k < n; ++k) {
                 double lora = 0.0;
                 for (int j = 0; j < r; ++j) lora += gh[tt * r + j] * bf(a[(int64_t)j * n + k]);
-                dx_out[q * n + k] = base[k] + lora;
+                if (mask) lora = mask[tt * n + k] ? q * lora : 0.0;   /* through the dropout */
+                dx_out[qq * n + k] = base[k] + lora;
             }
             free(base);
         }
@@ -185,7 +226,7 @@ int oracle_lora_bwd(int64_t T, int64_t n, int64_t m, int r, double alpha,
         for (k = 0; k < n; ++k) {
             for (int j = 0; j < r; ++j) {
                 double acc = 0.0;
-                for (int64_t tt = 0; tt < T; ++tt) acc += gh[tt * r + j] * bf(x[tt * n + k]);
+                for (int64_t tt = 0; tt < T; ++tt) acc += gh[tt * r + j] * xin(x, mask, q, tt * n + k);
                 da_out[(int64_t)j * n + k] = acc;
             }
         }
@@ -204,6 +245,74 @@ int oracle_lora_bwd(int64_t T, int64_t n, int64_t m, int r, double alpha,
     }
     free(h);
     free(gh);
+    return 0;
+}
+
+int oracle_lora_bwd(int64_t T, int64_t n, int64_t m, int r, double alpha,
+                    const uint16_t* x, const uint16_t* w0, const uint16_t* a,
+                    const uint16_t* b, const uint16_t* dy,
+                    const int64_t* rows, int64_t n_rows,
+                    double* dx_out, double* gh_out, double* da_out, double* db_out) {
+    return lora_bwd_impl(T, n, m, r, alpha, x, w0, a, b, dy, NULL, 1.0, rows, n_rows, dx_out, gh_out, da_out,
+                         db_out);
+}
+
+/* Backward with LoRA dropout (same mask and q as the forward). */
+int oracle_lora_bwd_dropout(int64_t T, int64_t n, int64_t m, int r, double alpha,
+                            const uint16_t* x, const uint16_t* w0, const uint16_t* a,
+                            const uint16_t* b, const uint16_t* dy,
+                            const uint8_t* mask, double q,
+                            const int64_t* rows, int64_t n_rows,
+                            double* dx_out, double* gh_out, double* da_out, double* db_out) {
+    if (!mask) return -1;
+    return lora_bwd_impl(T, n, m, r, alpha, x, w0, a, b, dy, mask, q, rows, n_rows, dx_out, gh_out, da_out,
+                         db_out);
+}
+
+/*
+ * Philox4x32-10 (Salmon, Moraes, Dror, Shaw, "Parallel random numbers: as
+ * easy as 1, 2, 3", SC'11): 10 rounds of
+ *   (c0, c1, c2, c3) <- (hi(M1 c2) ^ c1 ^ k0, lo(M1 c2), hi(M0 c0) ^ c3 ^ k1, lo(M0 c0))
+ * with the key bumped by (W0, W1) between rounds.
+ */
+void oracle_philox4x32_10(const uint32_t ctr_in[4], const uint32_t key_in[2], uint32_t out[4]) {
+    const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u, W0 = 0x9E3779B9u, W1 = 0xBB67AE85u;
+    uint32_t c[4] = {ctr_in[0], ctr_in[1], ctr_in[2], ctr_in[3]};
+    uint32_t k0 = key_in[0], k1 = key_in[1];
+    for (int round = 0; round < 10; ++round) {
+        if (round > 0) { k0 += W0; k1 += W1; }
+        const uint64_t p0 = (uint64_t)M0 * c[0];
+        const uint64_t p1 = (uint64_t)M1 * c[2];
+        const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c[1] ^ k0;
+        const uint32_t n1 = (uint32_t)p1;
+        const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c[3] ^ k1;
+        const uint32_t n3 = (uint32_t)p0;
+        c[0] = n0; c[1] = n1; c[2] = n2; c[3] = n3;
+    }
+    out[0] = c[0]; out[1] = c[1]; out[2] = c[2]; out[3] = c[3];
+}
+
+/* keep threshold: floor(p 2^32) for the fp32 dropout probability p in [0, 1) */
+uint32_t oracle_dropout_threshold(float p) {
+    const double v = (double)p * 4294967296.0;
+    return (uint32_t)v;   /* truncation == floor for v >= 0 */
+}
+
+/* M[t,k] in {0,1} for a [T, n] activation (header comment above). */
+int oracle_dropout_mask(int64_t T, int64_t n, float p, uint64_t seed, uint64_t offset, uint8_t* mask) {
+    if (T < 0 || n <= 0 || !(p >= 0.0f && p < 1.0f) || !mask) return -1;
+    const uint32_t thr = oracle_dropout_threshold(p);
+    const uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    int64_t t;
+#pragma omp parallel for schedule(static)
+    for (t = 0; t < T; ++t) {
+        for (int64_t k = 0; k < n; ++k) {
+            const uint32_t ctr[4] = {(uint32_t)(k / 4), (uint32_t)t, (uint32_t)offset, (uint32_t)(offset >> 32)};
+            uint32_t w[4];
+            oracle_philox4x32_10(ctr, key, w);
+            mask[t * n + k] = w[k % 4] >= thr ? 1 : 0;
+        }
+    }
     return 0;
 }
 
