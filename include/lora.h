@@ -112,6 +112,40 @@ lora_status lora_linear_bwd(const lora_dims* dims, const void* x, const void* w0
 lora_status lora_merge(const lora_dims* dims, const void* w0, const void* a,
                        const void* b, void* w_out, void* stream);
 
+/* ---------------- LoRA dropout (Listing 3 LORA_DROPOUT = 0.05) ----
+ * Inverted dropout on the ADAPTER input only (reading R9; the frozen
+ * path W0 x never sees it).  Keep mask M[t,k] in {0,1}, q = 1 / (1 - p):
+ *   y  = x W0^T + s (q (M . x) A^T) B^T (+ bias),   h = q (M . x) A^T
+ *   dX = dy W0 + q M . (gh A),   dA = q gh^T (M . x),   dB = s dy^T h
+ * M is a pure function of (t, k, seed, offset, p) -- Philox4x32-10 with
+ * counter (k/4, t, offset_lo, offset_hi) and key (seed_lo, seed_hi); element
+ * (t, k) is kept iff word k%4 >= floor(p * 2^32) -- so the backward, given
+ * the same lora_dropout, regenerates the forward's mask (nothing is stored).
+ * Use a fresh offset (or seed) per step and per linear.  p = 0 gives exactly
+ * the plain calls.  p must be in [0, 1) (LORA_ERR_INVALID otherwise). */
+typedef struct {
+    float p;          /* drop probability */
+    uint64_t seed;    /* Philox key */
+    uint64_t offset;  /* Philox counter high words: a stream per (step, linear) */
+} lora_dropout;
+
+/* As lora_linear_fwd, plus one launch (K0: h from the masked input). */
+size_t lora_linear_fwd_dropout_workspace_bytes(const lora_dims* dims);
+lora_status lora_linear_fwd_dropout(const lora_dims* dims, const lora_dropout* dropout,
+                                    const void* x, const void* w0, const void* a, const void* b,
+                                    const void* bias, void* y, float* h_out,
+                                    void* workspace, size_t workspace_bytes, void* stream);
+/* As lora_linear_bwd (h_saved must come from lora_linear_fwd_dropout with the
+ * same dropout, or NULL); the workspace also holds M . x [T, n] bf16. */
+size_t lora_linear_bwd_dropout_workspace_bytes(const lora_dims* dims);
+lora_status lora_linear_bwd_dropout(const lora_dims* dims, const lora_dropout* dropout,
+                                    const void* x, const void* w0, const void* a, const void* b,
+                                    const float* h_saved, const void* dy, void* dx, float* da, float* db,
+                                    int accumulate, void* workspace, size_t workspace_bytes, void* stream);
+/* The keep mask M [tokens, d_in] (uint8 0/1, device memory) the calls above use. */
+lora_status lora_dropout_mask(int64_t tokens, int64_t d_in, const lora_dropout* dropout, uint8_t* mask,
+                              void* stream);
+
 /* ---------------- Grouped calls: several independent LoRA linears ----------
  * Equivalent to `count` single calls (bitwise identical results), but the
  * fused tensor-core GEMMs of all problems whose rank falls in the same

@@ -54,6 +54,10 @@ class lora_bwd_problem(ctypes.Structure):
                 ("da", ctypes.c_void_p), ("db", ctypes.c_void_p)]
 
 
+class lora_dropout(ctypes.Structure):
+    _fields_ = [("p", ctypes.c_float), ("seed", ctypes.c_uint64), ("offset", ctypes.c_uint64)]
+
+
 LORA_MAX_GROUP = 8
 _vp = ctypes.c_void_p
 _fp = ctypes.c_void_p  # float* passed as raw address
@@ -68,6 +72,18 @@ lib.lora_linear_fwd.argtypes = [_dp, _vp, _vp, _vp, _vp, _vp, _vp, _fp, _vp, cty
 lib.lora_linear_fwd.restype = _st
 lib.lora_linear_bwd.argtypes = [_dp, _vp, _vp, _vp, _vp, _fp, _vp, _vp, _fp, _fp, ctypes.c_int,
                                 _vp, ctypes.c_size_t, _vp]
+_drp = ctypes.POINTER(lora_dropout)
+lib.lora_linear_fwd_dropout_workspace_bytes.argtypes = [_dp]
+lib.lora_linear_fwd_dropout_workspace_bytes.restype = ctypes.c_size_t
+lib.lora_linear_bwd_dropout_workspace_bytes.argtypes = [_dp]
+lib.lora_linear_bwd_dropout_workspace_bytes.restype = ctypes.c_size_t
+lib.lora_linear_fwd_dropout.argtypes = [_dp, _drp, _vp, _vp, _vp, _vp, _vp, _vp, _fp, _vp, ctypes.c_size_t, _vp]
+lib.lora_linear_fwd_dropout.restype = ctypes.c_int
+lib.lora_linear_bwd_dropout.argtypes = [_dp, _drp, _vp, _vp, _vp, _vp, _fp, _vp, _vp, _fp, _fp, ctypes.c_int,
+                                        _vp, ctypes.c_size_t, _vp]
+lib.lora_linear_bwd_dropout.restype = ctypes.c_int
+lib.lora_dropout_mask.argtypes = [ctypes.c_int64, ctypes.c_int64, _drp, _vp, _vp]
+lib.lora_dropout_mask.restype = ctypes.c_int
 lib.lora_linear_bwd.restype = _st
 lib.lora_linear_fwd_grouped_workspace_bytes.argtypes = [ctypes.c_int, _dp]
 lib.lora_linear_fwd_grouped_workspace_bytes.restype = ctypes.c_size_t
@@ -195,10 +211,26 @@ def lora_device_check() -> None:
     _check(lib.lora_device_check(), "lora_device_check")
 
 
+def _dropout(dropout):
+    """(p, seed, offset) -> lora_dropout (LoRA dropout; include/lora.h)."""
+    p, seed, offset = dropout
+    return lora_dropout(float(p), int(seed) & (2**64 - 1), int(offset) & (2**64 - 1))
+
+
+def lora_dropout_mask(T, n, dropout, device="cuda", stream=None):
+    """Keep mask M [T, n] uint8 of lora_linear_{fwd,bwd}(..., dropout=(p, seed, offset))."""
+    mask = torch.empty((T, n), dtype=torch.uint8, device=device)
+    dr = _dropout(dropout)
+    _check(lib.lora_dropout_mask(int(T), int(n), ctypes.byref(dr), _ptr(mask), _stream(stream)),
+           "lora_dropout_mask")
+    return mask
+
+
 def lora_linear_fwd(x, w0, a, b, alpha, bias=None, y=None, h_out=None, want_h=True,
-                    workspace=None, stream=None):
+                    workspace=None, stream=None, dropout=None):
     """Forward of Eq. 1.  x [T,n], w0 [m,n], a [r,n], b [m,r]
-    (bf16, CUDA).  Returns (y [T,m] bf16, h [T,r] fp32 or None)."""
+    (bf16, CUDA).  dropout = (p, seed, offset) applies LoRA dropout to the
+    adapter input.  Returns (y [T,m] bf16, h [T,r] fp32 or None)."""
     T, n = x.shape
     m, r = b.shape
     _bf16(x, "x", (T, n)); _bf16(w0, "w0", (m, n)); _bf16(a, "a", (r, n)); _bf16(b, "b", (m, r))
@@ -212,6 +244,14 @@ def lora_linear_fwd(x, w0, a, b, alpha, bias=None, y=None, h_out=None, want_h=Tr
     if h_out is not None:
         _f32(h_out, "h_out", (T, r))
     d = dims(T, n, m, r, alpha)
+    if dropout is not None:
+        need = int(lib.lora_linear_fwd_dropout_workspace_bytes(ctypes.byref(d)))
+        ws = workspace if workspace is not None else _workspace(need, x.device)
+        dr = _dropout(dropout)
+        st = lib.lora_linear_fwd_dropout(ctypes.byref(d), ctypes.byref(dr), _ptr(x), _ptr(w0), _ptr(a), _ptr(b),
+                                         _ptr(bias), _ptr(y), _ptr(h_out), _ptr(ws), ws.numel(), _stream(stream))
+        _check(st, "lora_linear_fwd_dropout")
+        return y, h_out
     need = lora_linear_fwd_workspace_bytes(d)
     ws = workspace if workspace is not None else _workspace(need, x.device)
     st = lib.lora_linear_fwd(ctypes.byref(d), _ptr(x), _ptr(w0), _ptr(a), _ptr(b), _ptr(bias),
@@ -221,8 +261,9 @@ def lora_linear_fwd(x, w0, a, b, alpha, bias=None, y=None, h_out=None, want_h=Tr
 
 
 def lora_linear_bwd(x, w0, a, b, dy, alpha, h_saved=None, want_dx=True, dx=None, da=None, db=None,
-                    accumulate=False, want_da=True, want_db=True, workspace=None, stream=None):
-    """Backward of Eq. 1.  Returns (dx [T,n] bf16 | None,
+                    accumulate=False, want_da=True, want_db=True, workspace=None, stream=None, dropout=None):
+    """Backward of Eq. 1; dropout as in lora_linear_fwd (same
+    (p, seed, offset) as the forward).  Returns (dx [T,n] bf16 | None,
     dA [r,n] fp32 | None, dB [m,r] fp32 | None)."""
     T, n = x.shape
     m, r = b.shape
@@ -243,6 +284,15 @@ def lora_linear_bwd(x, w0, a, b, dy, alpha, h_saved=None, want_dx=True, dx=None,
     if db is not None:
         _f32(db, "db", (m, r))
     d = dims(T, n, m, r, alpha)
+    if dropout is not None:
+        need = int(lib.lora_linear_bwd_dropout_workspace_bytes(ctypes.byref(d)))
+        ws = workspace if workspace is not None else _workspace(need, x.device)
+        dr = _dropout(dropout)
+        st = lib.lora_linear_bwd_dropout(ctypes.byref(d), ctypes.byref(dr), _ptr(x), _ptr(w0), _ptr(a), _ptr(b),
+                                         _ptr(h_saved), _ptr(dy), _ptr(dx), _ptr(da), _ptr(db),
+                                         1 if accumulate else 0, _ptr(ws), ws.numel(), _stream(stream))
+        _check(st, "lora_linear_bwd_dropout")
+        return dx, da, db
     need = lora_linear_bwd_workspace_bytes(d)
     ws = workspace if workspace is not None else _workspace(need, x.device)
     st = lib.lora_linear_bwd(ctypes.byref(d), _ptr(x), _ptr(w0), _ptr(a), _ptr(b), _ptr(h_saved),

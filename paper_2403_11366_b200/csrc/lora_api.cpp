@@ -164,20 +164,22 @@ static int cta_group_for(int64_t T) {
 // Forward workspace: B8 (B zero-padded to a multiple of 8 columns), used only
 // when r % 8 != 0 (sized unconditionally so it depends on dims alone).
 struct FwdWs {
-    size_t b8, total;
+    size_t b8, h, total;
 };
-static FwdWs fwd_ws(const lora_dims* d) {
+static FwdWs fwd_ws(const lora_dims* d, bool dropout = false) {
     FwdWs w;
     w.b8 = 0;
-    w.total = align256(size_t(d->d_out) * r8_of(d->rank) * 2);
+    w.h = align256(size_t(d->d_out) * r8_of(d->rank) * 2);
+    w.total = w.h;
+    if (dropout) w.total += align256(size_t(d->tokens > 0 ? d->tokens : 0) * d->rank * 4);   // K0's h
     return w;
 }
 
 // Backward workspace: B^T [r, m], gh [T, r] fp32, h [T, r] fp32 (when not saved).
 struct BwdWs {
-    size_t b8, gh, h, flags, cs_a, cs_b, total;
+    size_t b8, gh, h, flags, cs_a, cs_b, xm, total;
 };
-static BwdWs bwd_ws(const lora_dims* d) {
+static BwdWs bwd_ws(const lora_dims* d, bool dropout = false) {
     BwdWs w;
     const int64_t T = d->tokens > 0 ? d->tokens : 0;
     const int r = d->rank;
@@ -189,6 +191,8 @@ static BwdWs bwd_ws(const lora_dims* d) {
     const size_t cs = align256(size_t(3 * r8_of(r)) * size_t((T + 63) / 64 * 64) * 2);
     w.cs_a = off; off += cs;                                         // K3s: split gh
     w.cs_b = off; off += cs;                                         // K3s: split h
+    w.xm = off;                                                      // dropout: M . x [T, n] bf16
+    if (dropout) off += align256(size_t(T) * size_t(d->d_in) * 2);
     w.total = off;
     return w;
 }
@@ -210,7 +214,7 @@ static lora_status collect(GemmCollector* col, const FusedGemmMaps& maps, const 
 // ------------------------------------------------------------ forward
 lora_status fwd_impl(const lora_dims* d, const void* x, const void* w0, const void* a, const void* b,
                      const void* bias, void* y, float* h_out, void* ws, size_t ws_bytes,
-                     cudaStream_t stream, int* launches, GemmCollector* col) {
+                     cudaStream_t stream, int* launches, GemmCollector* col, const DropoutParams* drop) {
     lora_status st = check_dims(d, true);
     if (st != LORA_OK) return st;
     const int64_t T = d->tokens, n = d->d_in, m = d->d_out;
@@ -222,7 +226,7 @@ lora_status fwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
     for (int i = 0; i < 8; ++i)
         if (ptrs[i] && !aligned16(ptrs[i]))
             return fail(LORA_ERR_ALIGN, "lora_linear_fwd: %s = %p is not 16-byte aligned", names[i], ptrs[i]);
-    const FwdWs W = fwd_ws(d);
+    const FwdWs W = fwd_ws(d, drop != nullptr);
     if (!ws || ws_bytes < W.total)
         return fail(LORA_ERR_WORKSPACE, "lora_linear_fwd: workspace %zu bytes < required %zu", ws ? ws_bytes : 0,
                     W.total);
@@ -271,6 +275,18 @@ lora_status fwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
     p.gh = nullptr;
     p.flags = nullptr;
     p.epoch = 0;
+    p.h_in = nullptr;
+    p.drop = DropoutParams{};
+    if (drop && drop->thr > 0) {
+        // LoRA dropout: K0 computes h = q (M . x) A^T; K1 takes it instead of its in-MMA x A^T
+        float* hd = h_out ? h_out : reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + W.h);
+        cudaError_t e = launch_dropout_input(static_cast<const __nv_bfloat16*>(x), T, n,
+                                             static_cast<const __nv_bfloat16*>(a), r, *drop, hd, nullptr, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "dropout K0 launch");
+        ++*launches;
+        p.h_in = hd;
+        p.side_out = nullptr;
+    }
     if (col) return collect(col, maps, p, rp, cg);
     cudaError_t e = launch_fused_gemm(kModeFwd, rp, cg, maps, p, dev.sms, stream);
     if (e != cudaSuccess) return cuda_fail(e, "fused forward launch");
@@ -315,7 +331,7 @@ static lora_status launch_k3_mma(const GradArgs* pr, int count, cudaStream_t str
         const GradArgs& g = pr[i];
         const int r8 = (g.r + 7) / 8 * 8;
         if (g.da) {
-            GradMmaSet s = {g.da, 1, g.n, g.r, r8, 0, g.accumulate, 1.0f};
+            GradMmaSet s = {g.da, 1, g.n, g.r, r8, 0, g.accumulate, g.scale_a};
             sets[ns++] = {g.x, g.T, g.n, g.gh, g.cs_a, s};
         }
         if (g.db) {
@@ -444,7 +460,7 @@ lora_status launch_collected(int mode, GemmCollector& col, cudaStream_t stream, 
 lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const void* a, const void* b,
                      const float* h_saved, const void* dy, void* dx, float* da, float* db, int accumulate,
                      void* ws, size_t ws_bytes, cudaStream_t stream, int* launches, GemmCollector* col,
-                     int stages) {
+                     int stages, const DropoutParams* drop) {
     lora_status st = check_dims(d, true);
     if (st != LORA_OK) return st;
     const int64_t T = d->tokens, n = d->d_in, m = d->d_out;
@@ -457,7 +473,9 @@ lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
     for (int i = 0; i < 10; ++i)
         if (ptrs[i] && !aligned16(ptrs[i]))
             return fail(LORA_ERR_ALIGN, "lora_linear_bwd: %s = %p is not 16-byte aligned", names[i], ptrs[i]);
-    const BwdWs W = bwd_ws(d);
+    const bool dropping = drop && drop->thr > 0;
+    if (dropping && col) return fail(LORA_ERR_UNSUPPORTED, "grouped backward with LoRA dropout");
+    const BwdWs W = bwd_ws(d, drop != nullptr);
     if (!ws || ws_bytes < W.total)
         return fail(LORA_ERR_WORKSPACE, "lora_linear_bwd: workspace %zu bytes < required %zu", ws ? ws_bytes : 0,
                     W.total);
@@ -524,10 +542,14 @@ lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
         p.gh = gh;
         p.flags = reinterpret_cast<uint64_t*>(wsb + W.flags);
         p.epoch = next_epoch();
+        p.h_in = nullptr;
+        p.drop = dropping ? *drop : DropoutParams{};
         if (col) {
             if ((st = collect(col, maps, p, rp, cg)) != LORA_OK) return st;
         } else {
-            if ((e = launch_fused_gemm(kModeDx, rp, cg, maps, p, dev.sms, stream)) != cudaSuccess)
+            // dropout: the epilogue applies q M . (gh A) itself (no tail MMA)
+            if ((e = launch_fused_gemm(dropping ? kModeDxDrop : kModeDx, rp, cg, maps, p, dev.sms, stream)) !=
+                cudaSuccess)
                 return cuda_fail(e, "fused dX launch");
             ++*launches;
         }
@@ -540,7 +562,19 @@ lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
         ++*launches;
     }
     const float* hsrc = h_saved;
-    if (need_h) {
+    const __nv_bfloat16* xk3 = xa;   // K3's dA activation: x, or M . x under dropout
+    float scale_a = 1.0f;
+    if (dropping && (need_h || da)) {
+        // K0: M . x for dA (and h = q (M . x) A^T when it was not saved), one pass over x
+        auto* xm = reinterpret_cast<__nv_bfloat16*>(wsb + W.xm);
+        if ((e = launch_dropout_input(xa, T, n, aa, r, *drop, need_h ? hbuf : nullptr, da ? xm : nullptr,
+                                      stream)) != cudaSuccess)
+            return cuda_fail(e, "dropout K0 launch");
+        ++*launches;
+        if (need_h) hsrc = hbuf;
+        xk3 = xm;
+        scale_a = drop->q;
+    } else if (need_h) {
         if ((e = launch_rowproj(xa, T, n, aa, n, 0, r, 1.0f, hbuf, stream)) != cudaSuccess)
             return cuda_fail(e, "h rowproj");
         ++*launches;
@@ -549,7 +583,9 @@ lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
     if (da || db) {
         const K3Mode k3 = k3_mode();
         if (k3 == kK3Mma || k3 == kK3Cluster) {
-            GradArgs g = make_grad_args(T, n, m, r, s, xa, gh, dya, hsrc, da, db, accumulate);
+            if (dropping && k3 != kK3Mma) return fail(LORA_ERR_UNSUPPORTED, "LoRA dropout needs the default K3");
+            GradArgs g = make_grad_args(T, n, m, r, s, xk3, gh, dya, hsrc, da, db, accumulate);
+            g.scale_a = scale_a;
             g.cs_a = reinterpret_cast<__nv_bfloat16*>(wsb + W.cs_a);
             g.cs_b = reinterpret_cast<__nv_bfloat16*>(wsb + W.cs_b);
             if (col) {   // grouped backward: one K3 launch for the whole group
@@ -611,6 +647,24 @@ lora_status merge_impl(const lora_dims* d, const void* w0, const void* a, const 
 
 size_t fwd_workspace(const lora_dims* d) { return check_dims(d, true) == LORA_OK ? fwd_ws(d).total : 0; }
 size_t bwd_workspace(const lora_dims* d) { return check_dims(d, true) == LORA_OK ? bwd_ws(d).total : 0; }
+size_t fwd_workspace_dropout(const lora_dims* d) {
+    return check_dims(d, true) == LORA_OK ? fwd_ws(d, true).total : 0;
+}
+size_t bwd_workspace_dropout(const lora_dims* d) {
+    return check_dims(d, true) == LORA_OK ? bwd_ws(d, true).total : 0;
+}
+
+// lora_dropout -> kernel parameters (threshold floor(p 2^32) computed in fp64, as the oracle does)
+lora_status dropout_params(const lora_dropout* dr, DropoutParams* out) {
+    if (!dr) return fail(LORA_ERR_INVALID, "dropout is NULL");
+    if (!(dr->p >= 0.0f && dr->p < 1.0f))
+        return fail(LORA_ERR_INVALID, "dropout p = %g must be in [0, 1)", static_cast<double>(dr->p));
+    out->seed = dr->seed;
+    out->offset = dr->offset;
+    out->thr = static_cast<uint32_t>(static_cast<double>(dr->p) * 4294967296.0);
+    out->q = 1.0f / (1.0f - dr->p);
+    return LORA_OK;
+}
 
 }  // namespace lora_host
 
@@ -638,6 +692,54 @@ lora_status lora_linear_bwd(const lora_dims* dims, const void* x, const void* w0
     int launches = 0;
     lora_status st = bwd_impl(dims, x, w0, a, b, h_saved, dy, dx, da, db, accumulate, workspace, workspace_bytes,
                               static_cast<cudaStream_t>(stream), &launches);
+    set_launches(launches);
+    return st;
+}
+
+size_t lora_linear_fwd_dropout_workspace_bytes(const lora_dims* dims) { return fwd_workspace_dropout(dims); }
+size_t lora_linear_bwd_dropout_workspace_bytes(const lora_dims* dims) { return bwd_workspace_dropout(dims); }
+
+lora_status lora_linear_fwd_dropout(const lora_dims* dims, const lora_dropout* dropout, const void* x, const void* w0,
+                                    const void* a, const void* b, const void* bias, void* y, float* h_out,
+                                    void* workspace, size_t workspace_bytes, void* stream) {
+    int launches = 0;
+    DropoutParams dp;
+    lora_status st = dropout_params(dropout, &dp);
+    if (st == LORA_OK)
+        st = fwd_impl(dims, x, w0, a, b, bias, y, h_out, workspace, workspace_bytes, static_cast<cudaStream_t>(stream),
+                      &launches, nullptr, &dp);
+    set_launches(launches);
+    return st;
+}
+
+lora_status lora_linear_bwd_dropout(const lora_dims* dims, const lora_dropout* dropout, const void* x, const void* w0,
+                                    const void* a, const void* b, const float* h_saved, const void* dy, void* dx,
+                                    float* da, float* db, int accumulate, void* workspace, size_t workspace_bytes,
+                                    void* stream) {
+    int launches = 0;
+    DropoutParams dp;
+    lora_status st = dropout_params(dropout, &dp);
+    if (st == LORA_OK)
+        st = bwd_impl(dims, x, w0, a, b, h_saved, dy, dx, da, db, accumulate, workspace, workspace_bytes,
+                      static_cast<cudaStream_t>(stream), &launches, nullptr, 3, &dp);
+    set_launches(launches);
+    return st;
+}
+
+lora_status lora_dropout_mask(int64_t tokens, int64_t d_in, const lora_dropout* dropout, uint8_t* mask, void* stream) {
+    int launches = 0;
+    DropoutParams dp;
+    lora_status st = dropout_params(dropout, &dp);
+    if (st == LORA_OK && (tokens < 0 || d_in < 1)) st = fail(LORA_ERR_SHAPE, "mask shape %lld x %lld", (long long)tokens,
+                                                             (long long)d_in);
+    if (st == LORA_OK && tokens > 0 && !mask) st = fail(LORA_ERR_INVALID, "mask is NULL");
+    DevInfo dev;
+    if (st == LORA_OK) st = device_info(&dev);
+    if (st == LORA_OK && tokens > 0) {
+        cudaError_t e = launch_dropout_mask(tokens, d_in, dp, mask, dev.sms, static_cast<cudaStream_t>(stream));
+        if (e != cudaSuccess) st = cuda_fail(e, "dropout mask launch");
+        else ++launches;
+    }
     set_launches(launches);
     return st;
 }

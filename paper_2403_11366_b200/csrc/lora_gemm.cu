@@ -20,6 +20,12 @@
 //                               256 wide -- 128-byte-aligned MN-major W0 boxes --
 //                               and wait for the flag before their tail)
 //     dX   = bf16(acc + bf16(gh) A)  (epilogue tail MMA)
+// K2 dropout mode (MODE_DX_DROP, LoRA dropout, R9):
+//     dX   = bf16(acc + q M . (gh A))  -- the mask is per output element, so
+//                               no tail MMA: the epilogue applies gh A on the
+//                               CUDA cores from the A tile in shared memory
+//                               and the Philox keep bits of each element
+// K1 with dropout: h = q (M . x) A^T comes from K0 (p.h_in) instead of TMEM.
 //
 // Structure (persistent over output tiles, 6 warps per CTA):
 //   warp 0     : TMA producer (cp.async.bulk.tensor, SWIZZLE_128B, an
@@ -43,6 +49,7 @@
 #include <cstdint>
 
 #include "lora_kernels.h"
+#include "lora_philox.cuh"
 #include "sm100_ptx.cuh"
 
 namespace lora_sm100 {
@@ -84,7 +91,9 @@ struct GemmCfg {
         TAIL_ROW == 32 ? kLayoutSW32 : (TAIL_ROW == 64 ? kLayoutSW64 : kLayoutSW128);
     // tail B operand per CTA: fwd = B rows [BNH x R_PAD] K-major (swizzle = row size);
     //                         dx  = A [R_PAD x NBH*64] MN-major, 64-column SW128 blocks
-    static constexpr int TAILB_BYTES = (MODE == kModeFwd) ? BNH * TAIL_ROW : NBH * R_PAD * 128;
+    // (dx dropout mode: each CTA holds A for the FULL tile width -- its epilogue applies it on the CUDA cores)
+    static constexpr int TAILB_BYTES = (MODE == kModeFwd) ? BNH * TAIL_ROW
+                                                          : (MODE == kModeDxDrop ? NT / 64 : NBH) * R_PAD * 128;
     static constexpr int SH_BYTES = BM * TAIL_ROW;                // bf16(s h) / bf16(gh) tile
     static constexpr int BAR_BYTES = 1024;
     static constexpr int FIXED = round_up(TAILB_BYTES, 1024) + round_up(SH_BYTES, 1024) +
@@ -304,7 +313,7 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
                 const int wh = Cols::width(n_blk) / CG;                 // this CTA's B-operand columns
                 const int nh0 = n0 + static_cast<int>(crank) * wh;
                 const int nb = (wh + 63) / 64;                          // dx: 64-column W0 / A blocks
-                const bool gh_tile = (MODE == kModeDx) && n_blk == 0;
+                const bool gh_tile = (MODE != kModeFwd) && n_blk == 0;
                 const uint32_t stage_tx = (MODE == kModeFwd)
                     ? static_cast<uint32_t>(C::STAGE_BYTES)
                     : static_cast<uint32_t>(C::A_BYTES + nb * 64 * BK * 2 + (gh_tile ? C::NAR_BYTES : 0));
@@ -347,6 +356,12 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
                 if constexpr (MODE == kModeFwd) {
                     if (leader) mbar_arrive_expect_tx(tailop_full, CG * C::TAILB_BYTES);
                     tma_load<CG>(s_tailb, &mp.tail, 0, nh0, tailop_full);
+                } else if constexpr (MODE == kModeDxDrop) {
+                    // every CTA: A columns of the whole tile width, on its own barrier
+                    const int nbf = (Cols::width(n_blk) + 63) / 64;
+                    mbar_arrive_expect_tx(tailop_full, nbf * R_PAD * 128);
+                    for (int j = 0; j < nbf; ++j)
+                        tma_load_2d(s_tailb + j * (R_PAD * 128), &mp.tail, n0 + 64 * j, 0, tailop_full);
                 } else {
                     if (leader) mbar_arrive_expect_tx(tailop_full, CG * nb * R_PAD * 128);
                     for (int j = 0; j < nb; ++j)
@@ -366,7 +381,7 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
                 const TileRef tr = decode_tile<TM>(grp, tile);
                 const int n_blk = tr.n_blk;
                 const int num_k_blks = tr.num_k_blks;
-                const bool gh_tile = (MODE == kModeDx) && n_blk == 0;
+                const bool gh_tile = (MODE != kModeFwd) && n_blk == 0;
                 const uint32_t idesc_main = (MODE == kModeFwd) ? idesc_fwd : (gh_tile ? idesc_dx_first : idesc_dx_full);
                 const uint32_t acc = tl & 1;
                 const uint32_t acc_phase = (tl >> 1) & 1;
@@ -424,7 +439,7 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
             const int64_t row = static_cast<int64_t>(t_blk) * TM + crank * BM + row_local;
             const int n0 = Cols::start(n_blk);
             const int width = Cols::width(n_blk);
-            const bool gh_tile = (MODE == kModeDx) && n_blk == 0;
+            const bool gh_tile = (MODE != kModeFwd) && n_blk == 0;
             const uint32_t acc = tl & 1;
             const uint32_t acc_phase = (tl >> 1) & 1;
             mbar_wait(&tmem_full[acc], acc_phase);
@@ -433,7 +448,11 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
 
             // (1) the r_pad low-rank values of this row
             float hv[R_PAD];
-            if (MODE == kModeFwd || gh_tile) {
+            if (MODE == kModeFwd && p.h_in != nullptr) {
+                // fwd with dropout: h = q (M . x) A^T precomputed by K0 (the MMA's x A^T columns are unused)
+#pragma unroll
+                for (int j = 0; j < R_PAD; ++j) hv[j] = (j < p.r && row < p.T) ? p.h_in[row * p.r + j] : 0.0f;
+            } else if (MODE == kModeFwd || gh_tile) {
                 // fwd: h = x A^T in TMEM columns [BN, BN + r_pad); dx first tile: dY B in [128, ..)
                 const uint32_t col0 = (MODE == kModeFwd) ? BN : DX_BN0;
 #pragma unroll
@@ -444,19 +463,19 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
 #pragma unroll
                     for (int e = 0; e < 16; ++e) hv[16 * c + e] = __uint_as_float(v[e]);
                 }
-                if (MODE == kModeDx) {
+                if (MODE != kModeFwd) {
 #pragma unroll
                     for (int j = 0; j < R_PAD; ++j) hv[j] *= p.scale;     // gh = s (dY B)
                 }
                 // (2) side output: fwd h (for dB); dx gh (for the other tiles and for dA)
                 float* side = (MODE == kModeFwd) ? p.side_out : p.gh;
-                if (side != nullptr && (MODE == kModeDx || n_blk == 0) && row < p.T) {
+                if (side != nullptr && (MODE != kModeFwd || n_blk == 0) && row < p.T) {
                     float* dst = side + row * p.r;
 #pragma unroll
                     for (int j = 0; j < R_PAD; ++j)
                         if (j < p.r) dst[j] = hv[j];
                 }
-                if (MODE == kModeDx) {
+                if (MODE != kModeFwd) {
                     // publish: every thread's gh stores, then one release of the flag
                     __threadfence();
                     named_bar_sync(1, 128);
@@ -480,6 +499,10 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
 #pragma unroll
                 for (int j = 0; j < R_PAD; ++j) hv[j] = (j < p.r && row < p.T) ? src[j] : 0.0f;
             }
+            if constexpr (MODE == kModeDxDrop) {
+                // dropout: no tail MMA -- the epilogue adds q M . (gh A) itself (step 5)
+                mbar_wait(tailop_full, tl & 1);
+            } else {
             // (3) bf16(s h) / bf16(gh) -> swizzled K-major smem tile (tail MMA A operand)
             const float op_scale = (MODE == kModeFwd) ? p.scale : 1.0f;
 #pragma unroll
@@ -526,6 +549,7 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
             mbar_wait(tail_done, tl & 1);
             tc_fence_after();
             if (ew == 0 && lane == 0) mbar_arrive(tailop_empty);
+            }
 
             // (5) drain: acc -> (+ b0) -> bf16 (RNE) -> global
             const bool row_ok = row < p.T;
@@ -549,6 +573,33 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
                         for (int e = 0; e < 16; ++e)
                             if (col + e < p.N_out) f[e] += __bfloat162float(p.bias[col + e]);
                     }
+                    if constexpr (MODE == kModeDxDrop) {
+                        // f += q M . (gh A): A columns of this chunk from the MN-major SW128 tile
+                        const int lc = 16 * c;
+                        const uint8_t* blk = s_tailb + (lc / 64) * (R_PAD * 128);
+                        const uint32_t ch = static_cast<uint32_t>((lc % 64) / 8);
+                        float lo[16];
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) lo[e] = 0.0f;
+#pragma unroll
+                        for (int j = 0; j < R_PAD; ++j) {
+                            const uint4 a0 = *reinterpret_cast<const uint4*>(blk + swizzled_offset(j, ch, 128));
+                            const uint4 a1 = *reinterpret_cast<const uint4*>(blk + swizzled_offset(j, ch + 1, 128));
+                            const uint32_t aw[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+#pragma unroll
+                            for (int e = 0; e < 8; ++e) {
+                                const float2 av = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&aw[e]));
+                                lo[2 * e] = fmaf(hv[j], av.x, lo[2 * e]);
+                                lo[2 * e + 1] = fmaf(hv[j], av.y, lo[2 * e + 1]);
+                            }
+                        }
+                        uint32_t keep = 0;
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) keep |= dropout_keep4(p.drop, row, col / 4 + i) << (4 * i);
+#pragma unroll
+                        for (int e = 0; e < 16; ++e)
+                            if ((keep >> e) & 1u) f[e] = fmaf(p.drop.q, lo[e], f[e]);
+                    }
                     uint4 q0, q1;
                     q0.x = pack_bf16x2(f[0], f[1]);   q0.y = pack_bf16x2(f[2], f[3]);
                     q0.z = pack_bf16x2(f[4], f[5]);   q0.w = pack_bf16x2(f[6], f[7]);
@@ -557,6 +608,10 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
                     *reinterpret_cast<uint4*>(out_row + col) = q0;               // N_out % 8 == 0
                     if (col + 8 < p.N_out) *reinterpret_cast<uint4*>(out_row + col + 8) = q1;
                 }
+            }
+            if constexpr (MODE == kModeDxDrop) {
+                named_bar_sync(1, 128);   // every epilogue warp is done with the A tile
+                if (ew == 0 && lane == 0) mbar_arrive(tailop_empty);
             }
             tc_fence_before();
             __syncwarp();
@@ -655,11 +710,17 @@ static cudaError_t dispatch(int mode, int r_pad, FusedGemmGroup& grp, int num_sm
             case 32: return launch_impl<kModeFwd, 32, CG>(grp, num_sms, stream);
             case 64: return launch_impl<kModeFwd, 64, CG>(grp, num_sms, stream);
         }
-    } else {
+    } else if (mode == kModeDx) {
         switch (r_pad) {
             case 16: return launch_impl<kModeDx, 16, CG>(grp, num_sms, stream);
             case 32: return launch_impl<kModeDx, 32, CG>(grp, num_sms, stream);
             case 64: return launch_impl<kModeDx, 64, CG>(grp, num_sms, stream);
+        }
+    } else if (mode == kModeDxDrop) {
+        switch (r_pad) {
+            case 16: return launch_impl<kModeDxDrop, 16, CG>(grp, num_sms, stream);
+            case 32: return launch_impl<kModeDxDrop, 32, CG>(grp, num_sms, stream);
+            case 64: return launch_impl<kModeDxDrop, 64, CG>(grp, num_sms, stream);
         }
     }
     return cudaErrorInvalidValue;

@@ -744,6 +744,7 @@ GradArgs make_grad_args(int64_t T, int64_t n, int64_t m, int r, float scale, con
     GradArgs g = {};
     g.x = x; g.gh = gh; g.dy = dy; g.h = h; g.da = da; g.db = db;
     g.T = T; g.n = n; g.m = m; g.r = r; g.scale_b = scale; g.accumulate = accumulate;
+    g.scale_a = 1.0f;
     return g;
 }
 

@@ -30,11 +30,15 @@ struct GemmCollector {
 //             bit 1 = everything after K2 (gh pre-pass, h recompute, K3).
 lora_status fwd_impl(const lora_dims* d, const void* x, const void* w0, const void* a, const void* b,
                      const void* bias, void* y, float* h_out, void* ws, size_t ws_bytes,
-                     cudaStream_t stream, int* launches, GemmCollector* col = nullptr);
+                     cudaStream_t stream, int* launches, GemmCollector* col = nullptr,
+                     const lora_sm100::DropoutParams* drop = nullptr);
 lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const void* a, const void* b,
                      const float* h_saved, const void* dy, void* dx, float* da, float* db, int accumulate,
                      void* ws, size_t ws_bytes, cudaStream_t stream, int* launches,
-                     GemmCollector* col = nullptr, int stages = 3);
+                     GemmCollector* col = nullptr, int stages = 3,
+                     const lora_sm100::DropoutParams* drop = nullptr);
+size_t fwd_workspace_dropout(const lora_dims* d);
+size_t bwd_workspace_dropout(const lora_dims* d);
 // launch the collected problems, one grouped launch per (r_pad, CTA group) class
 lora_status launch_collected(int mode, GemmCollector& col, cudaStream_t stream, int* launches);
 // launch the collected K3 problems, one launch per rank bucket

@@ -9,10 +9,17 @@
 
 namespace lora_sm100 {
 
-enum : int { kModeFwd = 0, kModeDx = 1 };
+enum : int { kModeFwd = 0, kModeDx = 1, kModeDxDrop = 2 };
 
 // Programmatic dependent launch for the step's kernels (LORA_PDL=1; off by default).
 bool pdl_enabled();
+
+// LoRA dropout (lora_philox.cuh): keep(t, k) = Philox4x32-10((k/4, t, offset), seed)[k % 4] >= thr
+struct DropoutParams {
+    uint64_t seed, offset;
+    uint32_t thr;    // floor(p * 2^32); 0 = keep everything
+    float q;         // 1 / (1 - p)
+};
 
 struct FusedGemmParams {
     int64_t T;                    // token rows
@@ -26,6 +33,8 @@ struct FusedGemmParams {
     float* gh;                    // dx: gh [T, r] = s dY B, written by the first column tile
     uint64_t* flags;              // dx: one per (row block, CTA of the pair): gh published
     uint64_t epoch;               // dx: value the flags take in this launch (never reset)
+    const float* h_in;            // fwd with dropout: h [T, r] precomputed by K0 (else null: h from the MMA)
+    DropoutParams drop;           // dx dropout mode: dX += q M . (gh A) in the epilogue
 };
 
 struct FusedGemmMaps {
@@ -85,6 +94,7 @@ struct GradArgs {
     int accumulate;
     __nv_bfloat16* cs_a;      // tensor-core K3: split gh [3 r8, T_pad] (workspace)
     __nv_bfloat16* cs_b;      // tensor-core K3: split h  [3 r8, T_pad] (workspace)
+    float scale_a;            // dA multiplier (1, or q = 1/(1-p) when x is the dropout-masked M . x)
 };
 // several problems of the same rank bucket in one K3 launch
 struct GradGroup {
@@ -171,6 +181,13 @@ cudaError_t launch_merge(const __nv_bfloat16* w0, const __nv_bfloat16* a, const 
 
 // dst += src (fp32), used by the TP backward when accumulating reduced grads
 cudaError_t launch_add_f32(float* dst, const float* src, int64_t count, cudaStream_t stream);
+
+// K0 (dropout): h = q (M . x) A^T [T, r] fp32 and/or xm = M . x [T, n] bf16 (either may be null)
+cudaError_t launch_dropout_input(const __nv_bfloat16* x, int64_t T, int64_t n, const __nv_bfloat16* a, int r,
+                                 const DropoutParams& d, float* h, __nv_bfloat16* xm, cudaStream_t stream);
+// keep mask M [T, n] uint8 (for lora_dropout_mask)
+cudaError_t launch_dropout_mask(int64_t T, int64_t n, const DropoutParams& d, uint8_t* mask, int num_sms,
+                                cudaStream_t stream);
 
 // zero-fill helper for degenerate (T == 0) gradients
 cudaError_t launch_fill_zero(float* p, int64_t count, cudaStream_t stream);

@@ -1,0 +1,151 @@
+"""GPU parity of the LoRA-dropout path (Listing 3 LORA_DROPOUT, PAPER.md:82;
+DESIGN.md reading R9) against the fp64 oracle: the Philox keep mask bit for
+bit, then y, h, dX, dA, dB within the north-star tolerances, bitwise where the
+arithmetic is exact."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from synth import make_lora_inputs  # noqa: E402
+from tests.gpu_util import TOL_GRAD, TOL_OUT, dev_bf16, host_f64, relF, rne_bf16_f64  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def L():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2403_11366_b200 as L
+    L.lora_device_check()
+    return L
+
+
+@pytest.mark.parametrize("T,n,p,seed,offset", [(1, 8, 0.05, 1, 0), (257, 136, 0.05, 2403, 7),
+                                               (64, 13, 0.5, 3, 1 << 40), (1000, 4096, 0.3, 2**64 - 1, 2**63 + 5)])
+def test_mask_bit_exact(oracle_mod, L, T, n, p, seed, offset):
+    got = L.lora_dropout_mask(T, n, (p, seed, offset)).cpu().numpy()
+    ref = oracle_mod.dropout_mask(T, n, p, seed, offset)
+    np.testing.assert_array_equal(got, ref)
+
+
+def _run(L, d, alpha, drop, h_saved=True, want_dx=True):
+    x, w0, a, b, dy = (dev_bf16(d[k]) for k in ("x", "w0", "a", "b", "dy"))
+    y, h = L.lora_linear_fwd(x, w0, a, b, alpha, dropout=drop)
+    dx, da, db = L.lora_linear_bwd(x, w0, a, b, dy, alpha, h_saved=h if h_saved else None, want_dx=want_dx,
+                                   dropout=drop)
+    torch.cuda.synchronize()
+    return dict(y=y, h=h, dx=dx, da=da, db=db)
+
+
+@pytest.mark.parametrize("shape", [(300, 200, 264, 5), (129, 64, 520, 17), (257, 136, 256, 33), (64, 1024, 8, 64),
+                                   (700, 512, 488, 16), (1, 8, 8, 1), (384, 4096, 1024, 8)])
+def test_dropout_parity(oracle_mod, L, shape):
+    T, n, m, r = shape
+    drop = (0.05, 1000 + r, 3)
+    d = make_lora_inputs(T, n, m, r, seed=500 + r)
+    out = _run(L, d, 16.0, drop)
+    yo, ho = oracle_mod.lora_fwd(d["x"], d["w0"], d["a"], d["b"], 16.0, dropout=drop)
+    go = oracle_mod.lora_bwd(d["x"], d["w0"], d["a"], d["b"], d["dy"], 16.0, dropout=drop)
+    errs = {"y": relF(host_f64(out["y"]), yo), "h": relF(host_f64(out["h"]), ho),
+            "dx": relF(host_f64(out["dx"]), go["dx"]), "da": relF(host_f64(out["da"]), go["da"]),
+            "db": relF(host_f64(out["db"]), go["db"])}
+    assert errs["y"] <= TOL_OUT and errs["dx"] <= TOL_OUT, errs
+    assert errs["da"] <= TOL_GRAD and errs["db"] <= TOL_GRAD, errs
+    assert errs["h"] <= 1e-4, errs
+    # the mask really acts: without dropout the adapter terms differ well beyond rounding
+    y0, h0 = oracle_mod.lora_fwd(d["x"], d["w0"], d["a"], d["b"], 16.0)
+    if T * n > 64:
+        assert relF(host_f64(out["h"]), h0) > 1e-2
+
+
+def test_dropout_p0_is_the_plain_call_bitwise(L):
+    d = make_lora_inputs(300, 256, 200, 8, seed=601)
+    x, w0, a, b, dy = (dev_bf16(d[k]) for k in ("x", "w0", "a", "b", "dy"))
+    y0, h0 = L.lora_linear_fwd(x, w0, a, b, 16.0)
+    g0 = L.lora_linear_bwd(x, w0, a, b, dy, 16.0, h_saved=h0)
+    y1, h1 = L.lora_linear_fwd(x, w0, a, b, 16.0, dropout=(0.0, 9, 9))
+    g1 = L.lora_linear_bwd(x, w0, a, b, dy, 16.0, h_saved=h1, dropout=(0.0, 9, 9))
+    torch.cuda.synchronize()
+    assert torch.equal(y0, y1) and torch.equal(h0, h1)
+    for u, v in zip(g0, g1):
+        assert torch.equal(u, v)
+
+
+def _ternary_certified(oracle_mod, T, n, m, r, alpha, drop):
+    s = alpha / r
+    for seed in range(60):
+        d = make_lora_inputs(T, n, m, r, seed=7000 + seed, dist="ternary")
+        _, h = oracle_mod.lora_fwd(d["x"], d["w0"], d["a"], d["b"], alpha, dropout=drop)
+        go = oracle_mod.lora_bwd(d["x"], d["w0"], d["a"], d["b"], d["dy"], alpha, dropout=drop)
+        if np.array_equal(rne_bf16_f64(s * h), s * h) and np.array_equal(rne_bf16_f64(go["gh"]), go["gh"]):
+            return d
+    raise AssertionError("no certified ternary input found")
+
+
+@pytest.mark.parametrize("shape", [(128, 64, 64, 4), (300, 200, 264, 16)])
+def test_dropout_integer_exact_bitwise(oracle_mod, L, shape):
+    """p = 1/2 (q = 2 exact) on ternary inputs: every intermediate is a small
+    integer, so the GPU must match the oracle bitwise (catches a mask applied
+    to the wrong element, a missing q, a mask on the frozen path)."""
+    T, n, m, r = shape
+    alpha, drop = 4.0 * r, (0.5, 42, 5)
+    d = _ternary_certified(oracle_mod, T, n, m, r, alpha, drop)
+    out = _run(L, d, alpha, drop)
+    yo, ho = oracle_mod.lora_fwd(d["x"], d["w0"], d["a"], d["b"], alpha, dropout=drop)
+    go = oracle_mod.lora_bwd(d["x"], d["w0"], d["a"], d["b"], d["dy"], alpha, dropout=drop)
+    np.testing.assert_array_equal(host_f64(out["y"]), rne_bf16_f64(yo))
+    np.testing.assert_array_equal(host_f64(out["h"]), ho)
+    np.testing.assert_array_equal(host_f64(out["dx"]), rne_bf16_f64(go["dx"]))
+    np.testing.assert_array_equal(host_f64(out["da"]), go["da"])
+    np.testing.assert_array_equal(host_f64(out["db"]), go["db"])
+
+
+def test_dropout_recompute_h_and_skip_dx(oracle_mod, L):
+    """h_saved = NULL regenerates h from the same mask (bitwise equal grads);
+    dX = NULL takes the gh pre-pass path."""
+    d = make_lora_inputs(256, 192, 320, 16, seed=603)
+    drop = (0.1, 77, 1)
+    a1 = _run(L, d, 16.0, drop, h_saved=True)
+    a2 = _run(L, d, 16.0, drop, h_saved=False)
+    for k in ("dx", "da", "db"):
+        assert torch.equal(a1[k], a2[k]), k
+    a3 = _run(L, d, 16.0, drop, want_dx=False)
+    go = oracle_mod.lora_bwd(d["x"], d["w0"], d["a"], d["b"], d["dy"], 16.0, dropout=drop)
+    assert a3["dx"] is None
+    assert relF(host_f64(a3["da"]), go["da"]) <= TOL_GRAD
+    assert relF(host_f64(a3["db"]), go["db"]) <= TOL_GRAD
+
+
+def test_dropout_streams_and_determinism(L):
+    d = make_lora_inputs(256, 128, 128, 8, seed=604)
+    a1 = _run(L, d, 16.0, (0.05, 1, 0))
+    a2 = _run(L, d, 16.0, (0.05, 1, 0))
+    a3 = _run(L, d, 16.0, (0.05, 1, 1))
+    for k in ("y", "h", "dx", "da", "db"):
+        assert torch.equal(a1[k], a2[k]), k
+    assert not torch.equal(a1["h"], a3["h"])
+
+
+def test_dropout_cfg2_full_size_sampled_rows(oracle_mod, L):
+    """BASELINE.json configs[1] shape with the paper's LORA_DROPOUT = 0.05."""
+    T, n, m, r = 2048, 4096, 4096, 8
+    drop = (0.05, 2403, 11)
+    d = make_lora_inputs(T, n, m, r, seed=2403)
+    out = _run(L, d, 16.0, drop)
+    rows = np.unique(np.concatenate([[0, 1, 127, 128, T - 1], np.random.default_rng(8).choice(T, 24, replace=False)]))
+    yo, ho = oracle_mod.lora_fwd(d["x"], d["w0"], d["a"], d["b"], 16.0, rows=rows, dropout=drop)
+    go = oracle_mod.lora_bwd(d["x"], d["w0"], d["a"], d["b"], d["dy"], 16.0, rows=rows, dropout=drop)
+    assert relF(host_f64(out["y"])[rows], yo) <= TOL_OUT
+    assert relF(host_f64(out["h"])[rows], ho) <= 1e-4
+    assert relF(host_f64(out["dx"])[rows], go["dx"]) <= TOL_OUT
+    assert relF(host_f64(out["da"]), go["da"]) <= TOL_GRAD
+    assert relF(host_f64(out["db"]), go["db"]) <= TOL_GRAD
+
+
+def test_dropout_invalid_p(L):
+    d = make_lora_inputs(8, 8, 8, 2, seed=605)
+    x, w0, a, b = (dev_bf16(d[k]) for k in ("x", "w0", "a", "b"))
+    for p in (1.0, -0.1, float("nan")):
+        with pytest.raises(L.LoraError):
+            L.lora_linear_fwd(x, w0, a, b, 16.0, dropout=(p, 0, 0))
