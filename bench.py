@@ -248,9 +248,13 @@ def run_ours(args, wl):
                  db=torch.zeros((m, r), dtype=torch.float32, device=dev))
         dd = L.dims(T, n, m, r, l.alpha)
         import ctypes
-        e["ws_f"] = torch.empty(max(256, L.lora_linear_fwd_workspace_bytes(dd)), dtype=torch.uint8, device=dev)
-        e["ws_b"] = torch.empty(max(256, int(L.lib.lora_tp_linear_bwd_workspace_bytes(ctypes.byref(dd)))),
-                                dtype=torch.uint8, device=dev)
+        wf = L.lora_linear_fwd_workspace_bytes(dd)
+        wb = int(L.lib.lora_tp_linear_bwd_workspace_bytes(ctypes.byref(dd)))
+        if args.dropout > 0.0:
+            wf = max(wf, int(L.lib.lora_linear_fwd_dropout_workspace_bytes(ctypes.byref(dd))))
+            wb = max(wb, int(L.lib.lora_linear_bwd_dropout_workspace_bytes(ctypes.byref(dd))))
+        e["ws_f"] = torch.empty(max(256, wf), dtype=torch.uint8, device=dev)
+        e["ws_b"] = torch.empty(max(256, wb), dtype=torch.uint8, device=dev)
         lin.append(e)
     # the linears of a group read the SAME activation in the model (q/k/v read the
     # attention input, gate/up the MLP input): one shared x tensor per group
@@ -261,7 +265,11 @@ def run_ours(args, wl):
 
     # N = 1: the linears that share an input in the model (q,k,v / gate,up) run as
     # one grouped call (one persistent launch per fused GEMM)
-    use_groups = comm is None and not args.no_group
+    use_groups = comm is None and not args.no_group and args.dropout == 0.0
+    if args.dropout > 0.0 and comm is not None:
+        raise SystemExit("--dropout is single-GPU only (the TP entry points have no dropout variant)")
+    for i, e in enumerate(lin):   # one Philox stream per linear (offset = its index)
+        e["drop"] = (args.dropout, 2403, i) if args.dropout > 0.0 else None
     groups = []
     if use_groups:
         for gidx in wl.groups:
@@ -300,7 +308,7 @@ def run_ours(args, wl):
                 ev["f0"].record(stream)
             if comm is None:
                 L.lora_linear_fwd(e["x"], e["w0"], e["a"], e["b"], e["l"].alpha, y=e["y"], h_out=e["h"],
-                                  workspace=e["ws_f"], stream=torch.cuda.current_stream())
+                                  workspace=e["ws_f"], stream=torch.cuda.current_stream(), dropout=e["drop"])
             else:
                 tp.tp_linear_fwd(comm, e["spec"], e["x"], e["w0"], e["a"], e["b"], e["l"].alpha, y=e["y"],
                                  h_out=e["h"], workspace=e["ws_f"], stream=torch.cuda.current_stream())
@@ -310,7 +318,8 @@ def run_ours(args, wl):
         for e in lin:
             if comm is None:
                 L.lora_linear_bwd(e["x"], e["w0"], e["a"], e["b"], e["dy"], e["l"].alpha, h_saved=e["h"],
-                                  dx=e["dx"], da=e["da"], db=e["db"], workspace=e["ws_b"], stream=torch.cuda.current_stream())
+                                  dx=e["dx"], da=e["da"], db=e["db"], workspace=e["ws_b"],
+                                  stream=torch.cuda.current_stream(), dropout=e["drop"])
             else:
                 tp.tp_linear_bwd(comm, e["spec"], e["x"], e["w0"], e["a"], e["b"], e["dy"], e["l"].alpha,
                                  h_saved=e["h"], dx=e["dx"], da=e["da"], db=e["db"], workspace=e["ws_b"],
@@ -472,6 +481,7 @@ def run_ours(args, wl):
                        "cuda_graph": graph is not None,
                        "grouped_calls": [[wl.linears[i].name for i in g] for g in wl.groups] if use_groups else None,
                        "shared_inputs": [[wl.linears[i].name for i in g] for g in wl.groups if len(g) > 1],
+                       "lora_dropout": args.dropout,
                        "l2": "flushed between timed steps (2xL2 write then 2xL2 read, outside the "
                              "event pairs)"},
             "tokens_per_s": tokens * K / (total_ms * 1e-3),
@@ -505,6 +515,8 @@ def main():
     ap.add_argument("--config", default="cfg2", choices=sorted(WORKLOADS))
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dropout", type=float, default=0.0,
+                    help="LoRA dropout p (Listing 3 LORA_DROPOUT = 0.05); 0 = the north-star path")
     ap.add_argument("--no-group", action="store_true",
                     help="one call per linear instead of grouped calls for linears sharing an input")
     ap.add_argument("--graph", choices=["auto", "on", "off"], default="auto",

@@ -113,7 +113,7 @@ lora_status lora_merge(const lora_dims* dims, const void* w0, const void* a,
                        const void* b, void* w_out, void* stream);
 
 /* ---------------- LoRA dropout (Listing 3 LORA_DROPOUT = 0.05) ----
- * Inverted dropout on the ADAPTER input only (reading R9; the frozen
+ * Inverted dropout on the ADAPTER input only (reading R7; the frozen
  * path W0 x never sees it).  Keep mask M[t,k] in {0,1}, q = 1 / (1 - p):
  *   y  = x W0^T + s (q (M . x) A^T) B^T (+ bias),   h = q (M . x) A^T
  *   dX = dy W0 + q M . (gh A),   dA = q gh^T (M . x),   dB = s dy^T h

@@ -126,7 +126,7 @@ def dropout_threshold(p: float) -> int:
 
 def dropout_mask(T: int, n: int, p: float, seed: int, offset: int) -> np.ndarray:
     """LoRA-dropout keep mask M [T, n] uint8 (Listing 3 LORA_DROPOUT, PAPER.md:82;
-    DESIGN.md R9): M[t,k] = Philox4x32-10((k/4, t, offset), seed)[k % 4] >= floor(p 2^32)."""
+    DESIGN.md R7): M[t,k] = Philox4x32-10((k/4, t, offset), seed)[k % 4] >= floor(p 2^32)."""
     mask = np.empty((T, n), np.uint8)
     rc = _load().oracle_dropout_mask(int(T), int(n), float(np.float32(p)), int(seed) & (2**64 - 1),
                                      int(offset) & (2**64 - 1), mask.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)))
@@ -148,7 +148,7 @@ def lora_fwd(x, w0, a, b, alpha, bias=None, rows=None, dropout=None):
 
     All tensor arguments are bf16 bit patterns (uint16).  ``rows`` selects the
     tokens to evaluate (None: all).  ``dropout = (p, seed, offset)`` applies
-    LoRA dropout to the adapter input (R9).  Returns (y [n_rows, m],
+    LoRA dropout to the adapter input (R7).  Returns (y [n_rows, m],
     h [n_rows, r]) in float64.
     """
     T, n = x.shape

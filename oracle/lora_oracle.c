@@ -30,7 +30,7 @@
  *   W'[i,k] = W0[i,k] + s sum_j B[i,j] A[j,k]
  *
  * LoRA dropout (Listing 3, LORA_DROPOUT = 0.05; placement per
- * DESIGN.md reading R9: inverted dropout on the adapter input only, the
+ * DESIGN.md reading R7: inverted dropout on the adapter input only, the
  * frozen path never sees it): with keep mask M[t,k] in {0,1} and
  * q = 1/(1-p),  xd[t,k] = q M[t,k] x[t,k]  replaces x in "A x":
  *   h[t,j]  = sum_k xd[t,k] A[j,k]

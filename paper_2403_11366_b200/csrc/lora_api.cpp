@@ -177,7 +177,7 @@ static FwdWs fwd_ws(const lora_dims* d, bool dropout = false) {
 
 // Backward workspace: B^T [r, m], gh [T, r] fp32, h [T, r] fp32 (when not saved).
 struct BwdWs {
-    size_t b8, gh, h, flags, cs_a, cs_b, xm, total;
+    size_t b8, gh, h, flags, cs_a, cs_b, xm, bits, total;
 };
 static BwdWs bwd_ws(const lora_dims* d, bool dropout = false) {
     BwdWs w;
@@ -193,6 +193,8 @@ static BwdWs bwd_ws(const lora_dims* d, bool dropout = false) {
     w.cs_b = off; off += cs;                                         // K3s: split h
     w.xm = off;                                                      // dropout: M . x [T, n] bf16
     if (dropout) off += align256(size_t(T) * size_t(d->d_in) * 2);
+    w.bits = off;                                                    // dropout: keep bits [T, ceil(n/32)]
+    if (dropout) off += align256(size_t(T) * size_t((d->d_in + 31) / 32) * 4);
     w.total = off;
     return w;
 }
@@ -277,11 +279,13 @@ lora_status fwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
     p.epoch = 0;
     p.h_in = nullptr;
     p.drop = DropoutParams{};
+    p.drop_bits = nullptr;
     if (drop && drop->thr > 0) {
         // LoRA dropout: K0 computes h = q (M . x) A^T; K1 takes it instead of its in-MMA x A^T
         float* hd = h_out ? h_out : reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + W.h);
         cudaError_t e = launch_dropout_input(static_cast<const __nv_bfloat16*>(x), T, n,
-                                             static_cast<const __nv_bfloat16*>(a), r, *drop, hd, nullptr, stream);
+                                             static_cast<const __nv_bfloat16*>(a), r, *drop, hd, nullptr, nullptr,
+                                             dev.sms, stream);
         if (e != cudaSuccess) return cuda_fail(e, "dropout K0 launch");
         ++*launches;
         p.h_in = hd;
@@ -516,6 +520,16 @@ lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
     const bool need_gh = dx || da;
     const bool need_h = db && !h_saved;
 
+    auto* xm = reinterpret_cast<__nv_bfloat16*>(wsb + W.xm);
+    if (dropping && (stages & 1)) {
+        // K0: keep bits for K2's epilogue, M . x for dA, h = q (M . x) A^T when not saved -- one pass over x
+        if ((e = launch_dropout_input(static_cast<const __nv_bfloat16*>(x), T, n, static_cast<const __nv_bfloat16*>(a),
+                                      r, *drop, need_h ? hbuf : nullptr, da ? xm : nullptr,
+                                      dx ? reinterpret_cast<uint32_t*>(wsb + W.bits) : nullptr, dev.sms, stream)) !=
+            cudaSuccess)
+            return cuda_fail(e, "dropout K0 launch");
+        ++*launches;
+    }
     if (dx && (stages & 1)) {
         // K2 computes gh = s dY B itself (first column tile of each row block)
         const __nv_bfloat16* bsrc = static_cast<const __nv_bfloat16*>(b);
@@ -544,6 +558,7 @@ lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
         p.epoch = next_epoch();
         p.h_in = nullptr;
         p.drop = dropping ? *drop : DropoutParams{};
+        p.drop_bits = dropping ? reinterpret_cast<const uint32_t*>(wsb + W.bits) : nullptr;
         if (col) {
             if ((st = collect(col, maps, p, rp, cg)) != LORA_OK) return st;
         } else {
@@ -564,13 +579,7 @@ lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
     const float* hsrc = h_saved;
     const __nv_bfloat16* xk3 = xa;   // K3's dA activation: x, or M . x under dropout
     float scale_a = 1.0f;
-    if (dropping && (need_h || da)) {
-        // K0: M . x for dA (and h = q (M . x) A^T when it was not saved), one pass over x
-        auto* xm = reinterpret_cast<__nv_bfloat16*>(wsb + W.xm);
-        if ((e = launch_dropout_input(xa, T, n, aa, r, *drop, need_h ? hbuf : nullptr, da ? xm : nullptr,
-                                      stream)) != cudaSuccess)
-            return cuda_fail(e, "dropout K0 launch");
-        ++*launches;
+    if (dropping) {   // K0 (above) wrote M . x and, if needed, h
         if (need_h) hsrc = hbuf;
         xk3 = xm;
         scale_a = drop->q;

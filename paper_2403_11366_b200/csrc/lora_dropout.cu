@@ -1,12 +1,12 @@
 // lora_dropout.cu -- LoRA dropout (Listing 3 LORA_DROPOUT = 0.05, PAPER.md:82;
-// DESIGN.md reading R9: inverted dropout on the adapter input only; the
+// DESIGN.md reading R7: inverted dropout on the adapter input only; the
 // frozen path W0 x never sees it).  With keep mask M and q = 1 / (1 - p):
 //   h   = q (M . x) A^T                     (K0, replaces K1's in-MMA h)
 //   dX  = G W0 + q M . (gh A)               (K2 dropout mode, lora_gemm.cu)
 //   dA  = q gh^T (M . x)                    (K3 on xm = M . x)
-// K0 here: one warp per token row, 16-byte loads of x, the row's keep bits
-// from Philox (lora_philox.cuh), h in fp32 and/or xm = M . x in bf16 (exact:
-// zeroing only), streaming x once.
+// K0 here: streams x once (16-byte loads), draws the keep bits from Philox
+// (lora_philox.cuh) and writes any of: h in fp32, xm = M . x in bf16 (exact:
+// zeroing only) and the packed keep bits the dX epilogue reads.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -31,42 +31,70 @@ __device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8]) {
     }
 }
 
-// RB: register rank bucket (>= r)
-template <int RB>
+// RB: register rank bucket (>= r).  A block of 8 warps covers 8 / SPLIT token
+// rows; the SPLIT warps of a row take contiguous column ranges (more warps in
+// flight than one-warp-per-row at small T), and their partial h sums are
+// combined in warp order through shared memory (deterministic).  Each lane
+// handles 8 consecutive columns per step: one 16-byte load of x, two Philox
+// blocks for the 8 keep bits.  Outputs (any may be null):
+//   h [T, r] = q (M . x) A^T     xm [T, n] = M . x (bf16, exact)
+//   bits [T, ceil(n/32)] uint32: bit c of word w = keep(t, 32 w + c)
+template <int RB, int SPLIT>
 __global__ void __launch_bounds__(256) dropout_input_kernel(const bf16* __restrict__ x, int64_t T, int64_t n,
                                                             const bf16* __restrict__ a, int r, DropoutParams d,
-                                                            float* __restrict__ h, bf16* __restrict__ xm) {
+                                                            float* __restrict__ h, bf16* __restrict__ xm,
+                                                            uint32_t* __restrict__ bits) {
+    __shared__ float part[8][RB];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t t = static_cast<int64_t>(blockIdx.x) * 8 + warp;
-    if (t >= T) return;
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * (8 / SPLIT) + warp / SPLIT;
+    const int sub = warp % SPLIT;
+    const int64_t chunk = ((n + SPLIT * 256 - 1) / (SPLIT * 256)) * 256;   // columns per warp, multiple of 256
+    const int64_t k_lo = sub * chunk, k_hi = k_lo + chunk < n ? k_lo + chunk : n;
+    const int64_t nw = (n + 31) / 32;
     float acc[RB];
 #pragma unroll
     for (int j = 0; j < RB; ++j) acc[j] = 0.0f;
-    const bf16* xr = x + t * n;
-    for (int64_t k = lane * 8; k < n; k += 256) {
-        const uint4 u = __ldg(reinterpret_cast<const uint4*>(xr + k));
-        const uint32_t keep = dropout_keep4(d, t, k / 4) | (dropout_keep4(d, t, k / 4 + 1) << 4);
-        if (xm) {
-            const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-            uint32_t o[4];
+    if (t < T) {
+        const bf16* xr = x + t * n;
+        for (int64_t k0 = k_lo; k0 < k_hi; k0 += 256) {
+            const int64_t k = k0 + lane * 8;
+            const bool ok = k < k_hi;
+            uint4 u = make_uint4(0, 0, 0, 0);
+            uint32_t keep = 0;
+            if (ok) {
+                u = __ldg(reinterpret_cast<const uint4*>(xr + k));
+                keep = dropout_keep4(d, t, k / 4) | (dropout_keep4(d, t, k / 4 + 1) << 4);
+            }
+            if (bits) {
+                // 4 lanes = 32 consecutive columns = one mask word
+                uint32_t w = keep << (8 * (lane & 3));
+                w |= __shfl_xor_sync(0xffffffffu, w, 1);
+                w |= __shfl_xor_sync(0xffffffffu, w, 2);
+                if ((lane & 3) == 0 && k < k_hi) bits[t * nw + k / 32] = w;
+            }
+            if (!ok) continue;
+            if (xm) {
+                const uint32_t wv[4] = {u.x, u.y, u.z, u.w};
+                uint32_t o[4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
-                o[i] = (w[i] & ((keep >> (2 * i)) & 1u ? 0x0000FFFFu : 0u)) |
-                       (w[i] & ((keep >> (2 * i + 1)) & 1u ? 0xFFFF0000u : 0u));
-            *reinterpret_cast<uint4*>(xm + t * n + k) = make_uint4(o[0], o[1], o[2], o[3]);
-        }
-        if (h) {
-            float xv[8];
-            unpack8(u, xv);
+                for (int i = 0; i < 4; ++i)
+                    o[i] = (wv[i] & ((keep >> (2 * i)) & 1u ? 0x0000FFFFu : 0u)) |
+                           (wv[i] & ((keep >> (2 * i + 1)) & 1u ? 0xFFFF0000u : 0u));
+                *reinterpret_cast<uint4*>(xm + t * n + k) = make_uint4(o[0], o[1], o[2], o[3]);
+            }
+            if (h) {
+                float xv[8];
+                unpack8(u, xv);
 #pragma unroll
-            for (int c = 0; c < 8; ++c) xv[c] = (keep >> c) & 1u ? xv[c] : 0.0f;
+                for (int c = 0; c < 8; ++c) xv[c] = (keep >> c) & 1u ? xv[c] : 0.0f;
 #pragma unroll
-            for (int j = 0; j < RB; ++j) {
-                if (j < r) {
-                    float av[8];
-                    unpack8(__ldg(reinterpret_cast<const uint4*>(a + static_cast<int64_t>(j) * n + k)), av);
+                for (int j = 0; j < RB; ++j) {
+                    if (j < r) {
+                        float av[8];
+                        unpack8(__ldg(reinterpret_cast<const uint4*>(a + static_cast<int64_t>(j) * n + k)), av);
 #pragma unroll
-                    for (int c = 0; c < 8; ++c) acc[j] = fmaf(xv[c], av[c], acc[j]);
+                        for (int c = 0; c < 8; ++c) acc[j] = fmaf(xv[c], av[c], acc[j]);
+                    }
                 }
             }
         }
@@ -78,8 +106,18 @@ __global__ void __launch_bounds__(256) dropout_input_kernel(const bf16* __restri
         for (int o = 16; o > 0; o >>= 1) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
     if (lane == 0) {
 #pragma unroll
-        for (int j = 0; j < RB; ++j)
-            if (j < r) h[t * r + j] = d.q * acc[j];
+        for (int j = 0; j < RB; ++j) part[warp][j] = acc[j];
+    }
+    __syncthreads();
+    if (sub == 0 && lane == 0 && t < T) {
+#pragma unroll
+        for (int j = 0; j < RB; ++j) {
+            if (j < r) {
+                float v = part[warp][j];
+                for (int q = 1; q < SPLIT; ++q) v += part[warp + q][j];
+                h[t * r + j] = d.q * v;
+            }
+        }
     }
 }
 
@@ -97,15 +135,30 @@ __global__ void dropout_mask_kernel(int64_t T, int64_t n, DropoutParams d, uint8
 
 }  // namespace
 
+template <int RB>
+static void launch_input_rb(const bf16* x, int64_t T, int64_t n, const bf16* a, int r, const DropoutParams& d,
+                            float* h, bf16* xm, uint32_t* bits, int num_sms, cudaStream_t stream) {
+    // SPLIT warps per row when one warp per row would leave the SMs short of warps
+    const int64_t want_warps = static_cast<int64_t>(num_sms) * 48;
+    if (T * 2 >= want_warps || n <= 256) {
+        dropout_input_kernel<RB, 1><<<static_cast<unsigned>((T + 7) / 8), 256, 0, stream>>>(x, T, n, a, r, d, h,
+                                                                                          xm, bits);
+    } else if (T * 4 >= want_warps || n <= 1024) {
+        dropout_input_kernel<RB, 2><<<static_cast<unsigned>((T + 3) / 4), 256, 0, stream>>>(x, T, n, a, r, d, h,
+                                                                                          xm, bits);
+    } else {
+        dropout_input_kernel<RB, 8><<<static_cast<unsigned>(T), 256, 0, stream>>>(x, T, n, a, r, d, h, xm, bits);
+    }
+}
+
 cudaError_t launch_dropout_input(const bf16* x, int64_t T, int64_t n, const bf16* a, int r, const DropoutParams& d,
-                                 float* h, bf16* xm, cudaStream_t stream) {
-    if (T <= 0 || (!h && !xm)) return cudaSuccess;
-    const dim3 grid(static_cast<unsigned>((T + 7) / 8));
-    if (r <= 4) dropout_input_kernel<4><<<grid, 256, 0, stream>>>(x, T, n, a, r, d, h, xm);
-    else if (r <= 8) dropout_input_kernel<8><<<grid, 256, 0, stream>>>(x, T, n, a, r, d, h, xm);
-    else if (r <= 16) dropout_input_kernel<16><<<grid, 256, 0, stream>>>(x, T, n, a, r, d, h, xm);
-    else if (r <= 32) dropout_input_kernel<32><<<grid, 256, 0, stream>>>(x, T, n, a, r, d, h, xm);
-    else dropout_input_kernel<64><<<grid, 256, 0, stream>>>(x, T, n, a, r, d, h, xm);
+                                 float* h, bf16* xm, uint32_t* bits, int num_sms, cudaStream_t stream) {
+    if (T <= 0 || (!h && !xm && !bits)) return cudaSuccess;
+    if (r <= 4) launch_input_rb<4>(x, T, n, a, r, d, h, xm, bits, num_sms, stream);
+    else if (r <= 8) launch_input_rb<8>(x, T, n, a, r, d, h, xm, bits, num_sms, stream);
+    else if (r <= 16) launch_input_rb<16>(x, T, n, a, r, d, h, xm, bits, num_sms, stream);
+    else if (r <= 32) launch_input_rb<32>(x, T, n, a, r, d, h, xm, bits, num_sms, stream);
+    else launch_input_rb<64>(x, T, n, a, r, d, h, xm, bits, num_sms, stream);
     return cudaGetLastError();
 }
 

@@ -20,11 +20,11 @@
 //                               256 wide -- 128-byte-aligned MN-major W0 boxes --
 //                               and wait for the flag before their tail)
 //     dX   = bf16(acc + bf16(gh) A)  (epilogue tail MMA)
-// K2 dropout mode (MODE_DX_DROP, LoRA dropout, R9):
+// K2 dropout mode (MODE_DX_DROP, LoRA dropout, R7):
 //     dX   = bf16(acc + q M . (gh A))  -- the mask is per output element, so
 //                               no tail MMA: the epilogue applies gh A on the
 //                               CUDA cores from the A tile in shared memory
-//                               and the Philox keep bits of each element
+//                               and the keep bits K0 packed (32 per word)
 // K1 with dropout: h = q (M . x) A^T comes from K0 (p.h_in) instead of TMEM.
 //
 // Structure (persistent over output tiles, 6 warps per CTA):
@@ -49,7 +49,6 @@
 #include <cstdint>
 
 #include "lora_kernels.h"
-#include "lora_philox.cuh"
 #include "sm100_ptx.cuh"
 
 namespace lora_sm100 {
@@ -583,6 +582,7 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
                         for (int e = 0; e < 16; ++e) lo[e] = 0.0f;
 #pragma unroll
                         for (int j = 0; j < R_PAD; ++j) {
+                            if (j >= p.r) break;   // (uniform) rows r..r_pad-1 of A are zero
                             const uint4 a0 = *reinterpret_cast<const uint4*>(blk + swizzled_offset(j, ch, 128));
                             const uint4 a1 = *reinterpret_cast<const uint4*>(blk + swizzled_offset(j, ch + 1, 128));
                             const uint32_t aw[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
@@ -593,9 +593,9 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
                                 lo[2 * e + 1] = fmaf(hv[j], av.y, lo[2 * e + 1]);
                             }
                         }
-                        uint32_t keep = 0;
-#pragma unroll
-                        for (int i = 0; i < 4; ++i) keep |= dropout_keep4(p.drop, row, col / 4 + i) << (4 * i);
+                        // keep bits of the 16 columns, packed by K0 (32 per word; col % 16 == 0)
+                        const uint32_t keep =
+                            (p.drop_bits[row * ((p.N_out + 31) / 32) + col / 32] >> (col % 32)) & 0xFFFFu;
 #pragma unroll
                         for (int e = 0; e < 16; ++e)
                             if ((keep >> e) & 1u) f[e] = fmaf(p.drop.q, lo[e], f[e]);

@@ -35,6 +35,7 @@ struct FusedGemmParams {
     uint64_t epoch;               // dx: value the flags take in this launch (never reset)
     const float* h_in;            // fwd with dropout: h [T, r] precomputed by K0 (else null: h from the MMA)
     DropoutParams drop;           // dx dropout mode: dX += q M . (gh A) in the epilogue
+    const uint32_t* drop_bits;    // dx dropout mode: keep bits [T, ceil(N_out/32)] from K0
 };
 
 struct FusedGemmMaps {
@@ -182,9 +183,11 @@ cudaError_t launch_merge(const __nv_bfloat16* w0, const __nv_bfloat16* a, const 
 // dst += src (fp32), used by the TP backward when accumulating reduced grads
 cudaError_t launch_add_f32(float* dst, const float* src, int64_t count, cudaStream_t stream);
 
-// K0 (dropout): h = q (M . x) A^T [T, r] fp32 and/or xm = M . x [T, n] bf16 (either may be null)
+// K0 (dropout): h = q (M . x) A^T [T, r] fp32, xm = M . x [T, n] bf16 and the keep bits
+// [T, ceil(n/32)] uint32 (bit c of word w = keep(t, 32 w + c)); any output may be null
 cudaError_t launch_dropout_input(const __nv_bfloat16* x, int64_t T, int64_t n, const __nv_bfloat16* a, int r,
-                                 const DropoutParams& d, float* h, __nv_bfloat16* xm, cudaStream_t stream);
+                                 const DropoutParams& d, float* h, __nv_bfloat16* xm, uint32_t* bits, int num_sms,
+                                 cudaStream_t stream);
 // keep mask M [T, n] uint8 (for lora_dropout_mask)
 cudaError_t launch_dropout_mask(int64_t T, int64_t n, const DropoutParams& d, uint8_t* mask, int num_sms,
                                 cudaStream_t stream);

@@ -1,5 +1,5 @@
 // lora_philox.cuh -- LoRA-dropout keep mask on the device (Listing 3
-// LORA_DROPOUT; reading R9).
+// LORA_DROPOUT; reading R7).
 //
 // Counter-based, so the backward regenerates the forward's mask instead of
 // storing it:  for element (t, k) of a [T, n] adapter input,

@@ -1,5 +1,5 @@
 """GPU parity of the LoRA-dropout path (Listing 3 LORA_DROPOUT, PAPER.md:82;
-DESIGN.md reading R9) against the fp64 oracle: the Philox keep mask bit for
+DESIGN.md reading R7) against the fp64 oracle: the Philox keep mask bit for
 bit, then y, h, dX, dA, dB within the north-star tolerances, bitwise where the
 arithmetic is exact."""
 import numpy as np

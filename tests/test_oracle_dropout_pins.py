@@ -1,5 +1,5 @@
 """Pins for the oracle's LoRA-dropout functions (Listing 3 LORA_DROPOUT = 0.05,
-PAPER.md:82; placement and mask definition: DESIGN.md reading R9).
+PAPER.md:82; placement and mask definition: DESIGN.md reading R7).
 
 The mask generator is pinned to the published Philox4x32-10 known-answer
 vectors and to its counter layout; the dropout forward/backward are pinned by
