@@ -280,6 +280,9 @@ lora_status fwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
     p.h_in = nullptr;
     p.drop = DropoutParams{};
     p.drop_bits = nullptr;
+    p.cs_gh = p.cs_h = nullptr;
+    p.h_split_src = nullptr;
+    p.t_pad = 0;
     if (drop && drop->thr > 0) {
         // LoRA dropout: K0 computes h = q (M . x) A^T; K1 takes it instead of its in-MMA x A^T
         float* hd = h_out ? h_out : reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + W.h);
@@ -328,6 +331,7 @@ static lora_status launch_k3_mma(const GradArgs* pr, int count, cudaStream_t str
         int64_t T, N;
         const float* coef;
         __nv_bfloat16* cs;
+        bool ready;          // cs already written (by K2's gh tile)
         GradMmaSet set;
     } sets[kMaxGradSetsTotal];
     int ns = 0;
@@ -336,11 +340,11 @@ static lora_status launch_k3_mma(const GradArgs* pr, int count, cudaStream_t str
         const int r8 = (g.r + 7) / 8 * 8;
         if (g.da) {
             GradMmaSet s = {g.da, 1, g.n, g.r, r8, 0, g.accumulate, g.scale_a};
-            sets[ns++] = {g.x, g.T, g.n, g.gh, g.cs_a, s};
+            sets[ns++] = {g.x, g.T, g.n, g.gh, g.cs_a, g.cs_a_ready != 0, s};
         }
         if (g.db) {
             GradMmaSet s = {g.db, g.r, 1, g.r, r8, 0, g.accumulate, g.scale_b};
-            sets[ns++] = {g.dy, g.T, g.m, g.h, g.cs_b, s};
+            sets[ns++] = {g.dy, g.T, g.m, g.h, g.cs_b, g.cs_b_ready != 0, s};
         }
     }
     if (ns == 0) return LORA_OK;
@@ -381,10 +385,11 @@ static lora_status launch_k3_mma(const GradArgs* pr, int count, cudaStream_t str
             row += 3 * s.r8;
             G.set[k] = s;
             const int64_t tp = t_pad_of(sets[i].T);
-            if ((st = encode_2d(&G.csmap[k], sets[i].cs, tp, 3 * s.r8, tp * 2, 64, 3 * s.r8, 128, "K3 split "
-                                "coefficients")) != LORA_OK)
+            // inner extent T (not T_pad): TMA zero-fills the token tail, so the pad is never read
+            if ((st = encode_2d(&G.csmap[k], sets[i].cs, sets[i].T, 3 * s.r8, tp * 2, 64, 3 * s.r8, 128,
+                                "K3 split coefficients")) != LORA_OK)
                 return st;
-            SG.s[SG.count++] = {sets[i].coef, sets[i].cs, sets[i].T, tp, s.r, s.r8};
+            if (!sets[i].ready) SG.s[SG.count++] = {sets[i].coef, sets[i].cs, sets[i].T, tp, s.r, s.r8};
             ++k;
             ++J.nsets;
         }
@@ -394,9 +399,11 @@ static lora_status launch_k3_mma(const GradArgs* pr, int count, cudaStream_t str
             return st;
     }
     G.njobs = nj;
-    cudaError_t e = launch_coef_split(SG, stream);
-    if (e != cudaSuccess) return cuda_fail(e, "K3s (coefficient split) launch");
-    ++*launches;
+    cudaError_t e;
+    if (SG.count > 0) {   // coefficient matrices K2 did not already split
+        if ((e = launch_coef_split(SG, stream)) != cudaSuccess) return cuda_fail(e, "K3s (coefficient split) launch");
+        ++*launches;
+    }
     e = launch_grad_mma(G, dev.sms, stream);
     if (e != cudaSuccess) return cuda_fail(e, "K3 (tensor-core dA / dB) launch");
     ++*launches;
@@ -559,6 +566,11 @@ lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
         p.h_in = nullptr;
         p.drop = dropping ? *drop : DropoutParams{};
         p.drop_bits = dropping ? reinterpret_cast<const uint32_t*>(wsb + W.bits) : nullptr;
+        // the gh tile also writes K3's split coefficients (gh; h when it already exists)
+        p.t_pad = t_pad_of(T);
+        p.cs_gh = da ? reinterpret_cast<__nv_bfloat16*>(wsb + W.cs_a) : nullptr;
+        p.h_split_src = h_saved ? h_saved : (dropping && need_h ? hbuf : nullptr);
+        p.cs_h = db && p.h_split_src ? reinterpret_cast<__nv_bfloat16*>(wsb + W.cs_b) : nullptr;
         if (col) {
             if ((st = collect(col, maps, p, rp, cg)) != LORA_OK) return st;
         } else {
@@ -597,6 +609,8 @@ lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
             g.scale_a = scale_a;
             g.cs_a = reinterpret_cast<__nv_bfloat16*>(wsb + W.cs_a);
             g.cs_b = reinterpret_cast<__nv_bfloat16*>(wsb + W.cs_b);
+            g.cs_a_ready = dx != nullptr;                                        // K2 split gh
+            g.cs_b_ready = dx != nullptr && (h_saved != nullptr || (dropping && need_h));
             if (col) {   // grouped backward: one K3 launch for the whole group
                 if (col->k3_count >= kMaxGroup) return fail(LORA_ERR_UNSUPPORTED, "too many grouped problems");
                 col->k3[col->k3_count++] = g;

@@ -474,6 +474,29 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
                     for (int j = 0; j < R_PAD; ++j)
                         if (j < p.r) dst[j] = hv[j];
                 }
+                if (MODE != kModeFwd && row < p.T) {
+                    // K3's B operand: exact hi / mid / lo bf16 split of gh (and of the saved h),
+                    // token-contiguous rows of cs [3 r8, t_pad] (saves K3s a pass)
+                    const int r8 = (p.r + 7) / 8 * 8;
+                    auto split_store = [&](__nv_bfloat16* cs, int k, float v) {
+                        const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+                        const float r0 = v - __bfloat162float(hi);
+                        const __nv_bfloat16 md = __float2bfloat16_rn(r0);
+                        const __nv_bfloat16 lo = __float2bfloat16_rn(r0 - __bfloat162float(md));
+                        cs[static_cast<int64_t>(k) * p.t_pad + row] = hi;
+                        cs[static_cast<int64_t>(r8 + k) * p.t_pad + row] = md;
+                        cs[static_cast<int64_t>(2 * r8 + k) * p.t_pad + row] = lo;
+                    };
+                    if (p.cs_gh != nullptr) {
+#pragma unroll
+                        for (int k = 0; k < R_PAD; ++k)
+                            if (k < r8) split_store(p.cs_gh, k, k < p.r ? hv[k] : 0.0f);
+                    }
+                    if (p.cs_h != nullptr) {
+                        const float* hs = p.h_split_src + row * p.r;
+                        for (int k = 0; k < r8; ++k) split_store(p.cs_h, k, k < p.r ? hs[k] : 0.0f);
+                    }
+                }
                 if (MODE != kModeFwd) {
                     // publish: every thread's gh stores, then one release of the flag
                     __threadfence();

@@ -36,6 +36,12 @@ struct FusedGemmParams {
     const float* h_in;            // fwd with dropout: h [T, r] precomputed by K0 (else null: h from the MMA)
     DropoutParams drop;           // dx dropout mode: dX += q M . (gh A) in the epilogue
     const uint32_t* drop_bits;    // dx dropout mode: keep bits [T, ceil(N_out/32)] from K0
+    // dx: K3's split coefficients written by the gh tile (else null): cs_gh <- gh,
+    // cs_h <- h_split_src; [3 r8, t_pad] bf16 hi / mid / lo rows (see K3s)
+    __nv_bfloat16* cs_gh;
+    __nv_bfloat16* cs_h;
+    const float* h_split_src;
+    int64_t t_pad;
 };
 
 struct FusedGemmMaps {
@@ -96,6 +102,7 @@ struct GradArgs {
     __nv_bfloat16* cs_a;      // tensor-core K3: split gh [3 r8, T_pad] (workspace)
     __nv_bfloat16* cs_b;      // tensor-core K3: split h  [3 r8, T_pad] (workspace)
     float scale_a;            // dA multiplier (1, or q = 1/(1-p) when x is the dropout-masked M . x)
+    int cs_a_ready, cs_b_ready;   // split already written by K2 (no K3s work for that set)
 };
 // several problems of the same rank bucket in one K3 launch
 struct GradGroup {

@@ -255,7 +255,7 @@ def test_launch_counts(L):
     y, h = L.lora_linear_fwd(x, w0, a, b, 16.0)
     assert L.lora_last_launch_count() == 1          # fused K1 (r % 8 == 0: TMA reads B directly)
     L.lora_linear_bwd(x, w0, a, b, dy, 16.0, h_saved=h)
-    assert L.lora_last_launch_count() == 3          # fused K2 (computes gh itself) + K3s split + K3
+    assert L.lora_last_launch_count() == 2          # fused K2 (computes and splits gh, splits h) + K3
     d5 = make_lora_inputs(256, 128, 128, 5, seed=51)
     x, w0, a, b = (dev_bf16(d5[k]) for k in ("x", "w0", "a", "b"))
     L.lora_linear_fwd(x, w0, a, b, 16.0)
@@ -330,7 +330,7 @@ def test_grouped_launch_count(L):
     assert L.lora_last_launch_count() == 1
     L.lora_linear_bwd_grouped([(t["x"], t["w0"], t["a"], t["b"], t["dy"], h) for t, (_, h) in zip(ts, fo)],
                               [16.0, 16.0])
-    assert L.lora_last_launch_count() == 3      # one grouped dX launch + one K3s split + one grouped K3
+    assert L.lora_last_launch_count() == 2      # one grouped dX launch (+ K3 operand split) + one grouped K3
 
 
 # ------------------------------------------------------------------ merge
