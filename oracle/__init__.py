@@ -33,7 +33,7 @@ def build(force: bool = False) -> str:
     """Compile lora_oracle.c with gcc -O2 -fopenmp (no fast-math)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         subprocess.check_call(
-            ["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-std=c11", "-o", _LIB, _SRC])
+            ["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-std=c11", "-o", _LIB, _SRC, "-lm"])
     return _LIB
 
 
@@ -73,6 +73,9 @@ def _load():
         lib.oracle_dropout_mask.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_float, ctypes.c_uint64,
                                             ctypes.c_uint64, _u8p]
         lib.oracle_dropout_mask.restype = ctypes.c_int
+        lib.oracle_adam_step.argtypes = [ctypes.c_int64, _f64p, _f64p, _f64p, _f64p, ctypes.c_int64,
+                                         ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double]
+        lib.oracle_adam_step.restype = ctypes.c_int
         lib.oracle_scale.argtypes = [ctypes.c_int, ctypes.c_double]
         lib.oracle_scale.restype = ctypes.c_double
         lib.oracle_num_threads.restype = ctypes.c_int
@@ -215,3 +218,20 @@ def lora_merge(w0, a, b, alpha):
     if rc != 0:
         raise ValueError(f"oracle_lora_merge failed rc={rc}")
     return out
+
+
+def adam_step(theta, grad, m, v, t, lr, b1=0.9, b2=0.999, eps=1e-8):
+    """One bias-corrected Adam step (Kingma & Ba 2015, Alg. 1) in
+    fp64.  Returns new (theta, m, v) arrays (inputs are not modified)."""
+    th = np.array(theta, np.float64, copy=True).ravel()
+    g = np.ascontiguousarray(grad, np.float64).ravel()
+    mm = np.array(m, np.float64, copy=True).ravel()
+    vv = np.array(v, np.float64, copy=True).ravel()
+    assert th.size == g.size == mm.size == vv.size
+    rc = _load().oracle_adam_step(th.size, th.ctypes.data_as(_f64p), g.ctypes.data_as(_f64p),
+                                  mm.ctypes.data_as(_f64p), vv.ctypes.data_as(_f64p), int(t), float(lr), float(b1),
+                                  float(b2), float(eps))
+    if rc != 0:
+        raise ValueError(f"oracle_adam_step failed rc={rc}")
+    shape = np.shape(theta)
+    return th.reshape(shape), mm.reshape(shape), vv.reshape(shape)

@@ -52,6 +52,7 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#include <math.h>
 #ifdef _OPENMP
 #include <omp.h>
 #endif
@@ -333,6 +334,30 @@ int oracle_lora_merge(int64_t n, int64_t m, int r, double alpha,
             for (int j = 0; j < r; ++j) ba += bf(b[i * r + j]) * bf(a[(int64_t)j * n + k]);
             w_out[i * n + k] = bf(w0[i * n + k]) + s * ba;
         }
+    }
+    return 0;
+}
+
+/*
+ * Adapter update ("standard bias-corrected
+ * Adam"; the paper names no optimizer): Adam, Kingma & Ba, ICLR
+ * 2015, Algorithm 1, one step t >= 1 for `count` independent elements:
+ *   m <- b1 m + (1 - b1) g;   v <- b2 v + (1 - b2) g^2
+ *   m_hat = m / (1 - b1^t);   v_hat = v / (1 - b2^t)
+ *   theta <- theta - lr m_hat / (sqrt(v_hat) + eps)
+ * All in fp64, in place.
+ */
+int oracle_adam_step(int64_t count, double* theta, const double* grad, double* m, double* v, int64_t t,
+                     double lr, double b1, double b2, double eps) {
+    if (count < 0 || t < 1 || !theta || !grad || !m || !v) return -1;
+    const double bc1 = 1.0 - pow(b1, (double)t);
+    const double bc2 = 1.0 - pow(b2, (double)t);
+    for (int64_t i = 0; i < count; ++i) {
+        m[i] = b1 * m[i] + (1.0 - b1) * grad[i];
+        v[i] = b2 * v[i] + (1.0 - b2) * grad[i] * grad[i];
+        const double m_hat = m[i] / bc1;
+        const double v_hat = v[i] / bc2;
+        theta[i] = theta[i] - lr * m_hat / (sqrt(v_hat) + eps);
     }
     return 0;
 }
