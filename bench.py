@@ -216,8 +216,8 @@ def run_ours(args, wl):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
 
-    from paper_2403_11366_b200 import build as _build
-    _build.build()
+    import __graft_entry__
+    __graft_entry__._build_module().build()   # (by path: the package __init__ loads the library)
     import paper_2403_11366_b200 as L
     from paper_2403_11366_b200 import tp
     L.lora_device_check()

@@ -112,6 +112,33 @@ lora_status lora_linear_bwd(const lora_dims* dims, const void* x, const void* w0
 lora_status lora_merge(const lora_dims* dims, const void* w0, const void* a,
                        const void* b, void* w_out, void* stream);
 
+/* ---------------- Adapter update ----------------------------
+ * One bias-corrected Adam step (Kingma & Ba, ICLR 2015, Algorithm 1; the paper
+ * names no optimizer) for up to LORA_ADAM_MAX_TENSORS
+ * adapter tensors (every A and B of a model) in ONE launch, fp32 arithmetic:
+ *   m <- b1 m + (1-b1) g;  v <- b2 v + (1-b2) g^2
+ *   theta <- theta - lr (m / (1-b1^step)) / (sqrt(v / (1-b2^step)) + eps)
+ *   param <- RNE_bf16(theta)      (the bf16 A / B the fused kernels read)
+ * theta is `master` (fp32 master weights) when non-NULL, else `param` itself.
+ * grad is the dA / dB of lora_linear_bwd (after any TP all-reduce).  numel must
+ * be a multiple of 4 (A [r,n], B [m,r] with n, m multiples of 8 always are);
+ * pointers 16-byte aligned; step >= 1; lr >= 0; 0 <= beta < 1; eps >= 0.
+ * Only adapters have optimizer state; W0 is never touched. */
+#define LORA_ADAM_MAX_TENSORS 64
+typedef struct {
+    void* param;          /* bf16 [numel], updated */
+    float* master;        /* fp32 [numel] master weights, updated; or NULL */
+    const float* grad;    /* fp32 [numel] */
+    float* m;             /* fp32 [numel] first moment, updated */
+    float* v;             /* fp32 [numel] second moment, updated */
+    int64_t numel;
+} lora_adam_tensor;
+typedef struct {
+    float lr, beta1, beta2, eps;
+} lora_adam_hparams;
+lora_status lora_adam_step(int count, const lora_adam_tensor* tensors, const lora_adam_hparams* hparams,
+                           int64_t step, void* stream);
+
 /* ---------------- LoRA dropout (Listing 3 LORA_DROPOUT = 0.05) ----
  * Inverted dropout on the ADAPTER input only (reading R7; the frozen
  * path W0 x never sees it).  Keep mask M[t,k] in {0,1}, q = 1 / (1 - p):

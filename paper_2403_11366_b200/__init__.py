@@ -54,6 +54,18 @@ class lora_bwd_problem(ctypes.Structure):
                 ("da", ctypes.c_void_p), ("db", ctypes.c_void_p)]
 
 
+class lora_adam_tensor(ctypes.Structure):
+    _fields_ = [("param", ctypes.c_void_p), ("master", ctypes.c_void_p), ("grad", ctypes.c_void_p),
+                ("m", ctypes.c_void_p), ("v", ctypes.c_void_p), ("numel", ctypes.c_int64)]
+
+
+class lora_adam_hparams(ctypes.Structure):
+    _fields_ = [("lr", ctypes.c_float), ("beta1", ctypes.c_float), ("beta2", ctypes.c_float), ("eps", ctypes.c_float)]
+
+
+LORA_ADAM_MAX_TENSORS = 64
+
+
 class lora_dropout(ctypes.Structure):
     _fields_ = [("p", ctypes.c_float), ("seed", ctypes.c_uint64), ("offset", ctypes.c_uint64)]
 
@@ -82,6 +94,9 @@ lib.lora_linear_fwd_dropout.restype = ctypes.c_int
 lib.lora_linear_bwd_dropout.argtypes = [_dp, _drp, _vp, _vp, _vp, _vp, _fp, _vp, _vp, _fp, _fp, ctypes.c_int,
                                         _vp, ctypes.c_size_t, _vp]
 lib.lora_linear_bwd_dropout.restype = ctypes.c_int
+lib.lora_adam_step.argtypes = [ctypes.c_int, ctypes.POINTER(lora_adam_tensor), ctypes.POINTER(lora_adam_hparams),
+                               ctypes.c_int64, _vp]
+lib.lora_adam_step.restype = ctypes.c_int
 lib.lora_dropout_mask.argtypes = [ctypes.c_int64, ctypes.c_int64, _drp, _vp, _vp]
 lib.lora_dropout_mask.restype = ctypes.c_int
 lib.lora_linear_bwd.restype = _st
@@ -376,3 +391,24 @@ def lora_linear_bwd_grouped(problems, alphas, outs=None, accumulate=False, works
     _check(lib.lora_linear_bwd_grouped(G, dims_arr, probs, 1 if accumulate else 0, _ptr(ws), ws.numel(),
                                        _stream(stream)), "lora_linear_bwd_grouped")
     return res
+
+
+def lora_adam_step(tensors, step, lr, betas=(0.9, 0.999), eps=1e-8, stream=None):
+    """One bias-corrected Adam step for adapter tensors in ONE launch (SURVEY.md
+    8(f) N3; include/lora.h).  tensors: list of (param bf16, grad fp32, m fp32,
+    v fp32, master fp32 or None), all CUDA, same numel per entry; updated in place."""
+    n = len(tensors)
+    if not 1 <= n <= LORA_ADAM_MAX_TENSORS:
+        raise ValueError(f"1 <= len(tensors) <= {LORA_ADAM_MAX_TENSORS}")
+    arr = (lora_adam_tensor * n)()
+    for i, (p, g, m, v, w) in enumerate(tensors):
+        numel = p.numel()
+        if p.dtype != torch.bfloat16 or any(t.dtype != torch.float32 or t.numel() != numel
+                                            for t in (g, m, v) + ((w,) if w is not None else ())):
+            raise ValueError(f"tensor {i}: param bf16 and grad/m/v/master fp32 of equal numel")
+        for t in (p, g, m, v) + ((w,) if w is not None else ()):
+            if not t.is_contiguous() or not t.is_cuda:
+                raise ValueError(f"tensor {i}: contiguous CUDA tensors required")
+        arr[i] = lora_adam_tensor(_ptr(p), _ptr(w), _ptr(g), _ptr(m), _ptr(v), numel)
+    hp = lora_adam_hparams(float(lr), float(betas[0]), float(betas[1]), float(eps))
+    _check(lib.lora_adam_step(n, arr, ctypes.byref(hp), int(step), _stream(stream)), "lora_adam_step")

@@ -767,6 +767,44 @@ lora_status lora_dropout_mask(int64_t tokens, int64_t d_in, const lora_dropout* 
     return st;
 }
 
+lora_status lora_adam_step(int count, const lora_adam_tensor* tensors, const lora_adam_hparams* hp, int64_t step,
+                           void* stream) {
+    set_launches(0);
+    if (count < 1 || count > LORA_ADAM_MAX_TENSORS || !tensors || !hp)
+        return fail(LORA_ERR_INVALID, "lora_adam_step: need 1..%d tensors and hparams", LORA_ADAM_MAX_TENSORS);
+    if (step < 1) return fail(LORA_ERR_INVALID, "lora_adam_step: step = %lld must be >= 1", (long long)step);
+    if (!(hp->lr >= 0.0f) || !(hp->beta1 >= 0.0f && hp->beta1 < 1.0f) || !(hp->beta2 >= 0.0f && hp->beta2 < 1.0f) ||
+        !(hp->eps >= 0.0f))
+        return fail(LORA_ERR_INVALID, "lora_adam_step: lr >= 0, 0 <= beta < 1, eps >= 0 required");
+    static thread_local AdamGroup G;
+    G.count = count;
+    for (int i = 0; i < count; ++i) {
+        const lora_adam_tensor& t = tensors[i];
+        if (t.numel < 0 || t.numel % 4 != 0)
+            return fail(LORA_ERR_SHAPE, "lora_adam_step: tensor %d numel = %lld must be a multiple of 4", i,
+                        (long long)t.numel);
+        if (t.numel > 0 && (!t.param || !t.grad || !t.m || !t.v))
+            return fail(LORA_ERR_INVALID, "lora_adam_step: tensor %d has a NULL param / grad / m / v", i);
+        const void* ptrs[] = {t.param, t.master, t.grad, t.m, t.v};
+        for (const void* q : ptrs)
+            if (q && !aligned16(q)) return fail(LORA_ERR_ALIGN, "lora_adam_step: tensor %d pointer %p", i, q);
+        G.t[i] = {static_cast<__nv_bfloat16*>(t.param), t.master, t.grad, t.m, t.v, t.numel};
+    }
+    G.lr = hp->lr;
+    G.b1 = hp->beta1;
+    G.b2 = hp->beta2;
+    G.eps = hp->eps;
+    G.bc1 = static_cast<float>(1.0 - std::pow(static_cast<double>(hp->beta1), static_cast<double>(step)));
+    G.bc2 = static_cast<float>(1.0 - std::pow(static_cast<double>(hp->beta2), static_cast<double>(step)));
+    DevInfo dev;
+    lora_status st = device_info(&dev);
+    if (st != LORA_OK) return st;
+    cudaError_t e = launch_adam(G, dev.sms, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "adam launch");
+    set_launches(1);
+    return LORA_OK;
+}
+
 lora_status lora_merge(const lora_dims* dims, const void* w0, const void* a, const void* b, void* w_out,
                        void* stream) {
     int launches = 0;

@@ -190,6 +190,68 @@ cudaError_t launch_merge(const bf16* w0, const bf16* a, const bf16* b, int64_t n
     }
 }
 
+// ------------------------------------------------------------------ N3: adapter update
+// One bias-corrected Adam step (Kingma & Ba 2015, Alg. 1) for
+// all adapter tensors of a model in ONE launch: 4 elements per thread (16-byte
+// fp32 loads of grad / m / v / master, 8-byte bf16 param), grid-stride over the
+// concatenated element range.  fp32 arithmetic; the bf16 param the fused
+// kernels read is RNE(master).
+__global__ void __launch_bounds__(256) adam_kernel(const __grid_constant__ AdamGroup G) {
+    const int64_t total4 = G.start4[G.count];
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    int ti = 0;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total4; i += stride) {
+        while (i >= G.start4[ti + 1]) ++ti;   // i only grows: the tensor index only moves forward
+        const AdamTensor& t = G.t[ti];
+        const int64_t e = (i - G.start4[ti]) * 4;
+        const float4 g = *reinterpret_cast<const float4*>(t.grad + e);
+        float4 m = *reinterpret_cast<const float4*>(t.m + e);
+        float4 v = *reinterpret_cast<const float4*>(t.v + e);
+        float th[4];
+        if (t.master) {
+            const float4 w = *reinterpret_cast<const float4*>(t.master + e);
+            th[0] = w.x; th[1] = w.y; th[2] = w.z; th[3] = w.w;
+        } else {
+            const uint2 u = *reinterpret_cast<const uint2*>(t.param + e);
+            const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+            const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+            th[0] = a.x; th[1] = a.y; th[2] = b.x; th[3] = b.y;
+        }
+        float* mp = &m.x;
+        float* vp = &v.x;
+        const float* gp = &g.x;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            mp[c] = G.b1 * mp[c] + (1.0f - G.b1) * gp[c];
+            vp[c] = G.b2 * vp[c] + (1.0f - G.b2) * gp[c] * gp[c];
+            const float m_hat = mp[c] / G.bc1;
+            const float v_hat = vp[c] / G.bc2;
+            th[c] = th[c] - G.lr * m_hat / (sqrtf(v_hat) + G.eps);
+        }
+        *reinterpret_cast<float4*>(t.m + e) = m;
+        *reinterpret_cast<float4*>(t.v + e) = v;
+        if (t.master) *reinterpret_cast<float4*>(t.master + e) = make_float4(th[0], th[1], th[2], th[3]);
+        const __nv_bfloat162 p0 = __floats2bfloat162_rn(th[0], th[1]);
+        const __nv_bfloat162 p1 = __floats2bfloat162_rn(th[2], th[3]);
+        *reinterpret_cast<uint2*>(t.param + e) =
+            make_uint2(*reinterpret_cast<const uint32_t*>(&p0), *reinterpret_cast<const uint32_t*>(&p1));
+    }
+}
+
+cudaError_t launch_adam(AdamGroup& G, int num_sms, cudaStream_t stream) {
+    if (G.count < 1 || G.count > kMaxAdamTensors) return cudaErrorInvalidValue;
+    int64_t total4 = 0;
+    for (int i = 0; i < G.count; ++i) {
+        G.start4[i] = total4;
+        total4 += G.t[i].numel / 4;
+    }
+    G.start4[G.count] = total4;
+    if (total4 == 0) return cudaSuccess;
+    const int64_t blocks = std::min<int64_t>((total4 + 255) / 256, static_cast<int64_t>(num_sms) * 8);
+    adam_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(G);
+    return cudaGetLastError();
+}
+
 __global__ void add_f32_kernel(float* __restrict__ dst, const float* __restrict__ src, int64_t count) {
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += stride)

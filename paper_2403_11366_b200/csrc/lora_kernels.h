@@ -187,6 +187,24 @@ cudaError_t launch_merge(const __nv_bfloat16* w0, const __nv_bfloat16* a, const 
                          int64_t n, int64_t m, int r, float scale, __nv_bfloat16* w_out,
                          cudaStream_t stream);
 
+// N3: one Adam step for up to kMaxAdamTensors adapter tensors (numel % 4 == 0)
+constexpr int kMaxAdamTensors = 64;
+struct AdamTensor {
+    __nv_bfloat16* param;
+    float* master;      // may be null
+    const float* grad;
+    float* m;
+    float* v;
+    int64_t numel;
+};
+struct AdamGroup {
+    AdamTensor t[kMaxAdamTensors];
+    int64_t start4[kMaxAdamTensors + 1];   // filled in by launch_adam
+    int count;
+    float lr, b1, b2, eps, bc1, bc2;        // bc = 1 - beta^t
+};
+cudaError_t launch_adam(AdamGroup& G, int num_sms, cudaStream_t stream);
+
 // dst += src (fp32), used by the TP backward when accumulating reduced grads
 cudaError_t launch_add_f32(float* dst, const float* src, int64_t count, cudaStream_t stream);
 

@@ -26,7 +26,8 @@ VARIANTS.update({k: tuple(v) for k, v in EXTRA.items()})
 
 
 def build():
-    from paper_2403_11366_b200 import build as b
+    import __graft_entry__
+    b = __graft_entry__._build_module()
     os.makedirs(OUT, exist_ok=True)
     for name, defs in VARIANTS.items():
         b.build(out=os.path.join(OUT, f"liblora_{name}.so"), defines=defs)
