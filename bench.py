@@ -447,6 +447,43 @@ def run_ours(args, wl):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
 
+    # ---- the HBM-bound kernels of the path, timed alone (report them in
+    # GB/s against the measured HBM bandwidth): K4 merge of the first linear, and the
+    # gradient-only backward (gh pre-pass + K3s + K3) -- L2 flushed before each call
+    aux = {}
+    if world == 1:
+        e = lin[0]
+        l0_ = e["l"]
+        w_out = torch.empty_like(e["w0"])
+        da_, db_ = torch.empty_like(e["da"]), torch.empty_like(e["db"])
+
+        def timed(fn, reps=20):
+            for _ in range(3):
+                fn()
+            ts = []
+            for _ in range(reps):
+                flush.fill_(1)
+                a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a0.record(stream)
+                fn()
+                a1.record(stream)
+                torch.cuda.synchronize()
+                ts.append(a0.elapsed_time(a1) * 1e-3)
+            return float(np.median(ts))
+
+        T0, n0, m0, r0 = l0_.T, l0_.n, l0_.m, l0_.r
+        t_merge = timed(lambda: L.lora_merge(e["w0"], e["a"], e["b"], l0_.alpha, w_out=w_out,
+                                             stream=torch.cuda.current_stream()))
+        t_grads = timed(lambda: L.lora_linear_bwd(e["x"], e["w0"], e["a"], e["b"], e["dy"], l0_.alpha,
+                                                  h_saved=e["h"], want_dx=False, da=da_, db=db_,
+                                                  workspace=e["ws_b"], stream=torch.cuda.current_stream()))
+        merge_bytes = 4 * m0 * n0 + 2 * r0 * (m0 + n0)
+        # dY read twice (gh pre-pass, dB), x once, coefficients ~ 16 T r
+        grads_bytes = 2 * T0 * (2 * m0 + n0) + 16 * T0 * r0
+        aux = {"merge": {"us": t_merge * 1e6, "bytes": merge_bytes, "gbs": merge_bytes / t_merge / 1e9},
+               "grads_only": {"us": t_grads * 1e6, "bytes": grads_bytes, "gbs": grads_bytes / t_grads / 1e9,
+                              "kernels": "gh pre-pass + K3s split + K3 (lora_linear_bwd, dx = NULL)"}}
+
     # ---- report (rank 0)
     if rank == 0:
         peaks, peak_src = load_peaks()
@@ -498,6 +535,11 @@ def run_ours(args, wl):
             "gpu_launches": gpu_launches,
             "clocks": clk.summary(),
         }
+        if aux:
+            hbm = peaks.get("hbm_gbs", FALLBACK_PEAKS["hbm_gbs"])
+            for v in aux.values():
+                v["frac_of_hbm"] = v["gbs"] / hbm
+            line["hbm_bound_kernels"] = dict(aux, hbm_peak_gbs=hbm, linear=l0.name)
         print(json.dumps(line), flush=True)
     if comm is not None:
         comm.close()

@@ -339,11 +339,11 @@ static lora_status launch_k3_mma(const GradArgs* pr, int count, cudaStream_t str
         const GradArgs& g = pr[i];
         const int r8 = (g.r + 7) / 8 * 8;
         if (g.da) {
-            GradMmaSet s = {g.da, 1, g.n, g.r, r8, 0, g.accumulate, g.scale_a};
+            GradMmaSet s = {g.da, 1, g.n, g.r, r8, 0, g.accumulate, g.scale_a, 3};
             sets[ns++] = {g.x, g.T, g.n, g.gh, g.cs_a, g.cs_a_ready != 0, s};
         }
         if (g.db) {
-            GradMmaSet s = {g.db, g.r, 1, g.r, r8, 0, g.accumulate, g.scale_b};
+            GradMmaSet s = {g.db, g.r, 1, g.r, r8, 0, g.accumulate, g.scale_b, 3};
             sets[ns++] = {g.dy, g.T, g.m, g.h, g.cs_b, g.cs_b_ready != 0, s};
         }
     }
@@ -363,7 +363,7 @@ static lora_status launch_k3_mma(const GradArgs* pr, int count, cudaStream_t str
             }
         if (job_of[i] < 0) {
             GradMmaJob& J = G.job[nj];
-            J.T = sets[i].T; J.N = sets[i].N; J.nsets = 0;
+            J.T = sets[i].T; J.N = sets[i].N; J.nsets = 0; J.a_kmajor = 0;
             jx[nj] = sets[i].X;
             used[nj] = 0;
             job_of[i] = nj++;
@@ -406,6 +406,30 @@ static lora_status launch_k3_mma(const GradArgs* pr, int count, cudaStream_t str
     }
     e = launch_grad_mma(G, dev.sms, stream);
     if (e != cudaSuccess) return cuda_fail(e, "K3 (tensor-core dA / dB) launch");
+    ++*launches;
+    return LORA_OK;
+}
+
+// Row projection on the tensor cores: out[t, j] = scale * sum_k X[t, k] P[j, k] for
+// X [T, K] bf16 and P [r, K] bf16 (K-contiguous rows: A itself, or B^T) -- the K3
+// kernel with X read K-major and P as a single (unsplit, already bf16) coefficient set.
+// Used for gh = s dY B when dX is not requested and for h = x A^T when h was not saved.
+static lora_status launch_rowproj_mma(const void* X, int64_t T, int64_t K, const void* P, int r, float scale,
+                                      float* out, cudaStream_t stream, int* launches) {
+    DevInfo dev;
+    lora_status st = device_info(&dev);
+    if (st != LORA_OK) return st;
+    static thread_local GradMmaGroup G;
+    const int r8 = (r + 7) / 8 * 8;
+    GradMmaJob& J = G.job[0];
+    J.T = K; J.N = T; J.set0 = 0; J.nsets = 1; J.q_used = r8; J.q_pad = (r8 + 15) / 16 * 16; J.a_kmajor = 1;
+    G.set[0] = GradMmaSet{out, r, 1, r, r8, 0, 0, scale, 1};
+    if ((st = encode_2d(&G.xmap[0], X, K, T, K * 2, 64, 64, 128, "row-projection activation")) != LORA_OK) return st;
+    // P rows r..r8-1 are out of bounds: TMA zero-fills them
+    if ((st = encode_2d(&G.csmap[0], P, K, r, K * 2, 64, r8, 128, "row-projection operand")) != LORA_OK) return st;
+    G.njobs = 1;
+    cudaError_t e = launch_grad_mma(G, dev.sms, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "row projection (tensor cores) launch");
     ++*launches;
     return LORA_OK;
 }
@@ -583,10 +607,14 @@ lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
     }
     if (!(stages & 2)) return LORA_OK;
     if (!dx && da) {
-        // K2a: gh = s dY B [T, r] fp32 for dA when the input gradient is not requested
-        if ((e = launch_gh(dya, static_cast<const __nv_bfloat16*>(b), T, m, r, s, gh, stream)) != cudaSuccess)
-            return cuda_fail(e, "gh launch");
+        // K2a: gh = s dY B [T, r] fp32 for dA when the input gradient is not requested --
+        // B^T [r, m] (B6, into the unused B8 slot) then the tensor-core row projection
+        auto* bt = reinterpret_cast<__nv_bfloat16*>(wsb + W.b8);
+        if ((e = launch_pack_b(static_cast<const __nv_bfloat16*>(b), m, r, nullptr, bt, dev.sms, stream)) !=
+            cudaSuccess)
+            return cuda_fail(e, "B^T pack launch");
         ++*launches;
+        if ((st = launch_rowproj_mma(dya, T, m, bt, r, s, gh, stream, launches)) != LORA_OK) return st;
     }
     const float* hsrc = h_saved;
     const __nv_bfloat16* xk3 = xa;   // K3's dA activation: x, or M . x under dropout
@@ -596,9 +624,8 @@ lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
         xk3 = xm;
         scale_a = drop->q;
     } else if (need_h) {
-        if ((e = launch_rowproj(xa, T, n, aa, n, 0, r, 1.0f, hbuf, stream)) != cudaSuccess)
-            return cuda_fail(e, "h rowproj");
-        ++*launches;
+        // K3a: h = x A^T recomputed on the tensor cores (A [r, n] is already K-contiguous)
+        if ((st = launch_rowproj_mma(xa, T, n, aa, r, 1.0f, hbuf, stream, launches)) != LORA_OK) return st;
         hsrc = hbuf;
     }
     if (da || db) {

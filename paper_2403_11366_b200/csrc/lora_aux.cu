@@ -121,9 +121,17 @@ __global__ void __launch_bounds__(256) merge_kernel(const bf16* __restrict__ w0,
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t k0 = static_cast<int64_t>(blockIdx.x) * 256;
     const int64_t i0 = static_cast<int64_t>(blockIdx.y) * 64;
-    for (int idx = threadIdx.x; idx < RB * 256; idx += 256) {
-        const int j = idx >> 8, kk = idx & 255;
-        sA[idx] = (j < r && k0 + kk < n) ? __bfloat162float(a[static_cast<int64_t>(j) * n + k0 + kk]) : 0.0f;
+    for (int idx = threadIdx.x; idx < RB * 32; idx += 256) {   // 8 columns per thread (n % 8 == 0)
+        const int j = idx >> 5, kk = (idx & 31) * 8;
+        float f[8];
+        if (j < r && k0 + kk < n) {
+            bf16x8_to_f32(__ldg(reinterpret_cast<const uint4*>(a + static_cast<int64_t>(j) * n + k0 + kk)), f);
+        } else {
+#pragma unroll
+            for (int c = 0; c < 8; ++c) f[c] = 0.0f;
+        }
+        *reinterpret_cast<float4*>(sA + j * 256 + kk) = make_float4(f[0], f[1], f[2], f[3]);
+        *reinterpret_cast<float4*>(sA + j * 256 + kk + 4) = make_float4(f[4], f[5], f[6], f[7]);
     }
     for (int idx = threadIdx.x; idx < 64 * RB; idx += 256) {
         const int ii = idx / RB, j = idx - ii * RB;
@@ -132,14 +140,21 @@ __global__ void __launch_bounds__(256) merge_kernel(const bf16* __restrict__ w0,
     __syncthreads();
     const int kc = lane * 8;
     if (k0 + kc >= n) return;
-#pragma unroll 1
+    // all 8 rows' 16-byte W0 loads in flight before any math (HBM latency)
+    uint4 wraw[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const int64_t i = i0 + warp + 8 * q;
+        wraw[q] = i < m ? __ldg(reinterpret_cast<const uint4*>(w0 + i * n + k0 + kc)) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
     for (int q = 0; q < 8; ++q) {
         const int ii = warp + 8 * q;
         const int64_t i = i0 + ii;
         if (i >= m) break;
         const int64_t off = i * n + k0 + kc;
         float wv[8];
-        load_bf16_vec<8>(w0 + off, wv);
+        bf16x8_to_f32(wraw[q], wv);
         float ba[8];
 #pragma unroll
         for (int c = 0; c < 8; ++c) ba[c] = 0.0f;

@@ -208,16 +208,21 @@ __global__ void __launch_bounds__(THREADS, 1) grad_mma_kernel(const __grid_const
         if (lane == 0) {
             const int nbox = two ? 2 : 1;
             uint32_t tx = nbox * X_BOX;
-            for (int j = 0; j < J.nsets; ++j) tx += 3 * G.set[J.set0 + j].r8 * 128;
+            for (int j = 0; j < J.nsets; ++j) tx += G.set[J.set0 + j].nsplit * G.set[J.set0 + j].r8 * 128;
             const uint64_t pol = l2_policy_evict_first();
             for (int i = 0, s = 0, ph = 0; i < nkb; ++i) {
                 mbar_wait(&empty[s], ph ^ 1);
                 uint8_t* sx = smem + s * stage_bytes;
                 mbar_arrive_expect_tx(&full[s], tx);
                 const int t0 = (kb0 + i) * KB;
-                for (int b = 0; b < nbox; ++b)
-                    tma_load_2d_hint(sx + b * X_BOX, &G.xmap[jb], static_cast<int32_t>(col0 + 64 * b), t0,
-                                     &full[s], pol);
+                for (int b = 0; b < nbox; ++b) {
+                    if (J.a_kmajor)   // rows col0 + 64 b .. of X [N, T], reduction columns t0 ..
+                        tma_load_2d_hint(sx + b * X_BOX, &G.xmap[jb], t0, static_cast<int32_t>(col0 + 64 * b),
+                                         &full[s], pol);
+                    else              // columns col0 + 64 b .. of X [T, N], reduction rows t0 ..
+                        tma_load_2d_hint(sx + b * X_BOX, &G.xmap[jb], static_cast<int32_t>(col0 + 64 * b), t0,
+                                         &full[s], pol);
+                }
                 for (int j = 0; j < J.nsets; ++j)
                     tma_load_2d(sx + X_BYTES + G.set[J.set0 + j].row0 * 128, &G.csmap[J.set0 + j], t0, 0,
                                 &full[s]);
@@ -227,17 +232,20 @@ __global__ void __launch_bounds__(THREADS, 1) grad_mma_kernel(const __grid_const
     } else if (warp == 1) {
         // ---------------- MMA issuer
         if (lane == 0) {
-            const uint32_t idesc = make_idesc_bf16(128, static_cast<uint32_t>(q_pad), 1, 0);
+            const uint32_t idesc = make_idesc_bf16(128, static_cast<uint32_t>(q_pad), J.a_kmajor ? 0u : 1u, 0);
             for (int i = 0, s = 0, ph = 0; i < nkb; ++i) {
                 mbar_wait(&full[s], ph);
                 tc_fence_after();
                 const uint32_t sx = smem_u32(smem + s * stage_bytes);
 #pragma unroll
                 for (int kk = 0; kk < KB / 16; ++kk) {
-                    // X^T: two 64-column boxes, LBO = box stride, SBO = 8 tokens; Cs K-major SW128
-                    umma_f16(tmem_base, make_smem_desc(sx + kk * 16 * 128, X_BOX, 1024, kLayoutSW128),
-                             make_smem_desc(sx + X_BYTES + kk * 32, 16, 1024, kLayoutSW128), idesc,
-                             (i > 0 || kk > 0) ? 1u : 0u);
+                    // MN-major X^T: two 64-column boxes, LBO = box stride, SBO = 8 tokens;
+                    // K-major X: 128 rows of 128 bytes, SBO = 8 rows.  Cs: K-major SW128
+                    const uint64_t a_desc = J.a_kmajor
+                        ? make_smem_desc(sx + kk * 32, 16, 1024, kLayoutSW128)
+                        : make_smem_desc(sx + kk * 16 * 128, X_BOX, 1024, kLayoutSW128);
+                    umma_f16(tmem_base, a_desc, make_smem_desc(sx + X_BYTES + kk * 32, 16, 1024, kLayoutSW128),
+                             idesc, (i > 0 || kk > 0) ? 1u : 0u);
                 }
                 umma_commit(&empty[s]);
                 if (++s == stages) { s = 0; ph ^= 1; }
@@ -261,8 +269,13 @@ __global__ void __launch_bounds__(THREADS, 1) grad_mma_kernel(const __grid_const
                 uint32_t h[8], md[8], l[8];
                 if (nkb > 0) {   // warp-uniform
                     tmem_ld_32x32b_x8(tbase + st.row0 + k0, h);
-                    tmem_ld_32x32b_x8(tbase + st.row0 + st.r8 + k0, md);
-                    tmem_ld_32x32b_x8(tbase + st.row0 + 2 * st.r8 + k0, l);
+                    if (st.nsplit == 3) {
+                        tmem_ld_32x32b_x8(tbase + st.row0 + st.r8 + k0, md);
+                        tmem_ld_32x32b_x8(tbase + st.row0 + 2 * st.r8 + k0, l);
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) md[u] = l[u] = 0u;
+                    }
                     tmem_ld_wait();
                 }
 #pragma unroll

@@ -125,11 +125,13 @@ struct GradMmaSet {
     int64_t stride_col, stride_k;
     int r, r8, row0, accumulate;
     float scale;
+    int nsplit;                 // 3: rows hi / mid / lo of an fp32 coefficient (K3s); 1: a bf16 operand as is
 };
 struct GradMmaJob {
-    int64_t T, N;
+    int64_t T, N;               // T: reduction extent (k-blocks of 64), N: output extent (MMA M, 128 per CTA)
     int set0, nsets;            // sets [set0, set0 + nsets) of the group
-    int q_used, q_pad;          // q_used = 3 sum r8; q_pad = roundup(q_used, 16) (MMA N, <= 256)
+    int q_used, q_pad;          // q_used = sum nsplit r8; q_pad = roundup(q_used, 16) (MMA N, <= 256)
+    int a_kmajor;               // 0: X [T, N] read MN-major (dA, dB); 1: X [N, T] read K-major (row projections)
 };
 struct GradMmaGroup {
     CUtensorMap xmap[kMaxGradJobs];
