@@ -301,16 +301,12 @@ lora_status fwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
     return LORA_OK;
 }
 
-// K3 implementation: "mma" (default, tensor cores), or the CUDA-core
-// experiments "cluster" | "tma" | "ldg" (LORA_K3).
-enum K3Mode { kK3Mma, kK3Cluster, kK3Tma, kK3Ldg };
+// K3 implementation: "mma" (default, tensor cores) or the CUDA-core
+// comparison kernel "cluster" (LORA_K3=cluster).
+enum K3Mode { kK3Mma, kK3Cluster };
 static K3Mode k3_mode() {
     const char* v = getenv("LORA_K3");
-    if (!v) return kK3Mma;
-    if (!strcmp(v, "cluster")) return kK3Cluster;
-    if (!strcmp(v, "tma")) return kK3Tma;
-    if (!strcmp(v, "ldg")) return kK3Ldg;
-    return kK3Mma;
+    return v && !strcmp(v, "cluster") ? kK3Cluster : kK3Mma;
 }
 
 // K3 on the tensor cores for `count` problems: one dA set (X = x, C = gh) and
@@ -630,39 +626,20 @@ lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
     }
     if (da || db) {
         const K3Mode k3 = k3_mode();
-        if (k3 == kK3Mma || k3 == kK3Cluster) {
-            if (dropping && k3 != kK3Mma) return fail(LORA_ERR_UNSUPPORTED, "LoRA dropout needs the default K3");
-            GradArgs g = make_grad_args(T, n, m, r, s, xk3, gh, dya, hsrc, da, db, accumulate);
-            g.scale_a = scale_a;
-            g.cs_a = reinterpret_cast<__nv_bfloat16*>(wsb + W.cs_a);
-            g.cs_b = reinterpret_cast<__nv_bfloat16*>(wsb + W.cs_b);
-            g.cs_a_ready = dx != nullptr;                                        // K2 split gh
-            g.cs_b_ready = dx != nullptr && (h_saved != nullptr || (dropping && need_h));
-            if (col) {   // grouped backward: one K3 launch for the whole group
-                if (col->k3_count >= kMaxGroup) return fail(LORA_ERR_UNSUPPORTED, "too many grouped problems");
-                col->k3[col->k3_count++] = g;
-                return LORA_OK;
-            }
-            if (k3 == kK3Mma) return launch_k3_mma(&g, 1, stream, launches);
-            e = launch_grad_reduce_cluster(T, n, m, r, s, xa, gh, dya, hsrc, da, db, accumulate, stream, launches);
-        } else if (r % 4 == 0 && k3 == kK3Tma) {
-            // TMA-ring variant: coefficient rows (4r bytes) are TMA-legal when r % 4 == 0
-            GradMaps gm;
-            const int sc = grad_strip_cols();
-            if ((st = encode_2d(&gm.x, x, n, T, n * 2, sc, 64, 0, "x")) != LORA_OK) return st;
-            if ((st = encode_2d(&gm.dy, dy, m, T, m * 2, sc, 64, 0, "dy")) != LORA_OK) return st;
-            const float* ghp = da ? gh : hsrc;   // unused map when the gradient is not requested
-            const float* hp = db ? hsrc : gh;
-            if ((st = encode_2d(&gm.gh, ghp, r, T, size_t(r) * 4, r, 64, 0, "gh", CU_TENSOR_MAP_DATA_TYPE_FLOAT32)) !=
-                LORA_OK)
-                return st;
-            if ((st = encode_2d(&gm.h, hp, r, T, size_t(r) * 4, r, 64, 0, "h", CU_TENSOR_MAP_DATA_TYPE_FLOAT32)) !=
-                LORA_OK)
-                return st;
-            e = launch_grad_reduce_tma(gm, T, n, m, r, s, da, db, accumulate, stream, launches);
-        } else {
-            e = launch_grad_reduce(T, n, m, r, s, xa, gh, dya, hsrc, da, db, accumulate, stream, launches);
+        if (dropping && k3 != kK3Mma) return fail(LORA_ERR_UNSUPPORTED, "LoRA dropout needs the default K3");
+        GradArgs g = make_grad_args(T, n, m, r, s, xk3, gh, dya, hsrc, da, db, accumulate);
+        g.scale_a = scale_a;
+        g.cs_a = reinterpret_cast<__nv_bfloat16*>(wsb + W.cs_a);
+        g.cs_b = reinterpret_cast<__nv_bfloat16*>(wsb + W.cs_b);
+        g.cs_a_ready = dx != nullptr;                                        // K2 split gh
+        g.cs_b_ready = dx != nullptr && (h_saved != nullptr || (dropping && need_h));
+        if (col) {   // grouped backward: one K3 launch for the whole group
+            if (col->k3_count >= kMaxGroup) return fail(LORA_ERR_UNSUPPORTED, "too many grouped problems");
+            col->k3[col->k3_count++] = g;
+            return LORA_OK;
         }
+        if (k3 == kK3Mma) return launch_k3_mma(&g, 1, stream, launches);
+        e = launch_grad_reduce_cluster(T, n, m, r, s, xk3, gh, dya, hsrc, da, db, accumulate, stream, launches);
         if (e != cudaSuccess) return cuda_fail(e, "grad reduce launch");
     }
     return LORA_OK;

@@ -1,8 +1,8 @@
-// lora_aux.cu -- the CUDA-core kernels of the LoRA hot path (sm_100a):
-//   K3a rowproj     : h = x A^T or gh = s dY B for the NULL-h / NULL-dx paths
+// lora_aux.cu -- the CUDA-core kernels of the LoRA path (sm_100a):
 //   K4  merge       : W' = bf16(W0 + s B A) (Eq. 1 line 2)
-// These steps are skinny (rank r <= 64) and bandwidth-bound, so they run on
-// the CUDA cores ("Kernels").
+//   N3  adam        : one bias-corrected Adam step for the adapters
+//   helpers         : fp32 add (TP gradient accumulation), zero fill
+// All are bandwidth-bound elementwise work ("Kernels").
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -26,87 +26,7 @@ __device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float (&f)[8]) {
     }
 }
 
-template <int CPT>
-__device__ __forceinline__ void load_bf16_vec(const bf16* p, float (&f)[CPT]) {
-    if constexpr (CPT == 8) {
-        uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
-        bf16x8_to_f32(u, f);
-    } else if constexpr (CPT == 4) {
-        uint2 u = __ldg(reinterpret_cast<const uint2*>(p));
-        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
-        float2 a = __bfloat1622float2(h[0]), b = __bfloat1622float2(h[1]);
-        f[0] = a.x; f[1] = a.y; f[2] = b.x; f[3] = b.y;
-    } else {
-        uint32_t u = __ldg(reinterpret_cast<const unsigned int*>(p));
-        float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u));
-        f[0] = a.x; f[1] = a.y;
-    }
-}
-
 static int rank_bucket(int r) { return r <= 4 ? 4 : r <= 8 ? 8 : r <= 16 ? 16 : r <= 32 ? 32 : 64; }
-
-// ------------------------------------------------------------------ K3a
-// out[t, j] = scale * sum_k X[t, k] P(j, k), one warp per token row, 16-byte
-// loads of X.  P(j, k) = P[j * ldp + k] (A [r, n]) or, when p_t, P[k * ldp + j]
-// (B [m, r8] read row by row).
-template <int RB>
-__global__ void __launch_bounds__(256) rowproj_kernel(const bf16* __restrict__ X, int64_t T, int64_t K,
-                                                      const bf16* __restrict__ P, int64_t ldp, int p_t, int r,
-                                                      float scale, float* __restrict__ out) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + warp;
-    if (row >= T) return;
-    float acc[RB];
-#pragma unroll
-    for (int j = 0; j < RB; ++j) acc[j] = 0.0f;
-    const bf16* xr = X + row * K;
-    for (int64_t k = lane * 8; k < K; k += 256) {
-        float xv[8];
-        load_bf16_vec<8>(xr + k, xv);
-        if (!p_t) {
-#pragma unroll
-            for (int j = 0; j < RB; ++j) {
-                if (j < r) {
-                    float pv[8];
-                    load_bf16_vec<8>(P + static_cast<int64_t>(j) * ldp + k, pv);
-#pragma unroll
-                    for (int c = 0; c < 8; ++c) acc[j] = fmaf(xv[c], pv[c], acc[j]);
-                }
-            }
-        } else {
-#pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                const bf16* pr = P + (k + c) * ldp;
-#pragma unroll
-                for (int j = 0; j < RB; ++j)
-                    if (j < r) acc[j] = fmaf(xv[c], __bfloat162float(pr[j]), acc[j]);
-            }
-        }
-    }
-#pragma unroll
-    for (int j = 0; j < RB; ++j)
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
-    if (lane == 0) {
-#pragma unroll
-        for (int j = 0; j < RB; ++j)
-            if (j < r) out[row * r + j] = scale * acc[j];
-    }
-}
-
-cudaError_t launch_rowproj(const bf16* X, int64_t T, int64_t K, const bf16* P, int64_t ldp, int p_t, int r,
-                           float scale, float* out, cudaStream_t stream) {
-    if (T <= 0) return cudaSuccess;
-    const unsigned blocks = static_cast<unsigned>((T + 7) / 8);
-    switch (rank_bucket(r)) {
-        case 4: rowproj_kernel<4><<<blocks, 256, 0, stream>>>(X, T, K, P, ldp, p_t, r, scale, out); break;
-        case 8: rowproj_kernel<8><<<blocks, 256, 0, stream>>>(X, T, K, P, ldp, p_t, r, scale, out); break;
-        case 16: rowproj_kernel<16><<<blocks, 256, 0, stream>>>(X, T, K, P, ldp, p_t, r, scale, out); break;
-        case 32: rowproj_kernel<32><<<blocks, 256, 0, stream>>>(X, T, K, P, ldp, p_t, r, scale, out); break;
-        default: rowproj_kernel<64><<<blocks, 256, 0, stream>>>(X, T, K, P, ldp, p_t, r, scale, out); break;
-    }
-    return cudaGetLastError();
-}
 
 // ------------------------------------------------------------------ K4 merge
 // 64 rows x 256 columns per CTA; A[:, k0:k0+256] and B[i0:i0+64, :] staged in

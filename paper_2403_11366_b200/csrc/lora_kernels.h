@@ -76,16 +76,7 @@ cudaError_t launch_fused_gemm_group(int mode, int r_pad, int cta_group, FusedGem
 cudaError_t launch_pack_b(const __nv_bfloat16* b, int64_t m, int r, __nv_bfloat16* b8, __nv_bfloat16* bt,
                           int num_sms, cudaStream_t stream);
 
-// K2a: gh [T, r] = s dY B (fp32), read by K2's epilogue and by K3 (dA).
-cudaError_t launch_gh(const __nv_bfloat16* dy, const __nv_bfloat16* b, int64_t T, int64_t m, int r, float s,
-                      float* gh, cudaStream_t stream);
 
-// K3 (TMA ring variant, r % 4 == 0): x, dY boxes {32 cols, 64 rows} bf16, gh, h
-// boxes {r, 64 rows} fp32, no swizzle.
-struct GradMaps {
-    CUtensorMap x, dy, gh, h;
-};
-int grad_strip_cols();  // columns per K3 CTA (box inner extent of the x / dY maps)
 
 struct GradArgs {
     const __nv_bfloat16* x;   // [T, n]
@@ -96,7 +87,6 @@ struct GradArgs {
     float* db;                // [m, r] or null
     int64_t T, n, m;
     int r;
-    int strips_a;             // (strip kernels) CTAs [0, strips_a) own dA strips
     float scale_b;            // s
     int accumulate;
     __nv_bfloat16* cs_a;      // tensor-core K3: split gh [3 r8, T_pad] (workspace)
@@ -166,24 +156,11 @@ GradArgs make_grad_args(int64_t T, int64_t n, int64_t m, int r, float scale, con
 int grad_rank_bucket(int r);
 cudaError_t launch_grad_reduce_cluster_group(GradGroup& G, cudaStream_t stream, int* launches);
 
-// K3 v3 (default): T split over a cluster of 8 CTAs, DSMEM reduction in rank order.
+// CUDA-core K3 (LORA_K3=cluster): T split over a cluster of 8 CTAs, DSMEM reduction in rank order.
 cudaError_t launch_grad_reduce_cluster(int64_t T, int64_t n, int64_t m, int r, float scale,
                                        const __nv_bfloat16* x, const float* gh, const __nv_bfloat16* dy,
                                        const float* h, float* da, float* db, int accumulate,
                                        cudaStream_t stream, int* launches);
-cudaError_t launch_grad_reduce_tma(const GradMaps& maps, int64_t T, int64_t n, int64_t m, int r, float scale,
-                                   float* da, float* db, int accumulate, cudaStream_t stream, int* launches);
-
-// K3: dA = gh^T x, dB = s dY^T h; one CTA per 32-column strip over all tokens,
-// fixed summation order (deterministic), writes the final values.
-cudaError_t launch_grad_reduce(int64_t T, int64_t n, int64_t m, int r, float scale, const __nv_bfloat16* x,
-                               const float* gh, const __nv_bfloat16* dy, const float* h, float* da, float* db,
-                               int accumulate, cudaStream_t stream, int* launches);
-
-// K3a: out[t, j] = scale * sum_k X[t, k] P(j, k); P(j, k) = P[j * ldp + k], or P[k * ldp + j] if p_t.
-cudaError_t launch_rowproj(const __nv_bfloat16* X, int64_t T, int64_t K, const __nv_bfloat16* P, int64_t ldp,
-                           int p_t, int r, float scale, float* out, cudaStream_t stream);
-
 // K4: w_out = bf16(W0 + s * B A)
 cudaError_t launch_merge(const __nv_bfloat16* w0, const __nv_bfloat16* a, const __nv_bfloat16* b,
                          int64_t n, int64_t m, int r, float scale, __nv_bfloat16* w_out,

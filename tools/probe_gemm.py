@@ -99,8 +99,7 @@ def run():
     # the in-tree library with the CTA-pair choice forced either way
     tree = os.path.join(ROOT, "paper_2403_11366_b200", "liblora.so")
     jobs += [(f"tree_cg{cg}", tree, {"LORA_CTA_GROUP": str(cg)}) for cg in (1, 2)]
-    jobs += [("tree_k3ldg", tree, {"LORA_K3": "ldg"}), ("tree_k3tma", tree, {"LORA_K3": "tma"}),
-             ("tree_ghv1", tree, {"LORA_GH_V1": "1"})]
+    jobs += [("tree_k3cluster", tree, {"LORA_K3": "cluster"})]
     for name, lib, extra in jobs:
         if not os.path.exists(lib):
             continue
