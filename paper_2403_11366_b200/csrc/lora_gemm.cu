@@ -118,7 +118,14 @@ struct ColTiles {
         if (MODE == kModeFwd) return n_blk * BN;
         return n_blk == 0 ? 0 : DX_BN0 + (n_blk - 1) * BN;
     }
-    __device__ static int width(int n_blk) { return (MODE == kModeFwd || n_blk != 0) ? BN : DX_BN0; }
+    // dx: the last tile is only as wide as the columns left (rounded up to 128, so each
+    // CTA of a pair still holds whole 64-column blocks): its MMAs run at N = 128, not 256
+    __device__ static int width(int n_blk, int64_t n_out) {
+        if (MODE == kModeFwd) return BN;
+        if (n_blk == 0) return DX_BN0;
+        const int64_t left = (n_out - start(n_blk) + 127) / 128 * 128;
+        return left < BN ? static_cast<int>(left) : BN;
+    }
 };
 
 // 2-CTA helpers ---------------------------------------------------------------
@@ -309,7 +316,7 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
                 const int num_k_blks = tr.num_k_blks;
                 const int t0 = t_blk * TM + static_cast<int>(crank) * BM;
                 const int n0 = Cols::start(n_blk);
-                const int wh = Cols::width(n_blk) / CG;                 // this CTA's B-operand columns
+                const int wh = Cols::width(n_blk, grp.p[tr.g].N_out) / CG;   // this CTA's B-operand columns
                 const int nh0 = n0 + static_cast<int>(crank) * wh;
                 const int nb = (wh + 63) / 64;                          // dx: 64-column W0 / A blocks
                 const bool gh_tile = (MODE != kModeFwd) && n_blk == 0;
@@ -357,7 +364,7 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
                     tma_load<CG>(s_tailb, &mp.tail, 0, nh0, tailop_full);
                 } else if constexpr (MODE == kModeDxDrop) {
                     // every CTA: A columns of the whole tile width, on its own barrier
-                    const int nbf = (Cols::width(n_blk) + 63) / 64;
+                    const int nbf = (Cols::width(n_blk, grp.p[tr.g].N_out) + 63) / 64;
                     mbar_arrive_expect_tx(tailop_full, nbf * R_PAD * 128);
                     for (int j = 0; j < nbf; ++j)
                         tma_load_2d(s_tailb + j * (R_PAD * 128), &mp.tail, n0 + 64 * j, 0, tailop_full);
@@ -372,8 +379,6 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
         // ===================== MMA issuer (leader CTA) =====================
         if (leader && elect_one()) {
             constexpr uint32_t idesc_fwd = make_idesc_bf16(TM, NT, 0, 0);
-            constexpr uint32_t idesc_dx_full = make_idesc_bf16(TM, BN, 0, 1);
-            constexpr uint32_t idesc_dx_first = make_idesc_bf16(TM, DX_BN0, 0, 1);
             constexpr uint32_t idesc_nar = make_idesc_bf16(TM, C::NAR > 0 ? C::NAR : 16, 0, 1);
             uint32_t stage = 0, phase = 0, tl = 0;
             for (int tile = pair; tile < num_tiles; tile += npairs, ++tl) {
@@ -381,7 +386,9 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
                 const int n_blk = tr.n_blk;
                 const int num_k_blks = tr.num_k_blks;
                 const bool gh_tile = (MODE != kModeFwd) && n_blk == 0;
-                const uint32_t idesc_main = (MODE == kModeFwd) ? idesc_fwd : (gh_tile ? idesc_dx_first : idesc_dx_full);
+                const uint32_t idesc_main = (MODE == kModeFwd)
+                    ? idesc_fwd
+                    : make_idesc_bf16(TM, static_cast<uint32_t>(Cols::width(n_blk, grp.p[tr.g].N_out)), 0, 1);
                 const uint32_t acc = tl & 1;
                 const uint32_t acc_phase = (tl >> 1) & 1;
                 mbar_wait<CG == 2>(&tmem_empty[acc], acc_phase ^ 1);
@@ -426,8 +433,6 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
         const uint32_t quarter = warp & 3;       // TMEM lane quarter this warp may access
         const uint32_t row_local = quarter * 32 + lane;
         constexpr uint32_t idesc_tail_fwd = make_idesc_bf16(TM, BN, 0, 0);
-        constexpr uint32_t idesc_tail_dx_full = make_idesc_bf16(TM, BN, 0, 1);
-        constexpr uint32_t idesc_tail_dx_first = make_idesc_bf16(TM, DX_BN0, 0, 1);
         constexpr uint32_t tail_sbo = 8 * C::TAIL_ROW;
         uint32_t tl = 0;
         for (int tile = pair; tile < num_tiles; tile += npairs, ++tl) {
@@ -437,7 +442,7 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
             const int t_blk = tr.t_blk;
             const int64_t row = static_cast<int64_t>(t_blk) * TM + crank * BM + row_local;
             const int n0 = Cols::start(n_blk);
-            const int width = Cols::width(n_blk);
+            const int width = Cols::width(n_blk, p.N_out);
             const bool gh_tile = (MODE != kModeFwd) && n_blk == 0;
             const uint32_t acc = tl & 1;
             const uint32_t acc_phase = (tl >> 1) & 1;
@@ -549,7 +554,7 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
                     const uint32_t h_addr = smem_u32(s_h);
                     const uint32_t t_addr = smem_u32(s_tailb);
                     const uint32_t idesc_tail = (MODE == kModeFwd)
-                        ? idesc_tail_fwd : (gh_tile ? idesc_tail_dx_first : idesc_tail_dx_full);
+                        ? idesc_tail_fwd : make_idesc_bf16(TM, static_cast<uint32_t>(width), 0, 1);
 #ifndef LORA_PROBE_NO_TAIL
 #pragma unroll
                     for (int kk = 0; kk < R_PAD / UMMA_K; ++kk) {
