@@ -101,3 +101,42 @@ def test_no_device_is_an_error_not_a_fallback():
     st = _fwd(d, x=1 << 30, w0=2 << 30, a=3 << 30, b=4 << 30, y=5 << 30, ws=6 << 30)
     assert st in (4, 5)
     assert L.lib.lora_device_check() in (4, 5)
+
+
+def test_dropout_validation_codes():
+    """lora_linear_{fwd,bwd}_dropout / lora_dropout_mask reject a bad p before
+    anything else (LoRA dropout; include/lora.h)."""
+    d = L.dims(128, 64, 64, 4, 16.0)
+    for p in (1.0, -0.5, float("nan"), float("inf")):
+        dr = L.lora_dropout(p, 1, 2)
+        assert L.lib.lora_linear_fwd_dropout(ctypes.byref(d), ctypes.byref(dr), 16, 32, 48, 64, None, 80, None,
+                                             4096, 1 << 20, None) == 1
+        assert "dropout p" in L.lib.lora_last_error().decode()
+        assert L.lib.lora_linear_bwd_dropout(ctypes.byref(d), ctypes.byref(dr), 16, 32, 48, 64, None, 96, None,
+                                             None, None, 0, 4096, 1 << 20, None) == 1
+        assert L.lib.lora_dropout_mask(8, 8, ctypes.byref(dr), 16, None) == 1
+    dr = L.lora_dropout(0.1, 1, 2)
+    assert L.lib.lora_dropout_mask(8, 8, None, 16, None) == 1
+    assert L.lib.lora_dropout_mask(-1, 8, ctypes.byref(dr), 16, None) == 2
+    # dropout workspaces hold at least the plain ones (+ M . x and the keep bits for the backward)
+    assert L.lib.lora_linear_fwd_dropout_workspace_bytes(ctypes.byref(d)) >= L.lora_linear_fwd_workspace_bytes(d)
+    assert (L.lib.lora_linear_bwd_dropout_workspace_bytes(ctypes.byref(d)) >=
+            L.lora_linear_bwd_workspace_bytes(d) + 128 * 64 * 2)
+
+
+def test_adam_validation_codes():
+    """lora_adam_step validates before any launch."""
+    hp = L.lora_adam_hparams(1e-3, 0.9, 0.999, 1e-8)
+    t = (L.lora_adam_tensor * 1)(L.lora_adam_tensor(16, None, 32, 48, 64, 8))
+    assert L.lib.lora_adam_step(0, t, ctypes.byref(hp), 1, None) == 1            # count
+    assert L.lib.lora_adam_step(65, t, ctypes.byref(hp), 1, None) == 1
+    assert L.lib.lora_adam_step(1, t, None, 1, None) == 1
+    assert L.lib.lora_adam_step(1, t, ctypes.byref(hp), 0, None) == 1            # step >= 1
+    bad = L.lora_adam_hparams(1e-3, 1.0, 0.999, 1e-8)
+    assert L.lib.lora_adam_step(1, t, ctypes.byref(bad), 1, None) == 1           # beta1 < 1
+    t6 = (L.lora_adam_tensor * 1)(L.lora_adam_tensor(16, None, 32, 48, 64, 6))
+    assert L.lib.lora_adam_step(1, t6, ctypes.byref(hp), 1, None) == 2           # numel % 4
+    tn = (L.lora_adam_tensor * 1)(L.lora_adam_tensor(16, None, None, 48, 64, 8))
+    assert L.lib.lora_adam_step(1, tn, ctypes.byref(hp), 1, None) == 1           # NULL grad
+    ta = (L.lora_adam_tensor * 1)(L.lora_adam_tensor(16, 40, 32, 48, 64, 8))
+    assert L.lib.lora_adam_step(1, ta, ctypes.byref(hp), 1, None) == 3           # misaligned master
