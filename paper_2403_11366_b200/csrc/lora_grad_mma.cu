@@ -14,8 +14,10 @@
 //   fp32 accumulation rounds, as on the CUDA cores), token-contiguous, i.e.
 //   the K-major B operand of the MMA below.  Done once per coefficient
 //   matrix instead of once per column tile.
-// K3 (one CTA = 128 X columns x one token slice):
-//   MMA   D[c, q] += X^T[c, t] Cs[q, t]     M = 128 columns, N = q_pad, K = 16.
+// K3 (one CTA = kGradMmaCols = 128 X columns x one token slice; 256 = two M tiles
+// sharing Cs is a compile-time option, measured slower: half the CTAs):
+//   MMA   D[c, q] += X^T[c, t] Cs[q, t]     M = 128 columns (two MMAs sharing the Cs
+//         operand per k-step), N = q_pad, K = 16.
 //         A operand = the X tile exactly as TMA lands it ([64 tokens][64
 //         columns] SWIZZLE_128B boxes, read MN-major: no transpose pass).
 //         Several coefficient SETS sharing one X (dA of q/k/v all read x) are
@@ -44,8 +46,10 @@ namespace lora_sm100 {
 namespace {
 
 constexpr int KB = 64;              // tokens per k-block (one 128-byte SW128 row of Cs)
-constexpr int X_BOX = 64 * KB * 2;  // one [64 tokens][64 columns] bf16 box = 8 KiB
-constexpr int X_BYTES = 2 * X_BOX;  // 128 columns per CTA
+constexpr int MT = kGradMmaCols / 128;   // M = 128 MMAs per k-step (one per 128 X columns)
+constexpr int X_BOX = 64 * KB * 2;       // one [64 tokens][64 columns] bf16 box = 8 KiB
+constexpr int X_BYTES = 2 * MT * X_BOX;  // kGradMmaCols columns per CTA
+constexpr int ACC_STRIDE = 256;          // TMEM columns between the MT accumulators
 constexpr int THREADS = 192;
 constexpr int PA = kGradMmaCols + 4;   // dA partial row stride (floats)
 constexpr int SMEM_CTA_MAX = 227 * 1024;
@@ -67,7 +71,7 @@ __device__ __forceinline__ void tmem_dealloc_n(uint32_t taddr, uint32_t ncols) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
 }
 
-// dB partials: [128 columns][r4 + 4] floats; dA partials: [r][PA]
+// dB partials: [kGradMmaCols columns][r4 + 4] floats; dA partials: [r][PA]
 __device__ __host__ __forceinline__ int partial_floats(const GradMmaSet& st) {
     return st.stride_col == 1 ? st.r * PA : kGradMmaCols * ((st.r + 3) / 4 * 4 + 4);
 }
@@ -166,7 +170,8 @@ __global__ void __launch_bounds__(THREADS, 1) grad_mma_kernel(const __grid_const
     const int kps = (kb_total + S - 1) / S;
     const int kb0 = rank * kps;
     const int nkb = kb0 < kb_total ? (kb_total - kb0 < kps ? kb_total - kb0 : kps) : 0;
-    const bool two = col0 + 64 < J.N;   // the second 64-column box holds real columns
+    int nbox = 0;                        // 64-column boxes (K-major: 64-row boxes) holding real data
+    while (nbox < 2 * MT && col0 + 64 * nbox < J.N) ++nbox;
     const int q_pad = J.q_pad;
     const int q_used = J.q_used;
     const uint32_t warp = warp_id(), lane = lane_id();
@@ -206,7 +211,6 @@ __global__ void __launch_bounds__(THREADS, 1) grad_mma_kernel(const __grid_const
     if (warp == 0) {
         // ---------------- TMA producer: X boxes [64 tokens][64 columns] + Cs boxes [3 r8 rows][64 tokens]
         if (lane == 0) {
-            const int nbox = two ? 2 : 1;
             uint32_t tx = nbox * X_BOX;
             for (int j = 0; j < J.nsets; ++j) tx += G.set[J.set0 + j].nsplit * G.set[J.set0 + j].r8 * 128;
             const uint64_t pol = l2_policy_evict_first();
@@ -241,11 +245,16 @@ __global__ void __launch_bounds__(THREADS, 1) grad_mma_kernel(const __grid_const
                 for (int kk = 0; kk < KB / 16; ++kk) {
                     // MN-major X^T: two 64-column boxes, LBO = box stride, SBO = 8 tokens;
                     // K-major X: 128 rows of 128 bytes, SBO = 8 rows.  Cs: K-major SW128
-                    const uint64_t a_desc = J.a_kmajor
-                        ? make_smem_desc(sx + kk * 32, 16, 1024, kLayoutSW128)
-                        : make_smem_desc(sx + kk * 16 * 128, X_BOX, 1024, kLayoutSW128);
-                    umma_f16(tmem_base, a_desc, make_smem_desc(sx + X_BYTES + kk * 32, 16, 1024, kLayoutSW128),
-                             idesc, (i > 0 || kk > 0) ? 1u : 0u);
+                    const uint64_t b_desc = make_smem_desc(sx + X_BYTES + kk * 32, 16, 1024, kLayoutSW128);
+#pragma unroll
+                    for (int mt = 0; mt < MT; ++mt) {
+                        if (2 * mt >= nbox) break;
+                        const uint32_t sa = sx + mt * 2 * X_BOX;
+                        const uint64_t a_desc = J.a_kmajor
+                            ? make_smem_desc(sa + kk * 32, 16, 1024, kLayoutSW128)
+                            : make_smem_desc(sa + kk * 16 * 128, X_BOX, 1024, kLayoutSW128);
+                        umma_f16(tmem_base + mt * ACC_STRIDE, a_desc, b_desc, idesc, (i > 0 || kk > 0) ? 1u : 0u);
+                    }
                 }
                 umma_commit(&empty[s]);
                 if (++s == stages) { s = 0; ph ^= 1; }
@@ -258,16 +267,18 @@ __global__ void __launch_bounds__(THREADS, 1) grad_mma_kernel(const __grid_const
         tc_fence_after();
         K3_STAMP(1);
         const int lq = static_cast<int>(warp & 3);          // TMEM lane quarter of this warp
-        const int cl = lq * 32 + static_cast<int>(lane);    // column within the tile
+        for (int mt = 0; mt < MT; ++mt) {
+        const int cl = mt * 128 + lq * 32 + static_cast<int>(lane);   // column within the tile
         const bool col_ok = col0 + cl < J.N;
-        const uint32_t tbase = tmem_base + (static_cast<uint32_t>(lq * 32) << 16);
+        const bool live = nkb > 0 && 2 * mt < nbox;          // warp-uniform
+        const uint32_t tbase = tmem_base + (static_cast<uint32_t>(lq * 32) << 16) + mt * ACC_STRIDE;
         int poff = 0;
         for (int j = 0; j < J.nsets; ++j) {
             const GradMmaSet& st = G.set[J.set0 + j];
             const int r4p = (st.r + 3) / 4 * 4 + 4;
             for (int k0 = 0; k0 < st.r8; k0 += 8) {
                 uint32_t h[8], md[8], l[8];
-                if (nkb > 0) {   // warp-uniform
+                if (live) {
                     tmem_ld_32x32b_x8(tbase + st.row0 + k0, h);
                     if (st.nsplit == 3) {
                         tmem_ld_32x32b_x8(tbase + st.row0 + st.r8 + k0, md);
@@ -282,7 +293,7 @@ __global__ void __launch_bounds__(THREADS, 1) grad_mma_kernel(const __grid_const
                 for (int u = 0; u < 8; ++u) {
                     const int k = k0 + u;
                     if (k >= st.r) break;
-                    const float v = nkb > 0
+                    const float v = live
                         ? (__uint_as_float(h[u]) + __uint_as_float(md[u])) + __uint_as_float(l[u]) : 0.0f;
                     if (S == 1) {
                         if (col_ok) {
@@ -297,6 +308,7 @@ __global__ void __launch_bounds__(THREADS, 1) grad_mma_kernel(const __grid_const
                 }
             }
             poff += partial_floats(st);
+        }
         }
     }
     tc_fence_before();
@@ -409,10 +421,11 @@ cudaError_t launch_grad_mma(GradMmaGroup& G, int num_sms, cudaStream_t stream) {
     G.stage_bytes = X_BYTES + (qmax * 128 + 1023) / 1024 * 1024;
     G.tmem_cols = 32;
     while (G.tmem_cols < qmax) G.tmem_cols *= 2;
+    if (MT == 2) G.tmem_cols = 512;   // two accumulators at columns 0 and 256 (one CTA per SM)
     const int fixed = 1024 /* barriers */ + 1024 /* alignment */;
-    // two CTAs per SM when at least 3 stages fit in half the shared memory
-    int per_sm = 2;
-    int stages = (SMEM_SM / 2 - 1024 - fixed) / G.stage_bytes;
+    // two CTAs per SM when at least 3 stages fit in half the shared memory (and TMEM allows)
+    int per_sm = MT == 1 ? 2 : 1;
+    int stages = per_sm == 2 ? (SMEM_SM / 2 - 1024 - fixed) / G.stage_bytes : 0;
 #ifdef LORA_K3_ONE_PER_SM
     stages = 0;   // experiment: one CTA per SM, deep ring
 #endif

@@ -107,7 +107,10 @@ struct GradGroup {
 // set j occupies B-operand rows [row0, row0 + 3 r8) (hi, mid, lo), loaded by
 // TMA from its split array Cs [3 r8, T_pad] bf16 (csmap: box {64 tokens,
 // 3 r8 rows}, SWIZZLE_128B) that K3s wrote.
-constexpr int kGradMmaCols = 128;      // X columns per CTA (MMA M)
+#ifndef LORA_K3_COLS
+#define LORA_K3_COLS 128
+#endif
+constexpr int kGradMmaCols = LORA_K3_COLS;   // X columns per CTA (one M = 128 MMA per 128)
 constexpr int kMaxGradJobs = 16;
 constexpr int kMaxGradSetsTotal = 16;
 struct GradMmaSet {
