@@ -95,7 +95,8 @@ struct GemmCfg {
                                                           : (MODE == kModeDxDrop ? NT / 64 : NBH) * R_PAD * 128;
     static constexpr int SH_BYTES = BM * TAIL_ROW;                // bf16(s h) / bf16(gh) tile
     static constexpr int BAR_BYTES = 1024;
-    static constexpr int FIXED = round_up(TAILB_BYTES, 1024) + round_up(SH_BYTES, 1024) +
+    static constexpr int TAIL_BUFS = (MODE == kModeDxDrop) ? 2 : 1;   // dropout: double-buffered A tile
+    static constexpr int FIXED = TAIL_BUFS * round_up(TAILB_BYTES, 1024) + round_up(SH_BYTES, 1024) +
                                  BAR_BYTES + 1024 /* alignment slack */;
     static constexpr int STAGES = cmin(LORA_STAGES_CAP, (SMEM_LIMIT - FIXED) / STAGE_BYTES);
     static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + FIXED;
@@ -245,7 +246,7 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* stage_base = smem;
     uint8_t* s_tailb = smem + C::STAGES * C::STAGE_BYTES;
-    uint8_t* s_h = s_tailb + round_up(C::TAILB_BYTES, 1024);
+    uint8_t* s_h = s_tailb + C::TAIL_BUFS * round_up(C::TAILB_BYTES, 1024);
     uint64_t* bars = reinterpret_cast<uint64_t*>(s_h + round_up(C::SH_BYTES, 1024));
     uint64_t* full = bars;
     uint64_t* empty = bars + C::STAGES;
@@ -255,7 +256,9 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
     uint64_t* tailop_empty = tailop_full + 1;
     uint64_t* tail_done = tailop_empty + 1;
     uint64_t* sh_full = tail_done + 1;             // CG = 2: peer's s_h tile written
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(sh_full + 1);
+    uint64_t* tailop2_full = sh_full + 1;          // dx dropout mode: second A-tile buffer
+    uint64_t* tailop2_empty = tailop2_full + 1;
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tailop2_empty + 1);
 
     const uint32_t crank = (CG == 2) ? cluster_ctarank() : 0;
     const bool leader = crank == 0;
@@ -284,6 +287,8 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
         }
         mbar_init(tailop_full, 1);
         mbar_init(tailop_empty, 1);
+        mbar_init(tailop2_full, 1);
+        mbar_init(tailop2_empty, 1);
         mbar_init(tail_done, 1);
         mbar_init(sh_full, 1);
         fence_mbar_init();
@@ -358,16 +363,20 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
                     if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
                 }
                 // tail operand for this tile: fwd B rows; dx A columns (this CTA's half)
-                mbar_wait(tailop_empty, (tl & 1) ^ 1);
+                if constexpr (MODE != kModeDxDrop) mbar_wait(tailop_empty, (tl & 1) ^ 1);
                 if constexpr (MODE == kModeFwd) {
                     if (leader) mbar_arrive_expect_tx(tailop_full, CG * C::TAILB_BYTES);
                     tma_load<CG>(s_tailb, &mp.tail, 0, nh0, tailop_full);
                 } else if constexpr (MODE == kModeDxDrop) {
-                    // every CTA: A columns of the whole tile width, on its own barrier
+                    // every CTA: A columns of the whole tile width, on its own barrier, into
+                    // buffer tl & 1 (the epilogue holds a buffer for its whole drain)
+                    uint64_t* tf = (tl & 1) ? tailop2_full : tailop_full;
+                    mbar_wait((tl & 1) ? tailop2_empty : tailop_empty, ((tl >> 1) & 1) ^ 1);
+                    uint8_t* tb = s_tailb + (tl & 1) * round_up(C::TAILB_BYTES, 1024);
                     const int nbf = (Cols::width(n_blk, grp.p[tr.g].N_out) + 63) / 64;
-                    mbar_arrive_expect_tx(tailop_full, nbf * R_PAD * 128);
+                    mbar_arrive_expect_tx(tf, nbf * R_PAD * 128);
                     for (int j = 0; j < nbf; ++j)
-                        tma_load_2d(s_tailb + j * (R_PAD * 128), &mp.tail, n0 + 64 * j, 0, tailop_full);
+                        tma_load_2d(tb + j * (R_PAD * 128), &mp.tail, n0 + 64 * j, 0, tf);
                 } else {
                     if (leader) mbar_arrive_expect_tx(tailop_full, CG * nb * R_PAD * 128);
                     for (int j = 0; j < nb; ++j)
@@ -528,7 +537,7 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
             }
             if constexpr (MODE == kModeDxDrop) {
                 // dropout: no tail MMA -- the epilogue adds q M . (gh A) itself (step 5)
-                mbar_wait(tailop_full, tl & 1);
+                mbar_wait((tl & 1) ? tailop2_full : tailop_full, (tl >> 1) & 1);
             } else {
             // (3) bf16(s h) / bf16(gh) -> swizzled K-major smem tile (tail MMA A operand)
             const float op_scale = (MODE == kModeFwd) ? p.scale : 1.0f;
@@ -581,6 +590,15 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
             // (5) drain: acc -> (+ b0) -> bf16 (RNE) -> global
             const bool row_ok = row < p.T;
             __nv_bfloat16* out_row = p.out + row * p.N_out;
+            // dx dropout mode: this row's keep bits for the whole tile, loaded once up front
+            // (one global round trip instead of one per 16-column chunk)
+            uint32_t kw[(MODE == kModeDxDrop) ? NT / 32 : 1];
+            if constexpr (MODE == kModeDxDrop) {
+                const int64_t nw = (p.N_out + 31) / 32;
+#pragma unroll
+                for (int w = 0; w < NT / 32; ++w)
+                    kw[w] = (row_ok && n0 / 32 + w < nw && 32 * w < width) ? p.drop_bits[row * nw + n0 / 32 + w] : 0u;
+            }
 #pragma unroll 1
             for (int c = 0; c < width / 16; ++c) {
                 uint32_t v[16];
@@ -603,7 +621,8 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
                     if constexpr (MODE == kModeDxDrop) {
                         // f += q M . (gh A): A columns of this chunk from the MN-major SW128 tile
                         const int lc = 16 * c;
-                        const uint8_t* blk = s_tailb + (lc / 64) * (R_PAD * 128);
+                        const uint8_t* blk = s_tailb + (tl & 1) * round_up(C::TAILB_BYTES, 1024) +
+                                             (lc / 64) * (R_PAD * 128);
                         const uint32_t ch = static_cast<uint32_t>((lc % 64) / 8);
                         float lo[16];
 #pragma unroll
@@ -622,8 +641,7 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
                             }
                         }
                         // keep bits of the 16 columns, packed by K0 (32 per word; col % 16 == 0)
-                        const uint32_t keep =
-                            (p.drop_bits[row * ((p.N_out + 31) / 32) + col / 32] >> (col % 32)) & 0xFFFFu;
+                        const uint32_t keep = (kw[c >> 1] >> ((c & 1) * 16)) & 0xFFFFu;
 #pragma unroll
                         for (int e = 0; e < 16; ++e)
                             if ((keep >> e) & 1u) f[e] = fmaf(p.drop.q, lo[e], f[e]);
@@ -639,7 +657,7 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
             }
             if constexpr (MODE == kModeDxDrop) {
                 named_bar_sync(1, 128);   // every epilogue warp is done with the A tile
-                if (ew == 0 && lane == 0) mbar_arrive(tailop_empty);
+                if (ew == 0 && lane == 0) mbar_arrive((tl & 1) ? tailop2_empty : tailop_empty);
             }
             tc_fence_before();
             __syncwarp();
