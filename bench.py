@@ -49,6 +49,23 @@ def workload_flops(wl, T=None):
     return sum(algorithmic_flops(T or l.T, l.n, l.m, l.r) for l in wl.linears)
 
 
+def gpu_local_cpus(dev_index):
+    """CPUs on the same NUMA node as GPU `dev_index` (from sysfs), or None."""
+    try:
+        import torch
+        bus = torch.cuda.get_device_properties(dev_index).pci_bus_id.lower()
+        dom, rest = bus.split(":", 1) if bus.count(":") == 2 else ("0000", bus)
+        path = f"/sys/bus/pci/devices/{dom[-4:]}:{rest}/local_cpulist"
+        cpus = set()
+        for part in open(path).read().strip().split(","):
+            lo, _, hi = part.partition("-")
+            cpus.update(range(int(lo), int(hi or lo) + 1))
+        cpus &= os.sched_getaffinity(0)
+        return cpus or None
+    except Exception:
+        return None
+
+
 def fwd_flops(l, T=None):
     T = T or l.T
     return 2 * T * l.m * l.n + 2 * T * l.r * (l.n + l.m)
@@ -412,10 +429,20 @@ def run_ours(args, wl):
 
     # ---- end to end through the public API with host buffers
     xs = list({id(e["x"]): e["x"] for e in lin}.values())     # each distinct input once
-    hx = [t.cpu().pin_memory() for t in xs]
-    hdy = [e["dy"].cpu().pin_memory() for e in lin]
-    hda = [torch.empty_like(e["da"], device="cpu").pin_memory() for e in lin]
-    hdb = [torch.empty_like(e["db"], device="cpu").pin_memory() for e in lin]
+    # pinned host buffers on the GPU's own NUMA node (first touch by a thread bound to
+    # the GPU-local CPUs): a remote node halves the H2D bandwidth on a 2-socket host
+    old_aff = os.sched_getaffinity(0)
+    local = gpu_local_cpus(local_rank)
+    if local:
+        os.sched_setaffinity(0, local)
+    try:
+        hx = [t.cpu().pin_memory() for t in xs]
+        hdy = [e["dy"].cpu().pin_memory() for e in lin]
+        hda = [torch.zeros_like(e["da"], device="cpu").pin_memory() for e in lin]
+        hdb = [torch.zeros_like(e["db"], device="cpu").pin_memory() for e in lin]
+    finally:
+        if local:
+            os.sched_setaffinity(0, old_aff)
     h2d = sum(t.numel() * t.element_size() for t in hx + hdy)
     d2h = sum(t.numel() * t.element_size() for t in hda + hdb)
 
@@ -529,7 +556,9 @@ def run_ours(args, wl):
         traffic = None
         tp_path = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tp_path):
-            traffic = json.load(open(tp_path)).get("fused_fwd_bytes_per_launch")
+            tj = json.load(open(tp_path))
+            traffic = (tj.get("grouped_fwd_bytes_per_launch", {}).get(wl.key) if use_groups
+                       else tj.get("fused_fwd_bytes_per_launch_single"))
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             cval, cdt, R, thr = cpu_oracle_sample(wl, target_s=args.cpu_seconds)
