@@ -35,7 +35,6 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
-#include <cstdio>
 #include <cstdlib>
 
 #include "lora_kernels.h"
@@ -481,14 +480,10 @@ cudaError_t launch_grad_mma(GradMmaGroup& G, int num_sms, cudaStream_t stream) {
         cache_dev = dev;
     }
     G.S = grad_mma_cluster_size(tiles, kb_max, slots);
-    if (const char* fs = getenv("LORA_K3_S")) {   // experiments: force the token split
+    if (const char* fs = getenv("LORA_K3_S")) {   // tests / experiments: force the token split
         const int v = atoi(fs);
         if (v >= 1 && v <= 8) G.S = v;
     }
-    if (getenv("LORA_K3_DEBUG"))
-        printf("K3: tiles %d kb %d smem %d stages %d per_sm %d slots %d %d %d %d %d %d %d %d -> S = %d\n", tiles,
-               kb_max, smem, stages, per_sm, slots[1], slots[2], slots[3], slots[4], slots[5], slots[6], slots[7],
-               slots[8], G.S);
     cfg.gridDim = dim3(tiles, G.S);
     attr[0].val.clusterDim.y = G.S;
     e = cudaLaunchKernelEx(&cfg, grad_mma_kernel, G);

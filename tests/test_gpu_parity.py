@@ -384,3 +384,24 @@ def test_frozen_base_untouched(L):
     torch.cuda.synchronize()
     for k, v in t.items():
         assert np.array_equal(bits_of(v), d[k]), k
+
+
+@pytest.mark.parametrize("split", ["1", "2", "3", "4", "8"])
+def test_k3_token_split_paths(oracle_mod, L, split, monkeypatch):
+    """Every K3 token split S (cluster size; LORA_K3_S forces it) gives the
+    oracle's dA and dB: S = 1 stores straight from TMEM, S > 1 reduces the
+    cluster's partials over DSMEM (vectorised for dA and r % 4 == 0 dB, scalar
+    for r % 4 != 0), including ranks whose token slice is empty and
+    accumulate into existing gradients."""
+    monkeypatch.setenv("LORA_K3_S", split)
+    for (T, n, m, r) in [(700, 384, 264, 5), (256, 136, 512, 16), (64, 256, 128, 8)]:
+        d = make_lora_inputs(T, n, m, r, seed=900 + r)
+        x, w0, a, b, dy = (dev_bf16(d[k]) for k in ("x", "w0", "a", "b", "dy"))
+        y, h = L.lora_linear_fwd(x, w0, a, b, 16.0)
+        da0 = torch.full((r, n), 0.5, device="cuda")
+        db0 = torch.full((m, r), -1.0, device="cuda")
+        _, da, db = L.lora_linear_bwd(x, w0, a, b, dy, 16.0, h_saved=h, da=da0, db=db0, accumulate=True)
+        torch.cuda.synchronize()
+        go = oracle_mod.lora_bwd(d["x"], d["w0"], d["a"], d["b"], d["dy"], 16.0, want_dx=False)
+        assert relF(host_f64(da) - 0.5, go["da"]) <= TOL_GRAD, (split, T, n, m, r)
+        assert relF(host_f64(db) + 1.0, go["db"]) <= TOL_GRAD, (split, T, n, m, r)
