@@ -240,7 +240,7 @@ def run_ours(args, wl):
     L.lora_device_check()
 
     stream = torch.cuda.current_stream()
-    comm = tp.LoraComm() if world > 1 else None
+    comm = tp.LoraComm() if (world > 1 or args.force_tp) else None
 
     # ---- inputs (seeded, synthetic, sharded per rank), resident in HBM
     lin = []
@@ -368,19 +368,28 @@ def run_ours(args, wl):
     barrier()
 
     K = args.steps
-    use_graph = args.graph == "on" or (args.graph == "auto" and world == 1)
+    use_graph = args.graph in ("on", "auto")
     graph = None
     if use_graph:
-        # the whole step (every fwd + bwd launch) as one CUDA graph, replayed per step
+        # the whole step (every fwd + bwd launch, and under TP every NCCL collective)
+        # as one CUDA graph, replayed per step -- no host launch cost in the timed loop
         gstream = torch.cuda.Stream(device=dev)
         gstream.wait_stream(stream)
         graph = torch.cuda.CUDAGraph()
         launches["n"] = 0
-        with torch.cuda.stream(gstream):
-            with torch.cuda.graph(graph, stream=gstream):
-                step()
+        try:
+            with torch.cuda.stream(gstream):
+                with torch.cuda.graph(graph, stream=gstream):
+                    step()
+        except Exception as ex:   # (symmetric on every rank) -> time the eager step instead
+            if args.graph == "on":
+                raise
+            print(f"bench: CUDA graph capture failed ({ex!r}); timing eager steps", file=sys.stderr)
+            graph = None
+            torch.cuda.synchronize()
         stream.wait_stream(gstream)
         per_step_launches = launches["n"]
+    if graph is not None:
         for _ in range(3):
             graph.replay()
         barrier()
@@ -574,7 +583,7 @@ def run_ours(args, wl):
                        "linears": [f"{l.name}:{l.n}->{l.m}" for l in wl.linears],
                        "tokens": tokens, "rank": l0.r, "alpha": l0.alpha,
                        "global_batch": 1, "seq_len": tokens,
-                       "parallelism": f"tp{world}" if world > 1 else "single",
+                       "parallelism": f"tp{world}" if comm is not None else "single",
                        "cuda_graph": graph is not None,
                        "grouped_calls": [[wl.linears[i].name for i in g] for g in wl.groups] if use_groups else None,
                        "shared_inputs": [[wl.linears[i].name for i in g] for g in wl.groups if len(g) > 1],
@@ -619,6 +628,8 @@ def main():
     ap.add_argument("--config", default="cfg2", choices=sorted(WORKLOADS))
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--force-tp", action="store_true",
+                    help="run the tensor-parallel code path (NCCL communicator, TP entry points) even at N = 1")
     ap.add_argument("--dropout", type=float, default=0.0,
                     help="LoRA dropout p (Listing 3 LORA_DROPOUT = 0.05); 0 = the north-star path")
     ap.add_argument("--no-group", action="store_true",
