@@ -459,7 +459,7 @@ cudaError_t launch_grad_mma(GradMmaGroup& G, int num_sms, cudaStream_t stream) {
     // co-resident CTAs per cluster size (cached per smem size and device)
     static thread_local int cache_smem = -1, cache_dev = -1, slots[9];
     int dev = 0;
-    cudaGetDevice(&dev);
+    if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
     if (cache_smem != smem || cache_dev != dev) {
         slots[0] = 0;
         slots[1] = per_sm * num_sms;
