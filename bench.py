@@ -317,9 +317,63 @@ def run_ours(args, wl):
                                       stream=cur)
             launches["n"] += L.lora_last_launch_count()
 
+    # Tensor parallel (N > 1, or --force-tp): the COLUMN-parallel linears that share an
+    # input (q/k/v, gate/up) run as one grouped local forward (no collective in column
+    # mode) and one lora_tp_linear_bwd_column_group (their dX partials summed, ONE
+    # all-reduce); row-parallel linears (o, down) run one by one.
+    tp_groups = []
+    if comm is not None and not args.no_group and args.dropout == 0.0:
+        for gidx in (wl.groups or tuple((i,) for i in range(len(lin)))):
+            members = [lin[i] for i in gidx]
+            if len(members) > 1 and all(e["spec"].mode == tp.COLUMN for e in members):
+                ds = (L.lora_dims * len(members))(*[L.dims(e["l"].T, e["spec"].local_n, e["spec"].local_m,
+                                                           e["l"].r, e["l"].alpha) for e in members])
+                wsf = torch.empty(max(256, int(L.lib.lora_linear_fwd_grouped_workspace_bytes(len(members), ds))),
+                                  dtype=torch.uint8, device=dev)
+                wsb = torch.empty(max(256, int(L.lib.lora_tp_linear_bwd_column_group_workspace_bytes(
+                    len(members), ds))), dtype=torch.uint8, device=dev)
+                dx_sum = torch.empty_like(members[0]["dx"])
+                tp_groups.append((members, wsf, wsb, dx_sum))
+            else:
+                tp_groups.append((members, None, None, None))
+
+    def step_tp(ev=None):
+        cur = torch.cuda.current_stream()
+        for gi, (members, wsf, _, _) in enumerate(tp_groups):
+            if ev is not None and gi == 0:
+                ev["f0"].record(stream)
+            if wsf is not None:
+                L.lora_linear_fwd_grouped([(e["x"], e["w0"], e["a"], e["b"], None) for e in members],
+                                          [e["l"].alpha for e in members],
+                                          outs=[(e["y"], e["h"]) for e in members], workspace=wsf, stream=cur)
+                launches["n"] += L.lora_last_launch_count()
+            else:
+                for e in members:
+                    tp.tp_linear_fwd(comm, e["spec"], e["x"], e["w0"], e["a"], e["b"], e["l"].alpha, y=e["y"],
+                                     h_out=e["h"], workspace=e["ws_f"], stream=cur)
+                    launches["n"] += L.lora_last_launch_count()
+            if ev is not None and gi == 0:
+                ev["f1"].record(stream)
+        for members, _, wsb, dx_sum in tp_groups:
+            if wsb is not None:
+                tp.tp_linear_bwd_column_group(comm, [e["spec"] for e in members],
+                                              [(e["x"], e["w0"], e["a"], e["b"], e["dy"], e["h"]) for e in members],
+                                              [e["l"].alpha for e in members], dx_sum=dx_sum,
+                                              outs=[(e["dx"], e["da"], e["db"]) for e in members], workspace=wsb,
+                                              stream=cur)
+                launches["n"] += L.lora_last_launch_count()
+            else:
+                for e in members:
+                    tp.tp_linear_bwd(comm, e["spec"], e["x"], e["w0"], e["a"], e["b"], e["dy"], e["l"].alpha,
+                                     h_saved=e["h"], dx=e["dx"], da=e["da"], db=e["db"], workspace=e["ws_b"],
+                                     reduce_lora_grads=True, stream=cur)
+                    launches["n"] += L.lora_last_launch_count()
+
     def step(ev=None):
         if use_groups:
             return step_grouped(ev)
+        if tp_groups:
+            return step_tp(ev)
         for e in lin:
             if ev is not None and e is lin[0]:
                 ev["f0"].record(stream)
@@ -412,7 +466,7 @@ def run_ours(args, wl):
             if graph is not None:
                 graph.replay()
             else:
-                step(None if use_groups else fev[i])
+                step(None if (use_groups or tp_groups) else fev[i])
             ev1[i].record(stream)
         barrier()
     step_ms = [ev0[i].elapsed_time(ev1[i]) for i in range(K)]
@@ -421,7 +475,7 @@ def run_ours(args, wl):
     # CUDA events on its launching stream inside K further eager steps (same flush)
     if graph is not None:
         launches["n"] = per_step_launches * K
-    if graph is not None or use_groups:
+    if graph is not None or use_groups or tp_groups:
         n_before = launches["n"]
         for i in range(K):
             flush.fill_(i & 0xFF)
@@ -557,7 +611,7 @@ def run_ours(args, wl):
         value = flops_step * K / (total_ms * 1e-3) / 1e12
         tokens = wl.linears[0].T
         l0 = wl.linears[0]
-        roof_linears = [lin[i]["l"] for i in wl.groups[0]] if use_groups else [l0]
+        roof_linears = ([lin[i]["l"] for i in wl.groups[0]] if (use_groups or tp_groups) and wl.groups else [l0])
         f_fwd = sum(fwd_flops(l) for l in roof_linears) / world
         fwd_avg_s = float(np.mean(fwd_ms)) * 1e-3
         achieved = f_fwd / fwd_avg_s / 1e12
@@ -585,7 +639,8 @@ def run_ours(args, wl):
                        "global_batch": 1, "seq_len": tokens,
                        "parallelism": f"tp{world}" if comm is not None else "single",
                        "cuda_graph": graph is not None,
-                       "grouped_calls": [[wl.linears[i].name for i in g] for g in wl.groups] if use_groups else None,
+                       "grouped_calls": ([[wl.linears[i].name for i in g] for g in wl.groups]
+                                         if (use_groups or tp_groups) else None),
                        "shared_inputs": [[wl.linears[i].name for i in g] for g in wl.groups if len(g) > 1],
                        "lora_dropout": args.dropout,
                        "l2": "flushed between timed steps (2xL2 write then 2xL2 read, outside the "
@@ -595,7 +650,7 @@ def run_ours(args, wl):
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": (f"lora_linear_fwd_grouped of {[l.name for l in roof_linears]} (one fused K1 "
-                                    f"launch) inside the step, " if use_groups else
+                                    f"launch) inside the step, " if len(roof_linears) > 1 else
                                     f"lora_linear_fwd of '{l0.name}' (B6 pack + fused K1) inside the step, ") +
                                    f"{f_fwd / 1e9:.2f} algorithmic GFLOP per launch, avg {fwd_avg_s * 1e6:.1f} us",
                          "peak_source": peak_src + " bf16_tflops (burst)"},

@@ -251,6 +251,22 @@ lora_status lora_tp_linear_bwd(lora_comm* comm, lora_tp_mode mode, const lora_di
                                float* da, float* db, int accumulate, int reduce_lora_grads,
                                void* workspace, size_t workspace_bytes, void* stream);
 
+/* Tensor-parallel backward of a COLUMN-parallel group of linears that read the
+ * SAME input x (q, k, v or gate, up): the grouped local backward
+ * (one fused dX launch, one dA/dB launch), then the members' dX partials summed
+ * into dx_sum [T, d_in] bf16 (fp32 accumulation, one RNE) -- the gradient w.r.t.
+ * the shared input -- and ONE all-reduce of dx_sum instead of one per member;
+ * the members' partial dA are all-reduced in one NCCL group.  problems[g].x must
+ * all be the same pointer; problems[g].dx are the members' own partials (kept);
+ * dx_sum may be NULL (no dX wanted).  dB stays local (column mode).
+ * accumulate with reduce_lora_grads is rejected at N > 1 (accumulate locally,
+ * then lora_allreduce the sums).  Workspace: lora_linear_bwd_grouped_workspace_bytes. */
+size_t lora_tp_linear_bwd_column_group_workspace_bytes(int count, const lora_dims* local);
+lora_status lora_tp_linear_bwd_column_group(lora_comm* comm, int count, const lora_dims* local,
+                                            const lora_bwd_problem* problems, void* dx_sum, int accumulate,
+                                            int reduce_lora_grads, void* workspace, size_t workspace_bytes,
+                                            void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -138,6 +138,11 @@ lib.lora_tp_linear_bwd_workspace_bytes.restype = ctypes.c_size_t
 lib.lora_tp_linear_bwd.argtypes = [_vp, ctypes.c_int, _dp, _vp, _vp, _vp, _vp, _fp, _vp, _vp, _fp, _fp,
                                    ctypes.c_int, ctypes.c_int, _vp, ctypes.c_size_t, _vp]
 lib.lora_tp_linear_bwd.restype = _st
+lib.lora_tp_linear_bwd_column_group_workspace_bytes.argtypes = [ctypes.c_int, _dp]
+lib.lora_tp_linear_bwd_column_group_workspace_bytes.restype = ctypes.c_size_t
+lib.lora_tp_linear_bwd_column_group.argtypes = [_vp, ctypes.c_int, _dp, ctypes.POINTER(lora_bwd_problem), _vp,
+                                                ctypes.c_int, ctypes.c_int, _vp, ctypes.c_size_t, _vp]
+lib.lora_tp_linear_bwd_column_group.restype = _st
 
 STATUS = {0: "LORA_OK", 1: "LORA_ERR_INVALID", 2: "LORA_ERR_SHAPE", 3: "LORA_ERR_ALIGN",
           4: "LORA_ERR_UNSUPPORTED", 5: "LORA_ERR_CUDA", 6: "LORA_ERR_NCCL", 7: "LORA_ERR_WORKSPACE"}

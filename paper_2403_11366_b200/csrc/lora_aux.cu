@@ -187,6 +187,38 @@ cudaError_t launch_adam(AdamGroup& G, int num_sms, cudaStream_t stream) {
     return cudaGetLastError();
 }
 
+// dst = RNE_bf16(sum_g src_g), fp32 accumulation in g order (TP column group: the
+// members' dX partials w.r.t. their shared input); 8 elements per thread
+__global__ void __launch_bounds__(256) sum_bf16_kernel(const __grid_constant__ SumBf16Args A) {
+    const int64_t n8 = A.count / 8;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n8; i += stride) {
+        float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        for (int g = 0; g < A.n; ++g) {
+            float f[8];
+            bf16x8_to_f32(__ldg(reinterpret_cast<const uint4*>(A.src[g]) + i), f);
+#pragma unroll
+            for (int c = 0; c < 8; ++c) acc[c] += f[c];
+        }
+        uint4 o;
+        __nv_bfloat162 p0 = __floats2bfloat162_rn(acc[0], acc[1]), p1 = __floats2bfloat162_rn(acc[2], acc[3]);
+        __nv_bfloat162 p2 = __floats2bfloat162_rn(acc[4], acc[5]), p3 = __floats2bfloat162_rn(acc[6], acc[7]);
+        o.x = *reinterpret_cast<uint32_t*>(&p0);
+        o.y = *reinterpret_cast<uint32_t*>(&p1);
+        o.z = *reinterpret_cast<uint32_t*>(&p2);
+        o.w = *reinterpret_cast<uint32_t*>(&p3);
+        reinterpret_cast<uint4*>(A.dst)[i] = o;
+    }
+}
+
+cudaError_t launch_sum_bf16(const SumBf16Args& A, int num_sms, cudaStream_t stream) {
+    if (A.n < 1 || A.n > kMaxGroup || A.count % 8 != 0) return cudaErrorInvalidValue;
+    if (A.count == 0) return cudaSuccess;
+    const int64_t blocks = std::min<int64_t>((A.count / 8 + 255) / 256, static_cast<int64_t>(num_sms) * 8);
+    sum_bf16_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(A);
+    return cudaGetLastError();
+}
+
 __global__ void add_f32_kernel(float* __restrict__ dst, const float* __restrict__ src, int64_t count) {
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += stride)

@@ -34,6 +34,8 @@ struct NcclApi {
     ncclResult_t (*CommDestroy)(ncclComm_t);
     ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t);
     const char* (*GetErrorString)(ncclResult_t);
+    ncclResult_t (*GroupStart)();   // optional: batches several collectives into one launch
+    ncclResult_t (*GroupEnd)();
     bool ok = false;
 };
 
@@ -55,6 +57,8 @@ NcclApi* nccl() {
     api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
     api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(dlsym(h, "ncclAllReduce"));
     api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+    api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(dlsym(h, "ncclGroupStart"));
+    api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(dlsym(h, "ncclGroupEnd"));
     api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllReduce && api.GetErrorString;
     return api.ok ? &api : nullptr;
 }
@@ -208,6 +212,69 @@ lora_status lora_tp_linear_bwd(lora_comm* c, lora_tp_mode mode, const lora_dims*
             if (e != cudaSuccess) return cuda_fail(e, "grad accumulate launch");
             ++launches;
         }
+    }
+    set_launches(launches);
+    return LORA_OK;
+}
+
+size_t lora_tp_linear_bwd_column_group_workspace_bytes(int count, const lora_dims* local) {
+    return lora_linear_bwd_grouped_workspace_bytes(count, local);
+}
+
+lora_status lora_tp_linear_bwd_column_group(lora_comm* c, int count, const lora_dims* local,
+                                            const lora_bwd_problem* problems, void* dx_sum, int accumulate,
+                                            int reduce_lora_grads, void* workspace, size_t workspace_bytes,
+                                            void* stream) {
+    if (!c) return fail(LORA_ERR_INVALID, "lora_tp_linear_bwd_column_group: comm is NULL");
+    if (count < 1 || count > LORA_MAX_GROUP || !local || !problems)
+        return fail(LORA_ERR_INVALID, "lora_tp_linear_bwd_column_group: need 1..%d problems", LORA_MAX_GROUP);
+    if (accumulate && reduce_lora_grads && c->nranks > 1)
+        return fail(LORA_ERR_UNSUPPORTED, "lora_tp_linear_bwd_column_group: accumulate with reduce_lora_grads "
+                                          "(accumulate locally, then lora_allreduce the sums)");
+    for (int g = 0; g < count; ++g) {
+        if (local[g].tokens != local[0].tokens || local[g].d_in != local[0].d_in || problems[g].x != problems[0].x)
+            return fail(LORA_ERR_INVALID, "lora_tp_linear_bwd_column_group: problem %d does not share problem 0's "
+                                          "input x [T, d_in]", g);
+        if (dx_sum && !problems[g].dx)
+            return fail(LORA_ERR_INVALID, "lora_tp_linear_bwd_column_group: problem %d needs a dx buffer (the "
+                                          "members' partials are summed into dx_sum)", g);
+    }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    // (1) the grouped local backward: one fused K2 launch, one K3 launch
+    lora_status s = lora_linear_bwd_grouped(count, local, problems, accumulate, workspace, workspace_bytes, stream);
+    int launches = get_launches();
+    if (s != LORA_OK) return s;
+    // (2) dX w.r.t. the shared input: the members' partials summed (fp32, one RNE)
+    if (dx_sum) {
+        const int64_t T = local[0].tokens, n = local[0].d_in;
+        if (T > 0) {
+            lora_sm100::SumBf16Args A;
+            A.n = count;
+            A.count = T * n;
+            A.dst = static_cast<__nv_bfloat16*>(dx_sum);
+            for (int g = 0; g < count; ++g) A.src[g] = static_cast<const __nv_bfloat16*>(problems[g].dx);
+            int dev = 0, sms = 148;
+            if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            cudaError_t e = lora_sm100::launch_sum_bf16(A, sms, st);
+            if (e != cudaSuccess) return cuda_fail(e, "dX sum launch");
+            ++launches;
+            // (3) ONE all-reduce of the summed dX (q, k, v fused)
+            if ((s = allreduce_impl(c, dx_sum, size_t(T) * n, LORA_DT_BF16, st)) != LORA_OK) return s;
+        }
+    }
+    // (4) the partial dA of every member, batched into one NCCL group
+    if (reduce_lora_grads && c->nranks > 1) {
+        NcclApi* api = nccl();
+        if (!api) return fail(LORA_ERR_NCCL, "libnccl could not be loaded (set LORA_NCCL_LIB)");
+        if (api->GroupStart) api->GroupStart();
+        for (int g = 0; g < count && s == LORA_OK; ++g)
+            if (problems[g].da) s = allreduce_impl(c, problems[g].da, size_t(local[g].rank) * local[g].d_in,
+                                                   LORA_DT_F32, st);
+        if (api->GroupEnd) {
+            ncclResult_t r = api->GroupEnd();
+            if (s == LORA_OK && r != ncclSuccess) s = nccl_fail(api, r, "ncclGroupEnd");
+        }
+        if (s != LORA_OK) return s;
     }
     set_launches(launches);
     return LORA_OK;

@@ -187,6 +187,15 @@ struct AdamGroup {
 };
 cudaError_t launch_adam(AdamGroup& G, int num_sms, cudaStream_t stream);
 
+// dst = RNE_bf16(sum of n bf16 tensors of `count` elements, count % 8 == 0), fp32 accumulation
+struct SumBf16Args {
+    const __nv_bfloat16* src[kMaxGroup];
+    __nv_bfloat16* dst;
+    int64_t count;
+    int n;
+};
+cudaError_t launch_sum_bf16(const SumBf16Args& A, int num_sms, cudaStream_t stream);
+
 // dst += src (fp32), used by the TP backward when accumulating reduced grads
 cudaError_t launch_add_f32(float* dst, const float* src, int64_t count, cudaStream_t stream);
 

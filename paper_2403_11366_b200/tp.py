@@ -180,3 +180,48 @@ def tp_linear_bwd(comm: LoraComm, spec: ShardSpec, x, w0, a, b, dy, alpha, h_sav
                                   1 if reduce_lora_grads else 0, _ptr(ws), ws.numel(), _stream(stream)),
            "lora_tp_linear_bwd")
     return dx, da, db
+
+
+def tp_linear_bwd_column_group(comm: LoraComm, specs, problems, alphas, dx_sum=None, want_dx=True, outs=None,
+                               reduce_lora_grads=True, workspace=None, stream=None):
+    """lora_tp_linear_bwd_column_group: the backward of COLUMN-parallel linears that
+    read the same input (q/k/v, gate/up).  problems: list of
+    (x, w0, a, b, dy, h_saved) local shards with the SAME x tensor.  The members'
+    dX partials are summed into dx_sum (the gradient w.r.t. the shared input) and
+    all-reduced once.  Returns (dx_sum, [(dx_g, dA_g, dB_g)])."""
+    import torch
+
+    from . import _check, _ptr, _stream, _workspace, dims, lib, lora_bwd_problem, lora_dims
+    G = len(problems)
+    x = problems[0][0]
+    T = x.shape[0]
+    n = specs[0].local_n
+    if any(sp.mode != COLUMN for sp in specs):
+        raise ValueError("tp_linear_bwd_column_group is for COLUMN-parallel linears")
+    if any(p[0] is not x and p[0].data_ptr() != x.data_ptr() for p in problems):
+        raise ValueError("all problems must share the same input tensor x")
+    if dx_sum is None and want_dx:
+        dx_sum = torch.empty((T, n), dtype=torch.bfloat16, device=x.device)
+    dims_arr = (lora_dims * G)()
+    probs = (lora_bwd_problem * G)()
+    res = []
+    for g, ((xg, w0, a, b, dy, h), sp) in enumerate(zip(problems, specs)):
+        r = a.shape[0]
+        m = sp.local_m
+        dx, da, db = outs[g] if outs is not None else (None, None, None)
+        if dx is None and want_dx:
+            dx = torch.empty((T, n), dtype=torch.bfloat16, device=x.device)
+        if da is None:
+            da = torch.zeros((r, n), dtype=torch.float32, device=x.device)
+        if db is None:
+            db = torch.zeros((m, r), dtype=torch.float32, device=x.device)
+        dims_arr[g] = dims(T, n, m, r, alphas[g])
+        probs[g] = lora_bwd_problem(_ptr(xg), _ptr(w0), _ptr(a), _ptr(b), _ptr(h), _ptr(dy), _ptr(dx), _ptr(da),
+                                    _ptr(db))
+        res.append((dx, da, db))
+    need = int(lib.lora_tp_linear_bwd_column_group_workspace_bytes(G, dims_arr))
+    ws = workspace if workspace is not None else _workspace(need, x.device)
+    _check(lib.lora_tp_linear_bwd_column_group(comm.handle, G, dims_arr, probs, _ptr(dx_sum), 0,
+                                               1 if reduce_lora_grads else 0, _ptr(ws), ws.numel(),
+                                               _stream(stream)), "lora_tp_linear_bwd_column_group")
+    return dx_sum, res

@@ -55,3 +55,33 @@ def test_allreduce_n1_identity(comm):
     comm.allreduce(tb)
     torch.cuda.synchronize()
     assert torch.equal(tb, refb)
+
+
+def test_tp_column_group_sums_dx(comm, oracle_mod):
+    """lora_tp_linear_bwd_column_group (q, k, v fused): the
+    members' dX partials summed into the gradient w.r.t. the shared input, ONE
+    all-reduce; dA, dB as the single calls.  Checked at N = 1 against the fp64
+    oracle's sum of the members' dX."""
+    import paper_2403_11366_b200 as L
+    from paper_2403_11366_b200 import tp
+    from tests.gpu_util import TOL_GRAD, TOL_OUT, host_f64, relF
+    T, n = 512, 384
+    base = make_lora_inputs(T, n, 8, 8, seed=70)
+    x = dev_bf16(base["x"])
+    specs, probs, refs, singles = [], [], [], []
+    for i, (m, r) in enumerate([(256, 8), (136, 16), (192, 5)]):
+        d = make_lora_inputs(T, n, m, r, seed=71 + i)
+        d["x"] = base["x"]
+        w0, a, b, dy = (dev_bf16(d[k]) for k in ("w0", "a", "b", "dy"))
+        _, h = L.lora_linear_fwd(x, w0, a, b, 16.0)
+        specs.append(tp.ShardSpec(tp.COLUMN, 1, 0, n, m))
+        probs.append((x, w0, a, b, dy, h))
+        refs.append(oracle_mod.lora_bwd(d["x"], d["w0"], d["a"], d["b"], d["dy"], 16.0))
+        singles.append(L.lora_linear_bwd(x, w0, a, b, dy, 16.0, h_saved=h))
+    dx_sum, res = tp.tp_linear_bwd_column_group(comm, specs, probs, [16.0] * 3)
+    torch.cuda.synchronize()
+    assert relF(host_f64(dx_sum), sum(rf["dx"] for rf in refs)) <= TOL_OUT
+    for (dx, da, db), (dx1, da1, db1), rf in zip(res, singles, refs):
+        assert torch.equal(dx, dx1)                              # the members' own partials are kept
+        assert relF(host_f64(da), rf["da"]) <= TOL_GRAD and relF(host_f64(db), rf["db"]) <= TOL_GRAD
+        torch.testing.assert_close(da, da1, rtol=1e-5, atol=1e-5 * float(da1.abs().max()))
