@@ -597,10 +597,26 @@ def run_ours(args, wl):
         t_grads = timed(lambda: L.lora_linear_bwd(e["x"], e["w0"], e["a"], e["b"], e["dy"], l0_.alpha,
                                                   h_saved=e["h"], want_dx=False, da=da_, db=db_,
                                                   workspace=e["ws_b"], stream=torch.cuda.current_stream()))
+        # N3: one Adam step over every adapter tensor of the workload (A and B of each
+        # linear, fp32 master + moments): ONE launch; 30 bytes per parameter
+        ad = []
+        for e in lin:
+            for t, g in ((e["a"], e["da"]), (e["b"], e["db"])):
+                ad.append((t.clone(), g, torch.zeros_like(g), torch.zeros_like(g), t.float()))
+        adam_step_no = [0]
+
+        def adam_call():
+            adam_step_no[0] += 1
+            L.lora_adam_step(ad, adam_step_no[0], 1e-4, stream=torch.cuda.current_stream())
+
+        t_adam = timed(adam_call)
+        adam_bytes = 30 * sum(t[0].numel() for t in ad)
         merge_bytes = 4 * m0 * n0 + 2 * r0 * (m0 + n0)
         # dY read twice (gh pre-pass, dB), x once, coefficients ~ 16 T r
         grads_bytes = 2 * T0 * (2 * m0 + n0) + 16 * T0 * r0
         aux = {"merge": {"us": t_merge * 1e6, "bytes": merge_bytes, "gbs": merge_bytes / t_merge / 1e9},
+               "adam_all_adapters": {"us": t_adam * 1e6, "bytes": adam_bytes, "gbs": adam_bytes / t_adam / 1e9,
+                                     "tensors": len(ad)},
                "grads_only": {"us": t_grads * 1e6, "bytes": grads_bytes, "gbs": grads_bytes / t_grads / 1e9,
                               "kernels": "gh pre-pass + K3s split + K3 (lora_linear_bwd, dx = NULL)"}}
 
