@@ -177,7 +177,7 @@ static FwdWs fwd_ws(const lora_dims* d, bool dropout = false) {
 
 // Backward workspace: B^T [r, m], gh [T, r] fp32, h [T, r] fp32 (when not saved).
 struct BwdWs {
-    size_t b8, gh, h, flags, cs_a, cs_b, xm, bits, total;
+    size_t b8, gh, h, cs_a, cs_b, xm, bits, total;
 };
 static BwdWs bwd_ws(const lora_dims* d, bool dropout = false) {
     BwdWs w;
@@ -187,7 +187,6 @@ static BwdWs bwd_ws(const lora_dims* d, bool dropout = false) {
     w.b8 = off; off += align256(size_t(d->d_out) * r8_of(r) * 2);    // only used when r % 8 != 0
     w.gh = off; off += align256(size_t(T) * r * 4);
     w.h = off; off += align256(size_t(T) * r * 4);
-    w.flags = off; off += align256(size_t(T / 128 + 2) * 8);         // >= row blocks x CTAs per pair
     const size_t cs = align256(size_t(3 * r8_of(r)) * size_t((T + 63) / 64 * 64) * 2);
     w.cs_a = off; off += cs;                                         // K3s: split gh
     w.cs_b = off; off += cs;                                         // K3s: split h
@@ -199,17 +198,12 @@ static BwdWs bwd_ws(const lora_dims* d, bool dropout = false) {
     return w;
 }
 
-// Value the dX kernel's gh flags take in one launch: a per-process random base
-// plus a counter, so stale workspace contents never match by accident.
-static uint64_t next_epoch() {
-    static std::atomic<uint64_t> counter{0};
-    static const uint64_t base = [] {
-        uint64_t v = static_cast<uint64_t>(std::chrono::high_resolution_clock::now().time_since_epoch().count());
-        v ^= reinterpret_cast<uintptr_t>(&counter) * 0x9E3779B97F4A7C15ull;
-        return v | 1ull;
-    }();
-    return base + 2 * counter.fetch_add(1);
-}
+// The dX kernel's per-row-block gh flags live in the self-cleaning device sync
+// pool (lora_kernels.h): the gh tile raises them to 1 and the last consumer
+// (K2's last CTA, or K3's when K3 waits on them) zeroes them again, so a
+// captured CUDA graph replays correctly -- a per-call flag value baked into the
+// kernel parameters would already be set by the previous replay.
+static constexpr uint64_t kFlagSet = 1;
 
 static lora_status collect(GemmCollector* col, const FusedGemmMaps& maps, const FusedGemmParams& p, int rp, int cg);
 
@@ -277,6 +271,8 @@ lora_status fwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
     p.gh = nullptr;
     p.flags = nullptr;
     p.epoch = 0;
+    p.nflags = 0;
+    p.reset_flags = 0;
     p.h_in = nullptr;
     p.drop = DropoutParams{};
     p.drop_bits = nullptr;
@@ -335,11 +331,13 @@ static lora_status launch_k3_mma(const GradArgs* pr, int count, cudaStream_t str
         const GradArgs& g = pr[i];
         const int r8 = (g.r + 7) / 8 * 8;
         if (g.da) {
-            GradMmaSet s = {g.da, 1, g.n, g.r, r8, 0, g.accumulate, g.scale_a, 3};
+            GradMmaSet s = {g.da, 1, g.n, g.r, r8, 0, g.accumulate, g.scale_a, 3, nullptr, 0};
+            if (g.cs_a_ready && g.k2_flags) { s.wait_flags = g.k2_flags; s.wait_n = g.k2_nflags; }
             sets[ns++] = {g.x, g.T, g.n, g.gh, g.cs_a, g.cs_a_ready != 0, s};
         }
         if (g.db) {
-            GradMmaSet s = {g.db, g.r, 1, g.r, r8, 0, g.accumulate, g.scale_b, 3};
+            GradMmaSet s = {g.db, g.r, 1, g.r, r8, 0, g.accumulate, g.scale_b, 3, nullptr, 0};
+            if (g.cs_b_ready && g.k2_flags) { s.wait_flags = g.k2_flags; s.wait_n = g.k2_nflags; }
             sets[ns++] = {g.dy, g.T, g.m, g.h, g.cs_b, g.cs_b_ready != 0, s};
         }
     }
@@ -400,8 +398,24 @@ static lora_status launch_k3_mma(const GradArgs* pr, int count, cudaStream_t str
         if ((e = launch_coef_split(SG, stream)) != cudaSuccess) return cuda_fail(e, "K3s (coefficient split) launch");
         ++*launches;
     }
-    e = launch_grad_mma(G, dev.sms, stream);
-    if (e != cudaSuccess) return cuda_fail(e, "K3 (tensor-core dA / dB) launch");
+    // every coefficient set comes straight from the K2 launched just before (no K3s
+    // in between): K3 may start on the SMs K2 frees and wait on K2's flags instead
+    bool overlap = SG.count == 0, waits = false;
+    for (int i = 0; i < k; ++i) {
+        overlap = overlap && G.set[i].wait_flags != nullptr;
+        waits = waits || G.set[i].wait_flags != nullptr;
+    }
+    G.done = nullptr;
+    if (waits && (G.done = sync_pool_alloc(1, stream)) == nullptr)
+        e = cudaErrorMemoryAllocation;
+    else
+        e = launch_grad_mma(G, dev.sms, stream, overlap);
+    if (e != cudaSuccess) {
+        for (int i = 0; i < k; ++i)   // leave no raised flag behind in the pool
+            if (G.set[i].wait_flags)
+                cudaMemsetAsync(const_cast<uint64_t*>(G.set[i].wait_flags), 0, size_t(G.set[i].wait_n) * 8, stream);
+        return cuda_fail(e, "K3 (tensor-core dA / dB) launch");
+    }
     ++*launches;
     return LORA_OK;
 }
@@ -546,6 +560,7 @@ lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
     const auto* dya = static_cast<const __nv_bfloat16*>(dy);
     const bool need_gh = dx || da;
     const bool need_h = db && !h_saved;
+    const uint64_t* k2_flags = nullptr;   // this problem's K2 gh flags (stage 1; grouped stage 2: from col)
 
     auto* xm = reinterpret_cast<__nv_bfloat16*>(wsb + W.xm);
     if (dropping && (stages & 1)) {
@@ -581,8 +596,17 @@ lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
         p.out = static_cast<__nv_bfloat16*>(dx);
         p.side_out = nullptr;
         p.gh = gh;
-        p.flags = reinterpret_cast<uint64_t*>(wsb + W.flags);
-        p.epoch = next_epoch();
+        p.epoch = kFlagSet;
+        p.nflags = static_cast<int>(fused_gemm_row_blocks(T, cg) * cg);
+        p.flags = p.nflags > 0 ? reinterpret_cast<uint64_t*>(sync_pool_alloc(p.nflags, stream)) : nullptr;
+        if (p.nflags > 0 && p.flags == nullptr)
+            return fail(LORA_ERR_CUDA, "dX kernel: device sync pool exhausted or unavailable");
+        // K3 (tensor cores) waits on these flags and zeroes them when it reads a
+        // coefficient split this K2 writes; otherwise K2's last CTA does
+        const bool k3_waits = k3_mode() == kK3Mma &&
+                              (da != nullptr || (db != nullptr && (h_saved != nullptr || (dropping && need_h))));
+        p.reset_flags = k3_waits ? 0 : 1;
+        k2_flags = p.flags;
         p.h_in = nullptr;
         p.drop = dropping ? *drop : DropoutParams{};
         p.drop_bits = dropping ? reinterpret_cast<const uint32_t*>(wsb + W.bits) : nullptr;
@@ -633,6 +657,15 @@ lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
         g.cs_b = reinterpret_cast<__nv_bfloat16*>(wsb + W.cs_b);
         g.cs_a_ready = dx != nullptr;                                        // K2 split gh
         g.cs_b_ready = dx != nullptr && (h_saved != nullptr || (dropping && need_h));
+        if (dx && !k2_flags && col) {   // grouped: stage 1 collected this problem's K2
+            for (int i = 0; i < col->count; ++i)
+                if (col->p[i].out == dx) k2_flags = col->p[i].flags;
+        }
+        if (dx) {   // K2 raises these once a row block's split coefficients are written
+            if (!k2_flags && T > 0) return fail(LORA_ERR_INVALID, "lora_linear_bwd: internal: dX kernel flags not found");
+            g.k2_flags = k2_flags;
+            g.k2_nflags = static_cast<int>(fused_gemm_row_blocks(T, cta_group_for(T)) * cta_group_for(T));
+        }
         if (col) {   // grouped backward: one K3 launch for the whole group
             if (col->k3_count >= kMaxGroup) return fail(LORA_ERR_UNSUPPORTED, "too many grouped problems");
             col->k3[col->k3_count++] = g;

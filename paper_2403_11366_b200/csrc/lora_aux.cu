@@ -41,6 +41,17 @@ __global__ void __launch_bounds__(256) merge_kernel(const bf16* __restrict__ w0,
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t k0 = static_cast<int64_t>(blockIdx.x) * 256;
     const int64_t i0 = static_cast<int64_t>(blockIdx.y) * 64;
+    const int kc = lane * 8;
+    const bool col_ok = k0 + kc < n;
+    // this thread's 8 rows of W0 (16-byte loads) go in flight FIRST: their HBM
+    // latency overlaps the A / B staging below instead of following it
+    uint4 wraw[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const int64_t i = i0 + warp + 8 * q;
+        wraw[q] = (col_ok && i < m) ? __ldg(reinterpret_cast<const uint4*>(w0 + i * n + k0 + kc))
+                                    : make_uint4(0, 0, 0, 0);
+    }
     for (int idx = threadIdx.x; idx < RB * 32; idx += 256) {   // 8 columns per thread (n % 8 == 0)
         const int j = idx >> 5, kk = (idx & 31) * 8;
         float f[8];
@@ -58,15 +69,7 @@ __global__ void __launch_bounds__(256) merge_kernel(const bf16* __restrict__ w0,
         sB[idx] = (j < r && i0 + ii < m) ? __bfloat162float(b[(i0 + ii) * r + j]) : 0.0f;
     }
     __syncthreads();
-    const int kc = lane * 8;
-    if (k0 + kc >= n) return;
-    // all 8 rows' 16-byte W0 loads in flight before any math (HBM latency)
-    uint4 wraw[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-        const int64_t i = i0 + warp + 8 * q;
-        wraw[q] = i < m ? __ldg(reinterpret_cast<const uint4*>(w0 + i * n + k0 + kc)) : make_uint4(0, 0, 0, 0);
-    }
+    if (!col_ok) return;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
         const int ii = warp + 8 * q;

@@ -47,6 +47,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <mutex>
 
 #include "lora_kernels.h"
 #include "sm100_ptx.cuh"
@@ -200,14 +201,6 @@ __device__ __forceinline__ void tmem_dealloc_cg(uint32_t taddr) {
     } else {
         asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(taddr) : "memory");
     }
-}
-__device__ __forceinline__ uint64_t ld_acquire_u64(const uint64_t* p) {
-    uint64_t v;
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release_u64(uint64_t* p, uint64_t v) {
-    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 // Tile `tile` of a group -> (problem g, row block, column block, k-blocks).
@@ -679,6 +672,51 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
         tc_fence_after();
         tmem_dealloc_cg<CG>(tmem_base);
     }
+    // self-cleaning gh flags: every CTA is past its last flag wait; the last one
+    // out zeroes the flags no K3 will wait on, and the counter
+    if (MODE != kModeFwd && grp.done != nullptr && threadIdx.x == 0) {
+        if (atom_add_acq_rel_u64(grp.done, 1ull) == static_cast<unsigned long long>(gridDim.x) - 1) {
+            for (int g = 0; g < grp.count; ++g)
+                if (grp.p[g].reset_flags)
+                    for (int i = 0; i < grp.p[g].nflags; ++i) grp.p[g].flags[i] = 0;
+            *grp.done = 0;   // (visible to the next launch: kernel boundary)
+        }
+    }
+}
+
+// ----------------------------------------------------------------------------
+// sync pool (see lora_kernels.h)
+// ----------------------------------------------------------------------------
+constexpr int kSyncPoolWords = 1 << 18;   // 2 MiB of device memory
+constexpr int kSyncPoolRing = 1 << 17;    // [0, ring): eager calls, recycled; [ring, end): captured graphs
+__device__ unsigned long long g_sync_pool[kSyncPoolWords];
+
+unsigned long long* sync_pool_alloc(int words, cudaStream_t stream) {
+    static std::mutex mu;
+    static unsigned long long* base[64] = {};
+    static int ring_next[64] = {}, perm_next[64] = {};
+    if (words <= 0 || words > 4096) return nullptr;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess) return nullptr;
+    const int w = (words + 7) / 8 * 8;   // 64-byte granules
+    std::lock_guard<std::mutex> lk(mu);
+    if (base[dev] == nullptr) {
+        void* p = nullptr;
+        if (cudaGetSymbolAddress(&p, g_sync_pool) != cudaSuccess) return nullptr;
+        base[dev] = static_cast<unsigned long long*>(p);
+    }
+    if (cs != cudaStreamCaptureStatusNone) {
+        if (kSyncPoolRing + perm_next[dev] + w > kSyncPoolWords) return nullptr;
+        unsigned long long* r = base[dev] + kSyncPoolRing + perm_next[dev];
+        perm_next[dev] += w;
+        return r;
+    }
+    if (ring_next[dev] + w > kSyncPoolRing) ring_next[dev] = 0;
+    unsigned long long* r = base[dev] + ring_next[dev];
+    ring_next[dev] += w;
+    return r;
 }
 
 // ----------------------------------------------------------------------------
@@ -706,6 +744,13 @@ static cudaError_t launch_impl(FusedGemmGroup& grp, int num_sms, cudaStream_t st
         tiles += ((p.T + BM * CG - 1) / (BM * CG)) * col_tiles_host(MODE, R_PAD, p.N_out);
     }
     grp.tile_start[grp.count] = static_cast<int>(tiles);
+    grp.done = nullptr;
+    bool any_reset = false;
+    for (int g = 0; g < grp.count; ++g) any_reset = any_reset || (MODE != kModeFwd && grp.p[g].reset_flags);
+    if (any_reset) {   // someone must zero the flags at the end (no K3 waits on them)
+        grp.done = sync_pool_alloc(1, stream);
+        if (grp.done == nullptr) return cudaErrorMemoryAllocation;
+    }
     const int64_t units = num_sms / CG;
     const int grid = static_cast<int>((tiles < units ? tiles : units) * CG);
     if (grid <= 0) return cudaSuccess;

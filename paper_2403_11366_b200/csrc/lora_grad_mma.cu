@@ -144,6 +144,27 @@ cudaError_t launch_coef_split(const CoefSplitGroup& G, cudaStream_t stream) {
 }
 
 // ------------------------------------------------------------------ K3
+// Launch epilogue of every K3 CTA: wait until the preceding grid (K2, when K3
+// was launched overlapping it) has completed -- so stream order stays
+// transitive for the kernels after K3 -- then the last CTA out zeroes the K2
+// flags this launch waited on (self-cleaning sync pool, lora_kernels.h).
+__device__ __forceinline__ void k3_exit(const GradMmaGroup& G) {
+    if (G.done == nullptr || threadIdx.x != 0) {
+        griddep_wait();
+        return;
+    }
+    const unsigned long long ctas = static_cast<unsigned long long>(gridDim.x) * gridDim.y;
+    const bool last = atom_add_acq_rel_u64(G.done, 1ull) == ctas - 1;
+    griddep_wait();   // K2 complete: no tile of it still reads the flags
+    if (!last) return;
+    for (int jb = 0; jb < G.njobs; ++jb)
+        for (int j = 0; j < G.job[jb].nsets; ++j) {
+            const GradMmaSet& st = G.set[G.job[jb].set0 + j];
+            for (int f = 0; f < st.wait_n; ++f) const_cast<uint64_t*>(st.wait_flags)[f] = 0;
+        }
+    *G.done = 0;   // (visible to the next launch: kernel boundary)
+}
+
 __global__ void __launch_bounds__(THREADS, 1) grad_mma_kernel(const __grid_constant__ GradMmaGroup G) {
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
@@ -208,11 +229,31 @@ __global__ void __launch_bounds__(THREADS, 1) grad_mma_kernel(const __grid_const
     K3_STAMP(0);
 
     if (warp == 0) {
+        // coefficients produced by a still-running K2: the whole warp polls its row-block
+        // flags (32 relaxed loads in flight, not one acquire round trip per flag), then
+        // one fence makes the observed release stores an acquire for this thread's TMA
+        for (int j = 0; j < J.nsets; ++j) {
+            const GradMmaSet& st = G.set[J.set0 + j];
+            for (int f0 = 0; f0 < st.wait_n; f0 += 32) {
+                const int f = f0 + static_cast<int>(lane);
+                const uint64_t t_start = globaltimer_ns();
+                while (!__all_sync(0xffffffffu, f >= st.wait_n || ld_relaxed_u64(st.wait_flags + f) == 1ull)) {
+                    __nanosleep(128);
+                    if (globaltimer_ns() - t_start > 4000000000ull) {
+                        if (lane == 0) printf("lora K3: coefficient flag wait timed out (set %d)\n", J.set0 + j);
+                        __trap();
+                    }
+                }
+            }
+        }
+        fence_acq_rel_gpu();   // each lane: acquire of the flags it observed
+        __syncwarp();          // ... ordered before lane 0's TMA issue below
         // ---------------- TMA producer: X boxes [64 tokens][64 columns] + Cs boxes [3 r8 rows][64 tokens]
         if (lane == 0) {
             uint32_t tx = nbox * X_BOX;
             for (int j = 0; j < J.nsets; ++j) tx += G.set[J.set0 + j].nsplit * G.set[J.set0 + j].r8 * 128;
             const uint64_t pol = l2_policy_evict_first();
+            fence_proxy_async_global();
             for (int i = 0, s = 0, ph = 0; i < nkb; ++i) {
                 mbar_wait(&empty[s], ph ^ 1);
                 uint8_t* sx = smem + s * stage_bytes;
@@ -319,6 +360,7 @@ __global__ void __launch_bounds__(THREADS, 1) grad_mma_kernel(const __grid_const
             tmem_dealloc_n(tmem_base, G.tmem_cols);
         }
         K3_STAMP(3);
+        k3_exit(G);
         return;
     }
     cluster.sync();   // all partials of the cluster written (release / acquire)
@@ -382,12 +424,22 @@ __global__ void __launch_bounds__(THREADS, 1) grad_mma_kernel(const __grid_const
     }
     K3_STAMP(3);
     cluster.sync();   // peers may still read this CTA's partial
+    k3_exit(G);
 }
 
 // Token split S (cluster size): minimise waves x (k-blocks per CTA + a fixed
 // cost of ~6 k-blocks for prologue, epilogue and reduction); ties -> smaller S.
 // slots[S] = CTAs of cluster size S that can be co-resident (cluster
 // placement within GPCs makes this smaller than CTAs-per-SM x SMs for S > 1).
+// K3 / K2 overlap on by default; LORA_K3_OVERLAP=0 launches K3 in plain stream order.
+bool k3_overlap_enabled() {
+    static const bool on = [] {
+        const char* v = getenv("LORA_K3_OVERLAP");
+        return !(v && v[0] == '0');
+    }();
+    return on;
+}
+
 int grad_mma_cluster_size(int tiles, int kb_total, const int* slots) {
     int best = 1;
     long best_cost = -1;
@@ -400,7 +452,7 @@ int grad_mma_cluster_size(int tiles, int kb_total, const int* slots) {
     return best;
 }
 
-cudaError_t launch_grad_mma(GradMmaGroup& G, int num_sms, cudaStream_t stream) {
+cudaError_t launch_grad_mma(GradMmaGroup& G, int num_sms, cudaStream_t stream, bool overlap_prev) {
     if (G.njobs < 1 || G.njobs > kMaxGradJobs) return cudaErrorInvalidValue;
     int tiles = 0, qmax = 16, pmax = 0, kb_max = 1;
     for (int jb = 0; jb < G.njobs; ++jb) {
@@ -486,6 +538,11 @@ cudaError_t launch_grad_mma(GradMmaGroup& G, int num_sms, cudaStream_t stream) {
     }
     cfg.gridDim = dim3(tiles, G.S);
     attr[0].val.clusterDim.y = G.S;
+    cudaLaunchAttribute attrs[2] = {attr[0], {}};
+    attrs[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attrs[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attrs;
+    cfg.numAttrs = overlap_prev && k3_overlap_enabled() ? 2 : 1;
     e = cudaLaunchKernelEx(&cfg, grad_mma_kernel, G);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();

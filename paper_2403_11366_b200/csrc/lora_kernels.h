@@ -13,6 +13,7 @@ enum : int { kModeFwd = 0, kModeDx = 1, kModeDxDrop = 2 };
 
 // Programmatic dependent launch for the step's kernels (LORA_PDL=1; off by default).
 bool pdl_enabled();
+bool k3_overlap_enabled();   // LORA_K3_OVERLAP (default on)
 
 // LoRA dropout (lora_philox.cuh): keep(t, k) = Philox4x32-10((k/4, t, offset), seed)[k % 4] >= thr
 struct DropoutParams {
@@ -31,8 +32,10 @@ struct FusedGemmParams {
     __nv_bfloat16* out;           // y or dx, [T, N_out]
     float* side_out;              // fwd: h [T, r] (unscaled), may be null
     float* gh;                    // dx: gh [T, r] = s dY B, written by the first column tile
-    uint64_t* flags;              // dx: one per (row block, CTA of the pair): gh published
-    uint64_t epoch;               // dx: value the flags take in this launch (never reset)
+    uint64_t* flags;              // dx: one per (row block, CTA of the pair), sync pool: 1 = gh published
+    uint64_t epoch;               // dx: value a published flag holds (1)
+    int nflags;                   // dx: row blocks x CTAs per pair
+    int reset_flags;              // dx: 1 = this launch's last CTA zeroes the flags (no K3 waits on them)
     const float* h_in;            // fwd with dropout: h [T, r] precomputed by K0 (else null: h from the MMA)
     DropoutParams drop;           // dx dropout mode: dX += q M . (gh A) in the epilogue
     const uint32_t* drop_bits;    // dx dropout mode: keep bits [T, ceil(N_out/32)] from K0
@@ -56,7 +59,17 @@ struct FusedGemmGroup {
     FusedGemmParams p[kMaxGroup];
     int tile_start[kMaxGroup + 1];
     int count;
+    unsigned long long* done;     // dx: sync-pool launch counter (last CTA out resets flags), or null
 };
+
+// Device-side synchronisation words (K2's gh flags, launch done-counters): a
+// static __device__ pool, zero when the module loads.  Every protocol that
+// uses it returns its words to zero before its launch chain ends (the last
+// consumer resets), so no host memset is needed and captured CUDA graphs
+// replay correctly.  Eager calls take words from a recycled ring; calls made
+// while `stream` is capturing get words of their own for the graph's lifetime.
+// Returns null when the pool is exhausted (capture) or on a CUDA error.
+unsigned long long* sync_pool_alloc(int words, cudaStream_t stream);
 
 // K1 / K2.  r_pad in {16, 32, 64}; tiles are (128 * cta_group) x (256 - r_pad).
 // cta_group = 2 runs on CTA pairs (tcgen05 cta_group::2); the TMA boxes of
@@ -93,6 +106,8 @@ struct GradArgs {
     __nv_bfloat16* cs_b;      // tensor-core K3: split h  [3 r8, T_pad] (workspace)
     float scale_a;            // dA multiplier (1, or q = 1/(1-p) when x is the dropout-masked M . x)
     int cs_a_ready, cs_b_ready;   // split already written by K2 (no K3s work for that set)
+    const uint64_t* k2_flags;     // K2's per-row-block flags (value 1 once cs_* are written), or null
+    int k2_nflags;
 };
 // several problems of the same rank bucket in one K3 launch
 struct GradGroup {
@@ -119,6 +134,11 @@ struct GradMmaSet {
     int r, r8, row0, accumulate;
     float scale;
     int nsplit;                 // 3: rows hi / mid / lo of an fp32 coefficient (K3s); 1: a bf16 operand as is
+    // the dX kernel (K2) of the same backward writes this set's split coefficients
+    // and raises wait_flags[0 .. wait_n) to 1 per row block: K3 waits on them before
+    // its first coefficient load (lets K3 start while K2 is still running; else null)
+    const uint64_t* wait_flags;
+    int wait_n;
 };
 struct GradMmaJob {
     int64_t T, N;               // T: reduction extent (k-blocks of 64), N: output extent (MMA M, 128 per CTA)
@@ -130,13 +150,17 @@ struct GradMmaGroup {
     CUtensorMap xmap[kMaxGradJobs];
     CUtensorMap csmap[kMaxGradSetsTotal];
     GradMmaSet set[kMaxGradSetsTotal];
+    unsigned long long* done;   // sync-pool launch counter: the last CTA out zeroes every set's wait_flags
     GradMmaJob job[kMaxGradJobs];
     int tile_start[kMaxGradJobs + 1];
     int njobs;
     // filled in by launch_grad_mma
     int S, stages, stage_bytes, region_bytes, tmem_cols;
 };
-cudaError_t launch_grad_mma(GradMmaGroup& G, int num_sms, cudaStream_t stream);
+// overlap_prev: launch with programmatic stream serialization, so K3's CTAs
+// fill the SMs the preceding K2 frees in its last wave; only legal when every
+// set that K2 produces carries wait_flags and nothing else runs in between.
+cudaError_t launch_grad_mma(GradMmaGroup& G, int num_sms, cudaStream_t stream, bool overlap_prev = false);
 int grad_mma_cluster_size(int tiles, int kb_total, const int* slots /* [9], by cluster size */);
 
 // K3s: cs [3 r8, T_pad] bf16 = exact hi / mid / lo split of coef [T, r] fp32

@@ -405,3 +405,62 @@ def test_k3_token_split_paths(oracle_mod, L, split, monkeypatch):
         go = oracle_mod.lora_bwd(d["x"], d["w0"], d["a"], d["b"], d["dy"], 16.0, want_dx=False)
         assert relF(host_f64(da) - 0.5, go["da"]) <= TOL_GRAD, (split, T, n, m, r)
         assert relF(host_f64(db) + 1.0, go["db"]) <= TOL_GRAD, (split, T, n, m, r)
+
+
+def test_graph_replay_new_inputs(oracle_mod, L):
+    """A captured backward (grouped, K2 -> K3 overlapped) replayed with NEW dY and h
+    each time: every replay equals the eager call on the same inputs bit for bit
+    and the oracle within tolerance.  Guards the per-launch reset of K2's gh flags
+    (a flag value frozen into the graph would let later tiles and K3 read the
+    previous replay's gh) and K3's wait on them."""
+    T, n, m, r, alpha = 1024, 512, 768, 8, 16.0
+    base = make_lora_inputs(T, n, m, r, seed=77)
+    x, a_q, b_q = dev_bf16(base["x"]), dev_bf16(base["a"]), dev_bf16(base["b"])
+    w_q = dev_bf16(base["w0"])
+    other = make_lora_inputs(T, n, m, r, seed=78)
+    w_v, a_v, b_v = dev_bf16(other["w0"]), dev_bf16(other["a"]), dev_bf16(other["b"])
+    dy_q = torch.empty((T, m), dtype=torch.bfloat16, device="cuda")
+    dy_v = torch.empty_like(dy_q)
+    h_q = torch.empty((T, r), dtype=torch.float32, device="cuda")
+    h_v = torch.empty_like(h_q)
+    outs = [(torch.empty((T, n), dtype=torch.bfloat16, device="cuda"),
+             torch.empty((r, n), dtype=torch.float32, device="cuda"),
+             torch.empty((m, r), dtype=torch.float32, device="cuda")) for _ in range(2)]
+    probs = [(x, w_q, a_q, b_q, dy_q, h_q), (x, w_v, a_v, b_v, dy_v, h_v)]
+    ws = torch.empty(1 << 24, dtype=torch.uint8, device="cuda")
+
+    def load(seed):
+        d = make_lora_inputs(T, n, m, r, seed=seed)
+        dy_q.copy_(dev_bf16(d["dy"]))
+        dy_v.copy_(dev_bf16(make_lora_inputs(T, n, m, r, seed=seed + 500)["dy"]))
+        for hh, (ww, aa, bb) in ((h_q, (w_q, a_q, b_q)), (h_v, (w_v, a_v, b_v))):
+            _, h = L.lora_linear_fwd(x, ww, aa, bb, alpha)
+            hh.copy_(h)
+        torch.cuda.synchronize()
+
+    load(1000)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):   # warm-up outside capture (kernel attributes, maps)
+        L.lora_linear_bwd_grouped(probs, [alpha, alpha], outs=outs, workspace=ws, stream=s)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        L.lora_linear_bwd_grouped(probs, [alpha, alpha], outs=outs, workspace=ws, stream=s)
+    for seed in (1001, 1002, 1003):
+        load(seed)
+        g.replay()
+        torch.cuda.synchronize()
+        got = [[t.clone() for t in o] for o in outs]
+        ref = L.lora_linear_bwd_grouped(probs, [alpha, alpha], workspace=ws)
+        torch.cuda.synchronize()
+        for gi in range(2):
+            for t_got, t_ref in zip(got[gi], ref[gi]):
+                assert torch.equal(t_got, t_ref), f"replay seed {seed} member {gi}"
+        # member q against the oracle
+        dq = bits_of(dy_q)
+        go = oracle_mod.lora_bwd(base["x"], base["w0"], base["a"], base["b"], dq, alpha)
+        assert relF(host_f64(got[0][0]), go["dx"]) <= TOL_OUT
+        assert relF(host_f64(got[0][1]), go["da"]) <= TOL_GRAD
+        assert relF(host_f64(got[0][2]), go["db"]) <= TOL_GRAD
