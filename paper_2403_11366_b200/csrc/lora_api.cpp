@@ -163,8 +163,10 @@ static int cta_group_for(int64_t T) {
 
 // Forward workspace: B8 (B zero-padded to a multiple of 8 columns), used only
 // when r % 8 != 0 (sized unconditionally so it depends on dims alone).
+// Both also hold the fused GEMM's stream-K partial slots when the problem is
+// large enough to get a stream-K schedule (fused_gemm_partial_bytes).
 struct FwdWs {
-    size_t b8, h, total;
+    size_t b8, h, partial, partial_bytes, total;
 };
 static FwdWs fwd_ws(const lora_dims* d, bool dropout = false) {
     FwdWs w;
@@ -172,12 +174,15 @@ static FwdWs fwd_ws(const lora_dims* d, bool dropout = false) {
     w.h = align256(size_t(d->d_out) * r8_of(d->rank) * 2);
     w.total = w.h;
     if (dropout) w.total += align256(size_t(d->tokens > 0 ? d->tokens : 0) * d->rank * 4);   // K0's h
+    w.partial = w.total;
+    w.partial_bytes = fused_gemm_partial_bytes(d->tokens > 0 ? d->tokens : 0, d->d_out);
+    w.total += align256(w.partial_bytes);
     return w;
 }
 
 // Backward workspace: B^T [r, m], gh [T, r] fp32, h [T, r] fp32 (when not saved).
 struct BwdWs {
-    size_t b8, gh, h, cs_a, cs_b, xm, bits, total;
+    size_t b8, gh, h, cs_a, cs_b, xm, bits, partial, partial_bytes, total;
 };
 static BwdWs bwd_ws(const lora_dims* d, bool dropout = false) {
     BwdWs w;
@@ -194,6 +199,9 @@ static BwdWs bwd_ws(const lora_dims* d, bool dropout = false) {
     if (dropout) off += align256(size_t(T) * size_t(d->d_in) * 2);
     w.bits = off;                                                    // dropout: keep bits [T, ceil(n/32)]
     if (dropout) off += align256(size_t(T) * size_t((d->d_in + 31) / 32) * 4);
+    w.partial = off;                                                 // stream-K partials of the dX kernel
+    w.partial_bytes = fused_gemm_partial_bytes(T, d->d_in);
+    off += align256(w.partial_bytes);
     w.total = off;
     return w;
 }
@@ -279,6 +287,7 @@ lora_status fwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
     p.cs_gh = p.cs_h = nullptr;
     p.h_split_src = nullptr;
     p.t_pad = 0;
+    p.sk_partial = W.partial_bytes ? reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + W.partial) : nullptr;
     if (drop && drop->thr > 0) {
         // LoRA dropout: K0 computes h = q (M . x) A^T; K1 takes it instead of its in-MMA x A^T
         float* hd = h_out ? h_out : reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + W.h);
@@ -612,6 +621,7 @@ lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
         p.drop_bits = dropping ? reinterpret_cast<const uint32_t*>(wsb + W.bits) : nullptr;
         // the gh tile also writes K3's split coefficients (gh; h when it already exists)
         p.t_pad = t_pad_of(T);
+        p.sk_partial = W.partial_bytes ? reinterpret_cast<float*>(wsb + W.partial) : nullptr;
         p.cs_gh = da ? reinterpret_cast<__nv_bfloat16*>(wsb + W.cs_a) : nullptr;
         p.h_split_src = h_saved ? h_saved : (dropping && need_h ? hbuf : nullptr);
         p.cs_h = db && p.h_split_src ? reinterpret_cast<__nv_bfloat16*>(wsb + W.cs_b) : nullptr;

@@ -46,8 +46,10 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <mutex>
+#include <vector>
 
 #include "lora_kernels.h"
 #include "sm100_ptx.cuh"
@@ -102,6 +104,8 @@ struct GemmCfg {
     static constexpr int STAGES = cmin(LORA_STAGES_CAP, (SMEM_LIMIT - FIXED) / STAGE_BYTES);
     static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + FIXED;
     static_assert(STAGES >= 2, "shared memory budget");
+    // stream-K owners stage a contributor's partial in the idle ring (else: no stream-K)
+    static constexpr bool SK_OK = STAGES * STAGE_BYTES >= kPartialFloatsPerCta * 4;
     static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N");
     static_assert(CG == 1 || (BN > 128 && R_PAD % 16 == 0), "2-CTA split");
     static_assert(MODE == kModeFwd || DX_BN0 + NAR <= NT, "gh columns fit next to the first tile");
@@ -222,6 +226,130 @@ __device__ __forceinline__ TileRef decode_tile(const FusedGemmGroup& grp, int ti
     return t;
 }
 
+#ifdef LORA_PROBE_SK
+__device__ unsigned int g_probe_n;
+__device__ unsigned long long g_probe_buf[4 * 4096];
+#endif
+
+// ---------------------------------------------------------------- schedule
+// One unit of a pair's work: k-blocks [kb0, kb1) of tile (g, t_blk, n_blk).
+enum : int { kUnitFull = 0, kUnitOwner = 1, kUnitPart = 2 };
+struct Unit {
+    int g, t_blk, n_blk, kb0, kb1, kbt, role;
+    int64_t a;   // stream-K: cost offset of the tile on the body line
+    int w;       // stream-K: cost of one k-block of the tile (width / 128)
+};
+
+template <int MODE, int CG>
+struct Sched {
+    // tail tile i -> unit skeleton (tile coordinates, cost line offset, cost per k-block)
+    __device__ static Unit tail_unit(const FusedGemmGroup& grp, int i) {
+        const TileRef tr = decode_tile<BM * CG>(grp, grp.sk.D + i);
+        Unit u;
+        u.g = tr.g; u.t_blk = tr.t_blk; u.n_blk = tr.n_blk; u.kbt = tr.num_k_blks;
+        u.a = grp.sk.prefix[i];
+        u.w = (grp.sk.prefix[i + 1] - grp.sk.prefix[i]) / tr.num_k_blks;
+        u.kb0 = u.kb1 = 0;
+        u.role = kUnitFull;
+        return u;
+    }
+    // the tail tile containing cost offset x (binary search on the prefix)
+    __device__ static int tail_find(const StreamKSched& sk, int x) {
+        int lo = 0, hi = sk.ntail - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (sk.prefix[mid] <= x) lo = mid; else hi = mid - 1;
+        }
+        return lo;
+    }
+    // k-block range of tail tile `u` that pair q holds
+    __device__ static void seg(const StreamKSched& sk, const Unit& u, int q, int* kb0, int* kb1) {
+        const int64_t lo = sk.S[q] > u.a ? sk.S[q] - u.a : 0;
+        const int64_t hi = static_cast<int64_t>(sk.S[q + 1]) - u.a;
+        int b = static_cast<int>((lo + u.w - 1) / u.w);
+        int e = hi <= 0 ? 0 : static_cast<int>((hi + u.w - 1) / u.w);
+        *kb0 = b < u.kbt ? b : u.kbt;
+        *kb1 = e < u.kbt ? e : u.kbt;
+    }
+};
+
+// Iterates pair q's units; every warp role walks the same sequence.  Order:
+// its dx gh tiles, then its split-off tail segment (a partial for another
+// pair: short, never waits, and its fp32 drain hides under the next mainloop),
+// then its other data-parallel tiles, then the rest of its tail range (which
+// ends with the segment it owns, if any).
+template <int MODE, int CG, int BN>
+struct UnitIter {
+    using SC = Sched<MODE, CG>;
+    const FusedGemmGroup& grp;
+    int q, npairs, jA, jB, phase;
+    int x;                 // stream-K tail cursor
+    __device__ UnitIter(const FusedGemmGroup& gr, int pair, int np)
+        : grp(gr), q(pair), npairs(np), jA(pair), jB(pair), phase(0) {
+        x = grp.sk.enabled ? grp.sk.S[pair] : 0;
+    }
+    __device__ void dp_unit(Unit& u, int tile) {
+        const TileRef tr = decode_tile<BM * CG>(grp, tile);
+        u.g = tr.g; u.t_blk = tr.t_blk; u.n_blk = tr.n_blk;
+        u.kb0 = 0; u.kb1 = u.kbt = tr.num_k_blks; u.role = kUnitFull; u.a = 0; u.w = 0;
+    }
+    // first non-empty tail unit at or after x (does not advance x)
+    __device__ bool tail_peek(Unit& u, int& x_next) {
+        int xx = x;
+        while (xx < grp.sk.S[q + 1]) {
+            const int i = SC::tail_find(grp.sk, xx);
+            u = SC::tail_unit(grp, i);
+            SC::seg(grp.sk, u, q, &u.kb0, &u.kb1);
+            xx = grp.sk.prefix[i + 1];
+            if (u.kb1 <= u.kb0) continue;
+            u.role = u.kb0 > 0 ? kUnitPart : (u.kb1 < u.kbt ? kUnitOwner : kUnitFull);
+            x_next = xx;
+            return true;
+        }
+        x_next = xx;
+        return false;
+    }
+    __device__ bool next(Unit& u) {
+        if (!grp.sk.enabled) {
+            if (jB >= grp.tile_start[grp.count]) return false;
+            dp_unit(u, jB);
+            jB += npairs;
+            return true;
+        }
+        const int D = grp.sk.D;
+        if (phase == 0) {   // gh tiles (dx) of the data-parallel part
+            while (MODE != kModeFwd && jA < D) {
+                const int t = jA;
+                jA += npairs;
+                dp_unit(u, t);
+                if (u.n_blk == 0) return true;
+            }
+            phase = 1;
+        }
+        if (phase == 1) {   // the split-off segment of the tail, first
+            phase = 2;
+            int xn;
+            if (tail_peek(u, xn) && u.role == kUnitPart) {
+                x = xn;
+                return true;
+            }
+        }
+        if (phase == 2) {   // the other data-parallel tiles
+            while (jB < D) {
+                const int t = jB;
+                jB += npairs;
+                dp_unit(u, t);
+                if (MODE == kModeFwd || u.n_blk != 0) return true;
+            }
+            phase = 3;
+        }
+        int xn;
+        if (!tail_peek(u, xn)) return false;
+        x = xn;
+        return true;
+    }
+};
+
 // Maps per problem g (grp.maps[g]):
 //   act  x or dY [T, K]          w   W0 [m, n] (fwd CG=2: 128-row box)
 //   w2   fwd CG=2: W0 box of BN-128 rows
@@ -251,13 +379,13 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
     uint64_t* sh_full = tail_done + 1;             // CG = 2: peer's s_h tile written
     uint64_t* tailop2_full = sh_full + 1;          // dx dropout mode: second A-tile buffer
     uint64_t* tailop2_empty = tailop2_full + 1;
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tailop2_empty + 1);
+    uint64_t* part_full = tailop2_empty + 1;       // stream-K owner: first contributor's partial in the ring
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(part_full + 1);
 
     const uint32_t crank = (CG == 2) ? cluster_ctarank() : 0;
     const bool leader = crank == 0;
     const int pair = static_cast<int>(blockIdx.x) / CG;
     const int npairs = static_cast<int>(gridDim.x) / CG;
-    const int num_tiles = grp.tile_start[grp.count];
     const uint32_t warp = warp_id();
     const uint32_t lane = lane_id();
 
@@ -284,6 +412,7 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
         mbar_init(tailop2_empty, 1);
         mbar_init(tail_done, 1);
         mbar_init(sh_full, 1);
+        mbar_init(part_full, 1);
         fence_mbar_init();
     }
     if (warp == 2) tmem_alloc_cg<CG>(tmem_holder);
@@ -296,32 +425,33 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
     // no global memory is touched before the previous grid has completed.
     griddep_wait();
     if (threadIdx.x == 0) griddep_launch_dependents();
-#ifdef LORA_PROBE_CLOCK
+#if defined(LORA_PROBE_CLOCK) || defined(LORA_PROBE_SK)
     const long long probe_c0 = clock64();
     const uint64_t probe_t0 = globaltimer_ns();
+    (void)probe_c0;
 #endif
 
     if (warp == 0) {
         // ===================== TMA producer (both CTAs) =====================
         if (elect_one()) {
             const uint64_t pol_w = l2_policy_evict_last();
-            uint32_t stage = 0, phase = 0, tl = 0;
-            for (int tile = pair; tile < num_tiles; tile += npairs, ++tl) {
-                const TileRef tr = decode_tile<TM>(grp, tile);
-                const FusedGemmMaps& mp = grp.maps[tr.g];
-                const int n_blk = tr.n_blk;
-                const int t_blk = tr.t_blk;
-                const int num_k_blks = tr.num_k_blks;
+            uint32_t stage = 0, phase = 0, tl = 0, tt = 0;
+            UnitIter<MODE, CG, BN> it(grp, pair, npairs);
+            Unit un;
+            for (; it.next(un); ++tl) {
+                const FusedGemmMaps& mp = grp.maps[un.g];
+                const int n_blk = un.n_blk;
+                const int t_blk = un.t_blk;
                 const int t0 = t_blk * TM + static_cast<int>(crank) * BM;
                 const int n0 = Cols::start(n_blk);
-                const int wh = Cols::width(n_blk, grp.p[tr.g].N_out) / CG;   // this CTA's B-operand columns
+                const int wh = Cols::width(n_blk, grp.p[un.g].N_out) / CG;   // this CTA's B-operand columns
                 const int nh0 = n0 + static_cast<int>(crank) * wh;
                 const int nb = (wh + 63) / 64;                          // dx: 64-column W0 / A blocks
                 const bool gh_tile = (MODE != kModeFwd) && n_blk == 0;
                 const uint32_t stage_tx = (MODE == kModeFwd)
                     ? static_cast<uint32_t>(C::STAGE_BYTES)
                     : static_cast<uint32_t>(C::A_BYTES + nb * 64 * BK * 2 + (gh_tile ? C::NAR_BYTES : 0));
-                for (int kb = 0; kb < num_k_blks; ++kb) {
+                for (int kb = un.kb0; kb < un.kb1; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     uint8_t* sA = stage_base + stage * C::STAGE_BYTES;
                     uint8_t* sB = sA + C::A_BYTES;
@@ -355,18 +485,20 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
                     }
                     if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
                 }
-                // tail operand for this tile: fwd B rows; dx A columns (this CTA's half)
-                if constexpr (MODE != kModeDxDrop) mbar_wait(tailop_empty, (tl & 1) ^ 1);
+                // tail operand for this tile: fwd B rows; dx A columns (this CTA's half).
+                // Stream-K partial segments have no tail (the owner adds the LoRA term).
+                if (un.role == kUnitPart) continue;
+                if constexpr (MODE != kModeDxDrop) mbar_wait(tailop_empty, (tt & 1) ^ 1);
                 if constexpr (MODE == kModeFwd) {
                     if (leader) mbar_arrive_expect_tx(tailop_full, CG * C::TAILB_BYTES);
                     tma_load<CG>(s_tailb, &mp.tail, 0, nh0, tailop_full);
                 } else if constexpr (MODE == kModeDxDrop) {
                     // every CTA: A columns of the whole tile width, on its own barrier, into
-                    // buffer tl & 1 (the epilogue holds a buffer for its whole drain)
-                    uint64_t* tf = (tl & 1) ? tailop2_full : tailop_full;
-                    mbar_wait((tl & 1) ? tailop2_empty : tailop_empty, ((tl >> 1) & 1) ^ 1);
-                    uint8_t* tb = s_tailb + (tl & 1) * round_up(C::TAILB_BYTES, 1024);
-                    const int nbf = (Cols::width(n_blk, grp.p[tr.g].N_out) + 63) / 64;
+                    // buffer tt & 1 (the epilogue holds a buffer for its whole drain)
+                    uint64_t* tf = (tt & 1) ? tailop2_full : tailop_full;
+                    mbar_wait((tt & 1) ? tailop2_empty : tailop_empty, ((tt >> 1) & 1) ^ 1);
+                    uint8_t* tb = s_tailb + (tt & 1) * round_up(C::TAILB_BYTES, 1024);
+                    const int nbf = (Cols::width(n_blk, grp.p[un.g].N_out) + 63) / 64;
                     mbar_arrive_expect_tx(tf, nbf * R_PAD * 128);
                     for (int j = 0; j < nbf; ++j)
                         tma_load_2d(tb + j * (R_PAD * 128), &mp.tail, n0 + 64 * j, 0, tf);
@@ -375,6 +507,7 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
                     for (int j = 0; j < nb; ++j)
                         tma_load<CG>(s_tailb + j * (R_PAD * 128), &mp.tail, nh0 + 64 * j, 0, tailop_full);
                 }
+                ++tt;
             }
         }
     } else if (warp == 1) {
@@ -383,27 +516,27 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
             constexpr uint32_t idesc_fwd = make_idesc_bf16(TM, NT, 0, 0);
             constexpr uint32_t idesc_nar = make_idesc_bf16(TM, C::NAR > 0 ? C::NAR : 16, 0, 1);
             uint32_t stage = 0, phase = 0, tl = 0;
-            for (int tile = pair; tile < num_tiles; tile += npairs, ++tl) {
-                const TileRef tr = decode_tile<TM>(grp, tile);
-                const int n_blk = tr.n_blk;
-                const int num_k_blks = tr.num_k_blks;
+            UnitIter<MODE, CG, BN> it(grp, pair, npairs);
+            Unit un;
+            for (; it.next(un); ++tl) {
+                const int n_blk = un.n_blk;
                 const bool gh_tile = (MODE != kModeFwd) && n_blk == 0;
                 const uint32_t idesc_main = (MODE == kModeFwd)
                     ? idesc_fwd
-                    : make_idesc_bf16(TM, static_cast<uint32_t>(Cols::width(n_blk, grp.p[tr.g].N_out)), 0, 1);
+                    : make_idesc_bf16(TM, static_cast<uint32_t>(Cols::width(n_blk, grp.p[un.g].N_out)), 0, 1);
                 const uint32_t acc = tl & 1;
                 const uint32_t acc_phase = (tl >> 1) & 1;
                 mbar_wait<CG == 2>(&tmem_empty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * NT;
-                for (int kb = 0; kb < num_k_blks; ++kb) {
+                for (int kb = un.kb0; kb < un.kb1; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
                     const uint32_t a_addr = smem_u32(stage_base + stage * C::STAGE_BYTES);
                     const uint32_t b_addr = a_addr + C::A_BYTES;
 #pragma unroll
                     for (int kk = 0; kk < BK / UMMA_K; ++kk) {
-                        const uint32_t accum = (kb | kk) != 0;
+                        const uint32_t accum = (kb != un.kb0 || kk != 0) ? 1u : 0u;
                         const uint64_t a_desc = make_smem_desc(a_addr + kk * 32, 16, 1024, kLayoutSW128);
                         if constexpr (MODE == kModeFwd) {
                             // [W0 rows ; A rows] as one K-major N = 256 operand
@@ -436,12 +569,13 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
         const uint32_t row_local = quarter * 32 + lane;
         constexpr uint32_t idesc_tail_fwd = make_idesc_bf16(TM, BN, 0, 0);
         constexpr uint32_t tail_sbo = 8 * C::TAIL_ROW;
-        uint32_t tl = 0;
-        for (int tile = pair; tile < num_tiles; tile += npairs, ++tl) {
-            const TileRef tr = decode_tile<TM>(grp, tile);
-            const FusedGemmParams& p = grp.p[tr.g];
-            const int n_blk = tr.n_blk;
-            const int t_blk = tr.t_blk;
+        uint32_t tl = 0, tt = 0;
+        UnitIter<MODE, CG, BN> it(grp, pair, npairs);
+        Unit un;
+        for (; it.next(un); ++tl) {
+            const FusedGemmParams& p = grp.p[un.g];
+            const int n_blk = un.n_blk;
+            const int t_blk = un.t_blk;
             const int64_t row = static_cast<int64_t>(t_blk) * TM + crank * BM + row_local;
             const int n0 = Cols::start(n_blk);
             const int width = Cols::width(n_blk, p.N_out);
@@ -450,8 +584,115 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
             const uint32_t acc_phase = (tl >> 1) & 1;
             mbar_wait(&tmem_full[acc], acc_phase);
             tc_fence_after();
+#ifdef LORA_PROBE_SK
+            const uint64_t probe_u0 = globaltimer_ns();
+#endif
             const uint32_t tbase = tmem_base + ((quarter * 32) << 16) + acc * NT;
-
+            // stream-K partial slots: [chunk of 16 columns][128 rows][16] fp32 per CTA
+            constexpr int ACC_COLS = NT;   // fwd: BN output + r_pad h columns
+            auto slot_of = [&](int q) {
+                return grp.sk.partial + static_cast<int64_t>(q * CG + static_cast<int>(crank)) * kPartialFloatsPerCta;
+            };
+            if (un.role == kUnitPart) {
+                // (P) a split-off segment: raw fp32 accumulator -> this pair's slot, then publish
+                float* slot = slot_of(pair);
+                const int ncol = (MODE == kModeFwd) ? ACC_COLS : width;
+#pragma unroll 1
+                for (int c = 0; c < ncol / 16; ++c) {
+                    uint32_t v[16];
+                    tmem_ld_32x32b_x16(tbase + 16 * c, v);
+                    tmem_ld_wait();
+                    // [chunk][4 float4 groups][128 rows] float4: a warp stores 512 contiguous bytes
+                    float4* dst = reinterpret_cast<float4*>(slot) + static_cast<int64_t>(c) * 512 + row_local;
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        dst[e * 128] = make_float4(__uint_as_float(v[4 * e]), __uint_as_float(v[4 * e + 1]),
+                                                   __uint_as_float(v[4 * e + 2]), __uint_as_float(v[4 * e + 3]));
+                }
+                tc_fence_before();
+                __threadfence();
+                named_bar_sync(1, 128);
+                if (ew == 0 && lane == 0) st_release_u64(grp.sk.pflags + pair * CG + crank, 1ull);
+#ifdef LORA_PROBE_SK
+                if (ew == 0 && lane == 0 && crank == 0) {
+                    const unsigned i = atomicAdd(&g_probe_n, 1u);
+                    if (i < 4096) {
+                        unsigned long long* r = g_probe_buf + 4 * i;
+                        r[0] = (static_cast<unsigned long long>(pair) << 32) | (tl << 8) | static_cast<unsigned>(un.role);
+                        r[1] = (static_cast<unsigned long long>(un.kb0) << 32) | static_cast<unsigned>(un.kb1);
+                        r[2] = probe_u0 - probe_t0;
+                        r[3] = globaltimer_ns() - probe_t0;
+                    }
+                }
+#endif
+                __syncwarp();
+                if (lane == 0) {
+                    if (CG == 1) mbar_arrive(&tmem_empty[acc]);
+                    else mbar_arrive_cluster(&tmem_empty[acc], 0);
+                }
+                continue;
+            }
+            // owner of a split tile: the pairs after this one hold its other k-blocks.  Its
+            // segment is this pair's LAST unit, so the stage ring is idle: each contributor's
+            // partial in turn is bulk-copied into it and added into the TMEM accumulator
+            // (tcgen05.ld / st), in pair order, before anything reads the accumulator.
+            if (un.role == kUnitOwner) {
+                int cq[4];
+                int ncq = 0;
+                const int64_t b_end = un.a + static_cast<int64_t>(un.kbt) * un.w;
+                for (int q = pair + 1; q < npairs && grp.sk.S[q] < b_end; ++q) {
+                    int k0, k1;
+                    Sched<MODE, CG>::seg(grp.sk, un, q, &k0, &k1);
+                    if (k1 <= k0) continue;
+                    if (ncq == 4) __trap();   // planner bound: a tail tile spans at most 5 pairs
+                    cq[ncq++] = q;
+                }
+                const int ncol = (MODE == kModeFwd) ? ACC_COLS : width;
+                for (int i = 0; i < ncq; ++i) {
+                    if (ew == 0 && lane == 0) {
+                        uint64_t* f = grp.sk.pflags + cq[i] * CG + crank;
+                        const uint64_t t_start = globaltimer_ns();
+                        while (ld_acquire_u64(f) != 1ull) {
+                            __nanosleep(64);
+                            if (globaltimer_ns() - t_start > 4000000000ull) {
+                                printf("lora fused GEMM: stream-K partial wait timed out (pair %d <- %d)\n", pair,
+                                       cq[i]);
+                                __trap();
+                            }
+                        }
+                        *f = 0;   // consumed (self-cleaning)
+                        fence_proxy_async_global();
+                        fence_proxy_async_smem();   // our earlier generic reads of the ring come first
+                        const uint32_t bytes = static_cast<uint32_t>(ncol * 512);
+                        mbar_arrive_expect_tx(part_full, bytes);
+                        const float* src = slot_of(cq[i]);
+                        for (uint32_t off = 0; off < bytes; off += 32768u)
+                            bulk_load_1d(stage_base + off, src + off / 4, bytes - off < 32768u ? bytes - off : 32768u,
+                                         part_full);
+                    }
+                    mbar_wait(part_full, static_cast<uint32_t>(i & 1));
+                    const float4* s4 = reinterpret_cast<const float4*>(stage_base) + row_local;
+#pragma unroll 1
+                    for (int c = 0; c < ncol / 16; ++c) {
+                        uint32_t v[16];
+                        tmem_ld_32x32b_x16(tbase + 16 * c, v);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const float4 t4 = s4[(c * 4 + e) * 128];
+                            v[4 * e] = __float_as_uint(__uint_as_float(v[4 * e]) + t4.x);
+                            v[4 * e + 1] = __float_as_uint(__uint_as_float(v[4 * e + 1]) + t4.y);
+                            v[4 * e + 2] = __float_as_uint(__uint_as_float(v[4 * e + 2]) + t4.z);
+                            v[4 * e + 3] = __float_as_uint(__uint_as_float(v[4 * e + 3]) + t4.w);
+                        }
+                        tmem_st_32x32b_x16(tbase + 16 * c, v);
+                    }
+                    tmem_st_wait();
+                    tc_fence_before();
+                    named_bar_sync(1, 128);   // ring free for the next contributor; TMEM updated
+                    tc_fence_after();
+                }
+            }
             // (1) the r_pad low-rank values of this row
             float hv[R_PAD];
             if (MODE == kModeFwd && p.h_in != nullptr) {
@@ -530,7 +771,7 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
             }
             if constexpr (MODE == kModeDxDrop) {
                 // dropout: no tail MMA -- the epilogue adds q M . (gh A) itself (step 5)
-                mbar_wait((tl & 1) ? tailop2_full : tailop_full, (tl >> 1) & 1);
+                mbar_wait((tt & 1) ? tailop2_full : tailop_full, (tt >> 1) & 1);
             } else {
             // (3) bf16(s h) / bf16(gh) -> swizzled K-major smem tile (tail MMA A operand)
             const float op_scale = (MODE == kModeFwd) ? p.scale : 1.0f;
@@ -550,8 +791,8 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
                 if (CG == 2 && !leader) {
                     mbar_arrive_cluster(sh_full, 0);      // our half of s_h is ready
                 } else {
-                    if (CG == 2) mbar_wait<true>(sh_full, tl & 1);
-                    mbar_wait(tailop_full, tl & 1);
+                    if (CG == 2) mbar_wait<true>(sh_full, tt & 1);
+                    mbar_wait(tailop_full, tt & 1);
                     tc_fence_after();
                     const uint32_t h_addr = smem_u32(s_h);
                     const uint32_t t_addr = smem_u32(s_tailb);
@@ -575,7 +816,7 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
                     commit<CG>(tail_done);
                 }
             }
-            mbar_wait(tail_done, tl & 1);
+            mbar_wait(tail_done, tt & 1);
             tc_fence_after();
             if (ew == 0 && lane == 0) mbar_arrive(tailop_empty);
             }
@@ -614,7 +855,7 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
                     if constexpr (MODE == kModeDxDrop) {
                         // f += q M . (gh A): A columns of this chunk from the MN-major SW128 tile
                         const int lc = 16 * c;
-                        const uint8_t* blk = s_tailb + (tl & 1) * round_up(C::TAILB_BYTES, 1024) +
+                        const uint8_t* blk = s_tailb + (tt & 1) * round_up(C::TAILB_BYTES, 1024) +
                                              (lc / 64) * (R_PAD * 128);
                         const uint32_t ch = static_cast<uint32_t>((lc % 64) / 8);
                         float lo[16];
@@ -650,8 +891,21 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
             }
             if constexpr (MODE == kModeDxDrop) {
                 named_bar_sync(1, 128);   // every epilogue warp is done with the A tile
-                if (ew == 0 && lane == 0) mbar_arrive((tl & 1) ? tailop2_empty : tailop_empty);
+                if (ew == 0 && lane == 0) mbar_arrive((tt & 1) ? tailop2_empty : tailop_empty);
             }
+            ++tt;
+#ifdef LORA_PROBE_SK
+            if (ew == 0 && lane == 0 && crank == 0) {
+                const unsigned i = atomicAdd(&g_probe_n, 1u);
+                if (i < 4096) {
+                    unsigned long long* r = g_probe_buf + 4 * i;
+                    r[0] = (static_cast<unsigned long long>(pair) << 32) | (tl << 8) | static_cast<unsigned>(un.role);
+                    r[1] = (static_cast<unsigned long long>(un.kb0) << 32) | static_cast<unsigned>(un.kb1);
+                    r[2] = probe_u0 - probe_t0;
+                    r[3] = globaltimer_ns() - probe_t0;
+                }
+            }
+#endif
             tc_fence_before();
             __syncwarp();
             if (lane == 0) {
@@ -722,12 +976,107 @@ unsigned long long* sync_pool_alloc(int words, cudaStream_t stream) {
 // ----------------------------------------------------------------------------
 // host side
 // ----------------------------------------------------------------------------
+
 static int64_t col_tiles_host(int mode, int r_pad, int64_t n_out) {
     if (mode == kModeFwd) {
         const int bn = NT - r_pad;
         return (n_out + bn - 1) / bn;
     }
     return n_out <= DX_BN0 ? 1 : 1 + (n_out - DX_BN0 + NT - 1) / NT;
+}
+
+// The stream-K tail is opt-in (LORA_STREAMK=1, read per call): measured on B200
+// it does not beat the data-parallel schedule ("K1/K2 schedule"),
+// because every split exposes one more fused epilogue (5-10 us for a dX tile)
+// that the two TMEM accumulators otherwise hide under the next mainloop.
+static bool streamk_enabled() {
+    const char* v = getenv("LORA_STREAMK");
+    return v && v[0] == '1';
+}
+
+size_t fused_gemm_partial_bytes(int64_t T, int64_t N_out) {
+    // worth a stream-K schedule only when the launch has at least a wave of tiles
+    if (!streamk_enabled()) return 0;
+    const int64_t tiles = ((T + 255) / 256) * ((N_out + 255) / 256);
+    return tiles >= 32 ? size_t(kMaxPairs) * kPartialFloatsPerCta * sizeof(float) : 0;
+}
+
+// Host side of the schedule (lora_kernels.h, StreamKSched).
+template <int MODE, int R_PAD, int CG>
+static cudaError_t plan_stream_k(FusedGemmGroup& grp, int npairs, cudaStream_t stream) {
+    using C = GemmCfg<MODE, R_PAD, CG>;
+    StreamKSched& sk = grp.sk;
+    sk.enabled = 0;
+    sk.partial = grp.p[0].sk_partial;
+    sk.pflags = nullptr;
+    const int W = grp.tile_start[grp.count];
+    if (!C::SK_OK || !streamk_enabled() || sk.partial == nullptr || npairs < 2 || npairs > kMaxPairs || W <= npairs)
+        return cudaSuccess;
+    const int TM = BM * CG;
+    // per-tile cost in tile order (decode_tile): k-blocks x width / 128 (fwd: always N = 256)
+    std::vector<int> cost(W), is_gh(W, 0);
+    for (int g = 0; g < grp.count; ++g) {
+        const FusedGemmParams& p = grp.p[g];
+        const int ntb = static_cast<int>((p.T + TM - 1) / TM), kb = static_cast<int>((p.K + BK - 1) / BK);
+        const int nc = static_cast<int>(col_tiles_host(MODE, R_PAD, p.N_out));
+        for (int nb = 0; nb < nc; ++nb) {
+            int w = 2;
+            if (MODE != kModeFwd) {
+                const int64_t start = nb == 0 ? 0 : DX_BN0 + int64_t(nb - 1) * C::BN;
+                const int64_t width = nb == 0 ? DX_BN0 : std::min<int64_t>(C::BN, (p.N_out - start + 127) / 128 * 128);
+                w = static_cast<int>(width / 128);
+            }
+            for (int t = 0; t < ntb; ++t) {
+                cost[grp.tile_start[g] + nb * ntb + t] = kb * w;
+                is_gh[grp.tile_start[g] + nb * ntb + t] = MODE != kModeFwd && nb == 0;
+            }
+        }
+    }
+    // the tail = the last partial round of the data-parallel order
+    int D = W - W % npairs;
+    if (D == W) D = W - npairs;   // full rounds only: split the last one if loads are uneven
+    for (int i = D; i < W; ++i)
+        if (is_gh[i]) return cudaSuccess;   // a gh tile must not be split: keep data-parallel
+    std::vector<int64_t> load(npairs, 0);
+    for (int i = 0; i < D; ++i) load[i % npairs] += cost[i];
+    std::vector<int64_t> dp = load;
+    for (int i = D; i < W; ++i) dp[i % npairs] += cost[i];
+    int64_t tail = 0;
+    for (int i = D; i < W; ++i) tail += cost[i];
+    // smallest common finish time that absorbs the tail
+    int64_t lo = *std::max_element(load.begin(), load.end()), hi = lo + tail;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) / 2;
+        int64_t cap = 0;
+        for (int q = 0; q < npairs; ++q) cap += mid > load[q] ? mid - load[q] : 0;
+        if (cap >= tail) hi = mid; else lo = mid + 1;
+    }
+    const int64_t finish = lo;
+    const int64_t dp_finish = *std::max_element(dp.begin(), dp.end());
+    if (finish * 100 > dp_finish * 97) return cudaSuccess;   // < 3% to gain: keep data-parallel
+    if (tail > (1 << 30)) return cudaSuccess;
+    sk.D = D;
+    sk.ntail = W - D;
+    sk.prefix[0] = 0;
+    for (int i = 0; i < sk.ntail; ++i) sk.prefix[i + 1] = sk.prefix[i] + cost[D + i];
+    sk.S[0] = 0;
+    for (int q = 0; q < npairs; ++q) {
+        const int64_t b = finish > load[q] ? finish - load[q] : 0;
+        sk.S[q + 1] = static_cast<int>(std::min<int64_t>(tail, sk.S[q] + b));
+    }
+    sk.S[npairs] = static_cast<int>(tail);
+    // the kernel's owner handles at most 4 contributors per split tile
+    for (int i = 0; i < sk.ntail; ++i) {
+        const int64_t a = sk.prefix[i], b = sk.prefix[i + 1];
+        int holders = 0;
+        for (int q = 0; q < npairs; ++q)
+            if (sk.S[q] < b && sk.S[q + 1] > a) ++holders;
+        if (holders > 5) return cudaSuccess;   // (S stays unused: sk.enabled == 0)
+    }
+    sk.pflags = reinterpret_cast<uint64_t*>(sync_pool_alloc(npairs * CG, stream));
+    if (sk.pflags == nullptr) return cudaErrorMemoryAllocation;
+    sk.enabled = 1;
+    return cudaSuccess;
 }
 
 template <int MODE, int R_PAD, int CG>
@@ -754,6 +1103,7 @@ static cudaError_t launch_impl(FusedGemmGroup& grp, int num_sms, cudaStream_t st
     const int64_t units = num_sms / CG;
     const int grid = static_cast<int>((tiles < units ? tiles : units) * CG);
     if (grid <= 0) return cudaSuccess;
+    if ((e = plan_stream_k<MODE, R_PAD, CG>(grp, grid / CG, stream)) != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(NUM_THREADS);
@@ -833,3 +1183,17 @@ cudaError_t launch_fused_gemm(int mode, int r_pad, int cta_group, const FusedGem
 }
 
 }  // namespace lora_sm100
+
+#ifdef LORA_PROBE_SK
+// experiment only: copy and reset the unit timeline (pair<<32 | unit<<8 | role, kb0<<32 | kb1, t_mma_done, t_end)
+extern "C" int lora_probe_sk_dump(unsigned long long* host, int max_rows) {
+    unsigned n = 0;
+    cudaMemcpyFromSymbol(&n, lora_sm100::g_probe_n, sizeof(n));
+    if (n > 4096) n = 4096;
+    if (static_cast<int>(n) > max_rows) n = max_rows;
+    cudaMemcpyFromSymbol(host, lora_sm100::g_probe_buf, n * 4 * sizeof(unsigned long long));
+    const unsigned z = 0;
+    cudaMemcpyToSymbol(lora_sm100::g_probe_n, &z, sizeof(z));
+    return static_cast<int>(n);
+}
+#endif

@@ -45,10 +45,37 @@ struct FusedGemmParams {
     __nv_bfloat16* cs_h;
     const float* h_split_src;
     int64_t t_pad;
+    float* sk_partial;            // stream-K partial slots in this problem's workspace (group: p[0]'s), or null
 };
 
 struct FusedGemmMaps {
     CUtensorMap act, w, w2, nar, tail;
+};
+
+// Schedule of a fused-GEMM launch.  Tiles in
+// tile order [0, D) run data-parallel (pair q takes q, q + P, ...): the pairs
+// move through the W0 column blocks in lock-step rounds, so concurrent tiles
+// share their x / W0 k-blocks in L2.  The last partial round [D, W) would
+// leave pairs idle; its work is split over ALL pairs ("stream-K tail"): cost
+// units = one 64-deep k-block of a 128-column slab (a 256-wide tile k-block
+// costs 2), tail tile i occupies [prefix[i], prefix[i+1]) of one cost line,
+// and pair q takes [S[q], S[q+1]), sized so every pair's total is equal.  A
+// tile cut by a range boundary is finished by the pair holding its k-block 0
+// (the owner); the pairs holding the rest write fp32 partial accumulators to
+// `partial` (one slot per CTA: only a pair's first tail segment can start
+// mid-tile) and raise pflags; the owner adds them in pair order --
+// deterministic for a given launch shape.  dx gh tiles (column tile 0) are
+// never in the tail.
+constexpr int kMaxPairs = 148;
+constexpr int kPartialFloatsPerCta = 128 * 256;   // one CTA's 128 x 256 fp32 accumulator
+struct StreamKSched {
+    int enabled;                   // 0: data-parallel over all tiles
+    int D;                         // first tail tile
+    int ntail;                     // tail tiles (<= kMaxPairs)
+    int prefix[kMaxPairs + 1];     // tail cost prefix
+    int S[kMaxPairs + 1];          // tail cost range of pair q
+    float* partial;                // [P * CTAs per pair][kPartialFloatsPerCta] (caller workspace)
+    uint64_t* pflags;              // [P * CTAs per pair] sync pool: 1 = slot written; the owner zeroes it
 };
 
 // A group of independent LoRA linears (same rank bucket) processed by ONE
@@ -60,7 +87,10 @@ struct FusedGemmGroup {
     int tile_start[kMaxGroup + 1];
     int count;
     unsigned long long* done;     // dx: sync-pool launch counter (last CTA out resets flags), or null
+    StreamKSched sk;              // filled in by the launcher
 };
+// bytes of stream-K partial workspace a fused-GEMM launch may use (0: none)
+size_t fused_gemm_partial_bytes(int64_t T, int64_t N_out);
 
 // Device-side synchronisation words (K2's gh flags, launch done-counters): a
 // static __device__ pool, zero when the module loads.  Every protocol that

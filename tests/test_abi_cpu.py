@@ -2,6 +2,7 @@
 include/lora.h declares, and validates its arguments synchronously (returning
 the documented status before any CUDA call).  No compute is invoked here."""
 import ctypes
+import os
 
 import pytest
 
@@ -86,6 +87,16 @@ def test_workspace_sizes_scale_with_shape():
     f = L.lora_linear_fwd_workspace_bytes
     assert f(L.dims(2048, 4096, 4096, 8, 16.0)) >= 4096 * 8 * 2       # B8 [m, roundup(r, 8)]
     assert f(L.dims(2048, 4096, 4096, 8, 16.0)) == f(L.dims(7, 4096, 4096, 8, 16.0))
+    # opt-in stream-K schedule (LORA_STREAMK=1): launches with >= 32 tiles also get one
+    # fp32 128 x 256 partial accumulator slot per CTA of the 148-SM grid
+    slots = 148 * 128 * 256 * 4
+    base = f(L.dims(2048, 4096, 4096, 8, 16.0))
+    os.environ["LORA_STREAMK"] = "1"
+    try:
+        assert f(L.dims(2048, 4096, 4096, 8, 16.0)) == base + slots
+        assert f(L.dims(7, 4096, 4096, 8, 16.0)) == f(L.dims(7, 4096, 4096, 8, 16.0))
+    finally:
+        del os.environ["LORA_STREAMK"]
     b = L.lora_linear_bwd_workspace_bytes
     assert b(L.dims(4096, 4096, 11008, 16, 16.0)) > b(L.dims(2048, 4096, 11008, 16, 16.0))
     assert b(L.dims(128, 60, 64, 4, 16.0)) == 0          # invalid dims -> 0

@@ -464,3 +464,29 @@ def test_graph_replay_new_inputs(oracle_mod, L):
         assert relF(host_f64(got[0][0]), go["dx"]) <= TOL_OUT
         assert relF(host_f64(got[0][1]), go["da"]) <= TOL_GRAD
         assert relF(host_f64(got[0][2]), go["db"]) <= TOL_GRAD
+
+
+@pytest.mark.parametrize("shape", [
+    (2048, 4096, 4096, 8),   # cfg2: K1 144 tiles, K2 136 tiles on 74 CTA pairs
+    (1000, 1032, 2056, 16),  # ragged T, odd column-tile counts, r_pad 16
+    (1536, 2048, 3000, 24),  # r_pad 32, a 128-wide last dX tile
+])
+def test_stream_k_schedule(oracle_mod, L, shape, monkeypatch):
+    """With LORA_STREAMK=1, shapes with more tiles than CTA pairs run the stream-K
+    tail (split tiles finished by their owner from fp32 partials): y, dX match the oracle on
+    sampled rows, dA / dB in full, repeat calls are bitwise equal, and the
+    data-parallel schedule (LORA_STREAMK=0) agrees to fp32 re-association."""
+    T, n, m, r = shape
+    d = make_lora_inputs(T, n, m, r, seed=500 + r)
+    rows = np.sort(np.random.default_rng(5).choice(T, 96, replace=False))
+    monkeypatch.setenv("LORA_STREAMK", "1")   # opt-in schedule
+    out, errs = _check_against_oracle(oracle_mod, L, d, 16.0, rows=rows)
+    again = _run(L, d, 16.0)
+    for k in ("y", "h", "dx", "da", "db"):
+        assert torch.equal(out[k], again[k]), k
+    monkeypatch.setenv("LORA_STREAMK", "0")
+    dp = _run(L, d, 16.0)
+    for k in ("y", "dx"):
+        assert relF(host_f64(out[k]), host_f64(dp[k])) <= 2e-3, k   # bf16 outputs: rounding flips only
+    for k in ("h", "da", "db"):
+        assert relF(host_f64(out[k]), host_f64(dp[k])) <= 1e-5, k
