@@ -234,7 +234,10 @@ def run_ours(args, wl):
         dist.init_process_group("nccl", device_id=dev)
 
     import __graft_entry__
-    __graft_entry__._build_module().build()   # (by path: the package __init__ loads the library)
+    if local_rank == 0:   # one builder per node (no-op when liblora.so is current)
+        __graft_entry__._build_module().build()   # (by path: the package __init__ loads the library)
+    if world > 1:
+        dist.barrier(device_ids=[local_rank])
     import paper_2403_11366_b200 as L
     from paper_2403_11366_b200 import tp
     L.lora_device_check()

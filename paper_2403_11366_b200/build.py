@@ -67,10 +67,10 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None,
     cmd = [nvcc, *ARCH, "-O3", "-std=c++17", "-lineinfo", "-shared", "-Xcompiler", "-fPIC",
            "-Xptxas", "-v" if verbose else "-O3",
            "-I", INCLUDE, "-I", CSRC, "-I", _nccl_include(),
-           "-DLORA_BUILD", *[f"-D{d}" for d in defines], "-o", target + ".tmp",
+           "-DLORA_BUILD", *[f"-D{d}" for d in defines], "-o", f"{target}.tmp{os.getpid()}",
            *[os.path.join(CSRC, f) for f in SOURCES], "-ldl", "-lpthread"]
     subprocess.check_call(cmd)
-    os.replace(target + ".tmp", target)
+    os.replace(f"{target}.tmp{os.getpid()}", target)   # atomic: concurrent builders never see a partial file
     return target
 
 
