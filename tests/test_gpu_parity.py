@@ -490,3 +490,31 @@ def test_stream_k_schedule(oracle_mod, L, shape, monkeypatch):
         assert relF(host_f64(out[k]), host_f64(dp[k])) <= 2e-3, k   # bf16 outputs: rounding flips only
     for k in ("h", "da", "db"):
         assert relF(host_f64(out[k]), host_f64(dp[k])) <= 1e-5, k
+
+
+def test_sync_pool_ring_wraps(oracle_mod, L):
+    """K2's gh flags come from a recycled ring of a static device pool and are
+    zeroed by their last consumer: thousands of eager backward calls (more than
+    the ring holds) keep producing the same bits, with and without K3 reading
+    the flags, and the result still matches the oracle."""
+    T, n, m, r = 384, 256, 512, 8
+    d = make_lora_inputs(T, n, m, r, seed=91)
+    x, w0, a, b, dy = (dev_bf16(d[k]) for k in ("x", "w0", "a", "b", "dy"))
+    y, h = L.lora_linear_fwd(x, w0, a, b, 16.0)
+    ref = L.lora_linear_bwd(x, w0, a, b, dy, 16.0, h_saved=h)
+    ref_dx_only = L.lora_linear_bwd(x, w0, a, b, dy, 16.0, h_saved=h, want_da=False, want_db=False)
+    ws = torch.empty(1 << 22, dtype=torch.uint8, device="cuda")
+    outs = (torch.empty_like(ref[0]), torch.empty_like(ref[1]), torch.empty_like(ref[2]))
+    for i in range(9000):   # 16 pool words per call (flags + a done counter): the 131072-word ring wraps
+        if i % 2:
+            L.lora_linear_bwd(x, w0, a, b, dy, 16.0, h_saved=h, dx=outs[0], da=outs[1], db=outs[2], workspace=ws)
+        else:
+            L.lora_linear_bwd(x, w0, a, b, dy, 16.0, h_saved=h, dx=outs[0], want_da=False, want_db=False,
+                              workspace=ws)
+    torch.cuda.synchronize()
+    for u, v in zip(outs, ref):
+        assert torch.equal(u, v)
+    assert torch.equal(L.lora_linear_bwd(x, w0, a, b, dy, 16.0, h_saved=h, want_da=False, want_db=False)[0],
+                       ref_dx_only[0])
+    go = oracle_mod.lora_bwd(d["x"], d["w0"], d["a"], d["b"], d["dy"], 16.0)
+    assert relF(host_f64(outs[0]), go["dx"]) <= TOL_OUT
