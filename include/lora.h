@@ -18,7 +18,15 @@
  *   - Tensor pointers are DEVICE pointers to row-major, contiguous tensors.
  *     "bf16" tensors hold IEEE bfloat16 values (2 bytes each); fp32 tensors
  *     hold float.  The caller owns all memory; the library never allocates
- *     device memory inside a call (scratch comes from `workspace`).
+ *     device memory inside a call (scratch comes from `workspace`, whose
+ *     contents need no initialisation).  Cross-CTA / cross-kernel flags live
+ *     in a 2 MiB static device pool inside liblora.so (zero at load, returned
+ *     to zero by every launch chain that uses it), so calls may be captured
+ *     into CUDA graphs and replayed with new inputs.
+ *   - *_workspace_bytes() depend only on the dims -- and on the experimental
+ *     environment switch LORA_STREAMK=1 (stream-K tail schedule), which adds
+ *     148 fp32 128x256 partial slots (18.9 MB) for launches of >= 32 tiles:
+ *     query the size in the same environment the calls run in.
  *   - Every device pointer must be 16-byte aligned.  d_in and d_out must be
  *     multiples of 8 (so bf16 rows are 16-byte multiples, as TMA requires);
  *     1 <= rank <= 64; tokens >= 0.  Violations -> LORA_ERR_SHAPE /
