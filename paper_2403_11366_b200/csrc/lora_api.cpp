@@ -920,6 +920,17 @@ lora_status lora_linear_fwd_grouped(int count, const lora_dims* dims, const lora
 
 lora_status lora_linear_bwd_grouped(int count, const lora_dims* dims, const lora_bwd_problem* probs, int accumulate,
                                     void* workspace, size_t workspace_bytes, void* stream) {
+    return lora_host::bwd_grouped_impl(count, dims, probs, accumulate, workspace, workspace_bytes, stream, nullptr,
+                                       nullptr);
+}
+
+}  // extern "C"
+
+namespace lora_host {
+
+lora_status bwd_grouped_impl(int count, const lora_dims* dims, const lora_bwd_problem* probs, int accumulate,
+                             void* workspace, size_t workspace_bytes, void* stream,
+                             lora_status (*after_k2)(void* ctx, int* launches), void* ctx) {
     int launches = 0;
     lora_status st = check_group(count, dims, probs, "lora_linear_bwd_grouped");
     if (st != LORA_OK) return st;
@@ -944,11 +955,21 @@ lora_status lora_linear_bwd_grouped(int count, const lora_dims* dims, const lora
             set_launches(launches);
             return st;
         }
+        // work that needs only the dX kernel's outputs (the TP column group forks its dX
+        // sum and all-reduce here, so they overlap the dA / dB kernel below)
+        if (stage == 1 && after_k2 && (st = after_k2(ctx, &launches)) != LORA_OK) {
+            set_launches(launches);
+            return st;
+        }
     }
     st = launch_collected_k3(col, st_, &launches);
     set_launches(launches);
     return st;
 }
+
+}  // namespace lora_host
+
+extern "C" {
 
 const char* lora_status_string(lora_status s) {
     switch (s) {

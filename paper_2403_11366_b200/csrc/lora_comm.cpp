@@ -75,6 +75,10 @@ struct lora_comm {
     ncclComm_t comm;
     int nranks;
     int rank;
+    // side stream + fork / join events: the column group's dX sum and all-reduce
+    // run there, concurrently with the dA / dB kernel (created with the comm)
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 static_assert(sizeof(ncclUniqueId) == LORA_COMM_ID_BYTES, "NCCL unique id size");
@@ -118,6 +122,16 @@ lora_status lora_comm_init(int nranks, int rank, const uint8_t id[LORA_COMM_ID_B
         delete c;
         return nccl_fail(api, r, "ncclCommInitRank");
     }
+    // (no side stream -> the column group runs its collectives in stream order)
+    if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+        cudaGetLastError();
+        if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+        if (c->side) cudaStreamDestroy(c->side);
+        c->side = nullptr;
+        c->ev_fork = c->ev_join = nullptr;
+    }
     *out = c;
     return LORA_OK;
 }
@@ -126,6 +140,9 @@ lora_status lora_comm_destroy(lora_comm* c) {
     if (!c) return LORA_OK;
     NcclApi* api = nccl();
     if (api) api->CommDestroy(c->comm);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->side) cudaStreamDestroy(c->side);
     delete c;
     return LORA_OK;
 }
@@ -240,28 +257,57 @@ lora_status lora_tp_linear_bwd_column_group(lora_comm* c, int count, const lora_
                                           "members' partials are summed into dx_sum)", g);
     }
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    // (1) the grouped local backward: one fused K2 launch, one K3 launch
-    lora_status s = lora_linear_bwd_grouped(count, local, problems, accumulate, workspace, workspace_bytes, stream);
-    int launches = get_launches();
-    if (s != LORA_OK) return s;
-    // (2) dX w.r.t. the shared input: the members' partials summed (fp32, one RNE)
-    if (dx_sum) {
-        const int64_t T = local[0].tokens, n = local[0].d_in;
-        if (T > 0) {
-            lora_sm100::SumBf16Args A;
-            A.n = count;
-            A.count = T * n;
-            A.dst = static_cast<__nv_bfloat16*>(dx_sum);
-            for (int g = 0; g < count; ++g) A.src[g] = static_cast<const __nv_bfloat16*>(problems[g].dx);
-            int dev = 0, sms = 148;
-            if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            cudaError_t e = lora_sm100::launch_sum_bf16(A, sms, st);
-            if (e != cudaSuccess) return cuda_fail(e, "dX sum launch");
-            ++launches;
-            // (3) ONE all-reduce of the summed dX (q, k, v fused)
-            if ((s = allreduce_impl(c, dx_sum, size_t(T) * n, LORA_DT_BF16, st)) != LORA_OK) return s;
+    // (1) the grouped local backward: one fused K2 launch, one K3 launch.  Right after
+    // K2 is enqueued, (2) + (3) are forked onto the comm's side stream: the dX sum and
+    // its all-reduce need only K2's outputs, so they overlap K3 (SURVEY.md 8(e):
+    // "schedule the independent backward pieces concurrently"); joined before (4).
+    struct Fork {
+        lora_comm* c;
+        int count;
+        const lora_dims* local;
+        const lora_bwd_problem* problems;
+        void* dx_sum;
+        cudaStream_t st;
+        bool forked;
+    } fk = {c, count, local, problems, dx_sum, st, false};
+    auto dx_sum_and_reduce = [](void* ctx, int* launches) -> lora_status {
+        Fork& f = *static_cast<Fork*>(ctx);
+        const int64_t T = f.local[0].tokens, n = f.local[0].d_in;
+        if (!f.dx_sum || T <= 0) return LORA_OK;
+        cudaStream_t ss = f.st;
+        if (f.c->side) {
+            cudaError_t e = cudaEventRecord(f.c->ev_fork, f.st);
+            if (e == cudaSuccess) e = cudaStreamWaitEvent(f.c->side, f.c->ev_fork, 0);
+            if (e != cudaSuccess) return cuda_fail(e, "column group: fork onto the side stream");
+            ss = f.c->side;
+            f.forked = true;
         }
+        // (2) dX w.r.t. the shared input: the members' partials summed (fp32, one RNE)
+        lora_sm100::SumBf16Args A;
+        A.n = f.count;
+        A.count = T * n;
+        A.dst = static_cast<__nv_bfloat16*>(f.dx_sum);
+        for (int g = 0; g < f.count; ++g) A.src[g] = static_cast<const __nv_bfloat16*>(f.problems[g].dx);
+        int dev = 0, sms = 148;
+        if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaError_t e = lora_sm100::launch_sum_bf16(A, sms, ss);
+        if (e != cudaSuccess) return cuda_fail(e, "dX sum launch");
+        ++*launches;
+        // (3) ONE all-reduce of the summed dX (q, k, v fused)
+        lora_status s = allreduce_impl(f.c, f.dx_sum, size_t(T) * n, LORA_DT_BF16, ss);
+        if (s != LORA_OK) return s;
+        if (f.forked && (e = cudaEventRecord(f.c->ev_join, ss)) != cudaSuccess)
+            return cuda_fail(e, "column group: side stream join event");
+        return LORA_OK;
+    };
+    lora_status s = bwd_grouped_impl(count, local, problems, accumulate, workspace, workspace_bytes, stream,
+                                     dx_sum_and_reduce, &fk);
+    int launches = get_launches();
+    if (fk.forked) {   // join (also on failure: never leave the side stream dangling in a capture)
+        cudaError_t e = cudaStreamWaitEvent(st, c->ev_join, 0);
+        if (s == LORA_OK && e != cudaSuccess) s = cuda_fail(e, "column group: join the side stream");
     }
+    if (s != LORA_OK) return s;
     // (4) the partial dA of every member, batched into one NCCL group
     if (reduce_lora_grads && c->nranks > 1) {
         NcclApi* api = nccl();

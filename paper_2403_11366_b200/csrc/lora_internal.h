@@ -13,6 +13,14 @@ lora_status check_dims(const lora_dims* d, bool need_tokens);
 void set_launches(int n);
 int get_launches();
 
+// lora_linear_bwd_grouped with a hook run right after the grouped dX kernel is
+// enqueued (before the dA / dB kernel): after_k2(ctx, &launches) may enqueue
+// work that depends only on the members' dX (the TP column group's dX sum and
+// all-reduce, on a side stream).
+lora_status bwd_grouped_impl(int count, const lora_dims* dims, const lora_bwd_problem* probs, int accumulate,
+                             void* workspace, size_t workspace_bytes, void* stream,
+                             lora_status (*after_k2)(void* ctx, int* launches), void* ctx);
+
 // Fused-GEMM problems gathered by the grouped entry points (launched together).
 struct GemmCollector {
     int count = 0;

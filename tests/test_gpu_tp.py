@@ -85,3 +85,53 @@ def test_tp_column_group_sums_dx(comm, oracle_mod):
         assert torch.equal(dx, dx1)                              # the members' own partials are kept
         assert relF(host_f64(da), rf["da"]) <= TOL_GRAD and relF(host_f64(db), rf["db"]) <= TOL_GRAD
         torch.testing.assert_close(da, da1, rtol=1e-5, atol=1e-5 * float(da1.abs().max()))
+
+
+def test_tp_column_group_graph_replay(comm):
+    """The column group forks its dX sum + all-reduce onto the communicator's side
+    stream (overlapping the dA / dB kernel) and joins before the dA all-reduce:
+    captured into a CUDA graph and replayed with new upstream gradients it must
+    equal the eager call bitwise, every replay."""
+    import paper_2403_11366_b200 as L
+    from paper_2403_11366_b200 import tp
+    T, n = 512, 384
+    x = dev_bf16(make_lora_inputs(T, n, 8, 8, seed=80)["x"])
+    specs, probs, dys, shapes = [], [], [], [(256, 8), (192, 16)]
+    for i, (m, r) in enumerate(shapes):
+        d = make_lora_inputs(T, n, m, r, seed=81 + i)
+        w0, a, b = (dev_bf16(d[k]) for k in ("w0", "a", "b"))
+        _, h = L.lora_linear_fwd(x, w0, a, b, 16.0)
+        dy = torch.empty((T, m), dtype=torch.bfloat16, device="cuda")
+        dys.append(dy)
+        specs.append(tp.ShardSpec(tp.COLUMN, 1, 0, n, m))
+        probs.append((x, w0, a, b, dy, h))
+    dx_sum = torch.empty((T, n), dtype=torch.bfloat16, device="cuda")
+    outs = [(torch.empty((T, n), dtype=torch.bfloat16, device="cuda"), torch.empty((r, n), device="cuda"),
+             torch.empty((m, r), device="cuda")) for (m, r) in shapes]
+    ws = torch.empty(1 << 24, dtype=torch.uint8, device="cuda")
+
+    def load(seed):
+        for i, ((m, r), dy) in enumerate(zip(shapes, dys)):
+            dy.copy_(dev_bf16(make_lora_inputs(T, n, m, r, seed=seed + i)["dy"]))
+        torch.cuda.synchronize()
+
+    s = torch.cuda.Stream()
+    load(900)
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        tp.tp_linear_bwd_column_group(comm, specs, probs, [16.0] * 2, dx_sum=dx_sum, outs=outs, workspace=ws,
+                                      stream=s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        tp.tp_linear_bwd_column_group(comm, specs, probs, [16.0] * 2, dx_sum=dx_sum, outs=outs, workspace=ws,
+                                      stream=s)
+    for seed in (910, 920):
+        load(seed)
+        g.replay()
+        torch.cuda.synchronize()
+        got = [dx_sum.clone()] + [t.clone() for o in outs for t in o]
+        ref_sum, ref = tp.tp_linear_bwd_column_group(comm, specs, probs, [16.0] * 2, workspace=ws)
+        torch.cuda.synchronize()
+        for u, v in zip(got, [ref_sum] + [t for o in ref for t in o]):
+            assert torch.equal(u, v), f"replay {seed}"
