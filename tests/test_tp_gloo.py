@@ -1,4 +1,4 @@
-"""World-size-2 CPU (gloo) tests of the tensor-parallel host logic
+"""World-size-2 and -4 CPU (gloo) tests of the tensor-parallel host logic
 (paper_2403_11366_b200/tp.py): each rank takes its shard with the product's
 sharding functions, computes its local results (with the fp64 oracle standing
 in for the per-rank kernels, CPU only), and the partial results that
@@ -31,7 +31,7 @@ def _worker(rank, world, port, mode_name, q):
         import oracle
         from paper_2403_11366_b200 import tp
         from synth import make_lora_inputs
-        T, n, m, r, alpha = 24, 32, 48, 4, 16.0
+        T, n, m, r, alpha = 24, 64, 96, 4, 16.0   # shards of 16 / 32 and 24 / 48 columns
         d = make_lora_inputs(T, n, m, r, seed=77, bias=True)
         spec = tp.ShardSpec(tp.MODES[mode_name], world, rank, n, m)
         w0, a, b, bias = tp.shard_params(spec, d["w0"], d["a"], d["b"], d["bias"])
@@ -76,12 +76,13 @@ def _worker(rank, world, port, mode_name, q):
         q.put(("err", repr(e)))
 
 
+@pytest.mark.parametrize("world", [2, 4])
 @pytest.mark.parametrize("mode", ["column", "row"])
-def test_tp_world2_gloo_matches_unsharded(mode, oracle_mod):
+def test_tp_gloo_matches_unsharded(mode, world, oracle_mod):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, mode, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, mode, q)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
