@@ -26,13 +26,25 @@ __device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float (&f)[8]) {
     }
 }
 
+// two fp32 FMAs in one instruction (sm_100 FFMA2), each rounded to nearest
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;"
+        : "=l"(d)
+        : "l"(*reinterpret_cast<const uint64_t*>(&a)), "l"(*reinterpret_cast<const uint64_t*>(&b)),
+          "l"(*reinterpret_cast<const uint64_t*>(&c)));
+    return *reinterpret_cast<const float2*>(&d);
+}
+
 static int rank_bucket(int r) { return r <= 4 ? 4 : r <= 8 ? 8 : r <= 16 ? 16 : r <= 32 ? 32 : 64; }
 
 // ------------------------------------------------------------------ K4 merge
 // 64 rows x 256 columns per CTA; A[:, k0:k0+256] and B[i0:i0+64, :] staged in
-// shared memory as fp32; each thread owns 8 consecutive columns (16-byte IO).
+// shared memory as fp32; each thread owns 8 consecutive columns (16-byte IO)
+// of 8 rows.  Two CTAs per SM (128 registers: the 8 in-flight W0 rows spill a
+// few bytes while the products run; measured faster than 1 CTA per SM).
 template <int RB>
-__global__ void __launch_bounds__(256) merge_kernel(const bf16* __restrict__ w0, const bf16* __restrict__ a,
+__global__ void __launch_bounds__(256, 2) merge_kernel(const bf16* __restrict__ w0, const bf16* __restrict__ a,
                                                     const bf16* __restrict__ b, int64_t n, int64_t m, int r,
                                                     float s, bf16* __restrict__ w_out) {
     extern __shared__ float4 smem_f4[];
@@ -70,37 +82,45 @@ __global__ void __launch_bounds__(256) merge_kernel(const bf16* __restrict__ w0,
     }
     __syncthreads();
     if (!col_ok) return;
+    // The kernel is issue-bound, not HBM-bound, when every row re-reads A from
+    // shared memory and runs scalar FMAs: here A[j, kc..kc+8] is read once per j
+    // for all 8 rows, and the products run as packed FFMA2 (two fp32 FMAs per
+    // instruction, round-to-nearest each -- the same arithmetic, j ascending).
+    float2 acc[8][4];
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[q][c] = make_float2(0.0f, 0.0f);
+#pragma unroll
+    for (int j = 0; j < RB; ++j) {
+        if (j >= r) break;   // (uniform)
+        const float4 a0 = *reinterpret_cast<const float4*>(sA + j * 256 + kc);
+        const float4 a1 = *reinterpret_cast<const float4*>(sA + j * 256 + kc + 4);
+        const float2 av[4] = {make_float2(a0.x, a0.y), make_float2(a0.z, a0.w), make_float2(a1.x, a1.y),
+                              make_float2(a1.z, a1.w)};
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const float bij = sB[(warp + 8 * q) * RB + j];
+            const float2 bb = make_float2(bij, bij);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) acc[q][c] = ffma2(bb, av[c], acc[q][c]);
+        }
+    }
+    const float2 ss = make_float2(s, s);
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-        const int ii = warp + 8 * q;
-        const int64_t i = i0 + ii;
+        const int64_t i = i0 + warp + 8 * q;
         if (i >= m) break;
-        const int64_t off = i * n + k0 + kc;
         float wv[8];
         bf16x8_to_f32(wraw[q], wv);
-        float ba[8];
+        uint32_t o[4];
 #pragma unroll
-        for (int c = 0; c < 8; ++c) ba[c] = 0.0f;
-#pragma unroll
-        for (int j = 0; j < RB; ++j) {
-            const float bij = sB[ii * RB + j];
-            const float4 a0 = *reinterpret_cast<const float4*>(sA + j * 256 + kc);
-            const float4 a1 = *reinterpret_cast<const float4*>(sA + j * 256 + kc + 4);
-            ba[0] = fmaf(bij, a0.x, ba[0]); ba[1] = fmaf(bij, a0.y, ba[1]);
-            ba[2] = fmaf(bij, a0.z, ba[2]); ba[3] = fmaf(bij, a0.w, ba[3]);
-            ba[4] = fmaf(bij, a1.x, ba[4]); ba[5] = fmaf(bij, a1.y, ba[5]);
-            ba[6] = fmaf(bij, a1.z, ba[6]); ba[7] = fmaf(bij, a1.w, ba[7]);
+        for (int c = 0; c < 4; ++c) {
+            const float2 r2 = ffma2(ss, acc[q][c], make_float2(wv[2 * c], wv[2 * c + 1]));   // W0 + s (B A)
+            const __nv_bfloat162 p2 = __floats2bfloat162_rn(r2.x, r2.y);
+            o[c] = *reinterpret_cast<const uint32_t*>(&p2);
         }
-        uint4 o;
-        __nv_bfloat162 p0 = __floats2bfloat162_rn(wv[0] + s * ba[0], wv[1] + s * ba[1]);
-        __nv_bfloat162 p1 = __floats2bfloat162_rn(wv[2] + s * ba[2], wv[3] + s * ba[3]);
-        __nv_bfloat162 p2 = __floats2bfloat162_rn(wv[4] + s * ba[4], wv[5] + s * ba[5]);
-        __nv_bfloat162 p3 = __floats2bfloat162_rn(wv[6] + s * ba[6], wv[7] + s * ba[7]);
-        o.x = *reinterpret_cast<uint32_t*>(&p0);
-        o.y = *reinterpret_cast<uint32_t*>(&p1);
-        o.z = *reinterpret_cast<uint32_t*>(&p2);
-        o.w = *reinterpret_cast<uint32_t*>(&p3);
-        *reinterpret_cast<uint4*>(w_out + off) = o;
+        *reinterpret_cast<uint4*>(w_out + i * n + k0 + kc) = make_uint4(o[0], o[1], o[2], o[3]);
     }
 }
 
