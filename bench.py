@@ -572,7 +572,7 @@ def run_ours(args, wl):
 
     # ---- the HBM-bound kernels of the path, timed alone (report them in
     # GB/s against the measured HBM bandwidth): K4 merge of the first linear, and the
-    # gradient-only backward (gh pre-pass + K3s + K3) -- L2 flushed before each call
+    # gradient-only backward (B^T pack + h split, gh row projection + split, K3) -- L2 flushed before each call
     aux = {}
     if world == 1:
         e = lin[0]
@@ -621,7 +621,7 @@ def run_ours(args, wl):
                "adam_all_adapters": {"us": t_adam * 1e6, "bytes": adam_bytes, "gbs": adam_bytes / t_adam / 1e9,
                                      "tensors": len(ad)},
                "grads_only": {"us": t_grads * 1e6, "bytes": grads_bytes, "gbs": grads_bytes / t_grads / 1e9,
-                              "kernels": "gh pre-pass + K3s split + K3 (lora_linear_bwd, dx = NULL)"}}
+                              "kernels": "B^T pack + h split, gh row projection + gh split, K3 (lora_linear_bwd, dx = NULL)"}}
 
     # ---- report (rank 0)
     if rank == 0:

@@ -434,7 +434,8 @@ static lora_status launch_k3_mma(const GradArgs* pr, int count, cudaStream_t str
 // kernel with X read K-major and P as a single (unsplit, already bf16) coefficient set.
 // Used for gh = s dY B when dX is not requested and for h = x A^T when h was not saved.
 static lora_status launch_rowproj_mma(const void* X, int64_t T, int64_t K, const void* P, int r, float scale,
-                                      float* out, cudaStream_t stream, int* launches) {
+                                      float* out, cudaStream_t stream, int* launches,
+                                      __nv_bfloat16* cs_out = nullptr /* also K3's split, r % 8 == 0 */) {
     DevInfo dev;
     lora_status st = device_info(&dev);
     if (st != LORA_OK) return st;
@@ -443,6 +444,8 @@ static lora_status launch_rowproj_mma(const void* X, int64_t T, int64_t K, const
     GradMmaJob& J = G.job[0];
     J.T = K; J.N = T; J.set0 = 0; J.nsets = 1; J.q_used = r8; J.q_pad = (r8 + 15) / 16 * 16; J.a_kmajor = 1;
     G.set[0] = GradMmaSet{out, r, 1, r, r8, 0, 0, scale, 1};
+    G.set[0].cs_out = (cs_out && r == r8) ? cs_out : nullptr;
+    G.set[0].cs_t_pad = t_pad_of(T);
     if ((st = encode_2d(&G.xmap[0], X, K, T, K * 2, 64, 64, 128, "row-projection activation")) != LORA_OK) return st;
     // P rows r..r8-1 are out of bounds: TMA zero-fills them
     if ((st = encode_2d(&G.csmap[0], P, K, r, K * 2, 64, r8, 128, "row-projection operand")) != LORA_OK) return st;
@@ -570,6 +573,7 @@ lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
     const bool need_gh = dx || da;
     const bool need_h = db && !h_saved;
     const uint64_t* k2_flags = nullptr;   // this problem's K2 gh flags (stage 1; grouped stage 2: from col)
+    bool gh_split = false, h_split = false;   // a row projection already wrote K3's split of gh / h
 
     auto* xm = reinterpret_cast<__nv_bfloat16*>(wsb + W.xm);
     if (dropping && (stages & 1)) {
@@ -640,11 +644,19 @@ lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
         // K2a: gh = s dY B [T, r] fp32 for dA when the input gradient is not requested --
         // B^T [r, m] (B6, into the unused B8 slot) then the tensor-core row projection
         auto* bt = reinterpret_cast<__nv_bfloat16*>(wsb + W.b8);
-        if ((e = launch_pack_b(static_cast<const __nv_bfloat16*>(b), m, r, nullptr, bt, dev.sms, stream)) !=
-            cudaSuccess)
+        // the same launch splits the saved h for K3's dB when it can (no K3s pass)
+        h_split = db && h_saved && r % 8 == 0 && k3_mode() == kK3Mma && !dropping;
+        if ((e = launch_pack_b(static_cast<const __nv_bfloat16*>(b), m, r, nullptr, bt, dev.sms, stream,
+                               h_split ? h_saved : nullptr,
+                               h_split ? reinterpret_cast<__nv_bfloat16*>(wsb + W.cs_b) : nullptr, T,
+                               t_pad_of(T))) != cudaSuccess)
             return cuda_fail(e, "B^T pack launch");
         ++*launches;
-        if ((st = launch_rowproj_mma(dya, T, m, bt, r, s, gh, stream, launches)) != LORA_OK) return st;
+        // (r % 8 == 0: it also writes K3's split of gh -- no K3s pass)
+        gh_split = r % 8 == 0 && k3_mode() == kK3Mma;
+        if ((st = launch_rowproj_mma(dya, T, m, bt, r, s, gh, stream, launches,
+                                     gh_split ? reinterpret_cast<__nv_bfloat16*>(wsb + W.cs_a) : nullptr)) != LORA_OK)
+            return st;
     }
     const float* hsrc = h_saved;
     const __nv_bfloat16* xk3 = xa;   // K3's dA activation: x, or M . x under dropout
@@ -654,8 +666,12 @@ lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
         xk3 = xm;
         scale_a = drop->q;
     } else if (need_h) {
-        // K3a: h = x A^T recomputed on the tensor cores (A [r, n] is already K-contiguous)
-        if ((st = launch_rowproj_mma(xa, T, n, aa, r, 1.0f, hbuf, stream, launches)) != LORA_OK) return st;
+        // K3a: h = x A^T recomputed on the tensor cores (A [r, n] is already K-contiguous);
+        // r % 8 == 0: it also writes K3's split of h (no K3s pass)
+        h_split = r % 8 == 0 && k3_mode() == kK3Mma;
+        if ((st = launch_rowproj_mma(xa, T, n, aa, r, 1.0f, hbuf, stream, launches,
+                                     h_split ? reinterpret_cast<__nv_bfloat16*>(wsb + W.cs_b) : nullptr)) != LORA_OK)
+            return st;
         hsrc = hbuf;
     }
     if (da || db) {
@@ -665,8 +681,8 @@ lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
         g.scale_a = scale_a;
         g.cs_a = reinterpret_cast<__nv_bfloat16*>(wsb + W.cs_a);
         g.cs_b = reinterpret_cast<__nv_bfloat16*>(wsb + W.cs_b);
-        g.cs_a_ready = dx != nullptr;                                        // K2 split gh
-        g.cs_b_ready = dx != nullptr && (h_saved != nullptr || (dropping && need_h));
+        g.cs_a_ready = dx != nullptr || gh_split;                            // K2 / K2a split gh
+        g.cs_b_ready = (dx != nullptr && (h_saved != nullptr || (dropping && need_h))) || h_split;
         if (dx && !k2_flags && col) {   // grouped: stage 1 collected this problem's K2
             for (int i = 0; i < col->count; ++i)
                 if (col->p[i].out == dx) k2_flags = col->p[i].flags;

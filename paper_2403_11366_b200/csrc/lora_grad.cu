@@ -38,10 +38,23 @@ __device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float (&f)[8]) {
 //   pitch TMA needs (forward tail operand, only when r % 8 != 0);
 // bt[j, i] = B[i, j], [r, m]: K-major operand of the dX kernel's dY B MMA.
 __global__ void pack_b_kernel(const bf16* __restrict__ b, int64_t m, int r, int r8, bf16* __restrict__ b8,
-                              bf16* __restrict__ bt) {
+                              bf16* __restrict__ bt, const float* __restrict__ coef, bf16* __restrict__ cs,
+                              int64_t T, int64_t t_pad) {
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     const int64_t t0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const bf16 zero = __float2bfloat16(0.0f);
+    if (coef)   // K3's exact hi / mid / lo split of coef [T, r] (r == r8): cs [3 r8, t_pad]
+        for (int64_t idx = t0; idx < T * r; idx += stride) {
+            const int64_t t = idx / r;
+            const int k = static_cast<int>(idx - t * r);
+            const float v = coef[idx];
+            const bf16 hi = __float2bfloat16_rn(v);
+            const float r0 = v - __bfloat162float(hi);
+            const bf16 md = __float2bfloat16_rn(r0);
+            cs[static_cast<int64_t>(k) * t_pad + t] = hi;
+            cs[static_cast<int64_t>(r8 + k) * t_pad + t] = md;
+            cs[static_cast<int64_t>(2 * r8 + k) * t_pad + t] = __float2bfloat16_rn(r0 - __bfloat162float(md));
+        }
     if (b8)
         for (int64_t idx = t0; idx < m * r8; idx += stride) {
             const int64_t i = idx / r8;
@@ -55,11 +68,13 @@ __global__ void pack_b_kernel(const bf16* __restrict__ b, int64_t m, int r, int 
         }
 }
 
-cudaError_t launch_pack_b(const bf16* b, int64_t m, int r, bf16* b8, bf16* bt, int num_sms, cudaStream_t stream) {
+cudaError_t launch_pack_b(const bf16* b, int64_t m, int r, bf16* b8, bf16* bt, int num_sms, cudaStream_t stream,
+                          const float* coef, bf16* cs, int64_t T, int64_t t_pad) {
     const int r8 = (r + 7) / 8 * 8;
-    const int64_t work = m * r8;
+    if (coef && r != r8) return cudaErrorInvalidValue;   // no pad rows are written
+    const int64_t work = std::max<int64_t>(m * r8, coef ? T * r : 0);
     const int blocks = static_cast<int>(std::min<int64_t>((work + 255) / 256, 4LL * num_sms));
-    pack_b_kernel<<<blocks, 256, 0, stream>>>(b, m, r, r8, b8, bt);
+    pack_b_kernel<<<blocks, 256, 0, stream>>>(b, m, r, r8, b8, bt, coef, cs, T, t_pad);
     return cudaGetLastError();
 }
 

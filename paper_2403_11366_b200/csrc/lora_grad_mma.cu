@@ -143,6 +143,17 @@ cudaError_t launch_coef_split(const CoefSplitGroup& G, cudaStream_t stream) {
     return cudaGetLastError();
 }
 
+// exact 3-way bf16 split of v (hi + mid + lo == v) into K3's coefficient layout
+__device__ __forceinline__ void split3_store(const GradMmaSet& st, int k, int64_t c, float v) {
+    const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+    const float r0 = v - __bfloat162float(hi);
+    const __nv_bfloat16 md = __float2bfloat16_rn(r0);
+    const __nv_bfloat16 lo = __float2bfloat16_rn(r0 - __bfloat162float(md));
+    st.cs_out[static_cast<int64_t>(k) * st.cs_t_pad + c] = hi;
+    st.cs_out[static_cast<int64_t>(st.r8 + k) * st.cs_t_pad + c] = md;
+    st.cs_out[static_cast<int64_t>(2 * st.r8 + k) * st.cs_t_pad + c] = lo;
+}
+
 // ------------------------------------------------------------------ K3
 // Launch epilogue of every K3 CTA: wait until the preceding grid (K2, when K3
 // was launched overlapping it) has completed -- so stream order stays
@@ -339,6 +350,7 @@ __global__ void __launch_bounds__(THREADS, 1) grad_mma_kernel(const __grid_const
                         if (col_ok) {
                             float* dst = st.out + (col0 + cl) * st.stride_col + static_cast<int64_t>(k) * st.stride_k;
                             *dst = st.accumulate ? *dst + st.scale * v : st.scale * v;
+                            if (st.cs_out) split3_store(st, k, col0 + cl, st.scale * v);
                         }
                     } else if (st.stride_col == 1) {
                         partial[poff + k * PA + cl] = v;
@@ -401,6 +413,14 @@ __global__ void __launch_bounds__(THREADS, 1) grad_mma_kernel(const __grid_const
                 for (int q = 1; q < 8; ++q)
                     if (q < S) { sum.x += v[q].x; sum.y += v[q].y; sum.z += v[q].z; sum.w += v[q].w; }
                 sum.x *= st.scale; sum.y *= st.scale; sum.z *= st.scale; sum.w *= st.scale;
+                if (st.cs_out) {   // (row projections: never accumulate); 4 columns (dA^T) or 4 ranks
+                    const float sv[4] = {sum.x, sum.y, sum.z, sum.w};
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        if (is_a) split3_store(st, k, col0 + c + i, sv[i]);
+                        else split3_store(st, k + i, col0 + c, sv[i]);
+                    }
+                }
                 float4* d4 = reinterpret_cast<float4*>(dst);
                 if (st.accumulate) {
                     const float4 o4 = *d4;
@@ -417,6 +437,7 @@ __global__ void __launch_bounds__(THREADS, 1) grad_mma_kernel(const __grid_const
                 for (int q = 1; q < 8; ++q)
                     if (q < S) sum += v[q];
                 sum *= st.scale;
+                if (st.cs_out) split3_store(st, k, col0 + c, sum);
                 *dst = st.accumulate ? *dst + sum : sum;
             }
         }

@@ -117,7 +117,10 @@ cudaError_t launch_fused_gemm_group(int mode, int r_pad, int cta_group, FusedGem
 // row pitch must be a multiple of 16 bytes); bt [r, m] = B^T (dx narrow
 // operand, K-major).  Either output may be null.
 cudaError_t launch_pack_b(const __nv_bfloat16* b, int64_t m, int r, __nv_bfloat16* b8, __nv_bfloat16* bt,
-                          int num_sms, cudaStream_t stream);
+                          int num_sms, cudaStream_t stream, const float* coef = nullptr,
+                          __nv_bfloat16* cs = nullptr, int64_t T = 0, int64_t t_pad = 0);
+// (coef != null, r % 8 == 0: the same launch also writes K3's exact split of coef [T, r]
+//  into cs [3 r, t_pad] -- the dX-free backward's h, saving the K3s pass)
 
 
 
@@ -169,6 +172,11 @@ struct GradMmaSet {
     // its first coefficient load (lets K3 start while K2 is still running; else null)
     const uint64_t* wait_flags;
     int wait_n;
+    // optional (row projections): also write the exact hi / mid / lo bf16 split of
+    // scale * O[c, k] to cs_out [3 r8, cs_t_pad] (K3's coefficient operand; rows
+    // k < r only -- used when r == r8, so no pad rows exist)
+    __nv_bfloat16* cs_out;
+    int64_t cs_t_pad;
 };
 struct GradMmaJob {
     int64_t T, N;               // T: reduction extent (k-blocks of 64), N: output extent (MMA M, 128 per CTA)

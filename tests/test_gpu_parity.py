@@ -256,6 +256,8 @@ def test_launch_counts(L):
     assert L.lora_last_launch_count() == 1          # fused K1 (r % 8 == 0: TMA reads B directly)
     L.lora_linear_bwd(x, w0, a, b, dy, 16.0, h_saved=h)
     assert L.lora_last_launch_count() == 2          # fused K2 (computes and splits gh, splits h) + K3
+    L.lora_linear_bwd(x, w0, a, b, dy, 16.0, h_saved=h, want_dx=False)
+    assert L.lora_last_launch_count() == 3          # B^T pack + h split, gh row projection (+ split), K3
     d5 = make_lora_inputs(256, 128, 128, 5, seed=51)
     x, w0, a, b = (dev_bf16(d5[k]) for k in ("x", "w0", "a", "b"))
     L.lora_linear_fwd(x, w0, a, b, 16.0)
