@@ -858,21 +858,30 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
                         const uint8_t* blk = s_tailb + (tt & 1) * round_up(C::TAILB_BYTES, 1024) +
                                              (lc / 64) * (R_PAD * 128);
                         const uint32_t ch = static_cast<uint32_t>((lc % 64) / 8);
-                        float lo[16];
+                        // packed FFMA2 (two fp32 FMAs per instruction, same order and rounding)
+                        float2 lo2[8];
 #pragma unroll
-                        for (int e = 0; e < 16; ++e) lo[e] = 0.0f;
+                        for (int e = 0; e < 8; ++e) lo2[e] = make_float2(0.0f, 0.0f);
 #pragma unroll
                         for (int j = 0; j < R_PAD; ++j) {
                             if (j >= p.r) break;   // (uniform) rows r..r_pad-1 of A are zero
                             const uint4 a0 = *reinterpret_cast<const uint4*>(blk + swizzled_offset(j, ch, 128));
                             const uint4 a1 = *reinterpret_cast<const uint4*>(blk + swizzled_offset(j, ch + 1, 128));
                             const uint32_t aw[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+                            const float2 hh = make_float2(hv[j], hv[j]);
 #pragma unroll
                             for (int e = 0; e < 8; ++e) {
-                                const float2 av = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&aw[e]));
-                                lo[2 * e] = fmaf(hv[j], av.x, lo[2 * e]);
-                                lo[2 * e + 1] = fmaf(hv[j], av.y, lo[2 * e + 1]);
+                                // bf16 pair -> fp32 pair: the bf16 bits are the high halves
+                                const float2 av = make_float2(__uint_as_float(aw[e] << 16),
+                                                              __uint_as_float(aw[e] & 0xFFFF0000u));
+                                lo2[e] = ffma2(hh, av, lo2[e]);
                             }
+                        }
+                        float lo[16];
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) {
+                            lo[2 * e] = lo2[e].x;
+                            lo[2 * e + 1] = lo2[e].y;
                         }
                         // keep bits of the 16 columns, packed by K0 (32 per word; col % 16 == 0)
                         const uint32_t keep = (kw[c >> 1] >> ((c & 1) * 16)) & 0xFFFFu;
