@@ -8,7 +8,7 @@ mkdir -p $OUT
 python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1
 timeout 900 python -m pytest tests -m gpu -q > $OUT/gpu_tests.log 2>&1; echo "rc=$?" >> $OUT/gpu_tests.log
 timeout 120 python __graft_entry__.py --smoke > $OUT/smoke.log 2>&1
-for i in 1 2 3; do timeout 400 python bench.py | tail -1 >> $OUT/bench_cfg2_runs.jsonl; done
+for i in 1 2 3 4 5; do timeout 400 python bench.py | tail -1 >> $OUT/bench_cfg2_runs.jsonl; done
 for c in cfg3 cfg4 cfg5; do timeout 600 python bench.py --config $c --no-cpu-baseline | tail -1 >> $OUT/bench_${c}_runs.jsonl; done
 timeout 400 python bench.py --impl reference --steps 3 --warmup 3 | tail -1 > $OUT/bench_reference.json
 timeout 400 python bench.py --dropout 0.05 --no-cpu-baseline | tail -1 > $OUT/bench_cfg2_dropout.json
