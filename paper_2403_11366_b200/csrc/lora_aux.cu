@@ -8,6 +8,8 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
 
 #include "lora_kernels.h"
 
@@ -34,6 +36,12 @@ __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
         : "l"(*reinterpret_cast<const uint64_t*>(&a)), "l"(*reinterpret_cast<const uint64_t*>(&b)),
           "l"(*reinterpret_cast<const uint64_t*>(&c)));
     return *reinterpret_cast<const float2*>(&d);
+}
+
+// LORA_MERGE=oneshot: the one-shot merge kernel (comparison)
+static bool merge_one_shot() {
+    const char* v = getenv("LORA_MERGE");
+    return v && !strcmp(v, "oneshot");
 }
 
 static int rank_bucket(int r) { return r <= 4 ? 4 : r <= 8 ? 8 : r <= 16 ? 16 : r <= 32 ? 32 : 64; }
@@ -124,13 +132,143 @@ __global__ void __launch_bounds__(256, 2) merge_kernel(const bf16* __restrict__ 
     }
 }
 
+// Pipelined K4: a persistent CTA walks a contiguous range of 64 x 256 tiles
+// (column-block major, so A[:, k0:k0+256] is re-staged only when the column
+// block changes); the W0 tile and B's 64 rows of tile i+1 are in flight
+// (cp.async, double-buffered in shared memory) while tile i is computed and
+// stored -- the one-shot kernel above loaded, computed and stored in waves.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool ok) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+                 "l"(gmem), "r"(ok ? 16 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+template <int RB>
+__global__ void __launch_bounds__(256, 2) merge_pipe_kernel(const bf16* __restrict__ w0, const bf16* __restrict__ a,
+                                                            const bf16* __restrict__ b, int64_t n, int64_t m, int r,
+                                                            float s, bf16* __restrict__ w_out, int64_t ntiles,
+                                                            int64_t per_cta) {
+    extern __shared__ uint4 smem_u4[];
+    bf16* sW = reinterpret_cast<bf16*>(smem_u4);          // [2][64][256]
+    bf16* sBh = sW + 2 * 64 * 256;                         // [2][64 * RB]
+    float* sA = reinterpret_cast<float*>(sBh + 2 * 64 * RB);   // [RB][256]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int kc = lane * 8;
+    const int64_t nrb = (m + 63) / 64;
+    const int64_t t_begin = static_cast<int64_t>(blockIdx.x) * per_cta;
+    const int64_t t_end = t_begin + per_cta < ntiles ? t_begin + per_cta : ntiles;
+    if (t_begin >= t_end) return;
+    auto issue = [&](int64_t tile, int buf) {
+        const int64_t cb = tile / nrb, rb = tile - (tile / nrb) * nrb;
+        const int64_t k0 = cb * 256, i0 = rb * 64;
+        const bool col_ok = k0 + kc < n;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int64_t i = i0 + warp + 8 * q;
+            const bool ok = col_ok && i < m;
+            cp_async16(sW + (buf * 64 + warp + 8 * q) * 256 + kc, ok ? w0 + i * n + k0 + kc : w0, ok);
+        }
+        // B rows i0 .. i0 + 63 are one contiguous run of 64 r bf16 (16-byte chunks, r % 8 == 0 here)
+        const int64_t rows = m - i0 < 64 ? m - i0 : 64;
+        const int chunks = static_cast<int>(rows * r / 8);
+        for (int c = threadIdx.x; c < 8 * RB; c += 256)
+            cp_async16(sBh + buf * 64 * RB + c * 8, c < chunks ? b + i0 * r + c * 8 : b, c < chunks);
+        cp_async_commit();
+    };
+    issue(t_begin, 0);
+    int64_t cb_staged = -1;
+    for (int64_t t = t_begin; t < t_end; ++t) {
+        const int buf = static_cast<int>((t - t_begin) & 1);
+        const int64_t cb = t / nrb, rb = t - cb * nrb;
+        const int64_t k0 = cb * 256, i0 = rb * 64;
+        if (cb != cb_staged) {   // A[:, k0:k0+256] as fp32 (previous tile's readers are past the barrier)
+            for (int idx = threadIdx.x; idx < RB * 32; idx += 256) {
+                const int j = idx >> 5, kk = (idx & 31) * 8;
+                float f[8];
+                if (j < r && k0 + kk < n) {
+                    bf16x8_to_f32(__ldg(reinterpret_cast<const uint4*>(a + static_cast<int64_t>(j) * n + k0 + kk)), f);
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) f[c] = 0.0f;
+                }
+                *reinterpret_cast<float4*>(sA + j * 256 + kk) = make_float4(f[0], f[1], f[2], f[3]);
+                *reinterpret_cast<float4*>(sA + j * 256 + kk + 4) = make_float4(f[4], f[5], f[6], f[7]);
+            }
+            cb_staged = cb;
+        }
+        if (t + 1 < t_end) issue(t + 1, buf ^ 1);
+        else cp_async_commit();   // (empty group: wait_group 1 below then covers tile t)
+        cp_async_wait1();
+        __syncthreads();
+        if (k0 + kc < n) {
+            float2 acc[8][4];
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) acc[q][c] = make_float2(0.0f, 0.0f);
+            const bf16* bsm = sBh + buf * 64 * RB;
+#pragma unroll
+            for (int j = 0; j < RB; ++j) {
+                if (j >= r) break;   // (uniform)
+                const float4 a0 = *reinterpret_cast<const float4*>(sA + j * 256 + kc);
+                const float4 a1 = *reinterpret_cast<const float4*>(sA + j * 256 + kc + 4);
+                const float2 av[4] = {make_float2(a0.x, a0.y), make_float2(a0.z, a0.w), make_float2(a1.x, a1.y),
+                                      make_float2(a1.z, a1.w)};
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const float bij = __bfloat162float(bsm[(warp + 8 * q) * r + j]);
+                    const float2 bb = make_float2(bij, bij);
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) acc[q][c] = ffma2(bb, av[c], acc[q][c]);
+                }
+            }
+            const float2 ss = make_float2(s, s);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int64_t i = i0 + warp + 8 * q;
+                if (i >= m) break;
+                float wv[8];
+                bf16x8_to_f32(*reinterpret_cast<const uint4*>(sW + (buf * 64 + warp + 8 * q) * 256 + kc), wv);
+                uint32_t o[4];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const float2 r2 = ffma2(ss, acc[q][c], make_float2(wv[2 * c], wv[2 * c + 1]));
+                    const __nv_bfloat162 p2 = __floats2bfloat162_rn(r2.x, r2.y);
+                    o[c] = *reinterpret_cast<const uint32_t*>(&p2);
+                }
+                *reinterpret_cast<uint4*>(w_out + i * n + k0 + kc) = make_uint4(o[0], o[1], o[2], o[3]);
+            }
+        }
+        __syncthreads();   // buffer `buf` and sA are free for the next issue / staging
+    }
+}
+
 template <int RB>
 static cudaError_t launch_merge_rb(const bf16* w0, const bf16* a, const bf16* b, int64_t n, int64_t m,
                                    int r, float s, bf16* w_out, cudaStream_t stream) {
+    cudaError_t e;
+    if (r % 8 == 0 && !merge_one_shot()) {   // pipelined (B rows as 16-byte chunks need r % 8 == 0)
+        const size_t smem = 2 * 64 * 256 * 2 + 2 * 64 * RB * 2 + RB * 256 * 4;
+        auto kern = merge_pipe_kernel<RB>;
+        if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem))) !=
+            cudaSuccess)
+            return e;
+        int dev = 0, sms = 148, per_sm = 1;
+        if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem);
+        if (per_sm < 1) per_sm = 1;
+        const int64_t ntiles = ((n + 255) / 256) * ((m + 63) / 64);
+        const int64_t ctas = std::min<int64_t>(ntiles, int64_t(sms) * per_sm);
+        const int64_t per_cta = (ntiles + ctas - 1) / ctas;
+        kern<<<static_cast<unsigned>((ntiles + per_cta - 1) / per_cta), 256, smem, stream>>>(w0, a, b, n, m, r, s,
+                                                                                           w_out, ntiles, per_cta);
+        return cudaGetLastError();
+    }
     const size_t smem = (RB * 256 + 64 * RB) * sizeof(float);
     auto kern = merge_kernel<RB>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     dim3 grid(static_cast<unsigned>((n + 255) / 256), static_cast<unsigned>((m + 63) / 64));
     kern<<<grid, 256, smem, stream>>>(w0, a, b, n, m, r, s, w_out);
