@@ -144,36 +144,41 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool ok
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
+#ifndef LORA_MERGE_ROWS
+#define LORA_MERGE_ROWS 64
+#endif
+constexpr int kMergeTR = LORA_MERGE_ROWS;      // tile rows (8 warps x kMergeTR / 8 rows each)
+constexpr int kMergeQ = kMergeTR / 8;
 template <int RB>
 __global__ void __launch_bounds__(256, 2) merge_pipe_kernel(const bf16* __restrict__ w0, const bf16* __restrict__ a,
                                                             const bf16* __restrict__ b, int64_t n, int64_t m, int r,
                                                             float s, bf16* __restrict__ w_out, int64_t ntiles,
                                                             int64_t per_cta) {
     extern __shared__ uint4 smem_u4[];
-    bf16* sW = reinterpret_cast<bf16*>(smem_u4);          // [2][64][256]
-    bf16* sBh = sW + 2 * 64 * 256;                         // [2][64 * RB]
-    float* sA = reinterpret_cast<float*>(sBh + 2 * 64 * RB);   // [RB][256]
+    bf16* sW = reinterpret_cast<bf16*>(smem_u4);          // [2][TR][256]
+    bf16* sBh = sW + 2 * kMergeTR * 256;                   // [2][TR * RB]
+    float* sA = reinterpret_cast<float*>(sBh + 2 * kMergeTR * RB);   // [RB][256]
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int kc = lane * 8;
-    const int64_t nrb = (m + 63) / 64;
+    const int64_t nrb = (m + kMergeTR - 1) / kMergeTR;
     const int64_t t_begin = static_cast<int64_t>(blockIdx.x) * per_cta;
     const int64_t t_end = t_begin + per_cta < ntiles ? t_begin + per_cta : ntiles;
     if (t_begin >= t_end) return;
     auto issue = [&](int64_t tile, int buf) {
         const int64_t cb = tile / nrb, rb = tile - (tile / nrb) * nrb;
-        const int64_t k0 = cb * 256, i0 = rb * 64;
+        const int64_t k0 = cb * 256, i0 = rb * kMergeTR;
         const bool col_ok = k0 + kc < n;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
+        for (int q = 0; q < kMergeQ; ++q) {
             const int64_t i = i0 + warp + 8 * q;
             const bool ok = col_ok && i < m;
-            cp_async16(sW + (buf * 64 + warp + 8 * q) * 256 + kc, ok ? w0 + i * n + k0 + kc : w0, ok);
+            cp_async16(sW + (buf * kMergeTR + warp + 8 * q) * 256 + kc, ok ? w0 + i * n + k0 + kc : w0, ok);
         }
         // B rows i0 .. i0 + 63 are one contiguous run of 64 r bf16 (16-byte chunks, r % 8 == 0 here)
-        const int64_t rows = m - i0 < 64 ? m - i0 : 64;
+        const int64_t rows = m - i0 < kMergeTR ? m - i0 : kMergeTR;
         const int chunks = static_cast<int>(rows * r / 8);
-        for (int c = threadIdx.x; c < 8 * RB; c += 256)
-            cp_async16(sBh + buf * 64 * RB + c * 8, c < chunks ? b + i0 * r + c * 8 : b, c < chunks);
+        for (int c = threadIdx.x; c < kMergeTR * RB / 8; c += 256)
+            cp_async16(sBh + buf * kMergeTR * RB + c * 8, c < chunks ? b + i0 * r + c * 8 : b, c < chunks);
         cp_async_commit();
     };
     issue(t_begin, 0);
@@ -181,7 +186,7 @@ __global__ void __launch_bounds__(256, 2) merge_pipe_kernel(const bf16* __restri
     for (int64_t t = t_begin; t < t_end; ++t) {
         const int buf = static_cast<int>((t - t_begin) & 1);
         const int64_t cb = t / nrb, rb = t - cb * nrb;
-        const int64_t k0 = cb * 256, i0 = rb * 64;
+        const int64_t k0 = cb * 256, i0 = rb * kMergeTR;
         if (cb != cb_staged) {   // A[:, k0:k0+256] as fp32 (previous tile's readers are past the barrier)
             for (int idx = threadIdx.x; idx < RB * 32; idx += 256) {
                 const int j = idx >> 5, kk = (idx & 31) * 8;
@@ -202,12 +207,12 @@ __global__ void __launch_bounds__(256, 2) merge_pipe_kernel(const bf16* __restri
         cp_async_wait1();
         __syncthreads();
         if (k0 + kc < n) {
-            float2 acc[8][4];
+            float2 acc[kMergeQ][4];
 #pragma unroll
-            for (int q = 0; q < 8; ++q)
+            for (int q = 0; q < kMergeQ; ++q)
 #pragma unroll
                 for (int c = 0; c < 4; ++c) acc[q][c] = make_float2(0.0f, 0.0f);
-            const bf16* bsm = sBh + buf * 64 * RB;
+            const bf16* bsm = sBh + buf * kMergeTR * RB;
 #pragma unroll
             for (int j = 0; j < RB; ++j) {
                 if (j >= r) break;   // (uniform)
@@ -216,7 +221,7 @@ __global__ void __launch_bounds__(256, 2) merge_pipe_kernel(const bf16* __restri
                 const float2 av[4] = {make_float2(a0.x, a0.y), make_float2(a0.z, a0.w), make_float2(a1.x, a1.y),
                                       make_float2(a1.z, a1.w)};
 #pragma unroll
-                for (int q = 0; q < 8; ++q) {
+                for (int q = 0; q < kMergeQ; ++q) {
                     const float bij = __bfloat162float(bsm[(warp + 8 * q) * r + j]);
                     const float2 bb = make_float2(bij, bij);
 #pragma unroll
@@ -225,11 +230,11 @@ __global__ void __launch_bounds__(256, 2) merge_pipe_kernel(const bf16* __restri
             }
             const float2 ss = make_float2(s, s);
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
+            for (int q = 0; q < kMergeQ; ++q) {
                 const int64_t i = i0 + warp + 8 * q;
                 if (i >= m) break;
                 float wv[8];
-                bf16x8_to_f32(*reinterpret_cast<const uint4*>(sW + (buf * 64 + warp + 8 * q) * 256 + kc), wv);
+                bf16x8_to_f32(*reinterpret_cast<const uint4*>(sW + (buf * kMergeTR + warp + 8 * q) * 256 + kc), wv);
                 uint32_t o[4];
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
@@ -249,7 +254,7 @@ static cudaError_t launch_merge_rb(const bf16* w0, const bf16* a, const bf16* b,
                                    int r, float s, bf16* w_out, cudaStream_t stream) {
     cudaError_t e;
     if (r % 8 == 0 && !merge_one_shot()) {   // pipelined (B rows as 16-byte chunks need r % 8 == 0)
-        const size_t smem = 2 * 64 * 256 * 2 + 2 * 64 * RB * 2 + RB * 256 * 4;
+        const size_t smem = 2 * kMergeTR * 256 * 2 + 2 * kMergeTR * RB * 2 + RB * 256 * 4;
         auto kern = merge_pipe_kernel<RB>;
         if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem))) !=
             cudaSuccess)
@@ -259,7 +264,7 @@ static cudaError_t launch_merge_rb(const bf16* w0, const bf16* a, const bf16* b,
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem);
         if (per_sm < 1) per_sm = 1;
-        const int64_t ntiles = ((n + 255) / 256) * ((m + 63) / 64);
+        const int64_t ntiles = ((n + 255) / 256) * ((m + kMergeTR - 1) / kMergeTR);
         const int64_t ctas = std::min<int64_t>(ntiles, int64_t(sms) * per_sm);
         const int64_t per_cta = (ntiles + ctas - 1) / ctas;
         kern<<<static_cast<unsigned>((ntiles + per_cta - 1) / per_cta), 256, smem, stream>>>(w0, a, b, n, m, r, s,
