@@ -10,15 +10,20 @@ tokens/s.  One step = forward + backward of every LoRA linear of the workload
 batch 1 x seq 2048) on synthetic seeded bf16 data with inputs resident in HBM.
 FLOPs are algorithmic: 4 T m n + 6 T r (m + n) per linear (no dW0, no padding).
 At N > 1 the same global problem is tensor-sharded (column
-parallel q, v) over N processes launched by torchrun: strong scaling, NCCL
-all-reduces of dX and the LoRA-gradient bucket inside the step.
+parallel q/k/v/gate/up, row parallel o/down) over N processes launched by
+torchrun: strong scaling, NCCL all-reduces inside the step.  The default
+workload is cfg2 at N = 1 and cfg3 (the 7B decoder-layer LoRA set BASELINE.json
+names for 2/4/8 GPUs) at N > 1.
 
 Prints ONE JSON line on rank 0.  `--impl reference` times the fp64 CPU oracle
 (oracle/, the parity reference) on a bounded token sample of the same workload.
+The timed step (StepRunner) is importable: tests/test_gpu_bench_path.py checks
+exactly this step -- the same calls, buffers and CUDA graph -- against the oracle.
 """
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import subprocess
@@ -35,6 +40,7 @@ if ROOT not in sys.path:
 from synth import WORKLOADS, algorithmic_flops, make_lora_inputs  # noqa: E402
 
 FALLBACK_PEAKS = {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0}
+METRIC = "LoRA-linear fwd+bwd TFLOP/s (% bf16 peak) and tokens/s"
 
 
 def load_peaks():
@@ -47,6 +53,34 @@ def load_peaks():
 
 def workload_flops(wl, T=None):
     return sum(algorithmic_flops(T or l.T, l.n, l.m, l.r) for l in wl.linears)
+
+
+def fwd_flops(l, T=None):
+    T = T or l.T
+    return 2 * T * l.m * l.n + 2 * T * l.r * (l.n + l.m)
+
+
+def bwd_dx_flops(l, T=None):
+    """The fused dX kernel (K2): dY W0 + gh A and gh = s dY B."""
+    T = T or l.T
+    return 2 * T * l.m * l.n + 2 * T * l.r * (l.n + l.m)
+
+
+def cpu_model_name():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.lower().startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
 
 
 def gpu_local_cpus(dev_index):
@@ -66,16 +100,6 @@ def gpu_local_cpus(dev_index):
         return None
 
 
-def fwd_flops(l, T=None):
-    T = T or l.T
-    return 2 * T * l.m * l.n + 2 * T * l.r * (l.n + l.m)
-
-
-def bwd_flops(l, T=None):
-    T = T or l.T
-    return 2 * T * l.m * l.n + 4 * T * l.r * (l.n + l.m)
-
-
 # ----------------------------------------------------------------- clocks
 class ClockSampler:
     """Samples SM clock and clock-event (throttle) reasons with NVML during the
@@ -87,7 +111,7 @@ class ClockSampler:
         0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
     }
 
-    def __init__(self, device_index, period_s=0.005):
+    def __init__(self, device_index, period_s=0.002):
         self.period = period_s
         self.samples = []
         self.reasons = 0
@@ -204,18 +228,295 @@ def run_reference(args, wl):
     sample = (f"first {R} of {wl.linears[0].T} tokens of every linear of {wl.key} "
               f"(complete {R}-token fwd+bwd problems), fp64 C oracle, OpenMP {threads} threads")
     line = {
-        "impl": "reference", "metric": "LoRA-linear fwd+bwd TFLOP/s (% bf16 peak) and tokens/s",
+        "impl": "reference", "metric": METRIC,
         "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": K, "warmup": W,
         "ms_per_step": dt / K * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": wl.key, "description": wl.description, "sample_tokens": R},
         "tokens_per_s": R * K / dt,
         "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads, "kind": "oracle",
-                         "sample": sample},
+                         "sample": sample, "cpu_model": cpu_model_name()},
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+# ----------------------------------------------------------------- the timed step
+def _bits_to_dev(bits, dev):
+    import torch
+    arr = np.ascontiguousarray(bits, dtype=np.uint16)
+    return torch.from_numpy(arr.view(np.int16)).view(torch.bfloat16).to(dev)
+
+
+class StepRunner:
+    """One step of the workload: forward + backward of every LoRA linear, through
+    the public C ABI (via the binding), exactly as bench.py times it.
+
+    N = 1: the linears that read the same input in the model (q/k/v, gate/up)
+    share ONE x tensor and run as one grouped call each for fwd and bwd (one
+    persistent launch per fused GEMM).  TP (N > 1 or force_tp): column-parallel
+    groups run the grouped local forward + lora_tp_linear_bwd_column_group
+    (their dX partials summed, ONE all-reduce); row-parallel linears run
+    lora_tp_linear_fwd/bwd (y all-reduce / dB all-reduce).
+
+    `nsets` buffer sets of the step's inputs (x, dY) and outputs (y, dX) exist;
+    `use_set(k)` points the step at set k (the e2e leg captures one CUDA graph per
+    set and double-buffers host transfers against compute).  The numpy bit
+    patterns of the unsharded inputs stay in `host` for the parity checks."""
+
+    def __init__(self, wl, dev, world=1, rank=0, comm=None, group=True, dropout=0.0, nsets=1, seed0=2403):
+        import torch
+
+        import paper_2403_11366_b200 as L
+        from paper_2403_11366_b200 import tp
+        self.L, self.tp, self.torch = L, tp, torch
+        self.wl, self.dev, self.world, self.rank, self.comm = wl, dev, world, rank, comm
+        self.launches = 0
+        self.host = []
+        lin = []
+        for i, l in enumerate(wl.linears):
+            d = make_lora_inputs(l.T, l.n, l.m, l.r, seed=seed0 + i)
+            self.host.append(d)
+        # the linears of a group read the SAME activation in the model
+        for gidx in wl.groups:
+            for i in gidx[1:]:
+                self.host[i]["x"] = self.host[gidx[0]]["x"]
+        for i, l in enumerate(wl.linears):
+            d = self.host[i]
+            mode = tp.MODES[wl.tp_modes[i]]
+            spec = tp.ShardSpec(mode, world, rank, l.n, l.m)
+            w0, a, b, _ = tp.shard_params(spec, d["w0"], d["a"], d["b"])
+            T, n, m, r = l.T, spec.local_n, spec.local_m, l.r
+            e = dict(l=l, spec=spec, w0=_bits_to_dev(w0, dev), a=_bits_to_dev(a, dev), b=_bits_to_dev(b, dev),
+                     h=torch.empty((T, r), dtype=torch.float32, device=dev))
+            e["da_sets"] = [torch.zeros((r, n), dtype=torch.float32, device=dev) for _ in range(nsets)]
+            e["db_sets"] = [torch.zeros((m, r), dtype=torch.float32, device=dev) for _ in range(nsets)]
+            e["dy_sets"] = [_bits_to_dev(tp.shard_output_grad(spec, d["dy"]), dev)]
+            e["y_sets"] = [torch.empty((T, m), dtype=torch.bfloat16, device=dev) for _ in range(nsets)]
+            e["dx_sets"] = [torch.empty((T, n), dtype=torch.bfloat16, device=dev) for _ in range(nsets)]
+            dd = L.dims(T, n, m, r, l.alpha)
+            wf = L.lora_linear_fwd_workspace_bytes(dd)
+            wb = int(L.lib.lora_tp_linear_bwd_workspace_bytes(ctypes.byref(dd)))
+            if dropout > 0.0:
+                wf = max(wf, int(L.lib.lora_linear_fwd_dropout_workspace_bytes(ctypes.byref(dd))))
+                wb = max(wb, int(L.lib.lora_linear_bwd_dropout_workspace_bytes(ctypes.byref(dd))))
+            e["ws_f"] = torch.empty(max(256, wf), dtype=torch.uint8, device=dev)
+            e["ws_b"] = torch.empty(max(256, wb), dtype=torch.uint8, device=dev)
+            e["drop"] = (dropout, 2403, i) if dropout > 0.0 else None   # one Philox stream per linear
+            lin.append(e)
+        for gidx in wl.groups:   # one shared x tensor per group (per set)
+            x0 = _bits_to_dev(tp.shard_input(lin[gidx[0]]["spec"], self.host[gidx[0]]["x"]), dev)
+            for i in gidx:
+                lin[i]["x_sets"] = [x0]
+        for _ in range(1, nsets):
+            for gidx in wl.groups:
+                xk = torch.empty_like(lin[gidx[0]]["x_sets"][0])
+                for i in gidx:
+                    lin[i]["x_sets"].append(xk)
+            for e in lin:
+                e["dy_sets"].append(torch.empty_like(e["dy_sets"][0]))
+        self.lin = lin
+        self.nsets = nsets
+        self.use_set(0)
+
+        self.use_groups = comm is None and group and dropout == 0.0
+        if dropout > 0.0 and comm is not None:
+            raise SystemExit("--dropout is single-GPU only (the TP entry points have no dropout variant)")
+        self.groups = []
+        if self.use_groups:
+            for gidx in wl.groups:
+                members = [lin[i] for i in gidx]
+                ds = self._dims(members)
+                wsf = torch.empty(max(256, int(L.lib.lora_linear_fwd_grouped_workspace_bytes(len(members), ds))),
+                                  dtype=torch.uint8, device=dev)
+                wsb = torch.empty(max(256, int(L.lib.lora_linear_bwd_grouped_workspace_bytes(len(members), ds))),
+                                  dtype=torch.uint8, device=dev)
+                self.groups.append((members, wsf, wsb))
+        self.tp_groups = []
+        if comm is not None and group and dropout == 0.0:
+            for gidx in (wl.groups or tuple((i,) for i in range(len(lin)))):
+                members = [lin[i] for i in gidx]
+                if len(members) > 1 and all(e["spec"].mode == tp.COLUMN for e in members):
+                    ds = self._dims(members)
+                    wsf = torch.empty(max(256, int(L.lib.lora_linear_fwd_grouped_workspace_bytes(len(members), ds))),
+                                      dtype=torch.uint8, device=dev)
+                    wsb = torch.empty(max(256, int(L.lib.lora_tp_linear_bwd_column_group_workspace_bytes(
+                        len(members), ds))), dtype=torch.uint8, device=dev)
+                    dx_sum = [torch.empty_like(members[0]["dx_sets"][0]) for _ in range(nsets)]
+                    self.tp_groups.append((members, wsf, wsb, dx_sum))
+                else:
+                    self.tp_groups.append((members, None, None, None))
+
+    def _dims(self, members):
+        L = self.L
+        return (L.lora_dims * len(members))(*[L.dims(e["l"].T, e["spec"].local_n, e["spec"].local_m, e["l"].r,
+                                                     e["l"].alpha) for e in members])
+
+    def use_set(self, k):
+        self.k = k
+        for e in self.lin:
+            e["x"], e["dy"], e["y"], e["dx"] = e["x_sets"][k], e["dy_sets"][k], e["y_sets"][k], e["dx_sets"][k]
+            e["da"], e["db"] = e["da_sets"][k], e["db_sets"][k]
+
+    def distinct_x(self, k=0):
+        return list({id(e["x_sets"][k]): e["x_sets"][k] for e in self.lin}.values())
+
+    # ------------------------------------------------------------ one step
+    def step(self, ev=None):
+        """ev (optional): dict of torch.cuda.Events -- f0/f1 around the first forward
+        call, k2a/k2b and k3a/k3b around the first backward call's dX and dA/dB
+        kernels (lora_profile_next_bwd)."""
+        if self.use_groups:
+            return self._step_grouped(ev)
+        if self.tp_groups:
+            return self._step_tp(ev)
+        return self._step_single(ev)
+
+    def _prof_bwd(self, ev):
+        if ev is not None and "k2a" in ev:
+            self.L.lora_profile_next_bwd(ev["k2a"], ev["k2b"], ev["k3a"], ev["k3b"])
+
+    def _step_grouped(self, ev):
+        L = self.L
+        cur = self.torch.cuda.current_stream()
+        for gi, (members, wsf, _) in enumerate(self.groups):
+            if ev is not None and gi == 0:
+                ev["f0"].record(cur)
+            L.lora_linear_fwd_grouped([(e["x"], e["w0"], e["a"], e["b"], None) for e in members],
+                                      [e["l"].alpha for e in members], outs=[(e["y"], e["h"]) for e in members],
+                                      workspace=wsf, stream=cur)
+            self.launches += L.lora_last_launch_count()
+            if ev is not None and gi == 0:
+                ev["f1"].record(cur)
+        for gi, (members, _, wsb) in enumerate(self.groups):
+            if gi == 0:
+                self._prof_bwd(ev)
+            L.lora_linear_bwd_grouped([(e["x"], e["w0"], e["a"], e["b"], e["dy"], e["h"]) for e in members],
+                                      [e["l"].alpha for e in members],
+                                      outs=[(e["dx"], e["da"], e["db"]) for e in members], workspace=wsb, stream=cur)
+            self.launches += L.lora_last_launch_count()
+
+    def _step_tp(self, ev):
+        L, tp, comm = self.L, self.tp, self.comm
+        cur = self.torch.cuda.current_stream()
+        for gi, (members, wsf, _, _) in enumerate(self.tp_groups):
+            if ev is not None and gi == 0:
+                ev["f0"].record(cur)
+            if wsf is not None:
+                L.lora_linear_fwd_grouped([(e["x"], e["w0"], e["a"], e["b"], None) for e in members],
+                                          [e["l"].alpha for e in members],
+                                          outs=[(e["y"], e["h"]) for e in members], workspace=wsf, stream=cur)
+                self.launches += L.lora_last_launch_count()
+            else:
+                for e in members:
+                    tp.tp_linear_fwd(comm, e["spec"], e["x"], e["w0"], e["a"], e["b"], e["l"].alpha, y=e["y"],
+                                     h_out=e["h"], workspace=e["ws_f"], stream=cur)
+                    self.launches += L.lora_last_launch_count()
+            if ev is not None and gi == 0:
+                ev["f1"].record(cur)
+        for gi, (members, _, wsb, dx_sum) in enumerate(self.tp_groups):
+            if gi == 0:
+                self._prof_bwd(ev)
+            if wsb is not None:
+                tp.tp_linear_bwd_column_group(comm, [e["spec"] for e in members],
+                                              [(e["x"], e["w0"], e["a"], e["b"], e["dy"], e["h"]) for e in members],
+                                              [e["l"].alpha for e in members], dx_sum=dx_sum[self.k],
+                                              outs=[(e["dx"], e["da"], e["db"]) for e in members], workspace=wsb,
+                                              stream=cur)
+                self.launches += L.lora_last_launch_count()
+            else:
+                for e in members:
+                    tp.tp_linear_bwd(comm, e["spec"], e["x"], e["w0"], e["a"], e["b"], e["dy"], e["l"].alpha,
+                                     h_saved=e["h"], dx=e["dx"], da=e["da"], db=e["db"], workspace=e["ws_b"],
+                                     reduce_lora_grads=True, stream=cur)
+                    self.launches += L.lora_last_launch_count()
+
+    def _step_single(self, ev):
+        L, tp, comm = self.L, self.tp, self.comm
+        cur = self.torch.cuda.current_stream()
+        lin = self.lin
+        for e in lin:
+            if ev is not None and e is lin[0]:
+                ev["f0"].record(cur)
+            if comm is None:
+                L.lora_linear_fwd(e["x"], e["w0"], e["a"], e["b"], e["l"].alpha, y=e["y"], h_out=e["h"],
+                                  workspace=e["ws_f"], stream=cur, dropout=e["drop"])
+            else:
+                tp.tp_linear_fwd(comm, e["spec"], e["x"], e["w0"], e["a"], e["b"], e["l"].alpha, y=e["y"],
+                                 h_out=e["h"], workspace=e["ws_f"], stream=cur)
+            self.launches += L.lora_last_launch_count()
+            if ev is not None and e is lin[0]:
+                ev["f1"].record(cur)
+        for e in lin:
+            if e is lin[0]:
+                self._prof_bwd(ev)
+            if comm is None:
+                L.lora_linear_bwd(e["x"], e["w0"], e["a"], e["b"], e["dy"], e["l"].alpha, h_saved=e["h"],
+                                  dx=e["dx"], da=e["da"], db=e["db"], workspace=e["ws_b"], stream=cur,
+                                  dropout=e["drop"])
+            else:
+                tp.tp_linear_bwd(comm, e["spec"], e["x"], e["w0"], e["a"], e["b"], e["dy"], e["l"].alpha,
+                                 h_saved=e["h"], dx=e["dx"], da=e["da"], db=e["db"], workspace=e["ws_b"],
+                                 reduce_lora_grads=True, stream=cur)
+            self.launches += L.lora_last_launch_count()
+
+    def capture(self, k=0):
+        """The whole step (every fwd + bwd launch, and under TP every NCCL
+        collective) on buffer set k as one CUDA graph; returns (graph, launches
+        per replay)."""
+        torch = self.torch
+        self.use_set(k)
+        cur = torch.cuda.current_stream()
+        gstream = torch.cuda.Stream(device=self.dev)
+        gstream.wait_stream(cur)
+        graph = torch.cuda.CUDAGraph()
+        n0 = self.launches
+        with torch.cuda.stream(gstream):
+            with torch.cuda.graph(graph, stream=gstream):
+                self.step()
+        cur.wait_stream(gstream)
+        return graph, self.launches - n0
+
+    # ------------------------------------------------------------ parity
+    def parity(self, rows_per_linear=None, seed=7):
+        """The outputs currently in buffer set self.k against the fp64 oracle on the
+        same (unsharded) inputs: y, h and dX on sampled token rows (the first 256 --
+        one full CTA-pair tile --, 128 random and the last 32), dA and dB in full.
+        Only for the unsharded step (N = 1, not TP).  Returns a dict of relF maxima
+        over the linears plus the tolerance verdict."""
+        import oracle
+
+        from tests.gpu_util import host_f64 as to_f64
+        from tests.gpu_util import relF
+        if self.world != 1:
+            return None
+        self.torch.cuda.synchronize()
+        worst = {"y": 0.0, "h": 0.0, "dx": 0.0, "da": 0.0, "db": 0.0}
+        nrows = 0
+        for i, e in enumerate(self.lin):
+            l, d = e["l"], self.host[i]
+            T = l.T
+            if rows_per_linear is None:
+                rng = np.random.default_rng(seed + i)
+                rows = np.unique(np.concatenate([np.arange(min(256, T)), rng.choice(T, min(128, T), replace=False),
+                                                 np.arange(max(0, T - 32), T)]))
+            else:
+                rows = rows_per_linear
+            yo, ho = oracle.lora_fwd(d["x"], d["w0"], d["a"], d["b"], l.alpha, rows=rows)
+            go = oracle.lora_bwd(d["x"], d["w0"], d["a"], d["b"], d["dy"], l.alpha, rows=rows)
+            ri = self.torch.as_tensor(rows, device=self.dev)
+            got = {"y": to_f64(e["y"][ri]), "h": to_f64(e["h"][ri]), "dx": to_f64(e["dx"][ri]),
+                   "da": to_f64(e["da"]), "db": to_f64(e["db"])}
+            ref = {"y": yo, "h": ho, "dx": go["dx"], "da": go["da"], "db": go["db"]}
+            for k in worst:
+                worst[k] = max(worst[k], relF(got[k], ref[k]))
+            nrows += len(rows)
+        ok = worst["y"] <= 1e-2 and worst["dx"] <= 1e-2 and worst["da"] <= 2e-2 and worst["db"] <= 2e-2
+        return {"relF_max_over_linears": worst, "rows_checked_per_linear": int(nrows // len(self.lin)),
+                "tolerance": {"y": 1e-2, "dx": 1e-2, "da": 2e-2, "db": 2e-2}, "pass": bool(ok),
+                "what": "last timed CUDA-graph replay vs fp64 oracle: y, h, dX on the first 256 + 128 random + "
+                        "last 32 token rows of every linear, dA and dB in full"}
 
 
 # ----------------------------------------------------------------- GPU leg
@@ -244,161 +545,8 @@ def run_ours(args, wl):
 
     stream = torch.cuda.current_stream()
     comm = tp.LoraComm() if (world > 1 or args.force_tp) else None
-
-    # ---- inputs (seeded, synthetic, sharded per rank), resident in HBM
-    lin = []
-    for i, l in enumerate(wl.linears):
-        d = make_lora_inputs(l.T, l.n, l.m, l.r, seed=2403 + i)
-        mode = tp.MODES[wl.tp_modes[i]]
-        spec = tp.ShardSpec(mode, world, rank, l.n, l.m)
-        w0, a, b, _ = tp.shard_params(spec, d["w0"], d["a"], d["b"])
-        x = tp.shard_input(spec, d["x"])
-        dy = tp.shard_output_grad(spec, d["dy"])
-
-        def to_dev(arr):
-            arr = np.ascontiguousarray(arr, dtype=np.uint16)
-            return torch.from_numpy(arr.view(np.int16)).view(torch.bfloat16).to(dev)
-
-        T, n, m, r = l.T, spec.local_n, spec.local_m, l.r
-        e = dict(l=l, spec=spec, x=to_dev(x), w0=to_dev(w0), a=to_dev(a), b=to_dev(b), dy=to_dev(dy),
-                 y=torch.empty((T, m), dtype=torch.bfloat16, device=dev),
-                 h=torch.empty((T, r), dtype=torch.float32, device=dev),
-                 dx=torch.empty((T, n), dtype=torch.bfloat16, device=dev),
-                 da=torch.zeros((r, n), dtype=torch.float32, device=dev),
-                 db=torch.zeros((m, r), dtype=torch.float32, device=dev))
-        dd = L.dims(T, n, m, r, l.alpha)
-        import ctypes
-        wf = L.lora_linear_fwd_workspace_bytes(dd)
-        wb = int(L.lib.lora_tp_linear_bwd_workspace_bytes(ctypes.byref(dd)))
-        if args.dropout > 0.0:
-            wf = max(wf, int(L.lib.lora_linear_fwd_dropout_workspace_bytes(ctypes.byref(dd))))
-            wb = max(wb, int(L.lib.lora_linear_bwd_dropout_workspace_bytes(ctypes.byref(dd))))
-        e["ws_f"] = torch.empty(max(256, wf), dtype=torch.uint8, device=dev)
-        e["ws_b"] = torch.empty(max(256, wb), dtype=torch.uint8, device=dev)
-        lin.append(e)
-    # the linears of a group read the SAME activation in the model (q/k/v read the
-    # attention input, gate/up the MLP input): one shared x tensor per group
-    for gidx in wl.groups:
-        for i in gidx[1:]:
-            lin[i]["x"] = lin[gidx[0]]["x"]
-    launches = {"n": 0}
-
-    # N = 1: the linears that share an input in the model (q,k,v / gate,up) run as
-    # one grouped call (one persistent launch per fused GEMM)
-    use_groups = comm is None and not args.no_group and args.dropout == 0.0
-    if args.dropout > 0.0 and comm is not None:
-        raise SystemExit("--dropout is single-GPU only (the TP entry points have no dropout variant)")
-    for i, e in enumerate(lin):   # one Philox stream per linear (offset = its index)
-        e["drop"] = (args.dropout, 2403, i) if args.dropout > 0.0 else None
-    groups = []
-    if use_groups:
-        for gidx in wl.groups:
-            members = [lin[i] for i in gidx]
-            ds = (L.lora_dims * len(members))(*[L.dims(e["l"].T, e["spec"].local_n, e["spec"].local_m, e["l"].r,
-                                                       e["l"].alpha) for e in members])
-            wsf = torch.empty(max(256, int(L.lib.lora_linear_fwd_grouped_workspace_bytes(len(members), ds))),
-                              dtype=torch.uint8, device=dev)
-            wsb = torch.empty(max(256, int(L.lib.lora_linear_bwd_grouped_workspace_bytes(len(members), ds))),
-                              dtype=torch.uint8, device=dev)
-            groups.append((members, wsf, wsb))
-
-    def step_grouped(ev=None):
-        cur = torch.cuda.current_stream()
-        for gi, (members, wsf, _) in enumerate(groups):
-            if ev is not None and gi == 0:
-                ev["f0"].record(stream)
-            L.lora_linear_fwd_grouped([(e["x"], e["w0"], e["a"], e["b"], None) for e in members],
-                                      [e["l"].alpha for e in members], outs=[(e["y"], e["h"]) for e in members],
-                                      workspace=wsf, stream=cur)
-            launches["n"] += L.lora_last_launch_count()
-            if ev is not None and gi == 0:
-                ev["f1"].record(stream)
-        for members, _, wsb in groups:
-            L.lora_linear_bwd_grouped([(e["x"], e["w0"], e["a"], e["b"], e["dy"], e["h"]) for e in members],
-                                      [e["l"].alpha for e in members],
-                                      outs=[(e["dx"], e["da"], e["db"]) for e in members], workspace=wsb,
-                                      stream=cur)
-            launches["n"] += L.lora_last_launch_count()
-
-    # Tensor parallel (N > 1, or --force-tp): the COLUMN-parallel linears that share an
-    # input (q/k/v, gate/up) run as one grouped local forward (no collective in column
-    # mode) and one lora_tp_linear_bwd_column_group (their dX partials summed, ONE
-    # all-reduce); row-parallel linears (o, down) run one by one.
-    tp_groups = []
-    if comm is not None and not args.no_group and args.dropout == 0.0:
-        for gidx in (wl.groups or tuple((i,) for i in range(len(lin)))):
-            members = [lin[i] for i in gidx]
-            if len(members) > 1 and all(e["spec"].mode == tp.COLUMN for e in members):
-                ds = (L.lora_dims * len(members))(*[L.dims(e["l"].T, e["spec"].local_n, e["spec"].local_m,
-                                                           e["l"].r, e["l"].alpha) for e in members])
-                wsf = torch.empty(max(256, int(L.lib.lora_linear_fwd_grouped_workspace_bytes(len(members), ds))),
-                                  dtype=torch.uint8, device=dev)
-                wsb = torch.empty(max(256, int(L.lib.lora_tp_linear_bwd_column_group_workspace_bytes(
-                    len(members), ds))), dtype=torch.uint8, device=dev)
-                dx_sum = torch.empty_like(members[0]["dx"])
-                tp_groups.append((members, wsf, wsb, dx_sum))
-            else:
-                tp_groups.append((members, None, None, None))
-
-    def step_tp(ev=None):
-        cur = torch.cuda.current_stream()
-        for gi, (members, wsf, _, _) in enumerate(tp_groups):
-            if ev is not None and gi == 0:
-                ev["f0"].record(stream)
-            if wsf is not None:
-                L.lora_linear_fwd_grouped([(e["x"], e["w0"], e["a"], e["b"], None) for e in members],
-                                          [e["l"].alpha for e in members],
-                                          outs=[(e["y"], e["h"]) for e in members], workspace=wsf, stream=cur)
-                launches["n"] += L.lora_last_launch_count()
-            else:
-                for e in members:
-                    tp.tp_linear_fwd(comm, e["spec"], e["x"], e["w0"], e["a"], e["b"], e["l"].alpha, y=e["y"],
-                                     h_out=e["h"], workspace=e["ws_f"], stream=cur)
-                    launches["n"] += L.lora_last_launch_count()
-            if ev is not None and gi == 0:
-                ev["f1"].record(stream)
-        for members, _, wsb, dx_sum in tp_groups:
-            if wsb is not None:
-                tp.tp_linear_bwd_column_group(comm, [e["spec"] for e in members],
-                                              [(e["x"], e["w0"], e["a"], e["b"], e["dy"], e["h"]) for e in members],
-                                              [e["l"].alpha for e in members], dx_sum=dx_sum,
-                                              outs=[(e["dx"], e["da"], e["db"]) for e in members], workspace=wsb,
-                                              stream=cur)
-                launches["n"] += L.lora_last_launch_count()
-            else:
-                for e in members:
-                    tp.tp_linear_bwd(comm, e["spec"], e["x"], e["w0"], e["a"], e["b"], e["dy"], e["l"].alpha,
-                                     h_saved=e["h"], dx=e["dx"], da=e["da"], db=e["db"], workspace=e["ws_b"],
-                                     reduce_lora_grads=True, stream=cur)
-                    launches["n"] += L.lora_last_launch_count()
-
-    def step(ev=None):
-        if use_groups:
-            return step_grouped(ev)
-        if tp_groups:
-            return step_tp(ev)
-        for e in lin:
-            if ev is not None and e is lin[0]:
-                ev["f0"].record(stream)
-            if comm is None:
-                L.lora_linear_fwd(e["x"], e["w0"], e["a"], e["b"], e["l"].alpha, y=e["y"], h_out=e["h"],
-                                  workspace=e["ws_f"], stream=torch.cuda.current_stream(), dropout=e["drop"])
-            else:
-                tp.tp_linear_fwd(comm, e["spec"], e["x"], e["w0"], e["a"], e["b"], e["l"].alpha, y=e["y"],
-                                 h_out=e["h"], workspace=e["ws_f"], stream=torch.cuda.current_stream())
-            launches["n"] += L.lora_last_launch_count()
-            if ev is not None and e is lin[0]:
-                ev["f1"].record(stream)
-        for e in lin:
-            if comm is None:
-                L.lora_linear_bwd(e["x"], e["w0"], e["a"], e["b"], e["dy"], e["l"].alpha, h_saved=e["h"],
-                                  dx=e["dx"], da=e["da"], db=e["db"], workspace=e["ws_b"],
-                                  stream=torch.cuda.current_stream(), dropout=e["drop"])
-            else:
-                tp.tp_linear_bwd(comm, e["spec"], e["x"], e["w0"], e["a"], e["b"], e["dy"], e["l"].alpha,
-                                 h_saved=e["h"], dx=e["dx"], da=e["da"], db=e["db"], workspace=e["ws_b"],
-                                 reduce_lora_grads=True, stream=torch.cuda.current_stream())
-            launches["n"] += L.lora_last_launch_count()
+    R = StepRunner(wl, dev, world, rank, comm, group=not args.no_group, dropout=args.dropout, nsets=2)
+    lin = R.lin
 
     # L2 flush between timed steps, outside the event pairs: write a 2 x L2
     # buffer, then read a second 2 x L2 buffer, so the step starts with a cold
@@ -408,44 +556,33 @@ def run_ours(args, wl):
     flush_w = torch.empty(max(2 * l2, 256 << 20) // 4, dtype=torch.float32, device=dev)
     flush_r = torch.zeros_like(flush_w)
 
-    class _Flush:
-        def fill_(self, v):
-            flush_w.fill_(float(v))
-            torch.sum(flush_r)
-
-    flush = _Flush()
+    def flush(v):
+        flush_w.fill_(float(v))
+        torch.sum(flush_r)
 
     def barrier():
         if world > 1:
             dist.barrier(device_ids=[local_rank])
         torch.cuda.synchronize()
 
+    R.use_set(0)
     for _ in range(max(3, args.warmup)):
-        step()
+        R.step()
     barrier()
 
     K = args.steps
-    use_graph = args.graph in ("on", "auto")
     graph = None
-    if use_graph:
-        # the whole step (every fwd + bwd launch, and under TP every NCCL collective)
-        # as one CUDA graph, replayed per step -- no host launch cost in the timed loop
-        gstream = torch.cuda.Stream(device=dev)
-        gstream.wait_stream(stream)
-        graph = torch.cuda.CUDAGraph()
-        launches["n"] = 0
+    per_step_launches = None
+    if args.graph in ("on", "auto"):
         try:
-            with torch.cuda.stream(gstream):
-                with torch.cuda.graph(graph, stream=gstream):
-                    step()
+            graph, per_step_launches = R.capture(0)
         except Exception as ex:   # (symmetric on every rank) -> time the eager step instead
             if args.graph == "on":
                 raise
             print(f"bench: CUDA graph capture failed ({ex!r}); timing eager steps", file=sys.stderr)
             graph = None
             torch.cuda.synchronize()
-        stream.wait_stream(gstream)
-        per_step_launches = launches["n"]
+    R.use_set(0)
     if graph is not None:
         for _ in range(3):
             graph.replay()
@@ -458,99 +595,126 @@ def run_ours(args, wl):
             raise RuntimeError("CUDA graph capture of the step is empty")
     ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
     ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
-    fev = [dict(f0=torch.cuda.Event(enable_timing=True), f1=torch.cuda.Event(enable_timing=True))
-           for _ in range(K)]
-    launches["n"] = 0
+    R.launches = 0
     with ClockSampler(local_rank) as clk:
         barrier()
         for i in range(K):
-            flush.fill_(i & 0xFF)
+            flush(i & 0xFF)
             ev0[i].record(stream)
             if graph is not None:
                 graph.replay()
             else:
-                step(None if (use_groups or tp_groups) else fev[i])
+                R.step()
             ev1[i].record(stream)
         barrier()
     step_ms = [ev0[i].elapsed_time(ev1[i]) for i in range(K)]
-    # roofline kernel: the step's first forward launch -- the grouped fused K1 of the
-    # first group of linears (or the first linear's K1 when ungrouped) -- timed with
-    # CUDA events on its launching stream inside K further eager steps (same flush)
-    if graph is not None:
-        launches["n"] = per_step_launches * K
-    if graph is not None or use_groups or tp_groups:
-        n_before = launches["n"]
-        for i in range(K):
-            flush.fill_(i & 0xFF)
-            step(fev[i])
-        launches["n"] = n_before
-        barrier()
-    fwd_ms = [fev[i]["f0"].elapsed_time(fev[i]["f1"]) for i in range(K)]
+    gpu_launches = per_step_launches * K if graph is not None else R.launches
     total_ms = float(np.sum(step_ms))
     if world > 1:
         t = torch.tensor([total_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
-    gpu_launches = launches["n"]
 
-    # ---- end to end through the public API with host buffers
-    xs = list({id(e["x"]): e["x"] for e in lin}.values())     # each distinct input once
-    # pinned host buffers on the GPU's own NUMA node (first touch by a thread bound to
-    # the GPU-local CPUs): a remote node halves the H2D bandwidth on a 2-socket host
+    # ---- parity of the timed path itself: the outputs of the last timed replay vs the oracle
+    parity = None
+    if world == 1 and not args.no_parity:
+        parity = R.parity()
+
+    # ---- in-step kernel timing: K further eager steps (same flush), CUDA events on the
+    # launching stream around the first group's fused forward (K1) and, through the
+    # library's lora_profile_next_bwd hook, around its dX kernel (K2) and dA/dB kernel (K3)
+    names = ("f0", "f1", "k2a", "k2b", "k3a", "k3b")
+    fev = [{k: torch.cuda.Event(enable_timing=True) for k in names} for _ in range(K)]
+    for d_ in fev:   # create the events (torch creates them lazily on the first record)
+        for ev in d_.values():
+            ev.record(stream)
+    barrier()
+    n_keep = R.launches
+    for i in range(K):
+        flush(i & 0xFF)
+        R.step(fev[i])
+    barrier()
+    R.launches = n_keep
+    fwd_ms = [fev[i]["f0"].elapsed_time(fev[i]["f1"]) for i in range(K)]
+    k2_ms = [fev[i]["k2a"].elapsed_time(fev[i]["k2b"]) for i in range(K)]
+    k3_ms = [fev[i]["k3a"].elapsed_time(fev[i]["k3b"]) for i in range(K)]
+
+    # ---- end to end through the public API with host buffers: every step uploads its
+    # x and dY from pinned host memory and reads back y, dX, dA and dB.  Double-buffered
+    # (one CUDA graph per buffer set): step i+1's upload and step i-1's read-back run on
+    # copy streams while step i computes; all copies are inside the timed region.
+    xs0 = R.distinct_x(0)
     old_aff = os.sched_getaffinity(0)
     local = gpu_local_cpus(local_rank)
-    if local:
+    if local:   # pinned host buffers on the GPU's own NUMA node
         os.sched_setaffinity(0, local)
     try:
-        hx = [t.cpu().pin_memory() for t in xs]
-        hdy = [e["dy"].cpu().pin_memory() for e in lin]
-        hda = [torch.zeros_like(e["da"], device="cpu").pin_memory() for e in lin]
-        hdb = [torch.zeros_like(e["db"], device="cpu").pin_memory() for e in lin]
+        hx = [t.cpu().pin_memory() for t in xs0]
+        hdy = [e["dy_sets"][0].cpu().pin_memory() for e in lin]
+        hy = [torch.empty(e["y_sets"][0].shape, dtype=torch.bfloat16).pin_memory() for e in lin]
+        hdx = [torch.empty(e["dx_sets"][0].shape, dtype=torch.bfloat16).pin_memory() for e in lin]
+        hda = [torch.empty(e["da"].shape, dtype=torch.float32).pin_memory() for e in lin]
+        hdb = [torch.empty(e["db"].shape, dtype=torch.float32).pin_memory() for e in lin]
     finally:
         if local:
             os.sched_setaffinity(0, old_aff)
     h2d = sum(t.numel() * t.element_size() for t in hx + hdy)
-    d2h = sum(t.numel() * t.element_size() for t in hda + hdb)
-
-    # Double-buffered: step i computes from buffer set i % 2 while a copy stream
-    # uploads step i+1's inputs into the other set (the H2D copies of every step
-    # stay inside the timed region; they overlap the previous step's kernels).
-    x_of = [next(j for j, t in enumerate(xs) if t is e["x"]) for e in lin]
-    xbuf = [[t, torch.empty_like(t)] for t in xs]
-    dybuf = [[e["dy"], torch.empty_like(e["dy"])] for e in lin]
-    cstream = torch.cuda.Stream(device=dev)
+    d2h = sum(t.numel() * t.element_size() for t in hy + hdx + hda + hdb)
+    graphs = None
+    if graph is not None:
+        try:
+            graphs = [graph, R.capture(1)[0]]
+        except Exception as ex:
+            print(f"bench: e2e graph capture failed ({ex!r}); e2e runs eager steps", file=sys.stderr)
+            graphs = None
+    up = torch.cuda.Stream(device=dev)
+    down = torch.cuda.Stream(device=dev)
+    xsets = [R.distinct_x(k) for k in range(2)]
+    dsets = [[e["dy_sets"][k] for e in lin] for k in range(2)]
 
     def e2e_run(n_steps):
-        copied = [torch.cuda.Event(), torch.cuda.Event()]
-        used = [torch.cuda.Event(), torch.cuda.Event()]
+        uploaded = [torch.cuda.Event(), torch.cuda.Event()]
+        computed = [torch.cuda.Event(), torch.cuda.Event()]
+        drained = [torch.cuda.Event(), torch.cuda.Event()]
         start = torch.cuda.Event()
         start.record(stream)
-        cstream.wait_event(start)
+        up.wait_event(start)
+        down.wait_event(start)
 
         def upload(k):
-            with torch.cuda.stream(cstream):
-                for j, a_ in enumerate(hx):
-                    xbuf[j][k].copy_(a_, non_blocking=True)
-                for i, b_ in enumerate(hdy):
-                    dybuf[i][k].copy_(b_, non_blocking=True)
-                copied[k].record(cstream)
+            with torch.cuda.stream(up):
+                for dst, src in zip(xsets[k], hx):
+                    dst.copy_(src, non_blocking=True)
+                for dst, src in zip(dsets[k], hdy):
+                    dst.copy_(src, non_blocking=True)
+                uploaded[k].record(up)
 
         upload(0)
         for it in range(n_steps):
             k = it % 2
-            stream.wait_event(copied[k])
-            for i, e in enumerate(lin):
-                e["x"] = xbuf[x_of[i]][k]
-                e["dy"] = dybuf[i][k]
-            step()
-            used[k].record(stream)
-            for e, a_, b_ in zip(lin, hda, hdb):
-                a_.copy_(e["da"], non_blocking=True)
-                b_.copy_(e["db"], non_blocking=True)
+            stream.wait_event(uploaded[k])
+            if it >= 2:
+                stream.wait_event(drained[k])   # step it-2's outputs in set k are read back
+            if graphs is not None:
+                graphs[k].replay()
+            else:
+                R.use_set(k)
+                R.step()
+            computed[k].record(stream)
+            with torch.cuda.stream(down):
+                down.wait_event(computed[k])
+                for e, a_, b_, c_, d_ in zip(lin, hy, hdx, hda, hdb):
+                    a_.copy_(e["y_sets"][k], non_blocking=True)
+                    b_.copy_(e["dx_sets"][k], non_blocking=True)
+                    c_.copy_(e["da_sets"][k], non_blocking=True)
+                    d_.copy_(e["db_sets"][k], non_blocking=True)
+                drained[k].record(down)
             if it + 1 < n_steps:
                 if it >= 1:
-                    cstream.wait_event(used[1 - k])   # step it-1 is done with that set
+                    up.wait_event(computed[1 - k])   # step it-1 no longer reads set 1-k
                 upload(1 - k)
+        stream.wait_stream(down)
+        stream.wait_stream(up)
 
     e2e_run(3)
     barrier()
@@ -561,9 +725,7 @@ def run_ours(args, wl):
     e2e_run(Ke)
     s1.record(stream)
     barrier()
-    for i, e in enumerate(lin):   # back to the original buffers
-        e["x"] = xbuf[x_of[i]][0]
-        e["dy"] = dybuf[i][0]
+    R.use_set(0)
     e2e_ms = s0.elapsed_time(s1)
     if world > 1:
         t = torch.tensor([e2e_ms], device=dev)
@@ -571,8 +733,8 @@ def run_ours(args, wl):
         e2e_ms = float(t.item())
 
     # ---- the HBM-bound kernels of the path, timed alone (report them in
-    # GB/s against the measured HBM bandwidth): K4 merge of the first linear, and the
-    # gradient-only backward (B^T pack + h split, gh row projection + split, K3) -- L2 flushed before each call
+    # GB/s against the measured HBM bandwidth): K4 merge of the first linear, the
+    # gradient-only backward and one Adam step over every adapter -- L2 flushed before each
     aux = {}
     if world == 1:
         e = lin[0]
@@ -585,7 +747,7 @@ def run_ours(args, wl):
                 fn()
             ts = []
             for _ in range(reps):
-                flush.fill_(1)
+                flush(1)
                 a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a0.record(stream)
                 fn()
@@ -600,11 +762,9 @@ def run_ours(args, wl):
         t_grads = timed(lambda: L.lora_linear_bwd(e["x"], e["w0"], e["a"], e["b"], e["dy"], l0_.alpha,
                                                   h_saved=e["h"], want_dx=False, da=da_, db=db_,
                                                   workspace=e["ws_b"], stream=torch.cuda.current_stream()))
-        # N3: one Adam step over every adapter tensor of the workload (A and B of each
-        # linear, fp32 master + moments): ONE launch; 30 bytes per parameter
         ad = []
-        for e in lin:
-            for t, g in ((e["a"], e["da"]), (e["b"], e["db"])):
+        for e2 in lin:
+            for t, g in ((e2["a"], e2["da"]), (e2["b"], e2["db"])):
                 ad.append((t.clone(), g, torch.zeros_like(g), torch.zeros_like(g), t.float()))
         adam_step_no = [0]
 
@@ -621,7 +781,7 @@ def run_ours(args, wl):
                "adam_all_adapters": {"us": t_adam * 1e6, "bytes": adam_bytes, "gbs": adam_bytes / t_adam / 1e9,
                                      "tensors": len(ad)},
                "grads_only": {"us": t_grads * 1e6, "bytes": grads_bytes, "gbs": grads_bytes / t_grads / 1e9,
-                              "kernels": "B^T pack + h split, gh row projection + gh split, K3 (lora_linear_bwd, dx = NULL)"}}
+                              "kernels": "lora_linear_bwd with dx = NULL (gh row projection, K3)"}}
 
     # ---- report (rank 0)
     if rank == 0:
@@ -630,25 +790,35 @@ def run_ours(args, wl):
         value = flops_step * K / (total_ms * 1e-3) / 1e12
         tokens = wl.linears[0].T
         l0 = wl.linears[0]
-        roof_linears = ([lin[i]["l"] for i in wl.groups[0]] if (use_groups or tp_groups) and wl.groups else [l0])
+        grouped = bool(R.use_groups or R.tp_groups) and bool(wl.groups)
+        roof_linears = [lin[i]["l"] for i in wl.groups[0]] if grouped else [l0]
         f_fwd = sum(fwd_flops(l) for l in roof_linears) / world
+        f_dx = sum(bwd_dx_flops(l) for l in roof_linears) / world
         fwd_avg_s = float(np.mean(fwd_ms)) * 1e-3
+        k2_avg_s = float(np.mean(k2_ms)) * 1e-3
+        k3_avg_s = float(np.mean(k3_ms)) * 1e-3
         achieved = f_fwd / fwd_avg_s / 1e12
         peak = peaks.get("bf16_tflops", FALLBACK_PEAKS["bf16_tflops"])
+        hbm = peaks.get("hbm_gbs", FALLBACK_PEAKS["hbm_gbs"])
         traffic = None
         tp_path = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tp_path):
             tj = json.load(open(tp_path))
-            traffic = (tj.get("grouped_fwd_bytes_per_launch", {}).get(wl.key) if use_groups
+            traffic = (tj.get("grouped_fwd_bytes_per_launch", {}).get(wl.key) if R.use_groups
                        else tj.get("fused_fwd_bytes_per_launch_single"))
+        # K3 algorithmic bytes: every activation it reduces over read once (x once per
+        # group sharing it, dY per linear) -- SURVEY.md 8(d) "K3" row without the tiny coefficients
+        k3_lin = roof_linears
+        k3_bytes = (2 * tokens * k3_lin[0].n + sum(2 * tokens * l.m for l in k3_lin)) / world
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
-            cval, cdt, R, thr = cpu_oracle_sample(wl, target_s=args.cpu_seconds)
+            cval, cdt, Rt, thr = cpu_oracle_sample(wl, target_s=args.cpu_seconds)
             cpu = {"value": cval / 1e12, "unit": "TFLOP/s", "cores": thr, "kind": "oracle",
-                   "sample": f"first {R} of {tokens} tokens of every linear of {wl.key} (complete "
-                             f"{R}-token fwd+bwd problems), fp64 C oracle, {cdt:.1f} s"}
+                   "cpu_model": cpu_model_name(),
+                   "sample": f"first {Rt} of {tokens} tokens of every linear of {wl.key} (complete "
+                             f"{Rt}-token fwd+bwd problems), fp64 C oracle, {cdt:.1f} s"}
         line = {
-            "metric": "LoRA-linear fwd+bwd TFLOP/s (% bf16 peak) and tokens/s",
+            "metric": METRIC,
             "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
             "ms_per_step": total_ms / K, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
@@ -658,8 +828,7 @@ def run_ours(args, wl):
                        "global_batch": 1, "seq_len": tokens,
                        "parallelism": f"tp{world}" if comm is not None else "single",
                        "cuda_graph": graph is not None,
-                       "grouped_calls": ([[wl.linears[i].name for i in g] for g in wl.groups]
-                                         if (use_groups or tp_groups) else None),
+                       "grouped_calls": ([[wl.linears[i].name for i in g] for g in wl.groups] if grouped else None),
                        "shared_inputs": [[wl.linears[i].name for i in g] for g in wl.groups if len(g) > 1],
                        "lora_dropout": args.dropout,
                        "l2": "flushed between timed steps (2xL2 write then 2xL2 read, outside the "
@@ -670,18 +839,33 @@ def run_ours(args, wl):
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": (f"lora_linear_fwd_grouped of {[l.name for l in roof_linears]} (one fused K1 "
                                     f"launch) inside the step, " if len(roof_linears) > 1 else
-                                    f"lora_linear_fwd of '{l0.name}' (B6 pack + fused K1) inside the step, ") +
+                                    f"lora_linear_fwd of '{l0.name}' (fused K1) inside the step, ") +
                                    f"{f_fwd / 1e9:.2f} algorithmic GFLOP per launch, avg {fwd_avg_s * 1e6:.1f} us",
-                         "peak_source": peak_src + " bf16_tflops (burst)"},
+                         "peak_source": peak_src + " bf16_tflops (burst)",
+                         "traffic_source": "ncu --set full dram__bytes_read+write of this launch "
+                                           "(profiles/traffic.json, committed capture)"},
+            "kernels_in_step": {
+                "K1_fwd": {"us": fwd_avg_s * 1e6, "gflop": f_fwd / 1e9, "tflops": achieved,
+                           "frac_of_peak": achieved / peak},
+                "K2_dx": {"us": k2_avg_s * 1e6, "gflop": f_dx / 1e9, "tflops": f_dx / k2_avg_s / 1e12,
+                          "frac_of_peak": f_dx / k2_avg_s / 1e12 / peak},
+                "K3_dA_dB": {"us": k3_avg_s * 1e6, "bytes": k3_bytes, "gbs": k3_bytes / k3_avg_s / 1e9,
+                             "frac_of_hbm": k3_bytes / k3_avg_s / 1e9 / hbm},
+                "what": "first group's kernels, CUDA events on the launching stream inside K eager steps "
+                        "(L2 flushed); K2/K3 via lora_profile_next_bwd, so K3 runs after K2 instead of in "
+                        "its last wave"},
             "step_ms_median": float(np.median(step_ms)),
+            "parity": parity,
             "cpu_baseline": cpu,
             "e2e": {"value": flops_step * Ke / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
-                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "what": "public API, per step: H2D x, dY from pinned host; D2H y, dX, dA, dB; "
+                            "double-buffered, one CUDA graph per buffer set" if graphs else
+                            "public API, eager steps; H2D x, dY; D2H y, dX, dA, dB"},
             "gpu_launches": gpu_launches,
             "clocks": clk.summary(),
         }
         if aux:
-            hbm = peaks.get("hbm_gbs", FALLBACK_PEAKS["hbm_gbs"])
             for v in aux.values():
                 v["frac_of_hbm"] = v["gbs"] / hbm
             line["hbm_bound_kernels"] = dict(aux, hbm_peak_gbs=hbm, linear=l0.name)
@@ -699,9 +883,11 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="cfg2", choices=sorted(WORKLOADS))
+    ap.add_argument("--config", default=None, choices=sorted(WORKLOADS),
+                    help="workload (default: cfg2 at N = 1, cfg3 -- the sharded 7B layer set -- at N > 1)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true", help="skip the oracle check of the timed outputs")
     ap.add_argument("--force-tp", action="store_true",
                     help="run the tensor-parallel code path (NCCL communicator, TP entry points) even at N = 1")
     ap.add_argument("--dropout", type=float, default=0.0,
@@ -709,9 +895,11 @@ def main():
     ap.add_argument("--no-group", action="store_true",
                     help="one call per linear instead of grouped calls for linears sharing an input")
     ap.add_argument("--graph", choices=["auto", "on", "off"], default="auto",
-                    help="replay each step as one CUDA graph (auto: at N = 1)")
+                    help="replay each step as one CUDA graph (auto: at every N, eager if capture fails)")
     args = ap.parse_args()
-    wl = WORKLOADS[args.config]
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    cfg = args.config or ("cfg2" if world == 1 else "cfg3")
+    wl = WORKLOADS[cfg]
     if args.impl == "reference":
         return run_reference(args, wl)
     return run_ours(args, wl)

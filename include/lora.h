@@ -22,7 +22,8 @@
  *     contents need no initialisation).  Cross-CTA / cross-kernel flags live
  *     in a 2 MiB static device pool inside liblora.so (zero at load, returned
  *     to zero by every launch chain that uses it), so calls may be captured
- *     into CUDA graphs and replayed with new inputs.
+ *     into CUDA graphs and replayed with new inputs; words taken during a
+ *     capture belong to that graph until it is destroyed.
  *   - *_workspace_bytes() depend only on the dims -- and on the experimental
  *     environment switch LORA_STREAMK=1 (stream-K tail schedule), which adds
  *     148 fp32 128x256 partial slots (18.9 MB) for launches of >= 32 tiles:
@@ -218,6 +219,24 @@ lora_status lora_device_check(void);
  * enqueued (for the bench's gpu_launches accounting). */
 int lora_last_launch_count(void);
 
+/* Free words (8 bytes each) of the sync-pool region that calls made during CUDA
+ * graph capture draw from (131072 words per device).  Each captured backward
+ * takes ~16-80 words for its cross-CTA flags; they belong to the capturing
+ * graph and are returned when that graph and every executable instantiated
+ * from it are destroyed, so re-capturing never exhausts the region.  A capture
+ * that finds the region full (too many LIVE graphs) fails with LORA_ERR_CUDA.
+ * Diagnostics for tests; -1 if no CUDA device is current. */
+int lora_captured_sync_words_free(void);
+
+/* Measurement hook (bench.py's in-step roofline of the dX kernel): the next
+ * backward call on this thread (lora_linear_bwd, lora_linear_bwd_grouped, or
+ * the TP backward calls) records events[0] / events[1] (cudaEvent_t, may be
+ * NULL) on its stream right before / after the fused dX kernel (K2) launch and
+ * events[2] / events[3] around the dA / dB kernel (K3).  One-shot: cleared when
+ * that call returns.  Recording between K2 and K3 stops K3 from starting in
+ * K2's last wave, so these events time each kernel on its own. */
+lora_status lora_profile_next_bwd(void* const events[4]);
+
 /* ---------------- Tensor parallelism (R10-R13) ------
  * One process per GPU.  COLUMN: W0 and B sharded on d_out, A replicated;
  * ROW: W0 and A sharded on d_in, B replicated.  `local` holds the LOCAL shard
@@ -267,8 +286,8 @@ lora_status lora_tp_linear_bwd(lora_comm* comm, lora_tp_mode mode, const lora_di
  * the members' partial dA are all-reduced in one NCCL group.  problems[g].x must
  * all be the same pointer; problems[g].dx are the members' own partials (kept);
  * dx_sum may be NULL (no dX wanted).  dB stays local (column mode).
- * accumulate with reduce_lora_grads is rejected at N > 1 (accumulate locally,
- * then lora_allreduce the sums).  Workspace: lora_linear_bwd_grouped_workspace_bytes. */
+ * accumulate with reduce_lora_grads is rejected (LORA_ERR_UNSUPPORTED: accumulate
+ * locally with reduce_lora_grads = 0, then lora_allreduce the sums).  Workspace: lora_linear_bwd_grouped_workspace_bytes. */
 size_t lora_tp_linear_bwd_column_group_workspace_bytes(int count, const lora_dims* local);
 lora_status lora_tp_linear_bwd_column_group(lora_comm* comm, int count, const lora_dims* local,
                                             const lora_bwd_problem* problems, void* dx_sum, int accumulate,

@@ -144,6 +144,10 @@ lib.lora_tp_linear_bwd_column_group.argtypes = [_vp, ctypes.c_int, _dp, ctypes.P
                                                 ctypes.c_int, ctypes.c_int, _vp, ctypes.c_size_t, _vp]
 lib.lora_tp_linear_bwd_column_group.restype = _st
 
+lib.lora_captured_sync_words_free.restype = ctypes.c_int
+lib.lora_profile_next_bwd.argtypes = [ctypes.POINTER(_vp)]
+lib.lora_profile_next_bwd.restype = _st
+
 STATUS = {0: "LORA_OK", 1: "LORA_ERR_INVALID", 2: "LORA_ERR_SHAPE", 3: "LORA_ERR_ALIGN",
           4: "LORA_ERR_UNSUPPORTED", 5: "LORA_ERR_CUDA", 6: "LORA_ERR_NCCL", 7: "LORA_ERR_WORKSPACE"}
 
@@ -225,6 +229,18 @@ def lora_linear_bwd_workspace_bytes(d: lora_dims) -> int:
 
 def lora_last_launch_count() -> int:
     return int(lib.lora_last_launch_count())
+
+
+def lora_captured_sync_words_free() -> int:
+    """Free words of the sync-pool region used by calls made during graph capture."""
+    return int(lib.lora_captured_sync_words_free())
+
+
+def lora_profile_next_bwd(k2_begin=None, k2_end=None, k3_begin=None, k3_end=None) -> None:
+    """Record torch.cuda.Events around the dX kernel and the dA / dB kernel of the
+    next backward call on this thread (include/lora.h; one-shot)."""
+    arr = (_vp * 4)(*[ev.cuda_event if ev is not None else None for ev in (k2_begin, k2_end, k3_begin, k3_end)])
+    _check(lib.lora_profile_next_bwd(arr), "lora_profile_next_bwd")
 
 
 def lora_device_check() -> None:
@@ -366,9 +382,11 @@ def lora_linear_fwd_grouped(problems, alphas, outs=None, workspace=None, stream=
     return res
 
 
-def lora_linear_bwd_grouped(problems, alphas, outs=None, accumulate=False, workspace=None, stream=None):
+def lora_linear_bwd_grouped(problems, alphas, outs=None, accumulate=False, workspace=None, stream=None,
+                            want_dx=True, want_da=True, want_db=True):
     """Grouped backward.  problems: list of (x, w0, a, b, dy, h_saved_or_None);
-    outs: optional list of (dx, da, db).  Returns the list of (dx, da, db)."""
+    outs: optional list of (dx, da, db); want_*=False passes NULL for that output
+    of every problem (not allocated).  Returns the list of (dx, da, db)."""
     G = len(problems)
     if not 1 <= G <= LORA_MAX_GROUP:
         raise ValueError(f"1 <= len(problems) <= {LORA_MAX_GROUP}")
@@ -381,12 +399,13 @@ def lora_linear_bwd_grouped(problems, alphas, outs=None, accumulate=False, works
         _bf16(x, "x", (T, n)); _bf16(w0, "w0", (m, n)); _bf16(a, "a", (r, n)); _bf16(b, "b", (m, r))
         _bf16(dy, "dy", (T, m))
         dx, da, db = outs[g] if outs is not None else (None, None, None)
-        if dx is None:
+        if dx is None and want_dx:
             dx = torch.empty((T, n), dtype=torch.bfloat16, device=x.device)
-        if da is None:
+        if da is None and want_da:
             da = torch.zeros((r, n), dtype=torch.float32, device=x.device)
-        if db is None:
+        if db is None and want_db:
             db = torch.zeros((m, r), dtype=torch.float32, device=x.device)
+        dx, da, db = (dx if want_dx else None), (da if want_da else None), (db if want_db else None)
         dims_arr[g] = dims(T, n, m, r, alphas[g])
         probs[g] = lora_bwd_problem(_ptr(x), _ptr(w0), _ptr(a), _ptr(b), _ptr(h), _ptr(dy), _ptr(dx), _ptr(da),
                                     _ptr(db))

@@ -27,6 +27,16 @@ namespace lora_host {
 
 static thread_local std::string g_last_error;
 static thread_local int g_last_launches = 0;
+// lora_profile_next_bwd: CUDA events recorded around the dX kernel (0, 1) and the
+// dA / dB kernel (2, 3) of the next backward call on this thread (one-shot)
+static thread_local void* g_prof_events[4] = {};
+
+void prof_record(int i, cudaStream_t stream) {
+    if (g_prof_events[i]) cudaEventRecord(static_cast<cudaEvent_t>(g_prof_events[i]), stream);
+}
+void prof_clear() {
+    for (auto& e : g_prof_events) e = nullptr;
+}
 
 lora_status fail(lora_status st, const char* fmt, ...) {
     char buf[512];
@@ -218,7 +228,8 @@ static lora_status collect(GemmCollector* col, const FusedGemmMaps& maps, const 
 // ------------------------------------------------------------ forward
 lora_status fwd_impl(const lora_dims* d, const void* x, const void* w0, const void* a, const void* b,
                      const void* bias, void* y, float* h_out, void* ws, size_t ws_bytes,
-                     cudaStream_t stream, int* launches, GemmCollector* col, const DropoutParams* drop) {
+                     cudaStream_t stream, int* launches, GemmCollector* col, const DropoutParams* drop,
+                     bool validate_only) {
     lora_status st = check_dims(d, true);
     if (st != LORA_OK) return st;
     const int64_t T = d->tokens, n = d->d_in, m = d->d_out;
@@ -246,7 +257,7 @@ lora_status fwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
     if (overlap(y, yb, h_out, hb)) return fail(LORA_ERR_INVALID, "lora_linear_fwd: y overlaps h_out");
     DevInfo dev;
     if ((st = device_info(&dev)) != LORA_OK) return st;
-    if (T == 0) return LORA_OK;
+    if (T == 0 || validate_only) return LORA_OK;
 
     const int rp = r_pad_of(r);
     const int r8 = r8_of(r);
@@ -340,13 +351,13 @@ static lora_status launch_k3_mma(const GradArgs* pr, int count, cudaStream_t str
         const GradArgs& g = pr[i];
         const int r8 = (g.r + 7) / 8 * 8;
         if (g.da) {
-            GradMmaSet s = {g.da, 1, g.n, g.r, r8, 0, g.accumulate, g.scale_a, 3, nullptr, 0};
-            if (g.cs_a_ready && g.k2_flags) { s.wait_flags = g.k2_flags; s.wait_n = g.k2_nflags; }
+            GradMmaSet s = {g.da, 1, g.n, g.r, r8, 0, (g.accumulate & kAccA) ? 1 : 0, g.scale_a, 3, nullptr, 0};
+            if (g.cs_a_k2 && g.k2_flags) { s.wait_flags = g.k2_flags; s.wait_n = g.k2_nflags; }
             sets[ns++] = {g.x, g.T, g.n, g.gh, g.cs_a, g.cs_a_ready != 0, s};
         }
         if (g.db) {
-            GradMmaSet s = {g.db, g.r, 1, g.r, r8, 0, g.accumulate, g.scale_b, 3, nullptr, 0};
-            if (g.cs_b_ready && g.k2_flags) { s.wait_flags = g.k2_flags; s.wait_n = g.k2_nflags; }
+            GradMmaSet s = {g.db, g.r, 1, g.r, r8, 0, (g.accumulate & kAccB) ? 1 : 0, g.scale_b, 3, nullptr, 0};
+            if (g.cs_b_k2 && g.k2_flags) { s.wait_flags = g.k2_flags; s.wait_n = g.k2_nflags; }
             sets[ns++] = {g.dy, g.T, g.m, g.h, g.cs_b, g.cs_b_ready != 0, s};
         }
     }
@@ -415,10 +426,12 @@ static lora_status launch_k3_mma(const GradArgs* pr, int count, cudaStream_t str
         waits = waits || G.set[i].wait_flags != nullptr;
     }
     G.done = nullptr;
+    prof_record(2, stream);
     if (waits && (G.done = sync_pool_alloc(1, stream)) == nullptr)
         e = cudaErrorMemoryAllocation;
     else
         e = launch_grad_mma(G, dev.sms, stream, overlap);
+    prof_record(3, stream);
     if (e != cudaSuccess) {
         for (int i = 0; i < k; ++i)   // leave no raised flag behind in the pool
             if (G.set[i].wait_flags)
@@ -524,7 +537,7 @@ lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
     const int r = d->rank;
     if (!w0 || !a || !b || (T > 0 && (!x || !dy)))
         return fail(LORA_ERR_INVALID, "lora_linear_bwd: x, w0, a, b, dy must be non-NULL");
-    if (accumulate != 0 && accumulate != 1) return fail(LORA_ERR_INVALID, "accumulate must be 0 or 1");
+    if (accumulate < 0 || accumulate > (kAccA | kAccB)) return fail(LORA_ERR_INVALID, "accumulate must be 0 or 1");
     const void* ptrs[] = {x, w0, a, b, h_saved, dy, dx, da, db, ws};
     const char* names[] = {"x", "w0", "a", "b", "h_saved", "dy", "dx", "da", "db", "workspace"};
     for (int i = 0; i < 10; ++i)
@@ -553,11 +566,14 @@ lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
     }
     DevInfo dev;
     if ((st = device_info(&dev)) != LORA_OK) return st;
+    if (stages & kStageValidate) return LORA_OK;
     cudaError_t e;
     if (T == 0) {
-        if (!accumulate && (stages & 1)) {
-            if ((e = launch_fill_zero(da, int64_t(r) * n, stream)) != cudaSuccess) return cuda_fail(e, "memset dA");
-            if ((e = launch_fill_zero(db, int64_t(m) * r, stream)) != cudaSuccess) return cuda_fail(e, "memset dB");
+        if (stages & 1) {
+            if (!(accumulate & kAccA) && (e = launch_fill_zero(da, int64_t(r) * n, stream)) != cudaSuccess)
+                return cuda_fail(e, "memset dA");
+            if (!(accumulate & kAccB) && (e = launch_fill_zero(db, int64_t(m) * r, stream)) != cudaSuccess)
+                return cuda_fail(e, "memset dB");
         }
         return LORA_OK;
     }
@@ -633,9 +649,10 @@ lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
             if ((st = collect(col, maps, p, rp, cg)) != LORA_OK) return st;
         } else {
             // dropout: the epilogue applies q M . (gh A) itself (no tail MMA)
-            if ((e = launch_fused_gemm(dropping ? kModeDxDrop : kModeDx, rp, cg, maps, p, dev.sms, stream)) !=
-                cudaSuccess)
-                return cuda_fail(e, "fused dX launch");
+            prof_record(0, stream);
+            e = launch_fused_gemm(dropping ? kModeDxDrop : kModeDx, rp, cg, maps, p, dev.sms, stream);
+            prof_record(1, stream);
+            if (e != cudaSuccess) return cuda_fail(e, "fused dX launch");
             ++*launches;
         }
     }
@@ -681,8 +698,13 @@ lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
         g.scale_a = scale_a;
         g.cs_a = reinterpret_cast<__nv_bfloat16*>(wsb + W.cs_a);
         g.cs_b = reinterpret_cast<__nv_bfloat16*>(wsb + W.cs_b);
-        g.cs_a_ready = dx != nullptr || gh_split;                            // K2 / K2a split gh
-        g.cs_b_ready = (dx != nullptr && (h_saved != nullptr || (dropping && need_h))) || h_split;
+        // who wrote K3's split coefficients: K2 (then K3 waits on K2's per-row-block flags)
+        // or a row projection / pack launched after K2 in stream order (no wait: K2 may
+        // already have reset its flags -- they are only kept for K3 when k3_waits)
+        g.cs_a_k2 = dx != nullptr;
+        g.cs_b_k2 = dx != nullptr && (h_saved != nullptr || (dropping && need_h));
+        g.cs_a_ready = g.cs_a_k2 || gh_split;                             // K2 / K2a split gh
+        g.cs_b_ready = g.cs_b_k2 || h_split;                              // K2 / B6 / K3a split h
         if (dx && !k2_flags && col) {   // grouped: stage 1 collected this problem's K2
             for (int i = 0; i < col->count; ++i)
                 if (col->p[i].out == dx) k2_flags = col->p[i].flags;
@@ -776,8 +798,11 @@ lora_status lora_linear_bwd(const lora_dims* dims, const void* x, const void* w0
                             const float* h_saved, const void* dy, void* dx, float* da, float* db, int accumulate,
                             void* workspace, size_t workspace_bytes, void* stream) {
     int launches = 0;
-    lora_status st = bwd_impl(dims, x, w0, a, b, h_saved, dy, dx, da, db, accumulate, workspace, workspace_bytes,
+    if (accumulate != 0 && accumulate != 1) return fail(LORA_ERR_INVALID, "accumulate must be 0 or 1");
+    lora_status st = bwd_impl(dims, x, w0, a, b, h_saved, dy, dx, da, db, accumulate ? kAccA | kAccB : 0,
+                              workspace, workspace_bytes,
                               static_cast<cudaStream_t>(stream), &launches);
+    prof_clear();
     set_launches(launches);
     return st;
 }
@@ -803,10 +828,14 @@ lora_status lora_linear_bwd_dropout(const lora_dims* dims, const lora_dropout* d
                                     float* da, float* db, int accumulate, void* workspace, size_t workspace_bytes,
                                     void* stream) {
     int launches = 0;
+    ProfGuard pg;
     DropoutParams dp;
     lora_status st = dropout_params(dropout, &dp);
+    if (st == LORA_OK && accumulate != 0 && accumulate != 1)
+        st = fail(LORA_ERR_INVALID, "accumulate must be 0 or 1");
     if (st == LORA_OK)
-        st = bwd_impl(dims, x, w0, a, b, h_saved, dy, dx, da, db, accumulate, workspace, workspace_bytes,
+        st = bwd_impl(dims, x, w0, a, b, h_saved, dy, dx, da, db, accumulate ? kAccA | kAccB : 0, workspace,
+                      workspace_bytes,
                       static_cast<cudaStream_t>(stream), &launches, nullptr, 3, &dp);
     set_launches(launches);
     return st;
@@ -921,6 +950,15 @@ lora_status lora_linear_fwd_grouped(int count, const lora_dims* dims, const lora
     cudaStream_t st_ = static_cast<cudaStream_t>(stream);
     GemmCollector col;
     size_t off = 0;
+    for (int g = 0; g < count; ++g) {   // validation of every problem before anything is enqueued
+        const lora_fwd_problem& pr = probs[g];
+        const size_t wg = ws_align(fwd_workspace(&dims[g]));
+        st = fwd_impl(&dims[g], pr.x, pr.w0, pr.a, pr.b, pr.bias, pr.y, pr.h_out,
+                      static_cast<uint8_t*>(workspace) + off, wg, st_, &launches, &col, nullptr, true);
+        if (st != LORA_OK) { set_launches(0); return st; }
+        off += wg;
+    }
+    off = 0;
     for (int g = 0; g < count; ++g) {
         const lora_fwd_problem& pr = probs[g];
         const size_t wg = ws_align(fwd_workspace(&dims[g]));
@@ -936,8 +974,10 @@ lora_status lora_linear_fwd_grouped(int count, const lora_dims* dims, const lora
 
 lora_status lora_linear_bwd_grouped(int count, const lora_dims* dims, const lora_bwd_problem* probs, int accumulate,
                                     void* workspace, size_t workspace_bytes, void* stream) {
-    return lora_host::bwd_grouped_impl(count, dims, probs, accumulate, workspace, workspace_bytes, stream, nullptr,
-                                       nullptr);
+    const lora_status st = lora_host::bwd_grouped_impl(count, dims, probs, accumulate, workspace, workspace_bytes,
+                                                       stream, nullptr, nullptr);
+    lora_host::prof_clear();
+    return st;
 }
 
 }  // extern "C"
@@ -955,21 +995,40 @@ lora_status bwd_grouped_impl(int count, const lora_dims* dims, const lora_bwd_pr
     if (!workspace || workspace_bytes < need)
         return fail(LORA_ERR_WORKSPACE, "lora_linear_bwd_grouped: workspace %zu < required %zu", workspace_bytes,
                     need);
+    if (accumulate != 0 && accumulate != 1) return fail(LORA_ERR_INVALID, "accumulate must be 0 or 1");
+    const int acc = accumulate ? kAccA | kAccB : 0;
     cudaStream_t st_ = static_cast<cudaStream_t>(stream);
     GemmCollector col;
+    // validation of EVERY problem before anything is enqueued (include/lora.h)
+    {
+        size_t off = 0;
+        for (int g = 0; g < count; ++g) {
+            const lora_bwd_problem& pr = probs[g];
+            const size_t wg = ws_align(bwd_workspace(&dims[g]));
+            st = bwd_impl(&dims[g], pr.x, pr.w0, pr.a, pr.b, pr.h_saved, pr.dy, pr.dx, pr.da, pr.db, acc,
+                          static_cast<uint8_t*>(workspace) + off, wg, st_, &launches, &col, kStageValidate);
+            if (st != LORA_OK) { set_launches(0); return st; }
+            off += wg;
+        }
+    }
     for (int stage = 1; stage <= 2; ++stage) {
         size_t off = 0;
         for (int g = 0; g < count; ++g) {
             const lora_bwd_problem& pr = probs[g];
             const size_t wg = ws_align(bwd_workspace(&dims[g]));
-            st = bwd_impl(&dims[g], pr.x, pr.w0, pr.a, pr.b, pr.h_saved, pr.dy, pr.dx, pr.da, pr.db, accumulate,
+            st = bwd_impl(&dims[g], pr.x, pr.w0, pr.a, pr.b, pr.h_saved, pr.dy, pr.dx, pr.da, pr.db, acc,
                           static_cast<uint8_t*>(workspace) + off, wg, st_, &launches, &col, stage);
             if (st != LORA_OK) { set_launches(launches); return st; }
             off += wg;
         }
-        if (stage == 1 && (st = launch_collected(kModeDx, col, st_, &launches)) != LORA_OK) {
-            set_launches(launches);
-            return st;
+        if (stage == 1) {
+            prof_record(0, st_);
+            st = launch_collected(kModeDx, col, st_, &launches);
+            prof_record(1, st_);
+            if (st != LORA_OK) {
+                set_launches(launches);
+                return st;
+            }
         }
         // work that needs only the dX kernel's outputs (the TP column group forks its dX
         // sum and all-reduce here, so they overlap the dA / dB kernel below)
@@ -1011,5 +1070,16 @@ lora_status lora_device_check(void) {
 }
 
 int lora_last_launch_count(void) { return get_launches(); }
+
+lora_status lora_profile_next_bwd(void* const events[4]) {
+    for (int i = 0; i < 4; ++i) g_prof_events[i] = events ? events[i] : nullptr;
+    return LORA_OK;
+}
+
+int lora_captured_sync_words_free(void) {
+    int dev = -1;
+    if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+    return sync_pool_captured_free_words(dev);
+}
 
 }  // extern "C"

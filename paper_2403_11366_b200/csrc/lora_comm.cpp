@@ -86,7 +86,9 @@ static_assert(sizeof(ncclUniqueId) == LORA_COMM_ID_BYTES, "NCCL unique id size")
 static lora_status allreduce_impl(lora_comm* c, void* buf, size_t count, lora_dtype dt, cudaStream_t st) {
     NcclApi* api = nccl();
     if (!api) return fail(LORA_ERR_NCCL, "libnccl could not be loaded (set LORA_NCCL_LIB)");
-    if (count == 0 || c->nranks == 1) return LORA_OK;
+    if (count == 0) return LORA_OK;
+    // (nranks == 1 still issues the collective: the single-rank path runs -- and is
+    // graph-captured / timed -- exactly as at N > 1; NCCL's 1-rank all-reduce is a copy)
     ncclResult_t r = api->AllReduce(buf, buf, count, dt == LORA_DT_F32 ? ncclFloat32 : ncclBfloat16, ncclSum,
                                     c->comm, st);
     if (r != ncclSuccess) return nccl_fail(api, r, "ncclAllReduce");
@@ -184,6 +186,7 @@ lora_status lora_tp_linear_bwd(lora_comm* c, lora_tp_mode mode, const lora_dims*
                                const void* dy, void* dx, float* da, float* db, int accumulate,
                                int reduce_lora_grads, void* workspace, size_t workspace_bytes, void* stream) {
     int launches = 0;
+    ProfGuard pg;
     if (!c) return fail(LORA_ERR_INVALID, "lora_tp_linear_bwd: comm is NULL");
     if (mode != LORA_TP_COLUMN && mode != LORA_TP_ROW) return fail(LORA_ERR_INVALID, "bad TP mode");
     lora_status s = check_dims(local, true);
@@ -198,20 +201,18 @@ lora_status lora_tp_linear_bwd(lora_comm* c, lora_tp_mode mode, const lora_dims*
     float* partial_grad = (mode == LORA_TP_COLUMN) ? da : db;
     const size_t pcount = (mode == LORA_TP_COLUMN) ? size_t(local->rank) * local->d_in
                                                    : size_t(local->d_out) * local->rank;
-    const bool via_scratch = reduce_lora_grads && accumulate && partial_grad && c->nranks > 1;
+    if (accumulate != 0 && accumulate != 1) return fail(LORA_ERR_INVALID, "accumulate must be 0 or 1");
+    // accumulate + reduce: the partial gradient of THIS step is written to scratch
+    // (overwrite), all-reduced, then added into the caller's buffer; the other
+    // gradient is local and accumulates directly -- in the same single backward
+    // (per-gradient accumulate bits), so nothing is computed twice.
+    const bool via_scratch = reduce_lora_grads && accumulate && partial_grad;   // (also at N = 1: same path)
     float* da_out = (via_scratch && mode == LORA_TP_COLUMN) ? scratch : da;
     float* db_out = (via_scratch && mode == LORA_TP_ROW) ? scratch : db;
+    int acc = accumulate ? lora_sm100::kAccA | lora_sm100::kAccB : 0;
+    if (via_scratch) acc = (mode == LORA_TP_COLUMN) ? lora_sm100::kAccB : lora_sm100::kAccA;
     // bwd_impl sees a workspace that excludes the scratch tail
-    if (via_scratch) {
-        // da/db written with overwrite semantics into scratch, then reduced and added
-        s = bwd_impl(local, x, w0, a, b, h_saved, dy, dx, da_out, db_out, 0, workspace, base, st, &launches);
-        if (s == LORA_OK && mode == LORA_TP_COLUMN && db)
-            s = bwd_impl(local, x, w0, a, b, h_saved, dy, nullptr, nullptr, db, 1, workspace, base, st, &launches);
-        if (s == LORA_OK && mode == LORA_TP_ROW && da)
-            s = bwd_impl(local, x, w0, a, b, h_saved, dy, nullptr, da, nullptr, 1, workspace, base, st, &launches);
-    } else {
-        s = bwd_impl(local, x, w0, a, b, h_saved, dy, dx, da, db, accumulate, workspace, base, st, &launches);
-    }
+    s = bwd_impl(local, x, w0, a, b, h_saved, dy, dx, da_out, db_out, acc, workspace, base, st, &launches);
     if (s != LORA_OK) {
         set_launches(launches);
         return s;
@@ -242,10 +243,11 @@ lora_status lora_tp_linear_bwd_column_group(lora_comm* c, int count, const lora_
                                             const lora_bwd_problem* problems, void* dx_sum, int accumulate,
                                             int reduce_lora_grads, void* workspace, size_t workspace_bytes,
                                             void* stream) {
+    ProfGuard pg;
     if (!c) return fail(LORA_ERR_INVALID, "lora_tp_linear_bwd_column_group: comm is NULL");
     if (count < 1 || count > LORA_MAX_GROUP || !local || !problems)
         return fail(LORA_ERR_INVALID, "lora_tp_linear_bwd_column_group: need 1..%d problems", LORA_MAX_GROUP);
-    if (accumulate && reduce_lora_grads && c->nranks > 1)
+    if (accumulate && reduce_lora_grads)
         return fail(LORA_ERR_UNSUPPORTED, "lora_tp_linear_bwd_column_group: accumulate with reduce_lora_grads "
                                           "(accumulate locally, then lora_allreduce the sums)");
     for (int g = 0; g < count; ++g) {
@@ -309,7 +311,7 @@ lora_status lora_tp_linear_bwd_column_group(lora_comm* c, int count, const lora_
     }
     if (s != LORA_OK) return s;
     // (4) the partial dA of every member, batched into one NCCL group
-    if (reduce_lora_grads && c->nranks > 1) {
+    if (reduce_lora_grads) {
         NcclApi* api = nccl();
         if (!api) return fail(LORA_ERR_NCCL, "libnccl could not be loaded (set LORA_NCCL_LIB)");
         if (api->GroupStart) api->GroupStart();

@@ -654,7 +654,7 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
                         const uint64_t t_start = globaltimer_ns();
                         while (ld_acquire_u64(f) != 1ull) {
                             __nanosleep(64);
-                            if (globaltimer_ns() - t_start > 4000000000ull) {
+                            if (globaltimer_ns() - t_start > kWaitTimeoutNs) {
                                 printf("lora fused GEMM: stream-K partial wait timed out (pair %d <- %d)\n", pair,
                                        cq[i]);
                                 __trap();
@@ -759,7 +759,7 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
                     const uint64_t t_start = globaltimer_ns();
                     while (ld_acquire_u64(flag) != p.epoch) {
                         __nanosleep(64);
-                        if (globaltimer_ns() - t_start > 4000000000ull) {
+                        if (globaltimer_ns() - t_start > kWaitTimeoutNs) {
                             printf("lora dX kernel: gh flag wait timed out (row block %d)\n", t_blk);
                             __trap();
                         }
@@ -954,28 +954,114 @@ constexpr int kSyncPoolWords = 1 << 18;   // 2 MiB of device memory
 constexpr int kSyncPoolRing = 1 << 17;    // [0, ring): eager calls, recycled; [ring, end): captured graphs
 __device__ unsigned long long g_sync_pool[kSyncPoolWords];
 
+namespace {
+// Captured-graph region: first-fit free list of [offset, offset + len) word
+// ranges.  A range handed to a capturing stream is owned by that graph through
+// a cudaUserObject whose destructor (run by the CUDA runtime when the graph and
+// every executable instantiated from it are destroyed) returns it here -- so
+// re-capturing graphs for the life of a process never exhausts the region.
+// The words are zero when returned: every protocol resets its words before its
+// launch chain ends.
+struct CapturePool {
+    std::mutex mu;
+    std::vector<std::pair<int, int>> free_list[64];   // per device: sorted, coalesced
+    bool init[64] = {};
+};
+CapturePool& cap_pool() {
+    static CapturePool* p = new CapturePool();   // never destroyed: destructors may run at exit
+    return *p;
+}
+struct CapturedRange {
+    int dev, off, len;
+};
+void CUDART_CB release_captured(void* ptr) {
+    CapturedRange* r = static_cast<CapturedRange*>(ptr);
+    CapturePool& P = cap_pool();
+    {
+        std::lock_guard<std::mutex> lk(P.mu);
+        auto& fl = P.free_list[r->dev];
+        auto it = std::lower_bound(fl.begin(), fl.end(), std::make_pair(r->off, 0));
+        it = fl.insert(it, {r->off, r->len});
+        // coalesce with the neighbours
+        if (it + 1 != fl.end() && it->first + it->second == (it + 1)->first) {
+            it->second += (it + 1)->second;
+            fl.erase(it + 1);
+        }
+        if (it != fl.begin() && (it - 1)->first + (it - 1)->second == it->first) {
+            (it - 1)->second += it->second;
+            fl.erase(it);
+        }
+    }
+    delete r;
+}
+}  // namespace
+
+int sync_pool_captured_free_words(int dev) {
+    CapturePool& P = cap_pool();
+    std::lock_guard<std::mutex> lk(P.mu);
+    if (dev < 0 || dev >= 64) return 0;
+    if (!P.init[dev]) return kSyncPoolWords - kSyncPoolRing;
+    int n = 0;
+    for (const auto& f : P.free_list[dev]) n += f.second;
+    return n;
+}
+
 unsigned long long* sync_pool_alloc(int words, cudaStream_t stream) {
     static std::mutex mu;
     static unsigned long long* base[64] = {};
-    static int ring_next[64] = {}, perm_next[64] = {};
+    static int ring_next[64] = {};
     if (words <= 0 || words > 4096) return nullptr;
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess) return nullptr;
+    cudaGraph_t graph = nullptr;
+    if (cudaStreamGetCaptureInfo(stream, &cs, nullptr, &graph) != cudaSuccess) return nullptr;
     const int w = (words + 7) / 8 * 8;   // 64-byte granules
-    std::lock_guard<std::mutex> lk(mu);
-    if (base[dev] == nullptr) {
-        void* p = nullptr;
-        if (cudaGetSymbolAddress(&p, g_sync_pool) != cudaSuccess) return nullptr;
-        base[dev] = static_cast<unsigned long long*>(p);
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (base[dev] == nullptr) {
+            void* p = nullptr;
+            if (cudaGetSymbolAddress(&p, g_sync_pool) != cudaSuccess) return nullptr;
+            base[dev] = static_cast<unsigned long long*>(p);
+        }
     }
     if (cs != cudaStreamCaptureStatusNone) {
-        if (kSyncPoolRing + perm_next[dev] + w > kSyncPoolWords) return nullptr;
-        unsigned long long* r = base[dev] + kSyncPoolRing + perm_next[dev];
-        perm_next[dev] += w;
-        return r;
+        if (graph == nullptr) return nullptr;
+        CapturePool& P = cap_pool();
+        int off = -1;
+        {
+            std::lock_guard<std::mutex> lk(P.mu);
+            auto& fl = P.free_list[dev];
+            if (!P.init[dev]) {
+                fl.push_back({kSyncPoolRing, kSyncPoolWords - kSyncPoolRing});
+                P.init[dev] = true;
+            }
+            for (auto it = fl.begin(); it != fl.end(); ++it) {
+                if (it->second < w) continue;
+                off = it->first;
+                it->first += w;
+                it->second -= w;
+                if (it->second == 0) fl.erase(it);
+                break;
+            }
+        }
+        if (off < 0) return nullptr;   // every captured word is held by a live graph
+        CapturedRange* r = new CapturedRange{dev, off, w};
+        cudaUserObject_t obj;
+        if (cudaUserObjectCreate(&obj, r, release_captured, 1, cudaUserObjectNoDestructorSync) != cudaSuccess) {
+            release_captured(r);
+            return nullptr;
+        }
+        if (cudaGraphRetainUserObject(graph, obj, 1, cudaGraphUserObjectMove) != cudaSuccess) {
+            cudaUserObjectRelease(obj, 1);   // runs release_captured
+            return nullptr;
+        }
+        return base[dev] + off;
     }
+    // eager calls: a recycled ring.  A word is reused only after 2^17 words of later
+    // eager allocations on this device -- thousands of calls -- by which time the
+    // launch chain that used it has long completed (its stream had to run them).
+    std::lock_guard<std::mutex> lk(mu);
     if (ring_next[dev] + w > kSyncPoolRing) ring_next[dev] = 0;
     unsigned long long* r = base[dev] + ring_next[dev];
     ring_next[dev] += w;
@@ -998,6 +1084,14 @@ static int64_t col_tiles_host(int mode, int r_pad, int64_t n_out) {
 // it does not beat the data-parallel schedule ("K1/K2 schedule"),
 // because every split exposes one more fused epilogue (5-10 us for a dX tile)
 // that the two TMEM accumulators otherwise hide under the next mainloop.
+static bool coop_enabled() {
+    static const bool on = [] {
+        const char* s = getenv("LORA_COOP");
+        return !(s && s[0] == '0');
+    }();
+    return on;
+}
+
 static bool streamk_enabled() {
     const char* v = getenv("LORA_STREAMK");
     return v && v[0] == '1';
@@ -1118,15 +1212,21 @@ static cudaError_t launch_impl(FusedGemmGroup& grp, int num_sms, cudaStream_t st
     cfg.blockDim = dim3(NUM_THREADS);
     cfg.dynamicSmemBytes = C::SMEM_BYTES;
     cfg.stream = stream;
-    cudaLaunchAttribute attr[2];
+    cudaLaunchAttribute attr[3];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = CG;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    // CTAs that wait on flags other CTAs of the SAME grid raise (dX gh tiles,
+    // stream-K partials) need those producers resident: a cooperative launch
+    // guarantees the whole (persistent, <= 1 CTA per SM) grid is co-resident even
+    // when kernels on other streams hold SMs (LORA_COOP=0 turns it off)
+    attr[2].id = cudaLaunchAttributeCooperative;
+    attr[2].val.cooperative = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 2;
+    cfg.numAttrs = ((MODE != kModeFwd || grp.sk.enabled) && coop_enabled()) ? 3 : 2;
     e = cudaLaunchKernelEx(&cfg, kern, grp);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();

@@ -248,11 +248,11 @@ __global__ void __launch_bounds__(256, (RB >= 64 ? 1 : 2)) grad_cluster_kernel(c
             for (int q = 0; q < kCS; ++q) sum += cluster.map_shared_rank(part, q)[o];
             if (is_a) {
                 float* d = g.da + static_cast<int64_t>(j) * ncols + cb0 + col;
-                *d = g.accumulate ? *d + sum : sum;
+                *d = (g.accumulate & kAccA) ? *d + sum : sum;
             } else {
                 const float val = g.scale_b * sum;
                 float* d = g.db + (cb0 + col) * r + j;
-                *d = g.accumulate ? *d + val : val;
+                *d = (g.accumulate & kAccB) ? *d + val : val;
             }
         }
     }

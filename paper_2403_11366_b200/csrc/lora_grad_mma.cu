@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(THREADS, 1) grad_mma_kernel(const __grid_const
                 const uint64_t t_start = globaltimer_ns();
                 while (!__all_sync(0xffffffffu, f >= st.wait_n || ld_relaxed_u64(st.wait_flags + f) == 1ull)) {
                     __nanosleep(128);
-                    if (globaltimer_ns() - t_start > 4000000000ull) {
+                    if (globaltimer_ns() - t_start > kWaitTimeoutNs) {
                         if (lane == 0) printf("lora K3: coefficient flag wait timed out (set %d)\n", J.set0 + j);
                         __trap();
                     }

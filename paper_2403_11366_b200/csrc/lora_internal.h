@@ -11,6 +11,11 @@ lora_status fail(lora_status st, const char* fmt, ...);
 lora_status cuda_fail(cudaError_t e, const char* what);
 lora_status check_dims(const lora_dims* d, bool need_tokens);
 void set_launches(int n);
+void prof_record(int i, cudaStream_t stream);   // lora_profile_next_bwd events
+void prof_clear();
+struct ProfGuard {   // one-shot lora_profile_next_bwd events end with the public call
+    ~ProfGuard() { prof_clear(); }
+};
 int get_launches();
 
 // lora_linear_bwd_grouped with a hook run right after the grouped dX kernel is
@@ -39,7 +44,10 @@ struct GemmCollector {
 lora_status fwd_impl(const lora_dims* d, const void* x, const void* w0, const void* a, const void* b,
                      const void* bias, void* y, float* h_out, void* ws, size_t ws_bytes,
                      cudaStream_t stream, int* launches, GemmCollector* col = nullptr,
-                     const lora_sm100::DropoutParams* drop = nullptr);
+                     const lora_sm100::DropoutParams* drop = nullptr, bool validate_only = false);
+// bwd stage bit 2: validate the arguments only (the grouped calls check every
+// problem before enqueueing anything); accumulate is a lora_sm100::kAccA | kAccB mask
+constexpr int kStageValidate = 4;
 lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const void* a, const void* b,
                      const float* h_saved, const void* dy, void* dx, float* da, float* db, int accumulate,
                      void* ws, size_t ws_bytes, cudaStream_t stream, int* launches,

@@ -97,9 +97,13 @@ size_t fused_gemm_partial_bytes(int64_t T, int64_t N_out);
 // uses it returns its words to zero before its launch chain ends (the last
 // consumer resets), so no host memset is needed and captured CUDA graphs
 // replay correctly.  Eager calls take words from a recycled ring; calls made
-// while `stream` is capturing get words of their own for the graph's lifetime.
+// while `stream` is capturing get words of their own, owned by the capturing
+// graph (a cudaUserObject returns them when the graph is destroyed).
 // Returns null when the pool is exhausted (capture) or on a CUDA error.
 unsigned long long* sync_pool_alloc(int words, cudaStream_t stream);
+// words of the captured-graph region currently free on device `dev` (a graph's
+// words return when the graph and its executables are destroyed)
+int sync_pool_captured_free_words(int dev);
 
 // K1 / K2.  r_pad in {16, 32, 64}; tiles are (128 * cta_group) x (256 - r_pad).
 // cta_group = 2 runs on CTA pairs (tcgen05 cta_group::2); the TMA boxes of
@@ -124,6 +128,8 @@ cudaError_t launch_pack_b(const __nv_bfloat16* b, int64_t m, int r, __nv_bfloat1
 
 
 
+enum : int { kAccA = 1, kAccB = 2 };   // GradArgs::accumulate bits
+
 struct GradArgs {
     const __nv_bfloat16* x;   // [T, n]
     const float* gh;          // [T, r]   (dA coefficients, already scaled by s)
@@ -134,11 +140,14 @@ struct GradArgs {
     int64_t T, n, m;
     int r;
     float scale_b;            // s
-    int accumulate;
+    int accumulate;           // bit mask: kAccA adds into da, kAccB adds into db (else overwrite)
     __nv_bfloat16* cs_a;      // tensor-core K3: split gh [3 r8, T_pad] (workspace)
     __nv_bfloat16* cs_b;      // tensor-core K3: split h  [3 r8, T_pad] (workspace)
     float scale_a;            // dA multiplier (1, or q = 1/(1-p) when x is the dropout-masked M . x)
-    int cs_a_ready, cs_b_ready;   // split already written by K2 (no K3s work for that set)
+    int cs_a_ready, cs_b_ready;   // split already written (by K2 or a row projection): no K3s work for that set
+    int cs_a_k2, cs_b_k2;         // ... written by THIS backward's K2, which raises k2_flags per row block
+                                  // (only those sets wait on the flags; a row projection's split is
+                                  // ordered by the stream and K2 may already have reset its flags)
     const uint64_t* k2_flags;     // K2's per-row-block flags (value 1 once cs_* are written), or null
     int k2_nflags;
 };

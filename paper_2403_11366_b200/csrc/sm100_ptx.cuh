@@ -65,8 +65,16 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
+// Every spin wait (mbarrier phases, cross-CTA / cross-kernel flags) gives up
+// after kWaitTimeoutNs and traps instead of hanging the GPU forever.  The
+// launches whose CTAs wait on other CTAs' flags are cooperative (all CTAs
+// co-resident), so a legitimate wait is bounded by the producer's own work --
+// microseconds to milliseconds -- even when other streams' kernels (e.g. an
+// NCCL collective waiting on a slow peer) hold SMs; 20 s only fires on a bug.
+constexpr uint64_t kWaitTimeoutNs = 20000000000ull;
+
 // Blocking wait on the phase with parity `parity`.  A barrier that never
-// completes (a pipeline bug) traps after ~4 s instead of hanging the GPU.
+// completes (a pipeline bug) traps after kWaitTimeoutNs instead of hanging.
 // kCluster: acquire at cluster scope (the barrier receives arrivals from the
 // peer CTA of a 2-CTA pair).
 template <bool kCluster = false>
@@ -76,7 +84,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     if (probe()) return;
     const uint64_t t0 = globaltimer_ns();
     while (!probe()) {
-        if (globaltimer_ns() - t0 > 4000000000ull) {
+        if (globaltimer_ns() - t0 > kWaitTimeoutNs) {
             printf("lora kernel: mbarrier wait timed out (block %d thread %d parity %u)\n",
                    blockIdx.x, threadIdx.x, parity);
             __trap();

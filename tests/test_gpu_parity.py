@@ -520,3 +520,113 @@ def test_sync_pool_ring_wraps(oracle_mod, L):
                        ref_dx_only[0])
     go = oracle_mod.lora_bwd(d["x"], d["w0"], d["a"], d["b"], d["dy"], 16.0)
     assert relF(host_f64(outs[0]), go["dx"]) <= TOL_OUT
+
+
+@pytest.mark.parametrize("r", [8, 16, 6])
+def test_dx_and_db_without_da_recomputed_h(oracle_mod, L, r):
+    """dX and dB requested, dA not, h recomputed (h_saved = NULL): K2 does not
+    write a split K3 waits on (the h split comes from the row projection after
+    K2), so K3 must not wait on K2's flags (this combination used to
+    wait on flags K2 had already reset and trap).  Eager and grouped."""
+    T, n, m = 512, 256, 384
+    d = make_lora_inputs(T, n, m, r, seed=95 + r)
+    x, w0, a, b, dy = (dev_bf16(d[k]) for k in ("x", "w0", "a", "b", "dy"))
+    dx, da, db = L.lora_linear_bwd(x, w0, a, b, dy, 16.0, h_saved=None, want_da=False)
+    res = L.lora_linear_bwd_grouped([(x, w0, a, b, dy, None)], [16.0], want_da=False)
+    torch.cuda.synchronize()
+    go = oracle_mod.lora_bwd(d["x"], d["w0"], d["a"], d["b"], d["dy"], 16.0)
+    assert da is None
+    assert relF(host_f64(dx), go["dx"]) <= TOL_OUT
+    assert relF(host_f64(db), go["db"]) <= TOL_GRAD
+    assert res[0][1] is None
+    assert relF(host_f64(res[0][2]), go["db"]) <= TOL_GRAD
+    assert relF(host_f64(res[0][0]), go["dx"]) <= TOL_OUT
+    # and dA alone, dB alone, with and without dX, h saved or not
+    _, h = L.lora_linear_fwd(x, w0, a, b, 16.0)
+    for hs in (None, h):
+        for want_dx in (True, False):
+            for wa, wb in ((True, False), (False, True)):
+                o = L.lora_linear_bwd(x, w0, a, b, dy, 16.0, h_saved=hs, want_dx=want_dx, want_da=wa, want_db=wb)
+                torch.cuda.synchronize()
+                if wa:
+                    assert relF(host_f64(o[1]), go["da"]) <= TOL_GRAD
+                if wb:
+                    assert relF(host_f64(o[2]), go["db"]) <= TOL_GRAD
+                if want_dx:
+                    assert relF(host_f64(o[0]), go["dx"]) <= TOL_OUT
+
+
+def test_grouped_validates_every_problem_before_launch(L):
+    """A grouped call whose LAST problem is invalid returns the error with nothing
+    enqueued: no launch counted and the first problem's outputs untouched."""
+    d = make_lora_inputs(256, 128, 128, 8, seed=97)
+    x, w0, a, b, dy = (dev_bf16(d[k]) for k in ("x", "w0", "a", "b", "dy"))
+    y0 = torch.full((256, 128), 7.0, dtype=torch.bfloat16, device="cuda")
+    bad_x = torch.empty((256, 128), dtype=torch.bfloat16, device="cuda")[:, 1:].contiguous()   # shape check
+    with pytest.raises(ValueError):
+        L.lora_linear_fwd_grouped([(x, w0, a, b, None), (bad_x, w0, a, b, None)], [16.0, 16.0])
+    # misaligned pointer for problem 1 (passes the binding's checks, fails in the library)
+    big = torch.empty(256 * 128 + 8, dtype=torch.bfloat16, device="cuda")
+    x_mis = big[1:1 + 256 * 128].view(256, 128)
+    with pytest.raises(L.LoraError) as ei:
+        L.lora_linear_fwd_grouped([(x, w0, a, b, None), (x_mis, w0, a, b, None)], [16.0, 16.0],
+                                  outs=[(y0, None), (None, None)])
+    assert "ALIGN" in str(ei.value)
+    assert L.lora_last_launch_count() == 0
+    torch.cuda.synchronize()
+    assert torch.all(y0 == 7.0)
+    dx0 = torch.full((256, 128), 7.0, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(L.LoraError):
+        L.lora_linear_bwd_grouped([(x, w0, a, b, dy, None), (x_mis, w0, a, b, dy, None)], [16.0, 16.0],
+                                  outs=[(dx0, None, None), (None, None, None)])
+    assert L.lora_last_launch_count() == 0
+    torch.cuda.synchronize()
+    assert torch.all(dx0 == 7.0)
+
+
+def test_captured_sync_words_return_with_the_graph(L):
+    """Sync-pool words taken during graph capture belong to the graph and come back
+    when it is destroyed: capturing and dropping more graphs than the
+    region could hold at once (10000 x 16 words > 131072) keeps working, every
+    replay gives the eager result, and the free count returns to its start value."""
+    import gc
+    T, n, m, r = 256, 128, 256, 8
+    d = make_lora_inputs(T, n, m, r, seed=99)
+    x, w0, a, b, dy = (dev_bf16(d[k]) for k in ("x", "w0", "a", "b", "dy"))
+    y, h = L.lora_linear_fwd(x, w0, a, b, 16.0)
+    ref = L.lora_linear_bwd(x, w0, a, b, dy, 16.0, h_saved=h)
+    outs = [torch.empty_like(t) for t in ref]
+    ws = torch.empty(1 << 22, dtype=torch.uint8, device="cuda")
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        L.lora_linear_bwd(x, w0, a, b, dy, 16.0, h_saved=h, dx=outs[0], da=outs[1], db=outs[2], workspace=ws,
+                          stream=s)
+    torch.cuda.synchronize()
+    free0 = L.lora_captured_sync_words_free()
+    assert free0 > 0
+    for i in range(10000):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            L.lora_linear_bwd(x, w0, a, b, dy, 16.0, h_saved=h, dx=outs[0], da=outs[1], db=outs[2], workspace=ws,
+                              stream=s)
+        assert L.lora_captured_sync_words_free() < free0
+        if i % 2500 == 0:
+            for t in outs:
+                t.zero_()
+            g.replay()
+            torch.cuda.synchronize()
+            for u, v in zip(outs, ref):
+                assert torch.equal(u, v)
+        del g
+        if i % 500 == 499:
+            gc.collect()
+            torch.cuda.synchronize()
+    gc.collect()
+    torch.cuda.synchronize()
+    import time
+    for _ in range(100):   # the runtime runs user-object destructors asynchronously
+        if L.lora_captured_sync_words_free() == free0:
+            break
+        time.sleep(0.05)
+    assert L.lora_captured_sync_words_free() == free0
