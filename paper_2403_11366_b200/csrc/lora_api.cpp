@@ -296,6 +296,7 @@ lora_status fwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
     p.drop = DropoutParams{};
     p.drop_bits = nullptr;
     p.cs_gh = p.cs_h = nullptr;
+    p.cs_gh_rows = 0;
     p.h_split_src = nullptr;
     p.t_pad = 0;
     p.sk_partial = W.partial_bytes ? reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + W.partial) : nullptr;
@@ -624,7 +625,6 @@ lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
         p.bias = nullptr;
         p.out = static_cast<__nv_bfloat16*>(dx);
         p.side_out = nullptr;
-        p.gh = gh;
         p.epoch = kFlagSet;
         p.nflags = static_cast<int>(fused_gemm_row_blocks(T, cg) * cg);
         p.flags = p.nflags > 0 ? reinterpret_cast<uint64_t*>(sync_pool_alloc(p.nflags, stream)) : nullptr;
@@ -642,7 +642,11 @@ lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
         // the gh tile also writes K3's split coefficients (gh; h when it already exists)
         p.t_pad = t_pad_of(T);
         p.sk_partial = W.partial_bytes ? reinterpret_cast<float*>(wsb + W.partial) : nullptr;
-        p.cs_gh = da ? reinterpret_cast<__nv_bfloat16*>(wsb + W.cs_a) : nullptr;
+        // the gh tile publishes gh to the other tiles through cs_a (hi rows; the full
+        // split when dA -- or the dropout epilogue's fp32 gh -- needs it)
+        p.cs_gh = reinterpret_cast<__nv_bfloat16*>(wsb + W.cs_a);
+        p.cs_gh_rows = (da || dropping) ? 3 : 1;
+        p.gh = k3_mode() == kK3Cluster ? gh : nullptr;   // fp32 gh: only the CUDA-core K3 reads it
         p.h_split_src = h_saved ? h_saved : (dropping && need_h ? hbuf : nullptr);
         p.cs_h = db && p.h_split_src ? reinterpret_cast<__nv_bfloat16*>(wsb + W.cs_b) : nullptr;
         if (col) {

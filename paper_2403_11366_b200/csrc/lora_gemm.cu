@@ -226,6 +226,82 @@ __device__ __forceinline__ TileRef decode_tile(const FusedGemmGroup& grp, int ti
     return t;
 }
 
+// Rank-r rows of a row-major fp32 [T, r] array (h saved by the forward) for the
+// 32 token rows row0 .. row0+31 of a warp: lane L receives row row0+L.  A plain
+// per-lane row read strides the warp by 4r bytes (one sector per value); here the
+// warp reads its 32 r contiguous floats with coalesced 16-byte loads (r % 4 == 0,
+// r <= 16: at most 4 rounds) and transposes them with shuffles -- the register
+// component (j % 4) is uniform across lanes, only the source lane and round vary.
+template <int R_PAD>
+__device__ __forceinline__ void warp_load_rows(const float* base, int64_t row0, int64_t T, int r, uint32_t lane,
+                                               float (&hv)[R_PAD]) {
+    if (r % 4 == 0 && r <= 16) {
+        const int64_t nvalid = (T - row0) * r;   // floats of this warp block inside the array
+        const float4* b4 = reinterpret_cast<const float4*>(base + row0 * r);
+        float4 v[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int64_t idx = lane + 32 * i;
+            v[i] = (i < r / 4 && idx * 4 < nvalid) ? b4[idx] : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int j = 0; j < R_PAD; ++j) {
+            if (j >= 16) { hv[j] = 0.0f; continue; }
+            const int f4 = static_cast<int>(lane) * (r / 4) + j / 4;
+            const int src = f4 & 31, rnd = f4 >> 5;
+            float val = 0.0f;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                if (i >= r / 4) break;   // (warp-uniform)
+                const float c = (j & 3) == 0 ? v[i].x : (j & 3) == 1 ? v[i].y : (j & 3) == 2 ? v[i].z : v[i].w;
+                const float t = __shfl_sync(0xffffffffu, c, src);
+                if (rnd == i) val = t;
+            }
+            hv[j] = j < r ? val : 0.0f;
+        }
+        return;
+    }
+    const int64_t row = row0 + lane;
+#pragma unroll
+    for (int j = 0; j < R_PAD; ++j) hv[j] = (j < r && row < T) ? base[row * r + j] : 0.0f;
+}
+// The transpose of warp_load_rows: lane L holds row row0+L's values; the warp
+// stores its 32 r floats with coalesced 16-byte stores (r % 4 == 0, r <= 16).
+template <int R_PAD>
+__device__ __forceinline__ void warp_store_rows(float* base, int64_t row0, int64_t T, int r, uint32_t lane,
+                                                const float (&hv)[R_PAD]) {
+    if (r % 4 == 0 && r <= 16) {
+        const int64_t nvalid = (T - row0) * r;
+        float4* b4 = reinterpret_cast<float4*>(base + row0 * r);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            if (i >= r / 4) break;   // (warp-uniform)
+            const int q = static_cast<int>(lane) + 32 * i;   // float4 index in the warp block
+            const int srow = (4 * q) / r, g = ((4 * q) % r) / 4;   // source lane, column group
+            float o[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                float val = 0.0f;
+#pragma unroll
+                for (int gg = 0; gg < 4; ++gg) {
+                    if (4 * gg + c >= R_PAD || gg >= r / 4) break;
+                    const float t = __shfl_sync(0xffffffffu, hv[4 * gg + c], srow);
+                    if (g == gg) val = t;
+                }
+                o[c] = val;
+            }
+            if (static_cast<int64_t>(q) * 4 < nvalid) b4[q] = make_float4(o[0], o[1], o[2], o[3]);
+        }
+        return;
+    }
+    const int64_t row = row0 + lane;
+    if (row < T) {
+#pragma unroll
+        for (int j = 0; j < R_PAD; ++j)
+            if (j < r) base[row * r + j] = hv[j];
+    }
+}
+
 #ifdef LORA_PROBE_SK
 __device__ unsigned int g_probe_n;
 __device__ unsigned long long g_probe_buf[4 * 4096];
@@ -714,14 +790,10 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
 #pragma unroll
                     for (int j = 0; j < R_PAD; ++j) hv[j] *= p.scale;     // gh = s (dY B)
                 }
-                // (2) side output: fwd h (for dB); dx gh (for the other tiles and for dA)
+                // (2) side output: fwd h (for dB); dx fp32 gh only for the CUDA-core K3
                 float* side = (MODE == kModeFwd) ? p.side_out : p.gh;
-                if (side != nullptr && (MODE != kModeFwd || n_blk == 0) && row < p.T) {
-                    float* dst = side + row * p.r;
-#pragma unroll
-                    for (int j = 0; j < R_PAD; ++j)
-                        if (j < p.r) dst[j] = hv[j];
-                }
+                if (side != nullptr && (MODE != kModeFwd || n_blk == 0))   // (warp-uniform)
+                    warp_store_rows<R_PAD>(side, row - lane, p.T, p.r, lane, hv);
                 if (MODE != kModeFwd && row < p.T) {
                     // K3's B operand: exact hi / mid / lo bf16 split of gh (and of the saved h),
                     // token-contiguous rows of cs [3 r8, t_pad] (saves K3s a pass)
@@ -736,13 +808,34 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
                         cs[static_cast<int64_t>(2 * r8 + k) * p.t_pad + row] = lo;
                     };
                     if (p.cs_gh != nullptr) {
+                        if (p.cs_gh_rows == 3) {
 #pragma unroll
-                        for (int k = 0; k < R_PAD; ++k)
-                            if (k < r8) split_store(p.cs_gh, k, k < p.r ? hv[k] : 0.0f);
+                            for (int k = 0; k < R_PAD; ++k)
+                                if (k < r8) split_store(p.cs_gh, k, k < p.r ? hv[k] : 0.0f);
+                        } else {   // hi = bf16(gh) only: what the other tiles' tail MMA needs
+#pragma unroll
+                            for (int k = 0; k < R_PAD; ++k)
+                                if (k < p.r) p.cs_gh[static_cast<int64_t>(k) * p.t_pad + row] = __float2bfloat16_rn(hv[k]);
+                        }
                     }
-                    if (p.cs_h != nullptr) {
-                        const float* hs = p.h_split_src + row * p.r;
-                        for (int k = 0; k < r8; ++k) split_store(p.cs_h, k, k < p.r ? hs[k] : 0.0f);
+                }
+                if (MODE != kModeFwd && p.cs_h != nullptr) {   // (warp-uniform; rows >= T read as 0)
+                    float hs[R_PAD];
+                    warp_load_rows<R_PAD>(p.h_split_src, row - lane, p.T, p.r, lane, hs);
+                    if (row < p.T) {
+                        const int r8 = (p.r + 7) / 8 * 8;
+#pragma unroll
+                        for (int k = 0; k < R_PAD; ++k) {
+                            if (k >= r8) break;
+                            const float v = hs[k];
+                            const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+                            const float r0 = v - __bfloat162float(hi);
+                            const __nv_bfloat16 md = __float2bfloat16_rn(r0);
+                            const __nv_bfloat16 lo = __float2bfloat16_rn(r0 - __bfloat162float(md));
+                            p.cs_h[static_cast<int64_t>(k) * p.t_pad + row] = hi;
+                            p.cs_h[static_cast<int64_t>(r8 + k) * p.t_pad + row] = md;
+                            p.cs_h[static_cast<int64_t>(2 * r8 + k) * p.t_pad + row] = lo;
+                        }
                     }
                 }
                 if (MODE != kModeFwd) {
@@ -765,9 +858,22 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
                         }
                     }
                 }
-                const float* src = p.gh + row * p.r;
+                // gh of this row from the gh tile's token-contiguous split rows: one coalesced
+                // 64-byte load per rank index per warp (bf16(gh) = hi; dropout: hi + mid + lo,
+                // exactly the fp32 gh)
+                const int r8 = (p.r + 7) / 8 * 8;
 #pragma unroll
-                for (int j = 0; j < R_PAD; ++j) hv[j] = (j < p.r && row < p.T) ? src[j] : 0.0f;
+                for (int j = 0; j < R_PAD; ++j) {
+                    float v = 0.0f;
+                    if (j < p.r && row < p.T) {
+                        const __nv_bfloat16* c = p.cs_gh + static_cast<int64_t>(j) * p.t_pad + row;
+                        v = __bfloat162float(c[0]);
+                        if (MODE == kModeDxDrop)
+                            v = (v + __bfloat162float(c[static_cast<int64_t>(r8) * p.t_pad])) +
+                                __bfloat162float(c[static_cast<int64_t>(2 * r8) * p.t_pad]);
+                    }
+                    hv[j] = v;
+                }
             }
             if constexpr (MODE == kModeDxDrop) {
                 // dropout: no tail MMA -- the epilogue adds q M . (gh A) itself (step 5)

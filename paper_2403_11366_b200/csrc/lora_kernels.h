@@ -31,7 +31,7 @@ struct FusedGemmParams {
     const __nv_bfloat16* bias;    // fwd only; may be null
     __nv_bfloat16* out;           // y or dx, [T, N_out]
     float* side_out;              // fwd: h [T, r] (unscaled), may be null
-    float* gh;                    // dx: gh [T, r] = s dY B, written by the first column tile
+    float* gh;                    // dx: gh [T, r] fp32 = s dY B for the CUDA-core K3 (LORA_K3=cluster), or null
     uint64_t* flags;              // dx: one per (row block, CTA of the pair), sync pool: 1 = gh published
     uint64_t epoch;               // dx: value a published flag holds (1)
     int nflags;                   // dx: row blocks x CTAs per pair
@@ -40,8 +40,13 @@ struct FusedGemmParams {
     DropoutParams drop;           // dx dropout mode: dX += q M . (gh A) in the epilogue
     const uint32_t* drop_bits;    // dx dropout mode: keep bits [T, ceil(N_out/32)] from K0
     // dx: K3's split coefficients written by the gh tile (else null): cs_gh <- gh,
-    // cs_h <- h_split_src; [3 r8, t_pad] bf16 hi / mid / lo rows (see K3s)
+    // cs_h <- h_split_src; [3 r8, t_pad] bf16 hi / mid / lo rows (see K3s).
+    // cs_gh is also how the other column tiles of a row block read gh: token-
+    // contiguous rows, so a warp's 32 rows are one coalesced 64-byte load per rank
+    // index.  cs_gh_rows = 1 writes only hi = bf16(gh) (all the tail MMA needs),
+    // 3 the full split (dA wants it; dropout mode rebuilds fp32 gh = hi + mid + lo).
     __nv_bfloat16* cs_gh;
+    int cs_gh_rows;
     __nv_bfloat16* cs_h;
     const float* h_split_src;
     int64_t t_pad;
