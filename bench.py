@@ -777,11 +777,25 @@ def run_ours(args, wl):
         merge_bytes = 4 * m0 * n0 + 2 * r0 * (m0 + n0)
         # dY read twice (gh pre-pass, dB), x once, coefficients ~ 16 T r
         grads_bytes = 2 * T0 * (2 * m0 + n0) + 16 * T0 * r0
-        aux = {"merge": {"us": t_merge * 1e6, "bytes": merge_bytes, "gbs": merge_bytes / t_merge / 1e9},
+        # the achievable HBM rate at each kernel's size: a plain device copy (torch copy_)
+        # moving the same bytes (half read, half written), timed the same way -- MEASURED_PEAKS'
+        # hbm_gbs is a 2 GiB copy; at tens of MB the launch ramp and drain cost a few us
+        cp_src = torch.empty(max(merge_bytes, grads_bytes) // 4 + 64, dtype=torch.float16, device=dev)
+        cp_dst = torch.empty_like(cp_src)
+
+        def copy_ref(nbytes):
+            k = nbytes // 4
+            t = timed(lambda: cp_dst[:k].copy_(cp_src[:k]))
+            return {"us": t * 1e6, "gbs": 4 * k / t / 1e9}
+
+        aux = {"merge": {"us": t_merge * 1e6, "bytes": merge_bytes, "gbs": merge_bytes / t_merge / 1e9,
+                         "engine": "tcgen05 (B A in TMEM) + TMA load / store" if r0 % 8 == 0 and r0 <= 64
+                         else "CUDA cores", "same_bytes_copy": copy_ref(merge_bytes)},
                "adam_all_adapters": {"us": t_adam * 1e6, "bytes": adam_bytes, "gbs": adam_bytes / t_adam / 1e9,
                                      "tensors": len(ad)},
                "grads_only": {"us": t_grads * 1e6, "bytes": grads_bytes, "gbs": grads_bytes / t_grads / 1e9,
-                              "kernels": "lora_linear_bwd with dx = NULL (gh row projection, K3)"}}
+                              "kernels": "lora_linear_bwd with dx = NULL (gh row projection, K3)",
+                              "same_bytes_copy": copy_ref(grads_bytes)}}
 
     # ---- report (rank 0)
     if rank == 0:
@@ -868,6 +882,8 @@ def run_ours(args, wl):
         if aux:
             for v in aux.values():
                 v["frac_of_hbm"] = v["gbs"] / hbm
+                if "same_bytes_copy" in v:
+                    v["frac_of_same_bytes_copy"] = v["gbs"] / v["same_bytes_copy"]["gbs"]
             line["hbm_bound_kernels"] = dict(aux, hbm_peak_gbs=hbm, linear=l0.name)
         print(json.dumps(line), flush=True)
     if comm is not None:

@@ -18,7 +18,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "liblora.so")
-SOURCES = ["lora_gemm.cu", "lora_grad.cu", "lora_grad_mma.cu", "lora_dropout.cu", "lora_aux.cu", "lora_api.cpp", "lora_comm.cpp"]
+SOURCES = ["lora_gemm.cu", "lora_grad.cu", "lora_grad_mma.cu", "lora_dropout.cu", "lora_aux.cu", "lora_merge_mma.cu", "lora_api.cpp", "lora_comm.cpp"]
 HEADERS = ["sm100_ptx.cuh", "lora_philox.cuh", "lora_kernels.h", "lora_internal.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -59,17 +59,36 @@ def _stale() -> bool:
 
 def build(force: bool = False, verbose: bool = False, out: str | None = None,
           defines: tuple = ()) -> str:
-    """Build liblora.so (or, with `out`/`defines`, an experiment variant)."""
+    """Build liblora.so (or, with `out`/`defines`, an experiment variant).
+
+    Each source is compiled to an object in parallel (one nvcc per file), then
+    linked; the objects live in a per-process scratch directory next to the
+    library so concurrent builders never share a partial file."""
+    import shutil
+    import tempfile
+    from concurrent.futures import ThreadPoolExecutor
+
     target = out or LIB
     if out is None and not force and not _stale():
         return LIB
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-    cmd = [nvcc, *ARCH, "-O3", "-std=c++17", "-lineinfo", "-shared", "-Xcompiler", "-fPIC",
-           "-Xptxas", "-v" if verbose else "-O3",
-           "-I", INCLUDE, "-I", CSRC, "-I", _nccl_include(),
-           "-DLORA_BUILD", *[f"-D{d}" for d in defines], "-o", f"{target}.tmp{os.getpid()}",
-           *[os.path.join(CSRC, f) for f in SOURCES], "-ldl", "-lpthread"]
-    subprocess.check_call(cmd)
+    flags = [*ARCH, "-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC",
+             "-Xptxas", "-v" if verbose else "-O3",
+             "-I", INCLUDE, "-I", CSRC, "-I", _nccl_include(),
+             "-DLORA_BUILD", *[f"-D{d}" for d in defines]]
+    tmp = tempfile.mkdtemp(prefix=".build", dir=PKG)
+    try:
+        objs = [os.path.join(tmp, f + ".o") for f in SOURCES]
+
+        def compile_one(i):
+            subprocess.check_call([nvcc, *flags, "-c", "-o", objs[i], os.path.join(CSRC, SOURCES[i])])
+
+        with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 4)) as ex:
+            list(ex.map(compile_one, range(len(SOURCES))))
+        subprocess.check_call([nvcc, *ARCH, "-shared", "-o", f"{target}.tmp{os.getpid()}", *objs,
+                               "-ldl", "-lpthread"])
+    finally:
+        shutil.rmtree(tmp, ignore_errors=True)
     os.replace(f"{target}.tmp{os.getpid()}", target)   # atomic: concurrent builders never see a partial file
     return target
 

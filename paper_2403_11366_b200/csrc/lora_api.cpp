@@ -749,6 +749,21 @@ lora_status merge_impl(const lora_dims* d, const void* w0, const void* a, const 
         return fail(LORA_ERR_INVALID, "lora_merge: w_out overlaps a or b");
     DevInfo dev;
     if ((st = device_info(&dev)) != LORA_OK) return st;
+    const float s = d->alpha / static_cast<float>(r);
+    const char* mv = getenv("LORA_MERGE");
+    if (r % 8 == 0 && r <= 64 && !(mv && (!strcmp(mv, "cuda") || !strcmp(mv, "oneshot")))) {
+        // tensor cores (lora_merge_mma.cu): B's rows are 16-byte multiples, so B is a TMA operand as is
+        const int rp = r <= 16 ? 16 : (r <= 32 ? 32 : 64);
+        MergeMaps maps;
+        if ((st = encode_2d(&maps.w, w0, n, m, n * 2, 64, 128, 128, "w0")) != LORA_OK) return st;
+        if ((st = encode_2d(&maps.out, w_out, n, m, n * 2, 64, 128, 128, "w_out")) != LORA_OK) return st;
+        if ((st = encode_2d(&maps.b, b, r, m, r * 2, rp, 128, rp * 2, "b")) != LORA_OK) return st;
+        if ((st = encode_2d(&maps.a, a, n, r, n * 2, 64, rp, 128, "a")) != LORA_OK) return st;
+        cudaError_t e = launch_merge_mma(maps, rp, m, n, s, dev.sms, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "merge launch");
+        ++*launches;
+        return LORA_OK;
+    }
     cudaError_t e = launch_merge(static_cast<const __nv_bfloat16*>(w0), static_cast<const __nv_bfloat16*>(a),
                                  static_cast<const __nv_bfloat16*>(b), n, m, r, d->alpha / static_cast<float>(r),
                                  static_cast<__nv_bfloat16*>(w_out), stream);

@@ -245,6 +245,15 @@ cudaError_t launch_merge(const __nv_bfloat16* w0, const __nv_bfloat16* a, const 
                          int64_t n, int64_t m, int r, float scale, __nv_bfloat16* w_out,
                          cudaStream_t stream);
 
+// K4 on the tensor cores (lora_merge_mma.cu; r % 8 == 0, r <= 64): TMA maps of
+// W0 [m, n] and W' [m, n] (box 64 x 128, SW128), B [m, r] (box r_pad x 128,
+// swizzle 2 r_pad bytes), A [r, n] (box 64 x r_pad, SW128)
+struct MergeMaps {
+    CUtensorMap w, out, b, a;
+};
+cudaError_t launch_merge_mma(const MergeMaps& maps, int r_pad, int64_t m, int64_t n, float s, int num_sms,
+                             cudaStream_t stream);
+
 // N3: one Adam step for up to kMaxAdamTensors adapter tensors (numel % 4 == 0)
 constexpr int kMaxAdamTensors = 64;
 struct AdamTensor {

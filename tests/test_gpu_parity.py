@@ -336,7 +336,10 @@ def test_grouped_launch_count(L):
 
 
 # ------------------------------------------------------------------ merge
-@pytest.mark.parametrize("shape", [(64, 64, 4), (4096, 4096, 8), (1000, 520, 33)])
+# (n, m, r): r % 8 == 0 and r <= 64 run on the tensor cores (lora_merge_mma.cu,
+# r_pad 16 / 32 / 64, ragged row and column tiles), the rest on the CUDA cores
+@pytest.mark.parametrize("shape", [(64, 64, 4), (4096, 4096, 8), (1000, 520, 33), (520, 1000, 16),
+                                   (256, 384, 24), (384, 200, 64), (1024, 8192, 16), (8, 8, 8)])
 def test_merge_matches_oracle(oracle_mod, L, shape):
     """lora_merge = RNE_bf16(W0 + s B A) (Eq. 1 line 2): >= 99.9% of elements
     bit-equal to the rounded fp64 oracle, the rest within one bf16 ulp."""
