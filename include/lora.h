@@ -294,6 +294,59 @@ lora_status lora_tp_linear_bwd_column_group(lora_comm* comm, int count, const lo
                                             int reduce_lora_grads, void* workspace, size_t workspace_bytes,
                                             void* stream);
 
+/* ---------------- Comm-fused epilogues over peer memory ----
+ * PAPER.md:199 blames the multi-GPU slowdown on "cross-GPU communication
+ * overhead"; these calls fuse the two activation all-reduces of the TP linear
+ * with the GEMM that produces them.  Each rank's fused GEMM writes its partial
+ * output into a SYMMETRIC buffer and publishes every 128-row tile half as soon as
+ * it is stored; a reducer kernel on a side stream (forked from and joined back to
+ * `stream`) sums each published unit it owns (unit u -> rank u % N) over ranks
+ * (and group members) in fp32, in rank order, rounds once to bf16 and stores it
+ * into EVERY rank's output region with peer stores, while the GEMM computes
+ * the next tiles.  All ranks end with bitwise identical results.
+ *
+ * lora_symm: one per rank, created with the same data_bytes everywhere
+ * (device memory allocated by the library: [256 KiB control | data]); peers
+ * are mapped with CUDA IPC (lora_symm_ipc_handle on every rank, all-gather the
+ * handles, lora_symm_connect) or, to run the protocol on ONE GPU,
+ * lora_symm_connect_local joins N buffers of this process as N virtual ranks
+ * (each call then runs on its own stream).  Regions are given as byte offsets
+ * into the data region (lora_symm_ptr): 16-byte aligned, inside it, disjoint.
+ * One fused call at a time per lora_symm (calls on one stream are ordered).
+ * The output region holds the result until the next fused call that writes it.
+ * Errors: LORA_ERR_INVALID (not connected, wrong device, overlap),
+ * LORA_ERR_SHAPE (region outside the buffer), LORA_ERR_ALIGN, LORA_ERR_CUDA. */
+typedef struct lora_symm lora_symm;
+#define LORA_SYMM_HANDLE_BYTES 64
+lora_status lora_symm_create(size_t data_bytes, lora_symm** out);
+lora_status lora_symm_ipc_handle(const lora_symm* symm, uint8_t handle[LORA_SYMM_HANDLE_BYTES]);
+/* handles: nranks x LORA_SYMM_HANDLE_BYTES, rank order (this rank's own is ignored). */
+lora_status lora_symm_connect(lora_symm* symm, int nranks, int rank, const uint8_t* handles);
+lora_status lora_symm_connect_local(int nranks, lora_symm* const* group);
+void* lora_symm_ptr(const lora_symm* symm);        /* this rank's data region (device) */
+size_t lora_symm_bytes(const lora_symm* symm);
+lora_status lora_symm_destroy(lora_symm* symm);
+
+/* ROW-parallel forward (o, down) with the y all-reduce fused into the GEMM:
+ * the partial x_i W0_i^T + s (x_i A_i^T) B^T (+ bias on rank 0) goes to
+ * [part_offset, + T d_out 2) of the data region, the reduced y [T, d_out] bf16
+ * to [y_offset, ...) on every rank.  Other arguments as lora_tp_linear_fwd. */
+lora_status lora_tp_linear_fwd_fused(lora_symm* symm, const lora_dims* local, const void* x, const void* w0,
+                                     const void* a, const void* b, const void* bias, size_t part_offset,
+                                     size_t y_offset, float* h_out, void* workspace, size_t workspace_bytes,
+                                     void* stream);
+/* COLUMN-parallel group backward (q/k/v, gate/up sharing x) with the dX
+ * all-reduce fused into the grouped dX GEMM: member g's partial goes to
+ * [part_offset + g T d_in 2, ...), the gradient w.r.t. the shared input,
+ * sum over ranks and members, to [dx_offset, + T d_in 2) on every rank.
+ * problems[g].dx must be NULL.  dA partials are all-reduced over `comm` (NCCL)
+ * when reduce_lora_grads (comm may be NULL otherwise); dB stays local.
+ * Workspace: lora_linear_bwd_grouped_workspace_bytes. */
+lora_status lora_tp_linear_bwd_column_group_fused(lora_symm* symm, lora_comm* comm, int count,
+                                                  const lora_dims* local, const lora_bwd_problem* problems,
+                                                  size_t part_offset, size_t dx_offset, int reduce_lora_grads,
+                                                  void* workspace, size_t workspace_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -144,6 +144,29 @@ lib.lora_tp_linear_bwd_column_group.argtypes = [_vp, ctypes.c_int, _dp, ctypes.P
                                                 ctypes.c_int, ctypes.c_int, _vp, ctypes.c_size_t, _vp]
 lib.lora_tp_linear_bwd_column_group.restype = _st
 
+LORA_SYMM_HANDLE_BYTES = 64
+lib.lora_symm_create.argtypes = [ctypes.c_size_t, ctypes.POINTER(_vp)]
+lib.lora_symm_create.restype = _st
+lib.lora_symm_ipc_handle.argtypes = [_vp, ctypes.c_char_p]
+lib.lora_symm_ipc_handle.restype = _st
+lib.lora_symm_connect.argtypes = [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_char_p]
+lib.lora_symm_connect.restype = _st
+lib.lora_symm_connect_local.argtypes = [ctypes.c_int, ctypes.POINTER(_vp)]
+lib.lora_symm_connect_local.restype = _st
+lib.lora_symm_ptr.argtypes = [_vp]
+lib.lora_symm_ptr.restype = _vp
+lib.lora_symm_bytes.argtypes = [_vp]
+lib.lora_symm_bytes.restype = ctypes.c_size_t
+lib.lora_symm_destroy.argtypes = [_vp]
+lib.lora_symm_destroy.restype = _st
+lib.lora_tp_linear_fwd_fused.argtypes = [_vp, _dp, _vp, _vp, _vp, _vp, _vp, ctypes.c_size_t, ctypes.c_size_t, _fp,
+                                         _vp, ctypes.c_size_t, _vp]
+lib.lora_tp_linear_fwd_fused.restype = _st
+lib.lora_tp_linear_bwd_column_group_fused.argtypes = [_vp, _vp, ctypes.c_int, _dp, ctypes.POINTER(lora_bwd_problem),
+                                                      ctypes.c_size_t, ctypes.c_size_t, ctypes.c_int, _vp,
+                                                      ctypes.c_size_t, _vp]
+lib.lora_tp_linear_bwd_column_group_fused.restype = _st
+
 lib.lora_captured_sync_words_free.restype = ctypes.c_int
 lib.lora_profile_next_bwd.argtypes = [ctypes.POINTER(_vp)]
 lib.lora_profile_next_bwd.restype = _st

@@ -300,6 +300,7 @@ lora_status fwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
     p.h_split_src = nullptr;
     p.t_pad = 0;
     p.sk_partial = W.partial_bytes ? reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + W.partial) : nullptr;
+    p.unit_flags = nullptr;
     if (drop && drop->thr > 0) {
         // LoRA dropout: K0 computes h = q (M . x) A^T; K1 takes it instead of its in-MMA x A^T
         float* hd = h_out ? h_out : reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + W.h);
@@ -642,6 +643,7 @@ lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
         // the gh tile also writes K3's split coefficients (gh; h when it already exists)
         p.t_pad = t_pad_of(T);
         p.sk_partial = W.partial_bytes ? reinterpret_cast<float*>(wsb + W.partial) : nullptr;
+        p.unit_flags = nullptr;
         // the gh tile publishes gh to the other tiles through cs_a (hi rows; the full
         // split when dA -- or the dropout epilogue's fp32 gh -- needs it)
         p.cs_gh = reinterpret_cast<__nv_bfloat16*>(wsb + W.cs_a);
@@ -1005,7 +1007,8 @@ namespace lora_host {
 
 lora_status bwd_grouped_impl(int count, const lora_dims* dims, const lora_bwd_problem* probs, int accumulate,
                              void* workspace, size_t workspace_bytes, void* stream,
-                             lora_status (*after_k2)(void* ctx, int* launches), void* ctx) {
+                             lora_status (*after_k2)(void* ctx, int* launches), void* ctx,
+                             lora_status (*before_k2)(void* bctx, GemmCollector* col, int* launches), void* bctx) {
     int launches = 0;
     lora_status st = check_group(count, dims, probs, "lora_linear_bwd_grouped");
     if (st != LORA_OK) return st;
@@ -1039,6 +1042,10 @@ lora_status bwd_grouped_impl(int count, const lora_dims* dims, const lora_bwd_pr
                           static_cast<uint8_t*>(workspace) + off, wg, st_, &launches, &col, stage);
             if (st != LORA_OK) { set_launches(launches); return st; }
             off += wg;
+        }
+        if (stage == 1 && before_k2 && (st = before_k2(bctx, &col, &launches)) != LORA_OK) {
+            set_launches(launches);
+            return st;
         }
         if (stage == 1) {
             prof_record(0, st_);

@@ -114,6 +114,10 @@ lora_status lora_comm_init(int nranks, int rank, const uint8_t id[LORA_COMM_ID_B
         return fail(LORA_ERR_INVALID, "lora_comm_init: rank %d / nranks %d invalid", rank, nranks);
     NcclApi* api = nccl();
     if (!api) return fail(LORA_ERR_NCCL, "libnccl could not be loaded (set LORA_NCCL_LIB)");
+    // the fused kernels must not be lazily loaded at a first launch that lands next to an
+    // NCCL kernel waiting for a peer (the load would wait for that kernel)
+    lora_status ps = preload_kernels();
+    if (ps != LORA_OK) return ps;
     ncclUniqueId u;
     memcpy(&u, id, sizeof u);
     lora_comm* c = new lora_comm();

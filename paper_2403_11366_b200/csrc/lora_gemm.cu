@@ -1008,6 +1008,16 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
                 named_bar_sync(1, 128);   // every epilogue warp is done with the A tile
                 if (ew == 0 && lane == 0) mbar_arrive((tt & 1) ? tailop2_empty : tailop_empty);
             }
+            if (p.unit_flags != nullptr) {
+                // comm-fused epilogue: this CTA's 128 rows of the tile are stored -- publish
+                // them to the ranks' reducers (lora_symm.cu) with one system-scope release
+                __threadfence_system();
+                named_bar_sync(1, 128);
+                const int64_t nrow128 = (p.T + BM - 1) / BM;
+                const int64_t row128 = static_cast<int64_t>(t_blk) * CG + crank;
+                if (ew == 0 && lane == 0 && row128 < nrow128)   // (a pair's second CTA past T has no rows)
+                    st_release_sys_u32(p.unit_flags + n_blk * nrow128 + row128, 1u);
+            }
             ++tt;
 #ifdef LORA_PROBE_SK
             if (ew == 0 && lane == 0 && crank == 0) {
@@ -1340,6 +1350,21 @@ static cudaError_t launch_impl(FusedGemmGroup& grp, int num_sms, cudaStream_t st
 
 int fused_gemm_block_n(int mode, int r_pad) { return mode == kModeFwd ? NT - r_pad : NT; }
 
+// Column tiles of a fused-GEMM output as the kernel walks them (ColTiles):
+// starts[0 .. count] with starts[count] = n_out; returns count (or -1 > max).
+int fused_gemm_col_tiles(int mode, int r_pad, int64_t n_out, int* starts, int max) {
+    const int64_t count = col_tiles_host(mode, r_pad, n_out);
+    if (count > max) return -1;
+    for (int64_t c = 0; c < count; ++c) {
+        int64_t st;
+        if (mode == kModeFwd) st = c * (NT - r_pad);
+        else st = c == 0 ? 0 : DX_BN0 + (c - 1) * NT;
+        starts[c] = static_cast<int>(st);
+    }
+    starts[count] = static_cast<int>(n_out);
+    return static_cast<int>(count);
+}
+
 // Off by default: measured on B200 (cfg2 step replayed as a CUDA graph) PDL
 // launches were 6% slower than plain stream order (243 vs 258 us/step);
 // LORA_PDL=1 turns it on.
@@ -1395,6 +1420,33 @@ cudaError_t launch_fused_gemm(int mode, int r_pad, int cta_group, const FusedGem
     grp.maps[0] = maps;
     grp.p[0] = p;
     return launch_fused_gemm_group(mode, r_pad, cta_group, grp, num_sms, stream);
+}
+
+
+// Lazy module loading (the CUDA 12 default) loads a kernel at its first launch,
+// and that load waits for the device to drain.  A kernel that spins on another
+// one's output (the comm-fused reducer, lora_symm.cu) must therefore never be
+// running while the kernel it waits for is launched for the first time:
+// preload_*() loads every kernel of a file up front (cudaFuncGetAttributes).
+template <int CG>
+static cudaError_t preload_cg() {
+    cudaFuncAttributes a;
+    const void* ks[] = {
+        (const void*)lora_fused_gemm_kernel<kModeFwd, 16, CG>, (const void*)lora_fused_gemm_kernel<kModeFwd, 32, CG>,
+        (const void*)lora_fused_gemm_kernel<kModeFwd, 64, CG>, (const void*)lora_fused_gemm_kernel<kModeDx, 16, CG>,
+        (const void*)lora_fused_gemm_kernel<kModeDx, 32, CG>, (const void*)lora_fused_gemm_kernel<kModeDx, 64, CG>,
+        (const void*)lora_fused_gemm_kernel<kModeDxDrop, 16, CG>,
+        (const void*)lora_fused_gemm_kernel<kModeDxDrop, 32, CG>,
+        (const void*)lora_fused_gemm_kernel<kModeDxDrop, 64, CG>};
+    for (const void* k : ks) {
+        cudaError_t e = cudaFuncGetAttributes(&a, k);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+cudaError_t preload_gemm_kernels() {
+    cudaError_t e = preload_cg<1>();
+    return e != cudaSuccess ? e : preload_cg<2>();
 }
 
 }  // namespace lora_sm100

@@ -335,4 +335,10 @@ cudaError_t launch_grad_reduce_cluster(int64_t T, int64_t n, int64_t m, int r, f
     return launch_grad_reduce_cluster_group(G, stream, launches);
 }
 
+// (lazy loading: see preload_gemm_kernels in lora_gemm.cu)
+cudaError_t preload_grad_kernels() {
+    cudaFuncAttributes a;
+    return cudaFuncGetAttributes(&a, (const void*)pack_b_kernel);
+}
+
 }  // namespace lora_sm100

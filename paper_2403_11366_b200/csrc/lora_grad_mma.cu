@@ -569,4 +569,11 @@ cudaError_t launch_grad_mma(GradMmaGroup& G, int num_sms, cudaStream_t stream, b
     return cudaGetLastError();
 }
 
+// (lazy loading: see preload_gemm_kernels in lora_gemm.cu)
+cudaError_t preload_grad_mma_kernels() {
+    cudaFuncAttributes a;
+    cudaError_t e = cudaFuncGetAttributes(&a, (const void*)coef_split_kernel);
+    return e != cudaSuccess ? e : cudaFuncGetAttributes(&a, (const void*)grad_mma_kernel);
+}
+
 }  // namespace lora_sm100

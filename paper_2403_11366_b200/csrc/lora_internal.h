@@ -22,9 +22,18 @@ int get_launches();
 // enqueued (before the dA / dB kernel): after_k2(ctx, &launches) may enqueue
 // work that depends only on the members' dX (the TP column group's dX sum and
 // all-reduce, on a side stream).
+// before_k2(bctx, &col, &launches) runs right before the grouped dX kernel is
+// launched: it may edit the collected K2 parameters (the comm-fused epilogue sets
+// unit flags) and enqueue work that must precede K2 (the fused reducer's fork).
+struct GemmCollector;
 lora_status bwd_grouped_impl(int count, const lora_dims* dims, const lora_bwd_problem* probs, int accumulate,
                              void* workspace, size_t workspace_bytes, void* stream,
-                             lora_status (*after_k2)(void* ctx, int* launches), void* ctx);
+                             lora_status (*after_k2)(void* ctx, int* launches), void* ctx,
+                             lora_status (*before_k2)(void* bctx, GemmCollector* col, int* launches) = nullptr,
+                             void* bctx = nullptr);
+int r_pad_of(int r);
+// load the kernels launched next to spinning kernels (reducer, NCCL) -- lora_symm.cu
+lora_status preload_kernels();
 
 // Fused-GEMM problems gathered by the grouped entry points (launched together).
 struct GemmCollector {

@@ -51,6 +51,10 @@ struct FusedGemmParams {
     const float* h_split_src;
     int64_t t_pad;
     float* sk_partial;            // stream-K partial slots in this problem's workspace (group: p[0]'s), or null
+    // comm-fused epilogue (lora_symm.cu): after the 128-row half of an
+    // output tile is stored, one release store (system scope: peers read it over
+    // NVLink) sets unit_flags[n_blk * ceil(T / 128) + row128] = 1; null = off
+    uint32_t* unit_flags;
 };
 
 struct FusedGemmMaps {
@@ -244,6 +248,34 @@ cudaError_t launch_grad_reduce_cluster(int64_t T, int64_t n, int64_t m, int r, f
 cudaError_t launch_merge(const __nv_bfloat16* w0, const __nv_bfloat16* a, const __nv_bfloat16* b,
                          int64_t n, int64_t m, int r, float scale, __nv_bfloat16* w_out,
                          cudaStream_t stream);
+
+// column tiles of a fused-GEMM output (lora_gemm.cu ColTiles): starts[0..count], starts[count] = n_out
+int fused_gemm_col_tiles(int mode, int r_pad, int64_t n_out, int* starts, int max);
+
+// Comm-fused epilogue reducer (lora_symm.cu): sums the 128-row
+// output units the fused GEMMs of every rank (and every member of a group)
+// published into their symmetric partial regions, in (rank, member) order in
+// fp32, rounds once to bf16 and stores the result into every rank's output
+// region.  Unit u (flag index n_blk * nrow128 + row128) is reduced by rank u % N.
+constexpr int kSymmMaxRanks = 8;
+constexpr int kSymmMaxColTiles = 256;
+struct SymmReduceArgs {
+    int nranks, rank, nsrc;
+    int nrow128, ncol_tiles, units;
+    int64_t T, ncols, ld;
+    int col_start[kSymmMaxColTiles + 1];
+    const __nv_bfloat16* part[kSymmMaxRanks][kMaxGroup];
+    uint32_t* flags[kSymmMaxRanks];      // rank r's unit flags, [member][units]
+    __nv_bfloat16* out[kSymmMaxRanks];
+    uint32_t* done[kSymmMaxRanks];       // rank r's launch counter
+};
+cudaError_t launch_symm_reduce(const SymmReduceArgs& A, int ctas, cudaStream_t stream);
+// load every kernel the fused TP paths launch while a reducer may be spinning (lazy
+// module loading would otherwise load them at first launch, which waits for the
+// device to drain -- i.e. for the spinning reducer: a deadlock)
+cudaError_t preload_gemm_kernels();
+cudaError_t preload_grad_kernels();
+cudaError_t preload_grad_mma_kernels();
 
 // K4 on the tensor cores (lora_merge_mma.cu; r % 8 == 0, r <= 64): TMA maps of
 // W0 [m, n] and W' [m, n] (box 64 x 128, SW128), B [m, r] (box r_pad x 128,

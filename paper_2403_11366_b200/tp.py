@@ -225,3 +225,142 @@ def tp_linear_bwd_column_group(comm: LoraComm, specs, problems, alphas, dx_sum=N
                                                1 if reduce_lora_grads else 0, _ptr(ws), ws.numel(),
                                                _stream(stream)), "lora_tp_linear_bwd_column_group")
     return dx_sum, res
+
+
+# ------------------------------------------------- comm-fused epilogues (N2)
+class _DevView:
+    """__cuda_array_interface__ over raw device memory (a view into a lora_symm)."""
+
+    def __init__(self, ptr, shape, typestr):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+class SymmBuffer:
+    """A symmetric device buffer of liblora.so (lora_symm_*):
+    the same size on every rank, peers mapped with CUDA IPC.  The fused TP calls
+    write their partial outputs and results into regions of it (byte offsets).
+
+    SymmBuffer(nbytes, group) -- one per rank of a torch.distributed group
+        (IPC handles all-gathered over it).
+    SymmBuffer.local_group(nranks, nbytes) -- N buffers of THIS process on the
+        current device, joined as N virtual ranks (runs the protocol on one GPU)."""
+
+    def __init__(self, nbytes: int, group=None, _connect=True):
+        import torch.distributed as dist
+
+        from . import _check, lib
+        self._h = ctypes.c_void_p()
+        _check(lib.lora_symm_create(int(nbytes), ctypes.byref(self._h)), "lora_symm_create")
+        self.nbytes = int(lib.lora_symm_bytes(self._h))
+        self.world, self.rank = 1, 0
+        if not _connect:
+            return
+        if dist.is_initialized():
+            self.world, self.rank = dist.get_world_size(group), dist.get_rank(group)
+        mine = ctypes.create_string_buffer(64)
+        _check(lib.lora_symm_ipc_handle(self._h, mine), "lora_symm_ipc_handle")
+        handles = [None] * self.world
+        if self.world > 1:
+            dist.all_gather_object(handles, bytes(mine.raw), group=group)
+        else:
+            handles = [bytes(mine.raw)]
+        blob = ctypes.create_string_buffer(b"".join(handles), 64 * self.world)
+        _check(lib.lora_symm_connect(self._h, self.world, self.rank, blob), "lora_symm_connect")
+
+    @classmethod
+    def local_group(cls, nranks: int, nbytes: int):
+        from . import _check, lib
+        bufs = [cls(nbytes, _connect=False) for _ in range(nranks)]
+        arr = (ctypes.c_void_p * nranks)(*[b._h.value for b in bufs])
+        _check(lib.lora_symm_connect_local(nranks, arr), "lora_symm_connect_local")
+        for r, b in enumerate(bufs):
+            b.world, b.rank = nranks, r
+        return bufs
+
+    @property
+    def handle(self):
+        return self._h
+
+    def view(self, offset: int, shape, dtype="bf16"):
+        """A torch tensor over [offset, ...) of this rank's data region."""
+        import torch
+
+        from . import lib
+        base = lib.lora_symm_ptr(self._h)
+        typestr = {"bf16": "<f2", "f32": "<f4"}[dtype]
+        t = torch.as_tensor(_DevView(base + int(offset), shape, typestr), device="cuda")
+        return t.view(torch.bfloat16) if dtype == "bf16" else t
+
+    def close(self):
+        from . import lib
+        if self._h:
+            lib.lora_symm_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+
+def tp_linear_fwd_fused(symm: SymmBuffer, spec: ShardSpec, x, w0, a, b, alpha, bias=None, part_offset=0,
+                        y_offset=None, h_out=None, workspace=None, stream=None):
+    """lora_tp_linear_fwd_fused: ROW-parallel forward with the y all-reduce fused
+    into the GEMM.  Returns (y [T, m] -- a view of the symmetric buffer, valid until
+    the next fused call writing that region --, h [T, r])."""
+    import torch
+
+    from . import _bf16, _check, _ptr, _stream, _workspace, dims, lib, lora_linear_fwd_workspace_bytes
+    if spec.mode != ROW:
+        raise ValueError("tp_linear_fwd_fused is the ROW-parallel forward (its y is a partial sum)")
+    T, r = x.shape[0], a.shape[0]
+    n, m = spec.local_n, spec.local_m
+    _bf16(x, "x", (T, n)); _bf16(w0, "w0", (m, n)); _bf16(a, "a", (r, n)); _bf16(b, "b", (m, r))
+    yb = T * m * 2
+    if y_offset is None:
+        y_offset = part_offset + (yb + 255) // 256 * 256
+    if h_out is None:
+        h_out = torch.empty((T, r), dtype=torch.float32, device=x.device)
+    d = dims(T, n, m, r, alpha)
+    ws = workspace if workspace is not None else _workspace(lora_linear_fwd_workspace_bytes(d), x.device)
+    _check(lib.lora_tp_linear_fwd_fused(symm.handle, ctypes.byref(d), _ptr(x), _ptr(w0), _ptr(a), _ptr(b),
+                                        _ptr(bias), int(part_offset), int(y_offset), _ptr(h_out), _ptr(ws),
+                                        ws.numel(), _stream(stream)), "lora_tp_linear_fwd_fused")
+    return symm.view(y_offset, (T, m)), h_out
+
+
+def tp_linear_bwd_column_group_fused(symm: SymmBuffer, specs, problems, alphas, comm=None, part_offset=0,
+                                     dx_offset=None, outs=None, reduce_lora_grads=False, workspace=None,
+                                     stream=None):
+    """lora_tp_linear_bwd_column_group_fused: the COLUMN group backward with the dX
+    all-reduce (over ranks and members) fused into the grouped dX GEMM.
+    problems: (x, w0, a, b, dy, h_saved) local shards sharing x.  Returns
+    (dx_sum [T, n] -- a view of the symmetric buffer --, [(dA_g, dB_g)])."""
+    import torch
+
+    from . import _check, _ptr, _stream, _workspace, dims, lib, lora_bwd_problem, lora_dims
+    G = len(problems)
+    x = problems[0][0]
+    T, n = x.shape[0], specs[0].local_n
+    if any(sp.mode != COLUMN for sp in specs):
+        raise ValueError("the fused column-group backward is for COLUMN-parallel linears")
+    xb = T * n * 2
+    if dx_offset is None:
+        dx_offset = part_offset + (G * xb + 255) // 256 * 256
+    dims_arr = (lora_dims * G)()
+    probs = (lora_bwd_problem * G)()
+    res = []
+    for g, ((xg, w0, a, b, dy, h), sp) in enumerate(zip(problems, specs)):
+        r, m = a.shape[0], sp.local_m
+        da, db = outs[g] if outs is not None else (None, None)
+        if da is None:
+            da = torch.empty((r, n), dtype=torch.float32, device=x.device)
+        if db is None:
+            db = torch.empty((m, r), dtype=torch.float32, device=x.device)
+        dims_arr[g] = dims(T, n, m, r, alphas[g])
+        probs[g] = lora_bwd_problem(_ptr(xg), _ptr(w0), _ptr(a), _ptr(b), _ptr(h), _ptr(dy), None, _ptr(da),
+                                    _ptr(db))
+        res.append((da, db))
+    need = int(lib.lora_linear_bwd_grouped_workspace_bytes(G, dims_arr))
+    ws = workspace if workspace is not None else _workspace(need, x.device)
+    _check(lib.lora_tp_linear_bwd_column_group_fused(symm.handle, comm.handle if comm is not None else None, G,
+                                                     dims_arr, probs, int(part_offset), int(dx_offset),
+                                                     1 if reduce_lora_grads else 0, _ptr(ws), ws.numel(),
+                                                     _stream(stream)), "lora_tp_linear_bwd_column_group_fused")
+    return symm.view(dx_offset, (T, n)), res
