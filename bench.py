@@ -265,7 +265,8 @@ class StepRunner:
     set and double-buffers host transfers against compute).  The numpy bit
     patterns of the unsharded inputs stay in `host` for the parity checks."""
 
-    def __init__(self, wl, dev, world=1, rank=0, comm=None, group=True, dropout=0.0, nsets=1, seed0=2403):
+    def __init__(self, wl, dev, world=1, rank=0, comm=None, group=True, dropout=0.0, nsets=1, seed0=2403,
+                 comm_mode="nccl"):
         import torch
 
         import paper_2403_11366_b200 as L
@@ -347,6 +348,41 @@ class StepRunner:
                     self.tp_groups.append((members, wsf, wsb, dx_sum))
                 else:
                     self.tp_groups.append((members, None, None, None))
+        # comm-fused epilogues (lora_symm): one symmetric buffer per
+        # rank holding, per row-parallel linear, its partial y and the reduced y, and per
+        # column group its members' dX partials and the reduced dX w.r.t. the input
+        self.symm = None
+        self.comm_mode = comm_mode if comm is not None else "none"
+        if self.comm_mode == "fused":
+            if not self.tp_groups:
+                raise SystemExit("--comm fused needs the grouped TP step (no --no-group / --dropout)")
+            off, regions = 0, []
+
+            def region(nbytes):
+                nonlocal off
+                o = off
+                off += (nbytes + 255) // 256 * 256
+                return o
+
+            for members, wsf, wsb, dx_sum in self.tp_groups:
+                if wsb is not None:
+                    T, n = members[0]["l"].T, members[0]["spec"].local_n
+                    regions.append(("col", members, region(len(members) * T * n * 2), region(T * n * 2)))
+                else:
+                    for e in members:
+                        if e["spec"].mode == tp.ROW:
+                            T, m = e["l"].T, e["spec"].local_m
+                            regions.append(("row", e, region(T * m * 2), region(T * m * 2)))
+            self.symm = tp.SymmBuffer(off + 4096)
+            self.fused_regions = {}
+            for kind, obj, part, out in regions:
+                if kind == "row":
+                    self.fused_regions[id(obj)] = (part, out)
+                    T, m = obj["l"].T, obj["spec"].local_m
+                    obj["y_sets"] = [self.symm.view(out, (T, m))] * nsets   # y lives in the symmetric buffer
+                else:
+                    self.fused_regions[id(obj[0])] = (part, out)
+            self.use_set(self.k)
 
     def _dims(self, members):
         L = self.L
@@ -400,6 +436,7 @@ class StepRunner:
     def _step_tp(self, ev):
         L, tp, comm = self.L, self.tp, self.comm
         cur = self.torch.cuda.current_stream()
+        fused = self.comm_mode == "fused"
         for gi, (members, wsf, _, _) in enumerate(self.tp_groups):
             if ev is not None and gi == 0:
                 ev["f0"].record(cur)
@@ -410,15 +447,30 @@ class StepRunner:
                 self.launches += L.lora_last_launch_count()
             else:
                 for e in members:
-                    tp.tp_linear_fwd(comm, e["spec"], e["x"], e["w0"], e["a"], e["b"], e["l"].alpha, y=e["y"],
-                                     h_out=e["h"], workspace=e["ws_f"], stream=cur)
+                    if fused and e["spec"].mode == tp.ROW:   # y all-reduce fused into the GEMM
+                        part, out = self.fused_regions[id(e)]
+                        tp.tp_linear_fwd_fused(self.symm, e["spec"], e["x"], e["w0"], e["a"], e["b"], e["l"].alpha,
+                                               part_offset=part, y_offset=out, h_out=e["h"], workspace=e["ws_f"],
+                                               stream=cur)
+                    else:
+                        tp.tp_linear_fwd(comm, e["spec"], e["x"], e["w0"], e["a"], e["b"], e["l"].alpha,
+                                         y=e["y"], h_out=e["h"], workspace=e["ws_f"], stream=cur)
                     self.launches += L.lora_last_launch_count()
             if ev is not None and gi == 0:
                 ev["f1"].record(cur)
         for gi, (members, _, wsb, dx_sum) in enumerate(self.tp_groups):
             if gi == 0:
                 self._prof_bwd(ev)
-            if wsb is not None:
+            if wsb is not None and fused:   # dX all-reduce (over ranks and members) fused into K2
+                part, out = self.fused_regions[id(members[0])]
+                tp.tp_linear_bwd_column_group_fused(self.symm, [e["spec"] for e in members],
+                                                    [(e["x"], e["w0"], e["a"], e["b"], e["dy"], e["h"])
+                                                     for e in members], [e["l"].alpha for e in members],
+                                                    comm=comm, part_offset=part, dx_offset=out,
+                                                    outs=[(e["da"], e["db"]) for e in members],
+                                                    reduce_lora_grads=True, workspace=wsb, stream=cur)
+                self.launches += L.lora_last_launch_count()
+            elif wsb is not None:
                 tp.tp_linear_bwd_column_group(comm, [e["spec"] for e in members],
                                               [(e["x"], e["w0"], e["a"], e["b"], e["dy"], e["h"]) for e in members],
                                               [e["l"].alpha for e in members], dx_sum=dx_sum[self.k],
@@ -494,11 +546,22 @@ class StepRunner:
         self.torch.cuda.synchronize()
         worst = {"y": 0.0, "h": 0.0, "dx": 0.0, "da": 0.0, "db": 0.0}
         nrows = 0
+        # comm-fused column groups keep only the reduced dX w.r.t. their shared input
+        # (the members' partials live in the symmetric buffer): check that sum
+        fused_dx = {}
+        if self.comm_mode == "fused":
+            for members, _, wsb, _ in self.tp_groups:
+                if wsb is not None:
+                    part, out = self.fused_regions[id(members[0])]
+                    T, n = members[0]["l"].T, members[0]["spec"].local_n
+                    for e in members:
+                        fused_dx[id(e)] = (members, self.symm.view(out, (T, n)))
+        dx_sums = {}
         for i, e in enumerate(self.lin):
             l, d = e["l"], self.host[i]
             T = l.T
             if rows_per_linear is None:
-                rng = np.random.default_rng(seed + i)
+                rng = np.random.default_rng(seed + (0 if fused_dx else i))   # (a group's members: same rows)
                 rows = np.unique(np.concatenate([np.arange(min(256, T)), rng.choice(T, min(128, T), replace=False),
                                                  np.arange(max(0, T - 32), T)]))
             else:
@@ -506,10 +569,18 @@ class StepRunner:
             yo, ho = oracle.lora_fwd(d["x"], d["w0"], d["a"], d["b"], l.alpha, rows=rows)
             go = oracle.lora_bwd(d["x"], d["w0"], d["a"], d["b"], d["dy"], l.alpha, rows=rows)
             ri = self.torch.as_tensor(rows, device=self.dev)
-            got = {"y": to_f64(e["y"][ri]), "h": to_f64(e["h"][ri]), "dx": to_f64(e["dx"][ri]),
-                   "da": to_f64(e["da"]), "db": to_f64(e["db"])}
-            ref = {"y": yo, "h": ho, "dx": go["dx"], "da": go["da"], "db": go["db"]}
-            for k in worst:
+            got = {"y": to_f64(e["y"][ri]), "h": to_f64(e["h"][ri]), "da": to_f64(e["da"]), "db": to_f64(e["db"])}
+            ref = {"y": yo, "h": ho, "da": go["da"], "db": go["db"]}
+            if id(e) in fused_dx:
+                members, view = fused_dx[id(e)]
+                acc = dx_sums.setdefault(id(members[0]), [None, 0, view])
+                acc[0] = go["dx"] if acc[0] is None else acc[0] + go["dx"]
+                acc[1] += 1
+                if acc[1] == len(members):   # every member's oracle dX rows summed
+                    got["dx"], ref["dx"] = to_f64(view[ri]), acc[0]
+            else:
+                got["dx"], ref["dx"] = to_f64(e["dx"][ri]), go["dx"]
+            for k in ref:
                 worst[k] = max(worst[k], relF(got[k], ref[k]))
             nrows += len(rows)
         ok = worst["y"] <= 1e-2 and worst["dx"] <= 1e-2 and worst["da"] <= 2e-2 and worst["db"] <= 2e-2
@@ -545,7 +616,8 @@ def run_ours(args, wl):
 
     stream = torch.cuda.current_stream()
     comm = tp.LoraComm() if (world > 1 or args.force_tp) else None
-    R = StepRunner(wl, dev, world, rank, comm, group=not args.no_group, dropout=args.dropout, nsets=2)
+    R = StepRunner(wl, dev, world, rank, comm, group=not args.no_group, dropout=args.dropout, nsets=2,
+                   comm_mode=args.comm)
     lin = R.lin
 
     # L2 flush between timed steps, outside the event pairs: write a 2 x L2
@@ -841,6 +913,8 @@ def run_ours(args, wl):
                        "tokens": tokens, "rank": l0.r, "alpha": l0.alpha,
                        "global_batch": 1, "seq_len": tokens,
                        "parallelism": f"tp{world}" if comm is not None else "single",
+                       "tp_comm": (("fused into the GEMMs over peer memory (lora_symm)" if args.comm == "fused"
+                                    else "NCCL all-reduce after the GEMMs") if comm is not None else None),
                        "cuda_graph": graph is not None,
                        "grouped_calls": ([[wl.linears[i].name for i in g] for g in wl.groups] if grouped else None),
                        "shared_inputs": [[wl.linears[i].name for i in g] for g in wl.groups if len(g) > 1],
@@ -910,6 +984,9 @@ def main():
                     help="LoRA dropout p (Listing 3 LORA_DROPOUT = 0.05); 0 = the north-star path")
     ap.add_argument("--no-group", action="store_true",
                     help="one call per linear instead of grouped calls for linears sharing an input")
+    ap.add_argument("--comm", choices=["nccl", "fused"], default="nccl",
+                    help="TP activation all-reduces: NCCL calls after the GEMMs, or fused into the GEMMs over "
+                         "peer memory (lora_symm, SURVEY 8(f) N2)")
     ap.add_argument("--graph", choices=["auto", "on", "off"], default="auto",
                     help="replay each step as one CUDA graph (auto: at every N, eager if capture fails)")
     args = ap.parse_args()

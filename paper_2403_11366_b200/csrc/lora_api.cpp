@@ -514,6 +514,7 @@ lora_status launch_collected(int mode, GemmCollector& col, cudaStream_t stream, 
     for (int i = 0; i < col.count; ++i) {
         if (done[i]) continue;
         grp.count = 0;
+        grp.no_coop = col.no_coop ? 1 : 0;
         for (int j = i; j < col.count; ++j) {
             if (done[j] || col.rp[j] != col.rp[i] || col.cg[j] != col.cg[i]) continue;
             grp.maps[grp.count] = col.maps[j];

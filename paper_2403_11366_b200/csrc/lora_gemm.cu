@@ -1342,7 +1342,7 @@ static cudaError_t launch_impl(FusedGemmGroup& grp, int num_sms, cudaStream_t st
     attr[2].id = cudaLaunchAttributeCooperative;
     attr[2].val.cooperative = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = ((MODE != kModeFwd || grp.sk.enabled) && coop_enabled()) ? 3 : 2;
+    cfg.numAttrs = ((MODE != kModeFwd || grp.sk.enabled) && coop_enabled() && !grp.no_coop) ? 3 : 2;
     e = cudaLaunchKernelEx(&cfg, kern, grp);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
@@ -1417,6 +1417,7 @@ cudaError_t launch_fused_gemm(int mode, int r_pad, int cta_group, const FusedGem
                               const FusedGemmParams& p, int num_sms, cudaStream_t stream) {
     static thread_local FusedGemmGroup grp;   // ~6 KiB: keep it off the stack
     grp.count = 1;
+    grp.no_coop = 0;
     grp.maps[0] = maps;
     grp.p[0] = p;
     return launch_fused_gemm_group(mode, r_pad, cta_group, grp, num_sms, stream);

@@ -42,6 +42,7 @@ struct GemmCollector {
     lora_sm100::FusedGemmParams p[lora_sm100::kMaxGroup];
     int rp[lora_sm100::kMaxGroup];
     int cg[lora_sm100::kMaxGroup];
+    bool no_coop = false;   // launch the fused GEMMs non-cooperatively (comm-fused path)
     // K3 (dA, dB) problems of the grouped backward, launched together at the end
     int k3_count = 0;
     lora_sm100::GradArgs k3[lora_sm100::kMaxGroup];

@@ -96,6 +96,8 @@ struct FusedGemmGroup {
     int tile_start[kMaxGroup + 1];
     int count;
     unsigned long long* done;     // dx: sync-pool launch counter (last CTA out resets flags), or null
+    int no_coop;                  // 1: never a cooperative launch (the comm-fused path: a cooperative grid
+                                  // waits for the co-resident reducer it feeds -- lora_symm.cu)
     StreamKSched sk;              // filled in by the launcher
 };
 // bytes of stream-K partial workspace a fused-GEMM launch may use (0: none)

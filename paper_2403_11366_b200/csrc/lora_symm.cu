@@ -50,7 +50,8 @@ __device__ __forceinline__ uint4 ld_cg_u4(const void* p) {
     return v;
 }
 
-__global__ void __launch_bounds__(256) symm_reduce_kernel(const __grid_constant__ SymmReduceArgs A) {
+__global__ void __launch_bounds__(128, 4) symm_reduce_kernel(   // (4: <= 128 registers, see reducer_ctas)
+    const __grid_constant__ SymmReduceArgs A) {
     const int N = A.nranks, G = A.nsrc;
     const int nwait = N * G;
     for (int64_t k = blockIdx.x;; k += gridDim.x) {
@@ -78,23 +79,57 @@ __global__ void __launch_bounds__(256) symm_reduce_kernel(const __grid_constant_
             }
         }
         __syncthreads();
-        for (int i = threadIdx.x; i < rows * nv; i += blockDim.x) {
-            const int row = i / nv, v = i - (i / nv) * nv;
-            const int64_t off = (r0 + row) * A.ld + c0 + 8 * v;
-            float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-            for (int r = 0; r < N; ++r)
-                for (int g = 0; g < G; ++g) {
-                    const uint4 q = ld_cg_u4(A.part[r][g] + off);
-                    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+        // kV vectors (16 bytes) per thread per round, their loads for kSrc sources at a
+        // time all in flight before any is consumed: the reduction is latency-bound (peer
+        // loads), and the CTA must stay small enough to sit next to the GEMM's
+        constexpr int kV = 4, kSrc = 2;
+        const int total = rows * nv;
+        for (int i0 = threadIdx.x; i0 < total; i0 += kV * blockDim.x) {
+            int64_t off[kV];
+            bool ok[kV];
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        acc[2 * e] += __uint_as_float(w[e] << 16);
-                        acc[2 * e + 1] += __uint_as_float(w[e] & 0xFFFF0000u);
+            for (int v = 0; v < kV; ++v) {
+                const int i = i0 + v * blockDim.x;
+                ok[v] = i < total;
+                const int row = ok[v] ? i / nv : 0, cv = ok[v] ? i - (i / nv) * nv : 0;
+                off[v] = (r0 + row) * A.ld + c0 + 8 * cv;
+            }
+            float acc[kV][8];
+#pragma unroll
+            for (int v = 0; v < kV; ++v)
+#pragma unroll
+                for (int e = 0; e < 8; ++e) acc[v][e] = 0.0f;
+            for (int s0 = 0; s0 < nwait; s0 += kSrc) {   // (rank, member) order
+                uint4 q[kSrc][kV];
+#pragma unroll
+                for (int j = 0; j < kSrc; ++j) {
+                    const int sj = s0 + j;
+                    const __nv_bfloat16* src = sj < nwait ? A.part[sj / G][sj - (sj / G) * G] : nullptr;
+#pragma unroll
+                    for (int v = 0; v < kV; ++v)
+                        q[j][v] = (src != nullptr && ok[v]) ? ld_cg_u4(src + off[v]) : make_uint4(0, 0, 0, 0);
+                }
+#pragma unroll
+                for (int j = 0; j < kSrc; ++j) {
+                    if (s0 + j >= nwait) break;
+#pragma unroll
+                    for (int v = 0; v < kV; ++v) {
+                        const uint32_t w[4] = {q[j][v].x, q[j][v].y, q[j][v].z, q[j][v].w};
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            acc[v][2 * e] += __uint_as_float(w[e] << 16);
+                            acc[v][2 * e + 1] += __uint_as_float(w[e] & 0xFFFF0000u);
+                        }
                     }
                 }
-            const uint4 o = make_uint4(pack_bf16x2(acc[0], acc[1]), pack_bf16x2(acc[2], acc[3]),
-                                       pack_bf16x2(acc[4], acc[5]), pack_bf16x2(acc[6], acc[7]));
-            for (int r = 0; r < N; ++r) *reinterpret_cast<uint4*>(A.out[r] + off) = o;
+            }
+#pragma unroll
+            for (int v = 0; v < kV; ++v) {
+                if (!ok[v]) continue;
+                const uint4 o = make_uint4(pack_bf16x2(acc[v][0], acc[v][1]), pack_bf16x2(acc[v][2], acc[v][3]),
+                                           pack_bf16x2(acc[v][4], acc[v][5]), pack_bf16x2(acc[v][6], acc[v][7]));
+                for (int r = 0; r < N; ++r) *reinterpret_cast<uint4*>(A.out[r] + off[v]) = o;
+            }
         }
         __syncthreads();   // every read of this unit's partials is done: its flags may be reused
         if (static_cast<int>(threadIdx.x) < nwait) {
@@ -137,7 +172,7 @@ cudaError_t launch_symm_reduce(const SymmReduceArgs& A, int ctas, cudaStream_t s
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
-    symm_reduce_kernel<<<ctas, 256, 0, stream>>>(A);
+    symm_reduce_kernel<<<ctas, 128, 0, stream>>>(A);
     return cudaGetLastError();
 }
 
@@ -162,6 +197,7 @@ struct lora_symm {
     int nranks = 0, rank = 0;                   // 0 until connected
     uint8_t* peer[kSymmMaxRanks] = {};          // every rank's base (peer[rank] == base)
     bool opened[kSymmMaxRanks] = {};            // IPC mappings to close
+    bool local = false;                         // virtual ranks of one process on one GPU
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
@@ -234,17 +270,44 @@ static lora_status make_reduce_args(const lora_symm* s, int mode, int rp, int64_
     return LORA_OK;
 }
 
-static int reducer_ctas(const SymmReduceArgs& A) {
+// One CTA per owned unit, at most one per SM.  The GEMM's persistent CTAs own
+// fixed tiles the reducer waits for, so a GEMM CTA must fit next to a reducer CTA
+// on EVERY SM (launch order alone does not decide placement): the reducer CTA is
+// 4 warps x <= 128 registers, no shared memory -- one warp and 4 Ki registers per
+// SM sub-partition, inside the 5 Ki the dX kernel (6 warps x 176 registers, two
+// warps on sub-partitions 0 / 1, 214 KiB of shared memory) leaves of each 16 Ki
+// register file.  Measured on B200: this co-resides at cfg2 / cfg3; 201-register
+// reducer warps, or two 8-warp CTAs per SM, left GEMM CTAs unplaced (deadlock).
+// Virtual ranks on one GPU (connect_local) share the SMs: N reducers, each
+// capped at SMs / N.
+static int reducer_ctas(const SymmReduceArgs& A, int num_sms, bool local) {
     const int owned = (A.units + A.nranks - 1) / A.nranks;
-    return owned < 32 ? (owned > 0 ? owned : 1) : 32;
+    int cap = local ? num_sms / A.nranks : num_sms;
+    cap = cap > 0 ? cap : 1;
+    return owned < cap ? (owned > 0 ? owned : 1) : cap;
 }
 
 // fork the side stream off `st`, launch the reducer there
-static lora_status fork_reducer(lora_symm* s, const SymmReduceArgs& A, cudaStream_t st, int* launches) {
+// The side stream must not wait for the GEMM (the reducer runs next to it): the
+// fork event is recorded on `st` BEFORE the GEMM (record_fork), the reducer is
+// launched after the GEMM has been enqueued.
+static lora_status record_fork(lora_symm* s, cudaStream_t st) {
     cudaError_t e = cudaEventRecord(s->ev_fork, st);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(s->side, s->ev_fork, 0);
-    if (e != cudaSuccess) return cuda_fail(e, "symm: fork the reducer stream");
-    if ((e = launch_symm_reduce(A, reducer_ctas(A), s->side)) != cudaSuccess) return cuda_fail(e, "symm reduce launch");
+    return e == cudaSuccess ? LORA_OK : cuda_fail(e, "symm: fork the reducer stream");
+}
+
+static lora_status fork_reducer(lora_symm* s, const SymmReduceArgs& A, cudaStream_t st, int* launches,
+                                bool forked_already) {
+    cudaError_t e = cudaSuccess;
+    if (!forked_already) {
+        lora_status fs = record_fork(s, st);
+        if (fs != LORA_OK) return fs;
+    }
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->dev);
+    if ((e = launch_symm_reduce(A, reducer_ctas(A, sms, s->local), s->side)) != cudaSuccess)
+        return cuda_fail(e, "symm reduce launch");
     ++*launches;
     return LORA_OK;
 }
@@ -341,6 +404,7 @@ lora_status lora_symm_connect_local(int nranks, lora_symm* const* group) {
         for (int q = 0; q < nranks; ++q) group[r]->peer[q] = group[q]->base;
         group[r]->nranks = nranks;
         group[r]->rank = r;
+        group[r]->local = true;
     }
     return LORA_OK;
 }
@@ -396,15 +460,23 @@ lora_status lora_tp_linear_fwd_fused(lora_symm* s, const lora_dims* local, const
         set_launches(launches);
         return st;
     }
-    if ((st = fork_reducer(s, A, cs, &launches)) != LORA_OK) return st;
+    if ((st = record_fork(s, cs)) != LORA_OK) return st;
     for (int g = 0; g < col.count; ++g) {
         col.p[g].unit_flags = reinterpret_cast<uint32_t*>(s->base + kFlagsOff);
         col.p[g].sk_partial = nullptr;
     }
-    st = launch_collected(kModeFwd, col, cs, &launches);
-    const lora_status sj = join_reducer(s, cs);   // (also on failure: never leave the fork dangling)
+    col.no_coop = true;
+    // the GEMM is enqueued BEFORE the reducer: its persistent CTAs (which own the
+    // tiles the reducer waits for) are placed first, the reducer's fill in next to
+    // them -- the reverse order can leave GEMM CTAs unplaceable behind reducer CTAs
+    if ((st = launch_collected(kModeFwd, col, cs, &launches)) != LORA_OK) {
+        set_launches(launches);
+        return st;
+    }
+    if ((st = fork_reducer(s, A, cs, &launches, /*after_gemm=*/true)) != LORA_OK) return st;
+    st = join_reducer(s, cs);
     set_launches(launches);
-    return st != LORA_OK ? st : sj;
+    return st;
 }
 
 lora_status lora_tp_linear_bwd_column_group_fused(lora_symm* s, lora_comm* comm, int count, const lora_dims* local,
@@ -446,19 +518,28 @@ lora_status lora_tp_linear_bwd_column_group_fused(lora_symm* s, lora_comm* comm,
         cudaStream_t cs;
         bool forked;
     } ctx = {s, &A, cs, false};
-    // right before the grouped dX kernel: every member publishes its units, the reducer
-    // (forked here) sums them over members and ranks while K2 runs; K3 follows on `cs`
+    // right before the grouped dX kernel: every member publishes its units, and the
+    // side stream forks off here; right after K2 is enqueued the reducer is launched
+    // (GEMM first: see lora_tp_linear_fwd_fused) and sums the units over members and
+    // ranks while K2 runs; K3 follows on `cs`
     auto before_k2 = [](void* c, GemmCollector* col, int* launches) -> lora_status {
+        (void)launches;
         Ctx& k = *static_cast<Ctx*>(c);
         for (int g = 0; g < col->count; ++g) {
             col->p[g].unit_flags = reinterpret_cast<uint32_t*>(k.s->base + kFlagsOff) + int64_t(g) * k.A->units;
             col->p[g].sk_partial = nullptr;
         }
-        lora_status r = fork_reducer(k.s, *k.A, k.cs, launches);
+        // a cooperative dX launch would wait for the resident reducer, which waits for it
+        col->no_coop = true;
+        lora_status r = record_fork(k.s, k.cs);
         k.forked = r == LORA_OK;
         return r;
     };
-    st = bwd_grouped_impl(count, local, probs, 0, workspace, workspace_bytes, stream, nullptr, nullptr, before_k2,
+    auto after_k2 = [](void* c, int* launches) -> lora_status {
+        Ctx& k = *static_cast<Ctx*>(c);
+        return fork_reducer(k.s, *k.A, k.cs, launches, true);
+    };
+    st = bwd_grouped_impl(count, local, probs, 0, workspace, workspace_bytes, stream, after_k2, &ctx, before_k2,
                           &ctx);
     int launches = get_launches();
     if (ctx.forked) {
