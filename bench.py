@@ -317,6 +317,24 @@ class StepRunner:
                     lin[i]["x_sets"].append(xk)
             for e in lin:
                 e["dy_sets"].append(torch.empty_like(e["dy_sets"][0]))
+        # TP: the LoRA gradients that are partial sums on each rank (column: dA, row: dB;
+        # DESIGN.md R11-R12) are views of ONE flat fp32 bucket per buffer set, reduced by a
+        # single all-reduce at the end of the step instead of one per linear
+        self.grad_bucket = None
+        if comm is not None:
+            sizes = [(e["l"].r * e["spec"].local_n) if e["spec"].mode == tp.COLUMN
+                     else (e["spec"].local_m * e["l"].r) for e in lin]
+            total = sum(sizes)
+            self.grad_bucket = [torch.zeros(total, dtype=torch.float32, device=dev) for _ in range(nsets)]
+            for k in range(nsets):
+                off = 0
+                for e, sz in zip(lin, sizes):
+                    view = self.grad_bucket[k][off:off + sz]
+                    if e["spec"].mode == tp.COLUMN:
+                        e["da_sets"][k] = view.view(e["l"].r, e["spec"].local_n)
+                    else:
+                        e["db_sets"][k] = view.view(e["spec"].local_m, e["l"].r)
+                    off += sz
         self.lin = lin
         self.nsets = nsets
         self.use_set(0)
@@ -468,21 +486,22 @@ class StepRunner:
                                                      for e in members], [e["l"].alpha for e in members],
                                                     comm=comm, part_offset=part, dx_offset=out,
                                                     outs=[(e["da"], e["db"]) for e in members],
-                                                    reduce_lora_grads=True, workspace=wsb, stream=cur)
+                                                    reduce_lora_grads=False, workspace=wsb, stream=cur)
                 self.launches += L.lora_last_launch_count()
             elif wsb is not None:
                 tp.tp_linear_bwd_column_group(comm, [e["spec"] for e in members],
                                               [(e["x"], e["w0"], e["a"], e["b"], e["dy"], e["h"]) for e in members],
                                               [e["l"].alpha for e in members], dx_sum=dx_sum[self.k],
                                               outs=[(e["dx"], e["da"], e["db"]) for e in members], workspace=wsb,
-                                              stream=cur)
+                                              reduce_lora_grads=False, stream=cur)
                 self.launches += L.lora_last_launch_count()
             else:
                 for e in members:
                     tp.tp_linear_bwd(comm, e["spec"], e["x"], e["w0"], e["a"], e["b"], e["dy"], e["l"].alpha,
                                      h_saved=e["h"], dx=e["dx"], da=e["da"], db=e["db"], workspace=e["ws_b"],
-                                     reduce_lora_grads=True, stream=cur)
+                                     reduce_lora_grads=False, stream=cur)
                     self.launches += L.lora_last_launch_count()
+        comm.allreduce(self.grad_bucket[self.k], stream=cur)   # every partial LoRA gradient of the step
 
     def _step_single(self, ev):
         L, tp, comm = self.L, self.tp, self.comm
@@ -510,8 +529,10 @@ class StepRunner:
             else:
                 tp.tp_linear_bwd(comm, e["spec"], e["x"], e["w0"], e["a"], e["b"], e["dy"], e["l"].alpha,
                                  h_saved=e["h"], dx=e["dx"], da=e["da"], db=e["db"], workspace=e["ws_b"],
-                                 reduce_lora_grads=True, stream=cur)
+                                 reduce_lora_grads=False, stream=cur)
             self.launches += L.lora_last_launch_count()
+        if comm is not None:
+            comm.allreduce(self.grad_bucket[self.k], stream=cur)   # every partial LoRA gradient of the step
 
     def capture(self, k=0):
         """The whole step (every fwd + bwd launch, and under TP every NCCL

@@ -262,7 +262,11 @@ int lora_comm_rank(const lora_comm* comm);
 lora_status lora_allreduce(lora_comm* comm, void* buf, size_t count, lora_dtype dtype,
                            void* stream);
 
-/* Row mode: only rank 0 adds the bias (it is not sharded). */
+/* Row mode: only rank 0 adds the bias (it is not sharded).  Row mode with
+ * N > 1 and T >= 4096 runs in 4 token slices (multiples of 256 rows; LORA_TP_CHUNKS=k
+ * overrides): slice i's y all-reduce runs on the communicator's side stream while
+ * the GEMM of slice i + 1 runs on `stream` (joined before return).  y and h are
+ * the same as unsliced, bit for bit (rows are independent). */
 lora_status lora_tp_linear_fwd(lora_comm* comm, lora_tp_mode mode, const lora_dims* local,
                                const void* x, const void* w0, const void* a, const void* b,
                                const void* bias, void* y, float* h_out,

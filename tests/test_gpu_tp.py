@@ -135,3 +135,37 @@ def test_tp_column_group_graph_replay(comm):
         torch.cuda.synchronize()
         for u, v in zip(got, [ref_sum] + [t for o in ref for t in o]):
             assert torch.equal(u, v), f"replay {seed}"
+
+
+@pytest.mark.parametrize("chunks", ["2", "3", "5"])
+def test_tp_row_forward_token_slices(comm, chunks, monkeypatch):
+    """ROW-parallel forward in token slices (slice i's all-reduce overlapping the GEMM
+    of slice i + 1 on the communicator's side stream): y and h bitwise equal to the
+    unsliced call, including a ragged last slice, eager and replayed as a CUDA graph."""
+    import paper_2403_11366_b200 as L
+    from paper_2403_11366_b200 import tp
+    T, n, m, r = 1300, 256, 384, 8
+    d = make_lora_inputs(T, n, m, r, seed=63, bias=True)
+    x, w0, a, b, bias = (dev_bf16(d[k]) for k in ("x", "w0", "a", "b", "bias"))
+    spec = tp.ShardSpec(tp.ROW, 1, 0, n, m)
+    y1, h1 = L.lora_linear_fwd(x, w0, a, b, 16.0, bias=bias)
+    monkeypatch.setenv("LORA_TP_CHUNKS", chunks)
+    y2, h2 = tp.tp_linear_fwd(comm, spec, x, w0, a, b, 16.0, bias=bias)
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y2) and torch.equal(h1, h2)
+    # graph capture of the sliced fork / join
+    y3 = torch.empty_like(y1)
+    h3 = torch.empty_like(h1)
+    ws = torch.empty(L.lora_linear_fwd_workspace_bytes(L.dims(T, n, m, r, 16.0)) + 256, dtype=torch.uint8,
+                     device="cuda")
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            tp.tp_linear_fwd(comm, spec, x, w0, a, b, 16.0, bias=bias, y=y3, h_out=h3, workspace=ws, stream=s)
+    torch.cuda.current_stream().wait_stream(s)
+    y3.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y3) and torch.equal(h1, h3)
