@@ -351,6 +351,43 @@ lora_status lora_tp_linear_bwd_column_group_fused(lora_symm* symm, lora_comm* co
                                                   size_t part_offset, size_t dx_offset, int reduce_lora_grads,
                                                   void* workspace, size_t workspace_bytes, void* stream);
 
+/* ---------------- Merged-weight export ------------------
+ * PAPER.md:86-106 (Listing 4, huggingface_merger.py): the fine-tuned LoRA
+ * factors are folded into the base weights, W' = bf16(W0 + s B A) (Eq. 1 line 2,
+ * PAPER.md:118), and the model is saved in a Hugging Face-loadable format.  The
+ * file is safetensors: u64 little-endian header length, JSON header
+ * {name: {"dtype", "shape", "data_offsets"}, "__metadata__": {"format": "pt"}}
+ * padded with spaces to 8 bytes, then the raw tensors in order.
+ *
+ * lora_write_safetensors: HOST tensors, written as they are (CPU only).
+ * lora_export_merged: DEVICE tensors; an entry with a and b non-NULL is merged on
+ * the GPU (lora_merge: tensor cores; dims give d_out x d_in, rank, alpha; written
+ * as BF16 [d_out, d_in]), an entry with a == b == NULL is copied as it is (dtype,
+ * ndim, shape as given; w0 = the tensor).  The call allocates one device and one
+ * pinned host staging buffer of the largest entry, synchronizes `stream` per
+ * entry, and writes `path` (overwritten).  Names are the caller's (e.g.
+ * "model.layers.0.self_attn.q_proj.weight").  Errors: LORA_ERR_INVALID (NULL
+ * pointers, unwritable path), LORA_ERR_SHAPE, LORA_ERR_CUDA; a failed call may
+ * leave a partial file. */
+typedef struct {
+    const char* name;
+    int dtype;               /* lora_dtype */
+    int ndim;                /* 1..4 */
+    int64_t shape[4];
+    const void* data;        /* host */
+} lora_host_tensor;
+typedef struct {
+    const char* name;
+    const void* w0;          /* device: the base weight (or the tensor itself) */
+    const void* a;           /* device [rank, d_in] bf16, or NULL */
+    const void* b;           /* device [d_out, rank] bf16, or NULL */
+    lora_dims dims;          /* merged entries: d_out, d_in, rank, alpha (tokens ignored) */
+    int dtype, ndim;         /* unmerged entries */
+    int64_t shape[4];
+} lora_export_tensor;
+lora_status lora_write_safetensors(const char* path, int count, const lora_host_tensor* tensors);
+lora_status lora_export_merged(const char* path, int count, const lora_export_tensor* tensors, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -167,6 +167,21 @@ lib.lora_tp_linear_bwd_column_group_fused.argtypes = [_vp, _vp, ctypes.c_int, _d
                                                       ctypes.c_size_t, _vp]
 lib.lora_tp_linear_bwd_column_group_fused.restype = _st
 
+class lora_host_tensor(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char_p), ("dtype", ctypes.c_int), ("ndim", ctypes.c_int),
+                ("shape", ctypes.c_int64 * 4), ("data", ctypes.c_void_p)]
+
+
+class lora_export_tensor(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char_p), ("w0", ctypes.c_void_p), ("a", ctypes.c_void_p), ("b", ctypes.c_void_p),
+                ("dims", lora_dims), ("dtype", ctypes.c_int), ("ndim", ctypes.c_int), ("shape", ctypes.c_int64 * 4)]
+
+
+lib.lora_write_safetensors.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(lora_host_tensor)]
+lib.lora_write_safetensors.restype = _st
+lib.lora_export_merged.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(lora_export_tensor), _vp]
+lib.lora_export_merged.restype = _st
+
 lib.lora_captured_sync_words_free.restype = ctypes.c_int
 lib.lora_profile_next_bwd.argtypes = [ctypes.POINTER(_vp)]
 lib.lora_profile_next_bwd.restype = _st
@@ -459,3 +474,48 @@ def lora_adam_step(tensors, step, lr, betas=(0.9, 0.999), eps=1e-8, stream=None)
         arr[i] = lora_adam_tensor(_ptr(p), _ptr(w), _ptr(g), _ptr(m), _ptr(v), numel)
     hp = lora_adam_hparams(float(lr), float(betas[0]), float(betas[1]), float(eps))
     _check(lib.lora_adam_step(n, arr, ctypes.byref(hp), int(step), _stream(stream)), "lora_adam_step")
+
+
+# ------------------------------------------------ merged-weight export (N3)
+def _dt_code(dtype):
+    if dtype in (torch.float32, "float32", "f32"):
+        return 0
+    if dtype in (torch.bfloat16, "bfloat16", "bf16"):
+        return 1
+    raise ValueError(f"unsupported dtype {dtype} (float32 / bfloat16)")
+
+
+def write_safetensors(path, tensors):
+    """lora_write_safetensors: {name: contiguous CPU torch tensor (float32 / bfloat16)}."""
+    items = list(tensors.items())
+    arr = (lora_host_tensor * max(1, len(items)))()
+    keep = []
+    for i, (name, t) in enumerate(items):
+        t = t.contiguous()
+        keep.append(t)
+        shp = (ctypes.c_int64 * 4)(*(list(t.shape) + [0] * (4 - t.dim())))
+        arr[i] = lora_host_tensor(name.encode(), _dt_code(t.dtype), t.dim(), shp, t.data_ptr())
+    _check(lib.lora_write_safetensors(str(path).encode(), len(items), arr), "lora_write_safetensors")
+
+
+def export_merged(path, entries, stream=None):
+    """lora_export_merged.  entries: list of (name, w0, a, b, alpha) -- merged on the
+    GPU into W0 + s B A -- or (name, tensor) -- written as it is (CUDA tensors)."""
+    arr = (lora_export_tensor * max(1, len(entries)))()
+    for i, ent in enumerate(entries):
+        name = ent[0].encode()
+        if len(ent) == 5:
+            _, w0, a, b, alpha = ent
+            m, n = w0.shape
+            r = a.shape[0]
+            _bf16(w0, "w0", (m, n)); _bf16(a, "a", (r, n)); _bf16(b, "b", (m, r))
+            arr[i] = lora_export_tensor(name, _ptr(w0), _ptr(a), _ptr(b), dims(0, n, m, r, alpha), 1, 2,
+                                        (ctypes.c_int64 * 4)(m, n, 0, 0))
+        else:
+            t = ent[1]
+            if not (t.is_cuda and t.is_contiguous()):
+                raise ValueError(f"{ent[0]}: must be a contiguous CUDA tensor")
+            shp = (ctypes.c_int64 * 4)(*(list(t.shape) + [0] * (4 - t.dim())))
+            arr[i] = lora_export_tensor(name, _ptr(t), None, None, lora_dims(0, 0, 0, 0, 0.0), _dt_code(t.dtype),
+                                        t.dim(), shp)
+    _check(lib.lora_export_merged(str(path).encode(), len(entries), arr, _stream(stream)), "lora_export_merged")

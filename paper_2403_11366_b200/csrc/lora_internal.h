@@ -32,6 +32,8 @@ lora_status bwd_grouped_impl(int count, const lora_dims* dims, const lora_bwd_pr
                              lora_status (*before_k2)(void* bctx, GemmCollector* col, int* launches) = nullptr,
                              void* bctx = nullptr);
 int r_pad_of(int r);
+lora_status merge_impl(const lora_dims* d, const void* w0, const void* a, const void* b, void* w_out,
+                       cudaStream_t stream, int* launches);
 // load the kernels launched next to spinning kernels (reducer, NCCL) -- lora_symm.cu
 lora_status preload_kernels();
 
