@@ -388,6 +388,37 @@ typedef struct {
 lora_status lora_write_safetensors(const char* path, int count, const lora_host_tensor* tensors);
 lora_status lora_export_merged(const char* path, int count, const lora_export_tensor* tensors, void* stream);
 
+/* ---------------- Decoder-layer pieces -------------------
+ * The Llama-2 decoder layer (JORA builds on a Llama-2
+ * implementation; :195 the long-sequence RAFT setting) around the seven LoRA
+ * linears: RMSNorm, rotary position embedding, SwiGLU.  Device pointers, bf16
+ * row-major, 16-byte aligned; fp32 math, one RNE per output.  The attention is
+ * a library call (cuDNN SDPA) made by the Python layer.
+ *
+ * lora_rmsnorm_fwd: x2 = x + res (bf16; res may be NULL -> x2 = x; written to
+ *   x2_out if non-NULL), rstd[t] = 1/sqrt(mean_k x2[t,k]^2 + eps) (fp32 [T]),
+ *   y = g * (x2 * rstd).  dim % 8 == 0, 8 <= dim <= 8192.
+ * lora_rmsnorm_bwd: dx = dres + rstd * (g.dy - xh * mean(xh * g.dy)),
+ *   xh = x2 * rstd (g frozen: no dg; dres may be NULL).
+ * lora_rope: in place on q [T, ld] (heads x head_dim used per row), pair
+ *   (i, i + head_dim/2) of a head rotated by angle (pos0 + t) * theta^(-2i/head_dim);
+ *   inverse = 1 applies the transposed rotation (the backward).
+ * lora_swiglu_fwd: out = silu(gate) * up, count elements.
+ * lora_swiglu_bwd: dgate = da * up * silu'(gate), dup = da * silu(gate). */
+lora_status lora_rmsnorm_fwd(int64_t tokens, int64_t dim, float eps, const void* x, const void* res, const void* g,
+                             void* y, void* x2_out, float* rstd, void* stream);
+lora_status lora_rmsnorm_bwd(int64_t tokens, int64_t dim, const void* dy, const void* x2, const void* g,
+                             const float* rstd, const void* dres, void* dx, void* stream);
+lora_status lora_rope(int64_t tokens, int heads, int head_dim, int64_t ld, int64_t pos0, float theta, int inverse,
+                      void* q, void* stream);
+lora_status lora_swiglu_fwd(int64_t count, const void* gate, const void* up, void* out, void* stream);
+lora_status lora_swiglu_bwd(int64_t count, const void* gate, const void* up, const void* da, void* dgate, void* dup,
+                            void* stream);
+/* dst = bf16(sum_i srcs[i]) over `count` elements (fp32 accumulation in i order,
+ * one RNE; 1 <= n <= LORA_MAX_GROUP; dst may alias srcs[0]): residual adds and the
+ * members' dX partials of a group sharing an input. */
+lora_status lora_sum_bf16(int64_t count, int n, const void* const* srcs, void* dst, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -182,6 +182,20 @@ lib.lora_write_safetensors.restype = _st
 lib.lora_export_merged.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(lora_export_tensor), _vp]
 lib.lora_export_merged.restype = _st
 
+_i64 = ctypes.c_int64
+lib.lora_rmsnorm_fwd.argtypes = [_i64, _i64, ctypes.c_float, _vp, _vp, _vp, _vp, _vp, _fp, _vp]
+lib.lora_rmsnorm_fwd.restype = _st
+lib.lora_rmsnorm_bwd.argtypes = [_i64, _i64, _vp, _vp, _vp, _fp, _vp, _vp, _vp]
+lib.lora_rmsnorm_bwd.restype = _st
+lib.lora_rope.argtypes = [_i64, ctypes.c_int, ctypes.c_int, _i64, _i64, ctypes.c_float, ctypes.c_int, _vp, _vp]
+lib.lora_rope.restype = _st
+lib.lora_swiglu_fwd.argtypes = [_i64, _vp, _vp, _vp, _vp]
+lib.lora_swiglu_fwd.restype = _st
+lib.lora_swiglu_bwd.argtypes = [_i64, _vp, _vp, _vp, _vp, _vp, _vp]
+lib.lora_swiglu_bwd.restype = _st
+lib.lora_sum_bf16.argtypes = [_i64, ctypes.c_int, ctypes.POINTER(_vp), _vp, _vp]
+lib.lora_sum_bf16.restype = _st
+
 lib.lora_captured_sync_words_free.restype = ctypes.c_int
 lib.lora_profile_next_bwd.argtypes = [ctypes.POINTER(_vp)]
 lib.lora_profile_next_bwd.restype = _st
@@ -519,3 +533,54 @@ def export_merged(path, entries, stream=None):
             arr[i] = lora_export_tensor(name, _ptr(t), None, None, lora_dims(0, 0, 0, 0, 0.0), _dt_code(t.dtype),
                                         t.dim(), shp)
     _check(lib.lora_export_merged(str(path).encode(), len(entries), arr, _stream(stream)), "lora_export_merged")
+
+
+# ------------------------------------------------ decoder-layer pieces (N4)
+def lora_rmsnorm_fwd(x, g, eps, res=None, y=None, x2_out=None, rstd=None, stream=None):
+    """y = g * (x2 * rstd), x2 = x (+ res).  Returns (y, rstd [T] fp32)."""
+    T, d = x.shape
+    _bf16(x, "x", (T, d)); _bf16(g, "g", (d,))
+    if res is not None:
+        _bf16(res, "res", (T, d))
+    y = torch.empty_like(x) if y is None else y
+    rstd = torch.empty(T, dtype=torch.float32, device=x.device) if rstd is None else rstd
+    _check(lib.lora_rmsnorm_fwd(T, d, float(eps), _ptr(x), _ptr(res), _ptr(g), _ptr(y), _ptr(x2_out), _ptr(rstd),
+                                _stream(stream)), "lora_rmsnorm_fwd")
+    return y, rstd
+
+
+def lora_rmsnorm_bwd(dy, x2, g, rstd, dres=None, dx=None, stream=None):
+    T, d = dy.shape
+    dx = torch.empty_like(dy) if dx is None else dx
+    _check(lib.lora_rmsnorm_bwd(T, d, _ptr(dy), _ptr(x2), _ptr(g), _ptr(rstd), _ptr(dres), _ptr(dx),
+                                _stream(stream)), "lora_rmsnorm_bwd")
+    return dx
+
+
+def lora_rope(q, heads, head_dim, theta=10000.0, pos0=0, inverse=False, stream=None):
+    """In place on q [T, >= heads * head_dim] (row stride q.stride(0))."""
+    T = q.shape[0]
+    _check(lib.lora_rope(T, int(heads), int(head_dim), q.stride(0), int(pos0), float(theta), 1 if inverse else 0,
+                         _ptr(q), _stream(stream)), "lora_rope")
+    return q
+
+
+def lora_swiglu_fwd(gate, up, out=None, stream=None):
+    out = torch.empty_like(gate) if out is None else out
+    _check(lib.lora_swiglu_fwd(gate.numel(), _ptr(gate), _ptr(up), _ptr(out), _stream(stream)), "lora_swiglu_fwd")
+    return out
+
+
+def lora_swiglu_bwd(gate, up, da, dgate=None, dup=None, stream=None):
+    dgate = torch.empty_like(gate) if dgate is None else dgate
+    dup = torch.empty_like(up) if dup is None else dup
+    _check(lib.lora_swiglu_bwd(gate.numel(), _ptr(gate), _ptr(up), _ptr(da), _ptr(dgate), _ptr(dup),
+                               _stream(stream)), "lora_swiglu_bwd")
+    return dgate, dup
+
+
+def lora_sum_bf16(srcs, dst=None, stream=None):
+    dst = torch.empty_like(srcs[0]) if dst is None else dst
+    arr = (_vp * len(srcs))(*[_ptr(t) for t in srcs])
+    _check(lib.lora_sum_bf16(srcs[0].numel(), len(srcs), arr, _ptr(dst), _stream(stream)), "lora_sum_bf16")
+    return dst

@@ -18,7 +18,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "liblora.so")
-SOURCES = ["lora_gemm.cu", "lora_grad.cu", "lora_grad_mma.cu", "lora_dropout.cu", "lora_aux.cu", "lora_merge_mma.cu", "lora_symm.cu", "lora_api.cpp", "lora_comm.cpp", "lora_export.cpp"]
+SOURCES = ["lora_gemm.cu", "lora_grad.cu", "lora_grad_mma.cu", "lora_dropout.cu", "lora_aux.cu", "lora_merge_mma.cu", "lora_symm.cu", "lora_layer.cu", "lora_api.cpp", "lora_comm.cpp", "lora_export.cpp"]
 HEADERS = ["sm100_ptx.cuh", "lora_philox.cuh", "lora_kernels.h", "lora_internal.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -288,6 +288,21 @@ struct MergeMaps {
 cudaError_t launch_merge_mma(const MergeMaps& maps, int r_pad, int64_t m, int64_t n, float s, int num_sms,
                              cudaStream_t stream);
 
+// decoder-layer pieces (lora_layer.cu)
+cudaError_t launch_rmsnorm_fwd(const __nv_bfloat16* x, const __nv_bfloat16* res, const __nv_bfloat16* g, int64_t T,
+                               int d, float eps, __nv_bfloat16* y, __nv_bfloat16* x2_out, float* rstd,
+                               cudaStream_t stream);
+cudaError_t launch_rmsnorm_bwd(const __nv_bfloat16* dy, const __nv_bfloat16* x2, const __nv_bfloat16* g,
+                               const float* rstd, const __nv_bfloat16* dres, int64_t T, int d, __nv_bfloat16* dx,
+                               cudaStream_t stream);
+cudaError_t launch_rope(__nv_bfloat16* q, int64_t T, int heads, int D, int64_t ld, int64_t pos0, float theta,
+                        int inverse, int num_sms, cudaStream_t stream);
+cudaError_t launch_swiglu_fwd(const __nv_bfloat16* gate, const __nv_bfloat16* up, int64_t count, __nv_bfloat16* out,
+                              int num_sms, cudaStream_t stream);
+cudaError_t launch_swiglu_bwd(const __nv_bfloat16* gate, const __nv_bfloat16* up, const __nv_bfloat16* da,
+                              int64_t count, __nv_bfloat16* dgate, __nv_bfloat16* dup, int num_sms,
+                              cudaStream_t stream);
+
 // N3: one Adam step for up to kMaxAdamTensors adapter tensors (numel % 4 == 0)
 constexpr int kMaxAdamTensors = 64;
 struct AdamTensor {
