@@ -611,6 +611,96 @@ class StepRunner:
                         "last 32 token rows of every linear, dA and dB in full"}
 
 
+# --------------------------------------------------- decoder-layer workload (N4)
+LAYERS = {   # the Llama-2 decoder layer at the RAFT sequence length
+    "layer7b": dict(T=4096, d=4096, f=11008, heads=32, head_dim=128, r=16, alpha=16.0,
+                    description="Llama-2-7B decoder layer, LoRA r=16 on q,k,v,o,gate,up,down, seq 4096"),
+    "layer13b": dict(T=4096, d=5120, f=13824, heads=40, head_dim=128, r=8, alpha=16.0,
+                     description="Llama-2-13B decoder layer, LoRA r=8 on all seven projections, seq 4096"),
+}
+
+
+def run_layer(args, key):
+    """One decoder-layer train step (forward + backward of every piece) per step,
+    timed like the linear workloads (CUDA events, L2 flushed outside the events,
+    CUDA graph when capture works).  Single GPU (N = 1); the TP composition is
+    exercised by the tests."""
+    import torch
+
+    from paper_2403_11366_b200.layer import LlamaLayerLoRA, layer_flops
+    from synth import make_layer_inputs
+    c = LAYERS[key]
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(0)
+    import __graft_entry__
+    __graft_entry__._build_module().build()
+    import paper_2403_11366_b200 as L
+    L.lora_device_check()
+    bits = make_layer_inputs(c["T"], c["d"], c["f"], c["heads"], c["r"], seed=2403)
+    cfg = dict(heads=c["heads"], head_dim=c["head_dim"], eps=1e-5, theta=10000.0, alpha=c["alpha"], ffn=c["f"])
+    params = {k: _bits_to_dev(v, dev) for k, v in bits.items() if k not in ("x", "dout")}
+    x, dout = _bits_to_dev(bits["x"], dev), _bits_to_dev(bits["dout"], dev)
+    layer = LlamaLayerLoRA(params, cfg)
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    flush_w = torch.empty(max(2 * l2, 256 << 20) // 4, dtype=torch.float32, device=dev)
+    flush_r = torch.zeros_like(flush_w)
+
+    def step():
+        layer.forward(x)
+        layer.backward(dout)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    graph = None
+    if args.graph != "off":
+        try:
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(s):
+                with torch.cuda.graph(graph, stream=s):
+                    step()
+            torch.cuda.current_stream().wait_stream(s)
+            for _ in range(2):
+                graph.replay()
+            torch.cuda.synchronize()
+        except Exception as ex:
+            print(f"bench: layer graph capture failed ({ex!r}); timing eager steps", file=sys.stderr)
+            graph = None
+            torch.cuda.synchronize()
+    K = args.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    with ClockSampler(0) as clk:
+        for i in range(K):
+            flush_w.fill_(float(i & 0xFF))
+            torch.sum(flush_r)
+            ev[i][0].record()
+            if graph is not None:
+                graph.replay()
+            else:
+                step()
+            ev[i][1].record()
+        torch.cuda.synchronize()
+    ms = [a.elapsed_time(b) for a, b in ev]
+    total = float(np.sum(ms))
+    fl = layer_flops(c["T"], c["d"], c["f"], c["heads"], c["head_dim"], c["r"])
+    peaks, peak_src = load_peaks()
+    value = fl * K / (total * 1e-3) / 1e12
+    print(json.dumps({
+        "metric": "LoRA Llama-2 decoder-layer fwd+bwd TFLOP/s and tokens/s", "value": value, "unit": "TFLOP/s",
+        "n_gpus": 1, "steps": K, "warmup": args.warmup, "ms_per_step": total / K, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": key, "description": c["description"], "tokens": c["T"], "rank": c["r"],
+                   "cuda_graph": graph is not None, "attention": "cuDNN SDPA (causal), library call",
+                   "l2": "flushed between timed steps (outside the event pairs)"},
+        "tokens_per_s": c["T"] * K / (total * 1e-3),
+        "pct_of_bf16_peak": value / peaks["bf16_tflops"] * 100.0,
+        "flops_per_step": fl, "peak_source": peak_src,
+        "step_ms_median": float(np.median(ms)), "clocks": clk.summary()}), flush=True)
+    return 0
+
+
 # ----------------------------------------------------------------- GPU leg
 def run_ours(args, wl):
     import torch
@@ -1005,12 +1095,16 @@ def main():
                     help="LoRA dropout p (Listing 3 LORA_DROPOUT = 0.05); 0 = the north-star path")
     ap.add_argument("--no-group", action="store_true",
                     help="one call per linear instead of grouped calls for linears sharing an input")
+    ap.add_argument("--layer", choices=sorted(LAYERS), default=None,
+                    help="time the Llama-2 decoder-layer train step (SURVEY 8(f) N4) instead of the LoRA linears")
     ap.add_argument("--comm", choices=["nccl", "fused"], default="nccl",
                     help="TP activation all-reduces: NCCL calls after the GEMMs, or fused into the GEMMs over "
                          "peer memory (lora_symm, SURVEY 8(f) N2)")
     ap.add_argument("--graph", choices=["auto", "on", "off"], default="auto",
                     help="replay each step as one CUDA graph (auto: at every N, eager if capture fails)")
     args = ap.parse_args()
+    if args.layer:   # the decoder-layer workload
+        return run_layer(args, args.layer)
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     cfg = args.config or ("cfg2" if world == 1 else "cfg3")
     wl = WORKLOADS[cfg]

@@ -56,6 +56,8 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 }
 
 // one CTA of 128 threads per row; thread i owns 16-byte vectors i, i + 128, ...
+// (NV of them: the register arrays are sized for the row, not for the largest d)
+template <int NV>
 __global__ void __launch_bounds__(kRowThreads) rmsnorm_fwd_kernel(const __nv_bfloat16* __restrict__ x,
                                                                   const __nv_bfloat16* __restrict__ res,
                                                                   const __nv_bfloat16* __restrict__ g, int64_t T,
@@ -66,10 +68,10 @@ __global__ void __launch_bounds__(kRowThreads) rmsnorm_fwd_kernel(const __nv_bfl
     const int64_t t = blockIdx.x;
     if (t >= T) return;
     const int nv = d / 8;
-    float v[kMaxVec][8];
+    float v[NV][8];
     float ss = 0.0f;
 #pragma unroll
-    for (int j = 0; j < kMaxVec; ++j) {
+    for (int j = 0; j < NV; ++j) {
         const int c = threadIdx.x + j * kRowThreads;
         if (c >= nv) break;
         unpack8(*reinterpret_cast<const uint4*>(x + t * d + 8 * c), v[j]);
@@ -88,7 +90,7 @@ __global__ void __launch_bounds__(kRowThreads) rmsnorm_fwd_kernel(const __nv_bfl
     const float rstd = rsqrtf(block_sum(ss, red) / static_cast<float>(d) + eps);
     if (threadIdx.x == 0 && rstd_out) rstd_out[t] = rstd;
 #pragma unroll
-    for (int j = 0; j < kMaxVec; ++j) {
+    for (int j = 0; j < NV; ++j) {
         const int c = threadIdx.x + j * kRowThreads;
         if (c >= nv) break;
         float gv[8], o[8];
@@ -99,6 +101,7 @@ __global__ void __launch_bounds__(kRowThreads) rmsnorm_fwd_kernel(const __nv_bfl
     }
 }
 
+template <int NV>
 __global__ void __launch_bounds__(kRowThreads) rmsnorm_bwd_kernel(const __nv_bfloat16* __restrict__ dy,
                                                                   const __nv_bfloat16* __restrict__ x2,
                                                                   const __nv_bfloat16* __restrict__ g,
@@ -110,10 +113,10 @@ __global__ void __launch_bounds__(kRowThreads) rmsnorm_bwd_kernel(const __nv_bfl
     if (t >= T) return;
     const int nv = d / 8;
     const float rstd = rstd_in[t];
-    float xh[kMaxVec][8], gy[kMaxVec][8];
+    float xh[NV][8], gy[NV][8];
     float dot = 0.0f;
 #pragma unroll
-    for (int j = 0; j < kMaxVec; ++j) {
+    for (int j = 0; j < NV; ++j) {
         const int c = threadIdx.x + j * kRowThreads;
         if (c >= nv) break;
         float dv[8], gv[8];
@@ -129,7 +132,7 @@ __global__ void __launch_bounds__(kRowThreads) rmsnorm_bwd_kernel(const __nv_bfl
     }
     const float mean = block_sum(dot, red) / static_cast<float>(d);
 #pragma unroll
-    for (int j = 0; j < kMaxVec; ++j) {
+    for (int j = 0; j < NV; ++j) {
         const int c = threadIdx.x + j * kRowThreads;
         if (c >= nv) break;
         float o[8], rv[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
@@ -223,7 +226,12 @@ cudaError_t launch_rmsnorm_fwd(const __nv_bfloat16* x, const __nv_bfloat16* res,
                                cudaStream_t stream) {
     if (T <= 0) return cudaSuccess;
     if (d % 8 != 0 || d > kRowThreads * kMaxVec * 8) return cudaErrorInvalidValue;
-    rmsnorm_fwd_kernel<<<static_cast<unsigned>(T), kRowThreads, 0, stream>>>(x, res, g, T, d, eps, y, x2_out, rstd);
+    const int nv = (d / 8 + kRowThreads - 1) / kRowThreads;
+    const unsigned grid = static_cast<unsigned>(T);
+    if (nv <= 1) rmsnorm_fwd_kernel<1><<<grid, kRowThreads, 0, stream>>>(x, res, g, T, d, eps, y, x2_out, rstd);
+    else if (nv <= 2) rmsnorm_fwd_kernel<2><<<grid, kRowThreads, 0, stream>>>(x, res, g, T, d, eps, y, x2_out, rstd);
+    else if (nv <= 4) rmsnorm_fwd_kernel<4><<<grid, kRowThreads, 0, stream>>>(x, res, g, T, d, eps, y, x2_out, rstd);
+    else rmsnorm_fwd_kernel<8><<<grid, kRowThreads, 0, stream>>>(x, res, g, T, d, eps, y, x2_out, rstd);
     return cudaGetLastError();
 }
 
@@ -232,7 +240,12 @@ cudaError_t launch_rmsnorm_bwd(const __nv_bfloat16* dy, const __nv_bfloat16* x2,
                                cudaStream_t stream) {
     if (T <= 0) return cudaSuccess;
     if (d % 8 != 0 || d > kRowThreads * kMaxVec * 8) return cudaErrorInvalidValue;
-    rmsnorm_bwd_kernel<<<static_cast<unsigned>(T), kRowThreads, 0, stream>>>(dy, x2, g, rstd, dres, T, d, dx);
+    const int nv = (d / 8 + kRowThreads - 1) / kRowThreads;
+    const unsigned grid = static_cast<unsigned>(T);
+    if (nv <= 1) rmsnorm_bwd_kernel<1><<<grid, kRowThreads, 0, stream>>>(dy, x2, g, rstd, dres, T, d, dx);
+    else if (nv <= 2) rmsnorm_bwd_kernel<2><<<grid, kRowThreads, 0, stream>>>(dy, x2, g, rstd, dres, T, d, dx);
+    else if (nv <= 4) rmsnorm_bwd_kernel<4><<<grid, kRowThreads, 0, stream>>>(dy, x2, g, rstd, dres, T, d, dx);
+    else rmsnorm_bwd_kernel<8><<<grid, kRowThreads, 0, stream>>>(dy, x2, g, rstd, dres, T, d, dx);
     return cudaGetLastError();
 }
 
