@@ -1024,7 +1024,8 @@ def run_ours(args, wl):
                        "tokens": tokens, "rank": l0.r, "alpha": l0.alpha,
                        "global_batch": 1, "seq_len": tokens,
                        "parallelism": f"tp{world}" if comm is not None else "single",
-                       "tp_comm": (("fused into the GEMMs over peer memory (lora_symm)" if args.comm == "fused"
+                       "tp_comm": (("fused into the GEMMs over peer memory (lora_symm), reducer "
+                                    + str(R.symm.last_placement) if args.comm == "fused"
                                     else "NCCL all-reduce after the GEMMs") if comm is not None else None),
                        "cuda_graph": graph is not None,
                        "grouped_calls": ([[wl.linears[i].name for i in g] for g in wl.groups] if grouped else None),

@@ -329,6 +329,11 @@ lora_status lora_symm_connect(lora_symm* symm, int nranks, int rank, const uint8
 lora_status lora_symm_connect_local(int nranks, lora_symm* const* group);
 void* lora_symm_ptr(const lora_symm* symm);        /* this rank's data region (device) */
 size_t lora_symm_bytes(const lora_symm* symm);
+/* Where the last fused call's reducer ran (diagnostics): 1 co-resident with the
+ * GEMM (overlapping it), 2 after the GEMM (no reducer variant fits next to that
+ * GEMM's registers), 3 virtual ranks (GEMMs capped to SMs - 16, reducers on the
+ * rest); 0 before any call. */
+int lora_symm_last_placement(const lora_symm* symm);
 lora_status lora_symm_destroy(lora_symm* symm);
 
 /* ROW-parallel forward (o, down) with the y all-reduce fused into the GEMM:

@@ -157,6 +157,8 @@ lib.lora_symm_ptr.argtypes = [_vp]
 lib.lora_symm_ptr.restype = _vp
 lib.lora_symm_bytes.argtypes = [_vp]
 lib.lora_symm_bytes.restype = ctypes.c_size_t
+lib.lora_symm_last_placement.argtypes = [_vp]
+lib.lora_symm_last_placement.restype = ctypes.c_int
 lib.lora_symm_destroy.argtypes = [_vp]
 lib.lora_symm_destroy.restype = _st
 lib.lora_tp_linear_fwd_fused.argtypes = [_vp, _dp, _vp, _vp, _vp, _vp, _vp, ctypes.c_size_t, ctypes.c_size_t, _fp,

@@ -281,6 +281,9 @@ lora_status fwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
     if (cg == 2 && (st = encode_2d(&maps.w2, w0, n, m, n * 2, 64, BN - 128, 128, "w0")) != LORA_OK) return st;
     if ((st = encode_2d(&maps.nar, a, n, r, n * 2, 64, rp, 128, "a")) != LORA_OK) return st;
     if ((st = encode_2d(&maps.tail, bsrc, r8, m, r8 * 2, rp, BN / cg, rp * 2, "b")) != LORA_OK) return st;
+    // the TMA-store epilogue's output maps: y [T, m], boxes [128 x 32] SW64 and [128 x 16] SW32
+    if ((st = encode_2d(&maps.out32, y, m, T, m * 2, 32, 128, 64, "y")) != LORA_OK) return st;
+    if ((st = encode_2d(&maps.out16, y, m, T, m * 2, 16, 128, 32, "y")) != LORA_OK) return st;
     FusedGemmParams p;
     p.T = T; p.K = n; p.N_out = m; p.r = r;
     p.scale = d->alpha / static_cast<float>(r);
@@ -522,7 +525,8 @@ lora_status launch_collected(int mode, GemmCollector& col, cudaStream_t stream, 
             ++grp.count;
             done[j] = true;
         }
-        cudaError_t e = launch_fused_gemm_group(mode, col.rp[i], col.cg[i], grp, dev.sms, stream);
+        const int sms = (col.max_sms > 0 && col.max_sms < dev.sms) ? col.max_sms : dev.sms;
+        cudaError_t e = launch_fused_gemm_group(mode, col.rp[i], col.cg[i], grp, sms, stream);
         if (e != cudaSuccess) return cuda_fail(e, "grouped fused GEMM launch");
         ++*launches;
     }
@@ -622,6 +626,8 @@ lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
         maps.w2 = maps.w;
         if ((st = encode_2d(&maps.nar, bsrc, r8, m, r8 * 2, nar_h, 64, nar_h * 2, "b")) != LORA_OK) return st;
         if ((st = encode_2d(&maps.tail, a, n, r, n * 2, 64, rp, 128, "a")) != LORA_OK) return st;
+        if ((st = encode_2d(&maps.out32, dx, n, T, n * 2, 32, 128, 64, "dx")) != LORA_OK) return st;
+        if ((st = encode_2d(&maps.out16, dx, n, T, n * 2, 16, 128, 32, "dx")) != LORA_OK) return st;
         FusedGemmParams p;
         p.T = T; p.K = m; p.N_out = n; p.r = r; p.scale = s;
         p.bias = nullptr;

@@ -71,6 +71,9 @@ __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 #ifndef LORA_STAGES_CAP
 #define LORA_STAGES_CAP 8
 #endif
+#ifndef LORA_TMA_STORE   // 0: the epilogue stores y / dX with per-thread 16-byte stores (comparison)
+#define LORA_TMA_STORE 1
+#endif
 
 template <int MODE, int R_PAD, int CG>
 struct GemmCfg {
@@ -99,8 +102,17 @@ struct GemmCfg {
     static constexpr int SH_BYTES = BM * TAIL_ROW;                // bf16(s h) / bf16(gh) tile
     static constexpr int BAR_BYTES = 1024;
     static constexpr int TAIL_BUFS = (MODE == kModeDxDrop) ? 2 : 1;   // dropout: double-buffered A tile
-    static constexpr int FIXED = TAIL_BUFS * round_up(TAILB_BYTES, 1024) + round_up(SH_BYTES, 1024) +
-                                 BAR_BYTES + 1024 /* alignment slack */;
+    static constexpr int FIXED0 = TAIL_BUFS * round_up(TAILB_BYTES, 1024) + round_up(SH_BYTES, 1024) +
+                                  BAR_BYTES + 1024 /* alignment slack */;
+    // TMA-store epilogue: 8 KiB staging buffers ([128 rows][32 columns] bf16, SW64),
+    // two when they cost no pipeline stage, else one, else none (per-thread stores)
+    static constexpr int STG_BYTES = BM * 32 * 2;
+    static constexpr int STAGES0 = cmin(LORA_STAGES_CAP, (SMEM_LIMIT - FIXED0) / STAGE_BYTES);
+    static constexpr int STG_BUFS = !LORA_TMA_STORE ? 0
+        : (cmin(LORA_STAGES_CAP, (SMEM_LIMIT - FIXED0 - 2 * STG_BYTES) / STAGE_BYTES) == STAGES0 ? 2
+        : (cmin(LORA_STAGES_CAP, (SMEM_LIMIT - FIXED0 - STG_BYTES) / STAGE_BYTES) == STAGES0 ? 1 : 0));
+    static constexpr bool STORE_TMA = STG_BUFS > 0;
+    static constexpr int FIXED = FIXED0 + STG_BUFS * STG_BYTES;
     static constexpr int STAGES = cmin(LORA_STAGES_CAP, (SMEM_LIMIT - FIXED) / STAGE_BYTES);
     static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + FIXED;
     static_assert(STAGES >= 2, "shared memory budget");
@@ -444,7 +456,8 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
     uint8_t* stage_base = smem;
     uint8_t* s_tailb = smem + C::STAGES * C::STAGE_BYTES;
     uint8_t* s_h = s_tailb + C::TAIL_BUFS * round_up(C::TAILB_BYTES, 1024);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(s_h + round_up(C::SH_BYTES, 1024));
+    uint8_t* s_stg = s_h + round_up(C::SH_BYTES, 1024);            // TMA-store staging (STG_BUFS x 8 KiB)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(s_stg + C::STG_BUFS * C::STG_BYTES);
     uint64_t* full = bars;
     uint64_t* empty = bars + C::STAGES;
     uint64_t* tmem_full = bars + 2 * C::STAGES;
@@ -472,6 +485,10 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
         if (MODE == kModeFwd && CG == 2) tma_prefetch_desc(&mp.w2);
         tma_prefetch_desc(&mp.nar);
         tma_prefetch_desc(&mp.tail);
+        if (C::STORE_TMA) {
+            tma_prefetch_desc(&mp.out32);
+            tma_prefetch_desc(&mp.out16);
+        }
     }
     if (warp == 1 && lane == 0) {
         for (int s = 0; s < C::STAGES; ++s) {
@@ -939,6 +956,8 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
                 for (int w = 0; w < NT / 32; ++w)
                     kw[w] = (row_ok && n0 / 32 + w < nw && 32 * w < width) ? p.drop_bits[row * nw + n0 / 32 + w] : 0u;
             }
+            const bool storer = (ew == 0 && lane == 0);
+            const int64_t row0 = static_cast<int64_t>(t_blk) * TM + crank * BM;   // this CTA's first row
 #pragma unroll 1
             for (int c = 0; c < width / 16; ++c) {
                 uint32_t v[16];
@@ -948,7 +967,7 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
 #ifdef LORA_PROBE_NO_STORE
                 if (false) {
 #else
-                if (row_ok && col < p.N_out) {
+                if (C::STORE_TMA || (row_ok && col < p.N_out)) {
 #endif
                     float f[16];
 #pragma unroll
@@ -956,7 +975,7 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
                     if (MODE == kModeFwd && p.bias != nullptr) {
 #pragma unroll
                         for (int e = 0; e < 16; ++e)
-                            if (col + e < p.N_out) f[e] += __bfloat162float(p.bias[col + e]);
+                            if (col + e < p.N_out) f[e] += __bfloat162float(p.bias[col + e]);   // (bias [m])
                     }
                     if constexpr (MODE == kModeDxDrop) {
                         // f += q M . (gh A): A columns of this chunk from the MN-major SW128 tile
@@ -1000,8 +1019,41 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
                     q0.z = pack_bf16x2(f[4], f[5]);   q0.w = pack_bf16x2(f[6], f[7]);
                     q1.x = pack_bf16x2(f[8], f[9]);   q1.y = pack_bf16x2(f[10], f[11]);
                     q1.z = pack_bf16x2(f[12], f[13]); q1.w = pack_bf16x2(f[14], f[15]);
-                    *reinterpret_cast<uint4*>(out_row + col) = q0;               // N_out % 8 == 0
-                    if (col + 8 < p.N_out) *reinterpret_cast<uint4*>(out_row + col + 8) = q1;
+                    if constexpr (C::STORE_TMA) {
+                        // TMA-store epilogue: 32-column blocks (16 for a tile's odd tail: fwd
+                        // tiles are 256 - r_pad wide) staged swizzled in shared memory, then ONE
+                        // bulk tensor store per block by one thread; rows >= T and columns
+                        // >= N_out are clipped by the store
+                        const int blk = c >> 1, half = c & 1;
+                        const bool tail16 = (c == width / 16 - 1) && !half;   // a lone 16-column block
+                        const int buf = blk % C::STG_BUFS;
+                        uint8_t* sb = s_stg + buf * C::STG_BYTES;
+                        if (!half) {
+                            // the store issued STG_BUFS blocks ago has read this buffer
+                            if (storer) bulk_wait_group_read<C::STG_BUFS - 1>();
+                            named_bar_sync(1, 128);
+                        }
+                        if (tail16) {   // [128 rows][32 B], SW32
+                            *reinterpret_cast<uint4*>(sb + swizzled_offset(row_local, 0, 32)) = q0;
+                            *reinterpret_cast<uint4*>(sb + swizzled_offset(row_local, 1, 32)) = q1;
+                        } else {        // [128 rows][64 B], SW64
+                            *reinterpret_cast<uint4*>(sb + swizzled_offset(row_local, 2 * half, 64)) = q0;
+                            *reinterpret_cast<uint4*>(sb + swizzled_offset(row_local, 2 * half + 1, 64)) = q1;
+                        }
+                        if (half || tail16) {
+                            fence_proxy_async_smem();
+                            named_bar_sync(1, 128);
+                            if (storer) {
+                                const FusedGemmMaps& om = grp.maps[un.g];
+                                tma_store_2d(tail16 ? &om.out16 : &om.out32, sb,
+                                             static_cast<int32_t>(n0 + 32 * blk), static_cast<int32_t>(row0));
+                                bulk_commit_group();
+                            }
+                        }
+                    } else {
+                        *reinterpret_cast<uint4*>(out_row + col) = q0;               // N_out % 8 == 0
+                        if (col + 8 < p.N_out) *reinterpret_cast<uint4*>(out_row + col + 8) = q1;
+                    }
                 }
             }
             if constexpr (MODE == kModeDxDrop) {
@@ -1011,6 +1063,7 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
             if (p.unit_flags != nullptr) {
                 // comm-fused epilogue: this CTA's 128 rows of the tile are stored -- publish
                 // them to the ranks' reducers (lora_symm.cu) with one system-scope release
+                if (C::STORE_TMA && storer) bulk_wait_group<0>();   // the bulk stores have landed
                 __threadfence_system();
                 named_bar_sync(1, 128);
                 const int64_t nrow128 = (p.T + BM - 1) / BM;
@@ -1040,6 +1093,7 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
         }
     }
 
+    if (C::STORE_TMA && warp == 2 && lane == 0) bulk_wait_group<0>();   // every y / dX store performed
     tc_fence_before();
     if constexpr (CG == 2) cluster_sync(); else __syncthreads();
 #ifdef LORA_PROBE_CLOCK
@@ -1349,6 +1403,29 @@ static cudaError_t launch_impl(FusedGemmGroup& grp, int num_sms, cudaStream_t st
 }
 
 int fused_gemm_block_n(int mode, int r_pad) { return mode == kModeFwd ? NT - r_pad : NT; }
+
+template <int CG>
+static const void* gemm_fn(int mode, int r_pad) {
+    switch (mode * 100 + r_pad) {
+        case 16: return (const void*)lora_fused_gemm_kernel<kModeFwd, 16, CG>;
+        case 32: return (const void*)lora_fused_gemm_kernel<kModeFwd, 32, CG>;
+        case 64: return (const void*)lora_fused_gemm_kernel<kModeFwd, 64, CG>;
+        case 116: return (const void*)lora_fused_gemm_kernel<kModeDx, 16, CG>;
+        case 132: return (const void*)lora_fused_gemm_kernel<kModeDx, 32, CG>;
+        case 164: return (const void*)lora_fused_gemm_kernel<kModeDx, 64, CG>;
+        case 216: return (const void*)lora_fused_gemm_kernel<kModeDxDrop, 16, CG>;
+        case 232: return (const void*)lora_fused_gemm_kernel<kModeDxDrop, 32, CG>;
+        case 264: return (const void*)lora_fused_gemm_kernel<kModeDxDrop, 64, CG>;
+    }
+    return nullptr;
+}
+
+int fused_gemm_regs(int mode, int r_pad, int cta_group) {
+    const void* f = cta_group == 2 ? gemm_fn<2>(mode, r_pad) : gemm_fn<1>(mode, r_pad);
+    cudaFuncAttributes fa;
+    if (!f || cudaFuncGetAttributes(&fa, f) != cudaSuccess) return 255;
+    return fa.numRegs;
+}
 
 // Column tiles of a fused-GEMM output as the kernel walks them (ColTiles):
 // starts[0 .. count] with starts[count] = n_out; returns count (or -1 > max).

@@ -45,6 +45,7 @@ struct GemmCollector {
     int rp[lora_sm100::kMaxGroup];
     int cg[lora_sm100::kMaxGroup];
     bool no_coop = false;   // launch the fused GEMMs non-cooperatively (comm-fused path)
+    int max_sms = 0;        // > 0: the fused GEMMs use at most this many SMs (comm-fused path, virtual ranks)
     // K3 (dA, dB) problems of the grouped backward, launched together at the end
     int k3_count = 0;
     lora_sm100::GradArgs k3[lora_sm100::kMaxGroup];

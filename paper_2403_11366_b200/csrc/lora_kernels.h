@@ -59,6 +59,7 @@ struct FusedGemmParams {
 
 struct FusedGemmMaps {
     CUtensorMap act, w, w2, nar, tail;
+    CUtensorMap out32, out16;   // the output (y / dX) for the TMA-store epilogue: boxes [128 x 32] SW64, [128 x 16] SW32
 };
 
 // Schedule of a fused-GEMM launch.  Tiles in
@@ -271,7 +272,12 @@ struct SymmReduceArgs {
     __nv_bfloat16* out[kSymmMaxRanks];
     uint32_t* done[kSymmMaxRanks];       // rank r's launch counter
 };
-cudaError_t launch_symm_reduce(const SymmReduceArgs& A, int ctas, cudaStream_t stream);
+cudaError_t launch_symm_reduce(const SymmReduceArgs& A, int ctas, int variant, cudaStream_t stream);
+// which reducer variant fits next to one CTA of the GEMM (regs per thread, warps):
+// 0 (fat), 1 (lean), or -1 (none: the reducer must run after the GEMM)
+cudaError_t symm_reducer_plan(int gemm_regs, int gemm_warps, int* variant);
+// registers per thread of the fused-GEMM instantiation (mode, r_pad, CTA group)
+int fused_gemm_regs(int mode, int r_pad, int cta_group);
 // load every kernel the fused TP paths launch while a reducer may be spinning (lazy
 // module loading would otherwise load them at first launch, which waits for the
 // device to drain -- i.e. for the spinning reducer: a deadlock)

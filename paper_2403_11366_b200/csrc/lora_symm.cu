@@ -50,8 +50,10 @@ __device__ __forceinline__ uint4 ld_cg_u4(const void* p) {
     return v;
 }
 
-__global__ void __launch_bounds__(128, 4) symm_reduce_kernel(   // (4: <= 128 registers, see reducer_ctas)
-    const __grid_constant__ SymmReduceArgs A) {
+// KV 16-byte vectors per thread per round; MINB = CTAs per SM the launch bounds
+// assume, which caps the registers (65536 / (128 MINB)): KV 4 <= 128, KV 2 <= 80
+template <int KV, int MINB>
+__global__ void __launch_bounds__(128, MINB) symm_reduce_kernel(const __grid_constant__ SymmReduceArgs A) {
     const int N = A.nranks, G = A.nsrc;
     const int nwait = N * G;
     for (int64_t k = blockIdx.x;; k += gridDim.x) {
@@ -82,7 +84,7 @@ __global__ void __launch_bounds__(128, 4) symm_reduce_kernel(   // (4: <= 128 re
         // kV vectors (16 bytes) per thread per round, their loads for kSrc sources at a
         // time all in flight before any is consumed: the reduction is latency-bound (peer
         // loads), and the CTA must stay small enough to sit next to the GEMM's
-        constexpr int kV = 4, kSrc = 2;
+        constexpr int kV = KV, kSrc = 2;
         const int total = rows * nv;
         for (int i0 = threadIdx.x; i0 < total; i0 += kV * blockDim.x) {
             int64_t off[kV];
@@ -159,7 +161,32 @@ __global__ void __launch_bounds__(128, 4) symm_reduce_kernel(   // (4: <= 128 re
     }
 }
 
-cudaError_t launch_symm_reduce(const SymmReduceArgs& A, int ctas, cudaStream_t stream) {
+// Register footprint per SM sub-partition (16 Ki registers each) when one CTA of a
+// kernel with `warps` warps and `regs` registers per thread is resident: warp w
+// sits on sub-partition w % 4, registers are allocated per warp in units of 8 per
+// thread.  Returns the largest per-sub-partition use.
+static int smsp_regs(int warps, int regs) {
+    const int per_warp = (regs + 7) / 8 * 8 * 32;
+    return ((warps + 3) / 4) * per_warp;
+}
+
+cudaError_t symm_reducer_plan(int gemm_regs, int gemm_warps, int* variant) {
+    cudaFuncAttributes fa;
+    const int budget = 16384 - smsp_regs(gemm_warps, gemm_regs);
+    const void* ks[2] = {(const void*)symm_reduce_kernel<4, 4>, (const void*)symm_reduce_kernel<2, 6>};
+    for (int v = 0; v < 2; ++v) {
+        cudaError_t e = cudaFuncGetAttributes(&fa, ks[v]);
+        if (e != cudaSuccess) return e;
+        if (smsp_regs(4, fa.numRegs) <= budget) {   // 4 warps: one per sub-partition
+            *variant = v;
+            return cudaSuccess;
+        }
+    }
+    *variant = -1;   // no reducer fits next to this GEMM: run it after the GEMM
+    return cudaSuccess;
+}
+
+cudaError_t launch_symm_reduce(const SymmReduceArgs& A, int ctas, int variant, cudaStream_t stream) {
     if (A.nranks < 1 || A.nranks > kSymmMaxRanks || A.nsrc < 1 || A.nsrc > kMaxGroup || ctas < 1)
         return cudaErrorInvalidValue;
     // The reducer co-resides with the fused GEMM (~200 KiB of shared memory per SM;
@@ -167,12 +194,16 @@ cudaError_t launch_symm_reduce(const SymmReduceArgs& A, int ctas, cudaStream_t s
     // hosts a reducer CTA stays configured for a GEMM CTA next to it.
     static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(symm_reduce_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+        cudaError_t e = cudaFuncSetAttribute(symm_reduce_kernel<4, 4>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                              cudaSharedmemCarveoutMaxShared);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(symm_reduce_kernel<2, 6>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     cudaSharedmemCarveoutMaxShared);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
-    symm_reduce_kernel<<<ctas, 128, 0, stream>>>(A);
+    if (variant == 1) symm_reduce_kernel<2, 6><<<ctas, 128, 0, stream>>>(A);
+    else symm_reduce_kernel<4, 4><<<ctas, 128, 0, stream>>>(A);
     return cudaGetLastError();
 }
 
@@ -198,6 +229,7 @@ struct lora_symm {
     uint8_t* peer[kSymmMaxRanks] = {};          // every rank's base (peer[rank] == base)
     bool opened[kSymmMaxRanks] = {};            // IPC mappings to close
     bool local = false;                         // virtual ranks of one process on one GPU
+    int last_mode = 0;                          // last reducer placement: 1 co-resident, 2 after the GEMM, 3 split SMs
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
@@ -215,7 +247,8 @@ lora_status preload_kernels() {
     cudaFuncAttributes fa;
     if ((e = preload_gemm_kernels()) != cudaSuccess || (e = preload_grad_kernels()) != cudaSuccess ||
         (e = preload_grad_mma_kernels()) != cudaSuccess ||
-        (e = cudaFuncGetAttributes(&fa, (const void*)symm_reduce_kernel)) != cudaSuccess)
+        (e = cudaFuncGetAttributes(&fa, (const void*)symm_reduce_kernel<4, 4>)) != cudaSuccess ||
+        (e = cudaFuncGetAttributes(&fa, (const void*)symm_reduce_kernel<2, 6>)) != cudaSuccess)
         return cuda_fail(e, "kernel preload");
     done[dev] = true;
     return LORA_OK;
@@ -270,20 +303,24 @@ static lora_status make_reduce_args(const lora_symm* s, int mode, int rp, int64_
     return LORA_OK;
 }
 
-// One CTA per owned unit, at most one per SM.  The GEMM's persistent CTAs own
-// fixed tiles the reducer waits for, so a GEMM CTA must fit next to a reducer CTA
-// on EVERY SM (launch order alone does not decide placement): the reducer CTA is
-// 4 warps x <= 128 registers, no shared memory -- one warp and 4 Ki registers per
-// SM sub-partition, inside the 5 Ki the dX kernel (6 warps x 176 registers, two
-// warps on sub-partitions 0 / 1, 214 KiB of shared memory) leaves of each 16 Ki
-// register file.  Measured on B200: this co-resides at cfg2 / cfg3; 201-register
-// reducer warps, or two 8-warp CTAs per SM, left GEMM CTAs unplaced (deadlock).
-// Virtual ranks on one GPU (connect_local) share the SMs: N reducers, each
-// capped at SMs / N.
-static int reducer_ctas(const SymmReduceArgs& A, int num_sms, bool local) {
+// Placement (the GEMM's persistent CTAs own fixed tiles the reducer waits for, so
+// no reducer CTA may ever keep a GEMM CTA from being placed -- that deadlocks):
+//  * one rank per GPU: if a reducer variant fits next to one GEMM CTA on EVERY SM
+//    (per sub-partition register budget, symm_reducer_plan: the fused dX kernel
+//    has 6 warps of up to 254 registers, sub-partitions 0 / 1 carry two of them),
+//    the reducer runs co-resident, one CTA per SM at most, overlapping the GEMM;
+//    otherwise it runs after the GEMM (no overlap, no risk);
+//  * virtual ranks on one GPU (connect_local): the ranks' GEMMs run one after the
+//    other and every rank's reducer waits for all of them, so the SMs are split
+//    instead: the GEMMs are capped at (SMs - 16) / 2 CTA pairs and the N reducers
+//    share 8 CTAs (at most 8 SMs / TPCs, while 8 TPCs are left free).
+constexpr int kLocalReducerCtas = 8;
+constexpr int kLocalReservedSms = 2 * kLocalReducerCtas;
+
+static int reducer_ctas(const SymmReduceArgs& A, int num_sms, bool local, bool coresident) {
     const int owned = (A.units + A.nranks - 1) / A.nranks;
-    int cap = local ? num_sms / A.nranks : num_sms;
-    cap = cap > 0 ? cap : 1;
+    int cap = local ? (kLocalReducerCtas / A.nranks > 0 ? kLocalReducerCtas / A.nranks : 1)
+                    : (coresident ? num_sms : 2 * num_sms);
     return owned < cap ? (owned > 0 ? owned : 1) : cap;
 }
 
@@ -297,19 +334,47 @@ static lora_status record_fork(lora_symm* s, cudaStream_t st) {
     return e == cudaSuccess ? LORA_OK : cuda_fail(e, "symm: fork the reducer stream");
 }
 
+// Called right after the GEMM (registers per thread `gemm_regs`) was enqueued on `st`
+// (the fork event was recorded before it).
 static lora_status fork_reducer(lora_symm* s, const SymmReduceArgs& A, cudaStream_t st, int* launches,
-                                bool forked_already) {
-    cudaError_t e = cudaSuccess;
-    if (!forked_already) {
-        lora_status fs = record_fork(s, st);
-        if (fs != LORA_OK) return fs;
-    }
+                                int gemm_regs) {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->dev);
-    if ((e = launch_symm_reduce(A, reducer_ctas(A, sms, s->local), s->side)) != cudaSuccess)
+    int variant = 0;
+    cudaError_t e = cudaSuccess;
+    if (!s->local) {
+        if ((e = symm_reducer_plan(gemm_regs, 6, &variant)) != cudaSuccess) return cuda_fail(e, "symm reducer plan");
+        if (variant < 0) {   // nothing fits next to this GEMM: reduce after it
+            if ((e = cudaEventRecord(s->ev_fork, st)) == cudaSuccess) e = cudaStreamWaitEvent(s->side, s->ev_fork, 0);
+            if (e != cudaSuccess) return cuda_fail(e, "symm: order the reducer after the GEMM");
+            variant = 0;
+            s->last_mode = 2;
+        } else {
+            s->last_mode = 1;
+        }
+    } else {
+        s->last_mode = 3;
+    }
+    if ((e = launch_symm_reduce(A, reducer_ctas(A, sms, s->local, s->last_mode == 1), variant, s->side)) !=
+        cudaSuccess)
         return cuda_fail(e, "symm reduce launch");
     ++*launches;
     return LORA_OK;
+}
+
+static int max_gemm_regs(const GemmCollector& col, int mode) {
+    int r = 0;
+    for (int g = 0; g < col.count; ++g) {
+        const int v = fused_gemm_regs(mode, col.rp[g], col.cg[g]);
+        r = v > r ? v : r;
+    }
+    return r;
+}
+
+static int local_gemm_sms(const lora_symm* s) {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->dev);
+    return sms - kLocalReservedSms;
 }
 
 static lora_status join_reducer(lora_symm* s, cudaStream_t st) {
@@ -410,6 +475,7 @@ lora_status lora_symm_connect_local(int nranks, lora_symm* const* group) {
 }
 
 void* lora_symm_ptr(const lora_symm* s) { return s ? s->base + kCtlBytes : nullptr; }
+int lora_symm_last_placement(const lora_symm* s) { return s ? s->last_mode : 0; }
 size_t lora_symm_bytes(const lora_symm* s) { return s ? s->data_bytes : 0; }
 
 lora_status lora_symm_destroy(lora_symm* s) {
@@ -465,15 +531,13 @@ lora_status lora_tp_linear_fwd_fused(lora_symm* s, const lora_dims* local, const
         col.p[g].unit_flags = reinterpret_cast<uint32_t*>(s->base + kFlagsOff);
         col.p[g].sk_partial = nullptr;
     }
-    col.no_coop = true;
-    // the GEMM is enqueued BEFORE the reducer: its persistent CTAs (which own the
-    // tiles the reducer waits for) are placed first, the reducer's fill in next to
-    // them -- the reverse order can leave GEMM CTAs unplaceable behind reducer CTAs
+    if (s->local) col.max_sms = local_gemm_sms(s);
+    // the GEMM is enqueued before the reducer (see reducer_ctas for the placement rules)
     if ((st = launch_collected(kModeFwd, col, cs, &launches)) != LORA_OK) {
         set_launches(launches);
         return st;
     }
-    if ((st = fork_reducer(s, A, cs, &launches, /*after_gemm=*/true)) != LORA_OK) return st;
+    if ((st = fork_reducer(s, A, cs, &launches, max_gemm_regs(col, kModeFwd))) != LORA_OK) return st;
     st = join_reducer(s, cs);
     set_launches(launches);
     return st;
@@ -517,7 +581,8 @@ lora_status lora_tp_linear_bwd_column_group_fused(lora_symm* s, lora_comm* comm,
         const SymmReduceArgs* A;
         cudaStream_t cs;
         bool forked;
-    } ctx = {s, &A, cs, false};
+        int gemm_regs;
+    } ctx = {s, &A, cs, false, 255};
     // right before the grouped dX kernel: every member publishes its units, and the
     // side stream forks off here; right after K2 is enqueued the reducer is launched
     // (GEMM first: see lora_tp_linear_fwd_fused) and sums the units over members and
@@ -531,13 +596,15 @@ lora_status lora_tp_linear_bwd_column_group_fused(lora_symm* s, lora_comm* comm,
         }
         // a cooperative dX launch would wait for the resident reducer, which waits for it
         col->no_coop = true;
+        if (k.s->local) col->max_sms = local_gemm_sms(k.s);
+        k.gemm_regs = max_gemm_regs(*col, kModeDx);
         lora_status r = record_fork(k.s, k.cs);
         k.forked = r == LORA_OK;
         return r;
     };
     auto after_k2 = [](void* c, int* launches) -> lora_status {
         Ctx& k = *static_cast<Ctx*>(c);
-        return fork_reducer(k.s, *k.A, k.cs, launches, true);
+        return fork_reducer(k.s, *k.A, k.cs, launches, k.gemm_regs);
     };
     st = bwd_grouped_impl(count, local, probs, 0, workspace, workspace_bytes, stream, after_k2, &ctx, before_k2,
                           &ctx);

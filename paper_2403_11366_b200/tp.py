@@ -282,6 +282,12 @@ class SymmBuffer:
     def handle(self):
         return self._h
 
+    @property
+    def last_placement(self):
+        """1 co-resident reducer, 2 reducer after the GEMM, 3 virtual ranks (split SMs)."""
+        from . import lib
+        return {0: None, 1: "coresident", 2: "after_gemm", 3: "split_sms"}[lib.lora_symm_last_placement(self._h)]
+
     def view(self, offset: int, shape, dtype="bf16"):
         """A torch tensor over [offset, ...) of this rank's data region."""
         import torch

@@ -10,38 +10,38 @@ import torch
 from oracle import layer as OL
 from synth import bf16_bits_to_f64, make_layer_inputs
 
-torch.set_default_dtype(torch.float64)
+F64 = torch.float64
 
 
 def test_rmsnorm_closed_forms():
-    g = torch.tensor([1.0, 2.0, -3.0, 0.5])
+    g = torch.tensor([1.0, 2.0, -3.0, 0.5], dtype=F64)
     # a constant row c * 1 has rms |c|: the output is g * sign(c) (eps = 0)
     for c in (0.3, -7.0):
-        assert torch.allclose(OL.rmsnorm(torch.full((1, 4), c), g, 0.0), g * math.copysign(1.0, c), rtol=0, atol=1e-15)
-    x = torch.tensor([[3.0, 4.0, 0.0, 0.0]])     # mean square 25/4 -> rms 2.5
-    assert torch.allclose(OL.rmsnorm(x, torch.ones(4), 0.0), x / 2.5, rtol=0, atol=1e-15)
+        assert torch.allclose(OL.rmsnorm(torch.full((1, 4), c, dtype=F64), g, 0.0), g * math.copysign(1.0, c), rtol=0, atol=1e-15)
+    x = torch.tensor([[3.0, 4.0, 0.0, 0.0]], dtype=F64)     # mean square 25/4 -> rms 2.5
+    assert torch.allclose(OL.rmsnorm(x, torch.ones(4, dtype=F64), 0.0), x / 2.5, rtol=0, atol=1e-15)
     # eps: mean square 0 -> x / sqrt(eps)
-    assert torch.allclose(OL.rmsnorm(torch.tensor([[1e-3, 0, 0, 0]]), torch.ones(4), 0.25),
-                          torch.tensor([[2e-3, 0, 0, 0]]), rtol=1e-12)
+    assert torch.allclose(OL.rmsnorm(torch.tensor([[1e-3, 0, 0, 0]], dtype=F64), torch.ones(4, dtype=F64), 0.25),
+                          torch.tensor([[2e-3, 0, 0, 0]], dtype=F64), rtol=1e-12)
 
 
 def test_rope_closed_forms():
     # one pair (D = 2): angle = t exactly (theta^0 = 1); (1, 0) -> (cos t, sin t)
     T = 5
-    q = torch.tensor([[1.0, 0.0]] * T)
+    q = torch.tensor([[1.0, 0.0]] * T, dtype=F64)
     r = OL.rope(q, 1, 2, 10000.0)
     for t in range(T):
         assert abs(r[t, 0] - math.cos(t)) < 1e-15 and abs(r[t, 1] - math.sin(t)) < 1e-15
     # position 0 is the identity; the pair norms are preserved
     g = torch.Generator().manual_seed(0)
-    q = torch.randn(7, 3 * 16, generator=g)
+    q = torch.randn(7, 3 * 16, generator=g, dtype=F64)
     r = OL.rope(q, 3, 16, 500.0)
     assert torch.equal(r[0], q[0])
     qh, rh = q.reshape(7, 3, 2, 8), r.reshape(7, 3, 2, 8)
     assert torch.allclose((qh ** 2).sum(2), (rh ** 2).sum(2), rtol=1e-13)
     # relative positions: <RoPE(q)_t1, RoPE(k)_t2> depends on t1 - t2 only (same q, k rows at all t)
-    qq = torch.randn(1, 16, generator=g).repeat(6, 1)
-    kk = torch.randn(1, 16, generator=g).repeat(6, 1)
+    qq = torch.randn(1, 16, generator=g, dtype=F64).repeat(6, 1)
+    kk = torch.randn(1, 16, generator=g, dtype=F64).repeat(6, 1)
     rq, rk = OL.rope(qq, 1, 16, 10000.0), OL.rope(kk, 1, 16, 10000.0)
     assert abs(float(rq[4] @ rk[1] - rq[3] @ rk[0])) < 1e-12
     assert abs(float(rq[5] @ rk[5] - rq[0] @ rk[0])) < 1e-12
@@ -50,7 +50,7 @@ def test_rope_closed_forms():
 def test_attention_brute_force():
     g = torch.Generator().manual_seed(1)
     T, H, D = 5, 2, 4
-    q, k, v = (torch.randn(T, H * D, generator=g) for _ in range(3))
+    q, k, v = (torch.randn(T, H * D, generator=g, dtype=F64) for _ in range(3))
     o = OL.causal_attention(q, k, v, H, D)
     for h in range(H):
         sl = slice(h * D, (h + 1) * D)
@@ -62,15 +62,15 @@ def test_attention_brute_force():
             assert np.allclose(o[t, sl].numpy(), ref, rtol=1e-12, atol=1e-14)
     # T = 1: the output is v; equal keys: the causal prefix mean of v
     assert torch.allclose(OL.causal_attention(q[:1], k[:1], v[:1], H, D), v[:1], rtol=0, atol=1e-15)
-    kc = torch.ones(T, H * D)
-    qz = torch.zeros(T, H * D)
-    pm = torch.cumsum(v, 0) / torch.arange(1, T + 1)[:, None]
+    kc = torch.ones(T, H * D, dtype=F64)
+    qz = torch.zeros(T, H * D, dtype=F64)
+    pm = torch.cumsum(v, 0) / torch.arange(1, T + 1, dtype=F64)[:, None]
     assert torch.allclose(OL.causal_attention(qz, kc, v, H, D), pm, rtol=1e-13)
 
 
 def test_swiglu_closed_form():
-    g = torch.tensor([0.0, 1.0, -2.0, 30.0])
-    u = torch.tensor([5.0, 2.0, 3.0, 0.5])
+    g = torch.tensor([0.0, 1.0, -2.0, 30.0], dtype=F64)
+    u = torch.tensor([5.0, 2.0, 3.0, 0.5], dtype=F64)
     ref = [0.0, 2.0 / (1 + math.exp(-1.0)), 3.0 * -2.0 / (1 + math.exp(2.0)), 0.5 * 30.0 / (1 + math.exp(-30.0))]
     assert np.allclose(OL.swiglu(g, u).numpy(), ref, rtol=1e-15)
 
