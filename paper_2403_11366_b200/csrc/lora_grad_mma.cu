@@ -553,6 +553,13 @@ cudaError_t launch_grad_mma(GradMmaGroup& G, int num_sms, cudaStream_t stream, b
         cache_dev = dev;
     }
     G.S = grad_mma_cluster_size(tiles, kb_max, slots);
+    // Overlapping K2's last wave (programmatic stream serialization), short token
+    // ranges and enough column tiles for most SMs: no token split.  Measured at cfg2
+    // (96 tiles, 32 k-blocks; graph-replayed step, profiles/r02/k3_split.txt): S = 1
+    // 0.2019 ms per step vs 0.2101 for the cost model's S = 2 -- one-CTA jobs start
+    // on the SMs K2's finished pairs free and hide under its tail, although K3 alone
+    // takes longer (29 vs 23 us); at cfg3 (64 k-blocks) S = 1 was slower (2.351 vs 2.335).
+    if (overlap_prev && k3_overlap_enabled() && kb_max <= 32 && tiles * 10 >= num_sms * 6) G.S = 1;
     if (const char* fs = getenv("LORA_K3_S")) {   // tests / experiments: force the token split
         const int v = atoi(fs);
         if (v >= 1 && v <= 8) G.S = v;
