@@ -339,7 +339,8 @@ class StepRunner:
         self.nsets = nsets
         self.use_set(0)
 
-        self.use_groups = comm is None and group and dropout == 0.0
+        self.use_groups = comm is None and group
+        self.dropout = dropout
         if dropout > 0.0 and comm is not None:
             raise SystemExit("--dropout is single-GPU only (the TP entry points have no dropout variant)")
         self.groups = []
@@ -347,10 +348,14 @@ class StepRunner:
             for gidx in wl.groups:
                 members = [lin[i] for i in gidx]
                 ds = self._dims(members)
-                wsf = torch.empty(max(256, int(L.lib.lora_linear_fwd_grouped_workspace_bytes(len(members), ds))),
-                                  dtype=torch.uint8, device=dev)
-                wsb = torch.empty(max(256, int(L.lib.lora_linear_bwd_grouped_workspace_bytes(len(members), ds))),
-                                  dtype=torch.uint8, device=dev)
+                if dropout > 0.0:
+                    nf = int(L.lib.lora_linear_fwd_grouped_dropout_workspace_bytes(len(members), ds))
+                    nb = int(L.lib.lora_linear_bwd_grouped_dropout_workspace_bytes(len(members), ds))
+                else:
+                    nf = int(L.lib.lora_linear_fwd_grouped_workspace_bytes(len(members), ds))
+                    nb = int(L.lib.lora_linear_bwd_grouped_workspace_bytes(len(members), ds))
+                wsf = torch.empty(max(256, nf), dtype=torch.uint8, device=dev)
+                wsb = torch.empty(max(256, nb), dtype=torch.uint8, device=dev)
                 self.groups.append((members, wsf, wsb))
         self.tp_groups = []
         if comm is not None and group and dropout == 0.0:
@@ -437,18 +442,21 @@ class StepRunner:
         for gi, (members, wsf, _) in enumerate(self.groups):
             if ev is not None and gi == 0:
                 ev["f0"].record(cur)
+            drops = [e["drop"] for e in members] if self.dropout > 0.0 else None
             L.lora_linear_fwd_grouped([(e["x"], e["w0"], e["a"], e["b"], None) for e in members],
                                       [e["l"].alpha for e in members], outs=[(e["y"], e["h"]) for e in members],
-                                      workspace=wsf, stream=cur)
+                                      workspace=wsf, stream=cur, dropouts=drops)
             self.launches += L.lora_last_launch_count()
             if ev is not None and gi == 0:
                 ev["f1"].record(cur)
         for gi, (members, _, wsb) in enumerate(self.groups):
             if gi == 0:
                 self._prof_bwd(ev)
+            drops = [e["drop"] for e in members] if self.dropout > 0.0 else None
             L.lora_linear_bwd_grouped([(e["x"], e["w0"], e["a"], e["b"], e["dy"], e["h"]) for e in members],
                                       [e["l"].alpha for e in members],
-                                      outs=[(e["dx"], e["da"], e["db"]) for e in members], workspace=wsb, stream=cur)
+                                      outs=[(e["dx"], e["da"], e["db"]) for e in members], workspace=wsb, stream=cur,
+                                      dropouts=drops)
             self.launches += L.lora_last_launch_count()
 
     def _step_tp(self, ev):
@@ -587,8 +595,9 @@ class StepRunner:
                                                  np.arange(max(0, T - 32), T)]))
             else:
                 rows = rows_per_linear
-            yo, ho = oracle.lora_fwd(d["x"], d["w0"], d["a"], d["b"], l.alpha, rows=rows)
-            go = oracle.lora_bwd(d["x"], d["w0"], d["a"], d["b"], d["dy"], l.alpha, rows=rows)
+            kw = {"dropout": e["drop"]} if e["drop"] is not None else {}   # (LoRA dropout: the same mask)
+            yo, ho = oracle.lora_fwd(d["x"], d["w0"], d["a"], d["b"], l.alpha, rows=rows, **kw)
+            go = oracle.lora_bwd(d["x"], d["w0"], d["a"], d["b"], d["dy"], l.alpha, rows=rows, **kw)
             ri = self.torch.as_tensor(rows, device=self.dev)
             got = {"y": to_f64(e["y"][ri]), "h": to_f64(e["h"][ri]), "da": to_f64(e["da"]), "db": to_f64(e["db"])}
             ref = {"y": yo, "h": ho, "da": go["da"], "db": go["db"]}

@@ -207,6 +207,20 @@ size_t lora_linear_bwd_grouped_workspace_bytes(int count, const lora_dims* dims)
 lora_status lora_linear_bwd_grouped(int count, const lora_dims* dims, const lora_bwd_problem* problems,
                                     int accumulate, void* workspace, size_t workspace_bytes, void* stream);
 
+/* Grouped calls with LoRA dropout (Listing 3 LORA_DROPOUT; R7): one
+ * lora_dropout per problem (each linear draws its own mask: its own seed /
+ * offset); p must be > 0 for all problems or for none (one dX kernel mode per
+ * group).  Same semantics as `count` lora_linear_{fwd,bwd}_dropout calls, with
+ * the fused GEMMs of the group in one launch. */
+size_t lora_linear_fwd_grouped_dropout_workspace_bytes(int count, const lora_dims* dims);
+size_t lora_linear_bwd_grouped_dropout_workspace_bytes(int count, const lora_dims* dims);
+lora_status lora_linear_fwd_grouped_dropout(int count, const lora_dims* dims, const lora_dropout* dropouts,
+                                            const lora_fwd_problem* problems, void* workspace, size_t workspace_bytes,
+                                            void* stream);
+lora_status lora_linear_bwd_grouped_dropout(int count, const lora_dims* dims, const lora_dropout* dropouts,
+                                            const lora_bwd_problem* problems, int accumulate, void* workspace,
+                                            size_t workspace_bytes, void* stream);
+
 const char* lora_status_string(lora_status status);
 const char* lora_last_error(void);
 

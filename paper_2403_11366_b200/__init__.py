@@ -110,6 +110,16 @@ lib.lora_linear_fwd_grouped.restype = _st
 lib.lora_linear_bwd_grouped.argtypes = [ctypes.c_int, _dp, ctypes.POINTER(lora_bwd_problem), ctypes.c_int, _vp,
                                         ctypes.c_size_t, _vp]
 lib.lora_linear_bwd_grouped.restype = _st
+lib.lora_linear_fwd_grouped_dropout_workspace_bytes.argtypes = [ctypes.c_int, _dp]
+lib.lora_linear_fwd_grouped_dropout_workspace_bytes.restype = ctypes.c_size_t
+lib.lora_linear_bwd_grouped_dropout_workspace_bytes.argtypes = [ctypes.c_int, _dp]
+lib.lora_linear_bwd_grouped_dropout_workspace_bytes.restype = ctypes.c_size_t
+lib.lora_linear_fwd_grouped_dropout.argtypes = [ctypes.c_int, _dp, _drp, ctypes.POINTER(lora_fwd_problem), _vp,
+                                                ctypes.c_size_t, _vp]
+lib.lora_linear_fwd_grouped_dropout.restype = _st
+lib.lora_linear_bwd_grouped_dropout.argtypes = [ctypes.c_int, _dp, _drp, ctypes.POINTER(lora_bwd_problem),
+                                                ctypes.c_int, _vp, ctypes.c_size_t, _vp]
+lib.lora_linear_bwd_grouped_dropout.restype = _st
 lib.lora_merge.argtypes = [_dp, _vp, _vp, _vp, _vp, _vp]
 lib.lora_merge.restype = _st
 lib.lora_status_string.argtypes = [_st]
@@ -406,7 +416,7 @@ def lora_merge(w0, a, b, alpha, w_out=None, stream=None):
     return w_out
 
 
-def lora_linear_fwd_grouped(problems, alphas, outs=None, workspace=None, stream=None):
+def lora_linear_fwd_grouped(problems, alphas, outs=None, workspace=None, stream=None, dropouts=None):
     """Grouped forward (one persistent launch for the fused GEMMs).
 
     problems: list of (x, w0, a, b, bias_or_None); alphas: list of floats;
@@ -429,6 +439,13 @@ def lora_linear_fwd_grouped(problems, alphas, outs=None, workspace=None, stream=
         dims_arr[g] = dims(T, n, m, r, alphas[g])
         probs[g] = lora_fwd_problem(_ptr(x), _ptr(w0), _ptr(a), _ptr(b), _ptr(bias), _ptr(y), _ptr(h))
         res.append((y, h))
+    if dropouts is not None:   # one (p, seed, offset) per problem
+        drs = (lora_dropout * G)(*[_dropout(dr) for dr in dropouts])
+        need = int(lib.lora_linear_fwd_grouped_dropout_workspace_bytes(G, dims_arr))
+        ws = workspace if workspace is not None else _workspace(need, problems[0][0].device)
+        _check(lib.lora_linear_fwd_grouped_dropout(G, dims_arr, drs, probs, _ptr(ws), ws.numel(), _stream(stream)),
+               "lora_linear_fwd_grouped_dropout")
+        return res
     need = int(lib.lora_linear_fwd_grouped_workspace_bytes(G, dims_arr))
     ws = workspace if workspace is not None else _workspace(need, problems[0][0].device)
     _check(lib.lora_linear_fwd_grouped(G, dims_arr, probs, _ptr(ws), ws.numel(), _stream(stream)),
@@ -437,7 +454,7 @@ def lora_linear_fwd_grouped(problems, alphas, outs=None, workspace=None, stream=
 
 
 def lora_linear_bwd_grouped(problems, alphas, outs=None, accumulate=False, workspace=None, stream=None,
-                            want_dx=True, want_da=True, want_db=True):
+                            want_dx=True, want_da=True, want_db=True, dropouts=None):
     """Grouped backward.  problems: list of (x, w0, a, b, dy, h_saved_or_None);
     outs: optional list of (dx, da, db); want_*=False passes NULL for that output
     of every problem (not allocated).  Returns the list of (dx, da, db)."""
@@ -464,6 +481,13 @@ def lora_linear_bwd_grouped(problems, alphas, outs=None, accumulate=False, works
         probs[g] = lora_bwd_problem(_ptr(x), _ptr(w0), _ptr(a), _ptr(b), _ptr(h), _ptr(dy), _ptr(dx), _ptr(da),
                                     _ptr(db))
         res.append((dx, da, db))
+    if dropouts is not None:
+        drs = (lora_dropout * G)(*[_dropout(dr) for dr in dropouts])
+        need = int(lib.lora_linear_bwd_grouped_dropout_workspace_bytes(G, dims_arr))
+        ws = workspace if workspace is not None else _workspace(need, problems[0][0].device)
+        _check(lib.lora_linear_bwd_grouped_dropout(G, dims_arr, drs, probs, 1 if accumulate else 0, _ptr(ws),
+                                                   ws.numel(), _stream(stream)), "lora_linear_bwd_grouped_dropout")
+        return res
     need = int(lib.lora_linear_bwd_grouped_workspace_bytes(G, dims_arr))
     ws = workspace if workspace is not None else _workspace(need, problems[0][0].device)
     _check(lib.lora_linear_bwd_grouped(G, dims_arr, probs, 1 if accumulate else 0, _ptr(ws), ws.numel(),

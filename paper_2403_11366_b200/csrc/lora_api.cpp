@@ -224,6 +224,7 @@ static BwdWs bwd_ws(const lora_dims* d, bool dropout = false) {
 static constexpr uint64_t kFlagSet = 1;
 
 static lora_status collect(GemmCollector* col, const FusedGemmMaps& maps, const FusedGemmParams& p, int rp, int cg);
+static lora_status queue_k0(GemmCollector* col, const void* x, int64_t T, int64_t n, const DropoutMember& m);
 
 // ------------------------------------------------------------ forward
 lora_status fwd_impl(const lora_dims* d, const void* x, const void* w0, const void* a, const void* b,
@@ -305,15 +306,22 @@ lora_status fwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
     p.sk_partial = W.partial_bytes ? reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + W.partial) : nullptr;
     p.unit_flags = nullptr;
     if (drop && drop->thr > 0) {
-        // LoRA dropout: K0 computes h = q (M . x) A^T; K1 takes it instead of its in-MMA x A^T
+        // LoRA dropout: K0 computes h = q (M . x) A^T; K1 takes it instead of its in-MMA
+        // x A^T -- K0 is queued (grouped: one launch for every member sharing x) and K1
+        // overlaps it (programmatic stream serialization; its epilogue waits for K0)
         float* hd = h_out ? h_out : reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + W.h);
-        cudaError_t e = launch_dropout_input(static_cast<const __nv_bfloat16*>(x), T, n,
-                                             static_cast<const __nv_bfloat16*>(a), r, *drop, hd, nullptr, nullptr,
-                                             dev.sms, stream);
-        if (e != cudaSuccess) return cuda_fail(e, "dropout K0 launch");
-        ++*launches;
         p.h_in = hd;
         p.side_out = nullptr;
+        const DropoutMember mem{static_cast<const __nv_bfloat16*>(a), r, *drop, hd, nullptr, nullptr};
+        if (col) {
+            if ((st = queue_k0(col, x, T, n, mem)) != LORA_OK) return st;
+            return collect(col, maps, p, rp, cg);
+        }
+        GemmCollector one;
+        if ((st = queue_k0(&one, x, T, n, mem)) != LORA_OK) return st;
+        if ((st = collect(&one, maps, p, rp, cg)) != LORA_OK) return st;
+        if ((st = launch_collected_k0(one, stream, launches)) != LORA_OK) return st;
+        return launch_collected(kModeFwd, one, stream, launches);
     }
     if (col) return collect(col, maps, p, rp, cg);
     cudaError_t e = launch_fused_gemm(kModeFwd, rp, cg, maps, p, dev.sms, stream);
@@ -533,6 +541,37 @@ lora_status launch_collected(int mode, GemmCollector& col, cudaStream_t stream, 
     return LORA_OK;
 }
 
+// K0 of the collected problems, one launch per problem (each linear draws its
+// own mask), in stream order right before the fused GEMMs.  Measured and dropped
+// (cfg2 q+v, p = 0.05, graph-replayed step; DESIGN.md dropout path): one grouped
+// K0 launch for the members sharing x, and the fused GEMM launched with
+// programmatic stream serialization to overlap K0 (its epilogue waiting for
+// it) -- 0.318-0.350 ms vs 0.309: K0 is issue-bound on every SM and cannot share
+// them with the GEMM's CTAs, so the overlap only interferes.
+lora_status launch_collected_k0(GemmCollector& col, cudaStream_t stream, int* launches) {
+    if (col.k0.count == 0) return LORA_OK;
+    DevInfo dev;
+    lora_status st = device_info(&dev);
+    if (st != LORA_OK) return st;
+    cudaError_t e = launch_dropout_input_group(col.k0, dev.sms, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "dropout K0 launch");
+    *launches += col.k0.count;
+    col.k0.count = 0;
+    return LORA_OK;
+}
+
+// queue K0 work for `col` (one grouped launch later); members must share x
+static lora_status queue_k0(GemmCollector* col, const void* x, int64_t T, int64_t n, const DropoutMember& m) {
+    if (col->k0.count > 0 && (col->k0.x != x || col->k0.T != T || col->k0.n != n))
+        return fail(LORA_ERR_UNSUPPORTED, "grouped LoRA dropout: the problems must share the input x");
+    if (col->k0.count >= kMaxGroup) return fail(LORA_ERR_UNSUPPORTED, "more than %d grouped problems", kMaxGroup);
+    col->k0.x = static_cast<const __nv_bfloat16*>(x);
+    col->k0.T = T;
+    col->k0.n = n;
+    col->k0.m[col->k0.count++] = m;
+    return LORA_OK;
+}
+
 // ------------------------------------------------------------ backward
 lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const void* a, const void* b,
                      const float* h_saved, const void* dy, void* dx, float* da, float* db, int accumulate,
@@ -551,7 +590,6 @@ lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
         if (ptrs[i] && !aligned16(ptrs[i]))
             return fail(LORA_ERR_ALIGN, "lora_linear_bwd: %s = %p is not 16-byte aligned", names[i], ptrs[i]);
     const bool dropping = drop && drop->thr > 0;
-    if (dropping && col) return fail(LORA_ERR_UNSUPPORTED, "grouped backward with LoRA dropout");
     const BwdWs W = bwd_ws(d, drop != nullptr);
     if (!ws || ws_bytes < W.total)
         return fail(LORA_ERR_WORKSPACE, "lora_linear_bwd: workspace %zu bytes < required %zu", ws ? ws_bytes : 0,
@@ -599,14 +637,16 @@ lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
     bool gh_split = false, h_split = false;   // a row projection already wrote K3's split of gh / h
 
     auto* xm = reinterpret_cast<__nv_bfloat16*>(wsb + W.xm);
+    GemmCollector one;                      // single calls: K0 + K2 through a local collector
+    GemmCollector* k0col = col ? col : &one;
     if (dropping && (stages & 1)) {
-        // K0: keep bits for K2's epilogue, M . x for dA, h = q (M . x) A^T when not saved -- one pass over x
-        if ((e = launch_dropout_input(static_cast<const __nv_bfloat16*>(x), T, n, static_cast<const __nv_bfloat16*>(a),
-                                      r, *drop, need_h ? hbuf : nullptr, da ? xm : nullptr,
-                                      dx ? reinterpret_cast<uint32_t*>(wsb + W.bits) : nullptr, dev.sms, stream)) !=
-            cudaSuccess)
-            return cuda_fail(e, "dropout K0 launch");
-        ++*launches;
+        // K0: keep bits for K2's epilogue, M . x for dA, h = q (M . x) A^T when not saved -- one
+        // pass over x, queued (grouped: one launch for the members sharing x) right before K2,
+        // which overlaps it and waits for it in its epilogue only
+        const DropoutMember mem{static_cast<const __nv_bfloat16*>(a), r, *drop, need_h ? hbuf : nullptr,
+                                da ? xm : nullptr, dx ? reinterpret_cast<uint32_t*>(wsb + W.bits) : nullptr};
+        if ((st = queue_k0(k0col, x, T, n, mem)) != LORA_OK) return st;
+        if (!col && !dx && (st = launch_collected_k0(one, stream, launches)) != LORA_OK) return st;
     }
     if (dx && (stages & 1)) {
         // K2 computes gh = s dY B itself (first column tile of each row block)
@@ -660,10 +700,17 @@ lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
         p.cs_h = db && p.h_split_src ? reinterpret_cast<__nv_bfloat16*>(wsb + W.cs_b) : nullptr;
         if (col) {
             if ((st = collect(col, maps, p, rp, cg)) != LORA_OK) return st;
-        } else {
-            // dropout: the epilogue applies q M . (gh A) itself (no tail MMA)
+        } else if (dropping) {
+            // dropout: the epilogue applies q M . (gh A) itself (no tail MMA); K0 right before
+            if ((st = collect(&one, maps, p, rp, cg)) != LORA_OK) return st;
+            if ((st = launch_collected_k0(one, stream, launches)) != LORA_OK) return st;
             prof_record(0, stream);
-            e = launch_fused_gemm(dropping ? kModeDxDrop : kModeDx, rp, cg, maps, p, dev.sms, stream);
+            st = launch_collected(kModeDxDrop, one, stream, launches);
+            prof_record(1, stream);
+            if (st != LORA_OK) return st;
+        } else {
+            prof_record(0, stream);
+            e = launch_fused_gemm(kModeDx, rp, cg, maps, p, dev.sms, stream);
             prof_record(1, stream);
             if (e != cudaSuccess) return cuda_fail(e, "fused dX launch");
             ++*launches;
@@ -943,60 +990,109 @@ static lora_status check_group(int count, const lora_dims* dims, const void* pro
     return LORA_OK;
 }
 
-size_t lora_linear_fwd_grouped_workspace_bytes(int count, const lora_dims* dims) {
+static size_t fwd_grouped_ws(int count, const lora_dims* dims, bool dropout) {
     if (count < 1 || count > LORA_MAX_GROUP || !dims) return 0;
     size_t total = 0;
     for (int g = 0; g < count; ++g) {
-        const size_t w = fwd_workspace(&dims[g]);
+        const size_t w = dropout ? fwd_workspace_dropout(&dims[g]) : fwd_workspace(&dims[g]);
+        if (!w) return 0;
+        total += ws_align(w);
+    }
+    return total;
+}
+static size_t bwd_grouped_ws(int count, const lora_dims* dims, bool dropout) {
+    if (count < 1 || count > LORA_MAX_GROUP || !dims) return 0;
+    size_t total = 0;
+    for (int g = 0; g < count; ++g) {
+        const size_t w = dropout ? bwd_workspace_dropout(&dims[g]) : bwd_workspace(&dims[g]);
         if (!w) return 0;
         total += ws_align(w);
     }
     return total;
 }
 
+size_t lora_linear_fwd_grouped_workspace_bytes(int count, const lora_dims* dims) {
+    return fwd_grouped_ws(count, dims, false);
+}
 size_t lora_linear_bwd_grouped_workspace_bytes(int count, const lora_dims* dims) {
-    if (count < 1 || count > LORA_MAX_GROUP || !dims) return 0;
-    size_t total = 0;
-    for (int g = 0; g < count; ++g) {
-        const size_t w = bwd_workspace(&dims[g]);
-        if (!w) return 0;
-        total += ws_align(w);
+    return bwd_grouped_ws(count, dims, false);
+}
+size_t lora_linear_fwd_grouped_dropout_workspace_bytes(int count, const lora_dims* dims) {
+    return fwd_grouped_ws(count, dims, true);
+}
+size_t lora_linear_bwd_grouped_dropout_workspace_bytes(int count, const lora_dims* dims) {
+    return bwd_grouped_ws(count, dims, true);
+}
+
+// drops: per-problem dropout or NULL (no dropout)
+static lora_status fwd_grouped_impl(int count, const lora_dims* dims, const DropoutParams* drops,
+                                    const lora_fwd_problem* probs, void* workspace, size_t workspace_bytes,
+                                    void* stream, const char* fn) {
+    int launches = 0;
+    lora_status st = check_group(count, dims, probs, fn);
+    if (st != LORA_OK) return st;
+    const size_t need = fwd_grouped_ws(count, dims, drops != nullptr);
+    if (!need) return fail(LORA_ERR_SHAPE, "%s: invalid dims", fn);
+    if (!workspace || workspace_bytes < need)
+        return fail(LORA_ERR_WORKSPACE, "%s: workspace %zu < required %zu", fn, workspace_bytes, need);
+    cudaStream_t st_ = static_cast<cudaStream_t>(stream);
+    GemmCollector col;
+    for (int pass = 0; pass < 2; ++pass) {   // pass 0: validation of every problem before anything is enqueued
+        size_t off = 0;
+        for (int g = 0; g < count; ++g) {
+            const lora_fwd_problem& pr = probs[g];
+            const size_t wg = ws_align(drops ? fwd_workspace_dropout(&dims[g]) : fwd_workspace(&dims[g]));
+            st = fwd_impl(&dims[g], pr.x, pr.w0, pr.a, pr.b, pr.bias, pr.y, pr.h_out,
+                          static_cast<uint8_t*>(workspace) + off, wg, st_, &launches, &col,
+                          drops ? &drops[g] : nullptr, pass == 0);
+            if (st != LORA_OK) { set_launches(pass ? launches : 0); return st; }
+            off += wg;
+        }
     }
-    return total;
+    if ((st = launch_collected_k0(col, st_, &launches)) != LORA_OK) { set_launches(launches); return st; }
+    st = launch_collected(kModeFwd, col, st_, &launches);
+    set_launches(launches);
+    return st;
 }
 
 lora_status lora_linear_fwd_grouped(int count, const lora_dims* dims, const lora_fwd_problem* probs,
                                     void* workspace, size_t workspace_bytes, void* stream) {
-    int launches = 0;
-    lora_status st = check_group(count, dims, probs, "lora_linear_fwd_grouped");
-    if (st != LORA_OK) return st;
-    const size_t need = lora_linear_fwd_grouped_workspace_bytes(count, dims);
-    if (!need) return fail(LORA_ERR_SHAPE, "lora_linear_fwd_grouped: invalid dims");
-    if (!workspace || workspace_bytes < need)
-        return fail(LORA_ERR_WORKSPACE, "lora_linear_fwd_grouped: workspace %zu < required %zu", workspace_bytes,
-                    need);
-    cudaStream_t st_ = static_cast<cudaStream_t>(stream);
-    GemmCollector col;
-    size_t off = 0;
-    for (int g = 0; g < count; ++g) {   // validation of every problem before anything is enqueued
-        const lora_fwd_problem& pr = probs[g];
-        const size_t wg = ws_align(fwd_workspace(&dims[g]));
-        st = fwd_impl(&dims[g], pr.x, pr.w0, pr.a, pr.b, pr.bias, pr.y, pr.h_out,
-                      static_cast<uint8_t*>(workspace) + off, wg, st_, &launches, &col, nullptr, true);
-        if (st != LORA_OK) { set_launches(0); return st; }
-        off += wg;
-    }
-    off = 0;
+    return fwd_grouped_impl(count, dims, nullptr, probs, workspace, workspace_bytes, stream,
+                            "lora_linear_fwd_grouped");
+}
+
+static lora_status group_dropouts(int count, const lora_dropout* dropouts, DropoutParams* dp, const char* fn) {
+    if (!dropouts) return fail(LORA_ERR_INVALID, "%s: dropouts is NULL", fn);
+    if (count < 1 || count > LORA_MAX_GROUP) return fail(LORA_ERR_INVALID, "%s: count = %d", fn, count);
     for (int g = 0; g < count; ++g) {
-        const lora_fwd_problem& pr = probs[g];
-        const size_t wg = ws_align(fwd_workspace(&dims[g]));
-        st = fwd_impl(&dims[g], pr.x, pr.w0, pr.a, pr.b, pr.bias, pr.y, pr.h_out,
-                      static_cast<uint8_t*>(workspace) + off, wg, st_, &launches, &col);
-        if (st != LORA_OK) { set_launches(launches); return st; }
-        off += wg;
+        lora_status st = dropout_params(&dropouts[g], &dp[g]);
+        if (st != LORA_OK) return st;
+        if ((dp[g].thr > 0) != (dp[0].thr > 0))
+            return fail(LORA_ERR_UNSUPPORTED, "%s: problems %d and 0 disagree on p > 0 (one dX kernel mode per group)",
+                        fn, g);
     }
-    st = launch_collected(kModeFwd, col, st_, &launches);
-    set_launches(launches);
+    return LORA_OK;
+}
+
+lora_status lora_linear_fwd_grouped_dropout(int count, const lora_dims* dims, const lora_dropout* dropouts,
+                                            const lora_fwd_problem* probs, void* workspace, size_t workspace_bytes,
+                                            void* stream) {
+    DropoutParams dp[LORA_MAX_GROUP];
+    lora_status st = group_dropouts(count, dropouts, dp, "lora_linear_fwd_grouped_dropout");
+    if (st != LORA_OK) return st;
+    return fwd_grouped_impl(count, dims, dp, probs, workspace, workspace_bytes, stream,
+                            "lora_linear_fwd_grouped_dropout");
+}
+
+lora_status lora_linear_bwd_grouped_dropout(int count, const lora_dims* dims, const lora_dropout* dropouts,
+                                            const lora_bwd_problem* probs, int accumulate, void* workspace,
+                                            size_t workspace_bytes, void* stream) {
+    DropoutParams dp[LORA_MAX_GROUP];
+    lora_status st = group_dropouts(count, dropouts, dp, "lora_linear_bwd_grouped_dropout");
+    if (st == LORA_OK)
+        st = lora_host::bwd_grouped_impl(count, dims, probs, accumulate, workspace, workspace_bytes, stream, nullptr,
+                                         nullptr, nullptr, nullptr, dp);
+    lora_host::prof_clear();
     return st;
 }
 
@@ -1015,11 +1111,12 @@ namespace lora_host {
 lora_status bwd_grouped_impl(int count, const lora_dims* dims, const lora_bwd_problem* probs, int accumulate,
                              void* workspace, size_t workspace_bytes, void* stream,
                              lora_status (*after_k2)(void* ctx, int* launches), void* ctx,
-                             lora_status (*before_k2)(void* bctx, GemmCollector* col, int* launches), void* bctx) {
+                             lora_status (*before_k2)(void* bctx, GemmCollector* col, int* launches), void* bctx,
+                             const DropoutParams* drops) {
     int launches = 0;
     lora_status st = check_group(count, dims, probs, "lora_linear_bwd_grouped");
     if (st != LORA_OK) return st;
-    const size_t need = lora_linear_bwd_grouped_workspace_bytes(count, dims);
+    const size_t need = bwd_grouped_ws(count, dims, drops != nullptr);
     if (!need) return fail(LORA_ERR_SHAPE, "lora_linear_bwd_grouped: invalid dims");
     if (!workspace || workspace_bytes < need)
         return fail(LORA_ERR_WORKSPACE, "lora_linear_bwd_grouped: workspace %zu < required %zu", workspace_bytes,
@@ -1033,9 +1130,10 @@ lora_status bwd_grouped_impl(int count, const lora_dims* dims, const lora_bwd_pr
         size_t off = 0;
         for (int g = 0; g < count; ++g) {
             const lora_bwd_problem& pr = probs[g];
-            const size_t wg = ws_align(bwd_workspace(&dims[g]));
+            const size_t wg = ws_align(drops ? bwd_workspace_dropout(&dims[g]) : bwd_workspace(&dims[g]));
             st = bwd_impl(&dims[g], pr.x, pr.w0, pr.a, pr.b, pr.h_saved, pr.dy, pr.dx, pr.da, pr.db, acc,
-                          static_cast<uint8_t*>(workspace) + off, wg, st_, &launches, &col, kStageValidate);
+                          static_cast<uint8_t*>(workspace) + off, wg, st_, &launches, &col, kStageValidate,
+                          drops ? &drops[g] : nullptr);
             if (st != LORA_OK) { set_launches(0); return st; }
             off += wg;
         }
@@ -1044,9 +1142,10 @@ lora_status bwd_grouped_impl(int count, const lora_dims* dims, const lora_bwd_pr
         size_t off = 0;
         for (int g = 0; g < count; ++g) {
             const lora_bwd_problem& pr = probs[g];
-            const size_t wg = ws_align(bwd_workspace(&dims[g]));
+            const size_t wg = ws_align(drops ? bwd_workspace_dropout(&dims[g]) : bwd_workspace(&dims[g]));
             st = bwd_impl(&dims[g], pr.x, pr.w0, pr.a, pr.b, pr.h_saved, pr.dy, pr.dx, pr.da, pr.db, acc,
-                          static_cast<uint8_t*>(workspace) + off, wg, st_, &launches, &col, stage);
+                          static_cast<uint8_t*>(workspace) + off, wg, st_, &launches, &col, stage,
+                          drops ? &drops[g] : nullptr);
             if (st != LORA_OK) { set_launches(launches); return st; }
             off += wg;
         }
@@ -1055,8 +1154,12 @@ lora_status bwd_grouped_impl(int count, const lora_dims* dims, const lora_bwd_pr
             return st;
         }
         if (stage == 1) {
+            if ((st = launch_collected_k0(col, st_, &launches)) != LORA_OK) {
+                set_launches(launches);
+                return st;
+            }
             prof_record(0, st_);
-            st = launch_collected(kModeDx, col, st_, &launches);
+            st = launch_collected(drops && drops[0].thr > 0 ? kModeDxDrop : kModeDx, col, st_, &launches);
             prof_record(1, st_);
             if (st != LORA_OK) {
                 set_launches(launches);

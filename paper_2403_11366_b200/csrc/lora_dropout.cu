@@ -162,6 +162,17 @@ cudaError_t launch_dropout_input(const bf16* x, int64_t T, int64_t n, const bf16
     return cudaGetLastError();
 }
 
+// the members of a group one launch each (a grouped kernel indexing the members
+// dynamically measured 1.5x slower per member, dropout path)
+cudaError_t launch_dropout_input_group(const DropoutGroup& G, int num_sms, cudaStream_t stream) {
+    for (int g = 0; g < G.count; ++g) {
+        const DropoutMember& M = G.m[g];
+        cudaError_t e = launch_dropout_input(G.x, G.T, G.n, M.a, M.r, M.drop, M.h, M.xm, M.bits, num_sms, stream);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
 cudaError_t launch_dropout_mask(int64_t T, int64_t n, const DropoutParams& d, uint8_t* mask, int num_sms,
                                 cudaStream_t stream) {
     if (T <= 0) return cudaSuccess;

@@ -30,7 +30,7 @@ lora_status bwd_grouped_impl(int count, const lora_dims* dims, const lora_bwd_pr
                              void* workspace, size_t workspace_bytes, void* stream,
                              lora_status (*after_k2)(void* ctx, int* launches), void* ctx,
                              lora_status (*before_k2)(void* bctx, GemmCollector* col, int* launches) = nullptr,
-                             void* bctx = nullptr);
+                             void* bctx = nullptr, const lora_sm100::DropoutParams* drops = nullptr);
 int r_pad_of(int r);
 lora_status merge_impl(const lora_dims* d, const void* w0, const void* a, const void* b, void* w_out,
                        cudaStream_t stream, int* launches);
@@ -45,6 +45,9 @@ struct GemmCollector {
     int rp[lora_sm100::kMaxGroup];
     int cg[lora_sm100::kMaxGroup];
     bool no_coop = false;   // launch the fused GEMMs non-cooperatively (comm-fused path)
+    // LoRA dropout: the K0 work of the collected problems, launched right before the
+    // fused GEMMs (launch_collected_k0)
+    lora_sm100::DropoutGroup k0{};
     int max_sms = 0;        // > 0: the fused GEMMs use at most this many SMs (comm-fused path, virtual ranks)
     // K3 (dA, dB) problems of the grouped backward, launched together at the end
     int k3_count = 0;
@@ -70,6 +73,8 @@ size_t fwd_workspace_dropout(const lora_dims* d);
 size_t bwd_workspace_dropout(const lora_dims* d);
 // launch the collected problems, one grouped launch per (r_pad, CTA group) class
 lora_status launch_collected(int mode, GemmCollector& col, cudaStream_t stream, int* launches);
+// launch the collected K0 work (if any)
+lora_status launch_collected_k0(GemmCollector& col, cudaStream_t stream, int* launches);
 // launch the collected K3 problems, one launch per rank bucket
 lora_status launch_collected_k3(GemmCollector& col, cudaStream_t stream, int* launches);
 size_t fwd_workspace(const lora_dims* d);

@@ -341,6 +341,22 @@ cudaError_t launch_add_f32(float* dst, const float* src, int64_t count, cudaStre
 
 // K0 (dropout): h = q (M . x) A^T [T, r] fp32, xm = M . x [T, n] bf16 and the keep bits
 // [T, ceil(n/32)] uint32 (bit c of word w = keep(t, 32 w + c)); any output may be null
+// K0 for several linears that share x (each its own mask and outputs), one launch
+struct DropoutMember {
+    const __nv_bfloat16* a;
+    int r;
+    DropoutParams drop;
+    float* h;
+    __nv_bfloat16* xm;
+    uint32_t* bits;
+};
+struct DropoutGroup {
+    const __nv_bfloat16* x;
+    int64_t T, n;
+    int count;
+    DropoutMember m[kMaxGroup];
+};
+cudaError_t launch_dropout_input_group(const DropoutGroup& G, int num_sms, cudaStream_t stream);
 cudaError_t launch_dropout_input(const __nv_bfloat16* x, int64_t T, int64_t n, const __nv_bfloat16* a, int r,
                                  const DropoutParams& d, float* h, __nv_bfloat16* xm, uint32_t* bits, int num_sms,
                                  cudaStream_t stream);

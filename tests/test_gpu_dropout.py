@@ -149,3 +149,37 @@ def test_dropout_invalid_p(L):
     for p in (1.0, -0.1, float("nan")):
         with pytest.raises(L.LoraError):
             L.lora_linear_fwd(x, w0, a, b, 16.0, dropout=(p, 0, 0))
+
+
+@pytest.mark.parametrize("r,h_saved", [(8, True), (16, False), (5, True)])
+def test_grouped_dropout_equals_single_calls(oracle_mod, L, r, h_saved):
+    """lora_linear_{fwd,bwd}_grouped_dropout: q/k/v-like members sharing x, each with
+    its own mask (seed / offset), one fused launch per kernel -- bitwise the single
+    dropout calls, and the oracle's values."""
+    T, n = 300, 256
+    ms = (256, 128, 136)
+    alpha = 16.0
+    base = make_lora_inputs(T, n, ms[0], r, seed=620)
+    ds, drops = [], []
+    for g, m in enumerate(ms):
+        d = make_lora_inputs(T, n, m, r, seed=621 + g)
+        d["x"] = base["x"]
+        ds.append(d)
+        drops.append((0.05, 900 + g, 3 * g))
+    x = dev_bf16(base["x"])
+    ts = [{k: dev_bf16(d[k]) for k in ("w0", "a", "b", "dy")} for d in ds]
+    fo = L.lora_linear_fwd_grouped([(x, t["w0"], t["a"], t["b"], None) for t in ts], [alpha] * 3, dropouts=drops)
+    go = L.lora_linear_bwd_grouped([(x, t["w0"], t["a"], t["b"], t["dy"], h if h_saved else None)
+                                    for t, (_, h) in zip(ts, fo)], [alpha] * 3, dropouts=drops)
+    torch.cuda.synchronize()
+    for g, (t, d) in enumerate(zip(ts, ds)):
+        y1, h1 = L.lora_linear_fwd(x, t["w0"], t["a"], t["b"], alpha, dropout=drops[g])
+        dx1, da1, db1 = L.lora_linear_bwd(x, t["w0"], t["a"], t["b"], t["dy"], alpha,
+                                          h_saved=h1 if h_saved else None, dropout=drops[g])
+        torch.cuda.synchronize()
+        assert torch.equal(fo[g][0], y1) and torch.equal(fo[g][1], h1)
+        assert torch.equal(go[g][0], dx1) and torch.equal(go[g][1], da1) and torch.equal(go[g][2], db1)
+        yo, _ = oracle_mod.lora_fwd(d["x"], d["w0"], d["a"], d["b"], alpha, dropout=drops[g])
+        gor = oracle_mod.lora_bwd(d["x"], d["w0"], d["a"], d["b"], d["dy"], alpha, dropout=drops[g])
+        assert relF(host_f64(y1), yo) <= TOL_OUT and relF(host_f64(dx1), gor["dx"]) <= TOL_OUT
+        assert relF(host_f64(da1), gor["da"]) <= TOL_GRAD and relF(host_f64(db1), gor["db"]) <= TOL_GRAD
