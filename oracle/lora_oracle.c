@@ -37,10 +37,13 @@
  *   dX[t,k] = sum_i G[t,i] W0[i,k] + q M[t,k] sum_j gh[t,j] A[j,k]
  *   dA[j,k] = sum_t gh[t,j] xd[t,k]          (y, gh, dB unchanged given h)
  * M is a pure function of (t, k, seed, offset, p) through Philox4x32-10
- * (Salmon et al., SC'11), so the backward regenerates it:
- *   (w0..w3) = Philox4x32-10(counter = (k/4, t, offset_lo, offset_hi),
+ * (Salmon et al., SC'11), so the backward regenerates it; each 32-bit output
+ * word gives two 16-bit draws (R7, round 2: one Philox block per 8
+ * columns, p resolved to 2^-16):
+ *   (w0..w3) = Philox4x32-10(counter = (k/8, t, offset_lo, offset_hi),
  *                            key = (seed_lo, seed_hi));
- *   M[t,k] = (w_{k mod 4} >= floor(p 2^32)).
+ *   u[t,k]   = (w_{(k mod 8) / 2} >> (16 ((k mod 8) mod 2))) & 0xFFFF;
+ *   M[t,k]   = (u[t,k] >= floor(p 2^16)).
  *
  * Arithmetic: every input is a bf16 bit pattern ("brain
  * floating point"), widened exactly to double; every sum is accumulated in
@@ -293,9 +296,9 @@ void oracle_philox4x32_10(const uint32_t ctr_in[4], const uint32_t key_in[2], ui
     out[0] = c[0]; out[1] = c[1]; out[2] = c[2]; out[3] = c[3];
 }
 
-/* keep threshold: floor(p 2^32) for the fp32 dropout probability p in [0, 1) */
+/* keep threshold: floor(p 2^16) for the fp32 dropout probability p in [0, 1) */
 uint32_t oracle_dropout_threshold(float p) {
-    const double v = (double)p * 4294967296.0;
+    const double v = (double)p * 65536.0;
     return (uint32_t)v;   /* truncation == floor for v >= 0 */
 }
 
@@ -308,10 +311,11 @@ int oracle_dropout_mask(int64_t T, int64_t n, float p, uint64_t seed, uint64_t o
 #pragma omp parallel for schedule(static)
     for (t = 0; t < T; ++t) {
         for (int64_t k = 0; k < n; ++k) {
-            const uint32_t ctr[4] = {(uint32_t)(k / 4), (uint32_t)t, (uint32_t)offset, (uint32_t)(offset >> 32)};
+            const uint32_t ctr[4] = {(uint32_t)(k / 8), (uint32_t)t, (uint32_t)offset, (uint32_t)(offset >> 32)};
             uint32_t w[4];
             oracle_philox4x32_10(ctr, key, w);
-            mask[t * n + k] = w[k % 4] >= thr ? 1 : 0;
+            const uint32_t u = (w[(k % 8) / 2] >> (16 * ((k % 8) % 2))) & 0xFFFFu;
+            mask[t * n + k] = u >= thr ? 1 : 0;
         }
     }
     return 0;

@@ -30,17 +30,19 @@ def test_philox_known_answers(oracle_mod):
 
 
 def test_mask_counter_layout_and_threshold(oracle_mod):
-    """M[t,k] = Philox((k/4, t, offset_lo, offset_hi), (seed_lo, seed_hi))[k % 4] >= floor(p 2^32)."""
-    T, n, p, seed, off = 5, 24, 0.3, 0x1234567890ABCDEF, (7 << 32) | 9
+    """M[t,k] = 16-bit draw (k % 8) of Philox((k/8, t, offset_lo, offset_hi), (seed_lo, seed_hi))
+    >= floor(p 2^16): word (k % 8) / 2, low half for even k % 8 (R7)."""
+    T, n, p, seed, off = 5, 40, 0.3, 0x1234567890ABCDEF, (7 << 32) | 9
     m = oracle_mod.dropout_mask(T, n, p, seed, off)
     thr = oracle_mod.dropout_threshold(p)
-    assert thr == int(np.floor(float(np.float32(p)) * 2.0 ** 32))
-    assert oracle_mod.dropout_threshold(0.5) == 2 ** 31 and oracle_mod.dropout_threshold(0.0) == 0
+    assert thr == int(np.floor(float(np.float32(p)) * 2.0 ** 16))
+    assert oracle_mod.dropout_threshold(0.5) == 2 ** 15 and oracle_mod.dropout_threshold(0.0) == 0
     for t in range(T):
         for k in range(n):
-            w = oracle_mod.philox4x32_10((k // 4, t, off & 0xFFFFFFFF, off >> 32),
+            w = oracle_mod.philox4x32_10((k // 8, t, off & 0xFFFFFFFF, off >> 32),
                                          (seed & 0xFFFFFFFF, seed >> 32))
-            assert m[t, k] == (1 if w[k % 4] >= thr else 0)
+            u = (w[(k % 8) // 2] >> (16 * (k % 2))) & 0xFFFF
+            assert m[t, k] == (1 if u >= thr else 0)
 
 
 def test_mask_statistics_and_streams(oracle_mod):
