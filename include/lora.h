@@ -154,8 +154,9 @@ lora_status lora_adam_step(int count, const lora_adam_tensor* tensors, const lor
  *   y  = x W0^T + s (q (M . x) A^T) B^T (+ bias),   h = q (M . x) A^T
  *   dX = dy W0 + q M . (gh A),   dA = q gh^T (M . x),   dB = s dy^T h
  * M is a pure function of (t, k, seed, offset, p) -- Philox4x32-10 with
- * counter (k/4, t, offset_lo, offset_hi) and key (seed_lo, seed_hi); element
- * (t, k) is kept iff word k%4 >= floor(p * 2^32) -- so the backward, given
+ * counter (k/8, t, offset_lo, offset_hi) and key (seed_lo, seed_hi) gives eight
+ * 16-bit draws u = (word (k%8)/2 >> 16 (k%2)) & 0xFFFF; element (t, k) is kept
+ * iff u >= floor(p * 2^16) (p resolved to 2^-16) -- so the backward, given
  * the same lora_dropout, regenerates the forward's mask (nothing is stored).
  * Use a fresh offset (or seed) per step and per linear.  p = 0 gives exactly
  * the plain calls.  p must be in [0, 1) (LORA_ERR_INVALID otherwise). */

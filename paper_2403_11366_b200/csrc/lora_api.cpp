@@ -837,14 +837,14 @@ size_t bwd_workspace_dropout(const lora_dims* d) {
     return check_dims(d, true) == LORA_OK ? bwd_ws(d, true).total : 0;
 }
 
-// lora_dropout -> kernel parameters (threshold floor(p 2^32) computed in fp64, as the oracle does)
+// lora_dropout -> kernel parameters (threshold floor(p 2^16) computed in fp64, as the oracle does)
 lora_status dropout_params(const lora_dropout* dr, DropoutParams* out) {
     if (!dr) return fail(LORA_ERR_INVALID, "dropout is NULL");
     if (!(dr->p >= 0.0f && dr->p < 1.0f))
         return fail(LORA_ERR_INVALID, "dropout p = %g must be in [0, 1)", static_cast<double>(dr->p));
     out->seed = dr->seed;
     out->offset = dr->offset;
-    out->thr = static_cast<uint32_t>(static_cast<double>(dr->p) * 4294967296.0);
+    out->thr = static_cast<uint32_t>(static_cast<double>(dr->p) * 65536.0);   // 16-bit draws (R7)
     out->q = 1.0f / (1.0f - dr->p);
     return LORA_OK;
 }

@@ -10,6 +10,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstdint>
 
 #include "lora_kernels.h"
@@ -35,8 +36,8 @@ __device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8]) {
 // rows; the SPLIT warps of a row take contiguous column ranges (more warps in
 // flight than one-warp-per-row at small T), and their partial h sums are
 // combined in warp order through shared memory (deterministic).  Each lane
-// handles 8 consecutive columns per step: one 16-byte load of x, two Philox
-// blocks for the 8 keep bits.  Outputs (any may be null):
+// handles 8 consecutive columns per step: one 16-byte load of x, one Philox
+// block for the 8 keep bits.  Outputs (any may be null):
 //   h [T, r] = q (M . x) A^T     xm [T, n] = M . x (bf16, exact)
 //   bits [T, ceil(n/32)] uint32: bit c of word w = keep(t, 32 w + c)
 template <int RB, int SPLIT>
@@ -63,7 +64,7 @@ __global__ void __launch_bounds__(256) dropout_input_kernel(const bf16* __restri
             uint32_t keep = 0;
             if (ok) {
                 u = __ldg(reinterpret_cast<const uint4*>(xr + k));
-                keep = dropout_keep4(d, t, k / 4) | (dropout_keep4(d, t, k / 4 + 1) << 4);
+                keep = dropout_keep8(d, t, k / 8);   // (k % 8 == 0: one Philox block)
             }
             if (bits) {
                 // 4 lanes = 32 consecutive columns = one mask word
@@ -122,14 +123,14 @@ __global__ void __launch_bounds__(256) dropout_input_kernel(const bf16* __restri
 }
 
 __global__ void dropout_mask_kernel(int64_t T, int64_t n, DropoutParams d, uint8_t* __restrict__ mask) {
-    const int64_t n4 = (n + 3) / 4;
+    const int64_t n8 = (n + 7) / 8;
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < T * n4; i += stride) {
-        const int64_t t = i / n4, k4 = i - t * n4;
-        const uint32_t keep = dropout_keep4(d, t, k4);
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < T * n8; i += stride) {
+        const int64_t t = i / n8, k8 = i - t * n8;
+        const uint32_t keep = dropout_keep8(d, t, k8);
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
-            if (k4 * 4 + c < n) mask[t * n + k4 * 4 + c] = (keep >> c) & 1u;
+        for (int c = 0; c < 8; ++c)
+            if (k8 * 8 + c < n) mask[t * n + k8 * 8 + c] = (keep >> c) & 1u;
     }
 }
 
@@ -138,14 +139,32 @@ __global__ void dropout_mask_kernel(int64_t T, int64_t n, DropoutParams d, uint8
 template <int RB>
 static void launch_input_rb(const bf16* x, int64_t T, int64_t n, const bf16* a, int r, const DropoutParams& d,
                             float* h, bf16* xm, uint32_t* bits, int num_sms, cudaStream_t stream) {
-    // SPLIT warps per row when one warp per row would leave the SMs short of warps
-    const int64_t want_warps = static_cast<int64_t>(num_sms) * 48;
-    if (T * 2 >= want_warps || n <= 256) {
-        dropout_input_kernel<RB, 1><<<static_cast<unsigned>((T + 7) / 8), 256, 0, stream>>>(x, T, n, a, r, d, h,
-                                                                                          xm, bits);
-    } else if (T * 4 >= want_warps || n <= 1024) {
-        dropout_input_kernel<RB, 2><<<static_cast<unsigned>((T + 3) / 4), 256, 0, stream>>>(x, T, n, a, r, d, h,
-                                                                                          xm, bits);
+    // SPLIT warps per row: pick the split whose grid fills its last wave best (at
+    // cfg2, T = 2048: SPLIT 2 gave 512 CTAs = 1.15 waves of 3 CTAs / SM and ran
+    // at ~50% of its issue rate; SPLIT 8 gives 2048 CTAs = 4.6 waves)
+    static int per_sm[3] = {0, 0, 0};
+    if (!per_sm[0]) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[0], dropout_input_kernel<RB, 1>, 256, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[1], dropout_input_kernel<RB, 2>, 256, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[2], dropout_input_kernel<RB, 8>, 256, 0);
+        for (int i = 0; i < 3; ++i) per_sm[i] = per_sm[i] > 0 ? per_sm[i] : 1;
+    }
+    const int splits[3] = {1, 2, 8};
+    int best = 0;
+    double best_eff = -1.0;
+    for (int i = 0; i < 3; ++i) {
+        if (splits[i] > 1 && n <= 256 * (splits[i] / 2)) continue;   // a warp needs >= one 256-column step
+        const double blocks = static_cast<double>((T + 8 / splits[i] - 1) / (8 / splits[i]));
+        const double waves = blocks / (static_cast<double>(num_sms) * per_sm[i]);
+        const double eff = waves / std::ceil(waves);
+        if (eff > best_eff + 0.02) { best_eff = eff; best = i; }
+    }
+    if (best == 0) {
+        dropout_input_kernel<RB, 1><<<static_cast<unsigned>((T + 7) / 8), 256, 0, stream>>>(x, T, n, a, r, d, h, xm,
+                                                                                          bits);
+    } else if (best == 1) {
+        dropout_input_kernel<RB, 2><<<static_cast<unsigned>((T + 3) / 4), 256, 0, stream>>>(x, T, n, a, r, d, h, xm,
+                                                                                          bits);
     } else {
         dropout_input_kernel<RB, 8><<<static_cast<unsigned>(T), 256, 0, stream>>>(x, T, n, a, r, d, h, xm, bits);
     }

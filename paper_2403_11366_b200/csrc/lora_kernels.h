@@ -15,10 +15,10 @@ enum : int { kModeFwd = 0, kModeDx = 1, kModeDxDrop = 2 };
 bool pdl_enabled();
 bool k3_overlap_enabled();   // LORA_K3_OVERLAP (default on)
 
-// LoRA dropout (lora_philox.cuh): keep(t, k) = Philox4x32-10((k/4, t, offset), seed)[k % 4] >= thr
+// LoRA dropout (lora_philox.cuh): keep(t, k) = 16-bit draw (k % 8) of Philox4x32-10((k/8, t, offset), seed) >= thr
 struct DropoutParams {
     uint64_t seed, offset;
-    uint32_t thr;    // floor(p * 2^32); 0 = keep everything
+    uint32_t thr;    // floor(p * 2^16); 0 = keep everything
     float q;         // 1 / (1 - p)
 };
 

@@ -3,10 +3,11 @@
 //
 // Counter-based, so the backward regenerates the forward's mask instead of
 // storing it:  for element (t, k) of a [T, n] adapter input,
-//   (w0, w1, w2, w3) = Philox4x32-10(counter = (k / 4, t, offset_lo, offset_hi),
+//   (w0, w1, w2, w3) = Philox4x32-10(counter = (k / 8, t, offset_lo, offset_hi),
 //                                    key     = (seed_lo, seed_hi))
-//   keep(t, k)       = w_{k mod 4} >= thr,   thr = floor(p * 2^32).
-// One Philox block gives the keep bits of 4 consecutive columns.
+//   u(t, k)          = (w_{(k mod 8) / 2} >> 16 (k mod 2)) & 0xFFFF
+//   keep(t, k)       = u(t, k) >= thr,   thr = floor(p * 2^16).
+// One Philox block gives the keep bits of 8 consecutive columns (R7).
 #pragma once
 #include <cstdint>
 
@@ -33,14 +34,17 @@ __device__ __forceinline__ void philox4x32_10(uint32_t c0, uint32_t c1, uint32_t
     out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
 }
 
-// keep bits of columns 4*k4 .. 4*k4+3 of row t (bit i = column 4*k4 + i)
-__device__ __forceinline__ uint32_t dropout_keep4(const DropoutParams& d, int64_t t, int64_t k4) {
+// keep bits of columns 8*k8 .. 8*k8+7 of row t (bit i = column 8*k8 + i): one
+// Philox block gives eight 16-bit draws, draw i = half (i % 2) of word i / 2
+__device__ __forceinline__ uint32_t dropout_keep8(const DropoutParams& d, int64_t t, int64_t k8) {
     uint32_t w[4];
-    philox4x32_10(static_cast<uint32_t>(k4), static_cast<uint32_t>(t), static_cast<uint32_t>(d.offset),
+    philox4x32_10(static_cast<uint32_t>(k8), static_cast<uint32_t>(t), static_cast<uint32_t>(d.offset),
                   static_cast<uint32_t>(d.offset >> 32), static_cast<uint32_t>(d.seed),
                   static_cast<uint32_t>(d.seed >> 32), w);
-    return (w[0] >= d.thr ? 1u : 0u) | (w[1] >= d.thr ? 2u : 0u) | (w[2] >= d.thr ? 4u : 0u) |
-           (w[3] >= d.thr ? 8u : 0u);
+    uint32_t keep = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) keep |= (((w[i >> 1] >> (16 * (i & 1))) & 0xFFFFu) >= d.thr ? 1u : 0u) << i;
+    return keep;
 }
 
 }  // namespace lora_sm100
