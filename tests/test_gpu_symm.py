@@ -203,3 +203,68 @@ def test_row_fwd_fused_ipc_two_processes():
         assert exc is None, exc
         assert err <= TOL_OUT
     assert res[0][2] == res[1][2]   # both processes hold the same reduced y
+
+
+def _ipc_col_worker(rank, world, port, r, q):
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import torch.distributed as dist
+    try:
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+        import oracle
+        import paper_2403_11366_b200 as L
+        from paper_2403_11366_b200 import tp
+        T, n, ms, alpha = 256, 512, (512, 256), 16.0
+        base = make_lora_inputs(T, n, ms[0], r, seed=950)
+        ds = []
+        for g, m in enumerate(ms):
+            dg = make_lora_inputs(T, n, m, r, seed=951 + g)
+            dg["x"] = base["x"]
+            ds.append(dg)
+        x = dev_bf16(base["x"])
+        specs, probs = [], []
+        for g, (dg, m) in enumerate(zip(ds, ms)):
+            spec = tp.ShardSpec(tp.COLUMN, world, rank, n, m)
+            w0, a, b, _ = tp.shard_params(spec, dg["w0"], dg["a"], dg["b"])
+            w0, a, b = dev_bf16(w0), dev_bf16(a), dev_bf16(b)
+            _, h = L.lora_linear_fwd(x, w0, a, b, alpha)
+            specs.append(spec)
+            probs.append((x, w0, a, b, dev_bf16(tp.shard_output_grad(spec, dg["dy"])), h))
+        buf = tp.SymmBuffer(3 * T * n * 2 + 4096)
+        torch.cuda.synchronize()
+        dx, _ = tp.tp_linear_bwd_column_group_fused(buf, specs, probs, [alpha] * 2)
+        torch.cuda.synchronize()
+        ref = sum(oracle.lora_bwd(dg["x"], dg["w0"], dg["a"], dg["b"], dg["dy"], alpha)["dx"] for dg in ds)
+        err = relF(host_f64(dx), ref)
+        digest = int(dx.view(torch.int16).to(torch.int64).sum().item())
+        placement = buf.last_placement
+        dist.barrier()
+        buf.close()
+        q.put((rank, err, digest, placement, None))
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover - reported to the parent
+        q.put((rank, None, None, None, repr(e)))
+
+
+@pytest.mark.parametrize("r", [8, 32])
+def test_column_group_fused_ipc_two_processes(r):
+    """The CUDA IPC path of the fused column-group backward (one rank per process,
+    like one per GPU): r = 8 (the reducer fits next to the dX kernel: co-resident)
+    and r = 32 (a 226-register dX kernel leaves no room: the reducer runs after it)."""
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ipc_col_worker, args=(rk, 2, port, r, q)) for rk in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    for rank, err, digest, placement, exc in res:
+        assert exc is None, exc
+        assert err <= TOL_OUT
+    assert res[0][2] == res[1][2]
+    assert res[0][3] == ("coresident" if r == 8 else "after_gemm"), res[0][3]
