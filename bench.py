@@ -632,24 +632,48 @@ LAYERS = {   # the Llama-2 decoder layer at the RAFT sequence
 def run_layer(args, key):
     """One decoder-layer train step (forward + backward of every piece) per step,
     timed like the linear workloads (CUDA events, L2 flushed outside the events,
-    CUDA graph when capture works).  Single GPU (N = 1); the TP composition is
-    exercised by the tests."""
+    CUDA graph when capture works; max over ranks).  Under torchrun (or with
+    --force-tp at N = 1) the layer is tensor-parallel: q/k/v and
+    gate/up column-sharded (heads and FFN split), o and down row-sharded."""
     import torch
+    import torch.distributed as dist
 
+    from paper_2403_11366_b200 import tp
     from paper_2403_11366_b200.layer import LlamaLayerLoRA, layer_flops
     from synth import make_layer_inputs
     c = LAYERS[key]
-    dev = torch.device("cuda", 0)
-    torch.cuda.set_device(0)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
     import __graft_entry__
-    __graft_entry__._build_module().build()
+    if local_rank == 0:
+        __graft_entry__._build_module().build()
+    if world > 1:
+        dist.barrier(device_ids=[local_rank])
     import paper_2403_11366_b200 as L
     L.lora_device_check()
     bits = make_layer_inputs(c["T"], c["d"], c["f"], c["heads"], c["r"], seed=2403)
     cfg = dict(heads=c["heads"], head_dim=c["head_dim"], eps=1e-5, theta=10000.0, alpha=c["alpha"], ffn=c["f"])
-    params = {k: _bits_to_dev(v, dev) for k, v in bits.items() if k not in ("x", "dout")}
+    comm = tp.LoraComm() if (world > 1 or args.force_tp) else None
+    if comm is not None:   # this rank's shards (DESIGN.md R10-R11)
+        d_, f_ = c["d"], c["f"]
+        shard = {}
+        for p in ("q", "k", "v", "gate", "up", "o", "down"):
+            mode = tp.ROW if p in ("o", "down") else tp.COLUMN
+            n_, m_ = {"gate": (d_, f_), "up": (d_, f_), "down": (f_, d_)}.get(p, (d_, d_))
+            spec = tp.ShardSpec(mode, world, rank, n_, m_)
+            shard["w0_" + p], shard["a_" + p], shard["b_" + p], _ = tp.shard_params(
+                spec, bits["w0_" + p], bits["a_" + p], bits["b_" + p])
+        shard["g1"], shard["g2"] = bits["g1"], bits["g2"]
+        params = {k: _bits_to_dev(v, dev) for k, v in shard.items()}
+    else:
+        params = {k: _bits_to_dev(v, dev) for k, v in bits.items() if k not in ("x", "dout")}
     x, dout = _bits_to_dev(bits["x"], dev), _bits_to_dev(bits["dout"], dev)
-    layer = LlamaLayerLoRA(params, cfg)
+    layer = LlamaLayerLoRA(params, cfg, comm=comm)
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     flush_w = torch.empty(max(2 * l2, 256 << 20) // 4, dtype=torch.float32, device=dev)
     flush_r = torch.zeros_like(flush_w)
@@ -680,7 +704,10 @@ def run_layer(args, key):
             torch.cuda.synchronize()
     K = args.steps
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
-    with ClockSampler(0) as clk:
+    if world > 1:
+        dist.barrier(device_ids=[local_rank])
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
         for i in range(K):
             flush_w.fill_(float(i & 0xFF))
             torch.sum(flush_r)
@@ -693,18 +720,29 @@ def run_layer(args, key):
         torch.cuda.synchronize()
     ms = [a.elapsed_time(b) for a, b in ev]
     total = float(np.sum(ms))
+    if world > 1:
+        t = torch.tensor([total], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total = float(t.item())
     fl = layer_flops(c["T"], c["d"], c["f"], c["heads"], c["head_dim"], c["r"])
     peaks, peak_src = load_peaks()
     value = fl * K / (total * 1e-3) / 1e12
+    if comm is not None:
+        comm.close()
+    if world > 1:
+        dist.destroy_process_group()
+    if rank != 0:
+        return 0
     print(json.dumps({
         "metric": "LoRA Llama-2 decoder-layer fwd+bwd TFLOP/s and tokens/s", "value": value, "unit": "TFLOP/s",
-        "n_gpus": 1, "steps": K, "warmup": args.warmup, "ms_per_step": total / K, "higher_is_better": True,
+        "n_gpus": world, "steps": K, "warmup": args.warmup, "ms_per_step": total / K, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": key, "description": c["description"], "tokens": c["T"], "rank": c["r"],
+                   "parallelism": f"tp{world}" if comm is not None else "single",
                    "cuda_graph": graph is not None, "attention": "cuDNN SDPA (causal), library call",
                    "l2": "flushed between timed steps (outside the event pairs)"},
         "tokens_per_s": c["T"] * K / (total * 1e-3),
-        "pct_of_bf16_peak": value / peaks["bf16_tflops"] * 100.0,
+        "pct_of_bf16_peak": value / (peaks["bf16_tflops"] * world) * 100.0,
         "flops_per_step": fl, "peak_source": peak_src,
         "step_ms_median": float(np.median(ms)), "clocks": clk.summary()}), flush=True)
     return 0
