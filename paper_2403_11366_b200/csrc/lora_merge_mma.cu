@@ -38,6 +38,9 @@ namespace lora_sm100 {
 
 namespace {
 
+#ifndef LORA_MERGE_CTAS_PER_SM
+#define LORA_MERGE_CTAS_PER_SM 1
+#endif
 constexpr int kMBM = 128;          // W0 rows per tile (UMMA M)
 constexpr int kMThreads = 320;   // producer, MMA, 8 epilogue warps
 constexpr int kMSmemLimit = 227 * 1024;
@@ -50,14 +53,18 @@ struct MergeCfg {
     static constexpr int B_BYTES = kMBM * BROW;                  // B rows, K-major
     static constexpr int A_BYTES = NBOX * R_PAD * 128;           // A, 64-column MN-major blocks
     static constexpr int STAGE_BYTES = W_BYTES + B_BYTES + A_BYTES;
-    static constexpr int STAGES = (kMSmemLimit - 2048) / STAGE_BYTES > 8 ? 8 : (kMSmemLimit - 2048) / STAGE_BYTES;
+    // LORA_MERGE_CTAS_PER_SM CTAs per SM share the shared memory (experiment: 1 or 2)
+    static constexpr int HALF_SM = (228 * 1024) / 2 - 1024;
+    static constexpr int CTAS = (LORA_MERGE_CTAS_PER_SM == 2 && 2 * STAGE_BYTES + 2048 <= HALF_SM) ? 2 : 1;
+    static constexpr int SMEM_AVAIL = CTAS == 1 ? kMSmemLimit : HALF_SM;
+    static constexpr int STAGES = (SMEM_AVAIL - 2048) / STAGE_BYTES > 8 ? 8 : (SMEM_AVAIL - 2048) / STAGE_BYTES;
     static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /* barriers */ + 1024 /* alignment */;
     static constexpr uint32_t B_LAYOUT = BROW == 32 ? kLayoutSW32 : (BROW == 64 ? kLayoutSW64 : kLayoutSW128);
     static_assert(STAGES >= 2, "shared memory budget");
 };
 
 template <int R_PAD, int BN>
-__global__ void __launch_bounds__(kMThreads, 1) merge_mma_kernel(const __grid_constant__ MergeMaps mp, int64_t m,
+__global__ void __launch_bounds__(kMThreads, MergeCfg<R_PAD, BN>::CTAS) merge_mma_kernel(const __grid_constant__ MergeMaps mp, int64_t m,
                                                                 int64_t n, float s) {
     using C = MergeCfg<R_PAD, BN>;
     constexpr int kMBN = BN;
@@ -222,7 +229,8 @@ cudaError_t launch_rp(const MergeMaps& maps, int64_t m, int64_t n, float s, int 
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
     if (e != cudaSuccess) return e;
     const int64_t ntiles = ((m + kMBM - 1) / kMBM) * ((n + BN - 1) / BN);
-    const int grid = static_cast<int>(ntiles < num_sms ? ntiles : num_sms);
+    const int64_t slots = static_cast<int64_t>(num_sms) * C::CTAS;
+    const int grid = static_cast<int>(ntiles < slots ? ntiles : slots);
     if (grid <= 0) return cudaSuccess;
     kern<<<grid, kMThreads, C::SMEM_BYTES, stream>>>(maps, m, n, s);
     return cudaGetLastError();
