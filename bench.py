@@ -266,7 +266,7 @@ class StepRunner:
     patterns of the unsharded inputs stay in `host` for the parity checks."""
 
     def __init__(self, wl, dev, world=1, rank=0, comm=None, group=True, dropout=0.0, nsets=1, seed0=2403,
-                 comm_mode="nccl"):
+                 comm_mode="nccl", keep_mask="kept"):
         import torch
 
         import paper_2403_11366_b200 as L
@@ -304,7 +304,14 @@ class StepRunner:
                 wb = max(wb, int(L.lib.lora_linear_bwd_dropout_workspace_bytes(ctypes.byref(dd))))
             e["ws_f"] = torch.empty(max(256, wf), dtype=torch.uint8, device=dev)
             e["ws_b"] = torch.empty(max(256, wb), dtype=torch.uint8, device=dev)
-            e["drop"] = (dropout, 2403, i) if dropout > 0.0 else None   # one Philox stream per linear
+            # one Philox stream per linear; keep_mask "kept": the forward stores the keep bits
+            # (T n / 8 bytes, lora_dropout.keep_bits) and M . x (lora_dropout.masked_x), the
+            # backward reads them instead of drawing and masking again
+            e["drop"] = None
+            if dropout > 0.0:
+                e["drop"] = (dropout, 2403, i) + ((L.dropout_keep_bits(T, n, dev),
+                                                   torch.empty((T, n), dtype=torch.bfloat16, device=dev))
+                                                  if keep_mask == "kept" else ())
             lin.append(e)
         for gidx in wl.groups:   # one shared x tensor per group (per set)
             x0 = _bits_to_dev(tp.shard_input(lin[gidx[0]]["spec"], self.host[gidx[0]]["x"]), dev)
@@ -595,7 +602,7 @@ class StepRunner:
                                                  np.arange(max(0, T - 32), T)]))
             else:
                 rows = rows_per_linear
-            kw = {"dropout": e["drop"]} if e["drop"] is not None else {}   # (LoRA dropout: the same mask)
+            kw = {"dropout": e["drop"][:3]} if e["drop"] is not None else {}   # (LoRA dropout: the same mask)
             yo, ho = oracle.lora_fwd(d["x"], d["w0"], d["a"], d["b"], l.alpha, rows=rows, **kw)
             go = oracle.lora_bwd(d["x"], d["w0"], d["a"], d["b"], d["dy"], l.alpha, rows=rows, **kw)
             ri = self.torch.as_tensor(rows, device=self.dev)
@@ -775,7 +782,7 @@ def run_ours(args, wl):
     stream = torch.cuda.current_stream()
     comm = tp.LoraComm() if (world > 1 or args.force_tp) else None
     R = StepRunner(wl, dev, world, rank, comm, group=not args.no_group, dropout=args.dropout, nsets=2,
-                   comm_mode=args.comm)
+                   comm_mode=args.comm, keep_mask=args.dropout_mask)
     lin = R.lin
 
     # L2 flush between timed steps, outside the event pairs: write a 2 x L2
@@ -1078,6 +1085,10 @@ def run_ours(args, wl):
                        "grouped_calls": ([[wl.linears[i].name for i in g] for g in wl.groups] if grouped else None),
                        "shared_inputs": [[wl.linears[i].name for i in g] for g in wl.groups if len(g) > 1],
                        "lora_dropout": args.dropout,
+                       "dropout_mask": (None if args.dropout == 0.0 else
+                                        "kept: the forward stores the keep bits (T n / 8 bytes per linear) and "
+                                        "M . x (2 T n bytes), the backward reads them" if args.dropout_mask == "kept" else
+                                        "redrawn: the backward regenerates the Philox mask"),
                        "l2": "flushed between timed steps (2xL2 write then 2xL2 read, outside the "
                              "event pairs)"},
             "tokens_per_s": tokens * K / (total_ms * 1e-3),
@@ -1149,6 +1160,9 @@ def main():
                     help="run the tensor-parallel code path (NCCL communicator, TP entry points) even at N = 1")
     ap.add_argument("--dropout", type=float, default=0.0,
                     help="LoRA dropout p (Listing 3 LORA_DROPOUT = 0.05); 0 = the north-star path")
+    ap.add_argument("--dropout-mask", choices=("kept", "redraw"), default="kept",
+                    help="with --dropout: keep the forward's mask bits for the backward (lora_dropout.keep_bits) "
+                         "or redraw them")
     ap.add_argument("--no-group", action="store_true",
                     help="one call per linear instead of grouped calls for linears sharing an input")
     ap.add_argument("--layer", choices=sorted(LAYERS), default=None,

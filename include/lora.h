@@ -157,13 +157,26 @@ lora_status lora_adam_step(int count, const lora_adam_tensor* tensors, const lor
  * counter (k/8, t, offset_lo, offset_hi) and key (seed_lo, seed_hi) gives eight
  * 16-bit draws u = (word (k%8)/2 >> 16 (k%2)) & 0xFFFF; element (t, k) is kept
  * iff u >= floor(p * 2^16) (p resolved to 2^-16) -- so the backward, given
- * the same lora_dropout, regenerates the forward's mask (nothing is stored).
+ * the same lora_dropout, regenerates the forward's mask (nothing needs to be
+ * stored).  Optionally the caller keeps the mask instead: keep_bits, a device
+ * buffer of tokens x ceil(d_in / 32) uint32 (bit c of word w of row t =
+ * M[t, 32 w + c]; 16-byte aligned; owned by the caller), is WRITTEN by the
+ * forward calls and READ by the backward calls (which then draw nothing: the
+ * buffer must hold the bits the forward wrote with the same p, seed, offset).
+ * NULL: the backward redraws.  T n / 8 bytes per linear (1 MB at 2048 x 4096).
+ * Likewise masked_x, a device buffer of tokens x d_in bf16 (16-byte aligned):
+ * the forward writes M . x there (exact: zeroing only) and the backward reads
+ * it for dA instead of masking x again (2 T n bytes per linear, what a framework
+ * saves for the adapter's backward anyway).  With both buffers and h_saved the
+ * backward draws and masks nothing.  Both are untouched when p = 0.
  * Use a fresh offset (or seed) per step and per linear.  p = 0 gives exactly
  * the plain calls.  p must be in [0, 1) (LORA_ERR_INVALID otherwise). */
 typedef struct {
     float p;          /* drop probability */
     uint64_t seed;    /* Philox key */
     uint64_t offset;  /* Philox counter high words: a stream per (step, linear) */
+    uint32_t* keep_bits;  /* optional: [tokens, ceil(d_in/32)] keep mask, fwd writes / bwd reads */
+    void* masked_x;       /* optional: [tokens, d_in] bf16 M . x, fwd writes / bwd reads */
 } lora_dropout;
 
 /* As lora_linear_fwd, plus one launch (K0: h from the masked input). */

@@ -67,7 +67,8 @@ LORA_ADAM_MAX_TENSORS = 64
 
 
 class lora_dropout(ctypes.Structure):
-    _fields_ = [("p", ctypes.c_float), ("seed", ctypes.c_uint64), ("offset", ctypes.c_uint64)]
+    _fields_ = [("p", ctypes.c_float), ("seed", ctypes.c_uint64), ("offset", ctypes.c_uint64),
+                ("keep_bits", ctypes.c_void_p), ("masked_x", ctypes.c_void_p)]
 
 
 LORA_MAX_GROUP = 8
@@ -312,9 +313,24 @@ def lora_device_check() -> None:
 
 
 def _dropout(dropout):
-    """(p, seed, offset) -> lora_dropout (LoRA dropout; include/lora.h)."""
-    p, seed, offset = dropout
-    return lora_dropout(float(p), int(seed) & (2**64 - 1), int(offset) & (2**64 - 1))
+    """(p, seed, offset[, keep_bits[, masked_x]]) -> lora_dropout (LoRA dropout,
+    PAPER.md:82; include/lora.h).  keep_bits: optional int32 device tensor
+    [T, ceil(n/32)], masked_x: optional bf16 device tensor [T, n]; the forward
+    fills them (keep mask, M . x) and the backward reads them instead of redrawing."""
+    p, seed, offset = dropout[:3]
+    kb = dropout[3] if len(dropout) > 3 else None
+    mx = dropout[4] if len(dropout) > 4 else None
+    if kb is not None and (kb.dtype != torch.int32 or not kb.is_contiguous() or not kb.is_cuda):
+        raise ValueError("keep_bits must be a contiguous int32 CUDA tensor [T, ceil(n/32)]")
+    if mx is not None and (mx.dtype != torch.bfloat16 or not mx.is_contiguous() or not mx.is_cuda):
+        raise ValueError("masked_x must be a contiguous bf16 CUDA tensor [T, n]")
+    return lora_dropout(float(p), int(seed) & (2**64 - 1), int(offset) & (2**64 - 1),
+                        kb.data_ptr() if kb is not None else None, mx.data_ptr() if mx is not None else None)
+
+
+def dropout_keep_bits(T, n, device="cuda"):
+    """A keep-mask buffer for lora_dropout.keep_bits: int32 [T, ceil(n/32)]."""
+    return torch.empty((T, (n + 31) // 32), dtype=torch.int32, device=device)
 
 
 def lora_dropout_mask(T, n, dropout, device="cuda", stream=None):

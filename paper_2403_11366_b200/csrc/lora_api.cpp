@@ -312,7 +312,8 @@ lora_status fwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
         float* hd = h_out ? h_out : reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + W.h);
         p.h_in = hd;
         p.side_out = nullptr;
-        const DropoutMember mem{static_cast<const __nv_bfloat16*>(a), r, *drop, hd, nullptr, nullptr};
+        const DropoutMember mem{static_cast<const __nv_bfloat16*>(a), r, *drop, hd, drop->masked_x,
+                                drop->keep_bits, nullptr, {}};
         if (col) {
             if ((st = queue_k0(col, x, T, n, mem)) != LORA_OK) return st;
             return collect(col, maps, p, rp, cg);
@@ -541,21 +542,19 @@ lora_status launch_collected(int mode, GemmCollector& col, cudaStream_t stream, 
     return LORA_OK;
 }
 
-// K0 of the collected problems, one launch per problem (each linear draws its
-// own mask), in stream order right before the fused GEMMs.  Measured and dropped
-// (cfg2 q+v, p = 0.05, graph-replayed step; DESIGN.md dropout path): one grouped
-// K0 launch for the members sharing x, and the fused GEMM launched with
-// programmatic stream serialization to overlap K0 (its epilogue waiting for
-// it) -- 0.318-0.350 ms vs 0.309: K0 is issue-bound on every SM and cannot share
-// them with the GEMM's CTAs, so the overlap only interferes.
+// K0 of the collected problems (members sharing x, each its own mask), in
+// stream order right before the fused GEMMs: the forward's h products of all
+// members in one tensor-core launch, the backward's masked inputs and keep bits
+// in one streaming launch (lora_dropout.cu).  Measured and dropped (DESIGN.md
+// dropout path): the fused GEMM launched with programmatic stream serialization
+// to overlap K0 -- K0 fills every SM and cannot share them with the GEMM's CTAs.
 lora_status launch_collected_k0(GemmCollector& col, cudaStream_t stream, int* launches) {
     if (col.k0.count == 0) return LORA_OK;
     DevInfo dev;
     lora_status st = device_info(&dev);
     if (st != LORA_OK) return st;
-    cudaError_t e = launch_dropout_input_group(col.k0, dev.sms, stream);
+    cudaError_t e = launch_dropout_input_group(col.k0, dev.sms, stream, launches);
     if (e != cudaSuccess) return cuda_fail(e, "dropout K0 launch");
-    *launches += col.k0.count;
     col.k0.count = 0;
     return LORA_OK;
 }
@@ -636,15 +635,19 @@ lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
     const uint64_t* k2_flags = nullptr;   // this problem's K2 gh flags (stage 1; grouped stage 2: from col)
     bool gh_split = false, h_split = false;   // a row projection already wrote K3's split of gh / h
 
-    auto* xm = reinterpret_cast<__nv_bfloat16*>(wsb + W.xm);
+    // M . x for dA: the forward's (lora_dropout.masked_x) when the caller kept it, else K0 writes it
+    auto* xm = (drop && drop->masked_x) ? drop->masked_x : reinterpret_cast<__nv_bfloat16*>(wsb + W.xm);
     GemmCollector one;                      // single calls: K0 + K2 through a local collector
     GemmCollector* k0col = col ? col : &one;
     if (dropping && (stages & 1)) {
         // K0: keep bits for K2's epilogue, M . x for dA, h = q (M . x) A^T when not saved -- one
         // pass over x, queued (grouped: one launch for the members sharing x) right before K2,
         // which overlaps it and waits for it in its epilogue only
+        // (the caller's keep_bits from the forward: read, nothing drawn except for a recomputed h)
         const DropoutMember mem{static_cast<const __nv_bfloat16*>(a), r, *drop, need_h ? hbuf : nullptr,
-                                da ? xm : nullptr, dx ? reinterpret_cast<uint32_t*>(wsb + W.bits) : nullptr};
+                                (da && !drop->masked_x) ? xm : nullptr,
+                                (dx && !drop->keep_bits) ? reinterpret_cast<uint32_t*>(wsb + W.bits) : nullptr,
+                                drop->keep_bits, {}};
         if ((st = queue_k0(k0col, x, T, n, mem)) != LORA_OK) return st;
         if (!col && !dx && (st = launch_collected_k0(one, stream, launches)) != LORA_OK) return st;
     }
@@ -686,7 +689,8 @@ lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
         k2_flags = p.flags;
         p.h_in = nullptr;
         p.drop = dropping ? *drop : DropoutParams{};
-        p.drop_bits = dropping ? reinterpret_cast<const uint32_t*>(wsb + W.bits) : nullptr;
+        p.drop_bits = !dropping ? nullptr
+                      : drop->keep_bits ? drop->keep_bits : reinterpret_cast<const uint32_t*>(wsb + W.bits);
         // the gh tile also writes K3's split coefficients (gh; h when it already exists)
         p.t_pad = t_pad_of(T);
         p.sk_partial = W.partial_bytes ? reinterpret_cast<float*>(wsb + W.partial) : nullptr;
@@ -846,6 +850,12 @@ lora_status dropout_params(const lora_dropout* dr, DropoutParams* out) {
     out->offset = dr->offset;
     out->thr = static_cast<uint32_t>(static_cast<double>(dr->p) * 65536.0);   // 16-bit draws (R7)
     out->q = 1.0f / (1.0f - dr->p);
+    out->keep_bits = dr->keep_bits;
+    out->masked_x = static_cast<__nv_bfloat16*>(dr->masked_x);
+    if (dr->keep_bits && !aligned16(dr->keep_bits))
+        return fail(LORA_ERR_ALIGN, "dropout keep_bits = %p is not 16-byte aligned", static_cast<void*>(dr->keep_bits));
+    if (dr->masked_x && !aligned16(dr->masked_x))
+        return fail(LORA_ERR_ALIGN, "dropout masked_x = %p is not 16-byte aligned", dr->masked_x);
     return LORA_OK;
 }
 

@@ -78,9 +78,11 @@ __device__ __host__ __forceinline__ int partial_floats(const GradMmaSet& st) {
 }  // namespace
 
 #ifdef LORA_PROBE_K3
-// timing experiment only: per-CTA globaltimer stamps (start, main loop done,
-// partial written, reduction done)
-__device__ unsigned long long lora_k3_probe[16384 * 4];
+// timing experiment only: per-CTA globaltimer stamps (0 entry, 1 setup done,
+// 2 main loop done, 3 partial written, 4 reduction done, 5 exit) and, at
+// lora_k3_probe_host[0..1], a one-thread stamp kernel right before / after the launch
+constexpr int kProbeSlots = 6;
+__device__ unsigned long long lora_k3_probe[16384 * kProbeSlots + 2];
 extern "C" int lora_probe_k3_read(unsigned long long* host, int n) {   // read, then clear
     cudaError_t e = cudaMemcpyFromSymbol(host, lora_k3_probe, sizeof(unsigned long long) * n);
     void* p = nullptr;
@@ -88,10 +90,11 @@ extern "C" int lora_probe_k3_read(unsigned long long* host, int n) {   // read, 
     if (e == cudaSuccess) e = cudaMemset(p, 0, sizeof(lora_k3_probe));
     return static_cast<int>(e);
 }
+__global__ void k3_probe_stamp_kernel(int slot) { lora_k3_probe[16384 * kProbeSlots + slot] = globaltimer_ns(); }
 #define K3_STAMP(i)                                                                                   \
     do {                                                                                              \
         if (threadIdx.x == 64)                                                                        \
-            lora_k3_probe[(blockIdx.x * gridDim.y + blockIdx.y) * 4 + (i)] = globaltimer_ns();        \
+            lora_k3_probe[(blockIdx.x * gridDim.y + blockIdx.y) * kProbeSlots + (i)] = globaltimer_ns(); \
     } while (0)
 #else
 #define K3_STAMP(i) do {} while (0)
@@ -160,6 +163,7 @@ __device__ __forceinline__ void split3_store(const GradMmaSet& st, int k, int64_
 // transitive for the kernels after K3 -- then the last CTA out zeroes the K2
 // flags this launch waited on (self-cleaning sync pool, lora_kernels.h).
 __device__ __forceinline__ void k3_exit(const GradMmaGroup& G) {
+    K3_STAMP(5);
     if (G.done == nullptr || threadIdx.x != 0) {
         griddep_wait();
         return;
@@ -189,6 +193,7 @@ __global__ void __launch_bounds__(THREADS, 1) grad_mma_kernel(const __grid_const
     uint64_t* tmem_full = empty + MAX_STAGES;
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tmem_full + 1);
     float* partial = reinterpret_cast<float*>(smem);   // S > 1: reuses the ring after the main loop
+    K3_STAMP(0);
 
     const int tile = static_cast<int>(blockIdx.x);
     int jb = 0;
@@ -237,7 +242,7 @@ __global__ void __launch_bounds__(THREADS, 1) grad_mma_kernel(const __grid_const
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
-    K3_STAMP(0);
+    K3_STAMP(1);
 
     if (warp == 0) {
         // coefficients produced by a still-running K2: the whole warp polls its row-block
@@ -316,7 +321,7 @@ __global__ void __launch_bounds__(THREADS, 1) grad_mma_kernel(const __grid_const
         // ---------------- epilogue: TMEM -> (hi + mid + lo) -> global (S = 1) or partial (S > 1)
         mbar_wait(tmem_full, 0);
         tc_fence_after();
-        K3_STAMP(1);
+        K3_STAMP(2);
         const int lq = static_cast<int>(warp & 3);          // TMEM lane quarter of this warp
         for (int mt = 0; mt < MT; ++mt) {
         const int cl = mt * 128 + lq * 32 + static_cast<int>(lane);   // column within the tile
@@ -364,14 +369,14 @@ __global__ void __launch_bounds__(THREADS, 1) grad_mma_kernel(const __grid_const
         }
     }
     tc_fence_before();
-    if (warp == 2) K3_STAMP(2);
+    if (warp == 2) K3_STAMP(3);
     if (S == 1) {
         __syncthreads();
         if (warp == 1) {
             tc_fence_after();
             tmem_dealloc_n(tmem_base, G.tmem_cols);
         }
-        K3_STAMP(3);
+        K3_STAMP(4);
         k3_exit(G);
         return;
     }
@@ -443,7 +448,7 @@ __global__ void __launch_bounds__(THREADS, 1) grad_mma_kernel(const __grid_const
         }
         poff += partial_floats(st);
     }
-    K3_STAMP(3);
+    K3_STAMP(4);
     cluster.sync();   // peers may still read this CTA's partial
     k3_exit(G);
 }
@@ -571,8 +576,15 @@ cudaError_t launch_grad_mma(GradMmaGroup& G, int num_sms, cudaStream_t stream, b
     attrs[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attrs;
     cfg.numAttrs = overlap_prev && k3_overlap_enabled() ? 2 : 1;
+#ifdef LORA_PROBE_K3
+    k3_probe_stamp_kernel<<<1, 1, 0, stream>>>(0);
+#endif
+    if (getenv("LORA_K3_NOCLUSTER") && G.S == 1) cfg.numAttrs = 0;   // (experiment)
     e = cudaLaunchKernelEx(&cfg, grad_mma_kernel, G);
     if (e != cudaSuccess) return e;
+#ifdef LORA_PROBE_K3
+    k3_probe_stamp_kernel<<<1, 1, 0, stream>>>(1);
+#endif
     return cudaGetLastError();
 }
 

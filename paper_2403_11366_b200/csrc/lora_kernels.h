@@ -20,6 +20,8 @@ struct DropoutParams {
     uint64_t seed, offset;
     uint32_t thr;    // floor(p * 2^16); 0 = keep everything
     float q;         // 1 / (1 - p)
+    uint32_t* keep_bits;   // caller's keep-mask buffer (lora_dropout.keep_bits) or null
+    __nv_bfloat16* masked_x;   // caller's M . x buffer (lora_dropout.masked_x) or null
 };
 
 struct FusedGemmParams {
@@ -342,13 +344,23 @@ cudaError_t launch_add_f32(float* dst, const float* src, int64_t count, cudaStre
 // K0 (dropout): h = q (M . x) A^T [T, r] fp32, xm = M . x [T, n] bf16 and the keep bits
 // [T, ceil(n/32)] uint32 (bit c of word w = keep(t, 32 w + c)); any output may be null
 // K0 for several linears that share x (each its own mask and outputs), one launch
+// Philox4x32-10 of one member, prepared on the host (launch_dropout_input_group):
+// the ten round keys and the counter's offset words, so the device rounds take
+// them as constant operands; thr2 = thr in both 16-bit halves
+struct PhiloxKeys {
+    uint32_t k0[10], k1[10];
+    uint32_t c2, c3;
+    uint32_t thr2;
+};
 struct DropoutMember {
     const __nv_bfloat16* a;
     int r;
     DropoutParams drop;
     float* h;
     __nv_bfloat16* xm;
-    uint32_t* bits;
+    uint32_t* bits;          // keep bits out (fwd: the caller's buffer; bwd: K2's)
+    const uint32_t* bits_in; // bwd: the forward's keep bits -- read instead of drawn
+    PhiloxKeys keys;         // (filled by the launcher from drop)
 };
 struct DropoutGroup {
     const __nv_bfloat16* x;
@@ -356,10 +368,7 @@ struct DropoutGroup {
     int count;
     DropoutMember m[kMaxGroup];
 };
-cudaError_t launch_dropout_input_group(const DropoutGroup& G, int num_sms, cudaStream_t stream);
-cudaError_t launch_dropout_input(const __nv_bfloat16* x, int64_t T, int64_t n, const __nv_bfloat16* a, int r,
-                                 const DropoutParams& d, float* h, __nv_bfloat16* xm, uint32_t* bits, int num_sms,
-                                 cudaStream_t stream);
+cudaError_t launch_dropout_input_group(const DropoutGroup& G, int num_sms, cudaStream_t stream, int* launches);
 // keep mask M [T, n] uint8 (for lora_dropout_mask)
 cudaError_t launch_dropout_mask(int64_t T, int64_t n, const DropoutParams& d, uint8_t* mask, int num_sms,
                                 cudaStream_t stream);

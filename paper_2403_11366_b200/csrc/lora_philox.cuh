@@ -47,4 +47,35 @@ __device__ __forceinline__ uint32_t dropout_keep8(const DropoutParams& d, int64_
     return keep;
 }
 
+// The same generator with the round keys and offset words prepared on the host
+// (PhiloxKeys): w = Philox4x32-10(counter (c0, c1, K.c2, K.c3), key (seed)).
+__device__ __forceinline__ void philox4x32_10_keys(uint32_t c0, uint32_t c1, const PhiloxKeys& K,
+                                                   uint32_t (&out)[4]) {
+    uint32_t c2 = K.c2, c3 = K.c3;
+#pragma unroll
+    for (int round = 0; round < 10; ++round) {
+        const uint32_t lo0 = 0xD2511F53u * c0, hi0 = __umulhi(0xD2511F53u, c0);
+        const uint32_t lo1 = 0xCD9E8D57u * c2, hi1 = __umulhi(0xCD9E8D57u, c2);
+        const uint32_t n0 = hi1 ^ c1 ^ K.k0[round], n2 = hi0 ^ c3 ^ K.k1[round];
+        c0 = n0;
+        c1 = lo1;
+        c2 = n2;
+        c3 = lo0;
+    }
+    out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+// Keep masks of the two 16-bit draws of one Philox word: 0xFFFF in each half
+// whose draw u satisfies u >= thr (thr2 = thr in both halves).  SWAR unsigned
+// compare without a borrow between the halves: t's top bit per half = (u & 0x7FFF)
+// >= (thr & 0x7FFF); u >= thr = (u_H & ~thr_H) | (~(u_H ^ thr_H) & t_H); prmt then
+// replicates each half's top bit over the half.
+__device__ __forceinline__ uint32_t keep_mask_word(uint32_t w, uint32_t thr2) {
+    const uint32_t t = (w | 0x80008000u) - (thr2 & 0x7FFF7FFFu);
+    const uint32_t ge = (w & ~thr2) | (~(w ^ thr2) & t);
+    uint32_t m;
+    asm("prmt.b32 %0, %1, 0, 0xBB99;" : "=r"(m) : "r"(ge));
+    return m;
+}
+
 }  // namespace lora_sm100

@@ -183,3 +183,72 @@ def test_grouped_dropout_equals_single_calls(oracle_mod, L, r, h_saved):
         gor = oracle_mod.lora_bwd(d["x"], d["w0"], d["a"], d["b"], d["dy"], alpha, dropout=drops[g])
         assert relF(host_f64(y1), yo) <= TOL_OUT and relF(host_f64(dx1), gor["dx"]) <= TOL_OUT
         assert relF(host_f64(da1), gor["da"]) <= TOL_GRAD and relF(host_f64(db1), gor["db"]) <= TOL_GRAD
+
+
+def _pack_bits(mask):
+    """uint8 [T, n] keep mask -> the lora_dropout.keep_bits layout: int32 [T, ceil(n/32)],
+    bit c of word w of row t = mask[t, 32 w + c] (include/lora.h)."""
+    T, n = mask.shape
+    nw = (n + 31) // 32
+    m = np.zeros((T, nw * 32), dtype=np.uint64)
+    m[:, :n] = mask
+    words = (m.reshape(T, nw, 32) << np.arange(32, dtype=np.uint64)).sum(axis=2)
+    return words.astype(np.uint32).view(np.int32)
+
+
+@pytest.mark.parametrize("shape", [(300, 200, 264, 5), (257, 136, 256, 16), (33, 40, 64, 33), (384, 4096, 1024, 8)])
+def test_keep_bits_forward_writes_backward_reads(oracle_mod, L, shape):
+    """lora_dropout.keep_bits / masked_x: the forward writes the oracle's keep mask
+    bit for bit (packed 32 per word) and M . x exactly, and a backward that reads
+    them instead of redrawing gives bitwise the redrawing backward's dX, dA, dB
+    (h saved and recomputed; each buffer alone and both)."""
+    T, n, m, r = shape
+    d = make_lora_inputs(T, n, m, r, seed=700 + r)
+    x, w0, a, b, dy = (dev_bf16(d[k]) for k in ("x", "w0", "a", "b", "dy"))
+    drop = (0.05, 4242 + r, 11)
+    kb = L.dropout_keep_bits(T, n)
+    kb.fill_(-1)
+    mx = torch.full((T, n), 7.0, dtype=torch.bfloat16, device="cuda")
+    y1, h1 = L.lora_linear_fwd(x, w0, a, b, 16.0, dropout=drop + (kb, mx))
+    y0, h0 = L.lora_linear_fwd(x, w0, a, b, 16.0, dropout=drop)
+    torch.cuda.synchronize()
+    assert torch.equal(y0, y1) and torch.equal(h0, h1)
+    mask = oracle_mod.dropout_mask(T, n, *drop)
+    np.testing.assert_array_equal(kb.cpu().numpy(), _pack_bits(mask))
+    np.testing.assert_array_equal(mx.view(torch.int16).cpu().numpy(),
+                                  np.where(mask != 0, d["x"].view(np.int16), np.int16(0)))
+    for hs in (h0, None):
+        g0 = L.lora_linear_bwd(x, w0, a, b, dy, 16.0, h_saved=hs, dropout=drop)
+        for extra in ((kb,), (None, mx), (kb, mx)):
+            g1 = L.lora_linear_bwd(x, w0, a, b, dy, 16.0, h_saved=hs, dropout=drop + extra)
+            torch.cuda.synchronize()
+            for u, v in zip(g0, g1):
+                assert torch.equal(u, v)
+
+
+def test_keep_bits_grouped(oracle_mod, L):
+    """Grouped dropout calls with a keep_bits buffer per member: bitwise the calls
+    without, and each buffer holds that member's oracle mask."""
+    T, n, r = 260, 256, 8
+    ms = (256, 136)
+    base = make_lora_inputs(T, n, ms[0], r, seed=720)
+    x = dev_bf16(base["x"])
+    ts, drops, kbs = [], [], []
+    for g, m in enumerate(ms):
+        dd = make_lora_inputs(T, n, m, r, seed=721 + g)
+        ts.append({k: dev_bf16(dd[k]) for k in ("w0", "a", "b", "dy")})
+        drops.append((0.05, 77 + g, 5 * g))
+        kbs.append((L.dropout_keep_bits(T, n), torch.empty((T, n), dtype=torch.bfloat16, device="cuda")))
+    fo0 = L.lora_linear_fwd_grouped([(x, t["w0"], t["a"], t["b"], None) for t in ts], [16.0] * 2, dropouts=drops)
+    fo1 = L.lora_linear_fwd_grouped([(x, t["w0"], t["a"], t["b"], None) for t in ts], [16.0] * 2,
+                                    dropouts=[dr + kb for dr, kb in zip(drops, kbs)])
+    go0 = L.lora_linear_bwd_grouped([(x, t["w0"], t["a"], t["b"], t["dy"], h) for t, (_, h) in zip(ts, fo0)],
+                                    [16.0] * 2, dropouts=drops)
+    go1 = L.lora_linear_bwd_grouped([(x, t["w0"], t["a"], t["b"], t["dy"], h) for t, (_, h) in zip(ts, fo1)],
+                                    [16.0] * 2, dropouts=[dr + kb for dr, kb in zip(drops, kbs)])
+    torch.cuda.synchronize()
+    for g in range(2):
+        assert torch.equal(fo0[g][0], fo1[g][0]) and torch.equal(fo0[g][1], fo1[g][1])
+        for u, v in zip(go0[g], go1[g]):
+            assert torch.equal(u, v)
+        np.testing.assert_array_equal(kbs[g][0].cpu().numpy(), _pack_bits(oracle_mod.dropout_mask(T, n, *drops[g])))
