@@ -37,38 +37,6 @@ __global__ void dropout_mask_kernel(int64_t T, int64_t n, DropoutParams d, uint8
 
 
 // ------------------------------------------------------------------ K0 (grouped)
-// x word i (elements 8 k8 + 2i, 2i + 1 of a row) masked by member M's draws:
-// one Philox block (counter (k8, t)) gives the 16-bit draws of the 8 elements.
-__device__ __forceinline__ uint4 masked8(const uint4& u, const PhiloxKeys& K, uint32_t k8, uint32_t t,
-                                         uint32_t (&w)[4]) {
-    philox4x32_10_keys(k8, t, K, w);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) w[i] = keep_mask_word(w[i], K.thr2);
-    return make_uint4(u.x & w[0], u.y & w[1], u.z & w[2], u.w & w[3]);
-}
-
-// keep bits of the 8 elements (bit e = element e) from the 4 mask words, and back
-__device__ __forceinline__ uint32_t keep8_of(const uint32_t (&w)[4]) {
-    uint32_t keep = 0;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) keep |= ((w[i] >> 15) & 1u) << (2 * i) | ((w[i] >> 31) << (2 * i + 1));
-    return keep;
-}
-__device__ __forceinline__ uint4 masked8_bits(const uint4& u, uint32_t keep) {
-    uint32_t m[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) m[i] = ((keep >> (2 * i)) & 1u) * 0x0000FFFFu | ((keep >> (2 * i + 1)) & 1u) * 0xFFFF0000u;
-    return make_uint4(u.x & m[0], u.y & m[1], u.z & m[2], u.w & m[3]);
-}
-
-__device__ __forceinline__ void mma_bf16_16816(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
-                                               uint32_t b0, uint32_t b1) {
-    asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-                 "{%0,%1,%2,%3};"
-                 : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-                 : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
-}
-
 // Forward K0 of a group of linears sharing x: h_g = q_g (M_g . x) A_g^T for every
 // member g, x streamed from HBM once.  The masked products run on the tensor
 // cores (mma.sync m16n8k16, bf16 in, fp32 accumulate): one warp = 16 token rows

@@ -27,12 +27,14 @@
 //                               and the keep bits K0 packed (32 per word)
 // K1 with dropout: h = q (M . x) A^T comes from K0 (p.h_in) instead of TMEM.
 //
-// Structure (persistent over output tiles, 6 warps per CTA):
-//   warp 0     : TMA producer (cp.async.bulk.tensor, SWIZZLE_128B, an
+// Structure (persistent over output tiles, 6 warps per CTA; the producer and
+// the MMA issuer have the highest warp ids, which the warp schedulers favour):
+//   warps 0..3 : epilogue (tcgen05.ld from TMEM, side output h / gh, tail
+//                MMA, bf16 conversion, global stores); warp 0 owns TMEM
+//   (dX dropout mode, r_pad 16: warps 4..7 drain the upper half of each tile)
+//   warp 4(+4) : TMA producer (cp.async.bulk.tensor, SWIZZLE_128B, an
 //                STAGES-deep shared-memory ring guarded by mbarriers)
-//   warp 1     : tcgen05.mma issuer (one elected thread), TMEM allocator
-//   warps 2..5 : epilogue (tcgen05.ld from TMEM, side output h / gh, tail
-//                MMA, bf16 conversion, global stores)
+//   warp 5(+4) : tcgen05.mma issuer (one elected thread)
 // TMEM holds two 256-column fp32 accumulators (512 columns), so the epilogue
 // of tile i overlaps the main loop of tile i+1.
 //
@@ -61,6 +63,14 @@ constexpr int BK = 64;             // k-block: 64 bf16 = one 128-byte swizzle ro
 constexpr int UMMA_K = 16;         // K per tcgen05.mma kind::f16
 constexpr int NT = 256;            // TMEM columns per accumulator buffer
 constexpr int NUM_THREADS = 192;   // 6 warps
+// dX dropout mode (r_pad 16): 4 more epilogue warps drain the upper half of every
+// tile's columns (the CUDA-core q M . (gh A) term doubles the drain; registers
+// allow the extra warps only at r_pad 16)
+template <int MODE, int R_PAD>
+struct EpiHelpers {
+    static constexpr int WARPS = (MODE == kModeDxDrop && R_PAD == 16) ? 4 : 0;
+    static constexpr int THREADS = NUM_THREADS + 32 * WARPS;
+};
 constexpr int SMEM_LIMIT = 227 * 1024;
 constexpr int DX_BN0 = 128;        // dx: width of the first (gh-producing) column tile
 
@@ -70,6 +80,9 @@ __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 
 #ifndef LORA_STAGES_CAP
 #define LORA_STAGES_CAP 8
+#endif
+#ifndef LORA_DROP_FHFMA  // 0: the dropout dX epilogue widens A to fp32 and uses FFMA2 (comparison)
+#define LORA_DROP_FHFMA 1
 #endif
 #ifndef LORA_TMA_STORE   // 0: the epilogue stores y / dX with per-thread 16-byte stores (comparison)
 #define LORA_TMA_STORE 1
@@ -443,7 +456,7 @@ struct UnitIter {
 //   w2   fwd CG=2: W0 box of BN-128 rows
 //   nar  fwd: A [r,n]; dx: B [m,r8]          tail  fwd: B [m,r8]; dx: A [r,n]
 template <int MODE, int R_PAD, int CG>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+__global__ void __launch_bounds__(EpiHelpers<MODE, R_PAD>::THREADS, 1)
 lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
     using C = GemmCfg<MODE, R_PAD, CG>;
     using Cols = ColTiles<MODE, C::BN>;
@@ -478,7 +491,14 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
     const uint32_t warp = warp_id();
     const uint32_t lane = lane_id();
 
-    if (warp == 0 && lane < static_cast<uint32_t>(grp.count)) {
+    // Warp roles.  The SM sub-partition's scheduler favours the highest warp id among
+    // eligible warps, so the TMA producer and the MMA issuer take the two HIGHEST ids
+    // (no epilogue warp -- all of them busy on the CUDA cores in the dropout dX mode --
+    // can delay an MMA issue or a TMA refill): epilogue warps 0..3 (TMEM lane quarter =
+    // warp & 3), drain helpers 4..4+H-1 (dropout dX), producer 4+H, MMA issuer 5+H.
+    constexpr uint32_t kHelp = EpiHelpers<MODE, R_PAD>::WARPS;
+    constexpr uint32_t W_PROD = 4 + kHelp, W_MMA = 5 + kHelp;
+    if (warp == W_PROD && lane < static_cast<uint32_t>(grp.count)) {
         const FusedGemmMaps& mp = grp.maps[lane];
         tma_prefetch_desc(&mp.act);
         tma_prefetch_desc(&mp.w);
@@ -490,7 +510,7 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
             tma_prefetch_desc(&mp.out16);
         }
     }
-    if (warp == 1 && lane == 0) {
+    if (warp == W_MMA && lane == 0) {
         for (int s = 0; s < C::STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
@@ -508,7 +528,7 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
         mbar_init(part_full, 1);
         fence_mbar_init();
     }
-    if (warp == 2) tmem_alloc_cg<CG>(tmem_holder);
+    if (warp == 0) tmem_alloc_cg<CG>(tmem_holder);
     tc_fence_before();
     if constexpr (CG == 2) cluster_sync(); else __syncthreads();
     tc_fence_after();
@@ -524,7 +544,7 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
     (void)probe_c0;
 #endif
 
-    if (warp == 0) {
+    if (warp == W_PROD) {
         // ===================== TMA producer (both CTAs) =====================
         if (elect_one()) {
             const uint64_t pol_w = l2_policy_evict_last();
@@ -603,7 +623,7 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
                 ++tt;
             }
         }
-    } else if (warp == 1) {
+    } else if (warp == W_MMA) {
         // ===================== MMA issuer (leader CTA) =====================
         if (leader && elect_one()) {
             constexpr uint32_t idesc_fwd = make_idesc_bf16(TM, NT, 0, 0);
@@ -655,9 +675,119 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
                 commit<CG>(&tmem_full[acc]);
             }
         }
+    } else if (warp >= 4) {
+        // ===================== dropout dX drain helpers (warps 4..7, both CTAs) =====================
+        // Same rows as epilogue warp (warp - 4) (same TMEM lane quarter); per tile: the row's
+        // gh (TMEM for the gh tile, else the published split rows), bf16(q gh), then the
+        // upper half of the tile's 16-column chunks; a 256-thread barrier with the epilogue
+        // warps releases the A tile and the accumulator.  (Stream-K off: the schedule only.)
+        if constexpr (EpiHelpers<MODE, R_PAD>::WARPS > 0 && !C::STORE_TMA) {
+            if (!grp.sk.enabled) {
+                const uint32_t quarter = warp & 3;
+                const uint32_t row_local = quarter * 32 + lane;
+                uint32_t tl = 0, tt = 0;
+                UnitIter<MODE, CG, BN> it(grp, pair, npairs);
+                Unit un;
+                for (; it.next(un); ++tl, ++tt) {
+                    const FusedGemmParams& p = grp.p[un.g];
+                    const int n_blk = un.n_blk;
+                    const int t_blk = un.t_blk;
+                    const int64_t row = static_cast<int64_t>(t_blk) * TM + crank * BM + row_local;
+                    const int n0 = Cols::start(n_blk);
+                    const int width = Cols::width(n_blk, p.N_out);
+                    const uint32_t acc = tl & 1;
+                    mbar_wait(&tmem_full[acc], (tl >> 1) & 1);
+                    tc_fence_after();
+                    const uint32_t tbase = tmem_base + ((quarter * 32) << 16) + acc * NT;
+                    float hv[R_PAD];
+                    if (n_blk == 0) {
+#pragma unroll
+                        for (int c = 0; c < R_PAD / 16; ++c) {
+                            uint32_t v[16];
+                            tmem_ld_32x32b_x16(tbase + DX_BN0 + 16 * c, v);
+                            tmem_ld_wait();
+#pragma unroll
+                            for (int e = 0; e < 16; ++e) hv[16 * c + e] = p.scale * __uint_as_float(v[e]);
+                        }
+                    } else {
+                        const uint64_t* flag = p.flags + static_cast<int64_t>(t_blk) * CG + crank;
+                        const uint64_t t_start = globaltimer_ns();
+                        while (ld_acquire_u64(flag) != p.epoch) {
+                            __nanosleep(64);
+                            if (globaltimer_ns() - t_start > kWaitTimeoutNs) {
+                                printf("lora dX kernel: gh flag wait timed out (row block %d)\n", t_blk);
+                                __trap();
+                            }
+                        }
+                        const int r8 = (p.r + 7) / 8 * 8;
+#pragma unroll
+                        for (int j = 0; j < R_PAD; ++j) {
+                            float v = 0.0f;
+                            if (j < p.r && row < p.T) {
+                                const __nv_bfloat16* c = p.cs_gh + static_cast<int64_t>(j) * p.t_pad + row;
+                                v = (__bfloat162float(c[0]) + __bfloat162float(c[static_cast<int64_t>(r8) * p.t_pad])) +
+                                    __bfloat162float(c[static_cast<int64_t>(2 * r8) * p.t_pad]);
+                            }
+                            hv[j] = v;
+                        }
+                    }
+                    uint32_t gq[R_PAD];
+#pragma unroll
+                    for (int j = 0; j < R_PAD; ++j)
+                        gq[j] = static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(p.drop.q * hv[j])));
+                    mbar_wait((tt & 1) ? tailop2_full : tailop_full, (tt >> 1) & 1);
+                    const bool row_ok = row < p.T;
+                    __nv_bfloat16* out_row = p.out + row * p.N_out;
+                    const int nc = width / 16, c_split = (nc + 1) / 2;
+                    const int64_t nw = (p.N_out + 31) / 32;
+#pragma unroll 1
+                    for (int c = c_split; c < nc; ++c) {
+                        uint32_t v[16];
+                        tmem_ld_32x32b_x16(tbase + 16 * c, v);
+                        tmem_ld_wait();
+                        const int64_t col = n0 + 16 * c;
+                        if (!(row_ok && col < p.N_out)) continue;   // (after the warp-wide TMEM load)
+                        const uint32_t kword = p.drop_bits[row * nw + col / 32];
+                        float f[16];
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) f[e] = __uint_as_float(v[e]);
+                        const int lc = 16 * c;
+                        const uint8_t* blk = s_tailb + (tt & 1) * round_up(C::TAILB_BYTES, 1024) +
+                                             (lc / 64) * (R_PAD * 128);
+                        const uint32_t ch = static_cast<uint32_t>((lc % 64) / 8);
+                        float lo[16];
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) lo[e] = 0.0f;
+#pragma unroll
+                        for (int j = 0; j < R_PAD; ++j) {
+                            if (j >= p.r) break;
+                            const uint4 a0 = *reinterpret_cast<const uint4*>(blk + swizzled_offset(j, ch, 128));
+                            const uint4 a1 = *reinterpret_cast<const uint4*>(blk + swizzled_offset(j, ch + 1, 128));
+                            const uint32_t aw[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+#pragma unroll
+                            for (int e = 0; e < 8; ++e) fma_bf16_pair(gq[j], aw[e], lo[2 * e], lo[2 * e + 1]);
+                        }
+                        const uint32_t keep = (kword >> ((c & 1) * 16)) & 0xFFFFu;
+#pragma unroll
+                        for (int e = 0; e < 16; ++e)
+                            if ((keep >> e) & 1u) f[e] += lo[e];
+                        uint4 q0, q1;
+                        q0.x = pack_bf16x2(f[0], f[1]);   q0.y = pack_bf16x2(f[2], f[3]);
+                        q0.z = pack_bf16x2(f[4], f[5]);   q0.w = pack_bf16x2(f[6], f[7]);
+                        q1.x = pack_bf16x2(f[8], f[9]);   q1.y = pack_bf16x2(f[10], f[11]);
+                        q1.z = pack_bf16x2(f[12], f[13]); q1.w = pack_bf16x2(f[14], f[15]);
+                        *reinterpret_cast<uint4*>(out_row + col) = q0;
+                        if (col + 8 < p.N_out) *reinterpret_cast<uint4*>(out_row + col + 8) = q1;
+                    }
+                    if (p.unit_flags != nullptr) __threadfence_system();
+                    tc_fence_before();
+                    named_bar_sync(2, 32 * (4 + EpiHelpers<MODE, R_PAD>::WARPS));   // with the epilogue warps
+                }
+            }
+        }
     } else {
-        // ===================== epilogue (warps 2..5, both CTAs) =====================
-        const uint32_t ew = warp - 2;            // epilogue warp index 0..3
+        // ===================== epilogue (warps 0..3, both CTAs) =====================
+        const uint32_t ew = warp;                // epilogue warp index 0..3
         const uint32_t quarter = warp & 3;       // TMEM lane quarter this warp may access
         const uint32_t row_local = quarter * 32 + lane;
         constexpr uint32_t idesc_tail_fwd = make_idesc_bf16(TM, BN, 0, 0);
@@ -892,6 +1022,14 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
                     hv[j] = v;
                 }
             }
+#if LORA_DROP_FHFMA
+            uint32_t gq[(MODE == kModeDxDrop) ? R_PAD : 1];   // bf16(q gh_j) in the low half
+            if constexpr (MODE == kModeDxDrop) {
+#pragma unroll
+                for (int j = 0; j < R_PAD; ++j)
+                    gq[j] = static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(p.drop.q * hv[j])));
+            }
+#endif
             if constexpr (MODE == kModeDxDrop) {
                 // dropout: no tail MMA -- the epilogue adds q M . (gh A) itself (step 5)
                 mbar_wait((tt & 1) ? tailop2_full : tailop_full, (tt >> 1) & 1);
@@ -958,8 +1096,12 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
             }
             const bool storer = (ew == 0 && lane == 0);
             const int64_t row0 = static_cast<int64_t>(t_blk) * TM + crank * BM;   // this CTA's first row
+            // (dropout dX with helper warps: this group drains the lower half of the chunks)
+            constexpr bool kHelp = EpiHelpers<MODE, R_PAD>::WARPS > 0 && !C::STORE_TMA;
+            const bool helped = kHelp && !grp.sk.enabled;
+            const int c_end = helped ? (width / 16 + 1) / 2 : width / 16;
 #pragma unroll 1
-            for (int c = 0; c < width / 16; ++c) {
+            for (int c = 0; c < c_end; ++c) {
                 uint32_t v[16];
                 tmem_ld_32x32b_x16(tbase + 16 * c, v);
                 tmem_ld_wait();
@@ -983,12 +1125,36 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
                         const uint8_t* blk = s_tailb + (tt & 1) * round_up(C::TAILB_BYTES, 1024) +
                                              (lc / 64) * (R_PAD * 128);
                         const uint32_t ch = static_cast<uint32_t>((lc % 64) / 8);
+#if LORA_DROP_FHFMA
+                        // mixed-precision FMA (FHFMA.BF16: fp32 += bf16 x bf16, the A element taken
+                        // straight from its bf16 half -- no widening instructions) with the operand
+                        // gq_j = bf16(q gh_j), the same rounding of gh as the plain path's tail MMA
+                        float lo[16];
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) lo[e] = 0.0f;
+#pragma unroll
+                        for (int j = 0; j < R_PAD; ++j) {
+#ifdef LORA_PROBE_DROP_NOFMA
+                            break;   // timing experiment only: no q M . (gh A) term
+#endif
+                            if (j >= p.r) break;   // (uniform) rows r..r_pad-1 of A are zero
+                            const uint4 a0 = *reinterpret_cast<const uint4*>(blk + swizzled_offset(j, ch, 128));
+                            const uint4 a1 = *reinterpret_cast<const uint4*>(blk + swizzled_offset(j, ch + 1, 128));
+                            const uint32_t aw[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+#pragma unroll
+                            for (int e = 0; e < 8; ++e) fma_bf16_pair(gq[j], aw[e], lo[2 * e], lo[2 * e + 1]);
+                        }
+                        const float qs = 1.0f;   // (q is inside gq)
+#else
                         // packed FFMA2 (two fp32 FMAs per instruction, same order and rounding)
                         float2 lo2[8];
 #pragma unroll
                         for (int e = 0; e < 8; ++e) lo2[e] = make_float2(0.0f, 0.0f);
 #pragma unroll
                         for (int j = 0; j < R_PAD; ++j) {
+#ifdef LORA_PROBE_DROP_NOFMA
+                            break;   // timing experiment only: no q M . (gh A) term
+#endif
                             if (j >= p.r) break;   // (uniform) rows r..r_pad-1 of A are zero
                             const uint4 a0 = *reinterpret_cast<const uint4*>(blk + swizzled_offset(j, ch, 128));
                             const uint4 a1 = *reinterpret_cast<const uint4*>(blk + swizzled_offset(j, ch + 1, 128));
@@ -1008,11 +1174,13 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
                             lo[2 * e] = lo2[e].x;
                             lo[2 * e + 1] = lo2[e].y;
                         }
+                        const float qs = p.drop.q;
+#endif
                         // keep bits of the 16 columns, packed by K0 (32 per word; col % 16 == 0)
                         const uint32_t keep = (kw[c >> 1] >> ((c & 1) * 16)) & 0xFFFFu;
 #pragma unroll
                         for (int e = 0; e < 16; ++e)
-                            if ((keep >> e) & 1u) f[e] = fmaf(p.drop.q, lo[e], f[e]);
+                            if ((keep >> e) & 1u) f[e] = fmaf(qs, lo[e], f[e]);
                     }
                     uint4 q0, q1;
                     q0.x = pack_bf16x2(f[0], f[1]);   q0.y = pack_bf16x2(f[2], f[3]);
@@ -1057,7 +1225,14 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
                 }
             }
             if constexpr (MODE == kModeDxDrop) {
-                named_bar_sync(1, 128);   // every epilogue warp is done with the A tile
+                // every epilogue (and helper) warp is done with the A tile (and the accumulator)
+                if (helped) {
+                    tc_fence_before();
+                    named_bar_sync(2, 32 * (4 + EpiHelpers<MODE, R_PAD>::WARPS));
+                    tc_fence_after();
+                } else {
+                    named_bar_sync(1, 128);
+                }
                 if (ew == 0 && lane == 0) mbar_arrive((tt & 1) ? tailop2_empty : tailop_empty);
             }
             if (p.unit_flags != nullptr) {
@@ -1093,7 +1268,7 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
         }
     }
 
-    if (C::STORE_TMA && warp == 2 && lane == 0) bulk_wait_group<0>();   // every y / dX store performed
+    if (C::STORE_TMA && warp == 0 && lane == 0) bulk_wait_group<0>();   // every y / dX store performed
     tc_fence_before();
     if constexpr (CG == 2) cluster_sync(); else __syncthreads();
 #ifdef LORA_PROBE_CLOCK
@@ -1101,7 +1276,7 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
         printf("PROBE_CLOCK mode=%d block=%d cycles=%lld ns=%llu\n", MODE, blockIdx.x, clock64() - probe_c0,
                (unsigned long long)(globaltimer_ns() - probe_t0));
 #endif
-    if (warp == 2) {
+    if (warp == 0) {
         tc_fence_after();
         tmem_dealloc_cg<CG>(tmem_base);
     }
@@ -1379,7 +1554,7 @@ static cudaError_t launch_impl(FusedGemmGroup& grp, int num_sms, cudaStream_t st
     if ((e = plan_stream_k<MODE, R_PAD, CG>(grp, grid / CG, stream)) != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(NUM_THREADS);
+    cfg.blockDim = dim3(EpiHelpers<MODE, R_PAD>::THREADS);
     cfg.dynamicSmemBytes = C::SMEM_BYTES;
     cfg.stream = stream;
     cudaLaunchAttribute attr[3];

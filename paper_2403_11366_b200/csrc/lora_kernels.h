@@ -24,6 +24,15 @@ struct DropoutParams {
     __nv_bfloat16* masked_x;   // caller's M . x buffer (lora_dropout.masked_x) or null
 };
 
+// Philox4x32-10 of one member, prepared on the host (launch_dropout_input_group):
+// the ten round keys and the counter's offset words, so the device rounds take
+// them as constant operands; thr2 = thr in both 16-bit halves
+struct PhiloxKeys {
+    uint32_t k0[10], k1[10];
+    uint32_t c2, c3;
+    uint32_t thr2;
+};
+
 struct FusedGemmParams {
     int64_t T;                    // token rows
     int64_t K;                    // reduction extent (n fwd, m dx)
@@ -344,14 +353,6 @@ cudaError_t launch_add_f32(float* dst, const float* src, int64_t count, cudaStre
 // K0 (dropout): h = q (M . x) A^T [T, r] fp32, xm = M . x [T, n] bf16 and the keep bits
 // [T, ceil(n/32)] uint32 (bit c of word w = keep(t, 32 w + c)); any output may be null
 // K0 for several linears that share x (each its own mask and outputs), one launch
-// Philox4x32-10 of one member, prepared on the host (launch_dropout_input_group):
-// the ten round keys and the counter's offset words, so the device rounds take
-// them as constant operands; thr2 = thr in both 16-bit halves
-struct PhiloxKeys {
-    uint32_t k0[10], k1[10];
-    uint32_t c2, c3;
-    uint32_t thr2;
-};
 struct DropoutMember {
     const __nv_bfloat16* a;
     int r;

@@ -9,13 +9,14 @@
 // one tcgen05.mma per 16 of r puts (B A) for a 128 x 64 tile into TMEM, and
 // the CUDA cores only add W0, scale and round.
 //
-// Persistent, one CTA per SM, 10 warps:
-//   warp 0     TMA producer: W0 tile [128 x 64] (one SW128 box), B rows
+// Persistent, one CTA per SM, 10 warps (producer and MMA issuer on the two highest
+// warp ids, which the warp schedulers favour over the busy epilogue warps):
+//   warp 8     TMA producer: W0 tile [128 x 64] (one SW128 box), B rows
 //              [128 x r_pad] (K-major), A [r_pad x 64] (MN-major SW128) -> an
 //              up to 8-deep ring (small tiles: more bytes in flight per SM)
-//   warp 1     MMA issuer: D[i, k] = sum_j B[i, j] A[j, k], r_pad / 16 MMAs
+//   warp 9     MMA issuer: D[i, k] = sum_j B[i, j] A[j, k], r_pad / 16 MMAs
 //              (M = 128, N = 64) into one of two TMEM accumulators
-//   warps 2-9  epilogue: two warps per TMEM lane quarter (32 columns each; one
+//   warps 0-7  epilogue: two warps per TMEM lane quarter (32 columns each; one
 //              warp per SM sub-partition left the drain latency-bound), row i
 //              per thread: tcgen05.ld, out = fma(s, D, W0) with
 //              W0 read from the stage, RNE bf16 written back IN PLACE into the
@@ -78,16 +79,19 @@ __global__ void __launch_bounds__(kMThreads, MergeCfg<R_PAD, BN>::CTAS) merge_mm
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tmem_empty + 2);
 
     const uint32_t warp = warp_id(), lane = lane_id();
+    // the producer and the MMA issuer take the highest warp ids (the warp schedulers
+    // favour them over the eight busy epilogue warps): epilogue 0..7, producer 8, MMA 9
+    constexpr uint32_t W_PROD = 8, W_MMA = 9;
     const int64_t nrb = (m + kMBM - 1) / kMBM, ncb = (n + kMBN - 1) / kMBN;
     const int64_t ntiles = nrb * ncb;
 
-    if (warp == 0 && lane == 0) {
+    if (warp == W_PROD && lane == 0) {
         tma_prefetch_desc(&mp.w);
         tma_prefetch_desc(&mp.out);
         tma_prefetch_desc(&mp.b);
         tma_prefetch_desc(&mp.a);
     }
-    if (warp == 1 && lane == 0) {
+    if (warp == W_MMA && lane == 0) {
         for (int i = 0; i < C::STAGES; ++i) {
             mbar_init(&full[i], 1);
             mbar_init(&empty[i], 1);
@@ -98,13 +102,13 @@ __global__ void __launch_bounds__(kMThreads, MergeCfg<R_PAD, BN>::CTAS) merge_mm
         }
         fence_mbar_init();
     }
-    if (warp == 2) tmem_alloc<2 * kMBN>(tmem_holder);
+    if (warp == 0) tmem_alloc<2 * kMBN>(tmem_holder);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
 
-    if (warp == 0) {
+    if (warp == W_PROD) {
         // ===================== TMA producer =====================
         if (elect_one()) {
             const uint64_t pol_stream = l2_policy_evict_first();
@@ -125,7 +129,7 @@ __global__ void __launch_bounds__(kMThreads, MergeCfg<R_PAD, BN>::CTAS) merge_mm
                 if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
             }
         }
-    } else if (warp == 1) {
+    } else if (warp == W_MMA) {
         // ===================== MMA issuer =====================
         if (elect_one()) {
             constexpr uint32_t idesc = make_idesc_bf16(kMBM, kMBN, 0, 1);
@@ -151,12 +155,12 @@ __global__ void __launch_bounds__(kMThreads, MergeCfg<R_PAD, BN>::CTAS) merge_mm
             }
         }
     } else {
-        // ===================== epilogue (warps 2..9) =====================
+        // ===================== epilogue (warps 0..7) =====================
         const uint32_t quarter = warp & 3;            // TMEM lane quarter this warp may access
-        const uint32_t half = (warp - 2) >> 2;        // this warp's columns: [CW half, CW half + CW)
+        const uint32_t half = warp >> 2;              // this warp's columns: [CW half, CW half + CW)
         constexpr int CW = BN / 2;
         const uint32_t row_local = quarter * 32 + lane;
-        const bool storer = (warp == 2 && lane == 0);
+        const bool storer = (warp == 0 && lane == 0);
         const uint64_t pol_stream = l2_policy_evict_first();
         uint32_t stage = 0, phase = 0, tl = 0;
         int prev_stage = -1;
@@ -216,7 +220,7 @@ __global__ void __launch_bounds__(kMThreads, MergeCfg<R_PAD, BN>::CTAS) merge_mm
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 2) {
+    if (warp == 0) {
         tc_fence_after();
         tmem_dealloc<2 * kMBN>(tmem_base);
     }

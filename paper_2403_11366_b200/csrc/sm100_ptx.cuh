@@ -226,6 +226,18 @@ __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
     return *reinterpret_cast<const float2*>(&d);
 }
 
+// mixed-precision FMAs (sm_100 FHFMA.BF16): c0 += g.lo * w.lo, c1 += g.lo * w.hi with
+// bf16 operands taken from 16-bit halves, fp32 accumulate, each rounded to nearest
+__device__ __forceinline__ void fma_bf16_pair(uint32_t g, uint32_t w, float& c0, float& c1) {
+    asm("{ .reg .b16 gl, gh, wl, wh;\n"
+        "  mov.b32 {gl, gh}, %2;\n"
+        "  mov.b32 {wl, wh}, %3;\n"
+        "  fma.rn.f32.bf16 %0, gl, wl, %0;\n"
+        "  fma.rn.f32.bf16 %1, gl, wh, %1; }"
+        : "+f"(c0), "+f"(c1)
+        : "r"(g), "r"(w));
+}
+
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }

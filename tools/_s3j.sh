@@ -1,0 +1,7 @@
+#!/bin/bash
+OUT=gpurun_out/s3j; mkdir -p $OUT
+timeout 600 python -m pytest tests/test_gpu_dropout.py -q -x > $OUT/dropout_tests.log 2>&1; tail -15 $OUT/dropout_tests.log
+for f in 1 0; do
+  LORA_DROP_FUSED=$f timeout 300 python bench.py --dropout 0.05 --steps 30 --warmup 5 --no-cpu-baseline 2>&1 | grep '^{' | python -c "import json,sys; d=json.loads(sys.stdin.read()); k=d['kernels_in_step']; print('fused=$f', round(d['ms_per_step']*1e3,1), 'K1', round(k['K1_fwd']['us'],1), 'K2', round(k['K2_dx']['us'],1), 'K3', round(k['K3_dA_dB']['us'],1), d['parity']['pass'], d['parity']['relF_max_over_linears'])"
+done
+timeout 300 python bench.py --steps 30 --warmup 5 --no-cpu-baseline 2>&1 | grep '^{' | python -c "import json,sys; d=json.loads(sys.stdin.read()); k=d['kernels_in_step']; print('p=0', round(d['ms_per_step']*1e3,1), 'K1', round(k['K1_fwd']['us'],1), 'K2', round(k['K2_dx']['us'],1), d['parity']['pass'])"

@@ -34,6 +34,8 @@ buf = (ctypes.c_ulonglong * (4 * 4096))()
 for it in range(3):
     if mode == "dx":
         L.lora_linear_bwd(x, w0, a, b, dy, 16.0, want_da=False, want_db=False)
+    elif mode == "dxdrop":
+        L.lora_linear_bwd(x, w0, a, b, dy, 16.0, want_da=False, want_db=False, dropout=(0.05, 1, 2))
     else:
         L.lora_linear_fwd(x, w0, a, b, 16.0)
     torch.cuda.synchronize()
@@ -50,5 +52,7 @@ for it in range(3):
         ends[r[0]] = max(ends.get(r[0], 0), r[6])
     print(f"{mode} LORA_STREAMK={os.environ.get('LORA_STREAMK', '1')}: units {len(rows)} "
           f"max end {max(ends.values()):.1f} us, min end {min(ends.values()):.1f} us")
-    for r in rows:
+    epi = [r[6] - r[5] for r in rows]
+    print(f"epilogue (end - mma_done) us: median {np.median(epi):.2f} max {max(epi):.2f}")
+    for r in rows[:40]:
         print("pair %3d unit %d role %d kb %3d-%3d mma_done %7.1f end %7.1f" % r)
