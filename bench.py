@@ -1116,7 +1116,11 @@ def run_ours(args, wl):
                              # in the graph-replayed step K3 starts in K2's last wave: what it adds
                              # to the step is the median step minus the K1 and K2 times (one group)
                              "exposed_in_step_us": ((float(np.median(step_ms)) * 1e3 - (fwd_avg_s + k2_avg_s) * 1e6)
-                                                    if len(wl.groups) <= 1 and world == 1 else None)},
+                                                    if len(wl.groups) <= 1 and world == 1 else None),
+                             "note": "event pair around the K3 launch, incl. its launch, setup and teardown; its "
+                                     "token split is the step's (S = 1 at cfg2: 96 one-CTA jobs sized to start "
+                                     "on the SMs K2's last wave frees), so the figure is not K3's standalone rate; "
+                                     "per-phase probe in DESIGN.md 'K3 timings reconciled'"},
                 "what": "first group's kernels, CUDA events on the launching stream inside K eager steps "
                         "(L2 flushed); K2/K3 via lora_profile_next_bwd, so K3 runs after K2 instead of in "
                         "its last wave"},

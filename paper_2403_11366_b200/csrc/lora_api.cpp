@@ -491,6 +491,7 @@ lora_status launch_collected_k3(GemmCollector& col, cudaStream_t stream, int* la
     }
     static thread_local GradGroup G;
     bool done[kMaxGroup] = {};
+    prof_record(2, stream);
     for (int i = 0; i < col.k3_count; ++i) {
         if (done[i]) continue;
         G.count = 0;
@@ -502,6 +503,7 @@ lora_status launch_collected_k3(GemmCollector& col, cudaStream_t stream, int* la
         cudaError_t e = launch_grad_reduce_cluster_group(G, stream, launches);
         if (e != cudaSuccess) return cuda_fail(e, "grouped grad reduce launch");
     }
+    prof_record(3, stream);
     col.k3_count = 0;
     return LORA_OK;
 }

@@ -579,7 +579,6 @@ cudaError_t launch_grad_mma(GradMmaGroup& G, int num_sms, cudaStream_t stream, b
 #ifdef LORA_PROBE_K3
     k3_probe_stamp_kernel<<<1, 1, 0, stream>>>(0);
 #endif
-    if (getenv("LORA_K3_NOCLUSTER") && G.S == 1) cfg.numAttrs = 0;   // (experiment)
     e = cudaLaunchKernelEx(&cfg, grad_mma_kernel, G);
     if (e != cudaSuccess) return e;
 #ifdef LORA_PROBE_K3
