@@ -156,3 +156,19 @@ def test_adam_validation_codes():
     assert L.lib.lora_adam_step(1, tn, ctypes.byref(hp), 1, None) == 1           # NULL grad
     ta = (L.lora_adam_tensor * 1)(L.lora_adam_tensor(16, 40, 32, 48, 64, 8))
     assert L.lib.lora_adam_step(1, ta, ctypes.byref(hp), 1, None) == 3           # misaligned master
+
+
+def test_dropout_kept_buffers_validation():
+    """lora_dropout.keep_bits / masked_x (include/lora.h): misaligned buffers are
+    rejected with LORA_ERR_ALIGN before anything runs, naming the field; the
+    struct layout matches the header (p, seed, offset, keep_bits, masked_x)."""
+    assert ctypes.sizeof(L.lora_dropout) == 40
+    assert [f[0] for f in L.lora_dropout._fields_] == ["p", "seed", "offset", "keep_bits", "masked_x"]
+    d = L.dims(128, 64, 64, 4, 16.0)
+    for kb, mx, name in ((1 << 20 | 4, None, "keep_bits"), (None, 1 << 20 | 8, "masked_x")):
+        dr = L.lora_dropout(0.1, 1, 2, kb, mx)
+        assert L.lib.lora_linear_fwd_dropout(ctypes.byref(d), ctypes.byref(dr), 16, 32, 48, 64, None, 80, None,
+                                             4096, 1 << 20, None) == 3
+        assert name in L.lib.lora_last_error().decode()
+        assert L.lib.lora_linear_bwd_dropout(ctypes.byref(d), ctypes.byref(dr), 16, 32, 48, 64, None, 96, None,
+                                             None, None, 0, 4096, 1 << 20, None) == 3
