@@ -1017,7 +1017,7 @@ def run_ours(args, wl):
         # the achievable HBM rate at each kernel's size: a plain device copy (torch copy_)
         # moving the same bytes (half read, half written), timed the same way -- MEASURED_PEAKS'
         # hbm_gbs is a 2 GiB copy; at tens of MB the launch ramp and drain cost a few us
-        cp_src = torch.empty(max(merge_bytes, grads_bytes) // 4 + 64, dtype=torch.float16, device=dev)
+        cp_src = torch.empty(max(merge_bytes, grads_bytes, adam_bytes) // 4 + 64, dtype=torch.float16, device=dev)
         cp_dst = torch.empty_like(cp_src)
 
         def copy_ref(nbytes):
@@ -1029,7 +1029,7 @@ def run_ours(args, wl):
                          "engine": "tcgen05 (B A in TMEM) + TMA load / store" if r0 % 8 == 0 and r0 <= 64
                          else "CUDA cores", "same_bytes_copy": copy_ref(merge_bytes)},
                "adam_all_adapters": {"us": t_adam * 1e6, "bytes": adam_bytes, "gbs": adam_bytes / t_adam / 1e9,
-                                     "tensors": len(ad)},
+                                     "tensors": len(ad), "same_bytes_copy": copy_ref(adam_bytes)},
                "grads_only": {"us": t_grads * 1e6, "bytes": grads_bytes, "gbs": grads_bytes / t_grads / 1e9,
                               "kernels": "lora_linear_bwd with dx = NULL (gh row projection, K3)",
                               "same_bytes_copy": copy_ref(grads_bytes)}}
