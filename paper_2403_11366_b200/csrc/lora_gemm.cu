@@ -451,6 +451,28 @@ struct UnitIter {
     }
 };
 
+// Dropout dX epilogue term of one row and 16 columns: lo[e] = sum_j bf16(q gh_j) A[j, c + e]
+// with FHFMA.BF16 (fp32 accumulate, A straight from its bf16 halves in the MN-major SW128
+// A tile `blk`, chunk ch of its 128-byte rows)
+template <int R_PAD>
+__device__ __forceinline__ void drop_term16(const uint32_t (&gq)[R_PAD], const uint8_t* blk, uint32_t ch, int r,
+                                            float (&lo)[16]) {
+#pragma unroll
+    for (int e = 0; e < 16; ++e) lo[e] = 0.0f;
+#pragma unroll
+    for (int j = 0; j < R_PAD; ++j) {
+#ifdef LORA_PROBE_DROP_NOFMA
+        break;   // timing experiment only: no q M . (gh A) term
+#endif
+        if (j >= r) break;   // (uniform) rows r..r_pad-1 of A are zero
+        const uint4 a0 = *reinterpret_cast<const uint4*>(blk + swizzled_offset(j, ch, 128));
+        const uint4 a1 = *reinterpret_cast<const uint4*>(blk + swizzled_offset(j, ch + 1, 128));
+        const uint32_t aw[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+#pragma unroll
+        for (int e = 0; e < 8; ++e) fma_bf16_pair(gq[j], aw[e], lo[2 * e], lo[2 * e + 1]);
+    }
+}
+
 // Maps per problem g (grp.maps[g]):
 //   act  x or dY [T, K]          w   W0 [m, n] (fwd CG=2: 128-row box)
 //   w2   fwd CG=2: W0 box of BN-128 rows
@@ -756,17 +778,7 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
                                              (lc / 64) * (R_PAD * 128);
                         const uint32_t ch = static_cast<uint32_t>((lc % 64) / 8);
                         float lo[16];
-#pragma unroll
-                        for (int e = 0; e < 16; ++e) lo[e] = 0.0f;
-#pragma unroll
-                        for (int j = 0; j < R_PAD; ++j) {
-                            if (j >= p.r) break;
-                            const uint4 a0 = *reinterpret_cast<const uint4*>(blk + swizzled_offset(j, ch, 128));
-                            const uint4 a1 = *reinterpret_cast<const uint4*>(blk + swizzled_offset(j, ch + 1, 128));
-                            const uint32_t aw[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-#pragma unroll
-                            for (int e = 0; e < 8; ++e) fma_bf16_pair(gq[j], aw[e], lo[2 * e], lo[2 * e + 1]);
-                        }
+                        drop_term16<R_PAD>(gq, blk, ch, p.r, lo);
                         const uint32_t keep = (kword >> ((c & 1) * 16)) & 0xFFFFu;
 #pragma unroll
                         for (int e = 0; e < 16; ++e)
@@ -1130,20 +1142,7 @@ lora_fused_gemm_kernel(const __grid_constant__ FusedGemmGroup grp) {
                         // straight from its bf16 half -- no widening instructions) with the operand
                         // gq_j = bf16(q gh_j), the same rounding of gh as the plain path's tail MMA
                         float lo[16];
-#pragma unroll
-                        for (int e = 0; e < 16; ++e) lo[e] = 0.0f;
-#pragma unroll
-                        for (int j = 0; j < R_PAD; ++j) {
-#ifdef LORA_PROBE_DROP_NOFMA
-                            break;   // timing experiment only: no q M . (gh A) term
-#endif
-                            if (j >= p.r) break;   // (uniform) rows r..r_pad-1 of A are zero
-                            const uint4 a0 = *reinterpret_cast<const uint4*>(blk + swizzled_offset(j, ch, 128));
-                            const uint4 a1 = *reinterpret_cast<const uint4*>(blk + swizzled_offset(j, ch + 1, 128));
-                            const uint32_t aw[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-#pragma unroll
-                            for (int e = 0; e < 8; ++e) fma_bf16_pair(gq[j], aw[e], lo[2 * e], lo[2 * e + 1]);
-                        }
+                        drop_term16<R_PAD>(gq, blk, ch, p.r, lo);
                         const float qs = 1.0f;   // (q is inside gq)
 #else
                         // packed FFMA2 (two fp32 FMAs per instruction, same order and rounding)
