@@ -4,10 +4,13 @@
 //   h   = q (M . x) A^T                     (K0, replaces K1's in-MMA h)
 //   dX  = G W0 + q M . (gh A)               (K2 dropout mode, lora_gemm.cu)
 //   dA  = q gh^T (M . x)                    (K3 on xm = M . x)
-// K0 here, for a group of linears sharing x (each its own mask): the forward's
-// h of every member (tensor cores, one launch), and the backward's xm = M . x in
-// bf16 (exact: zeroing only) plus the packed keep bits the dX epilogue reads (one
-// streaming launch); keep bits drawn from Philox (lora_philox.cuh).
+// K0 here, for a group of linears sharing x (each its own mask), x read once:
+// the forward's h of every member (masked products on mma.sync, one launch) --
+// which also writes M . x and the packed keep bits when the caller keeps them
+// (lora_dropout.masked_x / keep_bits) -- and, for a backward without them, the
+// masked input xm = M . x in bf16 (exact: zeroing only) plus the keep bits the dX
+// epilogue reads (one streaming launch).  Keep bits drawn from Philox with the
+// round keys prepared on the host (lora_philox.cuh).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 

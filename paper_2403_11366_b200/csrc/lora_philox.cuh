@@ -1,13 +1,15 @@
 // lora_philox.cuh -- LoRA-dropout keep mask on the device (Listing 3
 // LORA_DROPOUT; reading R7).
 //
-// Counter-based, so the backward regenerates the forward's mask instead of
+// Counter-based, so the backward can regenerate the forward's mask instead of
 // storing it:  for element (t, k) of a [T, n] adapter input,
 //   (w0, w1, w2, w3) = Philox4x32-10(counter = (k / 8, t, offset_lo, offset_hi),
 //                                    key     = (seed_lo, seed_hi))
 //   u(t, k)          = (w_{(k mod 8) / 2} >> 16 (k mod 2)) & 0xFFFF
 //   keep(t, k)       = u(t, k) >= thr,   thr = floor(p * 2^16).
 // One Philox block gives the keep bits of 8 consecutive columns (R7).
+// Also here: the K0 helpers shared with the forward/backward dropout kernels
+// (masking of a 16-byte group of x, keep-bit packing, mma.sync m16n8k16).
 #pragma once
 #include <cstdint>
 
