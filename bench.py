@@ -301,7 +301,8 @@ class StepRunner:
             wb = int(L.lib.lora_tp_linear_bwd_workspace_bytes(ctypes.byref(dd)))
             if dropout > 0.0:
                 wf = max(wf, int(L.lib.lora_linear_fwd_dropout_workspace_bytes(ctypes.byref(dd))))
-                wb = max(wb, int(L.lib.lora_linear_bwd_dropout_workspace_bytes(ctypes.byref(dd))))
+                wb = max(wb, int(L.lib.lora_linear_bwd_dropout_workspace_bytes(ctypes.byref(dd))),
+                         int(L.lib.lora_tp_linear_bwd_dropout_workspace_bytes(ctypes.byref(dd))))
             e["ws_f"] = torch.empty(max(256, wf), dtype=torch.uint8, device=dev)
             e["ws_b"] = torch.empty(max(256, wb), dtype=torch.uint8, device=dev)
             # one Philox stream per linear; keep_mask "kept": the forward stores the keep bits
@@ -348,8 +349,8 @@ class StepRunner:
 
         self.use_groups = comm is None and group
         self.dropout = dropout
-        if dropout > 0.0 and comm is not None:
-            raise SystemExit("--dropout is single-GPU only (the TP entry points have no dropout variant)")
+        # (--dropout under TP: per-linear lora_tp_linear_{fwd,bwd}_dropout, the grouped TP
+        # column-group path has no dropout variant)
         self.groups = []
         if self.use_groups:
             for gidx in wl.groups:
@@ -530,7 +531,7 @@ class StepRunner:
                                   workspace=e["ws_f"], stream=cur, dropout=e["drop"])
             else:
                 tp.tp_linear_fwd(comm, e["spec"], e["x"], e["w0"], e["a"], e["b"], e["l"].alpha, y=e["y"],
-                                 h_out=e["h"], workspace=e["ws_f"], stream=cur)
+                                 h_out=e["h"], workspace=e["ws_f"], stream=cur, dropout=e["drop"])
             self.launches += L.lora_last_launch_count()
             if ev is not None and e is lin[0]:
                 ev["f1"].record(cur)
@@ -544,7 +545,7 @@ class StepRunner:
             else:
                 tp.tp_linear_bwd(comm, e["spec"], e["x"], e["w0"], e["a"], e["b"], e["dy"], e["l"].alpha,
                                  h_saved=e["h"], dx=e["dx"], da=e["da"], db=e["db"], workspace=e["ws_b"],
-                                 reduce_lora_grads=False, stream=cur)
+                                 reduce_lora_grads=False, stream=cur, dropout=e["drop"])
             self.launches += L.lora_last_launch_count()
         if comm is not None:
             comm.allreduce(self.grad_bucket[self.k], stream=cur)   # every partial LoRA gradient of the step

@@ -169,6 +169,9 @@ lora_status lora_adam_step(int count, const lora_adam_tensor* tensors, const lor
  * it for dA instead of masking x again (2 T n bytes per linear, what a framework
  * saves for the adapter's backward anyway).  With both buffers and h_saved the
  * backward draws and masks nothing.  Both are untouched when p = 0.
+ * A shard or token slice of a larger input (TP row mode shards x on d_in) passes
+ * its position (row_offset, col_offset) so every shard draws its part of the one
+ * mask of the full input; keep_bits / masked_x then have the local shape.
  * Use a fresh offset (or seed) per step and per linear.  p = 0 gives exactly
  * the plain calls.  p must be in [0, 1) (LORA_ERR_INVALID otherwise). */
 typedef struct {
@@ -177,6 +180,9 @@ typedef struct {
     uint64_t offset;  /* Philox counter high words: a stream per (step, linear) */
     uint32_t* keep_bits;  /* optional: [tokens, ceil(d_in/32)] keep mask, fwd writes / bwd reads */
     void* masked_x;       /* optional: [tokens, d_in] bf16 M . x, fwd writes / bwd reads */
+    int64_t row_offset;   /* where this call's x sits in the full adapter input: element (t, k) */
+    int64_t col_offset;   /*   draws the mask of (t + row_offset, k + col_offset); >= 0,
+                             col_offset % 8 == 0 (tensor-parallel shards, token slices; 0 = whole) */
 } lora_dropout;
 
 /* As lora_linear_fwd, plus one launch (K0: h from the masked input). */
@@ -309,6 +315,25 @@ lora_status lora_tp_linear_bwd(lora_comm* comm, lora_tp_mode mode, const lora_di
                                const float* h_saved, const void* dy, void* dx,
                                float* da, float* db, int accumulate, int reduce_lora_grads,
                                void* workspace, size_t workspace_bytes, void* stream);
+
+/* Tensor-parallel calls with LoRA dropout (Listing 3; R7).
+ * `dropout` describes the FULL adapter input's mask (p, seed, offset, row/col
+ * offsets of the full input, usually 0); ROW mode adds rank * local->d_in to its
+ * col_offset (x is sharded on d_in), so the shards' masks are the slices of one
+ * mask and the all-reduced result equals the unsharded dropout call.  keep_bits /
+ * masked_x, if given, are LOCAL buffers ([T, ceil(local d_in / 32)], [T, local
+ * d_in]).  Otherwise as lora_tp_linear_fwd / lora_tp_linear_bwd (workspaces: the
+ * *_dropout_workspace_bytes of the local dims, plus the bwd scratch). */
+size_t lora_tp_linear_bwd_dropout_workspace_bytes(const lora_dims* local);
+lora_status lora_tp_linear_fwd_dropout(lora_comm* comm, lora_tp_mode mode, const lora_dims* local,
+                                       const lora_dropout* dropout, const void* x, const void* w0, const void* a,
+                                       const void* b, const void* bias, void* y, float* h_out,
+                                       void* workspace, size_t workspace_bytes, void* stream);
+lora_status lora_tp_linear_bwd_dropout(lora_comm* comm, lora_tp_mode mode, const lora_dims* local,
+                                       const lora_dropout* dropout, const void* x, const void* w0, const void* a,
+                                       const void* b, const float* h_saved, const void* dy, void* dx,
+                                       float* da, float* db, int accumulate, int reduce_lora_grads,
+                                       void* workspace, size_t workspace_bytes, void* stream);
 
 /* Tensor-parallel backward of a COLUMN-parallel group of linears that read the
  * SAME input x (q, k, v or gate, up): the grouped local backward

@@ -68,7 +68,8 @@ LORA_ADAM_MAX_TENSORS = 64
 
 class lora_dropout(ctypes.Structure):
     _fields_ = [("p", ctypes.c_float), ("seed", ctypes.c_uint64), ("offset", ctypes.c_uint64),
-                ("keep_bits", ctypes.c_void_p), ("masked_x", ctypes.c_void_p)]
+                ("keep_bits", ctypes.c_void_p), ("masked_x", ctypes.c_void_p),
+                ("row_offset", ctypes.c_int64), ("col_offset", ctypes.c_int64)]
 
 
 LORA_MAX_GROUP = 8
@@ -149,6 +150,14 @@ lib.lora_tp_linear_bwd_workspace_bytes.restype = ctypes.c_size_t
 lib.lora_tp_linear_bwd.argtypes = [_vp, ctypes.c_int, _dp, _vp, _vp, _vp, _vp, _fp, _vp, _vp, _fp, _fp,
                                    ctypes.c_int, ctypes.c_int, _vp, ctypes.c_size_t, _vp]
 lib.lora_tp_linear_bwd.restype = _st
+lib.lora_tp_linear_fwd_dropout.argtypes = [_vp, ctypes.c_int, _dp, _drp, _vp, _vp, _vp, _vp, _vp, _vp, _fp, _vp,
+                                           ctypes.c_size_t, _vp]
+lib.lora_tp_linear_fwd_dropout.restype = _st
+lib.lora_tp_linear_bwd_dropout_workspace_bytes.argtypes = [_dp]
+lib.lora_tp_linear_bwd_dropout_workspace_bytes.restype = ctypes.c_size_t
+lib.lora_tp_linear_bwd_dropout.argtypes = [_vp, ctypes.c_int, _dp, _drp, _vp, _vp, _vp, _vp, _fp, _vp, _vp, _fp,
+                                           _fp, ctypes.c_int, ctypes.c_int, _vp, ctypes.c_size_t, _vp]
+lib.lora_tp_linear_bwd_dropout.restype = _st
 lib.lora_tp_linear_bwd_column_group_workspace_bytes.argtypes = [ctypes.c_int, _dp]
 lib.lora_tp_linear_bwd_column_group_workspace_bytes.restype = ctypes.c_size_t
 lib.lora_tp_linear_bwd_column_group.argtypes = [_vp, ctypes.c_int, _dp, ctypes.POINTER(lora_bwd_problem), _vp,
@@ -313,19 +322,24 @@ def lora_device_check() -> None:
 
 
 def _dropout(dropout):
-    """(p, seed, offset[, keep_bits[, masked_x]]) -> lora_dropout (LoRA dropout,
-    PAPER.md:82; include/lora.h).  keep_bits: optional int32 device tensor
-    [T, ceil(n/32)], masked_x: optional bf16 device tensor [T, n]; the forward
-    fills them (keep mask, M . x) and the backward reads them instead of redrawing."""
+    """(p, seed, offset[, keep_bits[, masked_x[, row_offset[, col_offset]]]]) -> lora_dropout
+    (LoRA dropout; include/lora.h).  keep_bits: optional int32 device
+    tensor [T, ceil(n/32)], masked_x: optional bf16 device tensor [T, n]; the forward
+    fills them (keep mask, M . x) and the backward reads them instead of redrawing.
+    row_offset / col_offset: this input's position in the full adapter input (its
+    element (t, k) draws the mask of (t + row_offset, k + col_offset))."""
     p, seed, offset = dropout[:3]
     kb = dropout[3] if len(dropout) > 3 else None
     mx = dropout[4] if len(dropout) > 4 else None
+    r0 = int(dropout[5]) if len(dropout) > 5 else 0
+    c0 = int(dropout[6]) if len(dropout) > 6 else 0
     if kb is not None and (kb.dtype != torch.int32 or not kb.is_contiguous() or not kb.is_cuda):
         raise ValueError("keep_bits must be a contiguous int32 CUDA tensor [T, ceil(n/32)]")
     if mx is not None and (mx.dtype != torch.bfloat16 or not mx.is_contiguous() or not mx.is_cuda):
         raise ValueError("masked_x must be a contiguous bf16 CUDA tensor [T, n]")
     return lora_dropout(float(p), int(seed) & (2**64 - 1), int(offset) & (2**64 - 1),
-                        kb.data_ptr() if kb is not None else None, mx.data_ptr() if mx is not None else None)
+                        kb.data_ptr() if kb is not None else None, mx.data_ptr() if mx is not None else None,
+                        r0, c0)
 
 
 def dropout_keep_bits(T, n, device="cuda"):

@@ -854,6 +854,12 @@ lora_status dropout_params(const lora_dropout* dr, DropoutParams* out) {
     out->q = 1.0f / (1.0f - dr->p);
     out->keep_bits = dr->keep_bits;
     out->masked_x = static_cast<__nv_bfloat16*>(dr->masked_x);
+    if (dr->row_offset < 0 || dr->col_offset < 0 || dr->col_offset % 8 != 0 || dr->row_offset > 0xFFFFFFFFll ||
+        dr->col_offset > 0x7FFFFFFF8ll)
+        return fail(LORA_ERR_INVALID, "dropout row_offset = %lld / col_offset = %lld: need >= 0 and col_offset %% 8 == 0",
+                    static_cast<long long>(dr->row_offset), static_cast<long long>(dr->col_offset));
+    out->row0 = dr->row_offset;
+    out->col0 = dr->col_offset;
     if (dr->keep_bits && !aligned16(dr->keep_bits))
         return fail(LORA_ERR_ALIGN, "dropout keep_bits = %p is not 16-byte aligned", static_cast<void*>(dr->keep_bits));
     if (dr->masked_x && !aligned16(dr->masked_x))

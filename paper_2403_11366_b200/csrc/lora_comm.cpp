@@ -183,18 +183,30 @@ size_t lora_tp_linear_bwd_workspace_bytes(const lora_dims* local) {
     return base + align256(scratch);
 }
 
-lora_status lora_tp_linear_fwd(lora_comm* c, lora_tp_mode mode, const lora_dims* local, const void* x,
-                               const void* w0, const void* a, const void* b, const void* bias, void* y,
-                               float* h_out, void* workspace, size_t workspace_bytes, void* stream) {
+// drop: LoRA dropout of the FULL input (null: none); row mode shifts its column
+// offset to this rank's shard, the token slices shift its row offset and the
+// kept-mask pointers
+static lora_status tp_fwd(lora_comm* c, lora_tp_mode mode, const lora_dims* local, const void* x,
+                          const void* w0, const void* a, const void* b, const void* bias, void* y,
+                          float* h_out, void* workspace, size_t workspace_bytes, void* stream,
+                          const lora_sm100::DropoutParams* drop0) {
     int launches = 0;
     if (!c) return fail(LORA_ERR_INVALID, "lora_tp_linear_fwd: comm is NULL");
     if (mode != LORA_TP_COLUMN && mode != LORA_TP_ROW) return fail(LORA_ERR_INVALID, "bad TP mode");
+    lora_sm100::DropoutParams dshard;
+    const lora_sm100::DropoutParams* drop = nullptr;
+    if (drop0) {
+        dshard = *drop0;
+        if (mode == LORA_TP_ROW) dshard.col0 += static_cast<int64_t>(c->rank) * local->d_in;
+        drop = &dshard;
+    }
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     // row mode: the (unsharded) bias is added once, by rank 0
     const void* b0 = (mode == LORA_TP_ROW && c->rank != 0) ? nullptr : bias;
     const int chunks = mode == LORA_TP_ROW ? tp_fwd_chunks(local->tokens, c->nranks) : 1;
     if (chunks <= 1 || !c->side) {
-        lora_status s = fwd_impl(local, x, w0, a, b, b0, y, h_out, workspace, workspace_bytes, st, &launches);
+        lora_status s = fwd_impl(local, x, w0, a, b, b0, y, h_out, workspace, workspace_bytes, st, &launches, nullptr,
+                                 drop);
         set_launches(launches);
         if (s != LORA_OK || mode == LORA_TP_COLUMN) return s;
         return allreduce_impl(c, y, size_t(local->tokens) * local->d_out, LORA_DT_BF16, st);
@@ -206,7 +218,7 @@ lora_status lora_tp_linear_fwd(lora_comm* c, lora_tp_mode mode, const lora_dims*
     // i + 1 runs on `stream`.  Every rank enqueues the same collectives in the
     // same order; the caller's stream joins the side stream at the end.
     lora_status s = fwd_impl(local, x, w0, a, b, b0, y, h_out, workspace, workspace_bytes, st, &launches, nullptr,
-                             nullptr, true);   // validate the whole problem first
+                             drop, true);   // validate the whole problem first
     if (s != LORA_OK) return s;
     const int64_t T = local->tokens, n = local->d_in, m = local->d_out;
     const int r = local->rank;
@@ -214,9 +226,16 @@ lora_status lora_tp_linear_fwd(lora_comm* c, lora_tp_mode mode, const lora_dims*
     for (int64_t t0 = 0; t0 < T && s == LORA_OK; t0 += tc) {
         lora_dims dc = *local;
         dc.tokens = (T - t0) < tc ? (T - t0) : tc;
+        lora_sm100::DropoutParams dslice;
+        if (drop) {   // this slice's rows of the one mask (and of the kept buffers)
+            dslice = *drop;
+            dslice.row0 += t0;
+            if (dslice.keep_bits) dslice.keep_bits += t0 * ((n + 31) / 32);
+            if (dslice.masked_x) dslice.masked_x += t0 * n;
+        }
         s = fwd_impl(&dc, static_cast<const uint8_t*>(x) + t0 * n * 2, w0, a, b, b0,
                      static_cast<uint8_t*>(y) + t0 * m * 2, h_out ? h_out + t0 * r : nullptr, workspace,
-                     workspace_bytes, st, &launches);
+                     workspace_bytes, st, &launches, nullptr, drop ? &dslice : nullptr);
         if (s != LORA_OK) break;
         cudaError_t e = cudaEventRecord(c->ev_fork, st);
         if (e == cudaSuccess) e = cudaStreamWaitEvent(c->side, c->ev_fork, 0);
@@ -230,21 +249,47 @@ lora_status lora_tp_linear_fwd(lora_comm* c, lora_tp_mode mode, const lora_dims*
     return s;
 }
 
-lora_status lora_tp_linear_bwd(lora_comm* c, lora_tp_mode mode, const lora_dims* local, const void* x,
-                               const void* w0, const void* a, const void* b, const float* h_saved,
-                               const void* dy, void* dx, float* da, float* db, int accumulate,
-                               int reduce_lora_grads, void* workspace, size_t workspace_bytes, void* stream) {
+lora_status lora_tp_linear_fwd(lora_comm* c, lora_tp_mode mode, const lora_dims* local, const void* x,
+                               const void* w0, const void* a, const void* b, const void* bias, void* y,
+                               float* h_out, void* workspace, size_t workspace_bytes, void* stream) {
+    return tp_fwd(c, mode, local, x, w0, a, b, bias, y, h_out, workspace, workspace_bytes, stream, nullptr);
+}
+
+lora_status lora_tp_linear_fwd_dropout(lora_comm* c, lora_tp_mode mode, const lora_dims* local,
+                                       const lora_dropout* dropout, const void* x, const void* w0, const void* a,
+                                       const void* b, const void* bias, void* y, float* h_out, void* workspace,
+                                       size_t workspace_bytes, void* stream) {
+    lora_sm100::DropoutParams dp;
+    lora_status st = dropout_params(dropout, &dp);
+    if (st != LORA_OK) return st;
+    return tp_fwd(c, mode, local, x, w0, a, b, bias, y, h_out, workspace, workspace_bytes, stream,
+                  dp.thr > 0 ? &dp : nullptr);
+}
+
+static lora_status tp_bwd(lora_comm* c, lora_tp_mode mode, const lora_dims* local, const void* x,
+                          const void* w0, const void* a, const void* b, const float* h_saved,
+                          const void* dy, void* dx, float* da, float* db, int accumulate,
+                          int reduce_lora_grads, void* workspace, size_t workspace_bytes, void* stream,
+                          const lora_sm100::DropoutParams* drop0) {
     int launches = 0;
     ProfGuard pg;
     if (!c) return fail(LORA_ERR_INVALID, "lora_tp_linear_bwd: comm is NULL");
     if (mode != LORA_TP_COLUMN && mode != LORA_TP_ROW) return fail(LORA_ERR_INVALID, "bad TP mode");
     lora_status s = check_dims(local, true);
     if (s != LORA_OK) return s;
-    const size_t need = lora_tp_linear_bwd_workspace_bytes(local);
+    lora_sm100::DropoutParams dshard;
+    const lora_sm100::DropoutParams* drop = nullptr;
+    if (drop0) {   // row mode: this rank's columns of the one mask
+        dshard = *drop0;
+        if (mode == LORA_TP_ROW) dshard.col0 += static_cast<int64_t>(c->rank) * local->d_in;
+        drop = &dshard;
+    }
+    const size_t need = drop0 ? lora_tp_linear_bwd_dropout_workspace_bytes(local)
+                              : lora_tp_linear_bwd_workspace_bytes(local);
     if (!workspace || workspace_bytes < need)
         return fail(LORA_ERR_WORKSPACE, "lora_tp_linear_bwd: workspace %zu < required %zu", workspace_bytes, need);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const size_t base = bwd_workspace(local);
+    const size_t base = drop0 ? bwd_workspace_dropout(local) : bwd_workspace(local);
     float* scratch = reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) + base);
     // the gradient that is a partial sum on this rank
     float* partial_grad = (mode == LORA_TP_COLUMN) ? da : db;
@@ -261,7 +306,8 @@ lora_status lora_tp_linear_bwd(lora_comm* c, lora_tp_mode mode, const lora_dims*
     int acc = accumulate ? lora_sm100::kAccA | lora_sm100::kAccB : 0;
     if (via_scratch) acc = (mode == LORA_TP_COLUMN) ? lora_sm100::kAccB : lora_sm100::kAccA;
     // bwd_impl sees a workspace that excludes the scratch tail
-    s = bwd_impl(local, x, w0, a, b, h_saved, dy, dx, da_out, db_out, acc, workspace, base, st, &launches);
+    s = bwd_impl(local, x, w0, a, b, h_saved, dy, dx, da_out, db_out, acc, workspace, base, st, &launches, nullptr, 3,
+                 drop);
     if (s != LORA_OK) {
         set_launches(launches);
         return s;
@@ -282,6 +328,33 @@ lora_status lora_tp_linear_bwd(lora_comm* c, lora_tp_mode mode, const lora_dims*
     }
     set_launches(launches);
     return LORA_OK;
+}
+
+lora_status lora_tp_linear_bwd(lora_comm* c, lora_tp_mode mode, const lora_dims* local, const void* x,
+                               const void* w0, const void* a, const void* b, const float* h_saved,
+                               const void* dy, void* dx, float* da, float* db, int accumulate,
+                               int reduce_lora_grads, void* workspace, size_t workspace_bytes, void* stream) {
+    return tp_bwd(c, mode, local, x, w0, a, b, h_saved, dy, dx, da, db, accumulate, reduce_lora_grads, workspace,
+                  workspace_bytes, stream, nullptr);
+}
+
+size_t lora_tp_linear_bwd_dropout_workspace_bytes(const lora_dims* local) {
+    const size_t base = bwd_workspace_dropout(local);
+    if (!base) return 0;
+    const size_t scratch = size_t(local->rank) * (local->d_in > local->d_out ? local->d_in : local->d_out) * 4;
+    return base + align256(scratch);
+}
+
+lora_status lora_tp_linear_bwd_dropout(lora_comm* c, lora_tp_mode mode, const lora_dims* local,
+                                       const lora_dropout* dropout, const void* x, const void* w0, const void* a,
+                                       const void* b, const float* h_saved, const void* dy, void* dx, float* da,
+                                       float* db, int accumulate, int reduce_lora_grads, void* workspace,
+                                       size_t workspace_bytes, void* stream) {
+    lora_sm100::DropoutParams dp;
+    lora_status st = dropout_params(dropout, &dp);
+    if (st != LORA_OK) return st;
+    return tp_bwd(c, mode, local, x, w0, a, b, h_saved, dy, dx, da, db, accumulate, reduce_lora_grads, workspace,
+                  workspace_bytes, stream, dp.thr > 0 ? &dp : nullptr);
 }
 
 size_t lora_tp_linear_bwd_column_group_workspace_bytes(int count, const lora_dims* local) {

@@ -206,6 +206,8 @@ static PhiloxKeys philox_keys(const DropoutParams& d) {
     K.c2 = static_cast<uint32_t>(d.offset);
     K.c3 = static_cast<uint32_t>(d.offset >> 32);
     K.thr2 = d.thr | (d.thr << 16);
+    K.k8_base = static_cast<uint32_t>(d.col0 / 8);
+    K.t_base = static_cast<uint32_t>(d.row0);
     return K;
 }
 

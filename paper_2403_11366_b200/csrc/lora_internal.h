@@ -70,6 +70,8 @@ lora_status bwd_impl(const lora_dims* d, const void* x, const void* w0, const vo
                      GemmCollector* col = nullptr, int stages = 3,
                      const lora_sm100::DropoutParams* drop = nullptr);
 size_t fwd_workspace_dropout(const lora_dims* d);
+// lora_dropout -> kernel parameters (validates p, alignment of the kept buffers, offsets)
+lora_status dropout_params(const lora_dropout* dr, lora_sm100::DropoutParams* out);
 size_t bwd_workspace_dropout(const lora_dims* d);
 // launch the collected problems, one grouped launch per (r_pad, CTA group) class
 lora_status launch_collected(int mode, GemmCollector& col, cudaStream_t stream, int* launches);

@@ -22,6 +22,7 @@ struct DropoutParams {
     float q;         // 1 / (1 - p)
     uint32_t* keep_bits;   // caller's keep-mask buffer (lora_dropout.keep_bits) or null
     __nv_bfloat16* masked_x;   // caller's M . x buffer (lora_dropout.masked_x) or null
+    int64_t row0, col0;    // position of this call's input in the full one (col0 % 8 == 0)
 };
 
 // Philox4x32-10 of one member, prepared on the host (launch_dropout_input_group):
@@ -31,6 +32,7 @@ struct PhiloxKeys {
     uint32_t k0[10], k1[10];
     uint32_t c2, c3;
     uint32_t thr2;
+    uint32_t k8_base, t_base;   // counter words c0 = k / 8 + k8_base, c1 = t + t_base (col0 / 8, row0)
 };
 
 struct FusedGemmParams {

@@ -40,7 +40,7 @@ __device__ __forceinline__ void philox4x32_10(uint32_t c0, uint32_t c1, uint32_t
 // Philox block gives eight 16-bit draws, draw i = half (i % 2) of word i / 2
 __device__ __forceinline__ uint32_t dropout_keep8(const DropoutParams& d, int64_t t, int64_t k8) {
     uint32_t w[4];
-    philox4x32_10(static_cast<uint32_t>(k8), static_cast<uint32_t>(t), static_cast<uint32_t>(d.offset),
+    philox4x32_10(static_cast<uint32_t>(k8 + d.col0 / 8), static_cast<uint32_t>(t + d.row0), static_cast<uint32_t>(d.offset),
                   static_cast<uint32_t>(d.offset >> 32), static_cast<uint32_t>(d.seed),
                   static_cast<uint32_t>(d.seed >> 32), w);
     uint32_t keep = 0;
@@ -84,7 +84,7 @@ __device__ __forceinline__ uint32_t keep_mask_word(uint32_t w, uint32_t thr2) {
 // one Philox block (counter (k8, t)) gives the 16-bit draws of the 8 elements.
 __device__ __forceinline__ uint4 masked8(const uint4& u, const PhiloxKeys& K, uint32_t k8, uint32_t t,
                                          uint32_t (&w)[4]) {
-    philox4x32_10_keys(k8, t, K, w);
+    philox4x32_10_keys(k8 + K.k8_base, t + K.t_base, K, w);
 #pragma unroll
     for (int i = 0; i < 4; ++i) w[i] = keep_mask_word(w[i], K.thr2);
     return make_uint4(u.x & w[0], u.y & w[1], u.z & w[2], u.w & w[3]);

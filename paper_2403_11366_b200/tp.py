@@ -135,11 +135,13 @@ class LoraComm:
 
 
 def tp_linear_fwd(comm: LoraComm, spec: ShardSpec, x, w0, a, b, alpha, bias=None, y=None, h_out=None,
-                  workspace=None, stream=None):
-    """lora_tp_linear_fwd on local shards.  Returns (y [T, local_m], h [T, r])."""
+                  workspace=None, stream=None, dropout=None):
+    """lora_tp_linear_fwd on local shards.  Returns (y [T, local_m], h [T, r]).
+    dropout: (p, seed, offset[, keep_bits[, masked_x]]) of the FULL input (keep_bits /
+    masked_x local) -> lora_tp_linear_fwd_dropout (row mode draws its shard's columns)."""
     import torch
 
-    from . import _bf16, _check, _ptr, _stream, _workspace, dims, lib, lora_linear_fwd_workspace_bytes
+    from . import _bf16, _check, _dropout, _ptr, _stream, _workspace, dims, lib, lora_linear_fwd_workspace_bytes
     T = x.shape[0]
     r = a.shape[0]
     n, m = spec.local_n, spec.local_m
@@ -149,6 +151,14 @@ def tp_linear_fwd(comm: LoraComm, spec: ShardSpec, x, w0, a, b, alpha, bias=None
     if h_out is None:
         h_out = torch.empty((T, r), dtype=torch.float32, device=x.device)
     d = dims(T, n, m, r, alpha)
+    if dropout is not None:
+        dr = _dropout(dropout)
+        need = int(lib.lora_linear_fwd_dropout_workspace_bytes(ctypes.byref(d)))
+        ws = workspace if workspace is not None else _workspace(need, x.device)
+        _check(lib.lora_tp_linear_fwd_dropout(comm.handle, spec.mode, ctypes.byref(d), ctypes.byref(dr), _ptr(x),
+                                              _ptr(w0), _ptr(a), _ptr(b), _ptr(bias), _ptr(y), _ptr(h_out), _ptr(ws),
+                                              ws.numel(), _stream(stream)), "lora_tp_linear_fwd_dropout")
+        return y, h_out
     ws = workspace if workspace is not None else _workspace(lora_linear_fwd_workspace_bytes(d), x.device)
     _check(lib.lora_tp_linear_fwd(comm.handle, spec.mode, ctypes.byref(d), _ptr(x), _ptr(w0), _ptr(a), _ptr(b),
                                   _ptr(bias), _ptr(y), _ptr(h_out), _ptr(ws), ws.numel(), _stream(stream)),
@@ -157,12 +167,14 @@ def tp_linear_fwd(comm: LoraComm, spec: ShardSpec, x, w0, a, b, alpha, bias=None
 
 
 def tp_linear_bwd(comm: LoraComm, spec: ShardSpec, x, w0, a, b, dy, alpha, h_saved=None, dx=None, da=None,
-                  db=None, accumulate=False, reduce_lora_grads=True, want_dx=True, workspace=None, stream=None):
+                  db=None, accumulate=False, reduce_lora_grads=True, want_dx=True, workspace=None, stream=None,
+                  dropout=None):
     """lora_tp_linear_bwd on local shards.  Returns (dx, dA, dB) local tensors
-    (dx / dA / dB already summed across ranks where they are partial)."""
+    (dx / dA / dB already summed across ranks where they are partial).  dropout:
+    as tp_linear_fwd (the same tuple as the forward) -> lora_tp_linear_bwd_dropout."""
     import torch
 
-    from . import _check, _ptr, _stream, _workspace, dims, lib
+    from . import _check, _dropout, _ptr, _stream, _workspace, dims, lib
     T = x.shape[0]
     r = a.shape[0]
     n, m = spec.local_n, spec.local_m
@@ -173,6 +185,15 @@ def tp_linear_bwd(comm: LoraComm, spec: ShardSpec, x, w0, a, b, dy, alpha, h_sav
     if db is None:
         db = torch.zeros((m, r), dtype=torch.float32, device=x.device)
     d = dims(T, n, m, r, alpha)
+    if dropout is not None:
+        dr = _dropout(dropout)
+        need = int(lib.lora_tp_linear_bwd_dropout_workspace_bytes(ctypes.byref(d)))
+        ws = workspace if workspace is not None else _workspace(need, x.device)
+        _check(lib.lora_tp_linear_bwd_dropout(comm.handle, spec.mode, ctypes.byref(d), ctypes.byref(dr), _ptr(x),
+                                              _ptr(w0), _ptr(a), _ptr(b), _ptr(h_saved), _ptr(dy), _ptr(dx), _ptr(da),
+                                              _ptr(db), 1 if accumulate else 0, 1 if reduce_lora_grads else 0,
+                                              _ptr(ws), ws.numel(), _stream(stream)), "lora_tp_linear_bwd_dropout")
+        return dx, da, db
     need = int(lib.lora_tp_linear_bwd_workspace_bytes(ctypes.byref(d)))
     ws = workspace if workspace is not None else _workspace(need, x.device)
     _check(lib.lora_tp_linear_bwd(comm.handle, spec.mode, ctypes.byref(d), _ptr(x), _ptr(w0), _ptr(a), _ptr(b),

@@ -160,10 +160,12 @@ def test_adam_validation_codes():
 
 def test_dropout_kept_buffers_validation():
     """lora_dropout.keep_bits / masked_x (include/lora.h): misaligned buffers are
-    rejected with LORA_ERR_ALIGN before anything runs, naming the field; the
-    struct layout matches the header (p, seed, offset, keep_bits, masked_x)."""
-    assert ctypes.sizeof(L.lora_dropout) == 40
-    assert [f[0] for f in L.lora_dropout._fields_] == ["p", "seed", "offset", "keep_bits", "masked_x"]
+    rejected with LORA_ERR_ALIGN before anything runs, naming the field; negative
+    offsets or a column offset that is not a multiple of 8 are LORA_ERR_INVALID;
+    the struct layout matches the header."""
+    assert ctypes.sizeof(L.lora_dropout) == 56
+    assert [f[0] for f in L.lora_dropout._fields_] == ["p", "seed", "offset", "keep_bits", "masked_x", "row_offset",
+                                                       "col_offset"]
     d = L.dims(128, 64, 64, 4, 16.0)
     for kb, mx, name in ((1 << 20 | 4, None, "keep_bits"), (None, 1 << 20 | 8, "masked_x")):
         dr = L.lora_dropout(0.1, 1, 2, kb, mx)
@@ -172,3 +174,9 @@ def test_dropout_kept_buffers_validation():
         assert name in L.lib.lora_last_error().decode()
         assert L.lib.lora_linear_bwd_dropout(ctypes.byref(d), ctypes.byref(dr), 16, 32, 48, 64, None, 96, None,
                                              None, None, 0, 4096, 1 << 20, None) == 3
+    for r0, c0 in ((-1, 0), (0, -8), (0, 4)):
+        dr = L.lora_dropout(0.1, 1, 2, None, None, r0, c0)
+        assert L.lib.lora_linear_fwd_dropout(ctypes.byref(d), ctypes.byref(dr), 16, 32, 48, 64, None, 80, None,
+                                             4096, 1 << 20, None) == 1
+        assert "offset" in L.lib.lora_last_error().decode()
+        assert L.lib.lora_dropout_mask(8, 8, ctypes.byref(dr), 16, None) == 1

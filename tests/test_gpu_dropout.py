@@ -252,3 +252,62 @@ def test_keep_bits_grouped(oracle_mod, L):
         for u, v in zip(go0[g], go1[g]):
             assert torch.equal(u, v)
         np.testing.assert_array_equal(kbs[g][0].cpu().numpy(), _pack_bits(oracle_mod.dropout_mask(T, n, *drops[g])))
+
+
+def test_mask_offsets_are_slices_of_the_full_mask(oracle_mod, L):
+    """lora_dropout row_offset / col_offset (include/lora.h): the mask of a sub-block
+    is the oracle's full mask sliced at that position, bit for bit."""
+    T, n, p, seed, off = 300, 200, 0.3, 99, 5
+    full = oracle_mod.dropout_mask(T, n, p, seed, off)
+    for r0, c0, t, k in ((0, 0, T, n), (17, 8, 100, 64), (129, 136, 171, 64), (299, 192, 1, 8)):
+        got = L.lora_dropout_mask(t, k, (p, seed, off, None, None, r0, c0)).cpu().numpy()
+        np.testing.assert_array_equal(got, full[r0:r0 + t, c0:c0 + k])
+
+
+def test_row_sharded_dropout_equals_unsharded_oracle(oracle_mod, L):
+    """The tensor-parallel ROW split with dropout, computed shard by shard on one GPU
+    (each shard's call with col_offset = its first input column):
+    summed y / h partials and concatenated dX / dA equal the UNSHARDED oracle with
+    the one mask of the full input; dB from the summed h too."""
+    T, n, m, r, alpha = 300, 256, 264, 8, 16.0
+    drop = (0.1, 321, 7)
+    d = make_lora_inputs(T, n, m, r, seed=731)
+    x, w0, a, b, dy = (dev_bf16(d[k]) for k in ("x", "w0", "a", "b", "dy"))
+    cuts = (0, 96, 256)
+    ys, hs = [], []
+    for s0, s1 in zip(cuts[:-1], cuts[1:]):
+        y, h = L.lora_linear_fwd(x[:, s0:s1].contiguous(), w0[:, s0:s1].contiguous(), a[:, s0:s1].contiguous(), b,
+                                 alpha, dropout=drop + (None, None, 0, s0))
+        ys.append(host_f64(y))
+        hs.append(host_f64(h))
+    yo, ho = oracle_mod.lora_fwd(d["x"], d["w0"], d["a"], d["b"], alpha, dropout=drop)
+    h_sum = sum(hs)
+    assert relF(h_sum, ho) <= 1e-5
+    assert relF(sum(ys), yo) <= TOL_OUT
+    go = oracle_mod.lora_bwd(d["x"], d["w0"], d["a"], d["b"], d["dy"], alpha, dropout=drop)
+    hfull = torch.from_numpy(h_sum.astype(np.float32)).cuda()
+    dxs, das = [], []
+    for s0, s1 in zip(cuts[:-1], cuts[1:]):
+        dx, da, db = L.lora_linear_bwd(x[:, s0:s1].contiguous(), w0[:, s0:s1].contiguous(),
+                                       a[:, s0:s1].contiguous(), b, dy, alpha, h_saved=hfull,
+                                       dropout=drop + (None, None, 0, s0))
+        dxs.append(host_f64(dx))
+        das.append(host_f64(da))
+        assert relF(host_f64(db), go["db"]) <= TOL_GRAD
+    assert relF(np.concatenate(dxs, axis=1), go["dx"]) <= TOL_OUT
+    assert relF(np.concatenate(das, axis=1), go["da"]) <= TOL_GRAD
+
+
+def test_token_slices_with_row_offset_are_bitwise_rows(L):
+    """A forward over tokens [t0, t1) with row_offset = t0 gives bitwise the rows
+    t0..t1 of the full call (the mask rows follow the offset; K0's per-row sums
+    and K1's K-loops do not depend on T)."""
+    T, n, m, r = 700, 256, 256, 16
+    d = make_lora_inputs(T, n, m, r, seed=741)
+    x, w0, a, b = (dev_bf16(d[k]) for k in ("x", "w0", "a", "b"))
+    drop = (0.05, 5, 6)
+    y, h = L.lora_linear_fwd(x, w0, a, b, 16.0, dropout=drop)
+    for t0, t1 in ((0, 256), (256, 512), (512, 700), (123, 457)):
+        ys, hs = L.lora_linear_fwd(x[t0:t1].contiguous(), w0, a, b, 16.0, dropout=drop + (None, None, t0, 0))
+        torch.cuda.synchronize()
+        assert torch.equal(ys, y[t0:t1]) and torch.equal(hs, h[t0:t1]), (t0, t1)

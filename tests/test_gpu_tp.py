@@ -169,3 +169,29 @@ def test_tp_row_forward_token_slices(comm, chunks, monkeypatch):
     g.replay()
     torch.cuda.synchronize()
     assert torch.equal(y1, y3) and torch.equal(h1, h3)
+
+
+@pytest.mark.parametrize("mode", ["column", "row"])
+@pytest.mark.parametrize("chunks", ["1", "3"])
+def test_tp_dropout_n1_equals_single_call(comm, mode, chunks, monkeypatch):
+    """lora_tp_linear_{fwd,bwd}_dropout at N = 1 (real NCCL communicator): bitwise
+    the single-GPU dropout calls, also with the ROW forward in token slices (each
+    slice draws its rows of the one mask; kept bits / M . x written per slice)."""
+    import paper_2403_11366_b200 as L
+    from paper_2403_11366_b200 import tp
+    T, n, m, r = 700, 256, 384, 8
+    d = make_lora_inputs(T, n, m, r, seed=67)
+    x, w0, a, b, dy = (dev_bf16(d[k]) for k in ("x", "w0", "a", "b", "dy"))
+    spec = tp.ShardSpec(tp.MODES[mode], 1, 0, n, m)
+    drop = (0.05, 11, 12)
+    kb1, kb2 = L.dropout_keep_bits(T, n), L.dropout_keep_bits(T, n)
+    mx1 = torch.empty((T, n), dtype=torch.bfloat16, device="cuda")
+    mx2 = torch.empty_like(mx1)
+    y1, h1 = L.lora_linear_fwd(x, w0, a, b, 16.0, dropout=drop + (kb1, mx1))
+    monkeypatch.setenv("LORA_TP_CHUNKS", chunks)
+    y2, h2 = tp.tp_linear_fwd(comm, spec, x, w0, a, b, 16.0, dropout=drop + (kb2, mx2))
+    dx1, da1, db1 = L.lora_linear_bwd(x, w0, a, b, dy, 16.0, h_saved=h1, dropout=drop + (kb1, mx1))
+    dx2, da2, db2 = tp.tp_linear_bwd(comm, spec, x, w0, a, b, dy, 16.0, h_saved=h2, dropout=drop + (kb2, mx2))
+    torch.cuda.synchronize()
+    for u, v in ((y1, y2), (h1, h2), (kb1, kb2), (mx1, mx2), (dx1, dx2), (da1, da2), (db1, db2)):
+        assert torch.equal(u, v)
