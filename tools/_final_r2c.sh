@@ -1,7 +1,7 @@
 #!/bin/bash
 # Round-2 closing evidence (session 3) on one B200, via gpurun from the repo root.
 set -u
-OUT=gpurun_out/r02_final2
+OUT=gpurun_out/${FINAL_OUT:-r02_final2}
 mkdir -p $OUT
 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > $OUT/smoke.log 2>&1; tail -2 $OUT/smoke.log
 timeout 1500 python -m pytest tests -m gpu -q > $OUT/gpu_tests.log 2>&1; tail -1 $OUT/gpu_tests.log
