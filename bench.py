@@ -1097,8 +1097,10 @@ def run_ours(args, wl):
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": (f"lora_linear_fwd_grouped of {[l.name for l in roof_linears]} (one fused K1 "
-                                    f"launch) inside the step, " if len(roof_linears) > 1 else
-                                    f"lora_linear_fwd of '{l0.name}' (fused K1) inside the step, ") +
+                                    f"launch{' + the dropout K0 launch before it' if args.dropout > 0 else ''}) "
+                                    f"inside the step, " if len(roof_linears) > 1 else
+                                    f"lora_linear_fwd of '{l0.name}' (fused K1"
+                                    f"{' + dropout K0' if args.dropout > 0 else ''}) inside the step, ") +
                                    f"{f_fwd / 1e9:.2f} algorithmic GFLOP per launch, avg {fwd_avg_s * 1e6:.1f} us",
                          "peak_source": peak_src + " bf16_tflops (burst)",
                          # the same kernel against the sustained figure (cuBLAS back to back for 4 s):
