@@ -349,8 +349,8 @@ class StepRunner:
 
         self.use_groups = comm is None and group
         self.dropout = dropout
-        # (--dropout under TP: per-linear lora_tp_linear_{fwd,bwd}_dropout, the grouped TP
-        # column-group path has no dropout variant)
+        # (--dropout under TP: grouped column members through lora_linear_fwd_grouped_dropout and
+        # lora_tp_linear_bwd_column_group_dropout, row linears through lora_tp_linear_{fwd,bwd}_dropout)
         self.groups = []
         if self.use_groups:
             for gidx in wl.groups:
@@ -366,15 +366,19 @@ class StepRunner:
                 wsb = torch.empty(max(256, nb), dtype=torch.uint8, device=dev)
                 self.groups.append((members, wsf, wsb))
         self.tp_groups = []
-        if comm is not None and group and dropout == 0.0:
+        if comm is not None and group:
             for gidx in (wl.groups or tuple((i,) for i in range(len(lin)))):
                 members = [lin[i] for i in gidx]
                 if len(members) > 1 and all(e["spec"].mode == tp.COLUMN for e in members):
                     ds = self._dims(members)
-                    wsf = torch.empty(max(256, int(L.lib.lora_linear_fwd_grouped_workspace_bytes(len(members), ds))),
-                                      dtype=torch.uint8, device=dev)
-                    wsb = torch.empty(max(256, int(L.lib.lora_tp_linear_bwd_column_group_workspace_bytes(
-                        len(members), ds))), dtype=torch.uint8, device=dev)
+                    if dropout > 0.0:
+                        nf = L.lib.lora_linear_fwd_grouped_dropout_workspace_bytes(len(members), ds)
+                        nb = L.lib.lora_tp_linear_bwd_column_group_dropout_workspace_bytes(len(members), ds)
+                    else:
+                        nf = L.lib.lora_linear_fwd_grouped_workspace_bytes(len(members), ds)
+                        nb = L.lib.lora_tp_linear_bwd_column_group_workspace_bytes(len(members), ds)
+                    wsf = torch.empty(max(256, int(nf)), dtype=torch.uint8, device=dev)
+                    wsb = torch.empty(max(256, int(nb)), dtype=torch.uint8, device=dev)
                     dx_sum = [torch.empty_like(members[0]["dx_sets"][0]) for _ in range(nsets)]
                     self.tp_groups.append((members, wsf, wsb, dx_sum))
                 else:
@@ -385,6 +389,8 @@ class StepRunner:
         self.symm = None
         self.comm_mode = comm_mode if comm is not None else "none"
         if self.comm_mode == "fused":
+            if dropout > 0.0:
+                raise SystemExit("--comm fused has no LoRA-dropout variant (use --comm nccl)")
             if not self.tp_groups:
                 raise SystemExit("--comm fused needs the grouped TP step (no --no-group / --dropout)")
             off, regions = 0, []
@@ -475,9 +481,11 @@ class StepRunner:
             if ev is not None and gi == 0:
                 ev["f0"].record(cur)
             if wsf is not None:
+                drops = [e["drop"] for e in members] if self.dropout > 0.0 else None
                 L.lora_linear_fwd_grouped([(e["x"], e["w0"], e["a"], e["b"], None) for e in members],
                                           [e["l"].alpha for e in members],
-                                          outs=[(e["y"], e["h"]) for e in members], workspace=wsf, stream=cur)
+                                          outs=[(e["y"], e["h"]) for e in members], workspace=wsf, stream=cur,
+                                          dropouts=drops)
                 self.launches += L.lora_last_launch_count()
             else:
                 for e in members:
@@ -488,7 +496,8 @@ class StepRunner:
                                                stream=cur)
                     else:
                         tp.tp_linear_fwd(comm, e["spec"], e["x"], e["w0"], e["a"], e["b"], e["l"].alpha,
-                                         y=e["y"], h_out=e["h"], workspace=e["ws_f"], stream=cur)
+                                         y=e["y"], h_out=e["h"], workspace=e["ws_f"], stream=cur,
+                                         dropout=e["drop"])
                     self.launches += L.lora_last_launch_count()
             if ev is not None and gi == 0:
                 ev["f1"].record(cur)
@@ -509,13 +518,14 @@ class StepRunner:
                                               [(e["x"], e["w0"], e["a"], e["b"], e["dy"], e["h"]) for e in members],
                                               [e["l"].alpha for e in members], dx_sum=dx_sum[self.k],
                                               outs=[(e["dx"], e["da"], e["db"]) for e in members], workspace=wsb,
-                                              reduce_lora_grads=False, stream=cur)
+                                              reduce_lora_grads=False, stream=cur,
+                                              dropouts=[e["drop"] for e in members] if self.dropout > 0.0 else None)
                 self.launches += L.lora_last_launch_count()
             else:
                 for e in members:
                     tp.tp_linear_bwd(comm, e["spec"], e["x"], e["w0"], e["a"], e["b"], e["dy"], e["l"].alpha,
                                      h_saved=e["h"], dx=e["dx"], da=e["da"], db=e["db"], workspace=e["ws_b"],
-                                     reduce_lora_grads=False, stream=cur)
+                                     reduce_lora_grads=False, stream=cur, dropout=e["drop"])
                     self.launches += L.lora_last_launch_count()
         comm.allreduce(self.grad_bucket[self.k], stream=cur)   # every partial LoRA gradient of the step
 

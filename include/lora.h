@@ -351,6 +351,16 @@ lora_status lora_tp_linear_bwd_column_group(lora_comm* comm, int count, const lo
                                             int reduce_lora_grads, void* workspace, size_t workspace_bytes,
                                             void* stream);
 
+/* The column-group backward with LoRA dropout: one lora_dropout per problem (each
+ * member's own mask of the replicated input; p > 0 for all or none), the same
+ * forward masks (lora_linear_fwd_grouped_dropout or the TP calls).  Workspace:
+ * lora_tp_linear_bwd_column_group_dropout_workspace_bytes. */
+size_t lora_tp_linear_bwd_column_group_dropout_workspace_bytes(int count, const lora_dims* local);
+lora_status lora_tp_linear_bwd_column_group_dropout(lora_comm* comm, int count, const lora_dims* local,
+                                                    const lora_dropout* dropouts, const lora_bwd_problem* problems,
+                                                    void* dx_sum, int accumulate, int reduce_lora_grads,
+                                                    void* workspace, size_t workspace_bytes, void* stream);
+
 /* ---------------- Comm-fused epilogues over peer memory ----
  * PAPER.md:199 blames the multi-GPU slowdown on "cross-GPU communication
  * overhead"; these calls fuse the two activation all-reduces of the TP linear

@@ -150,6 +150,12 @@ lib.lora_tp_linear_bwd_workspace_bytes.restype = ctypes.c_size_t
 lib.lora_tp_linear_bwd.argtypes = [_vp, ctypes.c_int, _dp, _vp, _vp, _vp, _vp, _fp, _vp, _vp, _fp, _fp,
                                    ctypes.c_int, ctypes.c_int, _vp, ctypes.c_size_t, _vp]
 lib.lora_tp_linear_bwd.restype = _st
+lib.lora_tp_linear_bwd_column_group_dropout_workspace_bytes.argtypes = [ctypes.c_int, _dp]
+lib.lora_tp_linear_bwd_column_group_dropout_workspace_bytes.restype = ctypes.c_size_t
+lib.lora_tp_linear_bwd_column_group_dropout.argtypes = [_vp, ctypes.c_int, _dp, _drp,
+                                                        ctypes.POINTER(lora_bwd_problem), _vp, ctypes.c_int,
+                                                        ctypes.c_int, _vp, ctypes.c_size_t, _vp]
+lib.lora_tp_linear_bwd_column_group_dropout.restype = _st
 lib.lora_tp_linear_fwd_dropout.argtypes = [_vp, ctypes.c_int, _dp, _drp, _vp, _vp, _vp, _vp, _vp, _vp, _fp, _vp,
                                            ctypes.c_size_t, _vp]
 lib.lora_tp_linear_fwd_dropout.restype = _st

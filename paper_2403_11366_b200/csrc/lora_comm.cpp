@@ -361,10 +361,10 @@ size_t lora_tp_linear_bwd_column_group_workspace_bytes(int count, const lora_dim
     return lora_linear_bwd_grouped_workspace_bytes(count, local);
 }
 
-lora_status lora_tp_linear_bwd_column_group(lora_comm* c, int count, const lora_dims* local,
-                                            const lora_bwd_problem* problems, void* dx_sum, int accumulate,
-                                            int reduce_lora_grads, void* workspace, size_t workspace_bytes,
-                                            void* stream) {
+static lora_status tp_bwd_column_group(lora_comm* c, int count, const lora_dims* local,
+                                       const lora_bwd_problem* problems, void* dx_sum, int accumulate,
+                                       int reduce_lora_grads, void* workspace, size_t workspace_bytes,
+                                       void* stream, const lora_sm100::DropoutParams* drops) {
     ProfGuard pg;
     if (!c) return fail(LORA_ERR_INVALID, "lora_tp_linear_bwd_column_group: comm is NULL");
     if (count < 1 || count > LORA_MAX_GROUP || !local || !problems)
@@ -425,7 +425,7 @@ lora_status lora_tp_linear_bwd_column_group(lora_comm* c, int count, const lora_
         return LORA_OK;
     };
     lora_status s = bwd_grouped_impl(count, local, problems, accumulate, workspace, workspace_bytes, stream,
-                                     dx_sum_and_reduce, &fk);
+                                     dx_sum_and_reduce, &fk, nullptr, nullptr, drops);
     int launches = get_launches();
     if (fk.forked) {   // join (also on failure: never leave the side stream dangling in a capture)
         cudaError_t e = cudaStreamWaitEvent(st, c->ev_join, 0);
@@ -448,6 +448,40 @@ lora_status lora_tp_linear_bwd_column_group(lora_comm* c, int count, const lora_
     }
     set_launches(launches);
     return LORA_OK;
+}
+
+lora_status lora_tp_linear_bwd_column_group(lora_comm* c, int count, const lora_dims* local,
+                                            const lora_bwd_problem* problems, void* dx_sum, int accumulate,
+                                            int reduce_lora_grads, void* workspace, size_t workspace_bytes,
+                                            void* stream) {
+    return tp_bwd_column_group(c, count, local, problems, dx_sum, accumulate, reduce_lora_grads, workspace,
+                               workspace_bytes, stream, nullptr);
+}
+
+size_t lora_tp_linear_bwd_column_group_dropout_workspace_bytes(int count, const lora_dims* local) {
+    return lora_linear_bwd_grouped_dropout_workspace_bytes(count, local);
+}
+
+lora_status lora_tp_linear_bwd_column_group_dropout(lora_comm* c, int count, const lora_dims* local,
+                                                    const lora_dropout* dropouts, const lora_bwd_problem* problems,
+                                                    void* dx_sum, int accumulate, int reduce_lora_grads,
+                                                    void* workspace, size_t workspace_bytes, void* stream) {
+    if (count < 1 || count > LORA_MAX_GROUP || !dropouts)
+        return fail(LORA_ERR_INVALID, "lora_tp_linear_bwd_column_group_dropout: need 1..%d problems and their "
+                                      "dropouts", LORA_MAX_GROUP);
+    lora_sm100::DropoutParams dp[LORA_MAX_GROUP];
+    int dropping = 0;
+    for (int g = 0; g < count; ++g) {
+        lora_status st = dropout_params(&dropouts[g], &dp[g]);
+        if (st != LORA_OK) return st;
+        dropping += dp[g].thr > 0 ? 1 : 0;
+    }
+    if (dropping != 0 && dropping != count)
+        return fail(LORA_ERR_INVALID, "lora_tp_linear_bwd_column_group_dropout: p must be > 0 for all problems "
+                                      "or for none");
+    // (COLUMN mode: x is replicated, every rank draws the full mask -- no offset)
+    return tp_bwd_column_group(c, count, local, problems, dx_sum, accumulate, reduce_lora_grads, workspace,
+                               workspace_bytes, stream, dropping ? dp : nullptr);
 }
 
 }  // extern "C"

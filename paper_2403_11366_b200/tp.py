@@ -204,15 +204,17 @@ def tp_linear_bwd(comm: LoraComm, spec: ShardSpec, x, w0, a, b, dy, alpha, h_sav
 
 
 def tp_linear_bwd_column_group(comm: LoraComm, specs, problems, alphas, dx_sum=None, want_dx=True, outs=None,
-                               reduce_lora_grads=True, workspace=None, stream=None):
+                               reduce_lora_grads=True, workspace=None, stream=None, dropouts=None):
     """lora_tp_linear_bwd_column_group: the backward of COLUMN-parallel linears that
     read the same input (q/k/v, gate/up).  problems: list of
     (x, w0, a, b, dy, h_saved) local shards with the SAME x tensor.  The members'
     dX partials are summed into dx_sum (the gradient w.r.t. the shared input) and
-    all-reduced once.  Returns (dx_sum, [(dx_g, dA_g, dB_g)])."""
+    all-reduced once.  dropouts: one (p, seed, offset[, keep_bits[, masked_x]]) per
+    member (the forward's) -> lora_tp_linear_bwd_column_group_dropout.
+    Returns (dx_sum, [(dx_g, dA_g, dB_g)])."""
     import torch
 
-    from . import _check, _ptr, _stream, _workspace, dims, lib, lora_bwd_problem, lora_dims
+    from . import _check, _dropout, _ptr, _stream, _workspace, dims, lib, lora_bwd_problem, lora_dims, lora_dropout
     G = len(problems)
     x = problems[0][0]
     T = x.shape[0]
@@ -240,6 +242,14 @@ def tp_linear_bwd_column_group(comm: LoraComm, specs, problems, alphas, dx_sum=N
         probs[g] = lora_bwd_problem(_ptr(xg), _ptr(w0), _ptr(a), _ptr(b), _ptr(h), _ptr(dy), _ptr(dx), _ptr(da),
                                     _ptr(db))
         res.append((dx, da, db))
+    if dropouts is not None:
+        drs = (lora_dropout * G)(*[_dropout(dr) for dr in dropouts])
+        need = int(lib.lora_tp_linear_bwd_column_group_dropout_workspace_bytes(G, dims_arr))
+        ws = workspace if workspace is not None else _workspace(need, x.device)
+        _check(lib.lora_tp_linear_bwd_column_group_dropout(comm.handle, G, dims_arr, drs, probs, _ptr(dx_sum), 0,
+                                                           1 if reduce_lora_grads else 0, _ptr(ws), ws.numel(),
+                                                           _stream(stream)), "lora_tp_linear_bwd_column_group_dropout")
+        return dx_sum, res
     need = int(lib.lora_tp_linear_bwd_column_group_workspace_bytes(G, dims_arr))
     ws = workspace if workspace is not None else _workspace(need, x.device)
     _check(lib.lora_tp_linear_bwd_column_group(comm.handle, G, dims_arr, probs, _ptr(dx_sum), 0,

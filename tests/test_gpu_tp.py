@@ -195,3 +195,33 @@ def test_tp_dropout_n1_equals_single_call(comm, mode, chunks, monkeypatch):
     torch.cuda.synchronize()
     for u, v in ((y1, y2), (h1, h2), (kb1, kb2), (mx1, mx2), (dx1, dx2), (da1, da2), (db1, db2)):
         assert torch.equal(u, v)
+
+
+def test_tp_column_group_dropout(comm, oracle_mod):
+    """lora_tp_linear_bwd_column_group_dropout at N = 1: the members' dX / dA / dB
+    bitwise the grouped single-GPU dropout backward (each member its own mask, the
+    forward's h), dx_sum == the oracle's sum of the members' dropout dX."""
+    import paper_2403_11366_b200 as L
+    from paper_2403_11366_b200 import tp
+    from tests.gpu_util import TOL_OUT, host_f64, relF
+    T, n = 384, 256
+    base = make_lora_inputs(T, n, 8, 8, seed=90)
+    x = dev_bf16(base["x"])
+    specs, probs, drops, refs = [], [], [], []
+    members = [(256, 8), (128, 8)]
+    ts = []
+    for i, (m, r) in enumerate(members):
+        d = make_lora_inputs(T, n, m, r, seed=91 + i)
+        d["x"] = base["x"]
+        ts.append({k: dev_bf16(d[k]) for k in ("w0", "a", "b", "dy")})
+        drops.append((0.05, 200 + i, 3 * i))
+        specs.append(tp.ShardSpec(tp.COLUMN, 1, 0, n, m))
+        refs.append(oracle_mod.lora_bwd(d["x"], d["w0"], d["a"], d["b"], d["dy"], 16.0, dropout=drops[-1]))
+    fo = L.lora_linear_fwd_grouped([(x, t["w0"], t["a"], t["b"], None) for t in ts], [16.0] * 2, dropouts=drops)
+    probs = [(x, t["w0"], t["a"], t["b"], t["dy"], h) for t, (_, h) in zip(ts, fo)]
+    g1 = L.lora_linear_bwd_grouped(probs, [16.0] * 2, dropouts=drops)
+    dx_sum, res = tp.tp_linear_bwd_column_group(comm, specs, probs, [16.0] * 2, dropouts=drops)
+    torch.cuda.synchronize()
+    for (dx, da, db), (dx1, da1, db1) in zip(res, g1):
+        assert torch.equal(dx, dx1) and torch.equal(da, da1) and torch.equal(db, db1)
+    assert relF(host_f64(dx_sum), sum(rf["dx"] for rf in refs)) <= TOL_OUT
