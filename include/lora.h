@@ -203,8 +203,11 @@ lora_status lora_dropout_mask(int64_t tokens, int64_t d_in, const lora_dropout* 
                               void* stream);
 
 /* ---------------- Grouped calls: several independent LoRA linears ----------
- * Equivalent to `count` single calls (bitwise identical results), but the
- * fused tensor-core GEMMs of all problems whose rank falls in the same
+ * Equivalent to `count` single calls -- y, h and dX bitwise identical; dA and
+ * dB identical up to fp32 re-association (the dA/dB kernel's token split is
+ * chosen for the whole launch, so a group may sum the token partials in
+ * other chunks than a single call; repeated calls are bitwise reproducible) --
+ * but the fused tensor-core GEMMs of all problems whose rank falls in the same
  * 16/32/64 bucket (and with the same T > 128 or not) run as ONE persistent
  * launch, which removes per-launch prologue / tail time.  Typical use: the
  * projections that share an input (q, k, v; gate, up).  Problems must not

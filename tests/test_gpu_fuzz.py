@@ -1,0 +1,80 @@
+"""Seeded fuzz of the grouped entry points (PAPER.md:115-120 Eq. 1, :111; Listing 3
+LORA_DROPOUT): random ragged shapes, ranks 1..64, 1-4 members
+sharing x, with and without LoRA dropout (kept mask or redrawn).  Every case
+checks the grouped calls against the single calls -- y, h, dX bitwise, dA / dB
+to fp32 re-association (include/lora.h: the dA/dB kernel's token split is
+chosen per launch) -- and the single calls against the fp64 oracle within the
+north-star tolerances."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from synth import make_lora_inputs  # noqa: E402
+from tests.gpu_util import TOL_GRAD, TOL_OUT, dev_bf16, host_f64, relF  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def L():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2403_11366_b200 as L
+    L.lora_device_check()
+    return L
+
+
+def _cases(n_cases=14, seed=20260):
+    rng = np.random.default_rng(seed)
+    out = []
+    for i in range(n_cases):
+        T = int(rng.integers(1, 700))
+        n = 8 * int(rng.integers(1, 80))
+        G = int(rng.integers(1, 5))
+        ms = [8 * int(rng.integers(1, 80)) for _ in range(G)]
+        rs = [int(rng.choice([1, 3, 5, 8, 12, 16, 24, 33, 64])) for _ in range(G)]
+        p = float(rng.choice([0.0, 0.0, 0.05, 0.3]))
+        keep = bool(rng.integers(0, 2))
+        out.append((i, T, n, tuple(ms), tuple(rs), p, keep))
+    return out
+
+
+@pytest.mark.parametrize("case", _cases(), ids=lambda c: f"c{c[0]}-T{c[1]}-n{c[2]}-G{len(c[3])}-p{c[5]}")
+def test_grouped_fuzz(oracle_mod, L, case):
+    i, T, n, ms, rs, p, keep = case
+    alpha = 16.0
+    base = make_lora_inputs(T, n, ms[0], rs[0], seed=30000 + i)
+    x = dev_bf16(base["x"])
+    ds, ts, drops = [], [], []
+    for g, (m, r) in enumerate(zip(ms, rs)):
+        d = make_lora_inputs(T, n, m, r, seed=30100 + 10 * i + g)
+        d["x"] = base["x"]
+        ds.append(d)
+        ts.append({k: dev_bf16(d[k]) for k in ("w0", "a", "b", "dy")})
+        if p > 0.0:
+            dr = (p, 77 + g, 1000 * i + g)
+            if keep:
+                dr = dr + (L.dropout_keep_bits(T, n), torch.empty((T, n), dtype=torch.bfloat16, device="cuda"))
+            drops.append(dr)
+    dropouts = drops if p > 0.0 else None
+    fo = L.lora_linear_fwd_grouped([(x, t["w0"], t["a"], t["b"], None) for t in ts], [alpha] * len(ts),
+                                   dropouts=dropouts)
+    go = L.lora_linear_bwd_grouped([(x, t["w0"], t["a"], t["b"], t["dy"], h) for t, (_, h) in zip(ts, fo)],
+                                   [alpha] * len(ts), dropouts=dropouts)
+    torch.cuda.synchronize()
+    for g, (t, d) in enumerate(zip(ts, ds)):
+        kw = {"dropout": drops[g]} if p > 0.0 else {}
+        y1, h1 = L.lora_linear_fwd(x, t["w0"], t["a"], t["b"], alpha, **kw)
+        dx1, da1, db1 = L.lora_linear_bwd(x, t["w0"], t["a"], t["b"], t["dy"], alpha, h_saved=h1, **kw)
+        torch.cuda.synchronize()
+        assert torch.equal(fo[g][0], y1) and torch.equal(fo[g][1], h1), (case, g)
+        assert torch.equal(go[g][0], dx1), (case, g)
+        for u, v in ((go[g][1], da1), (go[g][2], db1)):
+            torch.testing.assert_close(u, v, rtol=1e-5, atol=1e-5 * float(v.abs().max()) + 1e-30)
+        okw = {"dropout": drops[g][:3]} if p > 0.0 else {}
+        yo, _ = oracle_mod.lora_fwd(d["x"], d["w0"], d["a"], d["b"], alpha, **okw)
+        gor = oracle_mod.lora_bwd(d["x"], d["w0"], d["a"], d["b"], d["dy"], alpha, **okw)
+        errs = (relF(host_f64(y1), yo), relF(host_f64(dx1), gor["dx"]), relF(host_f64(da1), gor["da"]),
+                relF(host_f64(db1), gor["db"]))
+        assert errs[0] <= TOL_OUT and errs[1] <= TOL_OUT, (case, g, errs)
+        assert errs[2] <= TOL_GRAD and errs[3] <= TOL_GRAD, (case, g, errs)
