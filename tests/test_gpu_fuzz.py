@@ -78,3 +78,40 @@ def test_grouped_fuzz(oracle_mod, L, case):
                 relF(host_f64(db1), gor["db"]))
         assert errs[0] <= TOL_OUT and errs[1] <= TOL_OUT, (case, g, errs)
         assert errs[2] <= TOL_GRAD and errs[3] <= TOL_GRAD, (case, g, errs)
+
+
+def _single_cases(n_cases=12, seed=4242):
+    rng = np.random.default_rng(seed)
+    out = [(100, 1, 8, 8, 1), (101, 2, 8, 16, 64), (102, 129, 8, 4096, 16), (103, 3000, 4096, 8, 8)]
+    for i in range(n_cases):
+        out.append((i, int(rng.integers(1, 1500)), 8 * int(rng.integers(1, 200)), 8 * int(rng.integers(1, 200)),
+                    int(rng.integers(1, 65))))
+    return out
+
+
+@pytest.mark.parametrize("case", _single_cases(), ids=lambda c: f"c{c[0]}-T{c[1]}-n{c[2]}-m{c[3]}-r{c[4]}")
+def test_single_and_merge_fuzz(oracle_mod, L, case):
+    """Single fwd / bwd (h saved and recomputed, dX skipped) and the merge at random
+    and extreme shapes (T = 1, d = 8, r = 1 and 64, skinny and wide) against the
+    oracle; the merge is >= 99.9% bit-equal to RNE(oracle) and within 1e-2."""
+    from tests.gpu_util import rne_bf16_f64
+    i, T, n, m, r = case
+    d = make_lora_inputs(T, n, m, r, seed=40000 + i)
+    x, w0, a, b, dy = (dev_bf16(d[k]) for k in ("x", "w0", "a", "b", "dy"))
+    alpha = 16.0
+    y, h = L.lora_linear_fwd(x, w0, a, b, alpha)
+    dx, da, db = L.lora_linear_bwd(x, w0, a, b, dy, alpha, h_saved=h)
+    dx2, da2, db2 = L.lora_linear_bwd(x, w0, a, b, dy, alpha, h_saved=None, want_dx=False)
+    wm = L.lora_merge(w0, a, b, alpha)
+    torch.cuda.synchronize()
+    yo, ho = oracle_mod.lora_fwd(d["x"], d["w0"], d["a"], d["b"], alpha)
+    go = oracle_mod.lora_bwd(d["x"], d["w0"], d["a"], d["b"], d["dy"], alpha)
+    assert relF(host_f64(y), yo) <= TOL_OUT and relF(host_f64(h), ho) <= 1e-4
+    assert relF(host_f64(dx), go["dx"]) <= TOL_OUT
+    for da_, db_ in ((da, db), (da2, db2)):
+        assert relF(host_f64(da_), go["da"]) <= TOL_GRAD and relF(host_f64(db_), go["db"]) <= TOL_GRAD
+    assert dx2 is None
+    mo = oracle_mod.lora_merge(d["w0"], d["a"], d["b"], alpha)
+    got = host_f64(wm)
+    assert relF(got, mo) <= TOL_OUT
+    assert np.sum(got != rne_bf16_f64(mo)) <= max(2, 0.001 * got.size)
