@@ -115,3 +115,42 @@ def test_single_and_merge_fuzz(oracle_mod, L, case):
     got = host_f64(wm)
     assert relF(got, mo) <= TOL_OUT
     assert np.sum(got != rne_bf16_f64(mo)) <= max(2, 0.001 * got.size)
+
+
+@pytest.fixture(scope="module")
+def comm(L):
+    from paper_2403_11366_b200 import tp
+    c = tp.LoraComm()
+    yield c
+    c.close()
+
+
+def _tp_cases(n_cases=8, seed=777):
+    rng = np.random.default_rng(seed)
+    out = []
+    for i in range(n_cases):
+        out.append((i, int(rng.integers(1, 1300)), 8 * int(rng.integers(1, 100)), 8 * int(rng.integers(1, 100)),
+                    int(rng.integers(1, 65)), str(rng.choice(["column", "row"])), str(rng.choice(["1", "3"])),
+                    float(rng.choice([0.0, 0.05]))))
+    return out
+
+
+@pytest.mark.parametrize("case", _tp_cases(), ids=lambda c: f"c{c[0]}-T{c[1]}-{c[5]}-chunks{c[6]}-p{c[7]}")
+def test_tp_n1_fuzz(L, comm, case, monkeypatch):
+    """The tensor-parallel calls at N = 1 (real NCCL communicator) at random shapes,
+    modes, forward token slicing and dropout: bitwise the single calls."""
+    from paper_2403_11366_b200 import tp
+    i, T, n, m, r, mode, chunks, p = case
+    d = make_lora_inputs(T, n, m, r, seed=50000 + i)
+    x, w0, a, b, dy = (dev_bf16(d[k]) for k in ("x", "w0", "a", "b", "dy"))
+    spec = tp.ShardSpec(tp.MODES[mode], 1, 0, n, m)
+    drop = (p, 9 + i, 3 * i) if p > 0.0 else None
+    kw = {"dropout": drop} if drop else {}
+    y1, h1 = L.lora_linear_fwd(x, w0, a, b, 16.0, **kw)
+    dx1, da1, db1 = L.lora_linear_bwd(x, w0, a, b, dy, 16.0, h_saved=h1, **kw)
+    monkeypatch.setenv("LORA_TP_CHUNKS", chunks)
+    y2, h2 = tp.tp_linear_fwd(comm, spec, x, w0, a, b, 16.0, dropout=drop)
+    dx2, da2, db2 = tp.tp_linear_bwd(comm, spec, x, w0, a, b, dy, 16.0, h_saved=h2, dropout=drop)
+    torch.cuda.synchronize()
+    for u, v in ((y1, y2), (h1, h2), (dx1, dx2), (da1, da2), (db1, db2)):
+        assert torch.equal(u, v), case
