@@ -154,3 +154,67 @@ def test_tp_n1_fuzz(L, comm, case, monkeypatch):
     torch.cuda.synchronize()
     for u, v in ((y1, y2), (h1, h2), (dx1, dx2), (da1, da2), (db1, db2)):
         assert torch.equal(u, v), case
+
+
+@pytest.mark.parametrize("case", _cases(n_cases=6, seed=99), ids=lambda c: f"g{c[0]}-T{c[1]}-n{c[2]}-G{len(c[3])}-p{c[5]}")
+def test_grouped_graph_replay_fuzz(L, case):
+    """The grouped forward + backward (dropout with kept mask / M.x when p > 0,
+    accumulate into dA / dB) captured ONCE as a CUDA graph and replayed with new
+    inputs written in place: bitwise the eager calls on those inputs (the
+    self-cleaning sync words and the kept buffers carry no state across replays)."""
+    i, T, n, ms, rs, p, _ = case
+    alpha = 16.0
+    gen = torch.Generator(device="cuda").manual_seed(1234 + i)
+    x = torch.empty((T, n), dtype=torch.bfloat16, device="cuda")
+    ts = []
+    for m, r in zip(ms, rs):
+        ts.append({"w0": torch.randn((m, n), device="cuda", generator=gen).bfloat16() / n ** 0.5,
+                   "a": torch.randn((r, n), device="cuda", generator=gen).bfloat16() / n ** 0.5,
+                   "b": torch.randn((m, r), device="cuda", generator=gen).bfloat16() / r ** 0.5,
+                   "dy": torch.empty((T, m), dtype=torch.bfloat16, device="cuda")})
+    drops = None
+    if p > 0.0:
+        drops = [(p, 5 + g, 7 * g, L.dropout_keep_bits(T, n), torch.empty((T, n), dtype=torch.bfloat16, device="cuda"))
+                 for g in range(len(ts))]
+    G = len(ts)
+    ys = [(torch.empty((T, t["w0"].shape[0]), dtype=torch.bfloat16, device="cuda"),
+           torch.empty((T, t["a"].shape[0]), dtype=torch.float32, device="cuda")) for t in ts]
+    gs = [(torch.empty((T, n), dtype=torch.bfloat16, device="cuda"), torch.zeros_like(t["a"], dtype=torch.float32),
+           torch.zeros_like(t["b"], dtype=torch.float32)) for t in ts]
+
+    def fill(k):
+        x.copy_(torch.randn((T, n), device="cuda", generator=gen))
+        for t in ts:
+            t["dy"].copy_(torch.randn(t["dy"].shape, device="cuda", generator=gen))
+
+    def step(outs_f, outs_b, acc):
+        L.lora_linear_fwd_grouped([(x, t["w0"], t["a"], t["b"], None) for t in ts], [alpha] * G, outs=outs_f,
+                                  dropouts=drops)
+        L.lora_linear_bwd_grouped([(x, t["w0"], t["a"], t["b"], t["dy"], h) for t, (_, h) in zip(ts, outs_f)],
+                                  [alpha] * G, outs=outs_b, accumulate=acc, dropouts=drops)
+
+    fill(0)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        step(ys, gs, True)   # (warm-up: workspaces allocated outside the capture)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        step(ys, gs, True)
+    for k in range(2):
+        fill(k + 1)
+        for _, da, db in gs:
+            da.zero_()
+            db.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        ref_f = [(torch.empty_like(y), torch.empty_like(h)) for y, h in ys]
+        ref_b = [(torch.empty_like(dx), torch.zeros_like(da), torch.zeros_like(db)) for dx, da, db in gs]
+        step(ref_f, ref_b, True)
+        torch.cuda.synchronize()
+        for (y, h), (y1, h1) in zip(ys, ref_f):
+            assert torch.equal(y, y1) and torch.equal(h, h1), (case, k)
+        for (dx, da, db), (dx1, da1, db1) in zip(gs, ref_b):
+            assert torch.equal(dx, dx1) and torch.equal(da, da1) and torch.equal(db, db1), (case, k)
