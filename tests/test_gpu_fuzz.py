@@ -218,3 +218,38 @@ def test_grouped_graph_replay_fuzz(L, case):
             assert torch.equal(y, y1) and torch.equal(h, h1), (case, k)
         for (dx, da, db), (dx1, da1, db1) in zip(gs, ref_b):
             assert torch.equal(dx, dx1) and torch.equal(da, da1) and torch.equal(db, db1), (case, k)
+
+
+def _drop_cases(n_cases=8, seed=31337):
+    rng = np.random.default_rng(seed)
+    return [(i, int(rng.integers(1, 900)), 8 * int(rng.integers(1, 120)), 8 * int(rng.integers(1, 120)),
+             int(rng.integers(1, 65)), float(rng.choice([0.05, 0.2, 0.5])), bool(rng.integers(0, 2)),
+             bool(rng.integers(0, 2)), bool(rng.integers(0, 2))) for i in range(n_cases)]
+
+
+@pytest.mark.parametrize("case", _drop_cases(), ids=lambda c: f"d{c[0]}-T{c[1]}-r{c[4]}-p{c[5]}")
+def test_dropout_single_paths_fuzz(oracle_mod, L, case):
+    """Single dropout calls at random shapes and p, with the backward's h saved or
+    recomputed, dX wanted or skipped, the mask kept or redrawn: vs the oracle, and
+    every backward variant equal to the full one on what they share."""
+    i, T, n, m, r, p, recompute, skip_dx, keep = case
+    d = make_lora_inputs(T, n, m, r, seed=60000 + i)
+    x, w0, a, b, dy = (dev_bf16(d[k]) for k in ("x", "w0", "a", "b", "dy"))
+    drop = (p, 40 + i, 5 * i)
+    if keep:
+        drop = drop + (L.dropout_keep_bits(T, n), torch.empty((T, n), dtype=torch.bfloat16, device="cuda"))
+    y, h = L.lora_linear_fwd(x, w0, a, b, 16.0, dropout=drop)
+    dx, da, db = L.lora_linear_bwd(x, w0, a, b, dy, 16.0, h_saved=h, dropout=drop)
+    dx2, da2, db2 = L.lora_linear_bwd(x, w0, a, b, dy, 16.0, h_saved=None if recompute else h,
+                                      want_dx=not skip_dx, dropout=drop)
+    torch.cuda.synchronize()
+    yo, ho = oracle_mod.lora_fwd(d["x"], d["w0"], d["a"], d["b"], 16.0, dropout=drop[:3])
+    go = oracle_mod.lora_bwd(d["x"], d["w0"], d["a"], d["b"], d["dy"], 16.0, dropout=drop[:3])
+    assert relF(host_f64(y), yo) <= TOL_OUT and relF(host_f64(h), ho) <= 1e-4, case
+    assert relF(host_f64(dx), go["dx"]) <= TOL_OUT, case
+    for da_, db_ in ((da, db), (da2, db2)):
+        assert relF(host_f64(da_), go["da"]) <= TOL_GRAD and relF(host_f64(db_), go["db"]) <= TOL_GRAD, case
+    if not skip_dx:
+        assert relF(host_f64(dx2), go["dx"]) <= TOL_OUT, case
+    else:
+        assert dx2 is None
