@@ -268,3 +268,51 @@ def test_column_group_fused_ipc_two_processes(r):
         assert err <= TOL_OUT
     assert res[0][2] == res[1][2]
     assert res[0][3] == ("coresident" if r == 8 else "after_gemm"), res[0][3]
+
+
+def _symm_cases(n_cases=6, seed=8080):
+    rng = np.random.default_rng(seed)
+    out = []
+    for i in range(n_cases):
+        N = int(rng.choice([2, 4]))
+        out.append((i, N, int(rng.integers(1, 700)), 8 * N * int(rng.integers(1, 40)),
+                    8 * N * int(rng.integers(1, 40)), int(rng.choice([4, 8, 16, 24]))))
+    return out
+
+
+@pytest.mark.parametrize("case", _symm_cases(), ids=lambda c: f"s{c[0]}-N{c[1]}-T{c[2]}")
+def test_symm_fuzz(oracle_mod, case):
+    """Seeded random shapes for both comm-fused protocols at 2 / 4 virtual ranks:
+    the ROW forward's reduced y and the COLUMN-group backward's reduced dX (two
+    members) against the UNSHARDED oracle, ranks bitwise identical."""
+    from paper_2403_11366_b200 import tp
+    i, N, T, n, m, r = case
+    alpha = 16.0
+    d = make_lora_inputs(T, n, m, r, seed=9000 + i, bias=True)
+    yo, _ = oracle_mod.lora_fwd(d["x"], d["w0"], d["a"], d["b"], alpha, bias=d["bias"])
+    bufs = tp.SymmBuffer.local_group(N, 2 * T * m * 2 + 4096)
+    streams = [torch.cuda.Stream() for _ in range(N)]
+    try:
+        ys = _row_fwd(bufs, d, alpha, N, n, m, streams)
+        for y in ys[1:]:
+            assert torch.equal(y, ys[0])
+        assert relF(host_f64(ys[0]), yo) <= TOL_OUT
+    finally:
+        for b in bufs:
+            b.close()
+    ms = (m, 8 * N * (1 + i))
+    d_list = []
+    for g, mm in enumerate(ms):
+        dg = make_lora_inputs(T, n, mm, r, seed=9100 + 10 * i + g)
+        dg["x"] = d["x"]
+        d_list.append(dg)
+    ref = [oracle_mod.lora_bwd(dg["x"], dg["w0"], dg["a"], dg["b"], dg["dy"], alpha) for dg in d_list]
+    bufs = tp.SymmBuffer.local_group(N, (len(ms) + 1) * T * n * 2 + 4096)
+    try:
+        res = _col_group_bwd(bufs, d_list, alpha, N, n, ms, streams)
+        for dxs, _ in res[1:]:
+            assert torch.equal(dxs, res[0][0])
+        assert relF(host_f64(res[0][0]), sum(o["dx"] for o in ref)) <= TOL_OUT
+    finally:
+        for b in bufs:
+            b.close()
