@@ -147,11 +147,14 @@ def algorithmic_flops(T, n, m, r) -> int:
 def make_layer_inputs(T, d, f, heads, r, seed=DEFAULT_SEED):
     """Inputs of one Llama-2 decoder layer with LoRA on all seven projections
     (SURVEY.md 8(f) N4), as bf16 bit patterns: x, dout ~ N(0, 1); every W0 of
-    shape [m, n] ~ N(0, 1/n); A ~ N(0, 1/n); B ~ N(0, 1/(16 r)) (a trained
-    adapter's delta is a fraction of the base projection: at s = 16/r it is
-    ~1/2 of it; the single-linear recipe's B ~ N(0, 1/r) would make every block
-    output LoRA-dominated and the attention scores saturate); the RMSNorm
-    weights g1, g2 ~ 1 + N(0, 0.1^2).  One PCG64 stream per tensor, fixed order."""
+    shape [m, n] ~ N(0, 1/n); A ~ N(0, 1/n); B ~ N(0, r / 1024) (a trained
+    adapter's delta is a fraction of the base projection: with h ~ N(0, 1) per
+    rank index and s = 16 / r the delta's std is s sqrt(r) sqrt(r) / 32 = 1/2 of
+    the base's at EVERY rank -- round 2 used N(0, 1/(16 r)), which is this at
+    r = 8 only and made small-rank layers LoRA-dominated (std 4 at r = 1) with
+    saturated attention scores; the single-linear recipe's N(0, 1/r) would do so
+    at every rank); the RMSNorm weights g1, g2 ~ 1 + N(0, 0.1^2).  One PCG64
+    stream per tensor, fixed order."""
     shapes = {"q": (d, d), "k": (d, d), "v": (d, d), "o": (d, d), "gate": (f, d), "up": (f, d), "down": (d, f)}
     streams = np.random.SeedSequence(seed).spawn(4 + 3 * len(shapes))
     rng = iter(np.random.Generator(np.random.PCG64(s)) for s in streams)
@@ -162,5 +165,6 @@ def make_layer_inputs(T, d, f, heads, r, seed=DEFAULT_SEED):
     for name, (m, n) in shapes.items():
         out["w0_" + name] = f32_to_bf16_bits(next(rng).standard_normal((m, n), dtype=np.float32) / np.sqrt(n))
         out["a_" + name] = f32_to_bf16_bits(next(rng).standard_normal((r, n), dtype=np.float32) / np.sqrt(n))
-        out["b_" + name] = f32_to_bf16_bits(next(rng).standard_normal((m, r), dtype=np.float32) / np.sqrt(16 * r))
+        out["b_" + name] = f32_to_bf16_bits(next(rng).standard_normal((m, r), dtype=np.float32) *
+                                            np.float32(np.sqrt(r) / 32.0))
     return out

@@ -114,3 +114,20 @@ def test_layer_tp_path_one_rank():
     assert torch.equal(out1, out2) and torch.equal(dx1, dx2)
     for k in g1:
         assert torch.equal(g1[k], g2[k]), k
+
+
+def _layer_cases(n_cases=6, seed=555):
+    rng = np.random.default_rng(seed)
+    out = []
+    for i in range(n_cases):
+        H = int(rng.choice([1, 2, 4]))
+        hd = int(rng.choice([64, 128]))
+        out.append((int(rng.integers(16, 420)), H * hd, 8 * int(rng.integers(8, 200)), H, int(rng.integers(1, 33))))
+    return out
+
+
+@pytest.mark.parametrize("T,d,f,H,r", _layer_cases())
+def test_layer_fuzz(T, d, f, H, r):
+    """Seeded random layer configurations (T, heads, head_dim 64 / 128, ffn, rank) through
+    the same checks as test_layer_fwd_bwd_matches_oracle."""
+    test_layer_fwd_bwd_matches_oracle(T, d, f, H, r)
