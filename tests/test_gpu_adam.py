@@ -106,3 +106,33 @@ def test_lora_training_loop_reduces_loss(L):
     torch.cuda.synchronize()
     assert losses[-1] < 0.1 * losses[0], (losses[0], losses[-1])
     assert torch.equal(w0, w0_before)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_adam_fuzz(oracle_mod, L, seed):
+    """Seeded random adapter sets (1-12 tensors of r x n / m x r shapes, element
+    counts multiples of 8), hyper-parameters and gradient scales: three steps of
+    one launch each vs the fp64 oracle (fp32 master state)."""
+    rng = np.random.default_rng(900 + seed)
+    shapes = []
+    for _ in range(int(rng.integers(1, 13))):
+        r, d = int(rng.integers(1, 65)), 8 * int(rng.integers(1, 600))
+        shapes.append((r, d) if rng.integers(0, 2) else (d, r))
+    ts = _rand_tensors(shapes, 50 + seed)
+    lr, b1, b2 = float(rng.choice([1e-4, 1e-3, 3e-3])), float(rng.choice([0.8, 0.9])), float(rng.choice([0.99, 0.999]))
+    eps = 1e-8
+    gen = torch.Generator().manual_seed(60 + seed)
+    f32 = lambda z: float(np.float32(z))  # noqa: E731
+    for step in range(1, 4):
+        grads = [torch.randn(sh, generator=gen) * float(rng.choice([1e-3, 0.1, 1.0])) for sh in shapes]
+        L.lora_adam_step([(t["param"], g.cuda(), t["m"], t["v"], t["master"]) for t, g in zip(ts, grads)], step, lr,
+                         (b1, b2), eps)
+        torch.cuda.synchronize()
+        for t, g in zip(ts, grads):
+            t["w64"], t["m64"], t["v64"] = oracle_mod.adam_step(t["w64"], g.double().numpy(), t["m64"], t["v64"],
+                                                                step, f32(lr), f32(b1), f32(b2), f32(eps))
+    for t in ts:
+        scale = max(float(np.abs(t["m64"]).max()), 1e-12)
+        np.testing.assert_allclose(t["m"].cpu().double().numpy(), t["m64"], rtol=1e-5, atol=1e-6 * scale)
+        np.testing.assert_allclose(t["master"].cpu().double().numpy(), t["w64"], rtol=0, atol=5e-3 * lr)
+        assert torch.equal(t["param"].cpu(), t["master"].cpu().to(torch.bfloat16))
